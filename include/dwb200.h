@@ -1,0 +1,195 @@
+/*
+ * dwb200.h -- C ABI of libdwb200.so, the B200 (sm_100a) hot path of the
+ * Magneton / diffwatt differential energy debugger.
+ *
+ * The reference (/root/reference/pkg/src/diffwatt) is pure Python and has no
+ * FFI; its drop-in boundary is the Python API.  Each entry point
+ * below replaces the inner loop of one reference function, and the Python
+ * package paper_2512_08365_b200 binds them with ctypes behind the reference's
+ * own names (build_ledger, integrate, detect_waste, report):
+ *
+ *   dw_attribute        energy.integrate per interval            energy.py:90-130
+ *   dw_ledger           energy.build_ledger (ground_truth/sampled) energy.py:280-331
+ *   dw_fx_sum           EnergyLedger.operator_total               energy.py:273-274
+ *   dw_step_value_at    PowerSignal.value_at (the sampler's read) energy.py:57-66
+ *   dw_detect_pairs     detect.detect_waste per-pair rule         detect.py:72-130
+ *   dw_rank             detect.report ordering                    detect.py:256-278
+ *   dw_join_diff        signature hash-join + deltas + verdicts   (new)
+ *
+ * Conventions
+ *   - Every pointer argument named d_* is DEVICE memory owned by the caller.
+ *     The library allocates nothing: scratch comes from a caller workspace whose
+ *     size the matching *_workspace_size() returns.  Device pointers must be
+ *     16-byte aligned (torch / cudaMalloc allocations are).
+ *   - Calls are asynchronous on the given stream.  Data-dependent errors (an
+ *     interval outside the signal, unsorted input, ...) are written into the
+ *     workspace's status block; dw_status() synchronises the stream and reads it.
+ *     Argument errors are returned immediately.
+ *   - No global state: concurrent calls on different streams with different
+ *     workspaces are safe.
+ *   - Times are int64 microseconds, power fp64 watts, energy fp64 joules.
+ */
+#ifndef DWB200_H
+#define DWB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *dw_stream_t; /* == cudaStream_t */
+
+/* ------------------------------------------------------------- error codes */
+#define DW_OK 0
+#define DW_E_REVERSED (-1)  /* SignalError "interval end precedes start"   energy.py:93-94 */
+#define DW_E_SPAN (-2)      /* SignalError "interval [lo,hi] outside signal span [s,e]" energy.py:95-97 */
+#define DW_E_EMPTY (-3)     /* SignalError "empty power signal"            energy.py:53 */
+#define DW_E_ORDER (-4)     /* TraceError "power samples must be strictly increasing" trace_model.py:549-551 */
+#define DW_E_ARG (-5)       /* bad argument (null/misaligned pointer, n < 0, threshold) */
+#define DW_E_CUDA (-6)      /* a CUDA runtime error (launch failure, ...) */
+#define DW_E_WORKSPACE (-7) /* workspace smaller than *_workspace_size() */
+#define DW_E_UNSORTED (-8)  /* a set flagged sorted is not sorted by start */
+
+/* --------------------------------------------------------------- constants */
+#define DW_SIGNAL_STEP 0   /* ground truth: breakpoints of a piecewise-constant signal */
+#define DW_SIGNAL_LINEAR 1 /* samples: trapezoid with linear interpolation */
+#define DW_MAX_SETS 4      /* interval sets per dw_attribute call */
+/* Intervals spanning at most DW_DIRECT_MAX segments are summed sequentially in
+ * fp64 exactly as the reference does (bit-identical); longer ones are summed
+ * exactly in 2^-40 W*us fixed point and rounded once. */
+#define DW_DIRECT_MAX 256
+
+/* ------------------------------------------------------------------- types */
+typedef struct {
+    const int64_t *d_ts;   /* [n] strictly increasing timestamps */
+    const double *d_watts; /* [n] */
+    int64_t n;
+    int64_t span_hi; /* STEP: end of the last segment, max(trace end, ts[n-1]+1)
+                        (energy.py:80); LINEAR: ignored, the span is [ts[0], ts[n-1]] */
+    int32_t kind;    /* DW_SIGNAL_STEP | DW_SIGNAL_LINEAR */
+    int32_t validate_order; /* 1: check ts strictly increasing (DW_E_ORDER) */
+} dw_signal_t;
+
+typedef struct {
+    const int64_t *d_start; /* [n] */
+    const int64_t *d_end;   /* [n] */
+    int64_t n;
+    double *d_joules;       /* [n] out */
+    int32_t sorted;         /* 1: d_start is non-decreasing (checked: DW_E_UNSORTED);
+                               0: the library sorts a copy in the workspace */
+    int32_t pad;
+} dw_interval_set_t;
+
+typedef struct {
+    int32_t code;      /* first error class found, DW_OK if none */
+    int32_t bad_set;   /* set of the reported interval, -1 if none */
+    int64_t bad_index[DW_MAX_SETS]; /* per set: smallest index of an invalid interval, -1 if none */
+    int64_t order_index;            /* first i with ts[i+1] <= ts[i], -1 if none */
+    int64_t unsorted_index[DW_MAX_SETS]; /* first k with start[k] < start[k-1], -1 if none */
+    int64_t long_intervals;         /* intervals that took the fixed-point path */
+    double totals[4];               /* dw_ledger: total, operator_total, idle, unused */
+} dw_status_t;
+
+/* ---------------------------------------------------------- attribution */
+
+/* Workspace bytes for dw_attribute / dw_ledger with these sizes. */
+size_t dw_attribute_workspace_size(int64_t n_samples, const int64_t *set_sizes, int32_t nsets);
+
+/* joules[k] = integral of the signal over [start[k], end[k]] for every set.
+ * Replaces the per-interval energy.integrate calls of build_ledger
+ * (energy.py:312-316).  Errors -> status (first invalid interval per set). */
+int dw_attribute(const dw_signal_t *sig, dw_interval_set_t *sets, int32_t nsets,
+                 void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
+
+/* build_ledger for one trace: sets[0] = operators, sets[1] = kernels (either may
+ * be empty).  Also integrates the whole span and stores, in the status block,
+ * totals = {total_joules, operator_total, idle_joules = max(total - op_total, 0)}
+ * (energy.py:318-324).  operator_total is the exact sum rounded once. */
+int dw_ledger(const dw_signal_t *sig, dw_interval_set_t *ops, dw_interval_set_t *kernels,
+              void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
+
+/* Synchronise `stream` and copy the status block out of the workspace. Returns
+ * status->code. */
+int dw_status(const void *d_workspace, dw_stream_t stream, dw_status_t *status);
+
+/* Exact (2^-64 J fixed point) sum of d_x[0..n) rounded once -> *d_out. */
+size_t dw_fx_sum_workspace_size(int64_t n);
+int dw_fx_sum(const double *d_x, int64_t n, double *d_out, void *d_workspace,
+              size_t workspace_bytes, dw_stream_t stream);
+
+/* PowerSignal.value_at for the sampler (energy.py:57-66, 160-171): watts of the
+ * step signal at fractional times d_t (clamped to the span). */
+int dw_step_value_at(const dw_signal_t *sig, const double *d_t, int64_t m, double *d_out,
+                     dw_stream_t stream);
+
+/* ------------------------------------------------------------------ diff */
+
+/* Per-pair columns written by dw_detect_pairs / dw_join_diff. */
+typedef struct {
+    double *d_energy_a, *d_energy_b; /* [P] */
+    double *d_ratio;                 /* [P] high/low, 1.0 when equal, inf when low == 0 */
+    int64_t *d_latency_a, *d_latency_b; /* [P] max end - min start */
+    int8_t *d_verdict;               /* [P] 0 below_threshold, 1 tradeoff, 2 waste */
+    int8_t *d_side;                  /* [P] 0 "-", 1 "A", 2 "B" */
+    int8_t *d_informational;         /* [P] */
+    double *d_wasted;                /* [P] high - low */
+    uint64_t *d_key_hi, *d_key_lo;   /* [P] ranking key (report order = descending) */
+} dw_findings_t;
+
+/* detect_waste over CSR segment pairs (reference SubgraphPair lists).
+ * Per pair p: members d_mem_a[d_off_a[p]..d_off_a[p+1]) index ops of trace A
+ * (same for B).  Energies are CPython-3.12 sum() (Neumaier) over members in
+ * order, as subgraph_joules does.  d_out_diff may be NULL (0.0).  d_tie[p] is
+ * the rank of nodes_a under Python tuple order (the report tie-break). */
+int dw_detect_pairs(int64_t P, const int64_t *d_off_a, const int32_t *d_mem_a,
+                    const int64_t *d_off_b, const int32_t *d_mem_b,
+                    const double *d_joules_a, const double *d_joules_b,
+                    const int64_t *d_start_a, const int64_t *d_end_a,
+                    const int64_t *d_start_b, const int64_t *d_end_b,
+                    const double *d_out_diff, const int64_t *d_tie, double threshold,
+                    dw_findings_t *out, dw_stream_t stream);
+
+/* Order findings by (verdict != waste, -wasted_joules, nodes_a) -- detect.py:263-266.
+ * Writes the k best finding indices, best first, into d_order (k <= P; k == P
+ * is the full report order).  Also accumulates, into d_summary[0..3):
+ * {n_waste, wasted_joules (exact sum over waste findings), n_findings}. */
+size_t dw_rank_workspace_size(int64_t P, int64_t k);
+int dw_rank(int64_t P, const dw_findings_t *f, int64_t k, int64_t *d_order, double *d_summary,
+            void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
+
+/* Signature hash-join diff.  Operators of A and B
+ * are keyed by (sig, occurrence in op order); equal keys pair up, unmatched
+ * operators become one-sided findings.  Findings are numbered: A ops in order
+ * (matched or A-only), then B-only ops in order.  d_work_* (may be NULL = 1.0)
+ * is useful work per op; d_epw_* receives joules per unit of work.  d_rank_a[i]
+ * is the lexicographic rank of A op i's id (tie-break).  Outputs per finding:
+ * the dw_findings_t columns plus d_ia / d_ib (-1 on the empty side).
+ * *d_count receives {P, n_matched, n_a_only, n_b_only}. */
+typedef struct {
+    const uint64_t *d_sig;   /* [n] */
+    const int64_t *d_start, *d_end; /* [n] */
+    const double *d_joules;  /* [n] attributed energy */
+    const double *d_work;    /* [n] or NULL */
+    const int64_t *d_rank;   /* [n] id rank (A side tie-break), NULL = index */
+    int64_t n;
+} dw_join_side_t;
+
+size_t dw_join_workspace_size(int64_t na, int64_t nb);
+int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, double threshold,
+                 dw_findings_t *out, int64_t *d_ia, int64_t *d_ib, double *d_epw_a,
+                 double *d_epw_b, int64_t *d_count, void *d_workspace, size_t workspace_bytes,
+                 dw_stream_t stream);
+
+/* --------------------------------------------------------------- misc */
+const char *dw_version(void);
+const char *dw_error_string(int code);
+/* number of kernel launches issued by this library on the calling thread
+ * since the last reset (bench.py's gpu_launches) */
+int64_t dw_launch_count(int reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DWB200_H */

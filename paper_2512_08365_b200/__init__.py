@@ -1,0 +1,40 @@
+"""paper_2512_08365_b200 -- B200-native hot path of Magneton / diffwatt.
+
+Drop-in for the analysis hot path of the reference package
+(/root/reference/pkg/src/diffwatt): trace ingestion into columnar device
+buffers, per-operator energy attribution, the cross-system differential diff
+and ranked findings.  The compute runs in hand-written sm_100a CUDA kernels
+(csrc/, exported through the C ABI in include/dwb200.h); there is no CPU
+fallback.
+"""
+
+from .trace_model import (  # noqa: F401
+    KernelEvent,
+    OperatorEvent,
+    ParseError,
+    PowerSample,
+    Trace,
+    TraceError,
+    TraceHeader,
+    TraceReferenceError,
+    VersionError,
+    load_trace,
+    parse_trace_lines,
+    save_trace,
+    trace_to_lines,
+)
+from .columns import TraceColumns  # noqa: F401
+from .energy import (  # noqa: F401
+    EnergyLedger,
+    PowerSignal,
+    SignalError,
+    build_ledger,
+    ground_truth_signal,
+    integrate,
+    integrate_many,
+    mean_power,
+    sample_signal,
+    sampled_view,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,194 @@
+"""ctypes binding of libdwb200.so (include/dwb200.h).
+
+There is no CPU fallback: importing the compute entry points on a machine
+without the built library or without a CUDA device raises ``NativeUnavailable``
+the first time a kernel is needed.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import torch
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "_lib" / "libdwb200.so"
+
+DW_OK = 0
+DW_E_REVERSED = -1
+DW_E_SPAN = -2
+DW_E_EMPTY = -3
+DW_E_ORDER = -4
+DW_E_ARG = -5
+DW_E_CUDA = -6
+DW_E_WORKSPACE = -7
+DW_E_UNSORTED = -8
+
+DW_SIGNAL_STEP = 0
+DW_SIGNAL_LINEAR = 1
+DW_MAX_SETS = 4
+DW_DIRECT_MAX = 256
+
+# every symbol include/dwb200.h declares (tests check the .so exports them all)
+EXPORTED = (
+    "dw_attribute_workspace_size", "dw_attribute", "dw_ledger", "dw_status",
+    "dw_fx_sum_workspace_size", "dw_fx_sum", "dw_step_value_at", "dw_detect_pairs",
+    "dw_rank_workspace_size", "dw_rank", "dw_join_workspace_size", "dw_join_diff",
+    "dw_version", "dw_error_string", "dw_launch_count",
+)
+
+
+class NativeUnavailable(RuntimeError):
+    """libdwb200.so or a CUDA device is missing: the GPU path cannot run."""
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        super().__init__(f"{where}: dwb200 error {code} ({error_string(code)})")
+
+
+c_i64 = ctypes.c_int64
+c_i32 = ctypes.c_int32
+c_vp = ctypes.c_void_p
+
+
+class Signal(ctypes.Structure):
+    _fields_ = [("d_ts", c_vp), ("d_watts", c_vp), ("n", c_i64), ("span_hi", c_i64),
+                ("kind", c_i32), ("validate_order", c_i32)]
+
+
+class IntervalSet(ctypes.Structure):
+    _fields_ = [("d_start", c_vp), ("d_end", c_vp), ("n", c_i64), ("d_joules", c_vp),
+                ("sorted", c_i32), ("pad", c_i32)]
+
+
+class Status(ctypes.Structure):
+    _fields_ = [("code", c_i32), ("bad_set", c_i32), ("bad_index", c_i64 * DW_MAX_SETS),
+                ("order_index", c_i64), ("unsorted_index", c_i64 * DW_MAX_SETS),
+                ("long_intervals", c_i64), ("totals", ctypes.c_double * 4)]
+
+
+class Findings(ctypes.Structure):
+    _fields_ = [("d_energy_a", c_vp), ("d_energy_b", c_vp), ("d_ratio", c_vp),
+                ("d_latency_a", c_vp), ("d_latency_b", c_vp), ("d_verdict", c_vp),
+                ("d_side", c_vp), ("d_informational", c_vp), ("d_wasted", c_vp),
+                ("d_key_hi", c_vp), ("d_key_lo", c_vp)]
+
+
+class JoinSide(ctypes.Structure):
+    _fields_ = [("d_sig", c_vp), ("d_start", c_vp), ("d_end", c_vp), ("d_joules", c_vp),
+                ("d_work", c_vp), ("d_rank", c_vp), ("n", c_i64)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libdwb200.so (loudly failing when absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not LIB_PATH.exists():
+            raise NativeUnavailable(
+                f"{LIB_PATH} is not built; run `python -m paper_2512_08365_b200.build` "
+                "(there is no CPU fallback)")
+        L = ctypes.CDLL(str(LIB_PATH))
+        L.dw_attribute_workspace_size.restype = ctypes.c_size_t
+        L.dw_attribute_workspace_size.argtypes = [c_i64, ctypes.POINTER(c_i64), c_i32]
+        L.dw_attribute.argtypes = [ctypes.POINTER(Signal), ctypes.POINTER(IntervalSet), c_i32,
+                                   c_vp, ctypes.c_size_t, c_vp]
+        L.dw_ledger.argtypes = [ctypes.POINTER(Signal), ctypes.POINTER(IntervalSet),
+                                ctypes.POINTER(IntervalSet), c_vp, ctypes.c_size_t, c_vp]
+        L.dw_status.argtypes = [c_vp, c_vp, ctypes.POINTER(Status)]
+        L.dw_fx_sum_workspace_size.restype = ctypes.c_size_t
+        L.dw_fx_sum_workspace_size.argtypes = [c_i64]
+        L.dw_fx_sum.argtypes = [c_vp, c_i64, c_vp, c_vp, ctypes.c_size_t, c_vp]
+        L.dw_step_value_at.argtypes = [ctypes.POINTER(Signal), c_vp, c_i64, c_vp, c_vp]
+        L.dw_version.restype = ctypes.c_char_p
+        L.dw_error_string.restype = ctypes.c_char_p
+        L.dw_error_string.argtypes = [ctypes.c_int]
+        L.dw_launch_count.restype = c_i64
+        L.dw_launch_count.argtypes = [ctypes.c_int]
+        if hasattr(L, "dw_detect_pairs"):
+            L.dw_detect_pairs.argtypes = [c_i64] + [c_vp] * 12 + [ctypes.c_double,
+                                                                  ctypes.POINTER(Findings), c_vp]
+            L.dw_rank_workspace_size.restype = ctypes.c_size_t
+            L.dw_rank_workspace_size.argtypes = [c_i64, c_i64]
+            L.dw_rank.argtypes = [c_i64, ctypes.POINTER(Findings), c_i64, c_vp, c_vp, c_vp,
+                                  ctypes.c_size_t, c_vp]
+            L.dw_join_workspace_size.restype = ctypes.c_size_t
+            L.dw_join_workspace_size.argtypes = [c_i64, c_i64]
+            L.dw_join_diff.argtypes = [ctypes.POINTER(JoinSide), ctypes.POINTER(JoinSide),
+                                       ctypes.c_double, ctypes.POINTER(Findings), c_vp, c_vp,
+                                       c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp]
+        _lib = L
+        return L
+
+
+def error_string(code: int) -> str:
+    try:
+        return lib().dw_error_string(int(code)).decode()
+    except NativeUnavailable:
+        return str(code)
+
+
+def version() -> str:
+    return lib().dw_version().decode()
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(lib().dw_launch_count(1 if reset else 0))
+
+
+def device() -> torch.device:
+    """The CUDA device the GPU path runs on (current torch device)."""
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device: the dwb200 GPU path cannot run "
+                                "(there is no CPU fallback)")
+    lib()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def ptr(t) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr() if t.numel() else None
+
+
+def check(rc: int, where: str) -> None:
+    if rc != DW_OK:
+        raise NativeError(rc, where)
+
+
+class Workspace:
+    """Grow-only device scratch, one per (device, stream); caller-owned by the
+    library's contract (the library itself never allocates)."""
+
+    _pool: dict = {}
+
+    @classmethod
+    def get(cls, nbytes: int, stream=None) -> torch.Tensor:
+        dev = device()
+        key = (dev.index, stream_handle(stream))
+        buf = cls._pool.get(key)
+        if buf is None or buf.numel() < nbytes:
+            cls._pool[key] = None
+            buf = torch.empty(max(int(nbytes * 1.25), 1 << 20), dtype=torch.uint8, device=dev)
+            cls._pool[key] = buf
+        return buf
+
+    @classmethod
+    def clear(cls) -> None:
+        cls._pool.clear()

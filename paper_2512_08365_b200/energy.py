@@ -1,0 +1,511 @@
+"""Energy attribution -- drop-in for the reference's ``diffwatt.energy``.
+
+Same names, signatures, return types and exceptions as
+/root/reference/pkg/src/diffwatt/energy.py; the per-interval integration runs
+in libdwb200 on the GPU (csrc/attribute.cu), never on the host:
+
+    integrate(signal, (lo, hi))        energy.py:90-105   -> dw_attribute
+    build_ledger(trace, method, ...)   energy.py:280-331  -> dw_ledger
+    PowerSignal.value_at for sampling  energy.py:57-66    -> dw_step_value_at
+
+Numerics: intervals covering <= DW_DIRECT_MAX (256) power segments get the
+reference's own sequential fp64 sum, bit for bit; longer ones (and the ledger
+total) get an exact fixed-point sum rounded once, within 1e-12
+relative of the reference's sequential sum.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from collections.abc import Mapping
+from dataclasses import dataclass
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _native
+from .columns import TraceColumns
+from .trace_model import OperatorEvent, PowerSample, Trace
+
+US_PER_S = 1_000_000
+
+DEFAULT_SAMPLER_PERIOD_US = 40_000  # 25 Hz (energy.py:23)
+DEFAULT_SAMPLER_DELAY_US = 200_000  # energy.py:24
+DEFAULT_REPLAY_REPEAT = 1000
+REPLAY_MARGIN = 0.10
+
+IDLE_OP = "idle"
+
+METHODS = ("ground_truth", "sampled", "replay")
+
+
+class SignalError(ValueError):
+    pass
+
+
+# ----------------------------------------------------------------- signals
+
+
+class PowerSignal:
+    """Piecewise-constant ground truth, or a sampled view of one.
+
+    Constructor-compatible with the reference dataclass (energy.py:37-82):
+    ``PowerSignal(segments=...)`` / ``PowerSignal(samples=..., period_us=, delay_us=)``.
+    Internally it is columnar: ``ts``/``watts`` arrays plus ``span_hi`` (step)
+    -- see ``from_columns``.
+    """
+
+    __slots__ = ("_ts", "_w", "_span_hi", "_kind", "period_us", "delay_us", "_segments",
+                 "_samples", "_dev")
+
+    def __init__(self, segments=(), samples=(), period_us=None, delay_us=None):
+        self.period_us = period_us
+        self.delay_us = delay_us
+        self._segments = tuple(segments) if segments else ()
+        self._samples = tuple(samples) if samples else ()
+        self._dev = {}
+        if self._segments:
+            self._kind = _native.DW_SIGNAL_STEP
+            ts, w = [], []
+            prev_end = None
+            for s, e, watts in self._segments:
+                if prev_end is not None and s != prev_end:
+                    if s < prev_end:
+                        raise SignalError("overlapping ground-truth segments are not supported")
+                    ts.append(prev_end)  # a gap integrates to nothing: hold 0 W
+                    w.append(0.0)
+                ts.append(int(s))
+                w.append(float(watts))
+                prev_end = int(e)
+            self._ts = np.asarray(ts, dtype=np.int64)
+            self._w = np.asarray(w, dtype=np.float64)
+            self._span_hi = int(self._segments[-1][1])
+        elif self._samples:
+            self._kind = _native.DW_SIGNAL_LINEAR
+            self._ts = np.fromiter((s.timestamp for s in self._samples), dtype=np.int64,
+                                   count=len(self._samples))
+            self._w = np.fromiter((s.watts for s in self._samples), dtype=np.float64,
+                                  count=len(self._samples))
+            self._span_hi = int(self._ts[-1])
+        else:
+            self._kind = None
+            self._ts = self._w = None
+            self._span_hi = None
+
+    @classmethod
+    def from_columns(cls, ts, watts, span_hi=None, kind="step", period_us=None,
+                     delay_us=None) -> "PowerSignal":
+        """A signal over existing arrays (numpy or CUDA tensors): ``kind="step"``
+        takes breakpoints ts with the last segment ending at ``span_hi``;
+        ``kind="linear"`` takes samples."""
+        sig = cls.__new__(cls)
+        sig.period_us, sig.delay_us = period_us, delay_us
+        sig._segments = None
+        sig._samples = None
+        sig._dev = {}
+        sig._ts, sig._w = ts, watts
+        if kind == "step":
+            sig._kind = _native.DW_SIGNAL_STEP
+            sig._span_hi = int(span_hi)
+        else:
+            sig._kind = _native.DW_SIGNAL_LINEAR
+            last = ts[-1].item() if isinstance(ts, torch.Tensor) else ts[-1]
+            sig._span_hi = int(last)
+        return sig
+
+    # reference fields, materialised lazily
+    @property
+    def segments(self) -> tuple:
+        if self._segments is None:
+            if self._kind != _native.DW_SIGNAL_STEP:
+                self._segments = ()
+            else:
+                ts = _host(self._ts)
+                w = _host(self._w)
+                ends = np.append(ts[1:], self._span_hi)
+                self._segments = tuple(zip(ts.tolist(), ends.tolist(), w.tolist()))
+        return self._segments
+
+    @property
+    def samples(self) -> tuple:
+        if self._samples is None:
+            if self._kind != _native.DW_SIGNAL_LINEAR:
+                self._samples = ()
+            else:
+                self._samples = tuple(PowerSample(timestamp=t, watts=w) for t, w in
+                                      zip(_host(self._ts).tolist(), _host(self._w).tolist()))
+        return self._samples
+
+    @property
+    def is_ground_truth(self) -> bool:
+        return self._kind == _native.DW_SIGNAL_STEP
+
+    def __len__(self) -> int:
+        return 0 if self._ts is None else int(self._ts.shape[0])
+
+    def span(self) -> tuple[int, int]:
+        if self._kind is None or len(self) == 0:
+            raise SignalError("empty power signal")
+        first = self._ts[0].item() if isinstance(self._ts, torch.Tensor) else self._ts[0]
+        return int(first), int(self._span_hi)
+
+    def value_at(self, t_us: float) -> float:
+        """Ground-truth value at a time point, clamped to the signal span
+        (energy.py:57-66); evaluated on the device."""
+        if not self.is_ground_truth:
+            raise SignalError("value_at requires the ground-truth form")
+        return float(_value_at(self, np.asarray([t_us], dtype=np.float64))[0])
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, PowerSignal):
+            return NotImplemented
+        return (self._kind == other._kind and self.segments == other.segments
+                and self.samples == other.samples and self.period_us == other.period_us
+                and self.delay_us == other.delay_us)
+
+    def __repr__(self) -> str:
+        kind = {0: "step", 1: "linear"}.get(self._kind, "empty")
+        return f"PowerSignal({kind}, n={len(self)}, span_hi={self._span_hi})"
+
+    # device residency
+    def _device(self):
+        dev = _native.device()
+        key = dev.index
+        if key not in self._dev:
+            self._dev[key] = (_to_dev(self._ts, torch.int64, dev), _to_dev(self._w, torch.float64, dev))
+        return self._dev[key]
+
+    def _c_signal(self, validate_order=False) -> tuple:
+        ts_d, w_d = self._device()
+        sig = _native.Signal(ts_d.data_ptr(), w_d.data_ptr(), int(ts_d.numel()),
+                             int(self._span_hi), int(self._kind), 1 if validate_order else 0)
+        return sig, (ts_d, w_d)
+
+
+def _host(a):
+    if isinstance(a, torch.Tensor):
+        return a.cpu().numpy()
+    return np.asarray(a)
+
+
+def _to_dev(a, dtype, dev):
+    if isinstance(a, torch.Tensor):
+        return a.to(device=dev, dtype=dtype).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device=dev, dtype=dtype)
+
+
+def _value_at(sig: PowerSignal, t: np.ndarray) -> np.ndarray:
+    dev = _native.device()
+    csig, keep = sig._c_signal()
+    t_d = torch.from_numpy(np.ascontiguousarray(t, dtype=np.float64)).to(dev)
+    out = torch.empty_like(t_d)
+    rc = _native.lib().dw_step_value_at(ctypes.byref(csig), _native.ptr(t_d), t_d.numel(),
+                                        _native.ptr(out), _native.stream_handle())
+    _native.check(rc, "dw_step_value_at")
+    return out.cpu().numpy()
+
+
+def ground_truth_signal(trace) -> PowerSignal:
+    """PowerSignal.from_breakpoints over the trace's power records (energy.py:85-87)."""
+    cols = TraceColumns.from_trace(trace)
+    if cols.n_power == 0:
+        raise SignalError("trace carries no power records")
+    _, span_hi = cols.signal_span()
+    sig = PowerSignal.from_columns(cols.ts, cols.watts, span_hi, "step")
+    return sig
+
+
+# ----------------------------------------------------------------- integrate
+
+
+def _raise_interval_error(lo: int, hi: int, span: tuple[int, int]):
+    if hi < lo:
+        raise SignalError("interval end precedes start")
+    raise SignalError(f"interval [{lo},{hi}] outside signal span [{span[0]},{span[1]}]")
+
+
+def integrate_many(signal: PowerSignal, lo, hi) -> torch.Tensor:
+    """Joules for many intervals at once (device tensor out).  Errors follow
+    the reference: the first invalid interval raises SignalError."""
+    if signal._kind is None or len(signal) == 0:
+        raise SignalError("empty power signal")
+    dev = _native.device()
+    lo_d = _to_dev(lo, torch.int64, dev).reshape(-1)
+    hi_d = _to_dev(hi, torch.int64, dev).reshape(-1)
+    out = torch.empty(lo_d.numel(), dtype=torch.float64, device=dev)
+    sorted_ = bool(lo_d.numel() < 2 or bool((lo_d[1:] >= lo_d[:-1]).all().item()))
+    iset = _native.IntervalSet(_native.ptr(lo_d), _native.ptr(hi_d), lo_d.numel(),
+                               _native.ptr(out), 1 if sorted_ else 0, 0)
+    csig, keep = signal._c_signal()
+    sizes = (ctypes.c_int64 * 1)(lo_d.numel())
+    L = _native.lib()
+    nbytes = L.dw_attribute_workspace_size(csig.n, sizes, 1)
+    ws = _native.Workspace.get(nbytes)
+    stream = _native.stream_handle()
+    _native.check(L.dw_attribute(ctypes.byref(csig), ctypes.byref(iset), 1, ws.data_ptr(),
+                                 ws.numel(), stream), "dw_attribute")
+    st = _native.Status()
+    L.dw_status(ws.data_ptr(), stream, ctypes.byref(st))
+    if st.bad_index[0] >= 0:
+        k = st.bad_index[0]
+        _raise_interval_error(int(lo_d[k].item()), int(hi_d[k].item()), signal.span())
+    return out
+
+
+def integrate(signal: PowerSignal, interval: tuple[int, int]) -> float:
+    """Joules over ``interval``; exact for ground truth, trapezoidal for samples
+    (energy.py:90-105)."""
+    if not isinstance(signal, PowerSignal):
+        signal = _coerce_signal(signal)
+    lo, hi = interval
+    if hi < lo:
+        raise SignalError("interval end precedes start")
+    start, end = signal.span()
+    if lo < start or hi > end:
+        raise SignalError(f"interval [{lo},{hi}] outside signal span [{start},{end}]")
+    return float(integrate_many(signal, np.array([lo]), np.array([hi]))[0].item())
+
+
+def _coerce_signal(sig) -> PowerSignal:
+    """Accept the reference's PowerSignal dataclass too."""
+    segs = getattr(sig, "segments", ())
+    samples = getattr(sig, "samples", ())
+    return PowerSignal(segments=segs, samples=samples, period_us=getattr(sig, "period_us", None),
+                       delay_us=getattr(sig, "delay_us", None))
+
+
+def mean_power(signal: PowerSignal, interval: tuple[int, int]) -> float:
+    lo, hi = interval
+    if hi <= lo:
+        return 0.0
+    return integrate(signal, interval) * US_PER_S / (hi - lo)
+
+
+# ----------------------------------------------------------------- sampler
+
+
+def _sample_times(start: int, end: int, period_us: int) -> np.ndarray:
+    k = (end - start) // period_us
+    return start + period_us * np.arange(1, k + 1, dtype=np.int64)
+
+
+def sample_signal(truth: PowerSignal, period_us: int = DEFAULT_SAMPLER_PERIOD_US,
+                  delay_us: int = DEFAULT_SAMPLER_DELAY_US, seed: int = 0) -> PowerSignal:
+    """Vendor-counter emulation (energy.py:144-172): samples every ``period_us``
+    reading the truth at (t - delay), delay ~ U[0.5, 1.5] x ``delay_us`` drawn
+    from numpy's PCG64 exactly as the reference draws it (one vectorised draw
+    equals the reference's per-sample scalar draws).  The reads run on the GPU."""
+    if not truth.is_ground_truth:
+        raise SignalError("sample_signal requires a ground-truth signal")
+    if period_us <= 0:
+        raise SignalError("sampler period must be positive")
+    rng = np.random.default_rng(seed)
+    start, end = truth.span()
+    times = _sample_times(start, end, period_us)
+    if times.size == 0:
+        times = np.array([end], dtype=np.int64)
+    if delay_us:
+        delays = rng.uniform(0.5 * delay_us, 1.5 * delay_us, size=times.size)
+        query = times.astype(np.float64) - delays
+    else:
+        query = times.astype(np.float64)
+    watts = _value_at(truth, query)
+    return PowerSignal.from_columns(times, watts, kind="linear", period_us=period_us,
+                                    delay_us=delay_us)
+
+
+def sampled_view(trace, period_us: int = DEFAULT_SAMPLER_PERIOD_US,
+                 delay_us: int = DEFAULT_SAMPLER_DELAY_US, seed: int = 0) -> PowerSignal:
+    """sample_signal anchored at the span ends (energy.py:175-189)."""
+    truth = ground_truth_signal(trace)
+    sig = sample_signal(truth, period_us, delay_us, seed)
+    start, end = truth.span()
+    ts = _host(sig._ts)
+    w = _host(sig._w)
+    if ts[0] > start:
+        ts = np.concatenate([[start], ts])
+        w = np.concatenate([[w[0]], w])
+    if ts[-1] < end:
+        ts = np.concatenate([ts, [end]])
+        w = np.concatenate([w, [w[-1]]])
+    return PowerSignal.from_columns(ts.astype(np.int64), w.astype(np.float64), kind="linear",
+                                    period_us=period_us, delay_us=delay_us)
+
+
+# ----------------------------------------------------------------- ledger
+
+
+class JoulesView(Mapping):
+    """Read-only ``dict[str, float]`` view over a joules column (the
+    reference's per_operator / per_kernel dicts, energy.py:268-269), in the
+    reference's insertion order.  Values stay in HBM until first read."""
+
+    def __init__(self, ids: Optional[Sequence[str]], joules: torch.Tensor, prefix: str = "op"):
+        self._ids = ids
+        self._dev = joules
+        self._host = None
+        self._index = None
+        self._prefix = prefix
+
+    @property
+    def tensor(self) -> torch.Tensor:
+        return self._dev
+
+    def array(self) -> np.ndarray:
+        if self._host is None:
+            self._host = self._dev.cpu().numpy()
+        return self._host
+
+    def _id(self, i: int) -> str:
+        return self._ids[i] if self._ids is not None else f"{self._prefix}{i}"
+
+    def _idx(self):
+        if self._index is None:
+            n = len(self)
+            if self._ids is not None:
+                self._index = {k: i for i, k in enumerate(self._ids)}
+            else:
+                self._index = {f"{self._prefix}{i}": i for i in range(n)}
+        return self._index
+
+    def __getitem__(self, key):
+        return float(self.array()[self._idx()[key]])
+
+    def __iter__(self):
+        if self._ids is not None:
+            return iter(self._ids)
+        return (f"{self._prefix}{i}" for i in range(len(self)))
+
+    def __len__(self):
+        return int(self._dev.numel())
+
+    def __contains__(self, key):
+        return key in self._idx()
+
+    def values(self):
+        return self.array().tolist()
+
+    def items(self):
+        return zip(iter(self), self.array().tolist())
+
+    def __repr__(self):
+        return f"JoulesView(n={len(self)})"
+
+    def __eq__(self, other):
+        if isinstance(other, Mapping):
+            return dict(self.items()) == dict(other.items())
+        return NotImplemented
+
+
+@dataclass(frozen=True)
+class EnergyLedger:
+    """Per-kernel / per-operator joules plus the idle pseudo-operator
+    (energy.py:263-277)."""
+
+    method: str
+    per_kernel: Mapping[str, float]
+    per_operator: Mapping[str, float]
+    idle_joules: float
+    total_joules: float
+    op_total: Optional[float] = None  # exact device sum (operator_total)
+
+    def operator_total(self) -> float:
+        if self.op_total is not None:
+            return self.op_total
+        return sum(self.per_operator.values())
+
+    def subgraph_joules(self, op_ids: Iterable[str]) -> float:
+        return sum(self.per_operator[o] for o in op_ids)
+
+    def operator_tensor(self) -> Optional[torch.Tensor]:
+        return getattr(self.per_operator, "tensor", None)
+
+    def kernel_tensor(self) -> Optional[torch.Tensor]:
+        return getattr(self.per_kernel, "tensor", None)
+
+
+def _run_ledger(cols: TraceColumns, sig: PowerSignal, validate_order: bool):
+    """dw_ledger on the device; returns (per_op, per_k, total, op_total, idle)."""
+    dev = _native.device()
+    L = _native.lib()
+    op_s, op_e = cols.device("op_start"), cols.device("op_end")
+    k_s, k_e = cols.device("k_start"), cols.device("k_end")
+    per_op = torch.empty(cols.n_ops, dtype=torch.float64, device=dev)
+    per_k = torch.empty(cols.n_kernels, dtype=torch.float64, device=dev)
+    ops = _native.IntervalSet(_native.ptr(op_s), _native.ptr(op_e), cols.n_ops,
+                              _native.ptr(per_op), 1 if cols.ops_sorted else 0, 0)
+    kers = _native.IntervalSet(_native.ptr(k_s), _native.ptr(k_e), cols.n_kernels,
+                               _native.ptr(per_k), 1 if cols.kernels_sorted else 0, 0)
+    csig, keep = sig._c_signal(validate_order)
+    sizes = (ctypes.c_int64 * 2)(cols.n_ops, cols.n_kernels)
+    nbytes = L.dw_attribute_workspace_size(csig.n, sizes, 2)
+    ws = _native.Workspace.get(nbytes)
+    stream = _native.stream_handle()
+    _native.check(L.dw_ledger(ctypes.byref(csig), ctypes.byref(ops), ctypes.byref(kers),
+                              ws.data_ptr(), ws.numel(), stream), "dw_ledger")
+    st = _native.Status()
+    L.dw_status(ws.data_ptr(), stream, ctypes.byref(st))
+    return per_op, per_k, st
+
+
+def _raise_ledger_errors(cols: TraceColumns, st, span):
+    """First failing interval in build_ledger's iteration order (op, then its
+    kernels; energy.py:305-316) raises the reference's SignalError."""
+    if st.order_index >= 0:
+        from .trace_model import TraceError
+        raise TraceError("power samples must be strictly increasing in timestamp")
+    for j in (0, 1):
+        if st.unsorted_index[j] >= 0:
+            raise RuntimeError("internal: interval set flagged sorted is not sorted")
+    bad_op, bad_k = st.bad_index[0], st.bad_index[1]
+    if bad_op < 0 and bad_k < 0:
+        return
+    owner = None
+    if bad_k >= 0:
+        k_op = cols.k_op
+        owner = int(k_op[bad_k].item() if isinstance(k_op, torch.Tensor) else k_op[bad_k]) \
+            if k_op is not None else bad_k
+    if bad_op >= 0 and (owner is None or bad_op <= owner):
+        lo, hi = _read_pair(cols, "op_start", "op_end", bad_op)
+    else:
+        lo, hi = _read_pair(cols, "k_start", "k_end", bad_k)
+    _raise_interval_error(lo, hi, span)
+
+
+def _read_pair(cols, a, b, i):
+    x, y = getattr(cols, a), getattr(cols, b)
+    if isinstance(x, torch.Tensor):
+        return int(x[i].item()), int(y[i].item())
+    return int(x[i]), int(y[i])
+
+
+def build_ledger(trace, method: str = "ground_truth",
+                 period_us: int = DEFAULT_SAMPLER_PERIOD_US,
+                 delay_us: int = DEFAULT_SAMPLER_DELAY_US, repeat: int = DEFAULT_REPLAY_REPEAT,
+                 seed: int = 0, validate_order: bool = False) -> EnergyLedger:
+    """Attribute energy to kernels and operators (energy.py:280-331).
+
+    ``trace`` is a reference-style Trace (the reference's own objects work) or a
+    TraceColumns.  Gaps between kernels inside an operator's interval go to the
+    operator; gaps between operators go to ``idle``.
+    """
+    if method not in METHODS:
+        raise ValueError(f"unknown energy method {method!r}")
+    cols = TraceColumns.from_trace(trace)
+    truth = ground_truth_signal(cols)
+    if method == "replay":
+        from .replay import replay_ledger
+        return replay_ledger(trace, cols, truth, repeat, period_us, delay_us, seed)
+    if method == "ground_truth":
+        signal = truth
+    else:
+        signal = sampled_view(cols, period_us, delay_us, seed)
+    per_op, per_k, st = _run_ledger(cols, signal, validate_order)
+    _raise_ledger_errors(cols, st, truth.span())
+    total, op_total, idle = st.totals[0], st.totals[1], st.totals[2]
+    return EnergyLedger(method=method,
+                        per_kernel=JoulesView(cols.k_ids, per_k, "k"),
+                        per_operator=JoulesView(cols.op_ids, per_op, "op"),
+                        idle_joules=float(idle), total_joules=float(total),
+                        op_total=float(op_total))

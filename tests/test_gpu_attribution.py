@@ -1,0 +1,183 @@
+"""GPU parity: libdwb200 attribution vs the reference's golden vectors and the
+CPU oracle.  Bit-exact wherever the interval spans <= DW_DIRECT_MAX segments
+(the reference's own sequential fp64 sum); the fixed-point path for longer
+intervals is bit-exact against the oracle's MODE_DEVICE and within 1e-12
+relative of the reference."""
+import json
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import GOLDEN, load_scenario, scenario_names
+
+pytestmark = pytest.mark.gpu
+
+dw = pytest.importorskip("paper_2512_08365_b200")
+from paper_2512_08365_b200 import PowerSignal, SignalError, TraceColumns, build_ledger  # noqa: E402
+from paper_2512_08365_b200 import energy as E  # noqa: E402
+from paper_2512_08365_b200.trace_model import TraceError  # noqa: E402
+
+
+def _signals(g, with_span):
+    for s in range(len(g["sig_off"]) - 1):
+        sl = slice(g["sig_off"][s], g["sig_off"][s + 1])
+        iv = slice(g["iv_off"][s], g["iv_off"][s + 1])
+        span_hi = int(g["span"][s][1]) if with_span else None
+        yield g["ts"][sl], g["watts"][sl], span_hi, g["lo"][iv], g["hi"][iv], g["joules"][iv]
+
+
+def _nseg(ts, lo, hi):
+    a = np.searchsorted(ts, lo, side="right") - 1
+    b = np.searchsorted(ts, hi, side="left") - 1
+    return np.where(hi > lo, b - a + 1, 0)
+
+
+def test_step_golden(golden_step):
+    for ts, w, span_hi, lo, hi, ref in _signals(golden_step, True):
+        sig = PowerSignal.from_columns(ts, w, span_hi, "step")
+        got = E.integrate_many(sig, lo, hi).cpu().numpy()
+        short = _nseg(ts, lo, hi) <= oracle.DW_DIRECT_MAX
+        np.testing.assert_array_equal(got[short], ref[short])
+        np.testing.assert_allclose(got[~short], ref[~short], rtol=1e-12, atol=0)
+        np.testing.assert_array_equal(
+            got, oracle.integrate_step(ts, w, span_hi, lo, hi, oracle.MODE_DEVICE))
+
+
+def test_linear_golden(golden_linear):
+    for ts, w, _, lo, hi, ref in _signals(golden_linear, False):
+        sig = PowerSignal.from_columns(ts, w, kind="linear")
+        got = E.integrate_many(sig, lo, hi).cpu().numpy()
+        dev = oracle.integrate_linear(ts, w, lo, hi, oracle.MODE_DEVICE)
+        np.testing.assert_array_equal(got, dev)
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-300)
+
+
+def _cols(sc, side):
+    return TraceColumns.from_arrays(
+        sc[f"{side}_ts"], sc[f"{side}_watts"], sc[f"{side}_op_start"], sc[f"{side}_op_end"],
+        sc[f"{side}_k_start"], sc[f"{side}_k_end"], sc[f"{side}_k_op"],
+        trace_end=int(max(sc[f"{side}_span"][1] - 1, sc[f"{side}_ts"][-1])),
+        op_ids=[str(x) for x in sc[f"{side}_op_ids"]], k_ids=[str(x) for x in sc[f"{side}_k_ids"]])
+
+
+@pytest.mark.parametrize("name", scenario_names())
+def test_ledger_golden(name):
+    sc = load_scenario(name)
+    for side in ("a", "b"):
+        cols = _cols(sc, side)
+        assert cols.signal_span()[1] == sc[f"{side}_span"][1]
+        led = build_ledger(cols)
+        np.testing.assert_array_equal(led.per_operator.array(), sc[f"gt_{side}_per_op"])
+        np.testing.assert_array_equal(led.per_kernel.array(), sc[f"gt_{side}_per_k"])
+        total, idle = sc[f"gt_{side}_total_idle"]
+        assert led.total_joules == pytest.approx(total, rel=1e-12, abs=0)
+        assert abs(led.idle_joules - idle) <= 1e-12 * total
+        for tag, period, delay in (("s40", 40_000, 200_000), ("s1", 1_000, 0)):
+            if f"{tag}_{side}_per_op" not in sc:
+                continue
+            view = E.sampled_view(cols, period, delay, 0)
+            np.testing.assert_array_equal(E._host(view._ts), sc[f"{tag}_{side}_view_ts"])
+            np.testing.assert_array_equal(E._host(view._w), sc[f"{tag}_{side}_view_watts"])
+            led = build_ledger(cols, method="sampled", period_us=period, delay_us=delay, seed=0)
+            np.testing.assert_array_equal(led.per_operator.array(), sc[f"{tag}_{side}_per_op"])
+            np.testing.assert_array_equal(led.per_kernel.array(), sc[f"{tag}_{side}_per_k"])
+            total, idle = sc[f"{tag}_{side}_total_idle"]
+            assert led.total_joules == pytest.approx(total, rel=1e-12, abs=0)
+            assert abs(led.idle_joules - idle) <= 1e-12 * total
+
+
+def test_error_messages_match_reference():
+    with open(GOLDEN / "errors.json") as fh:
+        msgs = json.load(fh)
+    sig = PowerSignal(segments=((10, 100, 50.0), (100, 150, 70.0)))
+    for name, iv in (("outside_lo", (0, 100)), ("outside_hi", (20, 151)), ("reversed", (60, 50))):
+        with pytest.raises(SignalError) as ei:
+            E.integrate(sig, iv)
+        assert str(ei.value) == msgs[name]
+    with pytest.raises(SignalError) as ei:
+        PowerSignal().span()
+    assert str(ei.value) == msgs["empty"]
+
+
+def test_ledger_reports_first_bad_interval_in_reference_order():
+    ts = np.array([100, 200, 300], dtype=np.int64)
+    w = np.array([10.0, 20.0, 30.0])
+    # op 1's kernel is bad, op 2 is bad: the kernel (visited first) is reported
+    cols = TraceColumns.from_arrays(ts, w, np.array([100, 150, 250]), np.array([140, 260, 290]),
+                                    np.array([110, 149, 255]), np.array([120, 160, 280]),
+                                    np.array([0, 1, 2], dtype=np.int32), trace_end=300)
+    led = build_ledger(cols)
+    assert led.per_operator.array().shape == (3,)
+    bad = TraceColumns.from_arrays(ts, w, np.array([100, 150, 250]), np.array([140, 260, 240]),
+                                   np.array([110, 90, 255]), np.array([120, 160, 280]),
+                                   np.array([0, 1, 2], dtype=np.int32), trace_end=300)
+    with pytest.raises(SignalError, match=r"interval \[90,160\] outside signal span \[100,301\]"):
+        build_ledger(bad)
+    bad2 = TraceColumns.from_arrays(ts, w, np.array([100, 150, 250]), np.array([140, 140, 290]),
+                                    np.array([110, 150, 255]), np.array([120, 160, 280]),
+                                    np.array([0, 1, 2], dtype=np.int32), trace_end=300)
+    with pytest.raises(SignalError, match="interval end precedes start"):
+        build_ledger(bad2)
+
+
+def test_power_order_validated():
+    ts = np.array([100, 200, 200, 300], dtype=np.int64)
+    cols = TraceColumns.from_arrays(ts, np.ones(4), np.array([100]), np.array([150]))
+    with pytest.raises(TraceError, match="strictly increasing"):
+        build_ledger(cols, validate_order=True)
+
+
+def _random_case(seed, S, n, max_len, dense=False):
+    rng = np.random.default_rng(seed)
+    gaps = rng.integers(1, 4 if dense else 300, size=S)
+    ts = np.cumsum(gaps).astype(np.int64)
+    w = rng.uniform(50, 900, size=S)
+    span_hi = int(ts[-1]) + int(rng.integers(1, 500))
+    lo = np.sort(rng.integers(ts[0], span_hi, size=n))
+    ln = (rng.pareto(1.2, size=n) * max_len / 20).astype(np.int64)
+    hi = np.minimum(lo + ln, span_hi)
+    return ts, w, span_hi, lo, hi
+
+
+@pytest.mark.parametrize("seed,S,n,max_len", [(1, 300_000, 200_000, 3000), (2, 2_000_001, 500_000, 40_000),
+                                              (3, 5000, 100_000, 100)])
+def test_random_step_vs_oracle(seed, S, n, max_len):
+    ts, w, span_hi, lo, hi = _random_case(seed, S, n, max_len)
+    sig = PowerSignal.from_columns(ts, w, span_hi, "step")
+    got = E.integrate_many(sig, lo, hi).cpu().numpy()
+    np.testing.assert_array_equal(got, oracle.integrate_step(ts, w, span_hi, lo, hi, oracle.MODE_DEVICE))
+    ref = oracle.integrate_step(ts, w, span_hi, lo, hi, oracle.MODE_REFERENCE)
+    np.testing.assert_allclose(got, ref, rtol=1e-11, atol=0)
+
+
+@pytest.mark.parametrize("seed,S,n,max_len", [(4, 300_000, 200_000, 3000), (5, 1_000_003, 300_000, 20_000)])
+def test_random_linear_vs_oracle(seed, S, n, max_len):
+    ts, w, span_hi, lo, hi = _random_case(seed, S, n, max_len)
+    hi = np.minimum(hi, ts[-1])
+    lo = np.minimum(lo, hi)
+    sig = PowerSignal.from_columns(ts, w, kind="linear")
+    got = E.integrate_many(sig, lo, hi).cpu().numpy()
+    np.testing.assert_array_equal(got, oracle.integrate_linear(ts, w, lo, hi, oracle.MODE_DEVICE))
+
+
+def test_unsorted_sets_match_sorted():
+    ts, w, span_hi, lo, hi = _random_case(7, 100_000, 50_000, 2000)
+    perm = np.random.default_rng(0).permutation(lo.size)
+    sig = PowerSignal.from_columns(ts, w, span_hi, "step")
+    a = E.integrate_many(sig, lo, hi).cpu().numpy()
+    b = E.integrate_many(sig, lo[perm], hi[perm]).cpu().numpy()
+    np.testing.assert_array_equal(a[perm], b)
+
+
+def test_ledger_total_long_and_idle():
+    ts, w, span_hi, lo, hi = _random_case(8, 200_000, 20_000, 500)
+    cols = TraceColumns.from_arrays(ts, w, lo, hi, trace_end=span_hi - 1)
+    led = build_ledger(cols)
+    allseg = oracle.integrate_step(ts, w, span_hi, [ts[0]], [span_hi], oracle.MODE_DEVICE)[0]
+    assert led.total_joules == allseg
+    ref_total = oracle.integrate_step(ts, w, span_hi, [ts[0]], [span_hi], oracle.MODE_REFERENCE)[0]
+    assert led.total_joules == pytest.approx(ref_total, rel=1e-12)
+    assert led.operator_total() == oracle.fx_sum(led.per_operator.array())
+    assert led.idle_joules == max(led.total_joules - led.operator_total(), 0.0)

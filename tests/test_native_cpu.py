@@ -1,0 +1,41 @@
+"""CPU-side checks of the native boundary: the C-ABI library loads, exports
+every symbol include/dwb200.h declares, and the package fails loudly (never
+falls back) when no GPU is present."""
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+import torch
+
+from conftest import ROOT
+
+import paper_2512_08365_b200 as dw
+from paper_2512_08365_b200 import _native, build
+
+
+def _declared():
+    text = (ROOT / "include" / "dwb200.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:[\w\s\*]+?)\b(dw_\w+)\s*\(", text, re.M)))
+
+
+def test_header_declares_exactly_the_exported_list():
+    assert _declared() == sorted(_native.EXPORTED)
+
+
+def test_library_builds_and_exports_every_symbol():
+    build.build()
+    L = ctypes.CDLL(str(_native.LIB_PATH))
+    for name in _native.EXPORTED:
+        assert hasattr(L, name), name
+    assert _native.version().startswith("dwb200")
+    assert _native.error_string(_native.DW_E_SPAN) == "interval outside signal span"
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback_without_gpu():
+    import numpy as np
+    cols = dw.TraceColumns.from_arrays(np.array([0, 10]), np.array([1.0, 2.0]),
+                                       np.array([0]), np.array([5]))
+    with pytest.raises(_native.NativeUnavailable):
+        dw.build_ledger(cols)
