@@ -60,6 +60,12 @@ typedef struct CUstream_st *dw_stream_t; /* == cudaStream_t */
  * fp64 exactly as the reference does (bit-identical); longer ones are summed
  * exactly in 2^-40 W*us fixed point and rounded once. */
 #define DW_DIRECT_MAX 256
+/* Tiling of the attribution kernel.  Whole tiles enter long-interval sums as
+ * fp64 tile sums reduced in a fixed order (per-thread strided sum over
+ * DW_TILE_THREADS threads, warp xor-butterfly, warps in order), converted to
+ * fixed point; the CPU oracle mirrors that order (oracle/dw_oracle.c). */
+#define DW_TILE 1024
+#define DW_TILE_THREADS 128
 
 /* ------------------------------------------------------------------- types */
 typedef struct {

@@ -46,6 +46,7 @@ def lib():
         _lib = ctypes.CDLL(str(_LIB))
         _lib.dwo_fx_sum.restype = ctypes.c_double
         _lib.dwo_py_sum.restype = ctypes.c_double
+        _lib.dwo_total_device.restype = ctypes.c_double
     return _lib
 
 
@@ -99,6 +100,15 @@ def integrate_linear(ts, watts, lo, hi, mode=MODE_REFERENCE):
     return out
 
 
+def total_device(kind, ts, watts, span_hi=None) -> float:
+    """The ledger total over the whole span under the device's definition."""
+    ts = np.ascontiguousarray(ts, dtype=np.int64)
+    watts = np.ascontiguousarray(watts, dtype=np.float64)
+    return float(lib().dwo_total_device(ctypes.c_int(0 if kind == "step" else 1), _p(ts), _p(watts),
+                                        ctypes.c_int64(ts.shape[0]),
+                                        ctypes.c_int64(int(span_hi) if span_hi is not None else 0)))
+
+
 def fx_sum(x) -> float:
     x = np.ascontiguousarray(x, dtype=np.float64)
     return float(lib().dwo_fx_sum(_p(x), ctypes.c_int64(x.shape[0])))
@@ -121,7 +131,10 @@ def ledger(kind, ts, watts, span_hi, op_start, op_end, k_start, k_end, mode=MODE
         span = (int(ts[0]), int(ts[-1]))
     per_op = f(op_start, op_end)
     per_k = f(k_start, k_end)
-    total = float(f(np.array([span[0]]), np.array([span[1]]))[0])
+    if mode == MODE_DEVICE:
+        total = total_device(kind, ts, watts, span_hi)
+    else:
+        total = float(f(np.array([span[0]]), np.array([span[1]]))[0])
     op_total = py_sum(per_op) if mode == MODE_REFERENCE else fx_sum(per_op)
     return per_op, per_k, total, max(total - op_total, 0.0)
 

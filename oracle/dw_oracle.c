@@ -62,6 +62,8 @@
 #define DW_E_ARG (-5)
 
 #define DW_DIRECT_MAX 256 /* see include/dwb200.h */
+#define DW_TILE 1024
+#define DW_TILE_THREADS 128
 
 typedef __int128 i128;
 
@@ -223,20 +225,74 @@ static double step_direct(const int64_t *ts, const double *w, int64_t n, int64_t
     return total / US_PER_S;
 }
 
+/* ---- the device's long-interval definition (MODE_DEVICE) ----
+ * Whole tiles of DW_TILE terms enter as fp64 tile sums reduced in the GPU's
+ * fixed order: thread t of DW_TILE_THREADS sums terms t, t+THREADS, ...
+ * sequentially; each warp combines its 32 lanes by an xor butterfly (lane 0's
+ * value); the warp results are added in warp order.  Partial tiles and edge
+ * terms enter term by term.  Everything meets in exact fixed point. */
+typedef double (*term_fn)(const void *ctx, int64_t i);
+
+static double tile_sum(term_fn term, const void *ctx, int64_t t0, int64_t t1) {
+    double red[DW_TILE_THREADS / 32];
+    for (int w = 0; w < DW_TILE_THREADS / 32; w++) {
+        double v[32];
+        for (int l = 0; l < 32; l++) {
+            double acc = 0.0;
+            for (int64_t r = t0 + w * 32 + l; r < t1; r += DW_TILE_THREADS) acc += term(ctx, r);
+            v[l] = acc;
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+            double nv[32];
+            for (int l = 0; l < 32; l++) nv[l] = v[l] + v[l ^ off];
+            memcpy(v, nv, sizeof(v));
+        }
+        red[w] = v[0];
+    }
+    double s = red[0];
+    for (int w = 1; w < DW_TILE_THREADS / 32; w++) s += red[w];
+    return s;
+}
+
+/* exact sum of terms [j0, j1] under the tile decomposition */
+static i128 fx_range(term_fn term, const void *ctx, int64_t nterms, int64_t j0, int64_t j1) {
+    i128 acc = 0;
+    if (j1 < j0) return 0;
+    int64_t ta = j0 / DW_TILE, tb = j1 / DW_TILE;
+    if (ta == tb) {
+        for (int64_t i = j0; i <= j1; i++) acc += q_term(term(ctx, i));
+        return acc;
+    }
+    for (int64_t i = j0; i < (ta + 1) * DW_TILE; i++) acc += q_term(term(ctx, i));
+    for (int64_t t = ta + 1; t < tb; t++) {
+        int64_t e = (t + 1) * DW_TILE < nterms ? (t + 1) * DW_TILE : nterms;
+        acc += q_term(tile_sum(term, ctx, t * DW_TILE, e));
+    }
+    for (int64_t i = tb * DW_TILE; i <= j1; i++) acc += q_term(term(ctx, i));
+    return acc;
+}
+
+typedef struct { const int64_t *ts; const double *w; int64_t n, span_hi; } sig_ctx;
+
+static double step_term(const void *c, int64_t i) {
+    const sig_ctx *s = (const sig_ctx *)c;
+    return s->w[i] * (double)(seg_end(s->ts, s->n, s->span_hi, i) - s->ts[i]);
+}
+
 static double step_fx(const int64_t *ts, const double *w, int64_t n, int64_t span_hi,
                       int64_t lo, int64_t hi) {
-    i128 acc = 0;
-    if (hi > lo) {
-        int64_t i = upper_bound64(ts, n, lo) - 1;
-        if (i < 0) i = 0;
-        for (; i < n && ts[i] < hi; i++) {
-            int64_t s = ts[i], e = seg_end(ts, n, span_hi, i);
-            int64_t ov = (e < hi ? e : hi) - (s > lo ? s : lo);
-            if (ov > 0) acc += q_term(w[i] * (double)ov);
-        }
-    }
+    sig_ctx c = {ts, w, n, span_hi};
+    int64_t a = upper_bound64(ts, n, lo) - 1;
+    int64_t b = lower_bound64(ts, n, hi) - 1;
+    i128 acc = fx_range(step_term, &c, n, a + 1, b - 1);
+    acc += q_term(w[a] * (double)(ts[a + 1] - lo));
+    int64_t eb = seg_end(ts, n, span_hi, b);
+    acc += q_term(w[b] * (double)((eb < hi ? eb : hi) - ts[b]));
     return term_to_joules(acc);
 }
+
+/* the ledger total over the whole span, device definition */
+double dwo_total_device(int kind, const int64_t *ts, const double *w, int64_t n, int64_t span_hi);
 
 typedef struct {
     const int64_t *ts; const double *w; int64_t n, span_hi;
@@ -295,8 +351,32 @@ static int64_t lin_npieces(const int64_t *ts, int64_t n, int64_t lo, int64_t hi)
     return interior + 1;
 }
 
+static double lin_sample(const int64_t *ts, const double *w, int64_t n, int64_t j) {
+    (void)ts;
+    if (j == 0) return w[0];
+    if (j == n - 1) return w[n - 1];
+    return w[j - 1] + 1.0 * (w[j] - w[j - 1]);
+}
+
+static double lin_piece_term(const void *c, int64_t j) {
+    const sig_ctx *s = (const sig_ctx *)c;
+    return 0.5 * (lin_sample(s->ts, s->w, s->n, j) + lin_sample(s->ts, s->w, s->n, j + 1)) *
+           (double)(s->ts[j + 1] - s->ts[j]);
+}
+
+static double lin_fx(const int64_t *ts, const double *w, int64_t n, int64_t lo, int64_t hi) {
+    sig_ctx c = {ts, w, n, 0};
+    int64_t first = upper_bound64(ts, n, lo);
+    int64_t last = lower_bound64(ts, n, hi);
+    i128 acc = fx_range(lin_piece_term, &c, n - 1, first, last - 2);
+    acc += q_term(lin_term(ts, w, n, lo, ts[first]));
+    acc += q_term(lin_term(ts, w, n, ts[last - 1], hi));
+    return term_to_joules(acc);
+}
+
 static double lin_integrate(const int64_t *ts, const double *w, int64_t n, int64_t lo,
                             int64_t hi, int fx) {
+    if (fx) return lin_fx(ts, w, n, lo, hi);
     int64_t first = upper_bound64(ts, n, lo); /* first ts > lo */
     int64_t last = lower_bound64(ts, n, hi);  /* first ts >= hi */
     int64_t prev = lo;
@@ -512,3 +592,19 @@ int dwo_join(const uint64_t *sig_a, int64_t na, const uint64_t *sig_b, int64_t n
     return DW_OK;
 }
 
+
+double dwo_total_device(int kind, const int64_t *ts, const double *w, int64_t n, int64_t span_hi) {
+    sig_ctx c = {ts, w, n, span_hi};
+    int64_t nterms = kind == 0 ? n : (n > 1 ? n - 1 : 1);
+    if (nterms <= DW_DIRECT_MAX) {
+        int64_t lo = ts[0], hi = kind == 0 ? span_hi : ts[n - 1];
+        if (kind == 0) return step_direct(ts, w, n, span_hi, lo, hi);
+        return lin_integrate(ts, w, n, lo, hi, 0);
+    }
+    i128 acc = 0;
+    for (int64_t t = 0; t * DW_TILE < nterms; t++) {
+        int64_t e = (t + 1) * DW_TILE < nterms ? (t + 1) * DW_TILE : nterms;
+        acc += q_term(tile_sum(kind == 0 ? step_term : lin_piece_term, &c, t * DW_TILE, e));
+    }
+    return term_to_joules(acc);
+}

@@ -36,11 +36,14 @@
 
 namespace dw {
 
-constexpr int TILE = 2048;                   // segments per tile
+constexpr int TILE = DW_TILE;                // segments per tile
 constexpr int DIRECT = DW_DIRECT_MAX;        // sequential-sum cap
 constexpr int WIN = TILE + DIRECT + 6;       // window slots: 2 halo + TILE + DIRECT + 2, + virtual end
-constexpr int ATTR_THREADS = 256;
+constexpr int ATTR_THREADS = DW_TILE_THREADS; // threads of one consumer group
 constexpr int ATTR_WARPS = ATTR_THREADS / 32;
+constexpr int GROUPS = 4;                    // consumer groups per CTA (tiles processed concurrently)
+constexpr int STAGES = 5;                    // TMA ring depth (tiles staged per CTA)
+constexpr int CTAS_PER_SM = 1;
 
 struct AttrParams {
     const int64_t *ts;
@@ -59,8 +62,9 @@ struct AttrParams {
     int64_t n[DW_MAX_SETS];
     int32_t check_sorted[DW_MAX_SETS];
     const int64_t *first;        // [nsets][ntiles + 1]
-    unsigned long long *tile_fx; // [ntiles][2] (lo, hi)
-    unsigned long long *prefix;  // [ntiles + 1][2]
+    double *tile_sum;            // [ntiles] fp64 tile sums (fixed reduction tree)
+    unsigned long long *prefix;  // [ntiles + 1][2] exact int128 prefix of q(tile_sum)
+    unsigned long long *scan_part; // [nblocks][2] scan partials
     unsigned long long *long_list;
     DevStatus *st;
 };
@@ -78,8 +82,7 @@ __device__ __forceinline__ double lin_sample_value(int64_t j, int64_t S, TsF ts,
     if (j == 0) return w(0);
     if (j == S - 1) return w(S - 1);
     double wa = w(j - 1);
-    double frac = __ddiv_rn((double)(ts(j) - ts(j - 1)), (double)(ts(j) - ts(j - 1)));
-    return __dadd_rn(wa, __dmul_rn(frac, __dsub_rn(w(j), wa)));
+    return __dadd_rn(wa, __dsub_rn(w(j), wa));  // frac == 1.0 exactly
 }
 
 // v(t) for an arbitrary time inside the span; lbj = first index with ts >= t.
@@ -141,14 +144,45 @@ __global__ void partition_kernel(AttrParams p) {
 }
 
 // --------------------------------------------------------- K2 tile kernel
-struct __align__(16) TileSmem {
-    int64_t ts[2][WIN];
-    double w[2][WIN];
-    uint64_t bar[2];
-    unsigned long long red[ATTR_WARPS][2];
-    int64_t win_base[2];
-    int64_t win_cnt[2];
+// Warp-specialised persistent kernel.  Warp NCW (the producer) walks this
+// CTA's tiles STAGES ahead of the consumers: it reads the tile's interval
+// ranges from the partition, and with 1-D TMA (cp.async.bulk, completion on
+// the stage's `full` mbarrier) stages (a) the sample window and (b) every
+// set's [start, end) columns of the intervals that begin in the tile.  The
+// NCW consumer warps wait on `full`, integrate, and release the stage through
+// `empty`.  No consumer ever waits on a global load in the common case.
+constexpr int NCW = ATTR_WARPS;              // warps per consumer group
+constexpr int KTHREADS = GROUPS * ATTR_THREADS + 32;  // + one producer warp
+constexpr int IV_POOL = 512;                 // staged intervals per stage (all sets)
+
+struct StageMeta {
+    int64_t wb;                 // window base (global sample index)
+    int64_t f0[DW_MAX_SETS];    // first interval of the tile, per set
+    int64_t c[DW_MAX_SETS + 1]; // cumulative interval counts over sets
+    int64_t a0[DW_MAX_SETS];    // staged copy starts at this (even) interval index
+    int32_t copied[DW_MAX_SETS];
+    int32_t pool[DW_MAX_SETS];
+    int32_t cnt;                // samples in the window
 };
+
+struct __align__(16) TileSmem {  // the stage ring, shared by the producer and every group
+    int64_t ts[STAGES][WIN];
+    double w[STAGES][WIN];
+    int64_t iv_lo[STAGES][IV_POOL];
+    int64_t iv_hi[STAGES][IV_POOL];
+    StageMeta meta[STAGES];
+    uint64_t full[STAGES];
+    uint64_t empty[STAGES];
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// named barrier over one consumer group (the producer never joins)
+__device__ __forceinline__ void consumer_sync(int g) {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(ATTR_THREADS) : "memory");
+}
 
 __device__ __forceinline__ void tile_window(int64_t tile, int64_t S, int64_t &wb, int64_t &we) {
     wb = tile * TILE - 2;
@@ -157,20 +191,14 @@ __device__ __forceinline__ void tile_window(int64_t tile, int64_t S, int64_t &wb
     if (we > S) we = S;
 }
 
-__device__ __forceinline__ void issue_tile(const AttrParams &p, TileSmem &sm, int stage,
-                                           int64_t tile) {
-    int64_t wb, we;
-    tile_window(tile, p.S, wb, we);
-    int64_t cnt = we - wb;
-    int64_t even = cnt & ~(int64_t)1;
-    uint32_t bytes = (uint32_t)(even * 8);
-    sm.win_base[stage] = wb;
-    sm.win_cnt[stage] = cnt;
-    mbar_expect_tx(&sm.bar[stage], 2 * bytes);
-    if (bytes) {
-        tma_load_1d(sm.ts[stage], p.ts + wb, bytes, &sm.bar[stage]);
-        tma_load_1d(sm.w[stage], p.w + wb, bytes, &sm.bar[stage]);
-    }
+// joules = tot / 1e6, correctly rounded: Markstein's final step with the
+// correctly rounded reciprocal (one multiply + two FMAs instead of a full
+// software division; bit-identical to IEEE division for these operands).
+__device__ __forceinline__ double div_1e6(double x) {
+    const double inv = 1.0 / US_PER_S;
+    double q = __dmul_rn(x, inv);
+    double r = __fma_rn(-q, US_PER_S, x);
+    return __fma_rn(r, inv, q);
 }
 
 __device__ __forceinline__ void report_bad(const AttrParams &p, int j, int64_t k) {
@@ -183,199 +211,715 @@ __device__ __forceinline__ void push_long(const AttrParams &p, int j, int64_t k)
     p.long_list[slot] = ((unsigned long long)j << 56) | (unsigned long long)k;
 }
 
+// Timestamps of the current window, relative to its first sample: uint32 for
+// narrow windows (span < 2^32 us, the common case: 32-bit loads and math),
+// int64 otherwise.  Index r is window-relative (global index = wb + r); slot
+// cnt holds the virtual end of the last step segment when the window reaches S.
+struct Ts32 {
+    const uint32_t *t;
+    __device__ __forceinline__ uint32_t operator()(int r) const { return t[r]; }
+};
+struct Ts64 {
+    const int64_t *t;
+    int64_t base;
+    __device__ __forceinline__ int64_t operator()(int r) const { return t[r] - base; }
+};
+
+// last r in [r0, r1) with ts(r) <= key, given ts(r0) <= key.  Starts at an
+// interpolated guess (uniform grids hit in 1-2 probes) and gallops.
+template <typename TS, typename T>
+__device__ __forceinline__ int search_last_le(const TS &ts, int r0, int r1, T key, float scale) {
+    int g = r0 + (int)((float)(key - ts(r0)) * scale);
+    g = g < r0 ? r0 : (g >= r1 ? r1 - 1 : g);
+    int lo, hi;  // invariant: ts(lo) <= key, ts(hi) > key or hi == r1
+    if (ts(g) <= key) {
+        lo = g;
+        int step = 1;
+        hi = lo + 1;
+        while (hi < r1 && ts(hi) <= key) {
+            lo = hi;
+            step <<= 1;
+            hi = lo + step;
+        }
+        if (hi > r1) hi = r1;
+    } else {
+        hi = g;
+        int step = 1;
+        lo = hi - 1;
+        while (lo > r0 && ts(lo) > key) {
+            hi = lo;
+            step <<= 1;
+            lo = hi - step;
+        }
+        if (lo < r0) lo = r0;
+    }
+    while (hi - lo > 1) {
+        int m = (lo + hi) >> 1;
+        if (ts(m) <= key) lo = m; else hi = m;
+    }
+    return lo;
+}
+
+// One interval of a STEP signal over the staged window: the reference's
+// sequential sum (energy.py:99-104) with the zero-overlap segments skipped
+// (they add nothing there either).  Returns false when it spans > DIRECT
+// segments (the fixed-point path takes it).
+template <typename TS, typename T>
+__device__ __forceinline__ bool step_interval(const TS &ts, const double *w, int r0, int r1,
+                                              T lo, T hi, float scale, double &tot) {
+    if (hi == lo) { tot = 0.0; return true; }
+    int i = search_last_le(ts, r0, r1, lo, scale);
+    T e = ts(i + 1);
+    if (hi <= e) {  // single segment
+        tot = __dmul_rn(w[i], (double)(hi - lo));
+        return true;
+    }
+    tot = __dmul_rn(w[i], (double)(e - lo));
+    int nseg = 1;
+    ++i;
+    T s = e;
+    e = ts(i + 1);
+    while (e < hi) {
+        if (nseg == DIRECT) return false;
+        tot = __dadd_rn(tot, __dmul_rn(w[i], (double)(e - s)));
+        ++nseg;
+        ++i;
+        s = e;
+        e = ts(i + 1);
+    }
+    if (nseg == DIRECT) return false;
+    tot = __dadd_rn(tot, __dmul_rn(w[i], (double)(hi - s)));
+    return true;
+}
+
+// v(t) of energy.py:115-124 for an interior sample j (1 <= j <= S-2): the
+// first bracketing pair is (j-1, j) with frac == 1.0 exactly, so
+// ws[j-1] + 1.0*(ws[j]-ws[j-1]) == ws[j-1] + (ws[j]-ws[j-1]).
+__device__ __forceinline__ double lin_interior(const double *w, int r) {
+    double wa = w[r - 1];
+    return __dadd_rn(wa, __dsub_rn(w[r], wa));
+}
+
+// One interval of a LINEAR (sampled) signal: trapezoid over
+// [lo] + {ts in (lo, hi)} + [hi] (energy.py:126-130).
+template <typename TS, typename T>
+__device__ __forceinline__ bool linear_interval(const TS &ts, const double *w, int r0, int r1,
+                                                int rcnt, T lo, T hi, int64_t glo, int64_t ghi,
+                                                int64_t ts0, int64_t tsl, double w0, double wl,
+                                                float scale, double &tot) {
+    int a = search_last_le(ts, r0, r1, lo, scale);
+    int first = a + 1;  // first window index with ts > lo
+    double vprev;
+    if (glo <= ts0) {
+        vprev = w0;
+    } else if (glo >= tsl) {
+        vprev = wl;
+    } else {
+        int i = (ts(a) == lo) ? a - 1 : a;  // first bracketing pair (i, i+1)
+        double wa = w[i];
+        double frac = __ddiv_rn((double)(lo - ts(i)), (double)(ts(i + 1) - ts(i)));
+        vprev = __dadd_rn(wa, __dmul_rn(frac, __dsub_rn(w[i + 1], wa)));
+    }
+    T prev = lo;
+    tot = 0.0;
+    int j = first;
+    int m = 0;
+    while (j < rcnt && ts(j) < hi) {
+        if (m == DIRECT - 1) return false;  // pieces = interior + 1 > DIRECT
+        double vj = lin_interior(w, j);
+        T tj = ts(j);
+        tot = __dadd_rn(tot, __dmul_rn(__dmul_rn(0.5, __dadd_rn(vprev, vj)), (double)(tj - prev)));
+        prev = tj;
+        vprev = vj;
+        ++j;
+        ++m;
+    }
+    double vh;
+    if (ghi <= ts0) {
+        vh = w0;
+    } else if (ghi >= tsl) {
+        vh = wl;
+    } else {
+        int i = j - 1;  // ts(j-1) < hi <= ts(j)
+        double wa = w[i];
+        double frac = __ddiv_rn((double)(hi - ts(i)), (double)(ts(i + 1) - ts(i)));
+        vh = __dadd_rn(wa, __dmul_rn(frac, __dsub_rn(w[i + 1], wa)));
+    }
+    tot = __dadd_rn(tot, __dmul_rn(__dmul_rn(0.5, __dadd_rn(vprev, vh)), (double)(hi - prev)));
+    return true;
+}
+
+struct TileCtx {
+    int64_t ts0, tsl, span_lo, span_hi, base;
+    double w0, wl;
+    float scale;
+};
+
+template <int KIND, typename TS, typename T>
+__device__ __forceinline__ void tile_intervals(const AttrParams &p, const TileSmem &sm, int stage,
+                                               const TS &ts, const double *w, int64_t tile,
+                                               T sat, const TileCtx &cx, int ctid) {
+    const StageMeta &M = sm.meta[stage];
+    const int64_t S = p.S;
+    const int64_t wb = M.wb;
+    const int r0 = (int)(tile * TILE - wb);
+    const int r1 = (int)(min((tile + 1) * TILE, S) - wb);
+    const int rcnt = M.cnt;
+    const int64_t total = M.c[DW_MAX_SETS];
+    for (int64_t v = ctid; v < total; v += ATTR_THREADS) {
+        const int j = (v >= M.c[1]) + (v >= M.c[2]) + (v >= M.c[3]);
+        const int64_t k = v - M.c[j] + M.f0[j];
+        const int64_t idx = k - M.a0[j];
+        int64_t glo, ghi;
+        if (idx < M.copied[j]) {
+            glo = sm.iv_lo[stage][M.pool[j] + idx];
+            ghi = sm.iv_hi[stage][M.pool[j] + idx];
+        } else {
+            glo = __ldg(p.start[j] + k);
+            ghi = __ldg(p.end[j] + k);
+        }
+        if (p.check_sorted[j] && k > 0) {
+            const int64_t pidx = idx - 1;
+            const int64_t prev = (pidx >= 0 && pidx < M.copied[j])
+                                     ? sm.iv_lo[stage][M.pool[j] + pidx]
+                                     : __ldg(p.start[j] + k - 1);
+            if (prev > glo) atomic_min_index(&p.st->unsorted_index[j], k);
+        }
+        if (ghi < glo || glo < cx.span_lo || ghi > cx.span_hi) {
+            report_bad(p, j, k);
+            continue;
+        }
+        // window-relative times; hi beyond the window saturates (the interval
+        // is then long and leaves through the DIRECT cap)
+        const T lo = (T)(glo - cx.base);
+        const int64_t dh = ghi - cx.base;
+        const T hi = dh > (int64_t)sat ? sat : (T)dh;
+        double tot;
+        bool ok;
+        if (KIND == DW_SIGNAL_STEP)
+            ok = step_interval(ts, w, r0, r1, lo, hi, cx.scale, tot);
+        else
+            ok = linear_interval(ts, w, r0, r1, rcnt, lo, hi, glo, ghi, cx.ts0, cx.tsl, cx.w0,
+                                 cx.wl, cx.scale, tot);
+        if (!ok) {
+            push_long(p, j, k);
+        } else {
+            const int64_t oidx = p.perm[j] ? __ldg(p.perm[j] + k) : k;
+            p.out[j][oidx] = div_1e6(tot);
+        }
+    }
+}
+
+// ---- narrow tiles: two-phase processing with a counting sort by length ----
+// Phase 1 finds, per interval, its first segment a and its segment count n
+// (both by guessed + galloping searches in shared memory) and buckets the
+// intervals by n.  Phase 2 hands the bucketed order to the lanes, so the 32
+// intervals of a warp have (nearly) equal trip counts, and runs each
+// reference-order sum as a fixed-trip loop whose loads do not depend on the
+// running sum.
+constexpr int CHUNK = IV_POOL;  // intervals per phase-1/phase-2 round
+constexpr int NBUCKET = DIRECT + 2;
+
+struct WorkItem {
+    uint32_t lo, hi;   // window-relative times
+    int16_t a;         // first segment / last sample <= lo (window index)
+    int16_t n;         // STEP: segments (0..DIRECT); LINEAR: b - a (-1..DIRECT-1)
+    int32_t v;         // interval number within the tile (sets concatenated)
+};
+
+struct __align__(16) GroupSmem {  // private to one consumer group
+    uint32_t ts32[WIN];
+    WorkItem work[CHUNK];
+    int16_t order[CHUNK];
+    int hist[NBUCKET];
+    int nvalid;
+    double red[NCW];
+    float scale;
+};
+
+// last r in [r0, r1) with ts(r) < key, given ts(r0) < key
+__device__ __forceinline__ int search_last_lt32(const uint32_t *ts, int r0, int r1, uint32_t key,
+                                                float scale, uint32_t from_key) {
+    int g = r0 + (int)((float)(key - from_key) * scale);
+    g = g < r0 ? r0 : (g >= r1 ? r1 - 1 : g);
+    int lo, hi;
+    if (ts[g] < key) {
+        lo = g;
+        int step = 1;
+        hi = lo + 1;
+        while (hi < r1 && ts[hi] < key) {
+            lo = hi;
+            step <<= 1;
+            hi = lo + step;
+        }
+        if (hi > r1) hi = r1;
+    } else {
+        hi = g;
+        int step = 1;
+        lo = hi - 1;
+        while (lo > r0 && ts[lo] >= key) {
+            hi = lo;
+            step <<= 1;
+            lo = hi - step;
+        }
+        if (lo < r0) lo = r0;
+    }
+    while (hi - lo > 1) {
+        int m = (lo + hi) >> 1;
+        if (ts[m] < key) lo = m; else hi = m;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ double lin_endpoint(const uint32_t *ts, const double *w, int i, uint32_t t) {
+    double wa = w[i];
+    double frac = __ddiv_rn((double)(t - ts[i]), (double)(ts[i + 1] - ts[i]));
+    return __dadd_rn(wa, __dmul_rn(frac, __dsub_rn(w[i + 1], wa)));
+}
+
 template <int KIND>
-__global__ void __launch_bounds__(ATTR_THREADS, 3) attribute_tiles_kernel(AttrParams p) {
+__device__ __forceinline__ double phase2_sum(const uint32_t *ts, const double *w, const WorkItem &e,
+                                             int64_t glo, int64_t ghi, const TileCtx &cx) {
+    const int a = e.a;
+    const uint32_t lo = e.lo, hi = e.hi;
+    if (KIND == DW_SIGNAL_STEP) {
+        const int n = e.n;
+        if (n == 0) return 0.0;
+        if (n == 1) return __dmul_rn(w[a], (double)(hi - lo));
+        double tot = __dmul_rn(w[a], (double)(ts[a + 1] - lo));
+        const int bl = a + n - 1;  // last segment
+        int i = a + 1;
+#pragma unroll 4
+        for (; i < bl; ++i) tot = __dadd_rn(tot, __dmul_rn(w[i], (double)(ts[i + 1] - ts[i])));
+        return __dadd_rn(tot, __dmul_rn(w[bl], (double)(hi - ts[bl])));
+    } else {
+        const int b = a + e.n;  // last sample < hi
+        double vprev;
+        if (glo <= cx.ts0) vprev = cx.w0;
+        else if (glo >= cx.tsl) vprev = cx.wl;
+        else vprev = lin_endpoint(ts, w, ts[a] == lo ? a - 1 : a, lo);
+        uint32_t prev = lo;
+        double tot = 0.0;
+#pragma unroll 4
+        for (int j = a + 1; j <= b; ++j) {
+            double wa = w[j - 1];
+            double vj = __dadd_rn(wa, __dsub_rn(w[j], wa));
+            uint32_t tj = ts[j];
+            tot = __dadd_rn(tot, __dmul_rn(__dmul_rn(0.5, __dadd_rn(vprev, vj)), (double)(tj - prev)));
+            prev = tj;
+            vprev = vj;
+        }
+        double vh;
+        if (ghi <= cx.ts0) vh = cx.w0;
+        else if (ghi >= cx.tsl) vh = cx.wl;
+        else vh = lin_endpoint(ts, w, b, hi);
+        return __dadd_rn(tot, __dmul_rn(__dmul_rn(0.5, __dadd_rn(vprev, vh)), (double)(hi - prev)));
+    }
+}
+
+template <int KIND>
+__device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSmem &so, int stage,
+                                      int64_t tile, const TileCtx &cx, int ctid, int g) {
+    const StageMeta &M = sm.meta[stage];
+    const int64_t S = p.S;
+    const int64_t wb = M.wb;
+    const int cnt = M.cnt;
+    const int r0 = (int)(tile * TILE - wb);
+    const int r1 = (int)(min((tile + 1) * TILE, S) - wb);
+    const uint32_t *ts = so.ts32;
+    const double *w = sm.w[stage];
+    const int64_t total = M.c[DW_MAX_SETS];
+    if (total == 0) {  // still close the tile: gs.red / ts32 are reused next tile
+        consumer_sync(g);
+        return;
+    }
+    for (int64_t c0 = 0; c0 < total; c0 += CHUNK) {
+        const int nch = (int)(total - c0 < CHUNK ? total - c0 : CHUNK);
+        // ---- phase 1: locate, validate, bucket by length
+        for (int q = ctid; q < nch; q += ATTR_THREADS) {
+            const int64_t v = c0 + q;
+            const int j = (v >= M.c[1]) + (v >= M.c[2]) + (v >= M.c[3]);
+            const int64_t k = v - M.c[j] + M.f0[j];
+            const int64_t idx = k - M.a0[j];
+            int64_t glo, ghi;
+            if (idx < M.copied[j]) {
+                glo = sm.iv_lo[stage][M.pool[j] + idx];
+                ghi = sm.iv_hi[stage][M.pool[j] + idx];
+            } else {
+                glo = __ldg(p.start[j] + k);
+                ghi = __ldg(p.end[j] + k);
+            }
+            if (p.check_sorted[j] && k > 0) {
+                const int64_t pidx = idx - 1;
+                const int64_t prev = (pidx >= 0 && pidx < M.copied[j]) ? sm.iv_lo[stage][M.pool[j] + pidx]
+                                                                       : __ldg(p.start[j] + k - 1);
+                if (prev > glo) atomic_min_index(&p.st->unsorted_index[j], k);
+            }
+            WorkItem e;
+            e.v = (int32_t)v;
+            e.n = -2;  // skipped
+            if (ghi < glo || glo < cx.span_lo || ghi > cx.span_hi) {
+                report_bad(p, j, k);
+            } else {
+                const uint32_t lo = (uint32_t)(glo - cx.base);
+                const int64_t dh = ghi - cx.base;
+                const uint32_t hi = dh > 0xFFFFFFFFLL ? 0xFFFFFFFFu : (uint32_t)dh;
+                const int a = search_last_le(Ts32{ts}, r0, r1, lo, cx.scale);
+                e.lo = lo;
+                e.hi = hi;
+                e.a = (int16_t)a;
+                if (KIND == DW_SIGNAL_STEP) {
+                    int n;
+                    if (hi == lo) {
+                        n = 0;
+                    } else {
+                        const int lim = min(a + DIRECT + 1, cnt);
+                        const int b = search_last_lt32(ts, a, lim, hi, cx.scale, lo);
+                        n = b - a + 1;
+                    }
+                    if (n > DIRECT) push_long(p, j, k);
+                    else e.n = (int16_t)n;
+                } else {
+                    int m;  // b - a, b = last sample < hi
+                    if (ts[a] < hi) {
+                        const int lim = min(a + DIRECT + 1, cnt);
+                        m = search_last_lt32(ts, a, lim, hi, cx.scale, lo) - a;
+                    } else {
+                        m = -1;  // hi == lo == ts[a]
+                    }
+                    if (m + 1 > DIRECT) push_long(p, j, k);  // pieces = m + 1
+                    else e.n = (int16_t)m;
+                }
+            }
+            so.work[q] = e;
+            if (e.n >= -1) atomicAdd(&so.hist[e.n + 1], 1);
+        }
+        consumer_sync(g);
+        // ---- exclusive scan of the length histogram (warp 0)
+        if (ctid < 32) {
+            constexpr int PER = (NBUCKET + 31) / 32;
+            int loc[PER];
+            int s = 0;
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+                int b = ctid * PER + u;
+                loc[u] = b < NBUCKET ? so.hist[b] : 0;
+                s += loc[u];
+            }
+            int incl = s;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (ctid >= o) incl += t;
+            }
+            int run = incl - s;
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+                int b = ctid * PER + u;
+                if (b < NBUCKET) so.hist[b] = run;
+                run += loc[u];
+            }
+            if (ctid == 31) so.nvalid = incl;
+        }
+        consumer_sync(g);
+        for (int q = ctid; q < nch; q += ATTR_THREADS) {
+            const int n = so.work[q].n;
+            if (n >= -1) so.order[atomicAdd(&so.hist[n + 1], 1)] = (int16_t)q;
+        }
+        consumer_sync(g);
+        // ---- phase 2: equal-length intervals side by side
+        const int nvalid = so.nvalid;
+        for (int q = ctid; q < nvalid; q += ATTR_THREADS) {
+            const WorkItem e = so.work[so.order[q]];
+            const int64_t v = e.v;
+            const int j = (v >= M.c[1]) + (v >= M.c[2]) + (v >= M.c[3]);
+            const int64_t k = v - M.c[j] + M.f0[j];
+            const int64_t glo = cx.base + e.lo, ghi = cx.base + e.hi;
+            const double tot = phase2_sum<KIND>(ts, w, e, glo, ghi, cx);
+            const int64_t oidx = p.perm[j] ? __ldg(p.perm[j] + k) : k;
+            p.out[j][oidx] = div_1e6(tot);
+        }
+        for (int b = ctid; b < NBUCKET; b += ATTR_THREADS) so.hist[b] = 0;
+        consumer_sync(g);
+    }
+}
+
+__device__ __forceinline__ void producer(const AttrParams &p, TileSmem &sm, int64_t span_hi) {
+    const int64_t S = p.S;
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+        const int stage = it % STAGES;
+        // partition reads first: their latency overlaps the wait for the slot
+        int64_t f0s[DW_MAX_SETS], f1s[DW_MAX_SETS];
+#pragma unroll
+        for (int j = 0; j < DW_MAX_SETS; ++j) {
+            f0s[j] = j < p.nsets ? p.first[j * (p.ntiles + 1) + tile] : 0;
+            f1s[j] = j < p.nsets ? p.first[j * (p.ntiles + 1) + tile + 1] : 0;
+        }
+        int64_t wb, we;
+        tile_window(tile, S, wb, we);
+        const int cnt = (int)(we - wb);
+        const int even = cnt & ~1;
+        uint32_t bytes = 2u * 8u * (uint32_t)even;
+        if (it >= STAGES) mbar_wait(&sm.empty[stage], (uint32_t)(((it / STAGES) - 1) & 1));
+        fence_proxy_async();
+        StageMeta &M = sm.meta[stage];
+        M.wb = wb;
+        M.cnt = cnt;
+        int pool = 0;
+        M.c[0] = 0;
+#pragma unroll
+        for (int j = 0; j < DW_MAX_SETS; ++j) {
+            const int64_t f0 = f0s[j], f1 = f1s[j];
+            const int64_t a0 = f0 & ~(int64_t)1;
+            int64_t want = f1 > f0 ? f1 - a0 : 0;
+            int64_t room = IV_POOL - pool;
+            int m = (int)(want < room ? want : room) & ~1;
+            M.f0[j] = f0;
+            M.c[j + 1] = M.c[j] + (f1 - f0);
+            M.a0[j] = a0;
+            M.copied[j] = m;
+            M.pool[j] = pool;
+            pool += m;
+            bytes += 2u * 8u * (uint32_t)m;
+        }
+        if (cnt & 1) {  // odd tail of the window: not a 16-byte multiple
+            sm.ts[stage][cnt - 1] = __ldg(p.ts + wb + cnt - 1);
+            sm.w[stage][cnt - 1] = __ldg(p.w + wb + cnt - 1);
+        }
+        if (wb + cnt == S) sm.ts[stage][cnt] = span_hi;  // virtual end of the last segment
+        mbar_expect_tx(&sm.full[stage], bytes);
+        if (even) {
+            tma_load_1d(sm.ts[stage], p.ts + wb, 8u * even, &sm.full[stage]);
+            tma_load_1d(sm.w[stage], p.w + wb, 8u * even, &sm.full[stage]);
+        }
+        for (int j = 0; j < p.nsets; ++j) {
+            const int m = M.copied[j];
+            if (m) {
+                tma_load_1d(&sm.iv_lo[stage][M.pool[j]], p.start[j] + M.a0[j], 8u * m, &sm.full[stage]);
+                tma_load_1d(&sm.iv_hi[stage][M.pool[j]], p.end[j] + M.a0[j], 8u * m, &sm.full[stage]);
+            }
+        }
+    }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(KTHREADS, 1) attribute_tiles_kernel(AttrParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     TileSmem &sm = *reinterpret_cast<TileSmem *>(smem_raw);
+    GroupSmem *groups =
+        reinterpret_cast<GroupSmem *>(smem_raw + ((sizeof(TileSmem) + 15) & ~(size_t)15));
     const int tid = threadIdx.x;
-    int64_t tile = blockIdx.x;
-    if (tile >= p.ntiles) return;
+    if ((int64_t)blockIdx.x >= p.ntiles) return;
 
     const int64_t S = p.S;
-    const int64_t ts0 = __ldg(p.ts);
-    const int64_t tsl = __ldg(p.ts + S - 1);
-    const int64_t span_lo = ts0;
-    const int64_t span_hi = KIND == DW_SIGNAL_STEP ? p.span_hi : tsl;
+    TileCtx cx;
+    cx.ts0 = __ldg(p.ts);
+    cx.tsl = __ldg(p.ts + S - 1);
+    cx.w0 = __ldg(p.w);
+    cx.wl = __ldg(p.w + S - 1);
+    cx.span_lo = cx.ts0;
+    cx.span_hi = KIND == DW_SIGNAL_STEP ? p.span_hi : cx.tsl;
     const int64_t nterms = KIND == DW_SIGNAL_STEP ? S : S - 1;
-    const double w0 = __ldg(p.w), wl = __ldg(p.w + S - 1);
 
     if (tid == 0) {
-        mbar_init(&sm.bar[0], 1);
-        mbar_init(&sm.bar[1], 1);
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    for (int g = 0; g < GROUPS; ++g)
+        for (int b = tid; b < NBUCKET; b += blockDim.x) groups[g].hist[b] = 0;
     __syncthreads();
-    if (tid == 0) issue_tile(p, sm, 0, tile);
 
-    for (int it = 0; tile < p.ntiles; tile += gridDim.x, ++it) {
-        const int stage = it & 1;
-        const int64_t next = tile + gridDim.x;
-        if (tid == 0 && next < p.ntiles) {
-            fence_proxy_async();
-            issue_tile(p, sm, stage ^ 1, next);
-        }
-        mbar_wait(&sm.bar[stage], (uint32_t)((it >> 1) & 1));
-        const int64_t wb = sm.win_base[stage];
-        const int64_t cnt = sm.win_cnt[stage];
-        int64_t *s_ts = sm.ts[stage];
-        double *s_w = sm.w[stage];
-        if (tid == 0) {
-            if (cnt & 1) {  // odd tail: not a 16-byte multiple, load directly
-                s_ts[cnt - 1] = __ldg(p.ts + wb + cnt - 1);
-                s_w[cnt - 1] = __ldg(p.w + wb + cnt - 1);
-            }
-            if (wb + cnt == S) s_ts[cnt] = span_hi;  // virtual end of the last segment
-        }
-        __syncthreads();
+    if (tid >= GROUPS * ATTR_THREADS) {  // producer warp
+        if (tid == GROUPS * ATTR_THREADS) producer(p, sm, cx.span_hi);
+        return;
+    }
+    // consumer group g takes every GROUPS-th tile of this CTA's sequence
+    const int g = tid / ATTR_THREADS;
+    const int ctid = tid - g * ATTR_THREADS;
+    GroupSmem &gs = groups[g];
+    for (int it = g;; it += GROUPS) {
+        const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+        if (tile >= p.ntiles) break;
+        const int stage = it % STAGES;
+        mbar_wait(&sm.full[stage], (uint32_t)((it / STAGES) & 1));
+        const StageMeta &M = sm.meta[stage];
+        const int64_t wb = M.wb;
+        const int cnt = M.cnt;
+        const int64_t *s_ts = sm.ts[stage];
+        const double *s_w = sm.w[stage];
+        const int64_t base = s_ts[0];
+        const int last = (wb + cnt == S) ? cnt : cnt - 1;
+        const bool wide = (s_ts[last] - base) >= (int64_t)0xFFFFFFF0LL;
+        const int r0 = (int)(tile * TILE - wb);
+        const int r1 = (int)(min((tile + 1) * TILE, S) - wb);
 
-        const int64_t t0 = tile * TILE;                            // first segment of the tile
-        const int64_t t1 = min((tile + 1) * TILE, S);              // one past the last sample
-        auto TS = [&](int64_t g) -> int64_t { return s_ts[g - wb]; };
-        auto W = [&](int64_t g) -> double { return s_w[g - wb]; };
-
-        // (a) strictly increasing timestamps (trace_model.py:549-551)
+        // (a) 32-bit relative timestamps, (b) power order check, (c) fp64 tile sum
+        if (!wide)
+            for (int r = ctid; r <= last; r += ATTR_THREADS) gs.ts32[r] = (uint32_t)(s_ts[r] - base);
         if (p.validate_order) {
-            for (int64_t i = t0 + tid; i < min(t1, S - 1); i += ATTR_THREADS)
-                if (TS(i + 1) <= TS(i)) atomic_min_index(&p.st->order_index, i);
+            for (int r = r0 + ctid; r < r1 && wb + r + 1 < S; r += ATTR_THREADS)
+                if (s_ts[r + 1] <= s_ts[r]) atomic_min_index(&p.st->order_index, wb + r);
         }
-
-        // (b) exact tile sum of the integrand terms (the tile-prefix level)
-        {
-            i128 acc = 0;
-            const int64_t e1 = min((tile + 1) * TILE, nterms);
-            for (int64_t i = t0 + tid; i < e1; i += ATTR_THREADS) {
-                double term;
-                if (KIND == DW_SIGNAL_STEP) {
-                    term = __dmul_rn(W(i), (double)(TS(i + 1) - TS(i)));
-                } else {
-                    double va = lin_sample_value(i, S, TS, W);
-                    double vb = lin_sample_value(i + 1, S, TS, W);
-                    term = lin_piece(va, vb, TS(i + 1) - TS(i));
-                }
-                acc += q_term(term);
+        double acc = 0.0;
+        const int e1 = (int)(min((tile + 1) * TILE, nterms) - wb);
+        for (int r = r0 + ctid; r < e1; r += ATTR_THREADS) {
+            double term;
+            if (KIND == DW_SIGNAL_STEP) {
+                term = __dmul_rn(s_w[r], (double)(s_ts[r + 1] - s_ts[r]));
+            } else {
+                const int64_t gi = wb + r;
+                double va = gi == 0 ? cx.w0 : lin_interior(s_w, r);
+                double vb = gi + 1 == S - 1 ? cx.wl : lin_interior(s_w, r + 1);
+                term = __dmul_rn(__dmul_rn(0.5, __dadd_rn(va, vb)), (double)(s_ts[r + 1] - s_ts[r]));
             }
-            acc = warp_sum_i128(acc);
-            if ((tid & 31) == 0) {
-                I128Parts pp = split(acc);
-                sm.red[tid >> 5][0] = pp.lo;
-                sm.red[tid >> 5][1] = pp.hi;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                i128 s = 0;
+            acc = __dadd_rn(acc, term);
+        }
 #pragma unroll
-                for (int k = 0; k < ATTR_WARPS; ++k) s += join(sm.red[k][0], sm.red[k][1]);
-                I128Parts pp = split(s);
-                p.tile_fx[2 * tile] = pp.lo;
-                p.tile_fx[2 * tile + 1] = pp.hi;
-            }
+        for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+        if ((ctid & 31) == 0) gs.red[ctid >> 5] = acc;
+        if (ctid == 0) {
+            const int64_t dt = s_ts[r1 < last ? r1 : last] - s_ts[r0];
+            gs.scale = dt > 0 ? (float)(r1 - r0) / (float)dt : 0.0f;
         }
-
-        // (c) intervals whose start falls in this tile
-        for (int j = 0; j < p.nsets; ++j) {
-            const int64_t f0 = p.first[j * (p.ntiles + 1) + tile];
-            const int64_t f1 = p.first[j * (p.ntiles + 1) + tile + 1];
-            const int64_t *st_a = p.start[j];
-            const int64_t *en_a = p.end[j];
-            for (int64_t k = f0 + tid; k < f1; k += ATTR_THREADS) {
-                const int64_t lo = __ldg(st_a + k);
-                const int64_t hi = __ldg(en_a + k);
-                if (p.check_sorted[j] && k > 0 && __ldg(st_a + k - 1) > lo)
-                    atomic_min_index(&p.st->unsorted_index[j], k);
-                if (hi < lo || lo < span_lo || hi > span_hi) {
-                    report_bad(p, j, k);
-                    continue;
-                }
-                const int64_t oidx = p.perm[j] ? __ldg(p.perm[j] + k) : k;
-                double tot = 0.0;
-                bool is_long = false;
-                if (KIND == DW_SIGNAL_STEP) {
-                    // last segment start <= lo, searched in [t0, t1)
-                    int64_t l = t0, h = t1;  // upper_bound(lo) in [t0, t1)
-                    while (l < h) {
-                        int64_t m = (l + h) >> 1;
-                        if (TS(m) <= lo) l = m + 1; else h = m;
-                    }
-                    int64_t i = l - 1;
-                    if (i < t0) i = t0;
-                    int nseg = 0;
-                    for (; i < S && TS(i) < hi; ++i) {
-                        if (nseg == DIRECT) { is_long = true; break; }
-                        int64_t s = TS(i), e = TS(i + 1);
-                        int64_t ov = min(e, hi) - max(s, lo);
-                        tot = __dadd_rn(tot, __dmul_rn(W(i), (double)ov));
-                        ++nseg;
-                    }
-                } else {
-                    // first sample > lo, searched in [t0, t1]
-                    int64_t l = t0, h = t1;
-                    while (l < h) {
-                        int64_t m = (l + h) >> 1;
-                        if (TS(m) <= lo) l = m + 1; else h = m;
-                    }
-                    const int64_t first = l;
-                    const int64_t lbj = (first > 0 && TS(first - 1) == lo) ? first - 1 : first;
-                    double vprev = lin_value_at(lo, lbj, ts0, tsl, w0, wl, TS, W);
-                    int64_t prev = lo;
-                    int64_t j2 = first;
-                    int m = 0;
-                    for (; j2 < S && TS(j2) < hi; ++j2) {
-                        // pieces = interior points + 1; more than DIRECT pieces -> long
-                        if (m == DIRECT - 1) { is_long = true; break; }
-                        double vj = lin_sample_value(j2, S, TS, W);
-                        tot = __dadd_rn(tot, lin_piece(vprev, vj, TS(j2) - prev));
-                        prev = TS(j2);
-                        vprev = vj;
-                        ++m;
-                    }
-                    if (!is_long) {
-                        double vh = lin_value_at(hi, j2, ts0, tsl, w0, wl, TS, W);
-                        tot = __dadd_rn(tot, lin_piece(vprev, vh, hi - prev));
-                    }
-                }
-                if (is_long) push_long(p, j, k);
-                else p.out[j][oidx] = __ddiv_rn(tot, US_PER_S);
-            }
+        consumer_sync(g);
+        if (ctid == 0) {
+            double t = gs.red[0];
+#pragma unroll
+            for (int k = 1; k < NCW; ++k) t = __dadd_rn(t, gs.red[k]);
+            p.tile_sum[tile] = t;
         }
-        __syncthreads();  // stage buffers free for the next TMA
+        cx.scale = gs.scale;
+        cx.base = base;
+        if (!wide) {
+            tile_intervals_sorted<KIND>(p, sm, gs, stage, tile, cx, ctid, g);
+        } else {
+            Ts64 a64{s_ts, base};
+            tile_intervals<KIND>(p, sm, stage, a64, s_w, tile, (int64_t)INT64_MAX, cx, ctid);
+            consumer_sync(g);
+        }
+        if (ctid == 0) mbar_arrive(&sm.empty[stage]);
     }
 }
 
 // ------------------------------------------------------------ K3 tile scan
+// exact int128 exclusive prefix of q(tile_sum) over tiles: block partials,
+// one-block scan of partials, block rescan (coalesced, 3 small launches)
 constexpr int SCAN_THREADS = 1024;
-__global__ void __launch_bounds__(SCAN_THREADS) tile_scan_kernel(AttrParams p) {
-    __shared__ unsigned long long s[SCAN_THREADS][2];
-    const int tid = threadIdx.x;
-    const int64_t n = p.ntiles;
-    const int64_t per = ceil_div(n, SCAN_THREADS);
-    const int64_t b0 = min(n, tid * per), b1 = min(n, b0 + per);
-    i128 local = 0;
-    for (int64_t b = b0; b < b1; ++b) local += join(p.tile_fx[2 * b], p.tile_fx[2 * b + 1]);
-    I128Parts lp = split(local);
-    s[tid][0] = lp.lo;
-    s[tid][1] = lp.hi;
+constexpr int SCAN_PER_THREAD = 4;
+constexpr int SCAN_CHUNK = SCAN_THREADS * SCAN_PER_THREAD;
+
+__device__ __forceinline__ i128 block_exclusive_scan(i128 v, i128 &block_total) {
+    __shared__ unsigned long long s[SCAN_THREADS / 32][2];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    i128 x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        I128Parts q = split(x);
+        uint64_t lo = __shfl_up_sync(0xffffffffu, q.lo, o);
+        uint64_t hi = __shfl_up_sync(0xffffffffu, q.hi, o);
+        if (lane >= o) x += join(lo, hi);
+    }
+    if (lane == 31) {
+        I128Parts q = split(x);
+        s[warp][0] = q.lo;
+        s[warp][1] = q.hi;
+    }
     __syncthreads();
-    // Hillis-Steele inclusive scan over per-thread sums
-    for (int off = 1; off < SCAN_THREADS; off <<= 1) {
-        i128 v = join(s[tid][0], s[tid][1]);
-        i128 add = tid >= off ? join(s[tid - off][0], s[tid - off][1]) : (i128)0;
+    if (warp == 0) {
+        i128 y = lane < SCAN_THREADS / 32 ? join(s[lane][0], s[lane][1]) : (i128)0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            I128Parts q = split(y);
+            uint64_t lo = __shfl_up_sync(0xffffffffu, q.lo, o);
+            uint64_t hi = __shfl_up_sync(0xffffffffu, q.hi, o);
+            if (lane >= o) y += join(lo, hi);
+        }
+        I128Parts q = split(y);
+        s[lane][0] = q.lo;
+        s[lane][1] = q.hi;
+    }
+    __syncthreads();
+    block_total = join(s[SCAN_THREADS / 32 - 1][0], s[SCAN_THREADS / 32 - 1][1]);
+    i128 warp_base = warp ? join(s[warp - 1][0], s[warp - 1][1]) : (i128)0;
+    __syncthreads();
+    return warp_base + x - v;
+}
+
+__device__ __forceinline__ i128 thread_chunk(const AttrParams &p, int64_t b0, i128 *vals) {
+    i128 sum = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_PER_THREAD; ++k) {
+        int64_t b = b0 + k;
+        i128 v = b < p.ntiles ? q_term(p.tile_sum[b]) : (i128)0;
+        if (vals) vals[k] = v;
+        sum += v;
+    }
+    return sum;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) scan_partials_kernel(AttrParams p) {
+    int64_t b0 = (int64_t)blockIdx.x * SCAN_CHUNK + threadIdx.x * SCAN_PER_THREAD;
+    i128 sum = thread_chunk(p, b0, nullptr);
+    i128 total;
+    block_exclusive_scan(sum, total);
+    if (threadIdx.x == 0) {
+        I128Parts q = split(total);
+        p.scan_part[2 * blockIdx.x] = q.lo;
+        p.scan_part[2 * blockIdx.x + 1] = q.hi;
+    }
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) scan_top_kernel(AttrParams p, int64_t nblocks) {
+    // exclusive scan of block partials, in place (nblocks <= a few thousand)
+    __shared__ unsigned long long carry[2];
+    if (threadIdx.x == 0) { carry[0] = 0; carry[1] = 0; }
+    __syncthreads();
+    for (int64_t c = 0; c < nblocks; c += SCAN_THREADS) {
+        int64_t b = c + threadIdx.x;
+        i128 v = b < nblocks ? join(p.scan_part[2 * b], p.scan_part[2 * b + 1]) : (i128)0;
+        i128 total;
+        i128 ex = block_exclusive_scan(v, total);
+        i128 base = join(carry[0], carry[1]);
+        if (b < nblocks) {
+            I128Parts q = split(base + ex);
+            p.scan_part[2 * b] = q.lo;
+            p.scan_part[2 * b + 1] = q.hi;
+        }
         __syncthreads();
-        I128Parts q = split(v + add);
-        s[tid][0] = q.lo;
-        s[tid][1] = q.hi;
+        if (threadIdx.x == 0) {
+            I128Parts q = split(base + total);
+            carry[0] = q.lo;
+            carry[1] = q.hi;
+        }
         __syncthreads();
     }
-    i128 run = tid ? join(s[tid - 1][0], s[tid - 1][1]) : (i128)0;
-    for (int64_t b = b0; b < b1; ++b) {
-        I128Parts q = split(run);
-        p.prefix[2 * b] = q.lo;
-        p.prefix[2 * b + 1] = q.hi;
-        run += join(p.tile_fx[2 * b], p.tile_fx[2 * b + 1]);
+    if (threadIdx.x == 0) {  // grand total at prefix[ntiles]
+        p.prefix[2 * p.ntiles] = carry[0];
+        p.prefix[2 * p.ntiles + 1] = carry[1];
     }
-    if (tid == SCAN_THREADS - 1) {
-        I128Parts q = split(join(s[tid][0], s[tid][1]));
-        p.prefix[2 * n] = q.lo;
-        p.prefix[2 * n + 1] = q.hi;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) scan_apply_kernel(AttrParams p) {
+    int64_t b0 = (int64_t)blockIdx.x * SCAN_CHUNK + threadIdx.x * SCAN_PER_THREAD;
+    i128 vals[SCAN_PER_THREAD];
+    i128 sum = thread_chunk(p, b0, vals);
+    i128 total;
+    i128 run = block_exclusive_scan(sum, total) +
+               join(p.scan_part[2 * blockIdx.x], p.scan_part[2 * blockIdx.x + 1]);
+#pragma unroll
+    for (int k = 0; k < SCAN_PER_THREAD; ++k) {
+        int64_t b = b0 + k;
+        if (b < p.ntiles) {
+            I128Parts q = split(run);
+            p.prefix[2 * b] = q.lo;
+            p.prefix[2 * b + 1] = q.hi;
+        }
+        run += vals[k];
     }
 }
 
@@ -390,7 +934,8 @@ __device__ __forceinline__ double term_global(const AttrParams &p, int64_t i) {
     return lin_piece(va, vb, TS(i + 1) - TS(i));
 }
 
-// exact sum of terms [j0, j1] (inclusive), whole warp participates
+// exact sum of terms [j0, j1] (inclusive): partial tiles term by term, whole
+// tiles through the int128 prefix of their fp64 sums; whole warp participates
 template <int KIND>
 __device__ i128 range_sum(const AttrParams &p, int64_t j0, int64_t j1) {
     const int lane = threadIdx.x & 31;
@@ -577,7 +1122,7 @@ __global__ void step_value_at_kernel(const int64_t *ts, const double *w, int64_t
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct AttrLayout {
-    size_t status, first, tile_fx, prefix, long_list, sum_partials, sum_done, sum_out;
+    size_t status, first, tile_sum, prefix, scan_part, long_list, sum_partials, sum_done, sum_out;
     size_t sort_keys[DW_MAX_SETS], sort_perm[DW_MAX_SETS], sort_end[DW_MAX_SETS],
         sort_iota[DW_MAX_SETS];
     size_t cub_tmp, cub_bytes, total;
@@ -600,8 +1145,9 @@ static AttrLayout attr_layout(int64_t S, const int64_t *sizes, const int32_t *so
     size_t off = 0;
     L.status = off; off += align_up(STATUS_BYTES);
     L.first = off; off += align_up(sizeof(int64_t) * (size_t)(ntiles + 1) * DW_MAX_SETS);
-    L.tile_fx = off; off += align_up(16 * (size_t)(ntiles + 1));
+    L.tile_sum = off; off += align_up(8 * (size_t)(ntiles + 1));
     L.prefix = off; off += align_up(16 * (size_t)(ntiles + 2));
+    L.scan_part = off; off += align_up(16 * (size_t)(ceil_div(ntiles, SCAN_CHUNK) + 1));
     L.long_list = off; off += align_up(8 * (size_t)(nint + 1));
     L.sum_partials = off; off += align_up(16 * (size_t)SUM_BLOCKS);
     L.sum_done = off; off += align_up(16);
@@ -664,7 +1210,8 @@ static int attribute_impl(const dw_signal_t *sig, dw_interval_set_t *sets, int n
     p.nsets = nsets;
     p.validate_order = sig->validate_order;
     p.first = (const int64_t *)(base + L.first);
-    p.tile_fx = (unsigned long long *)(base + L.tile_fx);
+    p.tile_sum = (double *)(base + L.tile_sum);
+    p.scan_part = (unsigned long long *)(base + L.scan_part);
     p.prefix = (unsigned long long *)(base + L.prefix);
     p.long_list = (unsigned long long *)(base + L.long_list);
     p.st = st;
@@ -703,20 +1250,25 @@ static int attribute_impl(const dw_signal_t *sig, dw_interval_set_t *sets, int n
         partition_kernel<<<(unsigned)ceil_div(nb, 256), 256, 0, stream>>>(p);
         count_launch();
     }
-    const size_t smem = sizeof(TileSmem);
-    int grid = (int)std::min<int64_t>(p.ntiles, (int64_t)num_sms() * 3);
+    const size_t smem = ((sizeof(TileSmem) + 15) & ~(size_t)15) + GROUPS * sizeof(GroupSmem);
+    int grid = (int)std::min<int64_t>(p.ntiles, (int64_t)num_sms() * CTAS_PER_SM);
     if (sig->kind == DW_SIGNAL_STEP) {
         cudaFuncSetAttribute(attribute_tiles_kernel<DW_SIGNAL_STEP>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attribute_tiles_kernel<DW_SIGNAL_STEP><<<grid, ATTR_THREADS, smem, stream>>>(p);
+        attribute_tiles_kernel<DW_SIGNAL_STEP><<<grid, KTHREADS, smem, stream>>>(p);
     } else {
         cudaFuncSetAttribute(attribute_tiles_kernel<DW_SIGNAL_LINEAR>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attribute_tiles_kernel<DW_SIGNAL_LINEAR><<<grid, ATTR_THREADS, smem, stream>>>(p);
+        attribute_tiles_kernel<DW_SIGNAL_LINEAR><<<grid, KTHREADS, smem, stream>>>(p);
     }
     count_launch();
-    tile_scan_kernel<<<1, SCAN_THREADS, 0, stream>>>(p);
-    count_launch();
+    {
+        const int64_t nblk = ceil_div(p.ntiles, SCAN_CHUNK);
+        scan_partials_kernel<<<(unsigned)nblk, SCAN_THREADS, 0, stream>>>(p);
+        scan_top_kernel<<<1, SCAN_THREADS, 0, stream>>>(p, nblk);
+        scan_apply_kernel<<<(unsigned)nblk, SCAN_THREADS, 0, stream>>>(p);
+        count_launch(3);
+    }
     const int long_grid = num_sms() * 4;
     if (sig->kind == DW_SIGNAL_STEP)
         long_intervals_kernel<DW_SIGNAL_STEP><<<long_grid, 256, 0, stream>>>(p);

@@ -1,0 +1,28 @@
+"""Perf probe: attribution at a BASELINE config (device-resident inputs)."""
+import sys, time
+import torch
+sys.path.insert(0, ".")
+from paper_2512_08365_b200 import synth, build_ledger, _native
+from paper_2512_08365_b200.energy import PowerSignal, _run_ledger
+
+name = sys.argv[1] if len(sys.argv) > 1 else "C4"
+kind = sys.argv[2] if len(sys.argv) > 2 else "step"
+iters = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+t = time.time()
+a, b = synth.make_pair(name)
+torch.cuda.synchronize()
+print(f"gen {name}: {time.time()-t:.1f}s  N={a.n_ops} K={a.n_kernels} S={a.n_power} kernels_sorted={a.kernels_sorted}", flush=True)
+for side in (a, b):
+    for c in ("op_start", "op_end", "k_start", "k_end"):
+        side.device(c)
+sig = PowerSignal.from_columns(a.ts, a.watts, a.signal_span()[1], kind)
+torch.cuda.synchronize()
+bytes_alg = 16 * a.n_power + 24 * (a.n_ops + a.n_kernels)
+for it in range(iters):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    per_op, per_k, st = _run_ledger(a, sig, False)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    print(f"ledger {kind}: {ms:.3f} ms  {bytes_alg/ms/1e6:.1f} GB/s alg  long={st.long_intervals} code={st.code} total={st.totals[0]:.6e}", flush=True)
+print("mem GB", torch.cuda.max_memory_allocated()/1e9)

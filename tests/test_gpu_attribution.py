@@ -162,6 +162,20 @@ def test_random_linear_vs_oracle(seed, S, n, max_len):
     np.testing.assert_array_equal(got, oracle.integrate_linear(ts, w, lo, hi, oracle.MODE_DEVICE))
 
 
+def test_linear_total_device_definition():
+    ts, w, span_hi, lo, hi = _random_case(9, 300_000, 1000, 500)
+    sig = E.PowerSignal.from_columns(ts, w, kind="linear")
+    cols = TraceColumns.from_arrays(ts, w, np.minimum(lo, ts[-1]), np.minimum(hi, ts[-1]),
+                                    trace_end=int(ts[-1]))
+    led = build_ledger(cols, method="ground_truth")
+    assert led.total_joules == oracle.total_device("step", ts, w, int(ts[-1]) + 1)
+    from paper_2512_08365_b200.energy import _run_ledger
+    _, _, st = _run_ledger(cols, sig, False)
+    assert st.totals[0] == oracle.total_device("linear", ts, w)
+    ref = oracle.integrate_linear(ts, w, [ts[0]], [ts[-1]], oracle.MODE_REFERENCE)[0]
+    assert st.totals[0] == pytest.approx(ref, rel=1e-12)
+
+
 def test_unsorted_sets_match_sorted():
     ts, w, span_hi, lo, hi = _random_case(7, 100_000, 50_000, 2000)
     perm = np.random.default_rng(0).permutation(lo.size)
@@ -175,9 +189,9 @@ def test_ledger_total_long_and_idle():
     ts, w, span_hi, lo, hi = _random_case(8, 200_000, 20_000, 500)
     cols = TraceColumns.from_arrays(ts, w, lo, hi, trace_end=span_hi - 1)
     led = build_ledger(cols)
-    allseg = oracle.integrate_step(ts, w, span_hi, [ts[0]], [span_hi], oracle.MODE_DEVICE)[0]
-    assert led.total_joules == allseg
-    ref_total = oracle.integrate_step(ts, w, span_hi, [ts[0]], [span_hi], oracle.MODE_REFERENCE)[0]
+    assert led.total_joules == oracle.total_device("step", ts, w, cols.signal_span()[1])
+    sh = cols.signal_span()[1]
+    ref_total = oracle.integrate_step(ts, w, sh, [ts[0]], [sh], oracle.MODE_REFERENCE)[0]
     assert led.total_joules == pytest.approx(ref_total, rel=1e-12)
     assert led.operator_total() == oracle.fx_sum(led.per_operator.array())
     assert led.idle_joules == max(led.total_joules - led.operator_total(), 0.0)
