@@ -37,4 +37,13 @@ from .energy import (  # noqa: F401
     sampled_view,
 )
 
+from .detect import (  # noqa: F401
+    Report,
+    SubgraphPair,
+    WasteFinding,
+    detect_waste,
+    report,
+)
+from .join import join_diff, join_report, signature_of  # noqa: F401
+
 __version__ = "0.1.0"

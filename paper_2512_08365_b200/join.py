@@ -1,0 +1,191 @@
+"""Scale path of the differential diff: signature hash-join + deltas + ranked
+top-k, all on the device (csrc/diff.cu ``dw_join_diff`` and ``dw_rank``).
+
+The reference pairs operators through SVD tensor matching and dominator cuts
+(subgraph_match.py:322-422), a sequential graph algorithm.  At 1e8 operators
+the north star replaces that pairing with a join on operator signatures, which
+the reference does not define; the definition used here
+(DESIGN.md "signature join"):
+
+  * signature = 64-bit hash of (op name, layout-blind input shapes = element
+    counts, dtype, call site / config key).  Reference-style traces carry no
+    dtype or call site; they hash as "float64" and "".
+  * an operator's key is (signature, k) where k counts earlier operators of the
+    same signature in trace order (the k-th occurrence);
+  * equal keys pair up; unmatched operators become one-sided findings whose
+    other side is empty (energy 0, latency 0), judged by the reference's rule.
+
+Findings are numbered: A's operators in order (matched or A-only), then B-only
+operators in B order.  Ranking and verdicts follow detect.py exactly, with
+nodes_a = (op_id,) or () for B-only findings.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _native
+from .columns import TraceColumns
+from .detect import (DEFAULT_THRESHOLD, SIDES, VERDICT_WASTE, VERDICTS, FindingColumns,
+                     Report, SubgraphPair, WasteFinding, rank_order)
+from .energy import EnergyLedger
+
+
+def signature_of(op_name: str, shapes: Sequence[int] = (), dtype: str = "float64",
+                 callsite: str = "") -> int:
+    """64-bit signature of one operator (blake2b of the canonical fields)."""
+    text = "\x1f".join([op_name, ",".join(str(int(s)) for s in shapes), dtype, callsite])
+    return int.from_bytes(hashlib.blake2b(text.encode(), digest_size=8).digest(), "little")
+
+
+def trace_signatures(trace) -> np.ndarray:
+    """Signatures of a reference-style Trace's operators (op name + element
+    counts of its input tensors, in order)."""
+    out = np.empty(len(trace.operators), dtype=np.uint64)
+    tensors = getattr(trace, "tensors", {}) or {}
+    for i, op in enumerate(trace.operators):
+        shapes = []
+        for t in op.input_tensor_ids:
+            snaps = tensors.get(t)
+            shapes.append(int(np.prod(snaps[0].shape)) if snaps else 0)
+        out[i] = signature_of(op.op_name, shapes)
+    return out
+
+
+def _sig_tensor(cols: TraceColumns, trace, dev) -> torch.Tensor:
+    if cols.op_sig is None:
+        if trace is None or isinstance(trace, TraceColumns):
+            if cols.op_names is None:
+                raise ValueError("no operator signatures: give op_sig or op_names")
+            sig = np.array([signature_of(n) for n in cols.op_names], dtype=np.uint64)
+        else:
+            sig = trace_signatures(trace)
+        cols.op_sig = sig
+    s = cols.device("op_sig")
+    return s if s.dtype == torch.int64 else s.view(torch.int64)
+
+
+def _ranks(cols: TraceColumns, dev) -> Optional[torch.Tensor]:
+    """Lexicographic rank of op ids (nodes_a tie-break); identity when ids are
+    absent (synthetic ids are zero-padded, so rank == index)."""
+    if cols.op_rank is not None:
+        return cols.device("op_rank")
+    if cols.op_ids is None:
+        return None
+    order = sorted(range(len(cols.op_ids)), key=lambda i: cols.op_ids[i])
+    rank = np.empty(len(order), dtype=np.int64)
+    rank[np.asarray(order, dtype=np.int64)] = np.arange(len(order), dtype=np.int64)
+    cols.op_rank = rank
+    return cols.device("op_rank")
+
+
+@dataclass
+class JoinDiff:
+    """Device-resident result of dw_join_diff (+ dw_rank)."""
+
+    P: int
+    n_matched: int
+    n_a_only: int
+    n_b_only: int
+    columns: FindingColumns
+    ia: torch.Tensor
+    ib: torch.Tensor
+    epw_a: Optional[torch.Tensor]
+    epw_b: Optional[torch.Tensor]
+    order: torch.Tensor          # top-k finding indices, report order
+    n_waste: int
+    wasted_joules: float         # exact sum over all waste findings
+
+    def top_findings(self, cols_a: TraceColumns, cols_b: TraceColumns) -> list[WasteFinding]:
+        idx = self.order
+        h = self.columns.host(idx) if self.columns.ratio is not None else None
+        ia = self.ia[idx].cpu().numpy()
+        ib = self.ib[idx].cpu().numpy()
+        name = lambda ids, i, p: (ids[i] if ids is not None else f"{p}{i}")  # noqa: E731
+        out = []
+        for r in range(len(ia)):
+            na = (name(cols_a.op_ids, int(ia[r]), "a"),) if ia[r] >= 0 else ()
+            nb = (name(cols_b.op_ids, int(ib[r]), "b"),) if ib[r] >= 0 else ()
+            out.append(WasteFinding(
+                pair=SubgraphPair(nodes_a=na, nodes_b=nb), energy_a=float(h["energy_a"][r]),
+                energy_b=float(h["energy_b"][r]), energy_ratio=float(h["ratio"][r]),
+                latency_a=int(h["latency_a"][r]), latency_b=int(h["latency_b"][r]),
+                output_rel_diff=0.0, verdict=VERDICTS[h["verdict"][r]], category="unknown",
+                wasteful_side=SIDES[h["side"][r]], wasted_joules=float(h["wasted"][r]),
+                informational=bool(h["informational"][r])))
+        return out
+
+
+def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
+              threshold: float = DEFAULT_THRESHOLD, k: int = 100, *, full_columns: bool = True,
+              epw: bool = True, work_a=None, work_b=None, stream=None) -> JoinDiff:
+    """Signature-join diff of two traces with their ledgers; top-k ranked."""
+    if ledger_a.method != ledger_b.method:
+        raise ValueError(f"ledger method mismatch: {ledger_a.method!r} vs {ledger_b.method!r}")
+    if not 0 < threshold <= 1:
+        raise ValueError("threshold must be in (0, 1]")
+    dev = _native.device()
+    ca, cb = TraceColumns.from_trace(trace_a), TraceColumns.from_trace(trace_b)
+    sides = []
+    keep = []
+    for cols, trace, led, work in ((ca, trace_a, ledger_a, work_a), (cb, trace_b, ledger_b, work_b)):
+        sig = _sig_tensor(cols, trace, dev)
+        j = led.operator_tensor()
+        if j is None:
+            ids = cols.op_ids
+            j = torch.tensor([float(led.per_operator[o]) for o in ids], dtype=torch.float64, device=dev)
+        w = None
+        if work is not None:
+            w = work if isinstance(work, torch.Tensor) else torch.as_tensor(work, dtype=torch.float64)
+            w = w.to(dev)
+        elif cols.op_work is not None:
+            w = cols.device("op_work")
+        rank = _ranks(cols, dev) if cols is ca else None
+        s, e = cols.device("op_start"), cols.device("op_end")
+        keep += [sig, j, w, rank, s, e]
+        p = _native.ptr
+        sides.append(_native.JoinSide(p(sig), p(s), p(e), p(j), p(w), p(rank), cols.n_ops))
+    na, nb = ca.n_ops, cb.n_ops
+    Pmax = na + nb
+    fc = FindingColumns(Pmax, dev, full=full_columns)
+    ia = torch.empty(Pmax, dtype=torch.int64, device=dev)
+    ib = torch.empty(Pmax, dtype=torch.int64, device=dev)
+    epw_a = torch.empty(Pmax, dtype=torch.float64, device=dev) if epw else None
+    epw_b = torch.empty(Pmax, dtype=torch.float64, device=dev) if epw else None
+    count = torch.zeros(4, dtype=torch.int64, device=dev)
+    L = _native.lib()
+    ws = _native.Workspace.get(L.dw_join_workspace_size(na, nb), stream)
+    fs = fc.c_struct()
+    p = _native.ptr
+    rc = L.dw_join_diff(ctypes.byref(sides[0]), ctypes.byref(sides[1]), float(threshold),
+                        ctypes.byref(fs), p(ia), p(ib), p(epw_a), p(epw_b), p(count),
+                        ws.data_ptr(), ws.numel(), _native.stream_handle(stream))
+    _native.check(rc, "dw_join_diff")
+    P, matched, a_only, b_only = (int(x) for x in count.cpu().tolist())
+    kk = min(k, P)
+    order, summary = rank_order(fc.key_hi[:P], fc.key_lo[:P], kk)
+    sm = summary.cpu().tolist()
+    return JoinDiff(P=P, n_matched=matched, n_a_only=a_only, n_b_only=b_only, columns=fc,
+                    ia=ia, ib=ib, epw_a=epw_a, epw_b=epw_b, order=order, n_waste=int(sm[0]),
+                    wasted_joules=float(sm[1]))
+
+
+def join_report(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
+                threshold: float = DEFAULT_THRESHOLD, k: int = 100) -> tuple[Report, JoinDiff]:
+    """A reference-shaped Report holding the top-k findings of the join diff;
+    wasted_joules / end_to_end_waste_pct cover every waste finding."""
+    jd = join_diff(trace_a, trace_b, ledger_a, ledger_b, threshold, k)
+    ca, cb = TraceColumns.from_trace(trace_a), TraceColumns.from_trace(trace_b)
+    top = jd.top_findings(ca, cb)
+    ineff = max(ledger_a.total_joules, ledger_b.total_joules)
+    pct = jd.wasted_joules / ineff if ineff > 0 else 0.0
+    rep = Report(findings=tuple(top), total_a=ledger_a.total_joules, total_b=ledger_b.total_joules,
+                 wasted_joules=jd.wasted_joules, end_to_end_waste_pct=pct, method=ledger_a.method,
+                 threshold=threshold)
+    return rep, jd

@@ -226,7 +226,7 @@ def _make_pair_streams(cfg: SynthConfig, g, dev, t0: int):
     sides = []
     per = cfg.n_ops // cfg.streams
     a_streams = [_draw_ops(per, cfg, g, dev) for _ in range(cfg.streams)]
-    offs = [int(x) for x in torch.randint(0, 5000, (cfg.streams,), generator=g).tolist()]
+    offs = [int(x) for x in torch.randint(0, 5000, (cfg.streams,), generator=g, device=dev).tolist()]
     for side in (0, 1):
         parts = []
         for s, a in enumerate(a_streams):

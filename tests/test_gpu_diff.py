@@ -1,0 +1,140 @@
+"""GPU parity of the differential diff: detect_waste / report against the
+reference's golden findings and ranking (bit-exact), the signature join and
+top-k ranking against the CPU oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import load_scenario, pair_tuples, scenario_names
+
+pytestmark = pytest.mark.gpu
+
+from paper_2512_08365_b200 import (SubgraphPair, TraceColumns, build_ledger,  # noqa: E402
+                                   detect_waste, join_diff, report)
+from paper_2512_08365_b200 import detect as D  # noqa: E402
+from paper_2512_08365_b200 import synth  # noqa: E402
+
+VCODE = {"below_threshold": 0, "tradeoff": 1, "waste": 2}
+SCODE = {"-": 0, "A": 1, "B": 2}
+
+
+def _cols(sc, side):
+    return TraceColumns.from_arrays(
+        sc[f"{side}_ts"], sc[f"{side}_watts"], sc[f"{side}_op_start"], sc[f"{side}_op_end"],
+        sc[f"{side}_k_start"], sc[f"{side}_k_end"], sc[f"{side}_k_op"],
+        trace_end=int(max(sc[f"{side}_span"][1] - 1, sc[f"{side}_ts"][-1])),
+        op_ids=[str(x) for x in sc[f"{side}_op_ids"]], k_ids=[str(x) for x in sc[f"{side}_k_ids"]],
+        op_names=[str(x) for x in sc[f"{side}_op_names"]])
+
+
+@pytest.mark.parametrize("name", scenario_names())
+@pytest.mark.parametrize("tag,theta", [("det10", 0.10), ("det05", 0.05)])
+def test_detect_and_report_golden(name, tag, theta):
+    sc = load_scenario(name)
+    ca, cb = _cols(sc, "a"), _cols(sc, "b")
+    la, lb = build_ledger(ca), build_ledger(cb)
+    pairs = [SubgraphPair(nodes_a=na, nodes_b=nb) for na, nb in
+             zip(pair_tuples(sc, "a"), pair_tuples(sc, "b"))]
+    fs = detect_waste(pairs, la, lb, theta, trace_a=ca, trace_b=cb,
+                      output_diff=sc["pair_out_diff"])
+    np.testing.assert_array_equal([[f.energy_a, f.energy_b] for f in fs],
+                                  sc[f"{tag}_energy"].reshape(-1, 2))
+    np.testing.assert_array_equal([f.energy_ratio for f in fs], sc[f"{tag}_ratio"])
+    np.testing.assert_array_equal([[f.latency_a, f.latency_b] for f in fs],
+                                  sc[f"{tag}_lat"].reshape(-1, 2))
+    np.testing.assert_array_equal([VCODE[f.verdict] for f in fs], sc[f"{tag}_verdict"])
+    np.testing.assert_array_equal([SCODE[f.wasteful_side] for f in fs], sc[f"{tag}_side"])
+    np.testing.assert_array_equal([f.wasted_joules for f in fs], sc[f"{tag}_wasted"])
+    np.testing.assert_array_equal([f.informational for f in fs], sc[f"{tag}_info"])
+    doc = report(fs, la, lb, theta)
+    pos = {id(f): i for i, f in enumerate(fs)}
+    np.testing.assert_array_equal([pos[id(f)] for f in doc.findings], sc[f"{tag}_rank"])
+    total_a, total_b, wasted, pct = sc[f"{tag}_report"]
+    assert doc.wasted_joules == wasted
+    assert doc.total_a == pytest.approx(total_a, rel=1e-12)
+    assert doc.end_to_end_waste_pct == pytest.approx(pct, rel=1e-12, abs=1e-15)
+
+
+def test_detect_errors():
+    sc = load_scenario(scenario_names()[0])
+    ca, cb = _cols(sc, "a"), _cols(sc, "b")
+    la, lb = build_ledger(ca), build_ledger(cb)
+    lb2 = build_ledger(cb, method="sampled", period_us=1000, delay_us=0)
+    with pytest.raises(ValueError, match="method"):
+        detect_waste([], la, lb2, trace_a=ca, trace_b=cb)
+    with pytest.raises(ValueError, match="threshold"):
+        detect_waste([], la, lb, 0.0, trace_a=ca, trace_b=cb)
+
+
+@pytest.mark.parametrize("P,k,ties", [(1000, 1000, False), (200_000, 100, False),
+                                      (200_000, 5000, True), (3_000_000, 1000, True)])
+def test_rank_vs_oracle(P, k, ties):
+    rng = np.random.default_rng(P + k)
+    wasted = rng.exponential(1.0, size=P)
+    if ties:
+        wasted = np.round(wasted, 1)
+        wasted[rng.random(P) < 0.3] = 0.0
+    verdict = rng.choice([0, 1, 2], size=P, p=[0.7, 0.2, 0.1]).astype(np.int8)
+    tie = rng.integers(0, P // 3 + 1, size=P)
+    order_ref = oracle.rank(verdict, wasted, tie)
+    bits = wasted.view(np.uint64) & np.uint64(0x7FFFFFFFFFFFFFFF)
+    hi = bits | ((verdict == 2).astype(np.uint64) << np.uint64(63))
+    lo = ~(((tie.astype(np.uint64) + np.uint64(1)) << np.uint64(32)) | np.arange(P, dtype=np.uint64))
+    dev = torch.device("cuda")
+    order, summary = D.rank_order(torch.from_numpy(hi.view(np.int64)).to(dev),
+                                  torch.from_numpy(lo.view(np.int64)).to(dev), k)
+    np.testing.assert_array_equal(order.cpu().numpy(), order_ref[:k])
+    s = summary.cpu().numpy()
+    assert s[0] == (verdict == 2).sum()
+    assert s[1] == oracle.fx_sum(wasted[verdict == 2])
+
+
+def _join_oracle(ca, cb, ja, jb, theta):
+    sig_a = ca.host("op_sig").view(np.uint64)
+    sig_b = cb.host("op_sig").view(np.uint64)
+    ma, mb = oracle.join(sig_a, sig_b)
+    na = len(ma)
+    off_a, mem_a, off_b, mem_b = [0], [], [0], []
+    for i in range(na):
+        mem_a.append(i)
+        if ma[i] >= 0:
+            mem_b.append(int(ma[i]))
+        off_a.append(len(mem_a))
+        off_b.append(len(mem_b))
+    b_only = np.nonzero(mb < 0)[0]
+    for j in b_only:
+        mem_b.append(int(j))
+        off_a.append(len(mem_a))
+        off_b.append(len(mem_b))
+    d = oracle.detect(off_a, mem_a, off_b, mem_b, ja, jb, ca.host("op_start"), ca.host("op_end"),
+                      cb.host("op_start"), cb.host("op_end"), None, theta)
+    tie = np.concatenate([np.arange(na) + 1, np.zeros(len(b_only), dtype=np.int64)])
+    return ma, mb, b_only, d, oracle.rank(d["verdict"], d["wasted"], tie)
+
+
+@pytest.mark.parametrize("cfg,n", [("C2", 50_000), ("C3", 40_000), ("C4", 100_000)])
+def test_join_vs_oracle(cfg, n):
+    ca, cb = synth.make_pair(synth.scaled(synth.CONFIGS[cfg], n))
+    la, lb = build_ledger(ca), build_ledger(cb)
+    ja, jb = la.per_operator.array(), lb.per_operator.array()
+    jd = join_diff(ca, cb, la, lb, 0.10, k=500)
+    ma, mb, b_only, d, order_ref = _join_oracle(ca, cb, ja, jb, 0.10)
+    na = len(ma)
+    assert jd.P == na + len(b_only)
+    assert jd.n_matched == int((ma >= 0).sum())
+    np.testing.assert_array_equal(jd.ib[:na].cpu().numpy(), ma)
+    np.testing.assert_array_equal(jd.ib[na:jd.P].cpu().numpy(), b_only)
+    h = jd.columns.host()
+    P = jd.P
+    np.testing.assert_array_equal(h["energy_a"][:P], d["energy"][:, 0])
+    np.testing.assert_array_equal(h["energy_b"][:P], d["energy"][:, 1])
+    np.testing.assert_array_equal(h["ratio"][:P], d["ratio"])
+    np.testing.assert_array_equal(h["verdict"][:P], d["verdict"])
+    np.testing.assert_array_equal(h["side"][:P], d["side"])
+    np.testing.assert_array_equal(h["wasted"][:P], d["wasted"])
+    np.testing.assert_array_equal(jd.order.cpu().numpy(), order_ref[:500])
+    waste = d["verdict"] == 2
+    assert jd.n_waste == waste.sum()
+    assert jd.wasted_joules == oracle.fx_sum(d["wasted"][waste])
+    assert jd.n_waste > 0  # the injected misconfiguration / redundancy is found
