@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark of the Magneton/diffwatt hot path on B200 (one JSON line).
+
+A step = attribution of both traces of a pair (per-operator and per-kernel
+joules, trapezoid over the trace's 10 kHz power samples) + the signature-join
+differential diff + the top-k ranked report on the host: the BASELINE config 4
+workload (100M operators / 1e9 power samples per trace) on
+one B200, generated in HBM from a fixed seed.
+
+  value  operator intervals (ops + kernels, both traces) attributed per second,
+         inputs resident in HBM (inputs >> 126 MB L2, so no flush is needed)
+  e2e    the same metric through the public API (pipeline.analyze) from pinned
+         host buffers: every step copies both traces host->HBM and reads the
+         report back
+  N > 1  one process per GPU (torchrun), each rank its own pair (weak scaling);
+         the per-rank top-k candidates are merged over NCCL (all_gather).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "operator-intervals attributed/sec and power-samples/sec; trace-pair diff latency"
+UNIT = "operator-intervals/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--method", default="samples", choices=("samples", "ground_truth"))
+    ap.add_argument("--k", type=int, default=100)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-ops", type=int, default=2_000_000)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak_gbs():
+    try:
+        with open(ROOT / "MEASURED_PEAKS.json") as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def profiled_traffic(config: str, method: str):
+    """dram bytes per tile-kernel launch from the committed ncu --set full summary."""
+    try:
+        with open(ROOT / "profiles" / "traffic.json") as fh:
+            d = json.load(fh)
+        return d.get(f"{config}:{method}")
+    except (OSError, ValueError):
+        return None
+
+
+def attr_bytes(cols) -> int:
+    """Algorithmic bytes of one ledger: 16 B per power sample + 24 B per
+    interval (start/end in, joules out) -- SURVEY.md 8(d)."""
+    return 16 * cols.n_power + 24 * (cols.n_ops + cols.n_kernels)
+
+
+def diff_bytes(ca, cb, P: int) -> int:
+    return 32 * (ca.n_ops + cb.n_ops) + 32 * P
+
+
+# ------------------------------------------------------------------ CPU arm
+
+
+def cpu_sample(cfg_name: str, n_ops: int, seed_shift: int = 0):
+    """A bounded sample of the same workload, generated on the host."""
+    import numpy as np  # noqa: F401
+    from paper_2512_08365_b200 import synth
+    cfg = synth.scaled(synth.CONFIGS[cfg_name], n_ops)
+    from dataclasses import replace
+    cfg = replace(cfg, seed=cfg.seed + seed_shift)
+    ca, cb = synth.make_pair(cfg, device="cpu")
+    return ca, cb
+
+
+def cpu_step(ca, cb, method: str, k: int):
+    """The reference hot path restated in C (oracle/, pthreads over all host
+    cores): ledger of both traces, signature join, detect rule, report order."""
+    import numpy as np
+    import oracle
+    kind = "linear" if method == "samples" else "step"
+    out = []
+    for c in (ca, cb):
+        ts, w = c.host("ts"), c.host("watts")
+        span_hi = None if kind == "linear" else c.signal_span()[1]
+        out.append(oracle.ledger(kind, ts, w, span_hi, c.host("op_start"), c.host("op_end"),
+                                 c.host("k_start"), c.host("k_end")))
+    ja, jb = out[0][0], out[1][0]
+    sig_a = c_sig(ca)
+    sig_b = c_sig(cb)
+    ma, mb = oracle.join(sig_a, sig_b)
+    na = len(ma)
+    b_only = np.nonzero(mb < 0)[0]
+    off_a = np.concatenate([np.arange(na + 1), np.full(len(b_only), na)]).astype(np.int64)
+    mem_a = np.arange(na, dtype=np.int32)
+    has_b = (ma >= 0).astype(np.int64)
+    off_b = np.concatenate([[0], np.cumsum(has_b), np.sum(has_b) + np.arange(1, len(b_only) + 1)])
+    mem_b = np.concatenate([ma[ma >= 0], b_only]).astype(np.int32)
+    d = oracle.detect(off_a, mem_a, off_b, mem_b, ja, jb, ca.host("op_start"), ca.host("op_end"),
+                      cb.host("op_start"), cb.host("op_end"), None, 0.10)
+    tie = np.concatenate([np.arange(na) + 1, np.zeros(len(b_only), dtype=np.int64)])
+    order = oracle.rank(d["verdict"], d["wasted"], tie)
+    return order[:k]
+
+
+def c_sig(c):
+    import numpy as np
+    s = c.host("op_sig")
+    return np.ascontiguousarray(s).view(np.uint64)
+
+
+def cpu_baseline(args, steps: int = 1) -> dict:
+    import oracle
+    ca, cb = cpu_sample(args.config, args.cpu_sample_ops)
+    intervals = ca.n_ops + ca.n_kernels + cb.n_ops + cb.n_kernels
+    cpu_step(ca, cb, args.method, args.k)  # warm (page-in, thread start)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        cpu_step(ca, cb, args.method, args.k)
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": intervals / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "port",
+            "sample": (f"{args.config} distribution scaled to {ca.n_ops}+{cb.n_ops} ops, "
+                       f"{ca.n_power}+{cb.n_power} samples (pair); oracle/dw_oracle.c "
+                       f"reference-order sums, {oracle.num_threads()} threads"),
+            "seconds_per_step": dt}
+
+
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    import oracle
+    ca, cb = cpu_sample(args.config, args.cpu_sample_ops)
+    intervals = ca.n_ops + ca.n_kernels + cb.n_ops + cb.n_kernels
+    for _ in range(args.warmup):
+        cpu_step(ca, cb, args.method, args.k)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_step(ca, cb, args.method, args.k)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = intervals / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config} (bounded CPU sample)", "method": args.method,
+                   "ops_per_trace": ca.n_ops, "samples_per_trace": ca.n_power},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "port",
+                         "sample": f"{ca.n_ops}+{cb.n_ops} ops, {ca.n_power}+{cb.n_power} samples"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+
+
+def run_ours(args, rank: int, world: int, local: int):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_08365_b200 import _native, synth
+    from paper_2512_08365_b200.columns import TraceColumns
+    from paper_2512_08365_b200.pipeline import analyze
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    L = _native.lib()
+    from dataclasses import replace
+    cfg = replace(synth.CONFIGS[args.config], seed=synth.CONFIGS[args.config].seed + 1000 * rank)
+    ca, cb = synth.make_pair(cfg, dev)
+    for c in (ca, cb):
+        for n in TraceColumns.HOT:
+            c.device(n)
+    torch.cuda.synchronize()
+    intervals = ca.n_ops + ca.n_kernels + cb.n_ops + cb.n_kernels
+    samples = ca.n_power + cb.n_power
+
+    def step():
+        res = analyze(ca, cb, args.method, 0.10, args.k)
+        if world > 1:  # global top-k over every rank's pair: merge the k candidates
+            top = torch.stack([res.join.columns.key_hi[res.join.order],
+                               res.join.columns.key_lo[res.join.order]], 1)
+            gathered = [torch.empty_like(top) for _ in range(world)]
+            dist.all_gather(gathered, top)
+        return res
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    L.dw_kernel_time_ms(1)
+    L.dw_kernel_timing(1)
+    _native.launch_count(reset=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            res = step()
+        e1.record()
+        torch.cuda.synchronize()
+    L.dw_kernel_timing(0)
+    launches = _native.launch_count(reset=True)
+    kern_ms = L.dw_kernel_time_ms(1) / (2 * args.steps)  # per tile-kernel launch
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+
+    # phase split of one step (rank-local): attribution vs diff latency
+    from paper_2512_08365_b200.energy import build_ledger
+    from paper_2512_08365_b200.join import join_diff
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    la = build_ledger(ca, method=args.method)
+    lb = build_ledger(cb, method=args.method)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    jd = join_diff(ca, cb, la, lb, 0.10, args.k, full_columns=False, epw=False)
+    jd.top_findings(ca, cb)
+    t2 = time.perf_counter()
+    P = res.join.P
+
+    # ---- e2e through the public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        del res, la, lb, jd
+        pinned = []
+        for c in (ca, cb):
+            kw = {n: getattr(c, n).cpu().pin_memory() for n in TraceColumns.HOT}
+            hc = TraceColumns(ts=kw["ts"], watts=kw["watts"], trace_end=c.trace_end,
+                              op_start=kw["op_start"], op_end=kw["op_end"], k_start=kw["k_start"],
+                              k_end=kw["k_end"], op_sig=kw["op_sig"], ops_sorted=c.ops_sorted,
+                              kernels_sorted=c.kernels_sorted)
+            hc._dev["first_last"] = c._first_last_ts()
+            pinned.append(hc)
+        h2d = sum(getattr(pc, n).numel() * getattr(pc, n).element_size()
+                  for pc in pinned for n in TraceColumns.HOT)
+        for c in (ca, cb):
+            c._dev.clear()
+        del ca, cb
+        torch.cuda.empty_cache()
+        copy_stream = torch.cuda.Stream()
+
+        def e2e_step():
+            for pc in pinned:
+                pc.drop_device()
+            r = analyze(pinned[0], pinned[1], args.method, 0.10, args.k, copy_stream=copy_stream)
+            return r
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.e2e_steps):
+            r = e2e_step()
+        f1.record()
+        torch.cuda.synchronize()
+        e_ms = f0.elapsed_time(f1) / args.e2e_steps
+        te = torch.tensor([e_ms], device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        # d2h: top-k indices/keys/columns + ledger totals read back for the report
+        d2h = args.k * (8 * 2 + 8 * 6 + 3) + 8 * 8
+        e2e = {"value": world * intervals / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": float(te.item()), "overlap": "trace B H2D under trace A attribution"}
+
+    if rank != 0:
+        return
+    peak, peak_kind = measured_peak_gbs()
+    a_bytes = (attr_bytes(pinned[0]) + attr_bytes(pinned[1])) / 2 if e2e else None
+    if a_bytes is None:
+        a_bytes = (16 * samples + 24 * intervals) / 2
+    achieved = a_bytes / (kern_ms * 1e-3) / 1e9
+    step_bytes = 16 * samples + 24 * intervals + 32 * (2 * cfg.n_ops) + 32 * P
+    line = {
+        "metric": METRIC, "value": world * intervals / (ms_max / 1e3), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: trace pair, {cfg.n_ops} ops and "
+                               f"{cfg.n_samples} power samples per trace",
+                   "method": args.method, "intervals_per_pair": intervals,
+                   "samples_per_pair": samples, "findings": P, "top_k": args.k,
+                   "l2": "inputs (~44 GB/pair) >> 126 MB L2; no flush needed",
+                   "parallelism": f"pair-per-rank x{world}"},
+        "samples_per_s": world * samples / (ms_max / 1e3),
+        "attribution_ms": (t1 - t0) * 1e3, "diff_latency_ms": (t2 - t1) * 1e3,
+        "step_hbm_fraction": (step_bytes / (ms_max * 1e-3) / 1e9) / peak,
+        "roofline": {"bound": "hbm", "kernel": "attribute_tiles_kernel", "achieved": achieved,
+                     "peak": peak, "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "bytes_per_launch": a_bytes, "launch_ms": kern_ms,
+                     "traffic": profiled_traffic(args.config, args.method)},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+    }
+    if world == 1:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args)
+        except Exception as exc:  # noqa: BLE001 - the baseline must not hide the GPU line
+            line["cpu_baseline"] = {"error": repr(exc)}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        run_ours(args, rank, world, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

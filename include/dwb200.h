@@ -182,11 +182,15 @@ typedef struct {
     int64_t n;
 } dw_join_side_t;
 
-size_t dw_join_workspace_size(int64_t na, int64_t nb);
-int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, double threshold,
-                 dw_findings_t *out, int64_t *d_ia, int64_t *d_ib, double *d_epw_a,
-                 double *d_epw_b, int64_t *d_count, void *d_workspace, size_t workspace_bytes,
-                 dw_stream_t stream);
+/* max_distinct bounds the number of distinct signatures (hash table of
+ * 2 x max_distinct slots; <= 0 means na + nb).  DW_E_WORKSPACE is returned if
+ * the table overflows; retry with a larger bound.  Finding columns other than
+ * the keys may be NULL (not written). */
+size_t dw_join_workspace_size(int64_t na, int64_t nb, int64_t max_distinct);
+int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_distinct,
+                 double threshold, dw_findings_t *out, int64_t *d_ia, int64_t *d_ib,
+                 double *d_epw_a, double *d_epw_b, int64_t *d_count, void *d_workspace,
+                 size_t workspace_bytes, dw_stream_t stream);
 
 /* --------------------------------------------------------------- misc */
 const char *dw_version(void);
@@ -194,6 +198,11 @@ const char *dw_error_string(int code);
 /* number of kernel launches issued by this library on the calling thread
  * since the last reset (bench.py's gpu_launches) */
 int64_t dw_launch_count(int reset);
+/* Profiling hook for bench.py's roofline: when enabled, CUDA events bracket
+ * every attribution tile-kernel launch on its stream; dw_kernel_time_ms
+ * synchronises them and returns the summed device time. */
+int dw_kernel_timing(int enable);
+double dw_kernel_time_ms(int reset);
 
 #ifdef __cplusplus
 }

@@ -36,7 +36,7 @@ EXPORTED = (
     "dw_attribute_workspace_size", "dw_attribute", "dw_ledger", "dw_status",
     "dw_fx_sum_workspace_size", "dw_fx_sum", "dw_step_value_at", "dw_detect_pairs",
     "dw_rank_workspace_size", "dw_rank", "dw_join_workspace_size", "dw_join_diff",
-    "dw_version", "dw_error_string", "dw_launch_count",
+    "dw_version", "dw_error_string", "dw_launch_count", "dw_kernel_timing", "dw_kernel_time_ms",
 )
 
 
@@ -116,6 +116,9 @@ def lib():
         L.dw_error_string.argtypes = [ctypes.c_int]
         L.dw_launch_count.restype = c_i64
         L.dw_launch_count.argtypes = [ctypes.c_int]
+        L.dw_kernel_timing.argtypes = [ctypes.c_int]
+        L.dw_kernel_time_ms.restype = ctypes.c_double
+        L.dw_kernel_time_ms.argtypes = [ctypes.c_int]
         if hasattr(L, "dw_detect_pairs"):
             L.dw_detect_pairs.argtypes = [c_i64] + [c_vp] * 12 + [ctypes.c_double,
                                                                   ctypes.POINTER(Findings), c_vp]
@@ -124,8 +127,8 @@ def lib():
             L.dw_rank.argtypes = [c_i64, ctypes.POINTER(Findings), c_i64, c_vp, c_vp, c_vp,
                                   ctypes.c_size_t, c_vp]
             L.dw_join_workspace_size.restype = ctypes.c_size_t
-            L.dw_join_workspace_size.argtypes = [c_i64, c_i64]
-            L.dw_join_diff.argtypes = [ctypes.POINTER(JoinSide), ctypes.POINTER(JoinSide),
+            L.dw_join_workspace_size.argtypes = [c_i64, c_i64, c_i64]
+            L.dw_join_diff.argtypes = [ctypes.POINTER(JoinSide), ctypes.POINTER(JoinSide), c_i64,
                                        ctypes.c_double, ctypes.POINTER(Findings), c_vp, c_vp,
                                        c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp]
         _lib = L

@@ -107,6 +107,31 @@ class TraceColumns:
             self._dev[key] = t
         return t
 
+    HOT = ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "op_sig")
+
+    def prefetch(self, stream: "torch.cuda.Stream", names=HOT) -> None:
+        """Start the host->HBM copies of ``names`` on ``stream`` (pinned host
+        buffers copy asynchronously); later device() calls on another stream
+        wait for them."""
+        dev = _native.device()
+        with torch.cuda.stream(stream):
+            for n in names:
+                if getattr(self, n) is not None:
+                    self.device(n)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        self._dev["__ready__"] = ev
+
+    def wait_ready(self) -> None:
+        ev = self._dev.pop("__ready__", None)
+        if ev is not None:
+            torch.cuda.current_stream().wait_event(ev)
+
+    def drop_device(self) -> None:
+        """Forget the HBM copies (the next device() call copies again)."""
+        for k in [k for k in self._dev if isinstance(k, tuple)]:
+            del self._dev[k]
+
     def host(self, name: str) -> np.ndarray:
         src = getattr(self, name)
         if isinstance(src, torch.Tensor):

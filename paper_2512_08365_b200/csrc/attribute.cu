@@ -1252,6 +1252,7 @@ static int attribute_impl(const dw_signal_t *sig, dw_interval_set_t *sets, int n
     }
     const size_t smem = ((sizeof(TileSmem) + 15) & ~(size_t)15) + GROUPS * sizeof(GroupSmem);
     int grid = (int)std::min<int64_t>(p.ntiles, (int64_t)num_sms() * CTAS_PER_SM);
+    timing_begin(stream);
     if (sig->kind == DW_SIGNAL_STEP) {
         cudaFuncSetAttribute(attribute_tiles_kernel<DW_SIGNAL_STEP>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1261,6 +1262,7 @@ static int attribute_impl(const dw_signal_t *sig, dw_interval_set_t *sets, int n
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attribute_tiles_kernel<DW_SIGNAL_LINEAR><<<grid, KTHREADS, smem, stream>>>(p);
     }
+    timing_end(stream);
     count_launch();
     {
         const int64_t nblk = ceil_div(p.ntiles, SCAN_CHUNK);

@@ -6,8 +6,26 @@
 namespace dw {
 
 static thread_local int64_t g_launches = 0;
+static thread_local int g_timing = 0;
+static thread_local cudaEvent_t g_ev[2 * 64];
+static thread_local int g_nev = 0;
+static thread_local double g_pending_ms = 0.0;
 
 void count_launch(int n) { g_launches += n; }
+
+// Events around the attribution tile kernel (bench.py's roofline timing).
+void timing_begin(cudaStream_t s) {
+    if (!g_timing) return;
+    if (g_nev >= 64) return;
+    cudaEvent_t *e = &g_ev[2 * g_nev];
+    if (!e[0]) { cudaEventCreate(&e[0]); cudaEventCreate(&e[1]); }
+    cudaEventRecord(e[0], s);
+}
+void timing_end(cudaStream_t s) {
+    if (!g_timing || g_nev >= 64) return;
+    cudaEventRecord(g_ev[2 * g_nev + 1], s);
+    ++g_nev;
+}
 
 int num_sms() {
     static thread_local int cached_dev = -1, cached_sms = 0;
@@ -39,6 +57,25 @@ const char *dw_error_string(int code) {
         case DW_E_UNSORTED: return "interval set flagged sorted is not sorted by start";
         default: return "unknown error";
     }
+}
+
+int dw_kernel_timing(int enable) {
+    dw::g_timing = enable;
+    return DW_OK;
+}
+
+double dw_kernel_time_ms(int reset) {
+    using namespace dw;
+    double total = g_pending_ms;
+    for (int i = 0; i < g_nev; ++i) {
+        float ms = 0.f;
+        cudaEventSynchronize(g_ev[2 * i + 1]);
+        cudaEventElapsedTime(&ms, g_ev[2 * i], g_ev[2 * i + 1]);
+        total += ms;
+    }
+    g_nev = 0;
+    g_pending_ms = reset ? 0.0 : total;
+    return total;
 }
 
 int64_t dw_launch_count(int reset) {

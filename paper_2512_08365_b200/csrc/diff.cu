@@ -683,11 +683,13 @@ int dw_rank(int64_t P, const dw_findings_t *f, int64_t k, int64_t *d_order, doub
                      (cudaStream_t)stream);
 }
 
-size_t dw_join_workspace_size(int64_t na, int64_t nb) { return join_layout(na, nb, 0).total; }
+size_t dw_join_workspace_size(int64_t na, int64_t nb, int64_t max_distinct) {
+    return join_layout(na, nb, max_distinct).total;
+}
 
-int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, double threshold, dw_findings_t *out,
-                 int64_t *d_ia, int64_t *d_ib, double *d_epw_a, double *d_epw_b, int64_t *d_count,
-                 void *d_workspace, size_t workspace_bytes, dw_stream_t stream) {
+int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_distinct, double threshold,
+                 dw_findings_t *out, int64_t *d_ia, int64_t *d_ib, double *d_epw_a, double *d_epw_b,
+                 int64_t *d_count, void *d_workspace, size_t workspace_bytes, dw_stream_t stream) {
     if (!(threshold > 0.0 && threshold <= 1.0)) return DW_E_ARG;
     if (!a || !b || !out || !d_count || !d_workspace) return DW_E_ARG;
     const int64_t na = a->n, nb = b->n;
@@ -696,7 +698,7 @@ int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, double thresh
         (nb && (!b->d_sig || !b->d_start || !b->d_end || !b->d_joules)))
         return DW_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
-    JoinLayout L = join_layout(na, nb, 0);
+    JoinLayout L = join_layout(na, nb, max_distinct);
     if (workspace_bytes < L.total) return DW_E_WORKSPACE;
     char *base = (char *)d_workspace;
     JoinParams q{};

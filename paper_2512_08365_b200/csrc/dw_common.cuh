@@ -213,6 +213,8 @@ __device__ __forceinline__ void atomic_min_index(unsigned long long *p, int64_t 
 
 // host-side launch accounting (bench.py gpu_launches)
 void count_launch(int n = 1);
+void timing_begin(cudaStream_t s);
+void timing_end(cudaStream_t s);
 int num_sms();
 
 }  // namespace dw

@@ -74,29 +74,23 @@ class WasteFinding:
 
 
 class FindingColumns:
-    """Device columns of a batch of findings (one dw_findings_t)."""
+    """Device columns of a batch of findings (one dw_findings_t).  ``columns``
+    selects which optional columns are written (the ranking keys always are)."""
 
-    def __init__(self, P: int, dev, full: bool = True):
-        f64 = dict(dtype=torch.float64, device=dev)
-        i64 = dict(dtype=torch.int64, device=dev)
-        i8 = dict(dtype=torch.int8, device=dev)
+    ALL = ("energy_a", "energy_b", "ratio", "wasted", "latency_a", "latency_b", "verdict", "side",
+           "informational")
+    LEAN = ("ratio", "wasted", "verdict", "side", "informational")
+
+    def __init__(self, P: int, dev, full: bool = True, columns=None):
+        cols = self.ALL if (columns is None and full) else (columns or self.LEAN)
+        types = {"energy_a": torch.float64, "energy_b": torch.float64, "ratio": torch.float64,
+                 "wasted": torch.float64, "latency_a": torch.int64, "latency_b": torch.int64,
+                 "verdict": torch.int8, "side": torch.int8, "informational": torch.int8}
         self.P = P
-        self.key_hi = torch.empty(P, **i64)
-        self.key_lo = torch.empty(P, **i64)
-        if full:
-            self.energy_a = torch.empty(P, **f64)
-            self.energy_b = torch.empty(P, **f64)
-            self.ratio = torch.empty(P, **f64)
-            self.wasted = torch.empty(P, **f64)
-            self.latency_a = torch.empty(P, **i64)
-            self.latency_b = torch.empty(P, **i64)
-            self.verdict = torch.empty(P, **i8)
-            self.side = torch.empty(P, **i8)
-            self.informational = torch.empty(P, **i8)
-        else:
-            self.energy_a = self.energy_b = self.ratio = self.wasted = None
-            self.latency_a = self.latency_b = None
-            self.verdict = self.side = self.informational = None
+        self.key_hi = torch.empty(P, dtype=torch.int64, device=dev)
+        self.key_lo = torch.empty(P, dtype=torch.int64, device=dev)
+        for name in self.ALL:
+            setattr(self, name, torch.empty(P, dtype=types[name], device=dev) if name in cols else None)
 
     def c_struct(self) -> _native.Findings:
         p = _native.ptr

@@ -38,6 +38,10 @@ REPLAY_MARGIN = 0.10
 IDLE_OP = "idle"
 
 METHODS = ("ground_truth", "sampled", "replay")
+# Extension for traces whose power records are already high-rate meter
+# samples (the scale configs): integrate them with the sampled branch's
+# trapezoid (energy.py:108-130) as given, without re-sampling.
+EXTRA_METHODS = ("samples",)
 
 
 class SignalError(ValueError):
@@ -490,15 +494,30 @@ def build_ledger(trace, method: str = "ground_truth",
     TraceColumns.  Gaps between kernels inside an operator's interval go to the
     operator; gaps between operators go to ``idle``.
     """
-    if method not in METHODS:
+    if method not in METHODS and method not in EXTRA_METHODS:
         raise ValueError(f"unknown energy method {method!r}")
     cols = TraceColumns.from_trace(trace)
+    if method == "samples":
+        if cols.n_power == 0:
+            raise SignalError("trace carries no power records")
+        cols.wait_ready()
+        first, last = cols._first_last_ts()
+        signal = PowerSignal.from_columns(cols.device("ts"), cols.device("watts"), kind="linear")
+        signal._span_hi = last
+        per_op, per_k, st = _run_ledger(cols, signal, validate_order)
+        _raise_ledger_errors(cols, st, signal.span())
+        return EnergyLedger(method=method, per_kernel=JoulesView(cols.k_ids, per_k, "k"),
+                            per_operator=JoulesView(cols.op_ids, per_op, "op"),
+                            idle_joules=float(st.totals[2]), total_joules=float(st.totals[0]),
+                            op_total=float(st.totals[1]))
     truth = ground_truth_signal(cols)
     if method == "replay":
         from .replay import replay_ledger
         return replay_ledger(trace, cols, truth, repeat, period_us, delay_us, seed)
     if method == "ground_truth":
-        signal = truth
+        cols.wait_ready()
+        signal = PowerSignal.from_columns(cols.device("ts"), cols.device("watts"),
+                                          truth._span_hi, "step")
     else:
         signal = sampled_view(cols, period_us, delay_us, seed)
     per_op, per_k, st = _run_ledger(cols, signal, validate_order)

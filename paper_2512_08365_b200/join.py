@@ -102,29 +102,56 @@ class JoinDiff:
     n_waste: int
     wasted_joules: float         # exact sum over all waste findings
 
+    ja: Optional[torch.Tensor] = None    # operator joules of A / B (for lean columns)
+    jb: Optional[torch.Tensor] = None
+
     def top_findings(self, cols_a: TraceColumns, cols_b: TraceColumns) -> list[WasteFinding]:
+        """Materialise the top-k findings (report order) as reference-style
+        WasteFinding objects; columns not written by the join are gathered from
+        the ledgers on the device for these k rows only."""
         idx = self.order
-        h = self.columns.host(idx) if self.columns.ratio is not None else None
-        ia = self.ia[idx].cpu().numpy()
-        ib = self.ib[idx].cpu().numpy()
+        c = self.columns
+        ia_d, ib_d = self.ia[idx], self.ib[idx]
+        has_a, has_b = ia_d >= 0, ib_d >= 0
+        ia_c, ib_c = ia_d.clamp(min=0), ib_d.clamp(min=0)
+
+        def pick(name, fallback):
+            t = getattr(c, name)
+            return (t[idx] if t is not None else fallback()).cpu().numpy()
+
+        zero_f = torch.zeros((), dtype=torch.float64, device=idx.device)
+        zero_i = torch.zeros((), dtype=torch.int64, device=idx.device)
+        ea = pick("energy_a", lambda: torch.where(has_a, self.ja[ia_c], zero_f))
+        eb = pick("energy_b", lambda: torch.where(has_b, self.jb[ib_c], zero_f))
+        la = pick("latency_a", lambda: torch.where(
+            has_a, cols_a.device("op_end")[ia_c] - cols_a.device("op_start")[ia_c], zero_i))
+        lb = pick("latency_b", lambda: torch.where(
+            has_b, cols_b.device("op_end")[ib_c] - cols_b.device("op_start")[ib_c], zero_i))
+        h = {n: getattr(c, n)[idx].cpu().numpy() for n in ("ratio", "wasted", "verdict", "side",
+                                                            "informational")}
+        ia, ib = ia_d.cpu().numpy(), ib_d.cpu().numpy()
         name = lambda ids, i, p: (ids[i] if ids is not None else f"{p}{i}")  # noqa: E731
         out = []
         for r in range(len(ia)):
             na = (name(cols_a.op_ids, int(ia[r]), "a"),) if ia[r] >= 0 else ()
             nb = (name(cols_b.op_ids, int(ib[r]), "b"),) if ib[r] >= 0 else ()
             out.append(WasteFinding(
-                pair=SubgraphPair(nodes_a=na, nodes_b=nb), energy_a=float(h["energy_a"][r]),
-                energy_b=float(h["energy_b"][r]), energy_ratio=float(h["ratio"][r]),
-                latency_a=int(h["latency_a"][r]), latency_b=int(h["latency_b"][r]),
+                pair=SubgraphPair(nodes_a=na, nodes_b=nb), energy_a=float(ea[r]),
+                energy_b=float(eb[r]), energy_ratio=float(h["ratio"][r]),
+                latency_a=int(la[r]), latency_b=int(lb[r]),
                 output_rel_diff=0.0, verdict=VERDICTS[h["verdict"][r]], category="unknown",
                 wasteful_side=SIDES[h["side"][r]], wasted_joules=float(h["wasted"][r]),
                 informational=bool(h["informational"][r])))
         return out
 
 
+DEFAULT_MAX_DISTINCT = 1 << 20
+
+
 def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
               threshold: float = DEFAULT_THRESHOLD, k: int = 100, *, full_columns: bool = True,
-              epw: bool = True, work_a=None, work_b=None, stream=None) -> JoinDiff:
+              epw: bool = True, work_a=None, work_b=None, stream=None,
+              max_distinct: int = DEFAULT_MAX_DISTINCT) -> JoinDiff:
     """Signature-join diff of two traces with their ledgers; top-k ranked."""
     if ledger_a.method != ledger_b.method:
         raise ValueError(f"ledger method mismatch: {ledger_a.method!r} vs {ledger_b.method!r}")
@@ -160,12 +187,18 @@ def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
     epw_b = torch.empty(Pmax, dtype=torch.float64, device=dev) if epw else None
     count = torch.zeros(4, dtype=torch.int64, device=dev)
     L = _native.lib()
-    ws = _native.Workspace.get(L.dw_join_workspace_size(na, nb), stream)
     fs = fc.c_struct()
     p = _native.ptr
-    rc = L.dw_join_diff(ctypes.byref(sides[0]), ctypes.byref(sides[1]), float(threshold),
-                        ctypes.byref(fs), p(ia), p(ib), p(epw_a), p(epw_b), p(count),
-                        ws.data_ptr(), ws.numel(), _native.stream_handle(stream))
+    md = int(min(max_distinct, na + nb)) if max_distinct else 0
+    while True:
+        ws = _native.Workspace.get(L.dw_join_workspace_size(na, nb, md), stream)
+        rc = L.dw_join_diff(ctypes.byref(sides[0]), ctypes.byref(sides[1]), md, float(threshold),
+                            ctypes.byref(fs), p(ia), p(ib), p(epw_a), p(epw_b), p(count),
+                            ws.data_ptr(), ws.numel(), _native.stream_handle(stream))
+        if rc == _native.DW_E_WORKSPACE and md and md < na + nb:
+            md = min(4 * md, na + nb)  # more distinct signatures than the table held
+            continue
+        break
     _native.check(rc, "dw_join_diff")
     P, matched, a_only, b_only = (int(x) for x in count.cpu().tolist())
     kk = min(k, P)
@@ -173,7 +206,7 @@ def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
     sm = summary.cpu().tolist()
     return JoinDiff(P=P, n_matched=matched, n_a_only=a_only, n_b_only=b_only, columns=fc,
                     ia=ia, ib=ib, epw_a=epw_a, epw_b=epw_b, order=order, n_waste=int(sm[0]),
-                    wasted_joules=float(sm[1]))
+                    wasted_joules=float(sm[1]), ja=keep[1], jb=keep[7])
 
 
 def join_report(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
