@@ -258,8 +258,7 @@ def run_ours(args, rank: int, world: int, local: int):
     def step():
         res = analyze(ca, cb, args.method, 0.10, args.k)
         if world > 1:  # global top-k over every rank's pair: merge the k candidates
-            top = torch.stack([res.join.columns.key_hi[res.join.order],
-                               res.join.columns.key_lo[res.join.order]], 1)
+            top = torch.stack([res.join.columns.key_hi[res.join.order], res.join.order], 1)
             gathered = [torch.empty_like(top) for _ in range(world)]
             dist.all_gather(gathered, top)
         return res

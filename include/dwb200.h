@@ -132,7 +132,13 @@ int dw_step_value_at(const dw_signal_t *sig, const double *d_t, int64_t m, doubl
 
 /* ------------------------------------------------------------------ diff */
 
-/* Per-pair columns written by dw_detect_pairs / dw_join_diff. */
+/* Per-finding columns written by dw_detect_pairs / dw_join_diff.  Every column
+ * but d_key_hi may be NULL (not written).  The ranking key is the 128-bit
+ * (key_hi, key_lo), report order = descending: key_hi = waste flag << 63 |
+ * bits of wasted_joules; key_lo = ~((tie + 1) << 32 | finding index) with tie
+ * the rank of nodes_a.  When d_key_lo is NULL, dw_rank derives key_lo from the
+ * join's numbering: tie = d_tie_rank[f] (or f when NULL) for f < n_a, -1 for
+ * the B-only findings after them. */
 typedef struct {
     double *d_energy_a, *d_energy_b; /* [P] */
     double *d_ratio;                 /* [P] high/low, 1.0 when equal, inf when low == 0 */
@@ -141,7 +147,9 @@ typedef struct {
     int8_t *d_side;                  /* [P] 0 "-", 1 "A", 2 "B" */
     int8_t *d_informational;         /* [P] */
     double *d_wasted;                /* [P] high - low */
-    uint64_t *d_key_hi, *d_key_lo;   /* [P] ranking key (report order = descending) */
+    uint64_t *d_key_hi, *d_key_lo;   /* [P] ranking key */
+    const int64_t *d_tie_rank;       /* implicit key_lo: A-op id ranks (NULL = index) */
+    int64_t n_a;                     /* implicit key_lo: number of A-op findings */
 } dw_findings_t;
 
 /* detect_waste over CSR segment pairs (reference SubgraphPair lists).
@@ -168,10 +176,11 @@ int dw_rank(int64_t P, const dw_findings_t *f, int64_t k, int64_t *d_order, doub
 /* Signature hash-join diff.  Operators of A and B
  * are keyed by (sig, occurrence in op order); equal keys pair up, unmatched
  * operators become one-sided findings.  Findings are numbered: A ops in order
- * (matched or A-only), then B-only ops in order.  d_work_* (may be NULL = 1.0)
- * is useful work per op; d_epw_* receives joules per unit of work.  d_rank_a[i]
- * is the lexicographic rank of A op i's id (tie-break).  Outputs per finding:
- * the dw_findings_t columns plus d_ia / d_ib (-1 on the empty side).
+ * (f < n_a: matched or A-only), then B-only ops in B order (f = n_a + r).
+ * Outputs: d_match_a[i] = B op paired with A op i or -1; d_b_only[r] = the
+ * r-th B-only op; finding columns (out); d_epw_* (may be NULL) joules per unit
+ * of useful work (d_work NULL = 1 per op).  d_rank (A side) is the
+ * lexicographic rank of each A op id (report tie-break; NULL = index).
  * *d_count receives {P, n_matched, n_a_only, n_b_only}. */
 typedef struct {
     const uint64_t *d_sig;   /* [n] */
@@ -188,7 +197,7 @@ typedef struct {
  * the keys may be NULL (not written). */
 size_t dw_join_workspace_size(int64_t na, int64_t nb, int64_t max_distinct);
 int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_distinct,
-                 double threshold, dw_findings_t *out, int64_t *d_ia, int64_t *d_ib,
+                 double threshold, dw_findings_t *out, int32_t *d_match_a, int32_t *d_b_only,
                  double *d_epw_a, double *d_epw_b, int64_t *d_count, void *d_workspace,
                  size_t workspace_bytes, dw_stream_t stream);
 

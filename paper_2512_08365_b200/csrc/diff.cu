@@ -91,7 +91,7 @@ __device__ __forceinline__ void store_finding(const FindCols &o, int64_t f, doub
     if (o.info) o.info[f] = v.info;
     if (o.wasted) o.wasted[f] = v.wasted;
     o.khi[f] = key_hi(v.verdict, v.wasted);
-    o.klo[f] = key_lo(tie, f);
+    if (o.klo) o.klo[f] = key_lo(tie, f);
 }
 
 static FindCols cols_of(const dw_findings_t *f) {
@@ -147,6 +147,8 @@ __global__ void detect_pairs_kernel(int64_t P, const int64_t *off_a, const int32
 // ------------------------------------------------------------------ K6 rank
 struct RankParams {
     const uint64_t *khi, *klo;
+    const int64_t *tie_rank;   // implicit low keys (klo == NULL): join numbering
+    int64_t n_a;
     int64_t P, k;
     unsigned int *hist;        // [HIST_BINS]
     unsigned long long *sel;   // [2]: bin, count strictly above the bin
@@ -157,6 +159,14 @@ struct RankParams {
     int pos;                   // bit position of the current digit in the 128-bit key
     uint64_t phi, plo, mhi, mlo;  // prefix fixed so far and its mask
 };
+
+// the low key of finding i: stored, or implied by the join's numbering
+// (A findings: tie = rank of the A op; B-only findings: tie = -1)
+__device__ __forceinline__ uint64_t lo_of(const RankParams &r, int64_t i) {
+    if (r.klo) return r.klo[i];
+    const int64_t tie = i < r.n_a ? (r.tie_rank ? r.tie_rank[i] : i) : -1;
+    return key_lo(tie, i);
+}
 
 __device__ __forceinline__ unsigned digit128(uint64_t hi, uint64_t lo, int pos) {
     return pos >= 64 ? (unsigned)((hi >> (pos - 64)) & (HIST_BINS - 1))
@@ -172,7 +182,7 @@ __global__ void rank_hist_kernel(RankParams r) {
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t hi = r.khi[i];
         if ((hi & r.mhi) != r.phi) continue;
-        const uint64_t lo = need_lo ? r.klo[i] : 0;
+        const uint64_t lo = need_lo ? lo_of(r, i) : 0;
         if ((lo & r.mlo) != r.plo) continue;
         atomicAdd(&h[digit128(hi, lo, r.pos)], 1u);
     }
@@ -201,7 +211,7 @@ __global__ void rank_compact_kernel(RankParams r, uint64_t thr_hi, uint64_t thr_
          i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t hi = r.khi[i];
         if (hi < thr_hi) continue;
-        const uint64_t lo = r.klo[i];
+        const uint64_t lo = lo_of(r, i);
         if (hi == thr_hi && lo < thr_lo) continue;
         unsigned long long slot = atomicAdd(r.cand_n, 1ULL);
         if ((int64_t)slot < r.cand_cap) {
@@ -232,13 +242,21 @@ __global__ void waste_sum_kernel(const uint64_t *khi, int64_t P, unsigned long l
     __shared__ bool last;
     i128 acc = 0;
     unsigned long long cnt = 0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t k = khi[i];
-        if (k >> 63) {
-            acc += fx_from_double(__longlong_as_double((long long)(k & 0x7FFFFFFFFFFFFFFFULL)),
-                                  FX_JOULE_BITS);
-            ++cnt;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x * 4 + threadIdx.x; b < P; b += stride) {
+        uint64_t k[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = b + (int64_t)u * blockDim.x;
+            k[u] = i < P ? khi[i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (k[u] >> 63) {
+                acc += fx_from_double(__longlong_as_double((long long)(k[u] & 0x7FFFFFFFFFFFFFFFULL)),
+                                      FX_JOULE_BITS);
+                ++cnt;
+            }
         }
     }
     acc = warp_sum_i128(acc);
@@ -296,90 +314,134 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 struct JoinParams {
     const uint64_t *sig_a, *sig_b;
     int64_t na, nb;
-    uint64_t *table;  // [cap] keys
-    int32_t *slot_id; // [cap] dense id (1-based; 0 reserved for sig == EMPTY)
-    int64_t cap;      // power of two
-    int32_t *d_a, *d_b;
+    uint64_t *table;            // [cap] signature keys
+    int32_t *ids;               // [cap] dense id of the slot (1-based; 0 = not yet published)
+    unsigned int *next_id;      // id counter
+    int64_t cap;                // power of two
+    uint64_t *keys_a, *keys_b;  // (id << 32) | op index -- the radix sort input
     unsigned long long *overflow;
 };
 
-__global__ void join_insert_kernel(JoinParams q) {
-    const int64_t n = q.na + q.nb;
+// Signature -> dense id, in one pass: the thread whose CAS claims an empty
+// slot draws the id and publishes it; threads meeting the same signature spin
+// on the published id.  Ids depend on the race, but the pairing only needs
+// "same signature, same id" and the stable order inside an id, so the result
+// is deterministic.
+__device__ __forceinline__ int32_t sig_id(const JoinParams &q, uint64_t s) {
+    if (s == EMPTY) return 0;  // reserved id for the sentinel value
     const uint64_t mask = (uint64_t)q.cap - 1;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t s = i < q.na ? q.sig_a[i] : q.sig_b[i - q.na];
-        if (s == EMPTY) continue;
-        uint64_t h = mix64(s) & mask;
-        for (int64_t probe = 0;; ++probe) {
-            if (probe >= q.cap) {
-                atomicAdd(q.overflow, 1ULL);
-                break;
-            }
-            uint64_t k = q.table[h];
-            if (k == s) break;
+    uint64_t h = mix64(s) & mask;
+    for (int64_t probe = 0; probe < q.cap; ++probe) {
+        uint64_t k = q.table[h];
+        if (k == EMPTY) {
+            k = atomicCAS((unsigned long long *)&q.table[h], EMPTY, s);
             if (k == EMPTY) {
-                uint64_t old = atomicCAS((unsigned long long *)&q.table[h], EMPTY, s);
-                if (old == EMPTY || old == s) break;
+                const int32_t id = (int32_t)atomicAdd(q.next_id, 1u) + 1;
+                atomicExch((int *)&q.ids[h], id);
+                return id;
             }
-            h = (h + 1) & mask;
         }
+        if (k == s) {
+            int32_t id;
+            while ((id = *(volatile int32_t *)&q.ids[h]) == 0) {
+            }
+            return id;
+        }
+        h = (h + 1) & mask;
     }
+    atomicAdd(q.overflow, 1ULL);
+    return 0;
 }
 
-__global__ void join_flags_kernel(JoinParams q) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < q.cap;
-         i += (int64_t)gridDim.x * blockDim.x)
-        q.slot_id[i] = q.table[i] != EMPTY ? 1 : 0;
-}
+constexpr int ITEMS = 4;  // elements per thread in the streaming kernels (memory-level parallelism)
 
-__global__ void join_lookup_kernel(JoinParams q) {
+__global__ void join_hash_kernel(JoinParams q) {
     const int64_t n = q.na + q.nb;
     const uint64_t mask = (uint64_t)q.cap - 1;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t s = i < q.na ? q.sig_a[i] : q.sig_b[i - q.na];
-        int32_t id = 0;
-        if (s != EMPTY) {
-            uint64_t h = mix64(s) & mask;
-            while (q.table[h] != s) h = (h + 1) & mask;
-            id = q.slot_id[h];  // inclusive scan of occupancy: 1-based
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * ITEMS;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS + threadIdx.x; base < n; base += stride) {
+        uint64_t sg[ITEMS], tk[ITEMS], hh[ITEMS];
+        int32_t id[ITEMS];
+#pragma unroll
+        for (int u = 0; u < ITEMS; ++u) {
+            const int64_t i = base + (int64_t)u * blockDim.x;
+            sg[u] = i < n ? (i < q.na ? q.sig_a[i] : q.sig_b[i - q.na]) : EMPTY;
         }
-        if (i < q.na) q.d_a[i] = id;
-        else q.d_b[i - q.na] = id;
+        // speculative first probe for all items at once (present signatures
+        // resolve here: one L2 round trip for the table and the id)
+#pragma unroll
+        for (int u = 0; u < ITEMS; ++u) {
+            hh[u] = mix64(sg[u]) & mask;
+            tk[u] = q.table[hh[u]];
+            id[u] = *(volatile int32_t *)&q.ids[hh[u]];
+        }
+#pragma unroll
+        for (int u = 0; u < ITEMS; ++u) {
+            const int64_t i = base + (int64_t)u * blockDim.x;
+            if (i >= n) continue;
+            int32_t d = (tk[u] == sg[u] && id[u] != 0 && sg[u] != EMPTY) ? id[u] : sig_id(q, sg[u]);
+            const bool a = i < q.na;
+            const int64_t li = a ? i : i - q.na;
+            const uint64_t key = ((uint64_t)(uint32_t)d << 32) | (uint64_t)(uint32_t)li;
+            if (a) q.keys_a[li] = key;
+            else q.keys_b[li] = key;
+        }
     }
 }
 
-// run boundaries of a sorted id column -> first[d], count[d]
-__global__ void run_bounds_kernel(const int32_t *dsorted, int64_t n, int64_t *first, int64_t *count) {
+// runs of equal ids in a sorted key column -> first[id], end[id]
+__global__ void run_bounds_kernel(const uint64_t *sorted, int64_t n, int32_t *first, int32_t *end) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= n) return;
-    const int32_t d = dsorted[p];
-    if (p == 0 || dsorted[p - 1] != d) first[d] = p;
-    if (p == n - 1 || dsorted[p + 1] != d) count[d] = p + 1;  // end; turned into a count below
-}
-__global__ void run_counts_kernel(const int64_t *first, int64_t *count, int64_t D) {
-    const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (d >= D) return;
-    if (count[d] > 0) count[d] -= first[d];
+    const uint32_t d = (uint32_t)(sorted[p] >> 32);
+    if (p == 0 || (uint32_t)(sorted[p - 1] >> 32) != d) first[d] = (int32_t)p;
+    if (p == n - 1 || (uint32_t)(sorted[p + 1] >> 32) != d) end[d] = (int32_t)(p + 1);
 }
 
-// k-th occurrence pairing over A's sorted order
-__global__ void join_pair_kernel(const int32_t *da_sorted, const int64_t *ia_sorted, int64_t na,
-                                 const int64_t *first_a, const int64_t *first_b,
-                                 const int64_t *count_b, const int64_t *ib_sorted,
-                                 int64_t *match_a, int64_t *match_b) {
-    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= na) return;
-    const int32_t d = da_sorted[p];
-    const int64_t t = p - first_a[d];
-    const int64_t i = ia_sorted[p];
-    int64_t j = -1;
-    if (t < count_b[d]) {
-        j = ib_sorted[first_b[d] + t];
-        match_b[j] = i;
+// t-th occurrence of id d in A pairs with the t-th occurrence of d in B
+__global__ void join_pair_kernel(const uint64_t *sa, int64_t na, const int32_t *first_a,
+                                 const uint64_t *sb, const int32_t *first_b, const int32_t *end_b,
+                                 int32_t *match_a) {
+    const int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS + threadIdx.x;
+    uint64_t key[ITEMS];
+    int32_t fa[ITEMS], fb[ITEMS], eb[ITEMS], j[ITEMS];
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+        const int64_t p = base + (int64_t)u * blockDim.x;
+        key[u] = p < na ? sa[p] : 0;
     }
-    match_a[i] = j;
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+        const uint32_t d = (uint32_t)(key[u] >> 32);
+        fa[u] = first_a[d];
+        fb[u] = first_b[d];
+        eb[u] = end_b[d];
+    }
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+        const int64_t p = base + (int64_t)u * blockDim.x;
+        const int32_t t = (int32_t)p - fa[u];
+        j[u] = (p < na && eb[u] > 0 && t < eb[u] - fb[u]) ? (int32_t)(uint32_t)sb[fb[u] + t] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+        const int64_t p = base + (int64_t)u * blockDim.x;
+        if (p < na) match_a[(uint32_t)key[u]] = j[u];
+    }
+}
+
+// B operators beyond A's occurrence count of their signature: B-only
+__global__ void join_bonly_kernel(const uint64_t *sb, int64_t nb, const int32_t *first_b,
+                                  const int32_t *first_a, const int32_t *end_a, int32_t *b_only,
+                                  unsigned int *n_bonly) {
+    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= nb) return;
+    const uint64_t key = sb[q];
+    const uint32_t d = (uint32_t)(key >> 32);
+    const int32_t t = (int32_t)q - first_b[d];
+    const int32_t ea = end_a[d];
+    const int32_t ca = ea > 0 ? ea - first_a[d] : 0;
+    if (t >= ca) b_only[atomicAdd(n_bonly, 1u)] = (int32_t)(uint32_t)key;
 }
 
 struct JoinSideDev {
@@ -391,52 +453,59 @@ __device__ __forceinline__ double div_or_same(double e, const double *work, int6
     return work ? __ddiv_rn(e, work[i]) : e;
 }
 
-// findings for A ops (matched or A-only), in A order
-__global__ void join_findings_a_kernel(int64_t na, const int64_t *match_a, JoinSideDev A,
-                                       JoinSideDev B, double threshold, FindCols o, int64_t *ia,
-                                       int64_t *ib, double *epw_a, double *epw_b,
-                                       unsigned long long *n_matched) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= na) return;
-    const int64_t j = match_a[i];
-    const double ea = A.joules[i];
-    const int64_t la = A.end[i] - A.start[i];
-    double eb = 0.0;
-    int64_t lb = 0;
-    if (j >= 0) {
-        eb = B.joules[j];
-        lb = B.end[j] - B.start[j];
+// findings of A's operators (matched or A-only), in A order
+__global__ void join_findings_a_kernel(int64_t na, const int32_t *match_a, JoinSideDev A,
+                                       JoinSideDev B, double threshold, FindCols o, double *epw_a,
+                                       double *epw_b, unsigned long long *n_matched) {
+    const int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS + threadIdx.x;
+    int32_t j[ITEMS];
+    double ea[ITEMS], eb[ITEMS];
+    int64_t la[ITEMS], lb[ITEMS], tie[ITEMS];
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+        const int64_t i = base + (int64_t)u * blockDim.x;
+        const bool in = i < na;
+        j[u] = in ? match_a[i] : -1;
+        ea[u] = in ? A.joules[i] : 0.0;
+        la[u] = in ? A.end[i] - A.start[i] : 0;
+        tie[u] = in && A.rank ? A.rank[i] : i;
     }
-    const Verdict v = judge(ea, eb, la, lb, 0.0, threshold);
-    store_finding(o, i, ea, eb, la, lb, v, A.rank ? A.rank[i] : i);
-    if (ia) ia[i] = i;
-    if (ib) ib[i] = j;
-    if (epw_a) epw_a[i] = div_or_same(ea, A.work, i);
-    if (epw_b) epw_b[i] = j >= 0 ? div_or_same(eb, B.work, j) : 0.0;
-    // warp-aggregated matched count
-    const unsigned m = __ballot_sync(__activemask(), j >= 0);
-    if ((threadIdx.x & 31) == __ffs(__activemask()) - 1) atomicAdd(n_matched, (unsigned long long)__popc(m));
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+        eb[u] = 0.0;
+        lb[u] = 0;
+        if (j[u] >= 0) {
+            eb[u] = B.joules[j[u]];
+            lb[u] = B.end[j[u]] - B.start[j[u]];
+        }
+    }
+    unsigned cnt = 0;
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+        const int64_t i = base + (int64_t)u * blockDim.x;
+        if (i >= na) continue;
+        const Verdict v = judge(ea[u], eb[u], la[u], lb[u], 0.0, threshold);
+        store_finding(o, i, ea[u], eb[u], la[u], lb[u], v, tie[u]);
+        if (epw_a) epw_a[i] = div_or_same(ea[u], A.work, i);
+        if (epw_b) epw_b[i] = j[u] >= 0 ? div_or_same(eb[u], B.work, j[u]) : 0.0;
+        cnt += j[u] >= 0;
+    }
+    for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n_matched, (unsigned long long)cnt);
 }
 
-__global__ void unmatched_flags_kernel(const int64_t *match_b, int64_t nb, int32_t *flag) {
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j < nb) flag[j] = match_b[j] < 0 ? 1 : 0;
-}
-
-// B-only findings: numbered na + (exclusive rank among unmatched B ops)
-__global__ void join_findings_b_kernel(int64_t na, int64_t nb, const int64_t *match_b,
-                                       const int32_t *scan_incl, JoinSideDev B, double threshold,
-                                       FindCols o, int64_t *ia, int64_t *ib, double *epw_a,
+// B-only findings: numbered na + position in B order
+__global__ void join_findings_b_kernel(int64_t na, int64_t n_bonly, const int32_t *b_only,
+                                       JoinSideDev B, double threshold, FindCols o, double *epw_a,
                                        double *epw_b) {
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j >= nb || match_b[j] >= 0) return;
-    const int64_t f = na + scan_incl[j] - 1;
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= n_bonly) return;
+    const int32_t j = b_only[r];
+    const int64_t f = na + r;
     const double eb = B.joules[j];
     const int64_t lb = B.end[j] - B.start[j];
     const Verdict v = judge(0.0, eb, 0, lb, 0.0, threshold);
     store_finding(o, f, 0.0, eb, 0, lb, v, -1);  // nodes_a == () sorts first
-    if (ia) ia[f] = -1;
-    if (ib) ib[f] = j;
     if (epw_a) epw_a[f] = 0.0;
     if (epw_b) epw_b[f] = div_or_same(eb, B.work, j);
 }
@@ -504,9 +573,10 @@ static void sort_candidates(char *base, const RankLayout &L, int64_t n, cudaStre
     count_launch(5 + 8);
 }
 
-static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, int64_t k, int64_t *order,
-                     double *summary, void *ws, size_t ws_bytes, cudaStream_t s) {
-    if (P < 0 || k < 0 || k > P || (P && (!khi || !klo)) || (k && !order) || !ws) return DW_E_ARG;
+static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, const int64_t *tie_rank,
+                     int64_t n_a, int64_t k, int64_t *order, double *summary, void *ws,
+                     size_t ws_bytes, cudaStream_t s) {
+    if (P < 0 || k < 0 || k > P || (P && !khi) || (k && !order) || !ws) return DW_E_ARG;
     RankLayout L = rank_layout(P, k);
     if (ws_bytes < L.total) return DW_E_WORKSPACE;
     char *base = (char *)ws;
@@ -528,6 +598,8 @@ static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, int64_
     RankParams r{};
     r.khi = khi;
     r.klo = klo;
+    r.tie_rank = tie_rank;
+    r.n_a = n_a;
     r.P = P;
     r.k = k;
     r.hist = (unsigned int *)(base + L.hist);
@@ -590,9 +662,8 @@ static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, int64_
 }
 
 struct JoinLayout {
-    size_t table, slot_id, scan_tmp, scan_bytes, d_a, d_b, ds_a, ds_b, iota_a, iota_b, is_a, is_b,
-        first_a, count_a, first_b, count_b, match_a, match_b, flag_b, scan_b, cub, cub_bytes,
-        counters, total;
+    size_t table, ids, counters, keys_a, keys_b, sort_a, sort_b, first_a, end_a, first_b, end_b,
+        bonly_tmp, cub, cub_bytes, total;
     int64_t cap, D;
 };
 
@@ -604,43 +675,30 @@ static int64_t pow2_at_least(int64_t x) {
 
 static JoinLayout join_layout(int64_t na, int64_t nb, int64_t max_distinct) {
     JoinLayout L{};
-    if (max_distinct <= 0) max_distinct = na + nb;
-    L.cap = pow2_at_least(std::max<int64_t>(1024, 2 * std::min<int64_t>(max_distinct, na + nb)));
-    L.D = std::min<int64_t>(L.cap, na + nb) + 2;
+    if (max_distinct <= 0 || max_distinct > na + nb) max_distinct = na + nb;
+    L.cap = pow2_at_least(std::max<int64_t>(1024, 2 * max_distinct));
+    L.D = std::min<int64_t>(L.cap, na + nb) + 2;  // ids 1..distinct, 0 reserved
     size_t off = 0;
     L.table = off; off += au(8 * L.cap);
-    L.slot_id = off; off += au(4 * L.cap);
-    size_t sb = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, sb, (int32_t *)nullptr, (int32_t *)nullptr, (int)L.cap);
-    size_t sb2 = 0;
-    cub::DeviceScan::InclusiveSum(nullptr, sb2, (int32_t *)nullptr, (int32_t *)nullptr, (int)std::max<int64_t>(nb, 1));
-    L.scan_tmp = off;
-    L.scan_bytes = std::max(sb, sb2);
-    off += au(L.scan_bytes);
-    L.d_a = off; off += au(4 * na);
-    L.d_b = off; off += au(4 * nb);
-    L.ds_a = off; off += au(4 * na);
-    L.ds_b = off; off += au(4 * nb);
-    L.iota_a = off; off += au(8 * na);
-    L.iota_b = off; off += au(8 * nb);
-    L.is_a = off; off += au(8 * na);
-    L.is_b = off; off += au(8 * nb);
-    L.first_a = off; off += au(8 * L.D);
-    L.count_a = off; off += au(8 * L.D);
-    L.first_b = off; off += au(8 * L.D);
-    L.count_b = off; off += au(8 * L.D);
-    L.match_a = off; off += au(8 * na);
-    L.match_b = off; off += au(8 * nb);
-    L.flag_b = off; off += au(4 * nb);
-    L.scan_b = off; off += au(4 * nb);
-    size_t cs = 0;
-    const int64_t nmax = std::max<int64_t>(std::max(na, nb), 1);
-    cub::DeviceRadixSort::SortPairs(nullptr, cs, (const int32_t *)nullptr, (int32_t *)nullptr,
-                                    (const int64_t *)nullptr, (int64_t *)nullptr, (int)nmax);
-    L.cub = off;
-    L.cub_bytes = cs;
-    off += au(cs);
+    L.ids = off; off += au(4 * L.cap);
     L.counters = off; off += au(64);
+    L.keys_a = off; off += au(8 * na);
+    L.keys_b = off; off += au(8 * nb);
+    L.sort_a = off; off += au(8 * na);
+    L.sort_b = off; off += au(8 * nb);
+    L.first_a = off; off += au(4 * L.D);
+    L.end_a = off; off += au(4 * L.D);
+    L.first_b = off; off += au(4 * L.D);
+    L.end_b = off; off += au(4 * L.D);
+    L.bonly_tmp = off; off += au(4 * std::max<int64_t>(nb, 1));
+    size_t c1 = 0, c2 = 0;
+    const int64_t nmax = std::max<int64_t>(std::max(na, nb), 1);
+    cub::DeviceRadixSort::SortKeys(nullptr, c1, (const uint64_t *)nullptr, (uint64_t *)nullptr, (int)nmax);
+    cub::DeviceRadixSort::SortKeys(nullptr, c2, (const int32_t *)nullptr, (int32_t *)nullptr,
+                                   (int)std::max<int64_t>(nb, 1));
+    L.cub = off;
+    L.cub_bytes = std::max(c1, c2);
+    off += au(L.cub_bytes);
     L.total = off;
     return L;
 }
@@ -679,8 +737,8 @@ size_t dw_rank_workspace_size(int64_t P, int64_t k) { return rank_layout(P, k).t
 int dw_rank(int64_t P, const dw_findings_t *f, int64_t k, int64_t *d_order, double *d_summary,
             void *d_workspace, size_t workspace_bytes, dw_stream_t stream) {
     if (!f) return DW_E_ARG;
-    return rank_impl(P, f->d_key_hi, f->d_key_lo, k, d_order, d_summary, d_workspace, workspace_bytes,
-                     (cudaStream_t)stream);
+    return rank_impl(P, f->d_key_hi, f->d_key_lo, f->d_tie_rank, f->n_a, k, d_order, d_summary,
+                     d_workspace, workspace_bytes, (cudaStream_t)stream);
 }
 
 size_t dw_join_workspace_size(int64_t na, int64_t nb, int64_t max_distinct) {
@@ -688,14 +746,15 @@ size_t dw_join_workspace_size(int64_t na, int64_t nb, int64_t max_distinct) {
 }
 
 int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_distinct, double threshold,
-                 dw_findings_t *out, int64_t *d_ia, int64_t *d_ib, double *d_epw_a, double *d_epw_b,
-                 int64_t *d_count, void *d_workspace, size_t workspace_bytes, dw_stream_t stream) {
+                 dw_findings_t *out, int32_t *d_match_a, int32_t *d_b_only, double *d_epw_a,
+                 double *d_epw_b, int64_t *d_count, void *d_workspace, size_t workspace_bytes,
+                 dw_stream_t stream) {
     if (!(threshold > 0.0 && threshold <= 1.0)) return DW_E_ARG;
-    if (!a || !b || !out || !d_count || !d_workspace) return DW_E_ARG;
+    if (!a || !b || !out || !out->d_key_hi || !d_count || !d_workspace) return DW_E_ARG;
     const int64_t na = a->n, nb = b->n;
     if (na < 0 || nb < 0 || na + nb >= ((int64_t)1 << 31)) return DW_E_ARG;
-    if ((na && (!a->d_sig || !a->d_start || !a->d_end || !a->d_joules)) ||
-        (nb && (!b->d_sig || !b->d_start || !b->d_end || !b->d_joules)))
+    if ((na && (!a->d_sig || !a->d_start || !a->d_end || !a->d_joules || !d_match_a)) ||
+        (nb && (!b->d_sig || !b->d_start || !b->d_end || !b->d_joules || !d_b_only)))
         return DW_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     JoinLayout L = join_layout(na, nb, max_distinct);
@@ -707,78 +766,80 @@ int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_d
     q.na = na;
     q.nb = nb;
     q.table = (uint64_t *)(base + L.table);
-    q.slot_id = (int32_t *)(base + L.slot_id);
+    q.ids = (int32_t *)(base + L.ids);
     q.cap = L.cap;
-    q.d_a = (int32_t *)(base + L.d_a);
-    q.d_b = (int32_t *)(base + L.d_b);
+    q.keys_a = (uint64_t *)(base + L.keys_a);
+    q.keys_b = (uint64_t *)(base + L.keys_b);
     unsigned long long *counters = (unsigned long long *)(base + L.counters);
+    // counters: [0] overflow, [1] matched, [2] next_id (u32), [3] n_bonly (u32)
     q.overflow = counters;
+    q.next_id = (unsigned int *)(counters + 2);
+    unsigned int *n_bonly = (unsigned int *)(counters + 3);
     cudaMemsetAsync(counters, 0, 64, s);
     cudaMemsetAsync(q.table, 0xFF, 8 * L.cap, s);
-    const unsigned grid = (unsigned)(num_sms() * 16);
-    join_insert_kernel<<<grid, 256, 0, s>>>(q);
-    join_flags_kernel<<<grid, 256, 0, s>>>(q);
-    size_t sb = L.scan_bytes;
-    cub::DeviceScan::InclusiveSum(base + L.scan_tmp, sb, q.slot_id, q.slot_id, (int)L.cap, s);
-    join_lookup_kernel<<<grid, 256, 0, s>>>(q);
-    count_launch(5);
+    cudaMemsetAsync(q.ids, 0, 4 * L.cap, s);
+    const int64_t n = na + nb;
+    if (n) {
+        join_hash_kernel<<<(unsigned)std::min<int64_t>(num_sms() * 16, blocks_for(n, 256 * ITEMS)), 256, 0, s>>>(q);
+        count_launch();
+    }
     const int64_t D = L.D;
     const int nbits = bits_for(D);
-    int64_t *first_a = (int64_t *)(base + L.first_a), *count_a = (int64_t *)(base + L.count_a);
-    int64_t *first_b = (int64_t *)(base + L.first_b), *count_b = (int64_t *)(base + L.count_b);
-    cudaMemsetAsync(count_a, 0, 8 * D, s);
-    cudaMemsetAsync(count_b, 0, 8 * D, s);
-    int64_t *is_a = (int64_t *)(base + L.is_a), *is_b = (int64_t *)(base + L.is_b);
-    int32_t *ds_a = (int32_t *)(base + L.ds_a), *ds_b = (int32_t *)(base + L.ds_b);
-    size_t cs = L.cub_bytes;
-    if (na) {
-        iota64_kernel<<<blocks_for(na), 256, 0, s>>>((int64_t *)(base + L.iota_a), na);
-        cub::DeviceRadixSort::SortPairs(base + L.cub, cs, q.d_a, ds_a, (const int64_t *)(base + L.iota_a),
-                                        is_a, (int)na, 0, nbits, s);
-        run_bounds_kernel<<<blocks_for(na), 256, 0, s>>>(ds_a, na, first_a, count_a);
-        count_launch(6);
+    int32_t *first_a = (int32_t *)(base + L.first_a), *end_a = (int32_t *)(base + L.end_a);
+    int32_t *first_b = (int32_t *)(base + L.first_b), *end_b = (int32_t *)(base + L.end_b);
+    uint64_t *sa = (uint64_t *)(base + L.sort_a), *sb = (uint64_t *)(base + L.sort_b);
+    cudaMemsetAsync(end_a, 0, 4 * D, s);
+    cudaMemsetAsync(end_b, 0, 4 * D, s);
+    size_t cb = L.cub_bytes;
+    if (na) {  // stable: equal ids keep op order (the low 32 bits ride along)
+        cub::DeviceRadixSort::SortKeys(base + L.cub, cb, q.keys_a, sa, (int)na, 32, 32 + nbits, s);
+        run_bounds_kernel<<<blocks_for(na), 256, 0, s>>>(sa, na, first_a, end_a);
+        count_launch(4);
     }
     if (nb) {
-        iota64_kernel<<<blocks_for(nb), 256, 0, s>>>((int64_t *)(base + L.iota_b), nb);
-        cub::DeviceRadixSort::SortPairs(base + L.cub, cs, q.d_b, ds_b, (const int64_t *)(base + L.iota_b),
-                                        is_b, (int)nb, 0, nbits, s);
-        run_bounds_kernel<<<blocks_for(nb), 256, 0, s>>>(ds_b, nb, first_b, count_b);
-        count_launch(6);
+        cb = L.cub_bytes;
+        cub::DeviceRadixSort::SortKeys(base + L.cub, cb, q.keys_b, sb, (int)nb, 32, 32 + nbits, s);
+        run_bounds_kernel<<<blocks_for(nb), 256, 0, s>>>(sb, nb, first_b, end_b);
+        count_launch(4);
     }
-    run_counts_kernel<<<blocks_for(D), 256, 0, s>>>(first_a, count_a, D);
-    run_counts_kernel<<<blocks_for(D), 256, 0, s>>>(first_b, count_b, D);
-    int64_t *match_a = (int64_t *)(base + L.match_a), *match_b = (int64_t *)(base + L.match_b);
-    cudaMemsetAsync(match_b, 0xFF, 8 * std::max<int64_t>(nb, 1), s);
-    if (na)
-        join_pair_kernel<<<blocks_for(na), 256, 0, s>>>(ds_a, is_a, na, first_a, first_b, count_b, is_b,
-                                                         match_a, match_b);
-    count_launch(3);
+    if (na) {
+        join_pair_kernel<<<blocks_for(na, 256 * ITEMS), 256, 0, s>>>(sa, na, first_a, sb, first_b, end_b,
+                                                                     d_match_a);
+        count_launch();
+    }
+    int32_t *bonly_tmp = (int32_t *)(base + L.bonly_tmp);
+    if (nb) {
+        join_bonly_kernel<<<blocks_for(nb), 256, 0, s>>>(sb, nb, first_b, first_a, end_a, bonly_tmp, n_bonly);
+        count_launch();
+    }
+    unsigned long long hc[4] = {0, 0, 0, 0};  // overflow, matched, next_id, n_bonly
+    cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return DW_E_CUDA;
+    if (hc[0]) return DW_E_WORKSPACE;  // more distinct signatures than the table holds
+    const int64_t b_only = (int64_t)(unsigned int)hc[3];
+    if (b_only) {  // B-only operators in B order
+        cb = L.cub_bytes;
+        cub::DeviceRadixSort::SortKeys(base + L.cub, cb, bonly_tmp, d_b_only, (int)b_only, 0,
+                                       bits_for(nb), s);
+        count_launch(4);
+    }
     JoinSideDev A{a->d_start, a->d_end, a->d_rank, a->d_joules, a->d_work};
     JoinSideDev B{b->d_start, b->d_end, b->d_rank, b->d_joules, b->d_work};
     FindCols o = cols_of(out);
     if (na) {
-        join_findings_a_kernel<<<blocks_for(na), 256, 0, s>>>(na, match_a, A, B, threshold, o, d_ia, d_ib,
-                                                               d_epw_a, d_epw_b, counters + 1);
+        join_findings_a_kernel<<<blocks_for(na, 256 * ITEMS), 256, 0, s>>>(na, d_match_a, A, B, threshold, o,
+                                                                            d_epw_a, d_epw_b, counters + 1);
         count_launch();
     }
-    int32_t *flag_b = (int32_t *)(base + L.flag_b), *scan_b = (int32_t *)(base + L.scan_b);
-    if (nb) {
-        unmatched_flags_kernel<<<blocks_for(nb), 256, 0, s>>>(match_b, nb, flag_b);
-        sb = L.scan_bytes;
-        cub::DeviceScan::InclusiveSum(base + L.scan_tmp, sb, flag_b, scan_b, (int)nb, s);
-        join_findings_b_kernel<<<blocks_for(nb), 256, 0, s>>>(na, nb, match_b, scan_b, B, threshold, o,
-                                                               d_ia, d_ib, d_epw_a, d_epw_b);
-        count_launch(4);
+    if (b_only) {
+        join_findings_b_kernel<<<blocks_for(b_only), 256, 0, s>>>(na, b_only, d_b_only, B, threshold, o,
+                                                                   d_epw_a, d_epw_b);
+        count_launch();
     }
-    // counts: {P, matched, a_only, b_only} -- assembled on the host side of this call
-    unsigned long long host_c[2] = {0, 0};
-    int32_t b_only = 0;
-    cudaMemcpyAsync(host_c, counters, 16, cudaMemcpyDeviceToHost, s);
-    if (nb) cudaMemcpyAsync(&b_only, scan_b + nb - 1, 4, cudaMemcpyDeviceToHost, s);
+    unsigned long long matched = 0;
+    cudaMemcpyAsync(&matched, counters + 1, 8, cudaMemcpyDeviceToHost, s);
     if (cudaStreamSynchronize(s) != cudaSuccess) return DW_E_CUDA;
-    if (host_c[0]) return DW_E_WORKSPACE;  // hash table overflow
-    const int64_t matched = (int64_t)host_c[1];
-    const int64_t cnt[4] = {na + b_only, matched, na - matched, b_only};
+    const int64_t cnt[4] = {na + b_only, (int64_t)matched, na - (int64_t)matched, b_only};
     cudaMemcpyAsync(d_count, cnt, sizeof(cnt), cudaMemcpyHostToDevice, s);
     cudaStreamSynchronize(s);
     DW_CHECK_LAUNCH();

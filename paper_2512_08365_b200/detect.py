@@ -81,14 +81,16 @@ class FindingColumns:
            "informational")
     LEAN = ("ratio", "wasted", "verdict", "side", "informational")
 
-    def __init__(self, P: int, dev, full: bool = True, columns=None):
+    def __init__(self, P: int, dev, full: bool = True, columns=None, key_lo: bool = True,
+                 tie_rank=None, n_a: int = 0):
         cols = self.ALL if (columns is None and full) else (columns or self.LEAN)
+        self.tie_rank, self.n_a = tie_rank, n_a
         types = {"energy_a": torch.float64, "energy_b": torch.float64, "ratio": torch.float64,
                  "wasted": torch.float64, "latency_a": torch.int64, "latency_b": torch.int64,
                  "verdict": torch.int8, "side": torch.int8, "informational": torch.int8}
         self.P = P
         self.key_hi = torch.empty(P, dtype=torch.int64, device=dev)
-        self.key_lo = torch.empty(P, dtype=torch.int64, device=dev)
+        self.key_lo = torch.empty(P, dtype=torch.int64, device=dev) if key_lo else None
         for name in self.ALL:
             setattr(self, name, torch.empty(P, dtype=types[name], device=dev) if name in cols else None)
 
@@ -97,7 +99,7 @@ class FindingColumns:
         return _native.Findings(p(self.energy_a), p(self.energy_b), p(self.ratio),
                                 p(self.latency_a), p(self.latency_b), p(self.verdict),
                                 p(self.side), p(self.informational), p(self.wasted),
-                                p(self.key_hi), p(self.key_lo))
+                                p(self.key_hi), p(self.key_lo), p(self.tie_rank), int(self.n_a))
 
     def host(self, idx=None) -> dict:
         names = ("energy_a", "energy_b", "ratio", "wasted", "latency_a", "latency_b", "verdict",
@@ -290,9 +292,11 @@ def _host_keys(findings) -> tuple[np.ndarray, np.ndarray]:
     return hi.view(np.int64), lo.view(np.int64)
 
 
-def rank_order(key_hi: torch.Tensor, key_lo: torch.Tensor, k: int):
+def rank_order(key_hi: torch.Tensor, key_lo: Optional[torch.Tensor], k: int, tie_rank=None,
+               n_a: int = 0):
     """Indices of the k best findings (report order) and the device summary
-    {n_waste, wasted_joules (exact sum), P} -- dw_rank."""
+    {n_waste, wasted_joules (exact sum), P} -- dw_rank.  Without key_lo the low
+    key follows the join numbering (tie_rank / n_a)."""
     dev = _native.device()
     P = int(key_hi.numel())
     L = _native.lib()
@@ -301,7 +305,7 @@ def rank_order(key_hi: torch.Tensor, key_lo: torch.Tensor, k: int):
     order = torch.empty(max(k, 1), dtype=torch.int64, device=dev)
     summary = torch.zeros(4, dtype=torch.float64, device=dev)
     fs = _native.Findings(None, None, None, None, None, None, None, None, None,
-                          _native.ptr(key_hi), _native.ptr(key_lo))
+                          _native.ptr(key_hi), _native.ptr(key_lo), _native.ptr(tie_rank), int(n_a))
     rc = L.dw_rank(P, ctypes.byref(fs), int(k), _native.ptr(order), _native.ptr(summary),
                    ws.data_ptr(), ws.numel(), _native.stream_handle())
     _native.check(rc, "dw_rank")

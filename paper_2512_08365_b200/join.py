@@ -87,23 +87,36 @@ def _ranks(cols: TraceColumns, dev) -> Optional[torch.Tensor]:
 
 @dataclass
 class JoinDiff:
-    """Device-resident result of dw_join_diff (+ dw_rank)."""
+    """Device-resident result of dw_join_diff (+ dw_rank).  Finding f < n_a is
+    A op f (paired with match_a[f] or A-only); finding n_a + r is B-only op
+    b_only[r]."""
 
     P: int
+    n_a: int
     n_matched: int
     n_a_only: int
     n_b_only: int
     columns: FindingColumns
-    ia: torch.Tensor
-    ib: torch.Tensor
+    match_a: torch.Tensor        # int32 [n_a]
+    b_only: torch.Tensor         # int32 [n_b_only]
     epw_a: Optional[torch.Tensor]
     epw_b: Optional[torch.Tensor]
     order: torch.Tensor          # top-k finding indices, report order
     n_waste: int
     wasted_joules: float         # exact sum over all waste findings
-
     ja: Optional[torch.Tensor] = None    # operator joules of A / B (for lean columns)
     jb: Optional[torch.Tensor] = None
+
+    def pair_of(self, f: torch.Tensor):
+        """(A op, B op) of findings f (device tensors; -1 on an empty side)."""
+        is_a = f < self.n_a
+        ia = torch.where(is_a, f, torch.full_like(f, -1))
+        fa = f.clamp(max=max(self.n_a - 1, 0))
+        fb = (f - self.n_a).clamp(min=0, max=max(self.n_b_only - 1, 0))
+        ma = self.match_a[fa].to(torch.int64) if self.n_a else torch.full_like(f, -1)
+        bo = self.b_only[fb].to(torch.int64) if self.n_b_only else torch.full_like(f, -1)
+        ib = torch.where(is_a, ma, bo)
+        return ia, ib
 
     def top_findings(self, cols_a: TraceColumns, cols_b: TraceColumns) -> list[WasteFinding]:
         """Materialise the top-k findings (report order) as reference-style
@@ -111,7 +124,7 @@ class JoinDiff:
         the ledgers on the device for these k rows only."""
         idx = self.order
         c = self.columns
-        ia_d, ib_d = self.ia[idx], self.ib[idx]
+        ia_d, ib_d = self.pair_of(idx)
         has_a, has_b = ia_d >= 0, ib_d >= 0
         ia_c, ib_c = ia_d.clamp(min=0), ib_d.clamp(min=0)
 
@@ -180,9 +193,10 @@ def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
         sides.append(_native.JoinSide(p(sig), p(s), p(e), p(j), p(w), p(rank), cols.n_ops))
     na, nb = ca.n_ops, cb.n_ops
     Pmax = na + nb
-    fc = FindingColumns(Pmax, dev, full=full_columns)
-    ia = torch.empty(Pmax, dtype=torch.int64, device=dev)
-    ib = torch.empty(Pmax, dtype=torch.int64, device=dev)
+    rank_a = keep[3]
+    fc = FindingColumns(Pmax, dev, full=full_columns, key_lo=False, tie_rank=rank_a, n_a=na)
+    match_a = torch.empty(max(na, 1), dtype=torch.int32, device=dev)
+    bonly_t = torch.empty(max(nb, 1), dtype=torch.int32, device=dev)
     epw_a = torch.empty(Pmax, dtype=torch.float64, device=dev) if epw else None
     epw_b = torch.empty(Pmax, dtype=torch.float64, device=dev) if epw else None
     count = torch.zeros(4, dtype=torch.int64, device=dev)
@@ -193,7 +207,7 @@ def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
     while True:
         ws = _native.Workspace.get(L.dw_join_workspace_size(na, nb, md), stream)
         rc = L.dw_join_diff(ctypes.byref(sides[0]), ctypes.byref(sides[1]), md, float(threshold),
-                            ctypes.byref(fs), p(ia), p(ib), p(epw_a), p(epw_b), p(count),
+                            ctypes.byref(fs), p(match_a), p(bonly_t), p(epw_a), p(epw_b), p(count),
                             ws.data_ptr(), ws.numel(), _native.stream_handle(stream))
         if rc == _native.DW_E_WORKSPACE and md and md < na + nb:
             md = min(4 * md, na + nb)  # more distinct signatures than the table held
@@ -202,10 +216,11 @@ def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
     _native.check(rc, "dw_join_diff")
     P, matched, a_only, b_only = (int(x) for x in count.cpu().tolist())
     kk = min(k, P)
-    order, summary = rank_order(fc.key_hi[:P], fc.key_lo[:P], kk)
+    order, summary = rank_order(fc.key_hi[:P], None, kk, tie_rank=rank_a, n_a=na)
     sm = summary.cpu().tolist()
-    return JoinDiff(P=P, n_matched=matched, n_a_only=a_only, n_b_only=b_only, columns=fc,
-                    ia=ia, ib=ib, epw_a=epw_a, epw_b=epw_b, order=order, n_waste=int(sm[0]),
+    return JoinDiff(P=P, n_a=na, n_matched=matched, n_a_only=a_only, n_b_only=b_only, columns=fc,
+                    match_a=match_a[:na], b_only=bonly_t[:b_only],
+                    epw_a=epw_a, epw_b=epw_b, order=order, n_waste=int(sm[0]),
                     wasted_joules=float(sm[1]), ja=keep[1], jb=keep[7])
 
 

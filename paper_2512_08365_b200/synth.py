@@ -153,8 +153,10 @@ def _b_side(a: _Ops, cfg: SynthConfig, g: torch.Generator, dev) -> _Ops:
     op_mult = torch.where(hot, mult, torch.ones_like(mult))
     kop = torch.repeat_interleave(torch.arange(n, device=dev), a.kc)
     kw = a.kw * op_mult[kop]
-    # (iii) renamed ops
-    ren = torch.rand(n, generator=g, device=dev) < cfg.rename_frac
+    # (iii) api misuse: 0.1% of the signatures are served by a different
+    # operator on B -- every occurrence renamed (systematic, like a framework
+    # dispatching another kernel for that op everywhere)
+    ren = (((a.sig >> 32) & 0xFFFF).to(torch.float64) / 65536.0) < cfg.rename_frac
     sig = torch.where(ren, _splitmix64(a.sig ^ 0x5DEECE66D), a.sig)
     # (ii) inserted ops: one extra op after each selected position
     ins = torch.rand(n, generator=g, device=dev) < cfg.insert_frac

@@ -123,8 +123,11 @@ def test_join_vs_oracle(cfg, n):
     na = len(ma)
     assert jd.P == na + len(b_only)
     assert jd.n_matched == int((ma >= 0).sum())
-    np.testing.assert_array_equal(jd.ib[:na].cpu().numpy(), ma)
-    np.testing.assert_array_equal(jd.ib[na:jd.P].cpu().numpy(), b_only)
+    np.testing.assert_array_equal(jd.match_a.cpu().numpy(), ma)
+    np.testing.assert_array_equal(jd.b_only.cpu().numpy(), b_only)
+    f = torch.arange(jd.P, device="cuda")
+    ia, ib = jd.pair_of(f)
+    np.testing.assert_array_equal(ib.cpu().numpy(), np.concatenate([ma, b_only]))
     h = jd.columns.host()
     P = jd.P
     np.testing.assert_array_equal(h["energy_a"][:P], d["energy"][:, 0])
