@@ -240,6 +240,7 @@ def run_ours(args, rank: int, world: int, local: int):
 
     from paper_2512_08365_b200 import _native, synth
     from paper_2512_08365_b200.columns import TraceColumns
+    from paper_2512_08365_b200.dist import merge_topk
     from paper_2512_08365_b200.pipeline import analyze
 
     torch.cuda.set_device(local)
@@ -257,10 +258,12 @@ def run_ours(args, rank: int, world: int, local: int):
 
     def step():
         res = analyze(ca, cb, args.method, 0.10, args.k)
-        if world > 1:  # global top-k over every rank's pair: merge the k candidates
-            top = torch.stack([res.join.columns.key_hi[res.join.order], res.join.order], 1)
-            gathered = [torch.empty_like(top) for _ in range(world)]
-            dist.all_gather(gathered, top)
+        if world > 1:  # corpus top-k: merge every rank's k candidates over NCCL
+            jd = res.join
+            f = jd.order
+            tie = jd.pair_of(f)[0].clamp(min=-1)  # A-op index (== id rank here), -1 for B-only
+            lo = ~(((tie + 1) << 32) | f)
+            merge_topk(jd.columns.key_hi[f], lo, args.k)
         return res
 
     for _ in range(args.warmup):

@@ -296,8 +296,73 @@ def cfg1_record(ref):
     return rec
 
 
+def trace_vectors(ref):
+    """JSONL trace files written by the reference, its canonical re-emission,
+    and the reference's exceptions for malformed inputs (trace_model.py:341-586)."""
+    tdir = OUT / "traces"
+    tdir.mkdir(exist_ok=True)
+    sim, tm = ref.simulate, ref.tm
+    for name in ("tf32_misconfig", "join_redundant"):
+        pa, pb = sim.write_scenario(sim.preset(name), str(tdir / name))
+        for path in (pa, pb):
+            tr = tm.load_trace(path)
+            with open(path + ".canonical", "w") as fh:
+                fh.write("\n".join(tm.trace_to_lines(tr)) + "\n")
+    good = open(tdir / "tf32_misconfig" / "trace_a.jsonl").read().splitlines()
+    header = good[0]
+    op = next(l for l in good if '"type":"op"' in l)
+    cases = {
+        "empty": [],
+        "no_header": [op],
+        "bad_json": [header, "{not json"],
+        "bad_version": ['{"type":"header","schema_version":2,"system":"x","workload":"w","seed":0}'],
+        "dup_header": [header, header],
+        "unknown_type": [header, '{"type":"bogus"}'],
+        "missing_field": [header, '{"type":"power","timestamp":5}'],
+        "non_int": [header, '{"type":"power","timestamp":5.5,"watts":1.0}'],
+        "neg_watts": [header, '{"type":"power","timestamp":5,"watts":-1.0}'],
+        "power_order": [header, '{"type":"power","timestamp":5,"watts":1.0}',
+                        '{"type":"power","timestamp":5,"watts":2.0}'],
+        "op_end_lt_start": [header, '{"type":"op","op_id":"o","op_name":"n","input_tensor_ids":[],'
+                            '"output_tensor_ids":[],"kernel_ids":[],"start":10,"end":5}'],
+        "dup_op": [header] + ['{"type":"op","op_id":"o","op_name":"n","input_tensor_ids":[],'
+                              '"output_tensor_ids":[],"kernel_ids":[],"start":1,"end":5}'] * 2,
+        "missing_kernel": [header, '{"type":"op","op_id":"o","op_name":"n","input_tensor_ids":[],'
+                           '"output_tensor_ids":[],"kernel_ids":["k"],"start":1,"end":5}'],
+        "kernel_outside": [header, '{"type":"op","op_id":"o","op_name":"n","input_tensor_ids":[],'
+                           '"output_tensor_ids":[],"kernel_ids":["k"],"start":1,"end":5}',
+                           '{"type":"kernel","kernel_id":"k","kernel_name":"kn","correlation_id":1,'
+                           '"start":2,"end":9,"backtrace":["a"]}'],
+        "orphan_kernel": [header, '{"type":"kernel","kernel_id":"k","kernel_name":"kn","correlation_id":1,'
+                          '"start":2,"end":9,"backtrace":["a"]}'],
+        "kernel_zero_len": [header, '{"type":"kernel","kernel_id":"k","kernel_name":"kn","correlation_id":1,'
+                            '"start":2,"end":2,"backtrace":["a"]}'],
+        "missing_tensor": [header, '{"type":"op","op_id":"o","op_name":"n","input_tensor_ids":["t"],'
+                           '"output_tensor_ids":[],"kernel_ids":[],"start":1,"end":5}'],
+        "cycle": [header,
+                  '{"type":"tensor","tensor_id":"t1","run":0,"shape":[1],"values":[1.0]}',
+                  '{"type":"tensor","tensor_id":"t2","run":0,"shape":[1],"values":[1.0]}',
+                  '{"type":"op","op_id":"a","op_name":"n","input_tensor_ids":["t2"],'
+                  '"output_tensor_ids":["t1"],"kernel_ids":[],"start":1,"end":5}',
+                  '{"type":"op","op_id":"b","op_name":"n","input_tensor_ids":["t1"],'
+                  '"output_tensor_ids":["t2"],"kernel_ids":[],"start":1,"end":5}'],
+    }
+    out = {}
+    for name, lines in cases.items():
+        try:
+            tm.parse_trace_lines(lines)
+            out[name] = {"lines": lines, "exc": None, "msg": None}
+        except Exception as exc:  # noqa: BLE001 - record what the reference raises
+            out[name] = {"lines": lines, "exc": type(exc).__name__, "msg": str(exc)}
+    with open(tdir / "errors.json", "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+
+
 def main():
     ref = _import_reference()
+    if "--traces" in sys.argv:
+        trace_vectors(ref)
+        return
     if "--cfg1" in sys.argv:
         t0 = time.time()
         (OUT / "scenarios").mkdir(parents=True, exist_ok=True)

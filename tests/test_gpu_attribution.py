@@ -195,3 +195,32 @@ def test_ledger_total_long_and_idle():
     assert led.total_joules == pytest.approx(ref_total, rel=1e-12)
     assert led.operator_total() == oracle.fx_sum(led.per_operator.array())
     assert led.idle_joules == max(led.total_joules - led.operator_total(), 0.0)
+
+
+def test_ledger_of_loaded_trace_file_matches_golden():
+    from paper_2512_08365_b200 import load_trace
+    tr = load_trace(str(GOLDEN / "traces" / "tf32_misconfig" / "trace_a.jsonl"))
+    led = build_ledger(tr)
+    sc = load_scenario("preset_tf32_misconfig")
+    want = dict(zip((str(x) for x in sc["a_op_ids"]), sc["gt_a_per_op"]))
+    assert {k: led.per_operator[k] for k in want} == want
+
+
+def test_config1_golden():
+    """BASELINE config 1 (10,142 ops per side): ground truth ledgers bit-exact,
+    the 1 kHz sampled view and its first 500 op / kernel integrals bit-exact."""
+    sc = load_scenario("cfg1")
+    for side in ("a", "b"):
+        cols = _cols(sc, side)
+        led = build_ledger(cols)
+        np.testing.assert_array_equal(led.per_operator.array(), sc[f"gt_{side}_per_op"])
+        np.testing.assert_array_equal(led.per_kernel.array(), sc[f"gt_{side}_per_k"])
+        total, idle = sc[f"gt_{side}_total_idle"]
+        assert led.total_joules == pytest.approx(total, rel=1e-12)
+        assert abs(led.idle_joules - idle) <= 1e-12 * total
+        view = E.sampled_view(cols, 1_000, 0, 0)
+        np.testing.assert_array_equal(E._host(view._ts), sc[f"s1_{side}_view_ts"])
+        np.testing.assert_array_equal(E._host(view._w), sc[f"s1_{side}_view_watts"])
+        lin = build_ledger(cols, method="sampled", period_us=1_000, delay_us=0)
+        np.testing.assert_array_equal(lin.per_operator.array()[:500], sc[f"s1_{side}_per_op500"])
+        np.testing.assert_array_equal(lin.per_kernel.array()[:500], sc[f"s1_{side}_per_k500"])

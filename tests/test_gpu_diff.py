@@ -141,3 +141,18 @@ def test_join_vs_oracle(cfg, n):
     assert jd.n_waste == waste.sum()
     assert jd.wasted_joules == oracle.fx_sum(d["wasted"][waste])
     assert jd.n_waste > 0  # the injected misconfiguration / redundancy is found
+
+
+def test_config1_detect_and_report_golden():
+    sc = load_scenario("cfg1")
+    ca, cb = _cols(sc, "a"), _cols(sc, "b")
+    la, lb = build_ledger(ca), build_ledger(cb)
+    pairs = [SubgraphPair(nodes_a=na, nodes_b=nb) for na, nb in
+             zip(pair_tuples(sc, "a"), pair_tuples(sc, "b"))]
+    fs = detect_waste(pairs, la, lb, 0.10, trace_a=ca, trace_b=cb, output_diff=sc["pair_out_diff"])
+    np.testing.assert_array_equal([f.wasted_joules for f in fs], sc["det10_wasted"])
+    np.testing.assert_array_equal([VCODE[f.verdict] for f in fs], sc["det10_verdict"])
+    doc = report(fs, la, lb, 0.10)
+    pos = {id(f): i for i, f in enumerate(fs)}
+    np.testing.assert_array_equal([pos[id(f)] for f in doc.findings], sc["det10_rank"])
+    assert doc.wasted_joules == sc["det10_report"][2]
