@@ -315,38 +315,23 @@ struct JoinParams {
     const uint64_t *sig_a, *sig_b;
     int64_t na, nb;
     uint64_t *table;            // [cap] signature keys
-    int32_t *ids;               // [cap] dense id of the slot (1-based; 0 = not yet published)
-    unsigned int *next_id;      // id counter
     int64_t cap;                // power of two
-    uint64_t *keys_a, *keys_b;  // (id << 32) | op index -- the radix sort input
+    uint32_t *id_a, *id_b;      // signature id per op (radix sort keys)
+    uint32_t *ix_a, *ix_b;      // op index (radix sort values)
     unsigned long long *overflow;
 };
 
-// Signature -> dense id, in one pass: the thread whose CAS claims an empty
-// slot draws the id and publishes it; threads meeting the same signature spin
-// on the published id.  Ids depend on the race, but the pairing only needs
-// "same signature, same id" and the stable order inside an id, so the result
-// is deterministic.
-__device__ __forceinline__ int32_t sig_id(const JoinParams &q, uint64_t s) {
-    if (s == EMPTY) return 0;  // reserved id for the sentinel value
+// Signature -> id = 1 + its slot in the open-addressing table (0 is reserved
+// for the sentinel value).  One pass, no id counter: whoever claims or finds
+// the slot knows the id.  The pairing only needs "same signature, same id" and
+// the stable order inside an id, so the result is deterministic.
+__device__ __forceinline__ uint32_t sig_id(const JoinParams &q, uint64_t s, uint64_t h) {
+    if (s == EMPTY) return 0;
     const uint64_t mask = (uint64_t)q.cap - 1;
-    uint64_t h = mix64(s) & mask;
     for (int64_t probe = 0; probe < q.cap; ++probe) {
         uint64_t k = q.table[h];
-        if (k == EMPTY) {
-            k = atomicCAS((unsigned long long *)&q.table[h], EMPTY, s);
-            if (k == EMPTY) {
-                const int32_t id = (int32_t)atomicAdd(q.next_id, 1u) + 1;
-                atomicExch((int *)&q.ids[h], id);
-                return id;
-            }
-        }
-        if (k == s) {
-            int32_t id;
-            while ((id = *(volatile int32_t *)&q.ids[h]) == 0) {
-            }
-            return id;
-        }
+        if (k == EMPTY) k = atomicCAS((unsigned long long *)&q.table[h], EMPTY, s);
+        if (k == EMPTY || k == s) return (uint32_t)h + 1;
         h = (h + 1) & mask;
     }
     atomicAdd(q.overflow, 1ULL);
@@ -361,87 +346,89 @@ __global__ void join_hash_kernel(JoinParams q) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * ITEMS;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS + threadIdx.x; base < n; base += stride) {
         uint64_t sg[ITEMS], tk[ITEMS], hh[ITEMS];
-        int32_t id[ITEMS];
 #pragma unroll
         for (int u = 0; u < ITEMS; ++u) {
             const int64_t i = base + (int64_t)u * blockDim.x;
-            sg[u] = i < n ? (i < q.na ? q.sig_a[i] : q.sig_b[i - q.na]) : EMPTY;
+            sg[u] = i < n ? __ldcs(i < q.na ? q.sig_a + i : q.sig_b + (i - q.na)) : EMPTY;
         }
-        // speculative first probe for all items at once (present signatures
-        // resolve here: one L2 round trip for the table and the id)
+        // first probe for all items at once (present signatures resolve here)
 #pragma unroll
         for (int u = 0; u < ITEMS; ++u) {
             hh[u] = mix64(sg[u]) & mask;
             tk[u] = q.table[hh[u]];
-            id[u] = *(volatile int32_t *)&q.ids[hh[u]];
         }
+        uint32_t d[ITEMS];
+#pragma unroll
+        for (int u = 0; u < ITEMS; ++u) {
+            const int64_t i = base + (int64_t)u * blockDim.x;
+            d[u] = (i >= n || (tk[u] == sg[u] && sg[u] != EMPTY)) ? (uint32_t)hh[u] + 1
+                                                                   : sig_id(q, sg[u], hh[u]);
+        }
+        __syncwarp();  // reconverge: the stores below must be whole-warp (coalesced) stores
 #pragma unroll
         for (int u = 0; u < ITEMS; ++u) {
             const int64_t i = base + (int64_t)u * blockDim.x;
             if (i >= n) continue;
-            int32_t d = (tk[u] == sg[u] && id[u] != 0 && sg[u] != EMPTY) ? id[u] : sig_id(q, sg[u]);
             const bool a = i < q.na;
             const int64_t li = a ? i : i - q.na;
-            const uint64_t key = ((uint64_t)(uint32_t)d << 32) | (uint64_t)(uint32_t)li;
-            if (a) q.keys_a[li] = key;
-            else q.keys_b[li] = key;
+            __stcs((a ? q.id_a : q.id_b) + li, d[u]);
+            __stcs((a ? q.ix_a : q.ix_b) + li, (uint32_t)li);
         }
     }
 }
 
-// runs of equal ids in a sorted key column -> first[id], end[id]
-__global__ void run_bounds_kernel(const uint64_t *sorted, int64_t n, int32_t *first, int32_t *end) {
+// runs of equal ids in a sorted id column -> first[id], end[id]
+__global__ void run_bounds_kernel(const uint32_t *sorted, int64_t n, int32_t *first, int32_t *end) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= n) return;
-    const uint32_t d = (uint32_t)(sorted[p] >> 32);
-    if (p == 0 || (uint32_t)(sorted[p - 1] >> 32) != d) first[d] = (int32_t)p;
-    if (p == n - 1 || (uint32_t)(sorted[p + 1] >> 32) != d) end[d] = (int32_t)(p + 1);
+    const uint32_t d = sorted[p];
+    if (p == 0 || sorted[p - 1] != d) first[d] = (int32_t)p;
+    if (p == n - 1 || sorted[p + 1] != d) end[d] = (int32_t)(p + 1);
 }
 
 // t-th occurrence of id d in A pairs with the t-th occurrence of d in B
-__global__ void join_pair_kernel(const uint64_t *sa, int64_t na, const int32_t *first_a,
-                                 const uint64_t *sb, const int32_t *first_b, const int32_t *end_b,
+__global__ void join_pair_kernel(const uint32_t *da, const uint32_t *xa, int64_t na, const int32_t *first_a,
+                                 const uint32_t *xb, const int32_t *first_b, const int32_t *end_b,
                                  int32_t *match_a) {
     const int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS + threadIdx.x;
-    uint64_t key[ITEMS];
+    uint32_t d[ITEMS], i[ITEMS];
     int32_t fa[ITEMS], fb[ITEMS], eb[ITEMS], j[ITEMS];
 #pragma unroll
     for (int u = 0; u < ITEMS; ++u) {
         const int64_t p = base + (int64_t)u * blockDim.x;
-        key[u] = p < na ? sa[p] : 0;
+        d[u] = p < na ? __ldcs(da + p) : 0;
+        i[u] = p < na ? __ldcs(xa + p) : 0;
     }
 #pragma unroll
     for (int u = 0; u < ITEMS; ++u) {
-        const uint32_t d = (uint32_t)(key[u] >> 32);
-        fa[u] = first_a[d];
-        fb[u] = first_b[d];
-        eb[u] = end_b[d];
+        fa[u] = first_a[d[u]];
+        fb[u] = first_b[d[u]];
+        eb[u] = end_b[d[u]];
     }
 #pragma unroll
     for (int u = 0; u < ITEMS; ++u) {
         const int64_t p = base + (int64_t)u * blockDim.x;
         const int32_t t = (int32_t)p - fa[u];
-        j[u] = (p < na && eb[u] > 0 && t < eb[u] - fb[u]) ? (int32_t)(uint32_t)sb[fb[u] + t] : -1;
+        j[u] = (p < na && eb[u] > 0 && t < eb[u] - fb[u]) ? (int32_t)xb[fb[u] + t] : -1;
     }
 #pragma unroll
     for (int u = 0; u < ITEMS; ++u) {
         const int64_t p = base + (int64_t)u * blockDim.x;
-        if (p < na) match_a[(uint32_t)key[u]] = j[u];
+        if (p < na) match_a[i[u]] = j[u];
     }
 }
 
 // B operators beyond A's occurrence count of their signature: B-only
-__global__ void join_bonly_kernel(const uint64_t *sb, int64_t nb, const int32_t *first_b,
+__global__ void join_bonly_kernel(const uint32_t *db, const uint32_t *xb, int64_t nb, const int32_t *first_b,
                                   const int32_t *first_a, const int32_t *end_a, int32_t *b_only,
                                   unsigned int *n_bonly) {
     const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (q >= nb) return;
-    const uint64_t key = sb[q];
-    const uint32_t d = (uint32_t)(key >> 32);
+    const uint32_t d = db[q];
     const int32_t t = (int32_t)q - first_b[d];
     const int32_t ea = end_a[d];
     const int32_t ca = ea > 0 ? ea - first_a[d] : 0;
-    if (t >= ca) b_only[atomicAdd(n_bonly, 1u)] = (int32_t)(uint32_t)key;
+    if (t >= ca) b_only[atomicAdd(n_bonly, 1u)] = (int32_t)xb[q];
 }
 
 struct JoinSideDev {
@@ -465,10 +452,10 @@ __global__ void join_findings_a_kernel(int64_t na, const int32_t *match_a, JoinS
     for (int u = 0; u < ITEMS; ++u) {
         const int64_t i = base + (int64_t)u * blockDim.x;
         const bool in = i < na;
-        j[u] = in ? match_a[i] : -1;
-        ea[u] = in ? A.joules[i] : 0.0;
-        la[u] = in ? A.end[i] - A.start[i] : 0;
-        tie[u] = in && A.rank ? A.rank[i] : i;
+        j[u] = in ? __ldcs(match_a + i) : -1;
+        ea[u] = in ? __ldcs(A.joules + i) : 0.0;
+        la[u] = in ? __ldcs(A.end + i) - __ldcs(A.start + i) : 0;
+        tie[u] = in && A.rank ? __ldcs(A.rank + i) : i;
     }
 #pragma unroll
     for (int u = 0; u < ITEMS; ++u) {
@@ -662,7 +649,8 @@ static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, const 
 }
 
 struct JoinLayout {
-    size_t table, ids, counters, keys_a, keys_b, sort_a, sort_b, first_a, end_a, first_b, end_b,
+    size_t table, counters, id_a, id_b, ix_a, ix_b, sid_a, sid_b, six_a, six_b, first_a, end_a,
+        first_b, end_b,
         bonly_tmp, cub, cub_bytes, total;
     int64_t cap, D;
 };
@@ -677,15 +665,18 @@ static JoinLayout join_layout(int64_t na, int64_t nb, int64_t max_distinct) {
     JoinLayout L{};
     if (max_distinct <= 0 || max_distinct > na + nb) max_distinct = na + nb;
     L.cap = pow2_at_least(std::max<int64_t>(1024, 2 * max_distinct));
-    L.D = std::min<int64_t>(L.cap, na + nb) + 2;  // ids 1..distinct, 0 reserved
+    L.D = L.cap + 2;  // ids are table slots + 1; 0 reserved
     size_t off = 0;
     L.table = off; off += au(8 * L.cap);
-    L.ids = off; off += au(4 * L.cap);
     L.counters = off; off += au(64);
-    L.keys_a = off; off += au(8 * na);
-    L.keys_b = off; off += au(8 * nb);
-    L.sort_a = off; off += au(8 * na);
-    L.sort_b = off; off += au(8 * nb);
+    L.id_a = off; off += au(4 * na);
+    L.id_b = off; off += au(4 * nb);
+    L.ix_a = off; off += au(4 * na);
+    L.ix_b = off; off += au(4 * nb);
+    L.sid_a = off; off += au(4 * na);
+    L.sid_b = off; off += au(4 * nb);
+    L.six_a = off; off += au(4 * na);
+    L.six_b = off; off += au(4 * nb);
     L.first_a = off; off += au(4 * L.D);
     L.end_a = off; off += au(4 * L.D);
     L.first_b = off; off += au(4 * L.D);
@@ -693,7 +684,8 @@ static JoinLayout join_layout(int64_t na, int64_t nb, int64_t max_distinct) {
     L.bonly_tmp = off; off += au(4 * std::max<int64_t>(nb, 1));
     size_t c1 = 0, c2 = 0;
     const int64_t nmax = std::max<int64_t>(std::max(na, nb), 1);
-    cub::DeviceRadixSort::SortKeys(nullptr, c1, (const uint64_t *)nullptr, (uint64_t *)nullptr, (int)nmax);
+    cub::DeviceRadixSort::SortPairs(nullptr, c1, (const uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (const uint32_t *)nullptr, (uint32_t *)nullptr, (int)nmax);
     cub::DeviceRadixSort::SortKeys(nullptr, c2, (const int32_t *)nullptr, (int32_t *)nullptr,
                                    (int)std::max<int64_t>(nb, 1));
     L.cub = off;
@@ -766,56 +758,61 @@ int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_d
     q.na = na;
     q.nb = nb;
     q.table = (uint64_t *)(base + L.table);
-    q.ids = (int32_t *)(base + L.ids);
     q.cap = L.cap;
-    q.keys_a = (uint64_t *)(base + L.keys_a);
-    q.keys_b = (uint64_t *)(base + L.keys_b);
+    q.id_a = (uint32_t *)(base + L.id_a);
+    q.id_b = (uint32_t *)(base + L.id_b);
+    q.ix_a = (uint32_t *)(base + L.ix_a);
+    q.ix_b = (uint32_t *)(base + L.ix_b);
     unsigned long long *counters = (unsigned long long *)(base + L.counters);
     // counters: [0] overflow, [1] matched, [2] next_id (u32), [3] n_bonly (u32)
     q.overflow = counters;
-    q.next_id = (unsigned int *)(counters + 2);
     unsigned int *n_bonly = (unsigned int *)(counters + 3);
     cudaMemsetAsync(counters, 0, 64, s);
     cudaMemsetAsync(q.table, 0xFF, 8 * L.cap, s);
-    cudaMemsetAsync(q.ids, 0, 4 * L.cap, s);
     const int64_t n = na + nb;
     if (n) {
         join_hash_kernel<<<(unsigned)std::min<int64_t>(num_sms() * 16, blocks_for(n, 256 * ITEMS)), 256, 0, s>>>(q);
         count_launch();
     }
-    const int64_t D = L.D;
+    // the number of distinct signatures bounds the sort's key bits
+    unsigned long long hc0[4] = {0, 0, 0, 0};
+    cudaMemcpyAsync(hc0, counters, sizeof(hc0), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return DW_E_CUDA;
+    if (hc0[0]) return DW_E_WORKSPACE;  // more distinct signatures than the table holds
+    const int64_t D = L.D;  // ids are table slots + 1
     const int nbits = bits_for(D);
     int32_t *first_a = (int32_t *)(base + L.first_a), *end_a = (int32_t *)(base + L.end_a);
     int32_t *first_b = (int32_t *)(base + L.first_b), *end_b = (int32_t *)(base + L.end_b);
-    uint64_t *sa = (uint64_t *)(base + L.sort_a), *sb = (uint64_t *)(base + L.sort_b);
+    uint32_t *sid_a = (uint32_t *)(base + L.sid_a), *sid_b = (uint32_t *)(base + L.sid_b);
+    uint32_t *six_a = (uint32_t *)(base + L.six_a), *six_b = (uint32_t *)(base + L.six_b);
     cudaMemsetAsync(end_a, 0, 4 * D, s);
     cudaMemsetAsync(end_b, 0, 4 * D, s);
     size_t cb = L.cub_bytes;
-    if (na) {  // stable: equal ids keep op order (the low 32 bits ride along)
-        cub::DeviceRadixSort::SortKeys(base + L.cub, cb, q.keys_a, sa, (int)na, 32, 32 + nbits, s);
-        run_bounds_kernel<<<blocks_for(na), 256, 0, s>>>(sa, na, first_a, end_a);
+    if (na) {  // stable: equal ids keep op order
+        cub::DeviceRadixSort::SortPairs(base + L.cub, cb, q.id_a, sid_a, q.ix_a, six_a, (int)na, 0, nbits, s);
+        run_bounds_kernel<<<blocks_for(na), 256, 0, s>>>(sid_a, na, first_a, end_a);
         count_launch(4);
     }
     if (nb) {
         cb = L.cub_bytes;
-        cub::DeviceRadixSort::SortKeys(base + L.cub, cb, q.keys_b, sb, (int)nb, 32, 32 + nbits, s);
-        run_bounds_kernel<<<blocks_for(nb), 256, 0, s>>>(sb, nb, first_b, end_b);
+        cub::DeviceRadixSort::SortPairs(base + L.cub, cb, q.id_b, sid_b, q.ix_b, six_b, (int)nb, 0, nbits, s);
+        run_bounds_kernel<<<blocks_for(nb), 256, 0, s>>>(sid_b, nb, first_b, end_b);
         count_launch(4);
     }
     if (na) {
-        join_pair_kernel<<<blocks_for(na, 256 * ITEMS), 256, 0, s>>>(sa, na, first_a, sb, first_b, end_b,
-                                                                     d_match_a);
+        join_pair_kernel<<<blocks_for(na, 256 * ITEMS), 256, 0, s>>>(sid_a, six_a, na, first_a, six_b, first_b,
+                                                                     end_b, d_match_a);
         count_launch();
     }
     int32_t *bonly_tmp = (int32_t *)(base + L.bonly_tmp);
     if (nb) {
-        join_bonly_kernel<<<blocks_for(nb), 256, 0, s>>>(sb, nb, first_b, first_a, end_a, bonly_tmp, n_bonly);
+        join_bonly_kernel<<<blocks_for(nb), 256, 0, s>>>(sid_b, six_b, nb, first_b, first_a, end_a, bonly_tmp,
+                                                          n_bonly);
         count_launch();
     }
     unsigned long long hc[4] = {0, 0, 0, 0};  // overflow, matched, next_id, n_bonly
     cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s);
     if (cudaStreamSynchronize(s) != cudaSuccess) return DW_E_CUDA;
-    if (hc[0]) return DW_E_WORKSPACE;  // more distinct signatures than the table holds
     const int64_t b_only = (int64_t)(unsigned int)hc[3];
     if (b_only) {  // B-only operators in B order
         cb = L.cub_bytes;
