@@ -61,8 +61,8 @@ typedef struct CUstream_st *dw_stream_t; /* == cudaStream_t */
  * exactly in 2^-40 W*us fixed point and rounded once. */
 #define DW_DIRECT_MAX 256
 /* Tiling of the attribution kernel.  Whole tiles enter long-interval sums as
- * fp64 tile sums reduced in a fixed order (per-thread strided sum over
- * DW_TILE_THREADS threads, warp xor-butterfly, warps in order), converted to
+ * fp64 tile sums reduced in a fixed order (per-thread sums of term pairs
+ * strided over DW_TILE_THREADS threads, warp xor-butterfly, warps in order), converted to
  * fixed point; the CPU oracle mirrors that order (oracle/dw_oracle.c). */
 #define DW_TILE 1024
 #define DW_TILE_THREADS 128

@@ -227,9 +227,10 @@ static double step_direct(const int64_t *ts, const double *w, int64_t n, int64_t
 
 /* ---- the device's long-interval definition (MODE_DEVICE) ----
  * Whole tiles of DW_TILE terms enter as fp64 tile sums reduced in the GPU's
- * fixed order: thread t of DW_TILE_THREADS sums terms t, t+THREADS, ...
- * sequentially; each warp combines its 32 lanes by an xor butterfly (lane 0's
- * value); the warp results are added in warp order.  Partial tiles and edge
+ * fixed order: thread t of DW_TILE_THREADS sums the term pairs (2t, 2t+1),
+ * (2t + 2*THREADS, 2t + 2*THREADS + 1), ... sequentially; each warp
+ * combines its 32 lanes by an xor butterfly (lane 0's value); the warp
+ * results are added in warp order.  Partial tiles and edge
  * terms enter term by term.  Everything meets in exact fixed point. */
 typedef double (*term_fn)(const void *ctx, int64_t i);
 
@@ -239,7 +240,10 @@ static double tile_sum(term_fn term, const void *ctx, int64_t t0, int64_t t1) {
         double v[32];
         for (int l = 0; l < 32; l++) {
             double acc = 0.0;
-            for (int64_t r = t0 + w * 32 + l; r < t1; r += DW_TILE_THREADS) acc += term(ctx, r);
+            for (int64_t r = t0 + 2 * (w * 32 + l); r < t1; r += 2 * DW_TILE_THREADS) {
+                acc += term(ctx, r);
+                if (r + 1 < t1) acc += term(ctx, r + 1);
+            }
             v[l] = acc;
         }
         for (int off = 16; off > 0; off >>= 1) {

@@ -14,7 +14,11 @@ from pathlib import Path
 import torch
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "_lib" / "libdwb200.so"
+import os as _os
+
+# DWB200_LIB selects a diagnostic build (e.g. _lib/libdwb200_prof.so); the
+# default is the product library
+LIB_PATH = Path(_os.environ.get("DWB200_LIB") or (_PKG / "_lib" / "libdwb200.so"))
 
 DW_OK = 0
 DW_E_REVERSED = -1

@@ -46,8 +46,16 @@ def _stale() -> bool:
     return any(d.exists() and d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, variant: str = "") -> Path:
+    """Diagnostic variants, never the product library (scripts/probe_attr.py):
+    "prof" -- per-phase clock64 counters in the tile kernel (-DDW_PHASE_PROF,
+    dw_phase_prof()); "skip" -- consumers release every stage unprocessed
+    (-DDW_SKIP_CONSUMERS), the staging pipeline's own speed."""
+    lib = LIB if not variant else OUT_DIR / f"libdwb200_{variant}.so"
+    extra = {"prof": ["-DDW_PHASE_PROF"], "skip": ["-DDW_SKIP_CONSUMERS"]}.get(variant.split("_")[0], [])
+    if variant:  # experiment knobs for diagnostic builds only (e.g. -DDW_PREFETCH=0)
+        extra += os.environ.get("DWB200_NVCC_EXTRA", "").split()
+    if not variant and not force and not _stale():
         return LIB
     OUT_DIR.mkdir(exist_ok=True)
     objs = []
@@ -55,28 +63,30 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     for src in SOURCES:
         if not (CSRC / src).exists():
             continue
-        obj = OUT_DIR / (Path(src).stem + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", str(PKG.parent / "include"), "-c", str(CSRC / src),
+        obj = OUT_DIR / (Path(src).stem + variant + ".o")
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", str(PKG.parent / "include"), "-c", str(CSRC / src),
                "-o", str(obj)]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
         objs.append(str(obj))
-    tmp = OUT_DIR / "libdwb200.so.tmp"
+    tmp = OUT_DIR / (lib.name + ".tmp")
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
            *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         os.remove(o)
-    (OUT_DIR / "ptxas.log").write_text("\n".join(log))
+    if not variant:
+        (OUT_DIR / "ptxas.log").write_text("\n".join(log))
     if verbose:
         print("\n".join(log))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
+    print(build(force="--force" in sys.argv, verbose=True, variant=var))

@@ -45,6 +45,22 @@ constexpr int GROUPS = 4;                    // consumer groups per CTA (tiles p
 constexpr int STAGES = 5;                    // TMA ring depth (tiles staged per CTA)
 constexpr int CTAS_PER_SM = 1;
 
+#ifdef DW_PHASE_PROF
+// diagnostic build only: cycles per tile phase, summed over consumer groups
+// (thread 0 of each group) and the producer; read with dw_phase_prof()
+__device__ unsigned long long g_phase[16];
+#define PROF(i)                                                                 \
+    do {                                                                        \
+        if (ctid == 0) {                                                        \
+            long long t_ = clock64();                                           \
+            atomicAdd(&g_phase[i], (unsigned long long)(t_ - prof_t));          \
+            prof_t = t_;                                                        \
+        }                                                                       \
+    } while (0)
+#else
+#define PROF(i) do { (void)prof_t; } while (0)
+#endif
+
 struct AttrParams {
     const int64_t *ts;
     const double *w;
@@ -152,7 +168,8 @@ __global__ void partition_kernel(AttrParams p) {
 // NCW consumer warps wait on `full`, integrate, and release the stage through
 // `empty`.  No consumer ever waits on a global load in the common case.
 constexpr int NCW = ATTR_WARPS;              // warps per consumer group
-constexpr int KTHREADS = GROUPS * ATTR_THREADS + 32;  // + one producer warp
+constexpr int NPROD = 1;                     // producer warps
+constexpr int KTHREADS = GROUPS * ATTR_THREADS + 32 * NPROD;
 constexpr int IV_POOL = 512;                 // staged intervals per stage (all sets)
 
 struct StageMeta {
@@ -173,6 +190,7 @@ struct __align__(16) TileSmem {  // the stage ring, shared by the producer and e
     StageMeta meta[STAGES];
     uint64_t full[STAGES];
     uint64_t empty[STAGES];
+    int claim;                  // next position of this CTA's tile sequence to hand to a group
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -410,44 +428,82 @@ __device__ __forceinline__ void tile_intervals(const AttrParams &p, const TileSm
     }
 }
 
-// ---- narrow tiles: two-phase processing with a counting sort by length ----
-// Phase 1 finds, per interval, its first segment a and its segment count n
-// (both by guessed + galloping searches in shared memory) and buckets the
-// intervals by n.  Phase 2 hands the bucketed order to the lanes, so the 32
-// intervals of a warp have (nearly) equal trip counts, and runs each
-// reference-order sum as a fixed-trip loop whose loads do not depend on the
-// running sum.
+// ---- narrow tiles: precomputed terms, two phases, counting sort by length ----
+// Pass A writes the window's 32-bit relative timestamps (group smem) and then
+// every interior integrand term of the tile's pieces into the stage's int64
+// timestamp slots (no longer needed once ts32 exists); the tile sum is folded
+// from those same terms.  Phase 1 finds, per interval, its first piece a and
+// its interior-term count, and evaluates the two edge pieces (the only ones
+// that depend on lo / hi: the interpolated endpoint values and their
+// divisions).  A counting sort by interior count hands equal-length intervals
+// to the lanes of a warp, and phase 2 folds F0 + term[a+1] + ... + L in the
+// reference's order: one shared load and one dependent add per step.
 constexpr int CHUNK = IV_POOL;  // intervals per phase-1/phase-2 round
 constexpr int NBUCKET = DIRECT + 2;
 
-struct WorkItem {
-    uint32_t lo, hi;   // window-relative times
-    int16_t a;         // first segment / last sample <= lo (window index)
-    int16_t n;         // STEP: segments (0..DIRECT); LINEAR: b - a (-1..DIRECT-1)
-    int32_t v;         // interval number within the tile (sets concatenated)
-};
+// item meta: q (chunk index, 10 bits) | s (first interior term, 11 bits) << 10 |
+//            cnt (interior terms, 9 bits) << 21 | has_last << 30
+static_assert(CHUNK <= 1024 && WIN <= 2048 && DIRECT < 512, "item meta packing");
 
 struct __align__(16) GroupSmem {  // private to one consumer group
     uint32_t ts32[WIN];
-    WorkItem work[CHUNK];
+    double F0[CHUNK];    // first piece (0.0 + first piece for the trapezoid)
+    double L[CHUNK];     // last piece
+    uint32_t meta[CHUNK];
     int16_t order[CHUNK];
     int hist[NBUCKET];
     int nvalid;
     double red[NCW];
-    float scale;
+    int64_t kq[DW_MAX_SETS];  // per set: interval index = kq + chunk index
+    int next_it;              // the group's claimed next tile (sequence position)
 };
 
-// last r in [r0, r1) with ts(r) < key, given ts(r0) < key
-__device__ __forceinline__ int search_last_lt32(const uint32_t *ts, int r0, int r1, uint32_t key,
-                                                float scale, uint32_t from_key) {
-    int g = r0 + (int)((float)(key - from_key) * scale);
-    g = g < r0 ? r0 : (g >= r1 ? r1 - 1 : g);
-    int lo, hi;
-    if (ts[g] < key) {
-        lo = g;
+// num / den correctly rounded, for integers 0 <= num <= den < 2^32 (the
+// trapezoid's frac, energy.py:121).  Markstein's final step on a reciprocal
+// refined to ~1 ulp: the pre-rounding error is < 2^-50 ulp, while a quotient
+// of such integers is either exact or >= ulp / (4 den) > 2^-34 ulp away from
+// a rounding midpoint, so the result equals IEEE division (scripts/micro/
+// div_check.cu checks it against __ddiv_rn: exhaustive for den <= 4096 plus
+// 4e9 random pairs).  About a third of __ddiv_rn's instructions, no branch.
+__device__ __forceinline__ double div_u32(uint32_t num, uint32_t den) {
+    const double b = (double)den, a = (double)num;
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
+    double e = __fma_rn(-b, y, 1.0);
+    y = __fma_rn(y, e, y);
+    e = __fma_rn(-b, y, 1.0);
+    y = __fma_rn(y, e, y);
+    const double q = __dmul_rn(a, y);
+    const double r = __fma_rn(-q, b, a);
+    return __fma_rn(r, y, q);
+}
+
+// item meta: q (chunk index, 9 bits) | s (first interior term, 11 bits) << 9 |
+//            cnt (interior terms, 9 bits) << 20 | has_last << 29 | set << 30
+__device__ __forceinline__ uint32_t pack_meta(int q, int s, int cnt, int last, int j) {
+    return (uint32_t)q | ((uint32_t)s << 9) | ((uint32_t)cnt << 20) | ((uint32_t)last << 29) |
+           ((uint32_t)j << 30);
+}
+constexpr uint32_t META_NONE = 0xFFFFFFFFu;  // no valid item packs to it (s < WIN < 2047, cnt <= DIRECT < 511)
+static_assert(CHUNK == 512, "meta q field is 9 bits");
+
+// last r in [r0, r1) with ts[r] <= key, given ts[r0] <= key and kref <= key
+// (kref = ts[gref] or a time known to lie at or after it).  Probes the
+// interpolated guess and its successor (independent loads); a miss (sample
+// spacing not uniform) gallops from the guess, then bisects.
+__device__ __forceinline__ int find_le(const uint32_t *ts, int r0, int r1, uint32_t key, uint32_t kref,
+                                       int gref, float scale) {
+    const float off = (float)(key - kref) * scale;
+    int g = off >= (float)(r1 - 1 - gref) ? r1 - 1 : gref + (int)off;
+    if (g < r0) g = r0;
+    const uint32_t tg = ts[g], tn = ts[g + 1];
+    if (tg <= key && (g + 1 >= r1 || tn > key)) return g;
+    int lo, hi;  // ts[lo] <= key; ts[hi] > key or hi == r1
+    if (tg <= key) {
+        lo = g + 1;  // ts[g + 1] <= key here
         int step = 1;
         hi = lo + 1;
-        while (hi < r1 && ts[hi] < key) {
+        while (hi < r1 && ts[hi] <= key) {
             lo = hi;
             step <<= 1;
             hi = lo + step;
@@ -457,7 +513,7 @@ __device__ __forceinline__ int search_last_lt32(const uint32_t *ts, int r0, int 
         hi = g;
         int step = 1;
         lo = hi - 1;
-        while (lo > r0 && ts[lo] >= key) {
+        while (lo > r0 && ts[lo] > key) {
             hi = lo;
             step <<= 1;
             lo = hi - step;
@@ -465,154 +521,154 @@ __device__ __forceinline__ int search_last_lt32(const uint32_t *ts, int r0, int 
         if (lo < r0) lo = r0;
     }
     while (hi - lo > 1) {
-        int m = (lo + hi) >> 1;
-        if (ts[m] < key) lo = m; else hi = m;
+        const int m = (lo + hi) >> 1;
+        if (ts[m] <= key) lo = m; else hi = m;
     }
     return lo;
 }
 
-__device__ __forceinline__ double lin_endpoint(const uint32_t *ts, const double *w, int i, uint32_t t) {
-    double wa = w[i];
-    double frac = __ddiv_rn((double)(t - ts[i]), (double)(ts[i + 1] - ts[i]));
-    return __dadd_rn(wa, __dmul_rn(frac, __dsub_rn(w[i + 1], wa)));
-}
-
+// Phase 1 for one interval (window-relative lo <= hi, lo in the tile): edge
+// pieces and interior count.  Returns false when it spans more than DIRECT
+// pieces (the fixed-point path takes it).  Branch-free apart from the
+// search fallbacks.
 template <int KIND>
-__device__ __forceinline__ double phase2_sum(const uint32_t *ts, const double *w, const WorkItem &e,
-                                             int64_t glo, int64_t ghi, const TileCtx &cx) {
-    const int a = e.a;
-    const uint32_t lo = e.lo, hi = e.hi;
+__device__ __forceinline__ bool phase1_item(const uint32_t *ts, const double *w, int r0, int r1, int cnt_win,
+                                            uint32_t lo, uint32_t hi, bool lo_first, bool lo_last,
+                                            bool hi_first, bool hi_last, const TileCtx &cx, double &F0,
+                                            double &L, int &s, int &cnt, int &last) {
+    const int a = find_le(ts, r0, r1, lo, ts[r0], r0, cx.scale);
+    const int lim = min(a + DIRECT + 1, cnt_win);
+    const uint32_t ta = ts[a], ta1 = ts[a + 1];
+    s = a + 1;
     if (KIND == DW_SIGNAL_STEP) {
-        const int n = e.n;
-        if (n == 0) return 0.0;
-        if (n == 1) return __dmul_rn(w[a], (double)(hi - lo));
-        double tot = __dmul_rn(w[a], (double)(ts[a + 1] - lo));
-        const int bl = a + n - 1;  // last segment
-        int i = a + 1;
-#pragma unroll 4
-        for (; i < bl; ++i) tot = __dadd_rn(tot, __dmul_rn(w[i], (double)(ts[i + 1] - ts[i])));
-        return __dadd_rn(tot, __dmul_rn(w[bl], (double)(hi - ts[bl])));
+        // energy.py:99-104, zero-overlap segments skipped; b = last segment start < hi
+        const int b = hi > lo ? find_le(ts, a, lim, hi - 1, ts[a], a, cx.scale) : a;
+        const int n = hi > lo ? b - a + 1 : 0;  // segments
+        if (n > DIRECT) return false;
+        const double wa = w[a];
+        F0 = n == 0 ? 0.0 : __dmul_rn(wa, (double)((n == 1 ? hi : ta1) - lo));
+        L = __dmul_rn(w[b], (double)(hi - ts[b]));
+        cnt = n >= 2 ? n - 2 : 0;
+        last = n >= 2;
+        return true;
     } else {
-        const int b = a + e.n;  // last sample < hi
-        double vprev;
-        if (glo <= cx.ts0) vprev = cx.w0;
-        else if (glo >= cx.tsl) vprev = cx.wl;
-        else vprev = lin_endpoint(ts, w, ts[a] == lo ? a - 1 : a, lo);
-        uint32_t prev = lo;
-        double tot = 0.0;
-#pragma unroll 4
-        for (int j = a + 1; j <= b; ++j) {
-            double wa = w[j - 1];
-            double vj = __dadd_rn(wa, __dsub_rn(w[j], wa));
-            uint32_t tj = ts[j];
-            tot = __dadd_rn(tot, __dmul_rn(__dmul_rn(0.5, __dadd_rn(vprev, vj)), (double)(tj - prev)));
-            prev = tj;
-            vprev = vj;
-        }
-        double vh;
-        if (ghi <= cx.ts0) vh = cx.w0;
-        else if (ghi >= cx.tsl) vh = cx.wl;
-        else vh = lin_endpoint(ts, w, b, hi);
-        return __dadd_rn(tot, __dmul_rn(__dmul_rn(0.5, __dadd_rn(vprev, vh)), (double)(hi - prev)));
+        // energy.py:108-130: points [lo] + {ts in (lo, hi)} + [hi]; b = last sample < hi
+        const int b = ta < hi ? find_le(ts, a, lim, hi - 1, ta, a, cx.scale) : a - 1;
+        const int m = b - a;  // -1 only when hi == lo == ts[a]
+        if (m + 1 > DIRECT) return false;  // pieces = m + 1
+        // v(lo), v(hi): first bracketing pair (energy.py:115-124)
+        const int il = ta == lo && a > 0 ? a - 1 : a;  // (a == 0: lo is the first sample, vlo = w0)
+        const double wl0 = w[il], wl1 = w[il + 1];
+        const uint32_t tl0 = ts[il];
+        const double vlo_i = __dadd_rn(wl0, __dmul_rn(div_u32(lo - tl0, ts[il + 1] - tl0), __dsub_rn(wl1, wl0)));
+        const double vlo = lo_first ? cx.w0 : (lo_last ? cx.wl : vlo_i);
+        const double wh0 = w[b], wh1 = w[b + 1];
+        const uint32_t th0 = ts[b];
+        const double vhi_i = __dadd_rn(wh0, __dmul_rn(div_u32(hi - th0, ts[b + 1] - th0), __dsub_rn(wh1, wh0)));
+        const double vhi = hi_first ? cx.w0 : (hi_last ? cx.wl : vhi_i);
+        // interior values v(a+1), v(b) (the loads are in range even when unused)
+        const double wa0 = w[a], wa1 = w[a + 1];
+        const double v1 = __dadd_rn(wa0, __dsub_rn(wa1, wa0));
+        const double wbm = w[b > 0 ? b - 1 : 0];
+        const double vb = __dadd_rn(wbm, __dsub_rn(wh0, wbm));
+        const bool one = m <= 0;  // one piece [lo, hi]
+        const double vn = one ? vhi : v1;
+        const uint32_t tnx = one ? hi : ta1;
+        F0 = __dadd_rn(0.0, __dmul_rn(__dmul_rn(0.5, __dadd_rn(vlo, vn)), (double)(tnx - lo)));
+        L = __dmul_rn(__dmul_rn(0.5, __dadd_rn(vb, vhi)), (double)(hi - th0));
+        cnt = one ? 0 : m - 1;
+        last = !one;
+        return true;
     }
 }
 
 template <int KIND>
 __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSmem &so, int stage,
-                                      int64_t tile, const TileCtx &cx, int ctid, int g) {
+                                      int64_t tile, const TileCtx &cx, int ctid, int g,
+                                      long long &prof_t) {
     const StageMeta &M = sm.meta[stage];
     const int64_t S = p.S;
     const int64_t wb = M.wb;
-    const int cnt = M.cnt;
+    const int cnt_win = M.cnt;
     const int r0 = (int)(tile * TILE - wb);
     const int r1 = (int)(min((tile + 1) * TILE, S) - wb);
     const uint32_t *ts = so.ts32;
     const double *w = sm.w[stage];
+    const double *term = reinterpret_cast<const double *>(sm.ts[stage]);
     const int64_t total = M.c[DW_MAX_SETS];
-    if (total == 0) {  // still close the tile: gs.red / ts32 are reused next tile
-        consumer_sync(g);
-        return;
-    }
+    const int nsets = p.nsets;
     for (int64_t c0 = 0; c0 < total; c0 += CHUNK) {
         const int nch = (int)(total - c0 < CHUNK ? total - c0 : CHUNK);
-        // ---- phase 1: locate, validate, bucket by length
-        for (int q = ctid; q < nch; q += ATTR_THREADS) {
-            const int64_t v = c0 + q;
-            const int j = (v >= M.c[1]) + (v >= M.c[2]) + (v >= M.c[3]);
-            const int64_t k = v - M.c[j] + M.f0[j];
-            const int64_t idx = k - M.a0[j];
-            int64_t glo, ghi;
-            if (idx < M.copied[j]) {
-                glo = sm.iv_lo[stage][M.pool[j] + idx];
-                ghi = sm.iv_hi[stage][M.pool[j] + idx];
-            } else {
-                glo = __ldg(p.start[j] + k);
-                ghi = __ldg(p.end[j] + k);
-            }
-            if (p.check_sorted[j] && k > 0) {
-                const int64_t pidx = idx - 1;
-                const int64_t prev = (pidx >= 0 && pidx < M.copied[j]) ? sm.iv_lo[stage][M.pool[j] + pidx]
-                                                                       : __ldg(p.start[j] + k - 1);
-                if (prev > glo) atomic_min_index(&p.st->unsorted_index[j], k);
-            }
-            WorkItem e;
-            e.v = (int32_t)v;
-            e.n = -2;  // skipped
-            if (ghi < glo || glo < cx.span_lo || ghi > cx.span_hi) {
-                report_bad(p, j, k);
-            } else {
+        // ---- phase 1: locate, validate, edge pieces, bucket by length
+        for (int j = 0; j < nsets; ++j) {
+            const int64_t vb0 = M.c[j] > c0 ? M.c[j] : c0;
+            const int64_t vb1 = M.c[j + 1] < c0 + nch ? M.c[j + 1] : c0 + nch;
+            if (vb1 <= vb0) continue;
+            const int qa = (int)(vb0 - c0), qb = (int)(vb1 - c0);
+            const int64_t kq = M.f0[j] - M.c[j] + c0;  // k = kq + q
+            const int64_t iq = kq - M.a0[j];            // staged index = iq + q
+            const int copied = M.copied[j], pool = M.pool[j];
+            const bool chk = p.check_sorted[j];
+            const int64_t *gs_lo = p.start[j], *gs_hi = p.end[j];
+            for (int q = qa + ctid; q < qb; q += ATTR_THREADS) {
+                const int64_t k = kq + q;
+                const int64_t idx = iq + q;
+                int64_t glo, ghi;
+                const bool staged = idx < copied;
+                if (staged) {
+                    glo = sm.iv_lo[stage][pool + idx];
+                    ghi = sm.iv_hi[stage][pool + idx];
+                } else {
+                    glo = __ldg(gs_lo + k);
+                    ghi = __ldg(gs_hi + k);
+                }
+                if (chk && k > 0) {  // a set flagged sorted must be sorted by start
+                    const int64_t prev = staged && idx > 0 ? sm.iv_lo[stage][pool + idx - 1] : __ldg(gs_lo + k - 1);
+                    if (prev > glo) atomic_min_index(&p.st->unsorted_index[j], k);
+                }
+                if (ghi < glo || glo < cx.span_lo || ghi > cx.span_hi) {
+                    report_bad(p, j, k);
+                    so.meta[q] = META_NONE;
+                    continue;
+                }
                 const uint32_t lo = (uint32_t)(glo - cx.base);
                 const int64_t dh = ghi - cx.base;
                 const uint32_t hi = dh > 0xFFFFFFFFLL ? 0xFFFFFFFFu : (uint32_t)dh;
-                const int a = search_last_le(Ts32{ts}, r0, r1, lo, cx.scale);
-                e.lo = lo;
-                e.hi = hi;
-                e.a = (int16_t)a;
-                if (KIND == DW_SIGNAL_STEP) {
-                    int n;
-                    if (hi == lo) {
-                        n = 0;
-                    } else {
-                        const int lim = min(a + DIRECT + 1, cnt);
-                        const int b = search_last_lt32(ts, a, lim, hi, cx.scale, lo);
-                        n = b - a + 1;
-                    }
-                    if (n > DIRECT) push_long(p, j, k);
-                    else e.n = (int16_t)n;
-                } else {
-                    int m;  // b - a, b = last sample < hi
-                    if (ts[a] < hi) {
-                        const int lim = min(a + DIRECT + 1, cnt);
-                        m = search_last_lt32(ts, a, lim, hi, cx.scale, lo) - a;
-                    } else {
-                        m = -1;  // hi == lo == ts[a]
-                    }
-                    if (m + 1 > DIRECT) push_long(p, j, k);  // pieces = m + 1
-                    else e.n = (int16_t)m;
+                double F0, L;
+                int s, cnt, last;
+                if (!phase1_item<KIND>(ts, w, r0, r1, cnt_win, lo, hi, glo <= cx.ts0, glo >= cx.tsl,
+                                       ghi <= cx.ts0, ghi >= cx.tsl, cx, F0, L, s, cnt, last)) {
+                    push_long(p, j, k);
+                    so.meta[q] = META_NONE;
+                    continue;
                 }
+                so.F0[q] = F0;
+                so.L[q] = L;
+                so.meta[q] = pack_meta(q, s, cnt, last, j);
+                atomicAdd(&so.hist[cnt], 1);
             }
-            so.work[q] = e;
-            if (e.n >= -1) atomicAdd(&so.hist[e.n + 1], 1);
         }
+        if (ctid < DW_MAX_SETS) so.kq[ctid] = (ctid < nsets ? M.f0[ctid] - M.c[ctid] : 0) + c0;
         consumer_sync(g);
+        PROF(3);
         // ---- exclusive scan of the length histogram (warp 0)
         if (ctid < 32) {
             constexpr int PER = (NBUCKET + 31) / 32;
             int loc[PER];
-            int s = 0;
+            int sacc = 0;
 #pragma unroll
             for (int u = 0; u < PER; ++u) {
                 int b = ctid * PER + u;
                 loc[u] = b < NBUCKET ? so.hist[b] : 0;
-                s += loc[u];
+                sacc += loc[u];
             }
-            int incl = s;
+            int incl = sacc;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 int t = __shfl_up_sync(0xffffffffu, incl, o);
                 if (ctid >= o) incl += t;
             }
-            int run = incl - s;
+            int run = incl - sacc;
 #pragma unroll
             for (int u = 0; u < PER; ++u) {
                 int b = ctid * PER + u;
@@ -622,86 +678,172 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
             if (ctid == 31) so.nvalid = incl;
         }
         consumer_sync(g);
+        PROF(4);
+        // ---- scatter: bucket order
         for (int q = ctid; q < nch; q += ATTR_THREADS) {
-            const int n = so.work[q].n;
-            if (n >= -1) so.order[atomicAdd(&so.hist[n + 1], 1)] = (int16_t)q;
+            const uint32_t mt = so.meta[q];
+            if (mt != META_NONE) so.order[atomicAdd(&so.hist[(mt >> 20) & 511u], 1)] = (int16_t)q;
         }
         consumer_sync(g);
+        PROF(5);
         // ---- phase 2: equal-length intervals side by side
         const int nvalid = so.nvalid;
         for (int q = ctid; q < nvalid; q += ATTR_THREADS) {
-            const WorkItem e = so.work[so.order[q]];
-            const int64_t v = e.v;
-            const int j = (v >= M.c[1]) + (v >= M.c[2]) + (v >= M.c[3]);
-            const int64_t k = v - M.c[j] + M.f0[j];
-            const int64_t glo = cx.base + e.lo, ghi = cx.base + e.hi;
-            const double tot = phase2_sum<KIND>(ts, w, e, glo, ghi, cx);
+            const int qi = so.order[q];
+            const uint32_t mt = so.meta[qi];
+            const int s = (int)((mt >> 9) & 2047u);
+            const int cnt = (int)((mt >> 20) & 511u);
+            const int j = (int)(mt >> 30);
+            double tot = so.F0[qi];
+            const double *tp = term + s;
+#pragma unroll 4
+            for (int u = 0; u < cnt; ++u) tot = __dadd_rn(tot, tp[u]);
+            if ((mt >> 29) & 1u) tot = __dadd_rn(tot, so.L[qi]);
+            const int64_t k = so.kq[j] + qi;
             const int64_t oidx = p.perm[j] ? __ldg(p.perm[j] + k) : k;
             p.out[j][oidx] = div_1e6(tot);
         }
         for (int b = ctid; b < NBUCKET; b += ATTR_THREADS) so.hist[b] = 0;
         consumer_sync(g);
+        PROF(6);
     }
 }
 
-__device__ __forceinline__ void producer(const AttrParams &p, TileSmem &sm, int64_t span_hi) {
+// Producer warp pw of NPROD handles positions it = pw, pw + NPROD, ... of
+// this CTA's tile sequence (one tile per stage fill).  The partition bounds of
+// 32 of its tiles are fetched at once (one global-load latency per 32 tiles)
+// and handed out by shuffles; lane 0 waits for the slot, lays out the stage
+// and arms the barrier, and the bulk copies are issued by separate lanes.
+__device__ __forceinline__ void producer(const AttrParams &p, TileSmem &sm, int64_t span_hi, int pw) {
     const int64_t S = p.S;
-    int it = 0;
-    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
-        const int stage = it % STAGES;
-        // partition reads first: their latency overlaps the wait for the slot
-        int64_t f0s[DW_MAX_SETS], f1s[DW_MAX_SETS];
+    const int lane = threadIdx.x & 31;
+    const int64_t nb = p.ntiles + 1;
+    const int ctid = lane;
+    long long prof_t = clock64();
+    for (int b0 = 0;; b0 += 32) {
+        const int itb = pw + NPROD * b0;  // first position of this batch
+        if ((int64_t)blockIdx.x + (int64_t)itb * gridDim.x >= p.ntiles) break;
+        const int64_t tl = (int64_t)blockIdx.x + (int64_t)(itb + NPROD * lane) * gridDim.x;
+        int64_t fl[DW_MAX_SETS], fh[DW_MAX_SETS];
 #pragma unroll
         for (int j = 0; j < DW_MAX_SETS; ++j) {
-            f0s[j] = j < p.nsets ? p.first[j * (p.ntiles + 1) + tile] : 0;
-            f1s[j] = j < p.nsets ? p.first[j * (p.ntiles + 1) + tile + 1] : 0;
+            const bool ok = j < p.nsets && tl < p.ntiles;
+            fl[j] = ok ? __ldg(p.first + j * nb + tl) : 0;
+            fh[j] = ok ? __ldg(p.first + j * nb + tl + 1) : 0;
         }
-        int64_t wb, we;
-        tile_window(tile, S, wb, we);
-        const int cnt = (int)(we - wb);
-        const int even = cnt & ~1;
-        uint32_t bytes = 2u * 8u * (uint32_t)even;
-        if (it >= STAGES) mbar_wait(&sm.empty[stage], (uint32_t)(((it / STAGES) - 1) & 1));
-        fence_proxy_async();
-        StageMeta &M = sm.meta[stage];
-        M.wb = wb;
-        M.cnt = cnt;
-        int pool = 0;
-        M.c[0] = 0;
+        for (int u = 0; u < 32; ++u) {
+            const int it = itb + NPROD * u;
+            const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
+            if (tile >= p.ntiles) break;
+            int64_t f0s[DW_MAX_SETS], f1s[DW_MAX_SETS];
 #pragma unroll
-        for (int j = 0; j < DW_MAX_SETS; ++j) {
-            const int64_t f0 = f0s[j], f1 = f1s[j];
-            const int64_t a0 = f0 & ~(int64_t)1;
-            int64_t want = f1 > f0 ? f1 - a0 : 0;
-            int64_t room = IV_POOL - pool;
-            int m = (int)(want < room ? want : room) & ~1;
-            M.f0[j] = f0;
-            M.c[j + 1] = M.c[j] + (f1 - f0);
-            M.a0[j] = a0;
-            M.copied[j] = m;
-            M.pool[j] = pool;
-            pool += m;
-            bytes += 2u * 8u * (uint32_t)m;
-        }
-        if (cnt & 1) {  // odd tail of the window: not a 16-byte multiple
-            sm.ts[stage][cnt - 1] = __ldg(p.ts + wb + cnt - 1);
-            sm.w[stage][cnt - 1] = __ldg(p.w + wb + cnt - 1);
-        }
-        if (wb + cnt == S) sm.ts[stage][cnt] = span_hi;  // virtual end of the last segment
-        mbar_expect_tx(&sm.full[stage], bytes);
-        if (even) {
-            tma_load_1d(sm.ts[stage], p.ts + wb, 8u * even, &sm.full[stage]);
-            tma_load_1d(sm.w[stage], p.w + wb, 8u * even, &sm.full[stage]);
-        }
-        for (int j = 0; j < p.nsets; ++j) {
-            const int m = M.copied[j];
-            if (m) {
-                tma_load_1d(&sm.iv_lo[stage][M.pool[j]], p.start[j] + M.a0[j], 8u * m, &sm.full[stage]);
-                tma_load_1d(&sm.iv_hi[stage][M.pool[j]], p.end[j] + M.a0[j], 8u * m, &sm.full[stage]);
+            for (int j = 0; j < DW_MAX_SETS; ++j) {
+                f0s[j] = __shfl_sync(0xffffffffu, fl[j], u);
+                f1s[j] = __shfl_sync(0xffffffffu, fh[j], u);
             }
+            const int stage = it % STAGES;
+            StageMeta &M = sm.meta[stage];
+            int64_t wb, we;
+            tile_window(tile, S, wb, we);
+            const int cnt = (int)(we - wb);
+            const int even = cnt & ~1;
+            if (lane == 0) {
+                uint32_t bytes = 2u * 8u * (uint32_t)even;
+                PROF(8);
+                if (it >= STAGES) mbar_wait(&sm.empty[stage], (uint32_t)(((it / STAGES) - 1) & 1));
+                PROF(7);
+                fence_proxy_async();
+                M.wb = wb;
+                M.cnt = cnt;
+                int pool = 0;
+                M.c[0] = 0;
+#pragma unroll
+                for (int j = 0; j < DW_MAX_SETS; ++j) {
+                    const int64_t f0 = f0s[j], f1 = f1s[j];
+                    const int64_t a0 = f0 & ~(int64_t)1;
+                    int64_t want = f1 > f0 ? f1 - a0 : 0;
+                    int64_t room = IV_POOL - pool;
+                    int m = (int)(want < room ? want : room) & ~1;
+                    M.f0[j] = f0;
+                    M.c[j + 1] = M.c[j] + (f1 - f0);
+                    M.a0[j] = a0;
+                    M.copied[j] = m;
+                    M.pool[j] = pool;
+                    pool += m;
+                    bytes += 2u * 8u * (uint32_t)m;
+                }
+                if (cnt & 1) {  // odd tail of the window: not a 16-byte multiple
+                    sm.ts[stage][cnt - 1] = __ldg(p.ts + wb + cnt - 1);
+                    sm.w[stage][cnt - 1] = __ldg(p.w + wb + cnt - 1);
+                }
+                if (wb + cnt == S) sm.ts[stage][cnt] = span_hi;  // virtual end of the last segment
+                mbar_expect_tx(&sm.full[stage], bytes);
+            }
+            __syncwarp();
+            // lane 0: timestamps, lane 1: watts, lanes 2 + 2j / 3 + 2j: set j's starts / ends
+            if (lane < 2) {
+                if (even) tma_load_1d(lane ? (void *)sm.w[stage] : (void *)sm.ts[stage],
+                                      lane ? (const void *)(p.w + wb) : (const void *)(p.ts + wb), 8u * even,
+                                      &sm.full[stage]);
+            } else if (lane < 2 + 2 * p.nsets) {
+                const int j = (lane - 2) >> 1;
+                const int m = M.copied[j];
+                if (m) {
+                    const bool hi_col = (lane - 2) & 1;
+                    int64_t *dst = hi_col ? &sm.iv_hi[stage][M.pool[j]] : &sm.iv_lo[stage][M.pool[j]];
+                    const int64_t *src = (hi_col ? p.end[j] : p.start[j]) + M.a0[j];
+                    tma_load_1d(dst, src, 8u * m, &sm.full[stage]);
+                }
+            }
+            __syncwarp();
         }
     }
 }
+
+// Terms of pieces r, r+1 for r = r0 + 2*ctid + 2*ATTR_THREADS*k, r < rend,
+// stored to term[] (when non-null); returns this thread's partial of the tile
+// sum over pieces < e1, added in that order (the fixed order oracle/
+// dw_oracle.c tile_sum() restates).  Linear pieces use v(x) of energy.py:
+// 115-124 (w0 / wl at the signal's first / last sample, window indices rz0 /
+// rzS; elsewhere the interior form w[x-1] + (w[x] - w[x-1])).
+template <int KIND, typename WIDTH>
+__device__ __forceinline__ double pair_terms(const double *w, const WIDTH &width, int r0, int rend, int e1,
+                                             int rz0, int rzS, double w0, double wl, double *term, int ctid) {
+    double acc = 0.0;
+    for (int r = r0 + 2 * ctid; r < rend; r += 2 * ATTR_THREADS) {
+        const double2 wr = *reinterpret_cast<const double2 *>(w + r);  // w[r], w[r+1]
+        const double d0 = (double)width(r), d1 = (double)width(r + 1);
+        double t0, t1;
+        if (KIND == DW_SIGNAL_STEP) {
+            t0 = __dmul_rn(wr.x, d0);
+            t1 = __dmul_rn(wr.y, d1);
+        } else {
+            const double wm = w[r > 0 ? r - 1 : 0], w2 = w[r + 2];
+            const double v0 = r == rz0 ? w0 : __dadd_rn(wm, __dsub_rn(wr.x, wm));
+            const double v1 = __dadd_rn(wr.x, __dsub_rn(wr.y, wr.x));
+            const double v1b = r + 1 == rzS ? wl : v1;
+            const double v2 = r + 2 == rzS ? wl : __dadd_rn(wr.y, __dsub_rn(w2, wr.y));
+            t0 = __dmul_rn(__dmul_rn(0.5, __dadd_rn(v0, v1b)), d0);
+            t1 = __dmul_rn(__dmul_rn(0.5, __dadd_rn(v1, v2)), d1);
+        }
+        if (term) {
+            if (r + 1 < rend) *reinterpret_cast<double2 *>(term + r) = make_double2(t0, t1);
+            else term[r] = t0;
+        }
+        if (r < e1) acc = __dadd_rn(acc, t0);
+        if (r + 1 < e1) acc = __dadd_rn(acc, t1);
+    }
+    return acc;
+}
+
+struct Width32 {
+    const uint32_t *t;
+    __device__ __forceinline__ uint32_t operator()(int r) const { return t[r + 1] - t[r]; }
+};
+struct Width64 {
+    const int64_t *t;
+    __device__ __forceinline__ int64_t operator()(int r) const { return t[r + 1] - t[r]; }
+};
 
 template <int KIND>
 __global__ void __launch_bounds__(KTHREADS, 1) attribute_tiles_kernel(AttrParams p) {
@@ -732,21 +874,38 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_tiles_kernel(AttrParams
     }
     for (int g = 0; g < GROUPS; ++g)
         for (int b = tid; b < NBUCKET; b += blockDim.x) groups[g].hist[b] = 0;
+    if (tid < GROUPS) groups[tid].next_it = tid;
+    if (tid == 0) sm.claim = GROUPS;
     __syncthreads();
 
-    if (tid >= GROUPS * ATTR_THREADS) {  // producer warp
-        if (tid == GROUPS * ATTR_THREADS) producer(p, sm, cx.span_hi);
+    if (tid >= GROUPS * ATTR_THREADS) {  // producer warps
+        producer(p, sm, cx.span_hi, (tid - GROUPS * ATTR_THREADS) >> 5);
         return;
     }
-    // consumer group g takes every GROUPS-th tile of this CTA's sequence
+    // Consumer groups claim positions of this CTA's tile sequence in order
+    // (shared counter), so a group never waits on a stage two fills ahead of
+    // an unconsumed one (claims in flight span < STAGES positions: GROUPS <
+    // STAGES) and a slow tile does not hold up the others.
     const int g = tid / ATTR_THREADS;
     const int ctid = tid - g * ATTR_THREADS;
     GroupSmem &gs = groups[g];
-    for (int it = g;; it += GROUPS) {
+    long long prof_t = clock64();
+    for (;;) {
+        const int it = gs.next_it;
         const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
         if (tile >= p.ntiles) break;
         const int stage = it % STAGES;
         mbar_wait(&sm.full[stage], (uint32_t)((it / STAGES) & 1));
+        PROF(0);
+#ifdef DW_SKIP_CONSUMERS
+        consumer_sync(g);
+        if (ctid == 0) {
+            gs.next_it = atomicAdd(&sm.claim, 1);
+            mbar_arrive(&sm.empty[stage]);
+        }
+        consumer_sync(g);
+        continue;
+#endif
         const StageMeta &M = sm.meta[stage];
         const int64_t wb = M.wb;
         const int cnt = M.cnt;
@@ -758,46 +917,60 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_tiles_kernel(AttrParams
         const int r0 = (int)(tile * TILE - wb);
         const int r1 = (int)(min((tile + 1) * TILE, S) - wb);
 
-        // (a) 32-bit relative timestamps, (b) power order check, (c) fp64 tile sum
-        if (!wide)
-            for (int r = ctid; r <= last; r += ATTR_THREADS) gs.ts32[r] = (uint32_t)(s_ts[r] - base);
-        if (p.validate_order) {
+        const int e1 = (int)(min((tile + 1) * TILE, nterms) - wb);
+        const int rz0 = wb == 0 ? 0 : -1000;
+        const int rzS = (S - 1 - wb) < (int64_t)WIN ? (int)(S - 1 - wb) : -1000;
+        {
+            const int64_t dt = s_ts[r1 < last ? r1 : last] - s_ts[r0];
+            cx.scale = dt > 0 ? (float)(r1 - r0) / (float)dt : 0.0f;
+        }
+        cx.base = base;
+        if (p.validate_order) {  // strictly increasing power timestamps (int64 compare)
             for (int r = r0 + ctid; r < r1 && wb + r + 1 < S; r += ATTR_THREADS)
                 if (s_ts[r + 1] <= s_ts[r]) atomic_min_index(&p.st->order_index, wb + r);
         }
-        double acc = 0.0;
-        const int e1 = (int)(min((tile + 1) * TILE, nterms) - wb);
-        for (int r = r0 + ctid; r < e1; r += ATTR_THREADS) {
-            double term;
-            if (KIND == DW_SIGNAL_STEP) {
-                term = __dmul_rn(s_w[r], (double)(s_ts[r + 1] - s_ts[r]));
-            } else {
-                const int64_t gi = wb + r;
-                double va = gi == 0 ? cx.w0 : lin_interior(s_w, r);
-                double vb = gi + 1 == S - 1 ? cx.wl : lin_interior(s_w, r + 1);
-                term = __dmul_rn(__dmul_rn(0.5, __dadd_rn(va, vb)), (double)(s_ts[r + 1] - s_ts[r]));
-            }
-            acc = __dadd_rn(acc, term);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-        if ((ctid & 31) == 0) gs.red[ctid >> 5] = acc;
-        if (ctid == 0) {
-            const int64_t dt = s_ts[r1 < last ? r1 : last] - s_ts[r0];
-            gs.scale = dt > 0 ? (float)(r1 - r0) / (float)dt : 0.0f;
-        }
-        consumer_sync(g);
-        if (ctid == 0) {
-            double t = gs.red[0];
-#pragma unroll
-            for (int k = 1; k < NCW; ++k) t = __dadd_rn(t, gs.red[k]);
-            p.tile_sum[tile] = t;
-        }
-        cx.scale = gs.scale;
-        cx.base = base;
         if (!wide) {
-            tile_intervals_sorted<KIND>(p, sm, gs, stage, tile, cx, ctid, g);
+            // (a) 32-bit relative timestamps, two per thread
+            for (int r = 2 * ctid; r <= last; r += 2 * ATTR_THREADS) {
+                const longlong2 t2 = *reinterpret_cast<const longlong2 *>(s_ts + r);
+                const uint32_t x = (uint32_t)(t2.x - base), y = (uint32_t)(t2.y - base);
+                if (r + 1 <= last) *reinterpret_cast<uint2 *>(gs.ts32 + r) = make_uint2(x, y);
+                else gs.ts32[r] = x;
+            }
+            consumer_sync(g);
+            if (ctid == 0) gs.next_it = atomicAdd(&sm.claim, 1);  // every thread has read it
+            PROF(1);
+            // (b) interior terms of pieces r0 .. last-1 into the stage's ts slots
+            // (phase 1 searches ts32 from here on), (c) the tile-sum partials
+            double *term = reinterpret_cast<double *>(const_cast<int64_t *>(s_ts));
+            double acc = pair_terms<KIND>(s_w, Width32{gs.ts32}, r0, last, e1, rz0, rzS, cx.w0, cx.wl, term, ctid);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+            if ((ctid & 31) == 0) gs.red[ctid >> 5] = acc;
+            PROF(2);
+            if (M.c[DW_MAX_SETS] == 0) consumer_sync(g);  // no intervals: red must still be visible
+            tile_intervals_sorted<KIND>(p, sm, gs, stage, tile, cx, ctid, g, prof_t);
+            // (the first barrier inside published red[]; the last closed the tile)
+            if (ctid == 0) {
+                double t = gs.red[0];
+#pragma unroll
+                for (int k = 1; k < NCW; ++k) t = __dadd_rn(t, gs.red[k]);
+                p.tile_sum[tile] = t;
+            }
         } else {
+            double acc = pair_terms<KIND>(s_w, Width64{s_ts}, r0, e1, e1, rz0, rzS, cx.w0, cx.wl,
+                                          (double *)nullptr, ctid);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+            if ((ctid & 31) == 0) gs.red[ctid >> 5] = acc;
+            consumer_sync(g);
+            if (ctid == 0) gs.next_it = atomicAdd(&sm.claim, 1);  // every thread has read it
+            if (ctid == 0) {
+                double t = gs.red[0];
+#pragma unroll
+                for (int k = 1; k < NCW; ++k) t = __dadd_rn(t, gs.red[k]);
+                p.tile_sum[tile] = t;
+            }
             Ts64 a64{s_ts, base};
             tile_intervals<KIND>(p, sm, stage, a64, s_w, tile, (int64_t)INT64_MAX, cx, ctid);
             consumer_sync(g);
@@ -1381,6 +1554,17 @@ int dw_fx_sum(const double *d_x, int64_t n, double *d_out, void *d_workspace, si
     DW_CHECK_LAUNCH();
     return DW_OK;
 }
+
+#ifdef DW_PHASE_PROF
+int dw_phase_prof(unsigned long long *out16, int reset) {
+    if (cudaMemcpyFromSymbol(out16, g_phase, sizeof(g_phase)) != cudaSuccess) return DW_E_CUDA;
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+    }
+    return DW_OK;
+}
+#endif
 
 int dw_step_value_at(const dw_signal_t *sig, const double *d_t, int64_t m, double *d_out,
                      dw_stream_t stream) {

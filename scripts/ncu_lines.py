@@ -33,5 +33,5 @@ for r in sass:
 tot_i = sum(v[0] for v in agg.values()) or 1
 tot_s = sum(v[1] for v in agg.values()) or 1
 print(f"{'line':>5} {'inst%':>6} {'stall%':>6} {'shexc':>10}  source")
-for ln, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:40]:
+for ln, v in sorted(agg.items(), key=lambda kv: -kv[1][int(sys.argv[3]) if len(sys.argv) > 3 else 1])[:int(sys.argv[4]) if len(sys.argv) > 4 else 40]:
     print(f"{str(ln):>5} {100*v[0]/tot_i:6.2f} {100*v[1]/tot_s:6.2f} {v[2]:10.0f}  {line_src.get(ln, '')[:90]}")

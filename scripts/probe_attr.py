@@ -25,4 +25,19 @@ for it in range(iters):
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     print(f"ledger {kind}: {ms:.3f} ms  {bytes_alg/ms/1e6:.1f} GB/s alg  long={st.long_intervals} code={st.code} total={st.totals[0]:.6e}", flush=True)
+L = _native.lib()
+if hasattr(L, "dw_phase_prof"):
+    import ctypes
+    buf = (ctypes.c_ulonglong * 16)()
+    L.dw_phase_prof(buf, 1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); _run_ledger(a, sig, False); e1.record(); torch.cuda.synchronize()
+    L.dw_phase_prof(buf, 1)
+    nt = (a.n_power + 1023) // 1024
+    names = ["wait_full", "ts32+bar", "terms+tilesum", "phase1+bar", "scan+bar", "scatter+bar",
+             "phase2+bar", "prod_wait_empty", "prod_issue"]
+    print(f"phase cycles per tile (per group / producer), ledger {e0.elapsed_time(e1):.3f} ms:")
+    for i, nm in enumerate(names):
+        print(f"  {nm:16s} {buf[i] / nt:9.1f}")
+    print(f"  sum consumer     {sum(buf[i] for i in range(7)) / nt:9.1f}")
 print("mem GB", torch.cuda.max_memory_allocated()/1e9)
