@@ -59,13 +59,17 @@ typedef struct CUstream_st *dw_stream_t; /* == cudaStream_t */
 /* Intervals spanning at most DW_DIRECT_MAX segments are summed sequentially in
  * fp64 exactly as the reference does (bit-identical); longer ones are summed
  * exactly in 2^-40 W*us fixed point and rounded once. */
+#ifndef DW_DIRECT_MAX
 #define DW_DIRECT_MAX 256
+#endif
 /* Tiling of the attribution kernel.  Whole tiles enter long-interval sums as
  * fp64 tile sums reduced in a fixed order (per-thread sums of term pairs
  * strided over DW_TILE_THREADS threads, warp xor-butterfly, warps in order), converted to
  * fixed point; the CPU oracle mirrors that order (oracle/dw_oracle.c). */
 #define DW_TILE 1024
-#define DW_TILE_THREADS 128
+#ifndef DW_TILE_THREADS
+#define DW_TILE_THREADS 192
+#endif
 
 /* ------------------------------------------------------------------- types */
 typedef struct {

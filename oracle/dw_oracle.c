@@ -63,7 +63,7 @@
 
 #define DW_DIRECT_MAX 256 /* see include/dwb200.h */
 #define DW_TILE 1024
-#define DW_TILE_THREADS 128
+#define DW_TILE_THREADS 192
 
 typedef __int128 i128;
 

@@ -52,7 +52,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> Path
     dw_phase_prof()); "skip" -- consumers release every stage unprocessed
     (-DDW_SKIP_CONSUMERS), the staging pipeline's own speed."""
     lib = LIB if not variant else OUT_DIR / f"libdwb200_{variant}.so"
-    extra = {"prof": ["-DDW_PHASE_PROF"], "skip": ["-DDW_SKIP_CONSUMERS"]}.get(variant.split("_")[0], [])
+    extra = {"prof": ["-DDW_PHASE_PROF"], "skip": ["-DDW_SKIP_CONSUMERS"]}.get(variant.split("_")[0], [])[:]
     if variant:  # experiment knobs for diagnostic builds only (e.g. -DDW_PREFETCH=0)
         extra += os.environ.get("DWB200_NVCC_EXTRA", "").split()
     if not variant and not force and not _stale():

@@ -41,8 +41,14 @@ constexpr int DIRECT = DW_DIRECT_MAX;        // sequential-sum cap
 constexpr int WIN = TILE + DIRECT + 6;       // window slots: 2 halo + TILE + DIRECT + 2, + virtual end
 constexpr int ATTR_THREADS = DW_TILE_THREADS; // threads of one consumer group
 constexpr int ATTR_WARPS = ATTR_THREADS / 32;
-constexpr int GROUPS = 4;                    // consumer groups per CTA (tiles processed concurrently)
-constexpr int STAGES = 5;                    // TMA ring depth (tiles staged per CTA)
+#ifndef DW_GROUPS
+#define DW_GROUPS 4
+#endif
+constexpr int GROUPS = DW_GROUPS;            // consumer groups per CTA (tiles processed concurrently)
+#ifndef DW_STAGES
+#define DW_STAGES 5
+#endif
+constexpr int STAGES = DW_STAGES;            // TMA ring depth (tiles staged per CTA)
 constexpr int CTAS_PER_SM = 1;
 
 #ifdef DW_PHASE_PROF
@@ -170,7 +176,10 @@ __global__ void partition_kernel(AttrParams p) {
 constexpr int NCW = ATTR_WARPS;              // warps per consumer group
 constexpr int NPROD = 1;                     // producer warps
 constexpr int KTHREADS = GROUPS * ATTR_THREADS + 32 * NPROD;
-constexpr int IV_POOL = 512;                 // staged intervals per stage (all sets)
+#ifndef DW_IV_POOL
+#define DW_IV_POOL 512
+#endif
+constexpr int IV_POOL = DW_IV_POOL;          // staged intervals per stage (all sets)
 
 struct StageMeta {
     int64_t wb;                 // window base (global sample index)
@@ -438,7 +447,10 @@ __device__ __forceinline__ void tile_intervals(const AttrParams &p, const TileSm
 // divisions).  A counting sort by interior count hands equal-length intervals
 // to the lanes of a warp, and phase 2 folds F0 + term[a+1] + ... + L in the
 // reference's order: one shared load and one dependent add per step.
-constexpr int CHUNK = IV_POOL;  // intervals per phase-1/phase-2 round
+#ifndef DW_CHUNK
+#define DW_CHUNK 512
+#endif
+constexpr int CHUNK = DW_CHUNK;  // intervals per phase-1/phase-2 round
 constexpr int NBUCKET = DIRECT + 2;
 
 // item meta: q (chunk index, 10 bits) | s (first interior term, 11 bits) << 10 |
@@ -485,7 +497,8 @@ __device__ __forceinline__ uint32_t pack_meta(int q, int s, int cnt, int last, i
            ((uint32_t)j << 30);
 }
 constexpr uint32_t META_NONE = 0xFFFFFFFFu;  // no valid item packs to it (s < WIN < 2047, cnt <= DIRECT < 511)
-static_assert(CHUNK == 512, "meta q field is 9 bits");
+static_assert(CHUNK <= 512, "meta q field is 9 bits");
+static_assert(GROUPS < STAGES, "claims in flight must span fewer positions than the ring");
 
 // last r in [r0, r1) with ts[r] <= key, given ts[r0] <= key and kref <= key
 // (kref = ts[gref] or a time known to lie at or after it).  Probes the
@@ -597,56 +610,58 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
     const double *term = reinterpret_cast<const double *>(sm.ts[stage]);
     const int64_t total = M.c[DW_MAX_SETS];
     const int nsets = p.nsets;
+    (void)nsets;
     for (int64_t c0 = 0; c0 < total; c0 += CHUNK) {
         const int nch = (int)(total - c0 < CHUNK ? total - c0 : CHUNK);
-        // ---- phase 1: locate, validate, edge pieces, bucket by length
-        for (int j = 0; j < nsets; ++j) {
-            const int64_t vb0 = M.c[j] > c0 ? M.c[j] : c0;
-            const int64_t vb1 = M.c[j + 1] < c0 + nch ? M.c[j + 1] : c0 + nch;
-            if (vb1 <= vb0) continue;
-            const int qa = (int)(vb0 - c0), qb = (int)(vb1 - c0);
-            const int64_t kq = M.f0[j] - M.c[j] + c0;  // k = kq + q
-            const int64_t iq = kq - M.a0[j];            // staged index = iq + q
-            const int copied = M.copied[j], pool = M.pool[j];
-            const bool chk = p.check_sorted[j];
-            const int64_t *gs_lo = p.start[j], *gs_hi = p.end[j];
-            for (int q = qa + ctid; q < qb; q += ATTR_THREADS) {
-                const int64_t k = kq + q;
-                const int64_t idx = iq + q;
-                int64_t glo, ghi;
-                const bool staged = idx < copied;
-                if (staged) {
-                    glo = sm.iv_lo[stage][pool + idx];
-                    ghi = sm.iv_hi[stage][pool + idx];
-                } else {
-                    glo = __ldg(gs_lo + k);
-                    ghi = __ldg(gs_hi + k);
-                }
-                if (chk && k > 0) {  // a set flagged sorted must be sorted by start
-                    const int64_t prev = staged && idx > 0 ? sm.iv_lo[stage][pool + idx - 1] : __ldg(gs_lo + k - 1);
-                    if (prev > glo) atomic_min_index(&p.st->unsorted_index[j], k);
-                }
-                if (ghi < glo || glo < cx.span_lo || ghi > cx.span_hi) {
-                    report_bad(p, j, k);
-                    so.meta[q] = META_NONE;
-                    continue;
-                }
-                const uint32_t lo = (uint32_t)(glo - cx.base);
-                const int64_t dh = ghi - cx.base;
-                const uint32_t hi = dh > 0xFFFFFFFFLL ? 0xFFFFFFFFu : (uint32_t)dh;
-                double F0, L;
-                int s, cnt, last;
-                if (!phase1_item<KIND>(ts, w, r0, r1, cnt_win, lo, hi, glo <= cx.ts0, glo >= cx.tsl,
-                                       ghi <= cx.ts0, ghi >= cx.tsl, cx, F0, L, s, cnt, last)) {
-                    push_long(p, j, k);
-                    so.meta[q] = META_NONE;
-                    continue;
-                }
-                so.F0[q] = F0;
-                so.L[q] = L;
-                so.meta[q] = pack_meta(q, s, cnt, last, j);
-                atomicAdd(&so.hist[cnt], 1);
+        // ---- phase 1: locate, validate, edge pieces, bucket by length.  The
+        // chunk's items (sets concatenated) are strided over the group's
+        // threads, so every thread gets the same count whatever the set sizes.
+        int cb1, cb2, cb3;  // chunk-relative set boundaries
+        {
+            auto rel = [&](int64_t c) -> int { return c <= c0 ? 0 : (c >= c0 + nch ? nch : (int)(c - c0)); };
+            cb1 = rel(M.c[1]);
+            cb2 = rel(M.c[2]);
+            cb3 = rel(M.c[3]);
+        }
+        for (int q = ctid; q < nch; q += ATTR_THREADS) {
+            const int j = (q >= cb1) + (q >= cb2) + (q >= cb3);
+            const int64_t k = M.f0[j] - M.c[j] + c0 + q;
+            const int64_t idx = k - M.a0[j];  // staged index
+            const bool staged = idx < M.copied[j];
+            const int pool = M.pool[j];
+            const int64_t *gs_lo = p.start[j];
+            int64_t glo, ghi;
+            if (staged) {
+                glo = sm.iv_lo[stage][pool + idx];
+                ghi = sm.iv_hi[stage][pool + idx];
+            } else {
+                glo = __ldg(gs_lo + k);
+                ghi = __ldg(p.end[j] + k);
             }
+            if (p.check_sorted[j] && k > 0) {  // a set flagged sorted must be sorted by start
+                const int64_t prev = staged && idx > 0 ? sm.iv_lo[stage][pool + idx - 1] : __ldg(gs_lo + k - 1);
+                if (prev > glo) atomic_min_index(&p.st->unsorted_index[j], k);
+            }
+            if (ghi < glo || glo < cx.span_lo || ghi > cx.span_hi) {
+                report_bad(p, j, k);
+                so.meta[q] = META_NONE;
+                continue;
+            }
+            const uint32_t lo = (uint32_t)(glo - cx.base);
+            const int64_t dh = ghi - cx.base;
+            const uint32_t hi = dh > 0xFFFFFFFFLL ? 0xFFFFFFFFu : (uint32_t)dh;
+            double F0, L;
+            int s, cnt, last;
+            if (!phase1_item<KIND>(ts, w, r0, r1, cnt_win, lo, hi, glo <= cx.ts0, glo >= cx.tsl,
+                                   ghi <= cx.ts0, ghi >= cx.tsl, cx, F0, L, s, cnt, last)) {
+                push_long(p, j, k);
+                so.meta[q] = META_NONE;
+                continue;
+            }
+            so.F0[q] = F0;
+            so.L[q] = L;
+            so.meta[q] = pack_meta(q, s, cnt, last, j);
+            atomicAdd(&so.hist[cnt], 1);
         }
         if (ctid < DW_MAX_SETS) so.kq[ctid] = (ctid < nsets ? M.f0[ctid] - M.c[ctid] : 0) + c0;
         consumer_sync(g);
