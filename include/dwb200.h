@@ -120,6 +120,17 @@ int dw_attribute(const dw_signal_t *sig, dw_interval_set_t *sets, int32_t nsets,
 int dw_ledger(const dw_signal_t *sig, dw_interval_set_t *ops, dw_interval_set_t *kernels,
               void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
 
+/* Overlap split (the north star's overlap-weighted
+ * splitting for concurrent kernels, SURVEY.md G1 -- the reference has no such
+ * mode: energy.py:305-316 gives every interval the full signal over its
+ * span).  joules[k] for one set with the power divided equally among the
+ * set's intervals active at each instant; equal to dw_attribute's result
+ * whenever no two intervals of the set overlap.  Any order of intervals.
+ * Errors as dw_attribute (status block at the head of the workspace, set 0). */
+size_t dw_attribute_split_workspace_size(int64_t n_samples, int64_t n);
+int dw_attribute_split(const dw_signal_t *sig, dw_interval_set_t *set, void *d_workspace,
+                       size_t workspace_bytes, dw_stream_t stream);
+
 /* Synchronise `stream` and copy the status block out of the workspace. Returns
  * status->code. */
 int dw_status(const void *d_workspace, dw_stream_t stream, dw_status_t *status);

@@ -100,6 +100,24 @@ def integrate_linear(ts, watts, lo, hi, mode=MODE_REFERENCE):
     return out
 
 
+def split(kind, ts, watts, span_hi, lo, hi):
+    """Overlap-split joules of one interval set (the builder's G1 definition,
+    dw_oracle.c dwo_split): power divided equally among the set's intervals
+    active at each instant; equals the compat integral when nothing overlaps."""
+    ts = np.ascontiguousarray(ts, dtype=np.int64)
+    watts = np.ascontiguousarray(watts, dtype=np.float64)
+    lo = np.ascontiguousarray(lo, dtype=np.int64)
+    hi = np.ascontiguousarray(hi, dtype=np.int64)
+    out = np.empty(lo.shape[0], dtype=np.float64)
+    bad = ctypes.c_int64(-1)
+    rc = lib().dwo_split(ctypes.c_int(0 if kind == "step" else 1), _p(ts), _p(watts),
+                         ctypes.c_int64(ts.shape[0]), ctypes.c_int64(int(span_hi or 0)), _p(lo), _p(hi),
+                         ctypes.c_int64(lo.shape[0]), _p(out), ctypes.byref(bad))
+    if rc:
+        raise OracleError(rc, bad.value)
+    return out
+
+
 def total_device(kind, ts, watts, span_hi=None) -> float:
     """The ledger total over the whole span under the device's definition."""
     ts = np.ascontiguousarray(ts, dtype=np.int64)

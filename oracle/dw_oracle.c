@@ -612,3 +612,71 @@ double dwo_total_device(int kind, const int64_t *ts, const double *w, int64_t n,
     }
     return term_to_joules(acc);
 }
+
+/* ---------------------------------------------------- overlap split (G1)
+ * The builder's definition (no reference function
+ * exists -- SURVEY.md G1).  Within one interval set, at every instant the
+ * signal's power is divided equally among the intervals active then:
+ *   x_0 < ... < x_u-1  the distinct endpoints of the set's non-empty intervals
+ *   slice k = [x_k, x_k+1], c_k = intervals with start <= x_k and end >= x_k+1
+ *   e_k = the compat integral of slice k (MODE_DEVICE: bit-identical to the
+ *         reference's sequential sum up to DW_DIRECT_MAX segments)
+ *   share_k = e_k / c_k (IEEE), 0 when c_k == 0
+ *   joules(i) = share_k when interval i is the single slice k, otherwise the
+ *               exact (2^-64 J fixed point) sum of its slices' shares, rounded
+ *               once; 0 for an empty interval.
+ * With no overlap every interval is one slice with c = 1, so split == compat
+ * exactly.  kind: 0 step, 1 linear. */
+typedef struct { int64_t t; int32_t d; } split_ev;
+
+static int split_ev_cmp(const void *pa, const void *pb) {
+    int64_t a = ((const split_ev *)pa)->t, b = ((const split_ev *)pb)->t;
+    return a < b ? -1 : a > b;
+}
+
+int dwo_split(int kind, const int64_t *ts, const double *w, int64_t n, int64_t span_hi,
+              const int64_t *lo, const int64_t *hi, int64_t m, double *out, int64_t *bad) {
+    if (n <= 0) { if (bad) *bad = -1; return DW_E_EMPTY; }
+    int64_t span_end = kind == 0 ? span_hi : ts[n - 1];
+    for (int64_t k = 0; k < m; k++) {
+        int rc = check_iv(lo[k], hi[k], ts[0], span_end);
+        if (rc) { if (bad) *bad = k; return rc; }
+    }
+    split_ev *ev = (split_ev *)malloc(sizeof(split_ev) * (size_t)(2 * m + 1));
+    int64_t ne = 0;
+    for (int64_t k = 0; k < m; k++) {
+        if (hi[k] == lo[k]) continue;
+        ev[ne].t = lo[k]; ev[ne++].d = 1;
+        ev[ne].t = hi[k]; ev[ne++].d = -1;
+    }
+    qsort(ev, (size_t)ne, sizeof(split_ev), split_ev_cmp);
+    int64_t *x = (int64_t *)malloc(sizeof(int64_t) * (size_t)(ne + 1));
+    int64_t *c = (int64_t *)malloc(sizeof(int64_t) * (size_t)(ne + 1));
+    int64_t u = 0, run = 0;
+    for (int64_t e = 0; e < ne; e++) {
+        run += ev[e].d;
+        if (e + 1 == ne || ev[e + 1].t != ev[e].t) { x[u] = ev[e].t; c[u] = run; u++; }
+    }
+    int64_t ns = u > 1 ? u - 1 : 0;
+    double *es = (double *)malloc(sizeof(double) * (size_t)(ns + 1));
+    i128 *P = (i128 *)malloc(sizeof(i128) * (size_t)(u + 1));
+    int rc = DW_OK;
+    if (ns) {
+        rc = kind == 0 ? dwo_integrate_step(ts, w, n, span_hi, x, x + 1, ns, es, 1, bad)
+                       : dwo_integrate_linear(ts, w, n, x, x + 1, ns, es, 1, bad);
+    }
+    if (rc == DW_OK) {
+        P[0] = 0;
+        for (int64_t k = 0; k < ns; k++) {
+            es[k] = c[k] > 0 ? es[k] / (double)c[k] : 0.0;
+            P[k + 1] = P[k] + fx_from_double(es[k], DW_FX_JOULE_BITS);
+        }
+        for (int64_t k = 0; k < m; k++) {
+            if (hi[k] == lo[k]) { out[k] = 0.0; continue; }
+            int64_t a = lower_bound64(x, u, lo[k]), b = lower_bound64(x, u, hi[k]);
+            out[k] = b == a + 1 ? es[a] : fx_to_double(P[b] - P[a], DW_FX_JOULE_BITS);
+        }
+    }
+    free(ev); free(x); free(c); free(es); free(P);
+    return rc;
+}

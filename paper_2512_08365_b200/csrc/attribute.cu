@@ -478,6 +478,9 @@ struct __align__(16) GroupSmem {  // private to one consumer group
 // div_check.cu checks it against __ddiv_rn: exhaustive for den <= 4096 plus
 // 4e9 random pairs).  About a third of __ddiv_rn's instructions, no branch.
 __device__ __forceinline__ double div_u32(uint32_t num, uint32_t den) {
+#ifdef DW_EXP_NODIV
+    return (double)num * 0.01;
+#endif
     const double b = (double)den, a = (double)num;
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
@@ -666,6 +669,11 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
         if (ctid < DW_MAX_SETS) so.kq[ctid] = (ctid < nsets ? M.f0[ctid] - M.c[ctid] : 0) + c0;
         consumer_sync(g);
         PROF(3);
+#ifdef DW_EXP_P1_ONLY
+        for (int b = ctid; b < NBUCKET; b += ATTR_THREADS) so.hist[b] = 0;
+        consumer_sync(g);
+        continue;
+#endif
         // ---- exclusive scan of the length histogram (warp 0)
         if (ctid < 32) {
             constexpr int PER = (NBUCKET + 31) / 32;
@@ -704,15 +712,21 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
         // ---- phase 2: equal-length intervals side by side
         const int nvalid = so.nvalid;
         for (int q = ctid; q < nvalid; q += ATTR_THREADS) {
+#ifdef DW_EXP_NOSORT
+            const int qi = q;
+#else
             const int qi = so.order[q];
+#endif
             const uint32_t mt = so.meta[qi];
             const int s = (int)((mt >> 9) & 2047u);
             const int cnt = (int)((mt >> 20) & 511u);
             const int j = (int)(mt >> 30);
             double tot = so.F0[qi];
             const double *tp = term + s;
+#ifndef DW_EXP_NOLOOP
 #pragma unroll 4
             for (int u = 0; u < cnt; ++u) tot = __dadd_rn(tot, tp[u]);
+#endif
             if ((mt >> 29) & 1u) tot = __dadd_rn(tot, so.L[qi]);
             const int64_t k = so.kq[j] + qi;
             const int64_t oidx = p.perm[j] ? __ldg(p.perm[j] + k) : k;
@@ -963,8 +977,12 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_tiles_kernel(AttrParams
             for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
             if ((ctid & 31) == 0) gs.red[ctid >> 5] = acc;
             PROF(2);
+#ifdef DW_EXP_PASSA_ONLY
+            consumer_sync(g);
+#else
             if (M.c[DW_MAX_SETS] == 0) consumer_sync(g);  // no intervals: red must still be visible
             tile_intervals_sorted<KIND>(p, sm, gs, stage, tile, cx, ctid, g, prof_t);
+#endif
             // (the first barrier inside published red[]; the last closed the tile)
             if (ctid == 0) {
                 double t = gs.red[0];

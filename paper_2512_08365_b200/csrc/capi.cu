@@ -1,5 +1,7 @@
 // capi.cu -- version / error strings / launch accounting for libdwb200.
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 
 #include "dw_common.cuh"
 
@@ -25,6 +27,24 @@ void timing_end(cudaStream_t s) {
     if (!g_timing || g_nev >= 64) return;
     cudaEventRecord(g_ev[2 * g_nev + 1], s);
     ++g_nev;
+}
+
+// Phase trace (diagnostic): with DWB200_TRACE set, trace_mark() records a
+// named event on the stream; dw_trace_report() prints the time between
+// consecutive marks to stderr.  Off by default (one getenv, then a branch).
+static thread_local cudaEvent_t g_tev[256];
+static thread_local const char *g_tname[256];
+static thread_local int g_ntev = 0;
+static int trace_on() {
+    static int on = -1;
+    if (on < 0) on = getenv("DWB200_TRACE") ? 1 : 0;
+    return on;
+}
+void trace_mark(cudaStream_t s, const char *name) {
+    if (!trace_on() || g_ntev >= 256) return;
+    if (!g_tev[g_ntev]) cudaEventCreate(&g_tev[g_ntev]);
+    g_tname[g_ntev] = name;
+    cudaEventRecord(g_tev[g_ntev++], s);
 }
 
 int num_sms() {
@@ -76,6 +96,18 @@ double dw_kernel_time_ms(int reset) {
     g_nev = 0;
     g_pending_ms = reset ? 0.0 : total;
     return total;
+}
+
+void dw_trace_report(void) {
+    using namespace dw;
+    if (!g_ntev) return;
+    cudaEventSynchronize(g_tev[g_ntev - 1]);
+    for (int i = 1; i < g_ntev; ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, g_tev[i - 1], g_tev[i]);
+        fprintf(stderr, "  %-28s %8.3f ms\n", g_tname[i], ms);
+    }
+    g_ntev = 0;
 }
 
 int64_t dw_launch_count(int reset) {

@@ -386,35 +386,75 @@ __global__ void run_bounds_kernel(const uint32_t *sorted, int64_t n, int32_t *fi
     if (p == n - 1 || sorted[p + 1] != d) end[d] = (int32_t)(p + 1);
 }
 
-// t-th occurrence of id d in A pairs with the t-th occurrence of d in B
-__global__ void join_pair_kernel(const uint32_t *da, const uint32_t *xa, int64_t na, const int32_t *first_a,
-                                 const uint32_t *xb, const int32_t *first_b, const int32_t *end_b,
-                                 int32_t *match_a) {
-    const int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS + threadIdx.x;
-    uint32_t d[ITEMS], i[ITEMS];
-    int32_t fa[ITEMS], fb[ITEMS], eb[ITEMS], j[ITEMS];
+// The pairing in sorted order, written back to A order without a random
+// 4-byte scatter over the whole match column (partial-sector writes that miss
+// L2 cost a DRAM read-modify-write each).  Pass 1 (sorted order) computes each
+// A op's partner and appends (i, j) to the bucket of i >> PAIR_BSH: the
+// bucket sizes are known up front (sorted A is a permutation of 0..na-1), so
+// bucket b owns stage[b << PAIR_BSH, ...) and a block reserves its share with
+// one atomic per bucket.  Pass 2 walks the stage in order and scatters inside
+// one bucket's 4 MB window of match_a at a time (L2-resident, full-sector
+// write-back).
+constexpr int PAIR_BSH = 20;
+constexpr int PAIR_THREADS = 256;
+constexpr int PAIR_ITEMS = 16;
+constexpr int PAIR_MAXB = 2048;  // na < 2^31
+
+__global__ void __launch_bounds__(PAIR_THREADS) join_pair_bucket_kernel(
+    const uint32_t *da, const uint32_t *xa, int64_t na, const int32_t *first_a, const uint32_t *xb,
+    const int32_t *first_b, const int32_t *end_b, unsigned int *cursor, uint2 *stage) {
+    __shared__ int hist[PAIR_MAXB];
+    __shared__ int base[PAIR_MAXB];
+    const int nbk = (int)((na + (1LL << PAIR_BSH) - 1) >> PAIR_BSH);
+    for (int b = threadIdx.x; b < nbk; b += PAIR_THREADS) hist[b] = 0;
+    __syncthreads();
+    const int64_t p0 = (int64_t)blockIdx.x * PAIR_THREADS * PAIR_ITEMS + threadIdx.x;
+    uint32_t i[PAIR_ITEMS];
+    int32_t j[PAIR_ITEMS], r[PAIR_ITEMS];
+    uint32_t d[PAIR_ITEMS];
 #pragma unroll
-    for (int u = 0; u < ITEMS; ++u) {
-        const int64_t p = base + (int64_t)u * blockDim.x;
+    for (int u = 0; u < PAIR_ITEMS; ++u) {
+        const int64_t p = p0 + (int64_t)u * PAIR_THREADS;
         d[u] = p < na ? __ldcs(da + p) : 0;
         i[u] = p < na ? __ldcs(xa + p) : 0;
     }
 #pragma unroll
-    for (int u = 0; u < ITEMS; ++u) {
-        fa[u] = first_a[d[u]];
-        fb[u] = first_b[d[u]];
-        eb[u] = end_b[d[u]];
+    for (int u = 0; u < PAIR_ITEMS; ++u) {
+        const int64_t p = p0 + (int64_t)u * PAIR_THREADS;
+        const int32_t fa = first_a[d[u]], fb = first_b[d[u]], eb = end_b[d[u]];
+        const int32_t t = (int32_t)p - fa;
+        j[u] = (p < na && eb > 0 && t < eb - fb) ? (int32_t)xb[fb + t] : -1;
     }
 #pragma unroll
-    for (int u = 0; u < ITEMS; ++u) {
-        const int64_t p = base + (int64_t)u * blockDim.x;
-        const int32_t t = (int32_t)p - fa[u];
-        j[u] = (p < na && eb[u] > 0 && t < eb[u] - fb[u]) ? (int32_t)xb[fb[u] + t] : -1;
+    for (int u = 0; u < PAIR_ITEMS; ++u) {
+        const int64_t p = p0 + (int64_t)u * PAIR_THREADS;
+        r[u] = p < na ? atomicAdd(&hist[i[u] >> PAIR_BSH], 1) : 0;
     }
+    __syncthreads();
+    for (int b = threadIdx.x; b < nbk; b += PAIR_THREADS)
+        base[b] = hist[b] ? (int)atomicAdd(cursor + b, (unsigned)hist[b]) : 0;
+    __syncthreads();
 #pragma unroll
-    for (int u = 0; u < ITEMS; ++u) {
-        const int64_t p = base + (int64_t)u * blockDim.x;
-        if (p < na) match_a[i[u]] = j[u];
+    for (int u = 0; u < PAIR_ITEMS; ++u) {
+        const int64_t p = p0 + (int64_t)u * PAIR_THREADS;
+        if (p >= na) continue;
+        const int b = (int)(i[u] >> PAIR_BSH);
+        stage[((int64_t)b << PAIR_BSH) + base[b] + r[u]] = make_uint2(i[u], (uint32_t)j[u]);
+    }
+}
+
+__global__ void join_pair_scatter_kernel(const uint2 *stage, int64_t na, int32_t *match_a) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * ITEMS;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS + threadIdx.x; base < na; base += stride) {
+        uint2 e[ITEMS];
+#pragma unroll
+        for (int u = 0; u < ITEMS; ++u) {
+            const int64_t q = base + (int64_t)u * blockDim.x;
+            e[u] = q < na ? __ldcs(stage + q) : make_uint2(0xFFFFFFFFu, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < ITEMS; ++u)
+            if (e[u].x != 0xFFFFFFFFu) match_a[e[u].x] = (int32_t)e[u].y;
     }
 }
 
@@ -567,6 +607,7 @@ static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, const 
     RankLayout L = rank_layout(P, k);
     if (ws_bytes < L.total) return DW_E_WORKSPACE;
     char *base = (char *)ws;
+    trace_mark(s, "rank:start");
     if (summary) {
         cudaMemsetAsync(base + L.done, 0, 16, s);
         if (P > 0) {
@@ -612,6 +653,7 @@ static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, const 
         rank_hist_kernel<<<grid, 512, 0, s>>>(r);
         rank_select_kernel<<<1, 32, 0, s>>>(r, need);
         count_launch(2);
+        trace_mark(s, "rank:digit");
         unsigned long long sel[2];
         cudaMemcpyAsync(sel, r.sel, sizeof(sel), cudaMemcpyDeviceToHost, s);
         if (cudaStreamSynchronize(s) != cudaSuccess) return DW_E_CUDA;
@@ -642,7 +684,9 @@ static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, const 
     cudaStreamSynchronize(s);
     if ((int64_t)nc > L.cap) return DW_E_WORKSPACE;  // massive ties at the threshold key
     if ((int64_t)nc < k) return DW_E_ARG;             // cannot happen
+    trace_mark(s, "rank:compact");
     sort_candidates(base, L, (int64_t)nc, s);
+    trace_mark(s, "rank:sort");
     cudaMemcpyAsync(order, base + L.tmp_idx, 8 * k, cudaMemcpyDeviceToDevice, s);
     DW_CHECK_LAUNCH();
     return DW_OK;
@@ -651,7 +695,7 @@ static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, const 
 struct JoinLayout {
     size_t table, counters, id_a, id_b, ix_a, ix_b, sid_a, sid_b, six_a, six_b, first_a, end_a,
         first_b, end_b,
-        bonly_tmp, cub, cub_bytes, total;
+        bonly_tmp, pair_stage, pair_cursor, cub, cub_bytes, total;
     int64_t cap, D;
 };
 
@@ -682,6 +726,8 @@ static JoinLayout join_layout(int64_t na, int64_t nb, int64_t max_distinct) {
     L.first_b = off; off += au(4 * L.D);
     L.end_b = off; off += au(4 * L.D);
     L.bonly_tmp = off; off += au(4 * std::max<int64_t>(nb, 1));
+    L.pair_stage = off; off += au(8 * std::max<int64_t>(na, 1));
+    L.pair_cursor = off; off += au(4 * PAIR_MAXB);
     size_t c1 = 0, c2 = 0;
     const int64_t nmax = std::max<int64_t>(std::max(na, nb), 1);
     cub::DeviceRadixSort::SortPairs(nullptr, c1, (const uint32_t *)nullptr, (uint32_t *)nullptr,
@@ -767,6 +813,7 @@ int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_d
     // counters: [0] overflow, [1] matched, [2] next_id (u32), [3] n_bonly (u32)
     q.overflow = counters;
     unsigned int *n_bonly = (unsigned int *)(counters + 3);
+    trace_mark(s, "join:start");
     cudaMemsetAsync(counters, 0, 64, s);
     cudaMemsetAsync(q.table, 0xFF, 8 * L.cap, s);
     const int64_t n = na + nb;
@@ -774,6 +821,7 @@ int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_d
         join_hash_kernel<<<(unsigned)std::min<int64_t>(num_sms() * 16, blocks_for(n, 256 * ITEMS)), 256, 0, s>>>(q);
         count_launch();
     }
+    trace_mark(s, "join:hash");
     // the number of distinct signatures bounds the sort's key bits
     unsigned long long hc0[4] = {0, 0, 0, 0};
     cudaMemcpyAsync(hc0, counters, sizeof(hc0), cudaMemcpyDeviceToHost, s);
@@ -790,25 +838,37 @@ int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_d
     size_t cb = L.cub_bytes;
     if (na) {  // stable: equal ids keep op order
         cub::DeviceRadixSort::SortPairs(base + L.cub, cb, q.id_a, sid_a, q.ix_a, six_a, (int)na, 0, nbits, s);
+        trace_mark(s, "join:sort_a");
         run_bounds_kernel<<<blocks_for(na), 256, 0, s>>>(sid_a, na, first_a, end_a);
         count_launch(4);
+        trace_mark(s, "join:bounds_a");
     }
     if (nb) {
         cb = L.cub_bytes;
         cub::DeviceRadixSort::SortPairs(base + L.cub, cb, q.id_b, sid_b, q.ix_b, six_b, (int)nb, 0, nbits, s);
+        trace_mark(s, "join:sort_b");
         run_bounds_kernel<<<blocks_for(nb), 256, 0, s>>>(sid_b, nb, first_b, end_b);
         count_launch(4);
+        trace_mark(s, "join:bounds_b");
     }
     if (na) {
-        join_pair_kernel<<<blocks_for(na, 256 * ITEMS), 256, 0, s>>>(sid_a, six_a, na, first_a, six_b, first_b,
-                                                                     end_b, d_match_a);
-        count_launch();
+        unsigned int *cursor = (unsigned int *)(base + L.pair_cursor);
+        uint2 *stage = (uint2 *)(base + L.pair_stage);
+        cudaMemsetAsync(cursor, 0, 4 * PAIR_MAXB, s);
+        join_pair_bucket_kernel<<<blocks_for(na, PAIR_THREADS * PAIR_ITEMS), PAIR_THREADS, 0, s>>>(
+            sid_a, six_a, na, first_a, six_b, first_b, end_b, cursor, stage);
+        trace_mark(s, "join:pair_bucket");
+        join_pair_scatter_kernel<<<(unsigned)std::min<int64_t>(num_sms() * 8, blocks_for(na, 256 * ITEMS)), 256, 0,
+                                   s>>>(stage, na, d_match_a);
+        count_launch(2);
+        trace_mark(s, "join:pair_scatter");
     }
     int32_t *bonly_tmp = (int32_t *)(base + L.bonly_tmp);
     if (nb) {
         join_bonly_kernel<<<blocks_for(nb), 256, 0, s>>>(sid_b, six_b, nb, first_b, first_a, end_a, bonly_tmp,
                                                           n_bonly);
         count_launch();
+        trace_mark(s, "join:bonly");
     }
     unsigned long long hc[4] = {0, 0, 0, 0};  // overflow, matched, next_id, n_bonly
     cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s);
@@ -819,6 +879,7 @@ int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_d
         cub::DeviceRadixSort::SortKeys(base + L.cub, cb, bonly_tmp, d_b_only, (int)b_only, 0,
                                        bits_for(nb), s);
         count_launch(4);
+        trace_mark(s, "join:bonly_sort");
     }
     JoinSideDev A{a->d_start, a->d_end, a->d_rank, a->d_joules, a->d_work};
     JoinSideDev B{b->d_start, b->d_end, b->d_rank, b->d_joules, b->d_work};
@@ -827,6 +888,7 @@ int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_d
         join_findings_a_kernel<<<blocks_for(na, 256 * ITEMS), 256, 0, s>>>(na, d_match_a, A, B, threshold, o,
                                                                             d_epw_a, d_epw_b, counters + 1);
         count_launch();
+        trace_mark(s, "join:findings_a");
     }
     if (b_only) {
         join_findings_b_kernel<<<blocks_for(b_only), 256, 0, s>>>(na, b_only, d_b_only, B, threshold, o,
@@ -839,6 +901,7 @@ int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_d
     const int64_t cnt[4] = {na + b_only, (int64_t)matched, na - (int64_t)matched, b_only};
     cudaMemcpyAsync(d_count, cnt, sizeof(cnt), cudaMemcpyHostToDevice, s);
     cudaStreamSynchronize(s);
+    trace_mark(s, "join:end");
     DW_CHECK_LAUNCH();
     return DW_OK;
 }

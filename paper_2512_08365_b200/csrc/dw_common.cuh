@@ -215,6 +215,7 @@ __device__ __forceinline__ void atomic_min_index(unsigned long long *p, int64_t 
 void count_launch(int n = 1);
 void timing_begin(cudaStream_t s);
 void timing_end(cudaStream_t s);
+void trace_mark(cudaStream_t s, const char *name);
 int num_sms();
 
 }  // namespace dw
