@@ -13,7 +13,7 @@ def f(k):
     except (KeyError, ValueError): return None
 t_ms = f("gpu__time_duration.sum")
 t_unit = u.get("gpu__time_duration.sum", "")
-t_s = t_ms * (1e-3 if t_unit == "msecond" else 1e-6 if t_unit == "usecond" else 1e-9)
+t_s = t_ms * {"msecond": 1e-3, "ms": 1e-3, "usecond": 1e-6, "us": 1e-6, "s": 1.0, "second": 1.0}.get(t_unit, 1e-9)
 rd = f("dram__bytes_read.sum"); wr = f("dram__bytes_write.sum")
 scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "Tbyte": 1e12}
 rd_b = rd * scale.get(u.get("dram__bytes_read.sum"), 1); wr_b = wr * scale.get(u.get("dram__bytes_write.sum"), 1)
