@@ -257,6 +257,37 @@ def integrate_many(signal: PowerSignal, lo, hi) -> torch.Tensor:
     return out
 
 
+def integrate_split(signal: PowerSignal, lo, hi) -> torch.Tensor:
+    """Overlap-split joules of one interval set (device tensor out): the
+    signal's power divided equally among the set's intervals active at each
+    instant (the reference has no such mode, it
+    gives every interval the full signal -- SURVEY.md G1).  Equal to
+    ``integrate_many`` when no two intervals overlap.  Errors as
+    ``integrate_many``."""
+    if signal._kind is None or len(signal) == 0:
+        raise SignalError("empty power signal")
+    dev = _native.device()
+    lo_d = _to_dev(lo, torch.int64, dev).reshape(-1)
+    hi_d = _to_dev(hi, torch.int64, dev).reshape(-1)
+    out = torch.empty(lo_d.numel(), dtype=torch.float64, device=dev)
+    iset = _native.IntervalSet(_native.ptr(lo_d), _native.ptr(hi_d), lo_d.numel(), _native.ptr(out), 0, 0)
+    csig, keep = signal._c_signal()
+    L = _native.lib()
+    ws = _native.Workspace.get(L.dw_attribute_split_workspace_size(csig.n, lo_d.numel()))
+    stream = _native.stream_handle()
+    _native.check(L.dw_attribute_split(ctypes.byref(csig), ctypes.byref(iset), ws.data_ptr(), ws.numel(),
+                                       stream), "dw_attribute_split")
+    st = _native.Status()
+    L.dw_status(ws.data_ptr(), stream, ctypes.byref(st))
+    if st.order_index >= 0:
+        from .trace_model import TraceError
+        raise TraceError("power samples must be strictly increasing in timestamp")
+    if st.bad_index[0] >= 0:
+        k = st.bad_index[0]
+        _raise_interval_error(int(lo_d[k].item()), int(hi_d[k].item()), signal.span())
+    return out
+
+
 def integrate(signal: PowerSignal, interval: tuple[int, int]) -> float:
     """Joules over ``interval``; exact for ground truth, trapezoidal for samples
     (energy.py:90-105)."""
@@ -484,11 +515,38 @@ def _read_pair(cols, a, b, i):
     return int(x[i]), int(y[i])
 
 
+def _split_ledger(method: str, cols: TraceColumns, signal: PowerSignal, st) -> EnergyLedger:
+    """Split-mode ledger: the compat pass above validated the intervals and
+    integrated the span (total); here each set is split among its concurrently
+    active intervals and idle = max(total - exact sum of operators, 0)."""
+    per_op = integrate_split(signal, cols.device("op_start"), cols.device("op_end"))
+    per_k = integrate_split(signal, cols.device("k_start"), cols.device("k_end"))
+    op_total = _fx_sum(per_op)
+    total = float(st.totals[0])
+    return EnergyLedger(method=method, per_kernel=JoulesView(cols.k_ids, per_k, "k"),
+                        per_operator=JoulesView(cols.op_ids, per_op, "op"),
+                        idle_joules=max(total - op_total, 0.0), total_joules=total, op_total=op_total)
+
+
+def _fx_sum(x: torch.Tensor) -> float:
+    L = _native.lib()
+    out = torch.zeros(1, dtype=torch.float64, device=x.device)
+    ws = _native.Workspace.get(L.dw_fx_sum_workspace_size(x.numel()))
+    _native.check(L.dw_fx_sum(_native.ptr(x), x.numel(), _native.ptr(out), ws.data_ptr(), ws.numel(),
+                              _native.stream_handle()), "dw_fx_sum")
+    return float(out.item())
+
+
 def build_ledger(trace, method: str = "ground_truth",
                  period_us: int = DEFAULT_SAMPLER_PERIOD_US,
                  delay_us: int = DEFAULT_SAMPLER_DELAY_US, repeat: int = DEFAULT_REPLAY_REPEAT,
-                 seed: int = 0, validate_order: bool = False) -> EnergyLedger:
+                 seed: int = 0, validate_order: bool = False, overlap: str = "compat") -> EnergyLedger:
     """Attribute energy to kernels and operators (energy.py:280-331).
+
+    ``overlap="compat"`` (default) is the reference: every interval gets the
+    full signal over its span.  ``overlap="split"`` divides the power among
+    concurrently active operators (and, separately, kernels) -- see
+    ``integrate_split``; idle is then the energy outside every operator.
 
     ``trace`` is a reference-style Trace (the reference's own objects work) or a
     TraceColumns.  Gaps between kernels inside an operator's interval go to the
@@ -496,6 +554,8 @@ def build_ledger(trace, method: str = "ground_truth",
     """
     if method not in METHODS and method not in EXTRA_METHODS:
         raise ValueError(f"unknown energy method {method!r}")
+    if overlap not in ("compat", "split"):
+        raise ValueError(f"unknown overlap mode {overlap!r}")
     cols = TraceColumns.from_trace(trace)
     if method == "samples":
         if cols.n_power == 0:
@@ -506,6 +566,8 @@ def build_ledger(trace, method: str = "ground_truth",
         signal._span_hi = last
         per_op, per_k, st = _run_ledger(cols, signal, validate_order)
         _raise_ledger_errors(cols, st, signal.span())
+        if overlap == "split":
+            return _split_ledger(method, cols, signal, st)
         return EnergyLedger(method=method, per_kernel=JoulesView(cols.k_ids, per_k, "k"),
                             per_operator=JoulesView(cols.op_ids, per_op, "op"),
                             idle_joules=float(st.totals[2]), total_joules=float(st.totals[0]),
@@ -522,6 +584,8 @@ def build_ledger(trace, method: str = "ground_truth",
         signal = sampled_view(cols, period_us, delay_us, seed)
     per_op, per_k, st = _run_ledger(cols, signal, validate_order)
     _raise_ledger_errors(cols, st, truth.span())
+    if overlap == "split":
+        return _split_ledger(method, cols, signal, st)
     total, op_total, idle = st.totals[0], st.totals[1], st.totals[2]
     return EnergyLedger(method=method,
                         per_kernel=JoulesView(cols.k_ids, per_k, "k"),

@@ -138,3 +138,51 @@ def test_occurrence_and_join_definition():
     ma, mb = oracle.join(sig_a, sig_b)
     np.testing.assert_array_equal(ma, [1, 0, 2, 4, -1])
     np.testing.assert_array_equal(mb, [1, 0, 2, -1, 3, -1])
+
+
+# ------------------------------------------------ overlap split (G1) oracle
+
+def test_split_g1_example():
+    """ops [0,100) and [50,150) over 100 W then 300 W.  Compat
+    double-counts (0.01 + 0.02 > 0.025 J total); split shares the overlap."""
+    ts, w = np.array([0, 100]), np.array([100.0, 300.0])
+    lo, hi = np.array([0, 50]), np.array([100, 150])
+    np.testing.assert_array_equal(oracle.integrate_step(ts, w, 150, lo, hi, oracle.MODE_DEVICE), [0.01, 0.02])
+    got = oracle.split("step", ts, w, 150, lo, hi)
+    np.testing.assert_allclose(got, [0.0075, 0.0175], rtol=1e-15)
+    assert got.sum() == pytest.approx(0.025, rel=1e-15)
+
+
+@pytest.mark.parametrize("kind", ["step", "linear"])
+def test_split_equals_compat_without_overlap(kind):
+    from _split_cases import disjoint, signal
+    rng = np.random.default_rng(7 if kind == "step" else 8)
+    ts, w, span_hi = signal(rng, 3000, kind)
+    lo, hi = disjoint(rng, ts, span_hi, 400)
+    comp = (oracle.integrate_step(ts, w, span_hi, lo, hi, oracle.MODE_DEVICE) if kind == "step"
+            else oracle.integrate_linear(ts, w, lo, hi, oracle.MODE_DEVICE))
+    np.testing.assert_array_equal(oracle.split(kind, ts, w, span_hi, lo, hi), comp)
+
+
+@pytest.mark.parametrize("kind", ["step", "linear"])
+def test_split_conserves_union_energy(kind):
+    """Shares add up to the energy of the union of the set's intervals."""
+    from _split_cases import overlapping, signal
+    rng = np.random.default_rng(11)
+    ts, w, span_hi = signal(rng, 2000, kind)
+    lo, hi = overlapping(rng, ts, span_hi, 600)
+    got = oracle.split(kind, ts, w, span_hi, lo, hi)
+    order = np.argsort(lo, kind="stable")
+    ulo, uhi = [], []
+    for a, b in zip(lo[order], hi[order]):
+        if b <= a:
+            continue
+        if ulo and a <= uhi[-1]:
+            uhi[-1] = max(uhi[-1], b)
+        else:
+            ulo.append(a); uhi.append(b)
+    f = (lambda x, y: oracle.integrate_step(ts, w, span_hi, x, y, oracle.MODE_DEVICE)) if kind == "step" \
+        else (lambda x, y: oracle.integrate_linear(ts, w, x, y, oracle.MODE_DEVICE))
+    union = f(np.array(ulo), np.array(uhi)).sum()
+    assert got.sum() == pytest.approx(union, rel=1e-9)
+    assert np.all(got >= 0)
