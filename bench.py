@@ -49,6 +49,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-ops", type=int, default=2_000_000)
+    ap.add_argument("--shard", default="pair", choices=("pair", "window"),
+                    help="N>1: 'pair' = every rank its own trace pair (weak scaling, corpus); "
+                         "'window' = ONE pair split by time window over the ranks (strong scaling)")
+    ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"))
     return ap.parse_args()
 
 
@@ -390,6 +394,80 @@ def run_ours(args, rank: int, world: int, local: int):
     print(json.dumps(line), flush=True)
 
 
+def run_window(args, rank: int, world: int, local: int):
+    """One trace pair time-window-sharded over the ranks:
+    each rank attributes its window of both traces, crossing intervals and
+    totals combine exactly, and the signature join runs hash-partitioned
+    after one all-to-all.  Strong scaling: the work per step is one pair."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_08365_b200 import _native, shard, synth
+
+    torch.cuda.set_device(local)
+    _native.lib()
+    cfg = synth.CONFIGS[args.config]
+    ca, cb = synth.make_pair(cfg)
+    kind = "linear" if args.method == "samples" else "step"
+    comm = shard.Comm() if world > 1 else None
+    if comm is None:
+        class _One:
+            rank, world = 0, 1
+            all_gather_object = staticmethod(lambda o: [o])
+            all_to_all = staticmethod(lambda ts: ts)
+        comm = _One()
+    win_a = shard.plan(ca.n_power, world, kind)[rank]
+    win_b = shard.plan(cb.n_power, world, kind)[rank]
+    ia, ib = shard.rank_inputs(ca, kind, win_a), shard.rank_inputs(cb, kind, win_b)
+    for c in (ca, cb):
+        for n in ("op_sig", "op_start", "op_end"):
+            c.device(n)
+    torch.cuda.synchronize()
+    intervals = ca.n_ops + ca.n_kernels + cb.n_ops + cb.n_kernels
+
+    def step():
+        la = shard.sharded_ledger(ca, kind, comm, inputs=ia)
+        lb = shard.sharded_ledger(cb, kind, comm, inputs=ib)
+        return shard.sharded_join(shard.shard_ops(ca, la, True), shard.shard_ops(cb, lb, False), ca.n_ops, comm,
+                                  0.10, args.k)
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    _native.launch_count(reset=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            res = step()
+        e1.record()
+        torch.cuda.synchronize()
+    launches = _native.launch_count(reset=True)
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device="cuda" if args.dist_backend == "nccl" else "cpu")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": intervals / (ms_max / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config}: ONE trace pair, {cfg.n_ops} ops and {ca.n_power} power samples "
+                               f"per trace, time-window sharded", "method": args.method,
+                   "intervals_per_pair": intervals, "findings": res.P, "top_k": args.k,
+                   "parallelism": f"time-window x{world} ({args.dist_backend})"},
+        "samples_per_s": (ca.n_power + cb.n_power) / (ms_max / 1e3),
+        "gpu_launches": launches, "clocks": clocks.summary(),
+        "n_waste": res.n_waste, "wasted_joules": res.wasted_joules,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -401,10 +479,18 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        if args.dist_backend == "gloo":  # (test setups: several ranks may share one GPU)
+            local = local % max(torch.cuda.device_count(), 1)
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     try:
+        if args.shard == "window":
+            run_window(args, rank, world, local)
+            return
         run_ours(args, rank, world, local)
     finally:
         if world > 1:

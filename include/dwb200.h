@@ -120,6 +120,36 @@ int dw_attribute(const dw_signal_t *sig, dw_interval_set_t *sets, int32_t nsets,
 int dw_ledger(const dw_signal_t *sig, dw_interval_set_t *ops, dw_interval_set_t *kernels,
               void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
 
+/* One rank of a time-window-sharded trace.
+ * The rank holds the samples [g_off, g_off + n) of a signal of
+ * n_samples_global samples and owns the pieces (segments / trapezoid pieces,
+ * indexed by their left sample) [piece_lo, piece_hi).  g_off must be a
+ * multiple of DW_TILE, so the local tile grid is the global one. */
+typedef struct {
+    int64_t g_off, n_samples_global;
+    int64_t piece_lo, piece_hi;
+    int64_t ts_first, ts_last;  /* global first / last sample time (LINEAR edge rule) */
+    double w_first, w_last;     /* and their watts */
+} dw_window_t;
+
+/* dw_attribute on the rank's local signal (sig: the local samples; for STEP,
+ * span_hi = the next global sample time, or the global span end on the last
+ * rank) for the intervals it computes whole, plus:
+ *  - d_part[2e..2e+1]: exact int128 (2^-40 W*us, little-endian halves) share
+ *    of listed interval e (d_blo/d_bhi, longer than DW_DIRECT_MAX pieces,
+ *    crossing window edges) over the owned pieces -- summed over ranks and
+ *    rounded once it equals the one-GPU value bit for bit;
+ *  - d_tile_fx[2]: exact int128 sum of the owned whole-tile sums (the rank's
+ *    share of the ledger total, same scale). */
+int dw_attribute_window(const dw_signal_t *sig, dw_interval_set_t *sets, int32_t nsets, const dw_window_t *win,
+                        const int64_t *d_blo, const int64_t *d_bhi, int64_t nb, int64_t *d_part,
+                        int64_t *d_tile_fx, void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
+
+/* Exact 2^-64 J fixed-point sum of d_x[0..n) as int128 halves (not rounded):
+ * the per-rank share of a sharded operator_total.  Workspace as dw_fx_sum. */
+int dw_fx_sum_exact(const double *d_x, int64_t n, int64_t *d_out_fx, void *d_workspace,
+                    size_t workspace_bytes, dw_stream_t stream);
+
 /* Overlap split (the north star's overlap-weighted
  * splitting for concurrent kernels, SURVEY.md G1 -- the reference has no such
  * mode: energy.py:305-316 gives every interval the full signal over its

@@ -38,7 +38,7 @@ DW_DIRECT_MAX = 256
 # every symbol include/dwb200.h declares (tests check the .so exports them all)
 EXPORTED = (
     "dw_attribute_workspace_size", "dw_attribute", "dw_ledger", "dw_status",
-    "dw_attribute_split_workspace_size", "dw_attribute_split",
+    "dw_attribute_split_workspace_size", "dw_attribute_split", "dw_attribute_window", "dw_fx_sum_exact",
     "dw_fx_sum_workspace_size", "dw_fx_sum", "dw_step_value_at", "dw_detect_pairs",
     "dw_rank_workspace_size", "dw_rank", "dw_join_workspace_size", "dw_join_diff",
     "dw_version", "dw_error_string", "dw_launch_count", "dw_kernel_timing", "dw_kernel_time_ms",
@@ -68,6 +68,12 @@ class Signal(ctypes.Structure):
 class IntervalSet(ctypes.Structure):
     _fields_ = [("d_start", c_vp), ("d_end", c_vp), ("n", c_i64), ("d_joules", c_vp),
                 ("sorted", c_i32), ("pad", c_i32)]
+
+
+class Window(ctypes.Structure):
+    _fields_ = [("g_off", c_i64), ("n_samples_global", c_i64), ("piece_lo", c_i64), ("piece_hi", c_i64),
+                ("ts_first", c_i64), ("ts_last", c_i64), ("w_first", ctypes.c_double),
+                ("w_last", ctypes.c_double)]
 
 
 class Status(ctypes.Structure):
@@ -112,6 +118,10 @@ def lib():
         L.dw_ledger.argtypes = [ctypes.POINTER(Signal), ctypes.POINTER(IntervalSet),
                                 ctypes.POINTER(IntervalSet), c_vp, ctypes.c_size_t, c_vp]
         L.dw_status.argtypes = [c_vp, c_vp, ctypes.POINTER(Status)]
+        L.dw_attribute_window.argtypes = [ctypes.POINTER(Signal), ctypes.POINTER(IntervalSet), c_i32,
+                                          ctypes.POINTER(Window), c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
+                                          ctypes.c_size_t, c_vp]
+        L.dw_fx_sum_exact.argtypes = [c_vp, c_i64, c_vp, c_vp, ctypes.c_size_t, c_vp]
         L.dw_attribute_split_workspace_size.restype = ctypes.c_size_t
         L.dw_attribute_split_workspace_size.argtypes = [c_i64, c_i64]
         L.dw_attribute_split.argtypes = [ctypes.POINTER(Signal), ctypes.POINTER(IntervalSet), c_vp,

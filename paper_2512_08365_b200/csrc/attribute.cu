@@ -1220,12 +1220,128 @@ __global__ void __launch_bounds__(256) long_intervals_kernel(AttrParams p) {
     }
 }
 
+// --------------------------------------------- K7 time-window partials
+// One rank of a time-window-sharded trace holds the samples of
+// its owned pieces [P0, P1) (global indices) plus halos; its tile grid is the
+// global one (g_off, the global index of local sample 0, is a multiple of
+// DW_TILE).  For each listed interval -- an interval longer than DW_DIRECT_MAX
+// pieces that crosses window edges -- this computes the exact fixed-point
+// contribution of the pieces it owns, with the same decomposition as
+// long_intervals_kernel (edge pieces, partial tiles term by term, whole tiles
+// through the tile prefix), so the sum over ranks equals the one-GPU value
+// bit for bit.  Sample values use the GLOBAL first / last sample rules.
+struct WindowParams {
+    int64_t g_off, S_global, P0, P1;
+    int64_t ts0_g, tsl_g;  // global first / last sample time
+    double w0_g, wl_g;     // and watts
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(256) window_partials_kernel(AttrParams p, WindowParams wp, const int64_t *blo,
+                                                             const int64_t *bhi, int64_t nb,
+                                                             unsigned long long *part) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (gridDim.x * (int64_t)blockDim.x) >> 5;
+    const int64_t S = p.S, g = wp.g_off;
+    auto TS = [&](int64_t i) -> int64_t { return i < S ? __ldg(p.ts + i) : p.span_hi; };
+    auto W = [&](int64_t i) -> double { return __ldg(p.w + i); };
+    auto VS = [&](int64_t j) -> double {  // v(ts[j]) with the global boundary rules
+        if (j + g == 0 || j + g == wp.S_global - 1) return W(j);
+        const double wa = W(j - 1);
+        return __dadd_rn(wa, __dsub_rn(W(j), wa));
+    };
+    auto own = [&](int64_t jg) -> bool { return jg >= wp.P0 && jg < wp.P1; };
+    // owned share of range_sum over GLOBAL pieces [j0g, j1g], with the one-GPU
+    // decomposition: its first and last tiles term by term, the tiles between
+    // through their tile sums (each tile is owned by exactly one rank)
+    auto termwise = [&](int64_t a, int64_t b) -> i128 {  // global, clipped to the owned pieces
+        a = max(a, wp.P0);
+        b = min(b, wp.P1 - 1);
+        i128 acc = 0;
+        for (int64_t i = a + lane; i <= b; i += 32) acc += q_term(term_global<KIND>(p, i - g));
+        return warp_sum_i128(acc);
+    };
+    auto clipped = [&](int64_t j0g, int64_t j1g) -> i128 {
+        if (j1g < j0g) return (i128)0;
+        const int64_t ta = j0g / TILE, tb = j1g / TILE;
+        if (ta == tb) return termwise(j0g, j1g);
+        i128 s = termwise(j0g, (ta + 1) * TILE - 1) + termwise(tb * TILE, j1g);
+        const int64_t w0 = max(ta + 1, wp.P0 / TILE), w1 = min(tb, (wp.P1 + TILE - 1) / TILE);  // owned whole tiles
+        if (w1 > w0) {
+            const int64_t l0 = w0 - g / TILE, l1 = w1 - g / TILE;
+            s += join(p.prefix[2 * l1], p.prefix[2 * l1 + 1]) - join(p.prefix[2 * l0], p.prefix[2 * l0 + 1]);
+        }
+        return s;
+    };
+    for (int64_t e = warp; e < nb; e += nwarps) {
+        const int64_t lo = blo[e], hi = bhi[e];
+        i128 acc;
+        if (KIND == DW_SIGNAL_STEP) {
+            const int64_t al = upper_bound_g(p.ts, S, lo) - 1;     // segment holding lo (-1: before the data)
+            const int64_t bl = hi > TS(S) ? S : lower_bound_g(p.ts, S, hi) - 1;  // S: past the data
+            const int64_t ag = al < 0 ? g - 1 : al + g, bg = bl + g;
+            acc = clipped(ag + 1, bg - 1);
+            if (lane == 0) {
+                if (al >= 0 && own(ag)) acc += q_term(__dmul_rn(W(al), (double)(TS(al + 1) - lo)));
+                if (bl < S && own(bg)) acc += q_term(__dmul_rn(W(bl), (double)(min(TS(bl + 1), hi) - TS(bl))));
+            }
+        } else {
+            const int64_t fl = upper_bound_g(p.ts, S, lo);          // first sample > lo (0: at or before the data)
+            const int64_t ll = hi > TS(S - 1) ? S + 1 : lower_bound_g(p.ts, S, hi);  // first sample >= hi
+            const int64_t fg = fl + g, lg = ll + g;
+            acc = clipped(fg, lg - 2);
+            if (lane == 0) {
+                if (fl > 0 && own(fg - 1)) {  // left edge piece [lo, ts[first]]
+                    const int64_t i = (TS(fl - 1) == lo && fl - 1 > 0) ? fl - 2 : fl - 1;  // first bracketing pair
+                    double vlo;
+                    if (lo <= wp.ts0_g) vlo = wp.w0_g;
+                    else if (lo >= wp.tsl_g) vlo = wp.wl_g;
+                    else {
+                        const double wa = W(i);
+                        const double fr = __ddiv_rn((double)(lo - TS(i)), (double)(TS(i + 1) - TS(i)));
+                        vlo = __dadd_rn(wa, __dmul_rn(fr, __dsub_rn(W(i + 1), wa)));
+                    }
+                    acc += q_term(lin_piece(vlo, VS(fl), TS(fl) - lo));
+                }
+                if (ll <= S && own(lg - 1)) {  // right edge piece [ts[last-1], hi]
+                    const int64_t i = ll - 1;
+                    double vh;
+                    if (hi <= wp.ts0_g) vh = wp.w0_g;
+                    else if (hi >= wp.tsl_g) vh = wp.wl_g;
+                    else {
+                        const double wa = W(i);
+                        const double fr = __ddiv_rn((double)(hi - TS(i)), (double)(TS(i + 1) - TS(i)));
+                        vh = __dadd_rn(wa, __dmul_rn(fr, __dsub_rn(W(i + 1), wa)));
+                    }
+                    acc += q_term(lin_piece(VS(i), vh, hi - TS(i)));
+                }
+            }
+        }
+        if (lane == 0) {
+            const I128Parts pp = split(acc);
+            part[2 * e] = pp.lo;
+            part[2 * e + 1] = pp.hi;
+        }
+    }
+}
+
+// exact int128 sum of q(tile_sum) over local tiles [t0, t1) -> out[2]
+__global__ void tile_range_kernel(AttrParams p, int64_t t0, int64_t t1, unsigned long long *out) {
+    if (threadIdx.x != 0) return;
+    const i128 v = join(p.prefix[2 * t1], p.prefix[2 * t1 + 1]) - join(p.prefix[2 * t0], p.prefix[2 * t0 + 1]);
+    const I128Parts pp = split(v);
+    out[0] = pp.lo;
+    out[1] = pp.hi;
+}
+
 // ------------------------------------------------------- K5 sums / finalize
 constexpr int SUM_THREADS = 512;
 // Exact fixed-point sum (2^-64 J) with the last-block-done pattern.
 __global__ void __launch_bounds__(SUM_THREADS) fx_sum_kernel(const double *x, int64_t n,
                                                              unsigned long long *partials,
-                                                             unsigned int *done, double *out) {
+                                                             unsigned int *done, double *out,
+                                                             unsigned long long *out_fx = nullptr) {
     __shared__ unsigned long long red[SUM_THREADS / 32][2];
     __shared__ bool last;
     i128 acc = 0;
@@ -1256,7 +1372,12 @@ __global__ void __launch_bounds__(SUM_THREADS) fx_sum_kernel(const double *x, in
         for (unsigned b = 0; b < gridDim.x; ++b)
             s += join(((volatile unsigned long long *)partials)[2 * b],
                       ((volatile unsigned long long *)partials)[2 * b + 1]);
-        *out = fx_to_double(s, FX_JOULE_BITS);
+        if (out) *out = fx_to_double(s, FX_JOULE_BITS);
+        if (out_fx) {
+            const I128Parts pp = split(s);
+            out_fx[0] = pp.lo;
+            out_fx[1] = pp.hi;
+        }
         *done = 0;  // reusable
     }
 }
@@ -1378,9 +1499,18 @@ static AttrLayout attr_layout(int64_t S, const int64_t *sizes, const int32_t *so
 
 static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
+struct WindowJob {  // dw_attribute_window: work after the tile kernel on the same tile prefix
+    WindowParams wp;
+    const int64_t *blo, *bhi;
+    int64_t nb;
+    unsigned long long *part;  // [2 nb]
+    int64_t t0, t1;            // owned local tiles
+    unsigned long long *tile_fx;  // [2]
+};
+
 static int attribute_impl(const dw_signal_t *sig, dw_interval_set_t *sets, int nsets,
                           void *ws, size_t ws_bytes, cudaStream_t stream, bool ledger,
-                          dw_interval_set_t *ops_for_total) {
+                          dw_interval_set_t *ops_for_total, const WindowJob *wj = nullptr) {
     if (!sig || nsets < 0 || nsets > DW_MAX_SETS || (nsets && !sets) || !ws) return DW_E_ARG;
     if (sig->kind != DW_SIGNAL_STEP && sig->kind != DW_SIGNAL_LINEAR) return DW_E_ARG;
     if (!aligned16(ws)) return DW_E_ARG;
@@ -1484,6 +1614,20 @@ static int attribute_impl(const dw_signal_t *sig, dw_interval_set_t *sets, int n
         long_intervals_kernel<DW_SIGNAL_LINEAR><<<long_grid, 256, 0, stream>>>(p);
     count_launch();
 
+    if (wj) {
+        if (wj->nb > 0) {
+            const unsigned g = (unsigned)std::min<int64_t>(num_sms() * 4, ceil_div(wj->nb * 32, 256));
+            if (sig->kind == DW_SIGNAL_STEP)
+                window_partials_kernel<DW_SIGNAL_STEP><<<g, 256, 0, stream>>>(p, wj->wp, wj->blo, wj->bhi, wj->nb,
+                                                                              wj->part);
+            else
+                window_partials_kernel<DW_SIGNAL_LINEAR><<<g, 256, 0, stream>>>(p, wj->wp, wj->blo, wj->bhi,
+                                                                                wj->nb, wj->part);
+            count_launch();
+        }
+        tile_range_kernel<<<1, 32, 0, stream>>>(p, wj->t0, wj->t1, wj->tile_fx);
+        count_launch();
+    }
     if (ledger) {
         double *op_total = nullptr;
         if (ops_for_total && ops_for_total->n > 0) {
@@ -1531,6 +1675,46 @@ int dw_ledger(const dw_signal_t *sig, dw_interval_set_t *ops, dw_interval_set_t 
     dw_interval_set_t sets[2] = {*ops, *kernels};
     return attribute_impl(sig, sets, 2, d_workspace, workspace_bytes, (cudaStream_t)stream, true,
                           &sets[0]);
+}
+
+int dw_attribute_window(const dw_signal_t *sig, dw_interval_set_t *sets, int32_t nsets, const dw_window_t *win,
+                        const int64_t *d_blo, const int64_t *d_bhi, int64_t nb, int64_t *d_part,
+                        int64_t *d_tile_fx, void *d_workspace, size_t workspace_bytes, dw_stream_t stream) {
+    if (!win || (nb && (!d_blo || !d_bhi || !d_part)) || !d_tile_fx || nb < 0) return DW_E_ARG;
+    if (win->g_off % TILE) return DW_E_ARG;  // the local tile grid must be the global one
+    WindowJob wj{};
+    wj.wp = WindowParams{win->g_off, win->n_samples_global, win->piece_lo, win->piece_hi,
+                         win->ts_first, win->ts_last, win->w_first, win->w_last};
+    wj.blo = d_blo;
+    wj.bhi = d_bhi;
+    wj.nb = nb;
+    wj.part = (unsigned long long *)d_part;
+    const int64_t ntl = ceil_div(sig->n, TILE);
+    wj.t0 = std::min<int64_t>(std::max<int64_t>((win->piece_lo - win->g_off) / TILE, 0), ntl);
+    wj.t1 = std::min<int64_t>(std::max<int64_t>(ceil_div(win->piece_hi - win->g_off, TILE), wj.t0), ntl);
+    wj.tile_fx = (unsigned long long *)d_tile_fx;
+    return attribute_impl(sig, sets, nsets, d_workspace, workspace_bytes, (cudaStream_t)stream, false, nullptr,
+                          &wj);
+}
+
+int dw_fx_sum_exact(const double *d_x, int64_t n, int64_t *d_out_fx, void *d_workspace, size_t ws_bytes,
+                    dw_stream_t stream) {
+    if (n < 0 || !d_out_fx || !d_workspace || ws_bytes < dw_fx_sum_workspace_size(n)) return DW_E_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n == 0) {
+        cudaMemsetAsync(d_out_fx, 0, 16, s);
+        DW_CHECK_LAUNCH();
+        return DW_OK;
+    }
+    char *base = (char *)d_workspace;
+    unsigned blocks = (unsigned)std::min<int64_t>(SUM_BLOCKS, ceil_div(n, SUM_THREADS));
+    unsigned int *done = (unsigned int *)(base + 16 * (size_t)SUM_BLOCKS);
+    cudaMemsetAsync(done, 0, 16, s);
+    fx_sum_kernel<<<blocks, SUM_THREADS, 0, s>>>(d_x, n, (unsigned long long *)base, done, nullptr,
+                                                 (unsigned long long *)d_out_fx);
+    count_launch();
+    DW_CHECK_LAUNCH();
+    return DW_OK;
 }
 
 int dw_status(const void *d_workspace, dw_stream_t stream, dw_status_t *out) {

@@ -47,14 +47,21 @@ def merge_topk(key_hi: torch.Tensor, key_lo: torch.Tensor, k: int, group=None):
                       for r, c in enumerate(counts)])
     pos = torch.cat([torch.arange(int(c.item()), dtype=torch.int64, device=hi.device)
                      for c in counts])
-    # report order: descending hi, then ascending nodes_a tie (upper half of
-    # lo, stored complemented), then corpus order (rank, position) -- LSD with
-    # stable sorts
-    tie_part = (lo >> 32) & 0xFFFFFFFF
+    order = merge_order(hi, lo, rank, pos, k)
+    return rank[order], pos[order]
+
+
+def merge_order(hi: torch.Tensor, lo: torch.Tensor, rank: torch.Tensor, pos: torch.Tensor, k: int,
+                by_finding: bool = False):
+    """Report order of gathered candidates: descending hi, then ascending
+    nodes_a tie (upper half of lo, stored complemented), then corpus order
+    (rank, position) -- LSD with stable sorts.  Returns the first k indices.
+    ``by_finding``: the candidates are findings of ONE pair numbered globally
+    (sharded join), so the whole lo (tie, then finding index) orders ties."""
+    tie_part = _signed(lo) if by_finding else (lo >> 32) & 0xFFFFFFFF
     order = torch.arange(hi.numel(), device=hi.device)
     for key, desc in ((pos, False), (rank, False), (tie_part, True), (_signed(hi), True)):
         kk = key[order]
         idx = torch.sort(kk, descending=desc, stable=True).indices
         order = order[idx]
-    order = order[:k]
-    return rank[order], pos[order]
+    return order[:k]

@@ -1,0 +1,565 @@
+"""Time-window sharding of one trace across ranks.
+
+One process per GPU; rank g owns a contiguous, tile-aligned range of power
+samples and every interval (operator or kernel) whose start falls in it.
+
+    samples   [s_g, s_g+1) owned; the rank holds [s_g - DW_TILE, s_g+1 + H)
+              (H = DW_DIRECT_MAX + 4): one whole tile before (so the local
+              tile grid is the global one) and the halo after that any
+              interval of <= DW_DIRECT_MAX pieces starting in the window needs
+    pieces    [s_g, s_g+1) owned (the last rank: to the end of the signal)
+    intervals owned by the window holding their start; computed whole when
+              they end within the halo (bit-identical to one GPU: the same
+              sequential sum, or the same fixed-point decomposition on the
+              same tile sums); otherwise "crossing" -- necessarily longer than
+              DW_DIRECT_MAX pieces -- and every rank adds the exact int128
+              share of the pieces it owns (K7, csrc/attribute.cu
+              window_partials_kernel).  The shares are all-gathered and summed
+              exactly, then rounded once: the one-GPU value bit for bit.
+    totals    ledger total = exact sum of every rank's owned whole-tile sums;
+              operator_total = exact sum of every rank's 2^-64 J share.
+
+The exchanges are small (crossing intervals are at most the concurrency at
+each window edge) and go through ``Comm`` -- torch.distributed (NCCL on GPU,
+gloo on CPU) or an in-process loopback that runs the ranks one after the other
+(single-GPU parity tests).  The signature join of a sharded pair partitions
+operators by signature hash with one all-to-all (``sharded_join``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import numpy as np
+import torch
+
+from . import _native
+from .energy import SignalError, _raise_interval_error
+
+TILE = 1024
+HALO = _native.DW_DIRECT_MAX + 4
+US_PER_S = 1_000_000
+
+
+# ------------------------------------------------------------------ plan
+
+
+@dataclass(frozen=True)
+class Window:
+    rank: int
+    world: int
+    s0: int          # owned samples [s0, s1)
+    s1: int
+    p0: int          # owned pieces [p0, p1)
+    p1: int
+    l0: int          # held samples [l0, l1)
+    l1: int
+
+
+def plan(n_samples: int, world: int, kind: str) -> list[Window]:
+    """Tile-aligned windows of (nearly) equal sample count."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    if n_samples < 2 * TILE * world:
+        raise ValueError(f"{n_samples} samples are too few to shard over {world} ranks")
+    nterms = n_samples if kind == "step" else n_samples - 1
+    cuts = [0] + [int(round(g * n_samples / world / TILE)) * TILE for g in range(1, world)] + [n_samples]
+    out = []
+    for g in range(world):
+        s0, s1 = cuts[g], cuts[g + 1]
+        p1 = s1 if g < world - 1 else nterms
+        out.append(Window(g, world, s0, s1, s0, p1, max(s0 - TILE, 0), min(s1 + HALO, n_samples)))
+    return out
+
+
+# ----------------------------------------------------------------- comm
+
+
+class Comm:
+    """The two collectives the sharded path needs, over torch.distributed."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_gather_object(self, obj):
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def all_to_all(self, tensors: list[torch.Tensor]) -> list[torch.Tensor]:
+        """tensors[r] goes to rank r; returns what every rank sent here.  NCCL
+        moves device tensors directly (NVLink); gloo stages them on the host."""
+        dev = tensors[0].device
+        if self.dist.get_backend(self.group) == "gloo" and dev.type == "cuda":
+            return [t.to(dev) for t in self.all_to_all([t.cpu() for t in tensors])]
+        sizes = torch.tensor([t.numel() for t in tensors], dtype=torch.int64)
+        sizes_dev = sizes.to(tensors[0].device)
+        recv_sizes = torch.empty_like(sizes_dev)
+        self.dist.all_to_all_single(recv_sizes, sizes_dev, group=self.group)
+        rs = recv_sizes.cpu().tolist()
+        send = torch.cat(tensors)
+        recv = torch.empty(sum(rs), dtype=send.dtype, device=send.device)
+        self.dist.all_to_all_single(recv, send, output_split_sizes=rs, input_split_sizes=sizes.tolist(),
+                                    group=self.group)
+        return list(torch.split(recv, rs))
+
+
+# ------------------------------------------------------------ int128 helpers
+
+
+def _i128(lo: int, hi: int) -> int:
+    return (hi << 64) + (lo & 0xFFFFFFFFFFFFFFFF)
+
+
+def _pairs_to_ints(t: torch.Tensor) -> list[int]:
+    a = t.cpu().numpy().reshape(-1, 2)
+    return [_i128(int(x), int(y)) for x, y in a]
+
+
+def term_fx_to_joules(v: int) -> float:
+    """fx_to_double(v, 40) / 1e6 (csrc/dw_common.cuh): Python's int/int true
+    division is correctly rounded, like the device's fixed-point rounding."""
+    return (v / (1 << 40)) / US_PER_S
+
+
+def joule_fx_to_double(v: int) -> float:
+    return v / (1 << 64)
+
+
+# ---------------------------------------------------------- rank inputs
+
+
+@dataclass
+class RankInputs:
+    """What rank g holds of one trace (numpy or CUDA tensors)."""
+    window: Window
+    kind: str                 # "step" | "linear"
+    ts: torch.Tensor          # samples [l0, l1)
+    watts: torch.Tensor
+    span_hi: int              # STEP: next global sample time (global span end on the last rank)
+    glob: dict                # n_samples, ts_first, ts_last, w_first, w_last, span_lo, span_end
+    sets: list                # per set: dict(idx, start, end) of the owned intervals (global idx)
+
+
+def rank_inputs(cols, kind: str, window: Window, sets=("op", "k")) -> RankInputs:
+    """Carve rank g's inputs out of a full trace (the driver/test path; a
+    deployment reads only its window from the sharded trace files)."""
+    ts, w = cols.device("ts"), cols.device("watts")
+    S = int(ts.numel())
+    first, last = int(ts[0].item()), int(ts[-1].item())
+    span_end = cols.signal_span()[1] if kind == "step" else last
+    g = window
+    lts, lw = ts[g.l0:g.l1], w[g.l0:g.l1]
+    span_hi = int(ts[g.l1].item()) if g.l1 < S else span_end
+    t_lo = int(ts[g.s0].item()) if g.rank > 0 else None
+    t_hi = int(ts[g.s1].item()) if g.rank < g.world - 1 else None
+    out = []
+    for name in sets:
+        st = cols.device(f"{name}_start" if name == "op" else "k_start")
+        en = cols.device(f"{name}_end" if name == "op" else "k_end")
+        own = torch.ones_like(st, dtype=torch.bool)
+        if t_lo is not None:
+            own &= st >= t_lo
+        if t_hi is not None:
+            own &= st < t_hi
+        idx = torch.nonzero(own).flatten()
+        out.append({"idx": idx, "start": st[idx].contiguous(), "end": en[idx].contiguous()})
+    glob = {"n_samples": S, "ts_first": first, "ts_last": last, "w_first": float(w[0].item()),
+            "w_last": float(w[-1].item()), "span_lo": first, "span_end": span_end}
+    return RankInputs(g, kind, lts.contiguous(), lw.contiguous(), span_hi, glob, out)
+
+
+def _safe_end(inp: RankInputs) -> int:
+    """Owned intervals ending at or before this time are computed whole locally."""
+    g = inp.window
+    if g.rank == g.world - 1:
+        return inp.glob["span_end"]
+    return int(inp.ts[g.s1 + _native.DW_DIRECT_MAX - g.l0].item())
+
+
+def crossing(inp: RankInputs) -> list[dict]:
+    """Owned intervals that end beyond the halo (phase 1, rank-local)."""
+    safe = _safe_end(inp)
+    out = []
+    for j, s in enumerate(inp.sets):
+        m = s["end"] > safe
+        out.append({"set": j, "idx": s["idx"][m].cpu(), "start": s["start"][m].cpu(), "end": s["end"][m].cpu()})
+    return out
+
+
+def validate(inp: RankInputs) -> Optional[tuple]:
+    """First invalid owned interval per set (reference error order is op-major)."""
+    lo_ok, hi_ok = inp.glob["span_lo"], inp.glob["span_end"]
+    bad = []
+    for j, s in enumerate(inp.sets):
+        m = (s["end"] < s["start"]) | (s["start"] < lo_ok) | (s["end"] > hi_ok)
+        k = torch.nonzero(m).flatten()
+        bad.append(int(s["idx"][k[0]].item()) if k.numel() else -1)
+    return tuple(bad)
+
+
+@dataclass
+class RankResult:
+    joules: list             # per set: device f64 of the owned intervals computed whole (in inp order)
+    whole: list              # per set: bool mask (inp order) of the intervals computed whole
+    parts: list              # int128 shares of every crossing interval (union order)
+    tile_fx: int             # int128 share of the ledger total
+
+
+def compute(inp: RankInputs, union: list) -> RankResult:
+    """Phase 2 (rank-local, GPU): whole intervals + shares of the crossing ones."""
+    dev = _native.device()
+    L = _native.lib()
+    safe = _safe_end(inp)
+    g = inp.window
+    kinds = {"step": _native.DW_SIGNAL_STEP, "linear": _native.DW_SIGNAL_LINEAR}
+    sig = _native.Signal(_native.ptr(inp.ts), _native.ptr(inp.watts), int(inp.ts.numel()),
+                         int(inp.span_hi), kinds[inp.kind], 0)
+    keep, sets, whole, outs = [], [], [], []
+    for s in inp.sets:
+        m = s["end"] <= safe
+        st, en = s["start"][m].contiguous(), s["end"][m].contiguous()
+        out = torch.empty(st.numel(), dtype=torch.float64, device=dev)
+        keep += [st, en]
+        whole.append(m)
+        outs.append(out)
+        sets.append(_native.IntervalSet(_native.ptr(st), _native.ptr(en), st.numel(), _native.ptr(out),
+                                        1 if bool((st.numel() < 2) or bool((st[1:] >= st[:-1]).all())) else 0, 0))
+    arr = (_native.IntervalSet * max(len(sets), 1))(*sets)
+    blo = torch.cat([u["start"] for u in union]).to(dev) if union else torch.empty(0, dtype=torch.int64, device=dev)
+    bhi = torch.cat([u["end"] for u in union]).to(dev) if union else torch.empty(0, dtype=torch.int64, device=dev)
+    nb = int(blo.numel())
+    part = torch.zeros(max(2 * nb, 2), dtype=torch.int64, device=dev)
+    tile_fx = torch.zeros(2, dtype=torch.int64, device=dev)
+    win = _native.Window(g.l0, inp.glob["n_samples"], g.p0, g.p1, inp.glob["ts_first"], inp.glob["ts_last"],
+                         inp.glob["w_first"], inp.glob["w_last"])
+    sizes = (ctypes.c_int64 * max(len(sets), 1))(*[s.n for s in sets])
+    ws = _native.Workspace.get(L.dw_attribute_workspace_size(sig.n, sizes, len(sets)))
+    stream = _native.stream_handle()
+    _native.check(L.dw_attribute_window(ctypes.byref(sig), arr, len(sets), ctypes.byref(win), _native.ptr(blo),
+                                        _native.ptr(bhi), nb, _native.ptr(part), _native.ptr(tile_fx),
+                                        ws.data_ptr(), ws.numel(), stream), "dw_attribute_window")
+    st = _native.Status()
+    L.dw_status(ws.data_ptr(), stream, ctypes.byref(st))
+    if st.order_index >= 0:
+        from .trace_model import TraceError
+        raise TraceError("power samples must be strictly increasing in timestamp")
+    return RankResult(outs, whole, _pairs_to_ints(part[:2 * nb]) if nb else [], _pairs_to_ints(tile_fx)[0])
+
+
+def _fx_exact(x: torch.Tensor) -> int:
+    L = _native.lib()
+    out = torch.zeros(2, dtype=torch.int64, device=x.device)
+    ws = _native.Workspace.get(L.dw_fx_sum_workspace_size(x.numel()))
+    _native.check(L.dw_fx_sum_exact(_native.ptr(x), x.numel(), _native.ptr(out), ws.data_ptr(), ws.numel(),
+                                    _native.stream_handle()), "dw_fx_sum_exact")
+    return _pairs_to_ints(out)[0]
+
+
+@dataclass
+class ShardLedger:
+    """Rank g's share of a sharded ledger: joules of its owned intervals (global
+    indices ``idx`` per set) plus the global totals (equal on every rank)."""
+    idx: list
+    joules: list
+    total_joules: float
+    op_total: float
+    idle_joules: float
+
+
+def finish(inp: RankInputs, res: RankResult, union: list, all_parts: list, all_tiles: list) -> tuple:
+    """Phase 3 (rank-local): assemble this rank's owned joules from the whole
+    ones and the exactly summed shares of its crossing intervals."""
+    dev = res.joules[0].device if res.joules else _native.device()
+    sums = [sum(p[e] for p in all_parts) for e in range(len(all_parts[0]))] if all_parts and all_parts[0] else []
+    # crossing joules by (set, global index)
+    cross = {}
+    e = 0
+    for u in union:
+        for k in u["idx"].tolist():
+            cross[(u["set"], k)] = term_fx_to_joules(sums[e])
+            e += 1
+    out = []
+    for j, s in enumerate(inp.sets):
+        jl = torch.empty(s["idx"].numel(), dtype=torch.float64, device=dev)
+        m = res.whole[j]
+        jl[m] = res.joules[j]
+        rest = torch.nonzero(~m).flatten().tolist()
+        if rest:
+            gidx = s["idx"][~m].tolist()
+            jl[torch.tensor(rest, device=dev)] = torch.tensor([cross[(j, k)] for k in gidx], dtype=torch.float64,
+                                                                device=dev)
+        out.append(jl)
+    total = term_fx_to_joules(sum(all_tiles))
+    return out, total
+
+
+def _union(all_cross: list) -> list:
+    """Crossing intervals of every rank, in rank order (the same list everywhere)."""
+    return [c for rank_list in all_cross for c in rank_list if c["idx"].numel()]
+
+
+def sharded_ledger(cols, kind: str, comm: Comm, window: Optional[Window] = None,
+                   inputs: Optional[RankInputs] = None) -> ShardLedger:
+    """This rank's part of build_ledger over a time-window-sharded trace (two
+    small all_gather_object exchanges).  ``inputs``: the rank's window,
+    already carved (``rank_inputs``); ``cols`` then only serves error
+    reporting."""
+    if inputs is None:
+        if window is None:
+            window = plan(cols.n_power, comm.world, kind)[comm.rank]
+        inputs = rank_inputs(cols, kind, window)
+    inp = inputs
+    bad = comm.all_gather_object(validate(inp))
+    _raise_first_bad(cols, bad)
+    union = _union(comm.all_gather_object(crossing(inp)))
+    res = compute(inp, union)
+    gathered = comm.all_gather_object((res.parts, res.tile_fx))
+    joules, total = finish(inp, res, union, [g[0] for g in gathered], [g[1] for g in gathered])
+    op_fx = comm.all_gather_object(_fx_exact(joules[0]))
+    op_total = joule_fx_to_double(sum(op_fx))
+    return ShardLedger([s["idx"] for s in inp.sets], joules, total, op_total, max(total - op_total, 0.0))
+
+
+def _raise_first_bad(cols, bad: list) -> None:
+    ops = [b[0] for b in bad if b[0] >= 0]
+    ks = [b[1] for b in bad if b[1] >= 0]
+    if not ops and not ks:
+        return
+    bad_op = min(ops) if ops else -1
+    bad_k = min(ks) if ks else -1
+    owner = None
+    if bad_k >= 0 and cols.k_op is not None:
+        k_op = cols.k_op
+        owner = int(k_op[bad_k].item() if isinstance(k_op, torch.Tensor) else k_op[bad_k])
+    span = cols.signal_span()
+    if bad_op >= 0 and (owner is None or bad_op <= owner):
+        lo, hi = int(cols.device("op_start")[bad_op].item()), int(cols.device("op_end")[bad_op].item())
+    else:
+        lo, hi = int(cols.device("k_start")[bad_k].item()), int(cols.device("k_end")[bad_k].item())
+    _raise_interval_error(lo, hi, span)
+
+
+# ----------------------------------------------------- in-process loopback
+
+
+def sharded_ledger_loopback(cols, kind: str, world: int) -> list[ShardLedger]:
+    """All ranks of ``sharded_ledger`` in one process, one after the other
+    (the collectives become list operations) -- the single-GPU parity check of
+    the multi-GPU decomposition."""
+    wins = plan(cols.n_power, world, kind)
+    inps = [rank_inputs(cols, kind, w) for w in wins]
+    _raise_first_bad(cols, [validate(i) for i in inps])
+    union = _union([crossing(i) for i in inps])
+    res = [compute(i, union) for i in inps]
+    all_parts, all_tiles = [r.parts for r in res], [r.tile_fx for r in res]
+    fin = [finish(i, r, union, all_parts, all_tiles) for i, r in zip(inps, res)]
+    op_total = joule_fx_to_double(sum(_fx_exact(f[0][0]) for f in fin))
+    return [ShardLedger([s["idx"] for s in i.sets], f[0], f[1], op_total, max(f[1] - op_total, 0.0))
+            for i, f in zip(inps, fin)]
+
+
+def gather_ledger(parts: list[ShardLedger], n_ops: int, n_kernels: int):
+    """Reassemble full per-op / per-kernel columns from every rank's share."""
+    dev = parts[0].joules[0].device
+    op = torch.empty(n_ops, dtype=torch.float64, device=dev)
+    k = torch.empty(n_kernels, dtype=torch.float64, device=dev)
+    for p in parts:
+        op[p.idx[0].to(dev)] = p.joules[0].to(dev)
+        k[p.idx[1].to(dev)] = p.joules[1].to(dev)
+    return op, k
+
+
+# ------------------------------------------------------ sharded signature join
+
+
+@dataclass
+class ShardOps:
+    """One side's operators owned by this rank (global indices, increasing)."""
+    idx: torch.Tensor        # int64 global op index
+    sig: torch.Tensor        # int64 (the u64 signature's bits)
+    start: torch.Tensor
+    end: torch.Tensor
+    joules: torch.Tensor     # f64
+    rank: Optional[torch.Tensor] = None   # A side: id rank (report tie-break); None = index
+
+
+def shard_ops(cols, led: ShardLedger, side_a: bool) -> ShardOps:
+    idx = led.idx[0]
+    sig = cols.device("op_sig")
+    sig = sig if sig.dtype == torch.int64 else sig.view(torch.int64)
+    rank = None
+    if side_a:
+        rank = cols.device("op_rank")[idx] if cols.op_rank is not None else idx.clone()
+    return ShardOps(idx, sig[idx].contiguous(), cols.device("op_start")[idx].contiguous(),
+                    cols.device("op_end")[idx].contiguous(), led.joules[0].contiguous(), rank)
+
+
+def _dest(sig: torch.Tensor, world: int) -> torch.Tensor:
+    return ((sig ^ (sig >> 31)) & 0x7FFFFFFF) % world
+
+
+def _pack(o: ShardOps, with_rank: bool) -> torch.Tensor:
+    cols = [o.idx, o.sig, o.start, o.end, o.joules.view(torch.int64)]
+    if with_rank:
+        cols.append(o.rank)
+    return torch.stack(cols, dim=1)
+
+
+def _partition(o: ShardOps, world: int, with_rank: bool) -> list[torch.Tensor]:
+    """Records bound for each rank, in increasing global index."""
+    rec = _pack(o, with_rank)
+    d = _dest(o.sig, world)
+    order = torch.sort(d, stable=True).indices
+    counts = torch.bincount(d, minlength=world).cpu().tolist()
+    return [t.reshape(-1) for t in torch.split(rec[order], counts)]
+
+
+def _unpack(parts: list[torch.Tensor], width: int) -> dict:
+    rec = torch.cat([p.reshape(-1, width) for p in parts]) if parts else torch.empty(0, width, dtype=torch.int64)
+    rec = rec[torch.sort(rec[:, 0]).indices]  # global op order
+    out = {"idx": rec[:, 0].contiguous(), "sig": rec[:, 1].contiguous(), "start": rec[:, 2].contiguous(),
+           "end": rec[:, 3].contiguous(), "joules": rec[:, 4].contiguous().view(torch.float64)}
+    if width == 6:
+        out["rank"] = rec[:, 5].contiguous()
+    return out
+
+
+def _local_join(a: dict, b: dict, threshold: float, k: int):
+    """The one-GPU signature join over this rank's signatures."""
+    from .columns import TraceColumns
+    from .energy import EnergyLedger, JoulesView
+    from .join import join_diff
+    dev = a["sig"].device
+    empty = torch.empty(0, dtype=torch.int64, device=dev)
+
+    def cols(d, rank):
+        return TraceColumns(ts=empty, watts=empty.double(), trace_end=0, op_start=d["start"], op_end=d["end"],
+                            k_start=empty, k_end=empty, op_sig=d["sig"], op_rank=rank, ops_sorted=None,
+                            kernels_sorted=True)
+
+    def led(d):
+        return EnergyLedger(method="samples", per_kernel=JoulesView(None, empty.double(), "k"),
+                        per_operator=JoulesView(None, d["joules"], "op"), idle_joules=0.0, total_joules=0.0)
+
+    ca, cb = cols(a, a["rank"]), cols(b, None)
+    jd = join_diff(ca, cb, led(a), led(b), threshold, k, full_columns=False, epw=False)
+    return jd, ca, cb
+
+
+@dataclass
+class ShardJoinPart:
+    """Phase-2 product of one rank: its top-k candidates with global numbers."""
+    key_hi: torch.Tensor
+    key_lo: torch.Tensor
+    rows: list               # per candidate: (ia, ib, ea, eb, la, lb, ratio, wasted, verdict, side, info)
+    P: int
+    n_waste: int
+    wasted_fx: int
+    b_only_global: list
+
+
+def _local_part(jd, ca, cb, a: dict, b: dict) -> ShardJoinPart:
+    f = jd.order
+    ia_l, ib_l = jd.pair_of(f)
+    has_a, has_b = ia_l >= 0, ib_l >= 0
+    ia = torch.where(has_a, a["idx"][ia_l.clamp(min=0)], torch.full_like(ia_l, -1)) if a["idx"].numel() \
+        else torch.full_like(ia_l, -1)
+    ib = torch.where(has_b, b["idx"][ib_l.clamp(min=0)], torch.full_like(ib_l, -1)) if b["idx"].numel() \
+        else torch.full_like(ib_l, -1)
+    c = jd.columns
+    zf = torch.zeros((), dtype=torch.float64, device=f.device)
+    zi = torch.zeros((), dtype=torch.int64, device=f.device)
+    ea = torch.where(has_a, a["joules"][ia_l.clamp(min=0)], zf) if a["idx"].numel() else zf.expand_as(f)
+    eb = torch.where(has_b, b["joules"][ib_l.clamp(min=0)], zf) if b["idx"].numel() else zf.expand_as(f)
+    la = torch.where(has_a, (a["end"] - a["start"])[ia_l.clamp(min=0)], zi) if a["idx"].numel() else zi.expand_as(f)
+    lb = torch.where(has_b, (b["end"] - b["start"])[ib_l.clamp(min=0)], zi) if b["idx"].numel() else zi.expand_as(f)
+    tie = torch.where(has_a, a["rank"][ia_l.clamp(min=0)], torch.full_like(f, -1)) if a["idx"].numel() \
+        else torch.full_like(f, -1)
+    waste = c.verdict[: jd.P] == VERDICT_WASTE_I8
+    wasted_fx = _fx_exact(c.wasted[: jd.P][waste].contiguous()) if jd.P else 0
+    b_only_global = b["idx"][jd.b_only.to(torch.int64)].cpu().tolist() if jd.n_b_only else []
+    rows = list(zip(ia.cpu().tolist(), ib.cpu().tolist(), ea.cpu().tolist(), eb.cpu().tolist(),
+                    la.cpu().tolist(), lb.cpu().tolist(), c.ratio[f].cpu().tolist(), c.wasted[f].cpu().tolist(),
+                    c.verdict[f].cpu().tolist(), c.side[f].cpu().tolist(), c.informational[f].cpu().tolist()))
+    return ShardJoinPart(c.key_hi[f], None, rows, jd.P, int(waste.sum().item()), wasted_fx, b_only_global), tie
+
+
+VERDICT_WASTE_I8 = 2
+
+
+def _global_lo(part: ShardJoinPart, tie: torch.Tensor, n_a: int, b_only_sorted: list) -> torch.Tensor:
+    """key_lo = ~((tie + 1) << 32 | f) with the GLOBAL finding number f: the A
+    op index, or n_a + the position of the B op among all B-only ops."""
+    import bisect
+    f = []
+    for r in part.rows:
+        if r[0] >= 0:
+            f.append(r[0])
+        else:
+            f.append(n_a + bisect.bisect_left(b_only_sorted, r[1]))
+    f = torch.tensor(f, dtype=torch.int64, device=tie.device)
+    return ~(((tie + 1) << 32) | f)
+
+
+@dataclass
+class ShardJoinResult:
+    P: int
+    n_waste: int
+    wasted_joules: float
+    top: list                # rows in report order (global op indices)
+
+
+def sharded_join(A: ShardOps, B: ShardOps, n_a: int, comm: Comm, threshold: float = 0.10,
+                 k: int = 100) -> ShardJoinResult:
+    """Signature join of a time-window-sharded pair: operators go to the rank
+    of hash(signature) (one all-to-all, NCCL on GPU), where every occurrence
+    of their signature meets in global op order -- so the local join pairs
+    exactly as the one-GPU join.  Local top-k candidates carry global finding
+    numbers and merge over the ranks (dist.merge_order)."""
+    from .dist import merge_order
+    a = _unpack(comm.all_to_all(_partition(A, comm.world, True)), 6)
+    b = _unpack(comm.all_to_all(_partition(B, comm.world, False)), 5)
+    jd, ca, cb = _local_join(a, b, threshold, k)
+    part, tie = _local_part(jd, ca, cb, a, b)
+    b_only_sorted = sorted(x for lst in comm.all_gather_object(part.b_only_global) for x in lst)
+    lo = _global_lo(part, tie, n_a, b_only_sorted)
+    gathered = comm.all_gather_object((part.key_hi.cpu(), lo.cpu(), part.rows, part.P, part.n_waste,
+                                       part.wasted_fx))
+    return _merge(gathered, k)
+
+
+def _merge(gathered: list, k: int) -> ShardJoinResult:
+    from .dist import merge_order
+    hi = torch.cat([g[0] for g in gathered])
+    lo = torch.cat([g[1] for g in gathered])
+    rank = torch.cat([torch.full((len(g[2]),), r, dtype=torch.int64) for r, g in enumerate(gathered)])
+    pos = torch.cat([torch.arange(len(g[2]), dtype=torch.int64) for g in gathered])
+    order = merge_order(hi, lo, rank, pos, k, by_finding=True)
+    top = [gathered[int(rank[i])][2][int(pos[i])] for i in order.tolist()]
+    return ShardJoinResult(sum(g[3] for g in gathered), sum(g[4] for g in gathered),
+                           joule_fx_to_double(sum(g[5] for g in gathered)), top)
+
+
+def sharded_join_loopback(As: list, Bs: list, n_a: int, threshold: float = 0.10, k: int = 100) -> ShardJoinResult:
+    """Every rank of ``sharded_join`` in one process (single-GPU parity check)."""
+    world = len(As)
+    sends_a = [_partition(x, world, True) for x in As]
+    sends_b = [_partition(x, world, False) for x in Bs]
+    parts, ties = [], []
+    for r in range(world):
+        a = _unpack([sends_a[s][r] for s in range(world)], 6)
+        b = _unpack([sends_b[s][r] for s in range(world)], 5)
+        jd, ca, cb = _local_join(a, b, threshold, k)
+        p, t = _local_part(jd, ca, cb, a, b)
+        parts.append(p)
+        ties.append(t)
+    b_only_sorted = sorted(x for p in parts for x in p.b_only_global)
+    gathered = [(p.key_hi.cpu(), _global_lo(p, t, n_a, b_only_sorted).cpu(), p.rows, p.P, p.n_waste, p.wasted_fx)
+                for p, t in zip(parts, ties)]
+    return _merge(gathered, k)
