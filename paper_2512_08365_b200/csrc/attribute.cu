@@ -467,6 +467,7 @@ struct __align__(16) GroupSmem {  // private to one consumer group
     int nvalid;
     double red[NCW];
     int64_t kq[DW_MAX_SETS];  // per set: interval index = kq + chunk index
+    int4 desc[DW_MAX_SETS];   // per set: smem base, staged limit, first staged slot
     int next_it;              // the group's claimed next tile (sequence position)
 };
 
@@ -598,6 +599,18 @@ __device__ __forceinline__ bool phase1_item(const uint32_t *ts, const double *w,
     }
 }
 
+// Per-set item descriptors of the chunk starting at c0 (one thread per set):
+// item q of set j sits at smem index desc.x + q if q < desc.y (staged), and
+// is interval kq + q of the set.
+__device__ __forceinline__ void set_desc(const StageMeta &M, GroupSmem &so, int j, int64_t c0) {
+    const int64_t kq = M.f0[j] - M.c[j] + c0;            // interval index = kq + q
+    const int64_t base = M.pool[j] + (kq - M.a0[j]);     // smem index = base + q
+    const int64_t lim = M.a0[j] + M.copied[j] - kq;      // staged iff q < lim
+    so.kq[j] = kq;
+    auto clamp30 = [](int64_t v) -> int { return (int)(v < -(1LL << 30) ? -(1LL << 30) : (v > (1LL << 30) ? (1LL << 30) : v)); };
+    so.desc[j] = make_int4(clamp30(base), clamp30(lim), M.pool[j], 0);
+}
+
 template <int KIND>
 __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSmem &so, int stage,
                                       int64_t tile, const TileCtx &cx, int ctid, int g,
@@ -626,27 +639,35 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
             cb2 = rel(M.c[2]);
             cb3 = rel(M.c[3]);
         }
+        const int64_t *s_lo = sm.iv_lo[stage], *s_hi = sm.iv_hi[stage];
         for (int q = ctid; q < nch; q += ATTR_THREADS) {
             const int j = (q >= cb1) + (q >= cb2) + (q >= cb3);
-            const int64_t k = M.f0[j] - M.c[j] + c0 + q;
-            const int64_t idx = k - M.a0[j];  // staged index
-            const bool staged = idx < M.copied[j];
-            const int pool = M.pool[j];
-            const int64_t *gs_lo = p.start[j];
+            const int4 d = so.desc[j];  // {smem base, staged limit, smem first of the set}
+            const int si = d.x + q;
+            const bool staged = q < d.y;
             int64_t glo, ghi;
             if (staged) {
-                glo = sm.iv_lo[stage][pool + idx];
-                ghi = sm.iv_hi[stage][pool + idx];
+                glo = s_lo[si];
+                ghi = s_hi[si];
             } else {
-                glo = __ldg(gs_lo + k);
+                const int64_t k = so.kq[j] + q;
+                glo = __ldg(p.start[j] + k);
                 ghi = __ldg(p.end[j] + k);
             }
-            if (p.check_sorted[j] && k > 0) {  // a set flagged sorted must be sorted by start
-                const int64_t prev = staged && idx > 0 ? sm.iv_lo[stage][pool + idx - 1] : __ldg(gs_lo + k - 1);
-                if (prev > glo) atomic_min_index(&p.st->unsorted_index[j], k);
+            if (p.check_sorted[j]) {  // a set flagged sorted must be sorted by start
+                int64_t prev;
+                bool has_prev = true;
+                if (staged && si > d.z) {
+                    prev = s_lo[si - 1];
+                } else {
+                    const int64_t k = so.kq[j] + q;
+                    has_prev = k > 0;
+                    prev = has_prev ? __ldg(p.start[j] + k - 1) : glo;
+                }
+                if (has_prev && prev > glo) atomic_min_index(&p.st->unsorted_index[j], so.kq[j] + q);
             }
             if (ghi < glo || glo < cx.span_lo || ghi > cx.span_hi) {
-                report_bad(p, j, k);
+                report_bad(p, j, so.kq[j] + q);
                 so.meta[q] = META_NONE;
                 continue;
             }
@@ -657,7 +678,7 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
             int s, cnt, last;
             if (!phase1_item<KIND>(ts, w, r0, r1, cnt_win, lo, hi, glo <= cx.ts0, glo >= cx.tsl,
                                    ghi <= cx.ts0, ghi >= cx.tsl, cx, F0, L, s, cnt, last)) {
-                push_long(p, j, k);
+                push_long(p, j, so.kq[j] + q);
                 so.meta[q] = META_NONE;
                 continue;
             }
@@ -666,7 +687,6 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
             so.meta[q] = pack_meta(q, s, cnt, last, j);
             atomicAdd(&so.hist[cnt], 1);
         }
-        if (ctid < DW_MAX_SETS) so.kq[ctid] = (ctid < nsets ? M.f0[ctid] - M.c[ctid] : 0) + c0;
         consumer_sync(g);
         PROF(3);
 #ifdef DW_EXP_P1_ONLY
@@ -733,6 +753,7 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
             p.out[j][oidx] = div_1e6(tot);
         }
         for (int b = ctid; b < NBUCKET; b += ATTR_THREADS) so.hist[b] = 0;
+        if (ctid < DW_MAX_SETS && c0 + CHUNK < total) set_desc(M, so, ctid, c0 + CHUNK);
         consumer_sync(g);
         PROF(6);
     }
@@ -760,46 +781,49 @@ __device__ __forceinline__ void producer(const AttrParams &p, TileSmem &sm, int6
             fl[j] = ok ? __ldg(p.first + j * nb + tl) : 0;
             fh[j] = ok ? __ldg(p.first + j * nb + tl + 1) : 0;
         }
+        // lane u stages the u-th tile of the batch from its own registers
         for (int u = 0; u < 32; ++u) {
             const int it = itb + NPROD * u;
             const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
             if (tile >= p.ntiles) break;
-            int64_t f0s[DW_MAX_SETS], f1s[DW_MAX_SETS];
-#pragma unroll
-            for (int j = 0; j < DW_MAX_SETS; ++j) {
-                f0s[j] = __shfl_sync(0xffffffffu, fl[j], u);
-                f1s[j] = __shfl_sync(0xffffffffu, fh[j], u);
-            }
-            const int stage = it % STAGES;
-            StageMeta &M = sm.meta[stage];
-            int64_t wb, we;
-            tile_window(tile, S, wb, we);
-            const int cnt = (int)(we - wb);
-            const int even = cnt & ~1;
-            if (lane == 0) {
+            if (lane == u) {
+                const int stage = it % STAGES;
+                StageMeta &M = sm.meta[stage];
+                int64_t wb, we;
+                tile_window(tile, S, wb, we);
+                const int cnt = (int)(we - wb);
+                const int even = cnt & ~1;
                 uint32_t bytes = 2u * 8u * (uint32_t)even;
+                int64_t a0s[DW_MAX_SETS];
+                int ms[DW_MAX_SETS], pools[DW_MAX_SETS];
+                int pool = 0;
+#pragma unroll
+                for (int j = 0; j < DW_MAX_SETS; ++j) {
+                    const int64_t f0 = fl[j], f1 = fh[j];
+                    const int64_t a0 = f0 & ~(int64_t)1;
+                    const int64_t want = f1 > f0 ? f1 - a0 : 0;
+                    const int64_t room = IV_POOL - pool;
+                    const int m = (int)(want < room ? want : room) & ~1;
+                    a0s[j] = a0;
+                    ms[j] = m;
+                    pools[j] = pool;
+                    pool += m;
+                    bytes += 2u * 8u * (uint32_t)m;
+                }
                 PROF(8);
                 if (it >= STAGES) mbar_wait(&sm.empty[stage], (uint32_t)(((it / STAGES) - 1) & 1));
                 PROF(7);
                 fence_proxy_async();
                 M.wb = wb;
                 M.cnt = cnt;
-                int pool = 0;
                 M.c[0] = 0;
 #pragma unroll
                 for (int j = 0; j < DW_MAX_SETS; ++j) {
-                    const int64_t f0 = f0s[j], f1 = f1s[j];
-                    const int64_t a0 = f0 & ~(int64_t)1;
-                    int64_t want = f1 > f0 ? f1 - a0 : 0;
-                    int64_t room = IV_POOL - pool;
-                    int m = (int)(want < room ? want : room) & ~1;
-                    M.f0[j] = f0;
-                    M.c[j + 1] = M.c[j] + (f1 - f0);
-                    M.a0[j] = a0;
-                    M.copied[j] = m;
-                    M.pool[j] = pool;
-                    pool += m;
-                    bytes += 2u * 8u * (uint32_t)m;
+                    M.f0[j] = fl[j];
+                    M.c[j + 1] = M.c[j] + (fh[j] - fl[j]);
+                    M.a0[j] = a0s[j];
+                    M.copied[j] = ms[j];
+                    M.pool[j] = pools[j];
                 }
                 if (cnt & 1) {  // odd tail of the window: not a 16-byte multiple
                     sm.ts[stage][cnt - 1] = __ldg(p.ts + wb + cnt - 1);
@@ -807,21 +831,16 @@ __device__ __forceinline__ void producer(const AttrParams &p, TileSmem &sm, int6
                 }
                 if (wb + cnt == S) sm.ts[stage][cnt] = span_hi;  // virtual end of the last segment
                 mbar_expect_tx(&sm.full[stage], bytes);
-            }
-            __syncwarp();
-            // lane 0: timestamps, lane 1: watts, lanes 2 + 2j / 3 + 2j: set j's starts / ends
-            if (lane < 2) {
-                if (even) tma_load_1d(lane ? (void *)sm.w[stage] : (void *)sm.ts[stage],
-                                      lane ? (const void *)(p.w + wb) : (const void *)(p.ts + wb), 8u * even,
-                                      &sm.full[stage]);
-            } else if (lane < 2 + 2 * p.nsets) {
-                const int j = (lane - 2) >> 1;
-                const int m = M.copied[j];
-                if (m) {
-                    const bool hi_col = (lane - 2) & 1;
-                    int64_t *dst = hi_col ? &sm.iv_hi[stage][M.pool[j]] : &sm.iv_lo[stage][M.pool[j]];
-                    const int64_t *src = (hi_col ? p.end[j] : p.start[j]) + M.a0[j];
-                    tma_load_1d(dst, src, 8u * m, &sm.full[stage]);
+                if (even) {
+                    tma_load_1d(sm.ts[stage], p.ts + wb, 8u * even, &sm.full[stage]);
+                    tma_load_1d(sm.w[stage], p.w + wb, 8u * even, &sm.full[stage]);
+                }
+#pragma unroll
+                for (int j = 0; j < DW_MAX_SETS; ++j) {
+                    if (j < p.nsets && ms[j]) {
+                        tma_load_1d(&sm.iv_lo[stage][pools[j]], p.start[j] + a0s[j], 8u * ms[j], &sm.full[stage]);
+                        tma_load_1d(&sm.iv_hi[stage][pools[j]], p.end[j] + a0s[j], 8u * ms[j], &sm.full[stage]);
+                    }
                 }
             }
             __syncwarp();
@@ -958,6 +977,7 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_tiles_kernel(AttrParams
             for (int r = r0 + ctid; r < r1 && wb + r + 1 < S; r += ATTR_THREADS)
                 if (s_ts[r + 1] <= s_ts[r]) atomic_min_index(&p.st->order_index, wb + r);
         }
+        if (ctid < DW_MAX_SETS) set_desc(M, gs, ctid, 0);  // published by the next barrier
         if (!wide) {
             // (a) 32-bit relative timestamps, two per thread
             for (int r = 2 * ctid; r <= last; r += 2 * ATTR_THREADS) {
