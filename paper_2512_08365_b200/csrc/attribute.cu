@@ -466,8 +466,8 @@ struct __align__(16) GroupSmem {  // private to one consumer group
     int hist[NBUCKET];
     int nvalid;
     double red[NCW];
-    int64_t kq[DW_MAX_SETS];  // per set: interval index = kq + chunk index
-    int4 desc[DW_MAX_SETS];   // per set: smem base, staged limit, first staged slot
+    int64_t kq[2][DW_MAX_SETS];  // per chunk parity, per set: interval index = kq + chunk index
+    int4 desc[2][DW_MAX_SETS];   // per chunk parity, per set: smem base, staged limit, first staged slot
     int next_it;              // the group's claimed next tile (sequence position)
 };
 
@@ -603,12 +603,13 @@ __device__ __forceinline__ bool phase1_item(const uint32_t *ts, const double *w,
 // item q of set j sits at smem index desc.x + q if q < desc.y (staged), and
 // is interval kq + q of the set.
 __device__ __forceinline__ void set_desc(const StageMeta &M, GroupSmem &so, int j, int64_t c0) {
+    const int par = (int)((c0 / CHUNK) & 1);  // double-buffered: the previous chunk's phase 2 may still read
     const int64_t kq = M.f0[j] - M.c[j] + c0;            // interval index = kq + q
     const int64_t base = M.pool[j] + (kq - M.a0[j]);     // smem index = base + q
     const int64_t lim = M.a0[j] + M.copied[j] - kq;      // staged iff q < lim
-    so.kq[j] = kq;
+    so.kq[par][j] = kq;
     auto clamp30 = [](int64_t v) -> int { return (int)(v < -(1LL << 30) ? -(1LL << 30) : (v > (1LL << 30) ? (1LL << 30) : v)); };
-    so.desc[j] = make_int4(clamp30(base), clamp30(lim), M.pool[j], 0);
+    so.desc[par][j] = make_int4(clamp30(base), clamp30(lim), M.pool[j], 0);
 }
 
 template <int KIND>
@@ -640,9 +641,12 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
             cb3 = rel(M.c[3]);
         }
         const int64_t *s_lo = sm.iv_lo[stage], *s_hi = sm.iv_hi[stage];
+        const int par = (int)((c0 / CHUNK) & 1);
+        const int4 *cdesc = so.desc[par];
+        const int64_t *ckq = so.kq[par];
         for (int q = ctid; q < nch; q += ATTR_THREADS) {
             const int j = (q >= cb1) + (q >= cb2) + (q >= cb3);
-            const int4 d = so.desc[j];  // {smem base, staged limit, smem first of the set}
+            const int4 d = cdesc[j];  // {smem base, staged limit, smem first of the set}
             const int si = d.x + q;
             const bool staged = q < d.y;
             int64_t glo, ghi;
@@ -650,7 +654,7 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
                 glo = s_lo[si];
                 ghi = s_hi[si];
             } else {
-                const int64_t k = so.kq[j] + q;
+                const int64_t k = ckq[j] + q;
                 glo = __ldg(p.start[j] + k);
                 ghi = __ldg(p.end[j] + k);
             }
@@ -660,14 +664,14 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
                 if (staged && si > d.z) {
                     prev = s_lo[si - 1];
                 } else {
-                    const int64_t k = so.kq[j] + q;
+                    const int64_t k = ckq[j] + q;
                     has_prev = k > 0;
                     prev = has_prev ? __ldg(p.start[j] + k - 1) : glo;
                 }
-                if (has_prev && prev > glo) atomic_min_index(&p.st->unsorted_index[j], so.kq[j] + q);
+                if (has_prev && prev > glo) atomic_min_index(&p.st->unsorted_index[j], ckq[j] + q);
             }
             if (ghi < glo || glo < cx.span_lo || ghi > cx.span_hi) {
-                report_bad(p, j, so.kq[j] + q);
+                report_bad(p, j, ckq[j] + q);
                 so.meta[q] = META_NONE;
                 continue;
             }
@@ -678,7 +682,7 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
             int s, cnt, last;
             if (!phase1_item<KIND>(ts, w, r0, r1, cnt_win, lo, hi, glo <= cx.ts0, glo >= cx.tsl,
                                    ghi <= cx.ts0, ghi >= cx.tsl, cx, F0, L, s, cnt, last)) {
-                push_long(p, j, so.kq[j] + q);
+                push_long(p, j, ckq[j] + q);
                 so.meta[q] = META_NONE;
                 continue;
             }
@@ -748,7 +752,7 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
             for (int u = 0; u < cnt; ++u) tot = __dadd_rn(tot, tp[u]);
 #endif
             if ((mt >> 29) & 1u) tot = __dadd_rn(tot, so.L[qi]);
-            const int64_t k = so.kq[j] + qi;
+            const int64_t k = ckq[j] + qi;
             const int64_t oidx = p.perm[j] ? __ldg(p.perm[j] + k) : k;
             p.out[j][oidx] = div_1e6(tot);
         }
