@@ -443,21 +443,6 @@ __global__ void __launch_bounds__(PAIR_THREADS) join_pair_bucket_kernel(
     }
 }
 
-__global__ void join_pair_scatter_kernel(const uint2 *stage, int64_t na, int32_t *match_a) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * ITEMS;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS + threadIdx.x; base < na; base += stride) {
-        uint2 e[ITEMS];
-#pragma unroll
-        for (int u = 0; u < ITEMS; ++u) {
-            const int64_t q = base + (int64_t)u * blockDim.x;
-            e[u] = q < na ? __ldcs(stage + q) : make_uint2(0xFFFFFFFFu, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < ITEMS; ++u)
-            if (e[u].x != 0xFFFFFFFFu) match_a[e[u].x] = (int32_t)e[u].y;
-    }
-}
-
 // B operators beyond A's occurrence count of their signature: B-only
 __global__ void join_bonly_kernel(const uint32_t *db, const uint32_t *xb, int64_t nb, const int32_t *first_b,
                                   const int32_t *first_a, const int32_t *end_a, int32_t *b_only,
@@ -480,42 +465,97 @@ __device__ __forceinline__ double div_or_same(double e, const double *work, int6
     return work ? __ddiv_rn(e, work[i]) : e;
 }
 
-// findings of A's operators (matched or A-only), in A order
-__global__ void join_findings_a_kernel(int64_t na, const int32_t *match_a, JoinSideDev A,
-                                       JoinSideDev B, double threshold, FindCols o, double *epw_a,
-                                       double *epw_b, unsigned long long *n_matched) {
-    const int64_t base = (int64_t)blockIdx.x * blockDim.x * ITEMS + threadIdx.x;
-    int32_t j[ITEMS];
-    double ea[ITEMS], eb[ITEMS];
-    int64_t la[ITEMS], lb[ITEMS], tie[ITEMS];
+// Pass 1.5 and 2 of the pairing write-back, fused with the A-side findings.
+// Pass 1.5 re-partitions every bucket of the stage by window (i >> WIN_BSH,
+// 16384 A ops) -- again with known window sizes, so window w owns
+// stage2[w << WIN_BSH, ...).  Pass 2 gives each window to one CTA: it lays the
+// window's partners out in shared memory, then walks the window's A ops in
+// order -- coalesced match_a writes, coalesced A-side reads, the verdict, and
+// coalesced finding columns -- with only the B-side reads random.
+constexpr int WIN_BSH = 14;
+constexpr int WIN_OPS = 1 << WIN_BSH;
+constexpr int SUB_CHUNK = 4096;  // divides 1 << PAIR_BSH: a chunk never straddles buckets
+constexpr int WF_THREADS = 512;
+
+__global__ void __launch_bounds__(256) join_pair_sub_kernel(const uint2 *stage, int64_t na, unsigned int *cursor2,
+                                                            uint2 *stage2) {
+    constexpr int NSUB = 1 << (PAIR_BSH - WIN_BSH);
+    __shared__ int hist[NSUB];
+    __shared__ int base[NSUB];
+    const int64_t c0 = (int64_t)blockIdx.x * SUB_CHUNK;
+    const int64_t b = c0 >> PAIR_BSH;
+    for (int k = threadIdx.x; k < NSUB; k += 256) hist[k] = 0;
+    __syncthreads();
+    constexpr int PER = SUB_CHUNK / 256;
+    uint2 e[PER];
+    int r[PER];
 #pragma unroll
-    for (int u = 0; u < ITEMS; ++u) {
-        const int64_t i = base + (int64_t)u * blockDim.x;
-        const bool in = i < na;
-        j[u] = in ? __ldcs(match_a + i) : -1;
-        ea[u] = in ? __ldcs(A.joules + i) : 0.0;
-        la[u] = in ? __ldcs(A.end + i) - __ldcs(A.start + i) : 0;
-        tie[u] = in && A.rank ? __ldcs(A.rank + i) : i;
+    for (int u = 0; u < PER; ++u) {
+        const int64_t q = c0 + (int64_t)u * 256 + threadIdx.x;
+        e[u] = q < na ? __ldcs(stage + q) : make_uint2(0, 0);
+        r[u] = q < na ? atomicAdd(&hist[(e[u].x >> WIN_BSH) & (NSUB - 1)], 1) : 0;
     }
+    __syncthreads();
+    for (int k = threadIdx.x; k < NSUB; k += 256)
+        base[k] = hist[k] ? (int)atomicAdd(cursor2 + (b << (PAIR_BSH - WIN_BSH)) + k, (unsigned)hist[k]) : 0;
+    __syncthreads();
 #pragma unroll
-    for (int u = 0; u < ITEMS; ++u) {
-        eb[u] = 0.0;
-        lb[u] = 0;
-        if (j[u] >= 0) {
-            eb[u] = B.joules[j[u]];
-            lb[u] = B.end[j[u]] - B.start[j[u]];
-        }
+    for (int u = 0; u < PER; ++u) {
+        const int64_t q = c0 + (int64_t)u * 256 + threadIdx.x;
+        if (q >= na) continue;
+        const int64_t w = e[u].x >> WIN_BSH;
+        stage2[(w << WIN_BSH) + base[w & (NSUB - 1)] + r[u]] = e[u];
     }
+}
+
+__global__ void __launch_bounds__(WF_THREADS) join_window_findings_kernel(
+    const uint2 *stage2, int64_t na, int32_t *match_a, JoinSideDev A, JoinSideDev B, double threshold, FindCols o,
+    double *epw_a, double *epw_b, unsigned long long *n_matched) {
+    extern __shared__ int32_t jw[];  // [WIN_OPS]
+    const int64_t i0 = (int64_t)blockIdx.x << WIN_BSH;
+    const int n = (int)(na - i0 < (int64_t)WIN_OPS ? na - i0 : (int64_t)WIN_OPS);
+    for (int q = threadIdx.x; q < n; q += WF_THREADS) {
+        const uint2 e = __ldcs(stage2 + i0 + q);
+        jw[e.x - (uint32_t)i0] = (int32_t)e.y;
+    }
+    __syncthreads();
+    constexpr int U = 4;
     unsigned cnt = 0;
+    for (int q0 = threadIdx.x; q0 < n; q0 += WF_THREADS * U) {
+        int32_t j[U];
+        double ea[U], eb[U];
+        int64_t la[U], lb[U], tie[U];
 #pragma unroll
-    for (int u = 0; u < ITEMS; ++u) {
-        const int64_t i = base + (int64_t)u * blockDim.x;
-        if (i >= na) continue;
-        const Verdict v = judge(ea[u], eb[u], la[u], lb[u], 0.0, threshold);
-        store_finding(o, i, ea[u], eb[u], la[u], lb[u], v, tie[u]);
-        if (epw_a) epw_a[i] = div_or_same(ea[u], A.work, i);
-        if (epw_b) epw_b[i] = j[u] >= 0 ? div_or_same(eb[u], B.work, j[u]) : 0.0;
-        cnt += j[u] >= 0;
+        for (int u = 0; u < U; ++u) {
+            const int q = q0 + u * WF_THREADS;
+            const int64_t i = i0 + q;
+            const bool in = q < n;
+            j[u] = in ? jw[q] : -1;
+            ea[u] = in ? __ldcs(A.joules + i) : 0.0;
+            la[u] = in ? __ldcs(A.end + i) - __ldcs(A.start + i) : 0;
+            tie[u] = in && A.rank ? __ldcs(A.rank + i) : i;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            eb[u] = 0.0;
+            lb[u] = 0;
+            if (j[u] >= 0) {
+                eb[u] = B.joules[j[u]];
+                lb[u] = B.end[j[u]] - B.start[j[u]];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int q = q0 + u * WF_THREADS;
+            if (q >= n) continue;
+            const int64_t i = i0 + q;
+            match_a[i] = j[u];
+            const Verdict v = judge(ea[u], eb[u], la[u], lb[u], 0.0, threshold);
+            store_finding(o, i, ea[u], eb[u], la[u], lb[u], v, tie[u]);
+            if (epw_a) epw_a[i] = div_or_same(ea[u], A.work, i);
+            if (epw_b) epw_b[i] = j[u] >= 0 ? div_or_same(eb[u], B.work, j[u]) : 0.0;
+            cnt += j[u] >= 0;
+        }
     }
     for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
     if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n_matched, (unsigned long long)cnt);
@@ -695,7 +735,7 @@ static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, const 
 struct JoinLayout {
     size_t table, counters, id_a, id_b, ix_a, ix_b, sid_a, sid_b, six_a, six_b, first_a, end_a,
         first_b, end_b,
-        bonly_tmp, pair_stage, pair_cursor, cub, cub_bytes, total;
+        bonly_tmp, pair_stage, pair_cursor, win_stage, win_cursor, cub, cub_bytes, total;
     int64_t cap, D;
 };
 
@@ -728,6 +768,8 @@ static JoinLayout join_layout(int64_t na, int64_t nb, int64_t max_distinct) {
     L.bonly_tmp = off; off += au(4 * std::max<int64_t>(nb, 1));
     L.pair_stage = off; off += au(8 * std::max<int64_t>(na, 1));
     L.pair_cursor = off; off += au(4 * PAIR_MAXB);
+    L.win_stage = off; off += au(8 * std::max<int64_t>(na, 1));
+    L.win_cursor = off; off += au(4 * ((std::max<int64_t>(na, 1) + WIN_OPS - 1) / WIN_OPS));
     size_t c1 = 0, c2 = 0;
     const int64_t nmax = std::max<int64_t>(std::max(na, nb), 1);
     cub::DeviceRadixSort::SortPairs(nullptr, c1, (const uint32_t *)nullptr, (uint32_t *)nullptr,
@@ -858,10 +900,13 @@ int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_d
         join_pair_bucket_kernel<<<blocks_for(na, PAIR_THREADS * PAIR_ITEMS), PAIR_THREADS, 0, s>>>(
             sid_a, six_a, na, first_a, six_b, first_b, end_b, cursor, stage);
         trace_mark(s, "join:pair_bucket");
-        join_pair_scatter_kernel<<<(unsigned)std::min<int64_t>(num_sms() * 8, blocks_for(na, 256 * ITEMS)), 256, 0,
-                                   s>>>(stage, na, d_match_a);
-        count_launch(2);
-        trace_mark(s, "join:pair_scatter");
+        unsigned int *cursor2 = (unsigned int *)(base + L.win_cursor);
+        uint2 *stage2 = (uint2 *)(base + L.win_stage);
+        const int64_t nwin = (na + WIN_OPS - 1) / WIN_OPS;
+        cudaMemsetAsync(cursor2, 0, 4 * nwin, s);
+        join_pair_sub_kernel<<<(unsigned)((na + SUB_CHUNK - 1) / SUB_CHUNK), 256, 0, s>>>(stage, na, cursor2, stage2);
+        count_launch(1);
+        trace_mark(s, "join:pair_sub");
     }
     int32_t *bonly_tmp = (int32_t *)(base + L.bonly_tmp);
     if (nb) {
@@ -885,8 +930,12 @@ int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_d
     JoinSideDev B{b->d_start, b->d_end, b->d_rank, b->d_joules, b->d_work};
     FindCols o = cols_of(out);
     if (na) {
-        join_findings_a_kernel<<<blocks_for(na, 256 * ITEMS), 256, 0, s>>>(na, d_match_a, A, B, threshold, o,
-                                                                            d_epw_a, d_epw_b, counters + 1);
+        const uint2 *stage2 = (const uint2 *)(base + L.win_stage);
+        const int64_t nwin = (na + WIN_OPS - 1) / WIN_OPS;
+        const size_t smem = 4 * (size_t)WIN_OPS;
+        cudaFuncSetAttribute(join_window_findings_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        join_window_findings_kernel<<<(unsigned)nwin, WF_THREADS, smem, s>>>(stage2, na, d_match_a, A, B, threshold,
+                                                                            o, d_epw_a, d_epw_b, counters + 1);
         count_launch();
         trace_mark(s, "join:findings_a");
     }
