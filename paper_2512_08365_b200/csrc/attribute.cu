@@ -437,21 +437,22 @@ __device__ __forceinline__ void tile_intervals(const AttrParams &p, const TileSm
     }
 }
 
-// ---- narrow tiles: precomputed terms, two phases, counting sort by length ----
+// ---- narrow tiles: precomputed terms, two phases ----
 // Pass A writes the window's 32-bit relative timestamps (group smem) and then
 // every interior integrand term of the tile's pieces into the stage's int64
 // timestamp slots (no longer needed once ts32 exists); the tile sum is folded
-// from those same terms.  Phase 1 finds, per interval, its first piece a and
-// its interior-term count, and evaluates the two edge pieces (the only ones
-// that depend on lo / hi: the interpolated endpoint values and their
-// divisions).  A counting sort by interior count hands equal-length intervals
-// to the lanes of a warp, and phase 2 folds F0 + term[a+1] + ... + L in the
-// reference's order: one shared load and one dependent add per step.
+// from those same terms.  Phase 1 (concurrent with the terms: it only needs
+// ts32) finds, per interval, its first piece a and its interior-term count,
+// and evaluates the two edge pieces (the only ones that depend on lo / hi:
+// the interpolated endpoint values and their divisions).  Phase 2 folds
+// F0 + term[a+1] + ... + L in the reference's order: one shared load and one
+// dependent add per step.  (A counting sort by length to cut lane divergence
+// in phase 2 was measured and dropped: on C4 its histogram, scan, scatter and
+// two extra barriers cost more than the divergence it removes.)
 #ifndef DW_CHUNK
 #define DW_CHUNK 512
 #endif
 constexpr int CHUNK = DW_CHUNK;  // intervals per phase-1/phase-2 round
-constexpr int NBUCKET = DIRECT + 2;
 
 // item meta: q (chunk index, 10 bits) | s (first interior term, 11 bits) << 10 |
 //            cnt (interior terms, 9 bits) << 21 | has_last << 30
@@ -462,9 +463,6 @@ struct __align__(16) GroupSmem {  // private to one consumer group
     double F0[CHUNK];    // first piece (0.0 + first piece for the trapezoid)
     double L[CHUNK];     // last piece
     uint32_t meta[CHUNK];
-    int16_t order[CHUNK];
-    int hist[NBUCKET];
-    int nvalid;
     double red[NCW];
     int64_t kq[2][DW_MAX_SETS];  // per chunk parity, per set: interval index = kq + chunk index
     int4 desc[2][DW_MAX_SETS];   // per chunk parity, per set: smem base, staged limit, first staged slot
@@ -613,7 +611,7 @@ __device__ __forceinline__ void set_desc(const StageMeta &M, GroupSmem &so, int 
 }
 
 template <int KIND>
-__device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSmem &so, int stage,
+__device__ void tile_intervals_two_pass(const AttrParams &p, TileSmem &sm, GroupSmem &so, int stage,
                                       int64_t tile, const TileCtx &cx, int ctid, int g,
                                       long long &prof_t) {
     const StageMeta &M = sm.meta[stage];
@@ -658,6 +656,7 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
                 glo = __ldg(p.start[j] + k);
                 ghi = __ldg(p.end[j] + k);
             }
+#ifndef DW_EXP_NOCHECK
             if (p.check_sorted[j]) {  // a set flagged sorted must be sorted by start
                 int64_t prev;
                 bool has_prev = true;
@@ -675,6 +674,7 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
                 so.meta[q] = META_NONE;
                 continue;
             }
+#endif
             const uint32_t lo = (uint32_t)(glo - cx.base);
             const int64_t dh = ghi - cx.base;
             const uint32_t hi = dh > 0xFFFFFFFFLL ? 0xFFFFFFFFu : (uint32_t)dh;
@@ -689,74 +689,30 @@ __device__ void tile_intervals_sorted(const AttrParams &p, TileSmem &sm, GroupSm
             so.F0[q] = F0;
             so.L[q] = L;
             so.meta[q] = pack_meta(q, s, cnt, last, j);
-            atomicAdd(&so.hist[cnt], 1);
+
         }
         consumer_sync(g);
         PROF(3);
 #ifdef DW_EXP_P1_ONLY
-        for (int b = ctid; b < NBUCKET; b += ATTR_THREADS) so.hist[b] = 0;
         consumer_sync(g);
         continue;
 #endif
-        // ---- exclusive scan of the length histogram (warp 0)
-        if (ctid < 32) {
-            constexpr int PER = (NBUCKET + 31) / 32;
-            int loc[PER];
-            int sacc = 0;
-#pragma unroll
-            for (int u = 0; u < PER; ++u) {
-                int b = ctid * PER + u;
-                loc[u] = b < NBUCKET ? so.hist[b] : 0;
-                sacc += loc[u];
-            }
-            int incl = sacc;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (ctid >= o) incl += t;
-            }
-            int run = incl - sacc;
-#pragma unroll
-            for (int u = 0; u < PER; ++u) {
-                int b = ctid * PER + u;
-                if (b < NBUCKET) so.hist[b] = run;
-                run += loc[u];
-            }
-            if (ctid == 31) so.nvalid = incl;
-        }
-        consumer_sync(g);
-        PROF(4);
-        // ---- scatter: bucket order
+        // ---- phase 2: the interior folds, items in chunk order
         for (int q = ctid; q < nch; q += ATTR_THREADS) {
             const uint32_t mt = so.meta[q];
-            if (mt != META_NONE) so.order[atomicAdd(&so.hist[(mt >> 20) & 511u], 1)] = (int16_t)q;
-        }
-        consumer_sync(g);
-        PROF(5);
-        // ---- phase 2: equal-length intervals side by side
-        const int nvalid = so.nvalid;
-        for (int q = ctid; q < nvalid; q += ATTR_THREADS) {
-#ifdef DW_EXP_NOSORT
-            const int qi = q;
-#else
-            const int qi = so.order[q];
-#endif
-            const uint32_t mt = so.meta[qi];
+            if (mt == META_NONE) continue;
             const int s = (int)((mt >> 9) & 2047u);
             const int cnt = (int)((mt >> 20) & 511u);
             const int j = (int)(mt >> 30);
-            double tot = so.F0[qi];
+            double tot = so.F0[q];
             const double *tp = term + s;
-#ifndef DW_EXP_NOLOOP
 #pragma unroll 4
             for (int u = 0; u < cnt; ++u) tot = __dadd_rn(tot, tp[u]);
-#endif
-            if ((mt >> 29) & 1u) tot = __dadd_rn(tot, so.L[qi]);
-            const int64_t k = ckq[j] + qi;
+            if ((mt >> 29) & 1u) tot = __dadd_rn(tot, so.L[q]);
+            const int64_t k = ckq[j] + q;
             const int64_t oidx = p.perm[j] ? __ldg(p.perm[j] + k) : k;
             p.out[j][oidx] = div_1e6(tot);
         }
-        for (int b = ctid; b < NBUCKET; b += ATTR_THREADS) so.hist[b] = 0;
         if (ctid < DW_MAX_SETS && c0 + CHUNK < total) set_desc(M, so, ctid, c0 + CHUNK);
         consumer_sync(g);
         PROF(6);
@@ -924,8 +880,6 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_tiles_kernel(AttrParams
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int g = 0; g < GROUPS; ++g)
-        for (int b = tid; b < NBUCKET; b += blockDim.x) groups[g].hist[b] = 0;
     if (tid < GROUPS) groups[tid].next_it = tid;
     if (tid == 0) sm.claim = GROUPS;
     __syncthreads();
@@ -1001,13 +955,12 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_tiles_kernel(AttrParams
             for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
             if ((ctid & 31) == 0) gs.red[ctid >> 5] = acc;
             PROF(2);
+            if (M.c[DW_MAX_SETS] == 0) consumer_sync(g);  // no intervals: red must still be visible
 #ifdef DW_EXP_PASSA_ONLY
             consumer_sync(g);
 #else
-            if (M.c[DW_MAX_SETS] == 0) consumer_sync(g);  // no intervals: red must still be visible
-            tile_intervals_sorted<KIND>(p, sm, gs, stage, tile, cx, ctid, g, prof_t);
+            tile_intervals_two_pass<KIND>(p, sm, gs, stage, tile, cx, ctid, g, prof_t);
 #endif
-            // (the first barrier inside published red[]; the last closed the tile)
             if (ctid == 0) {
                 double t = gs.red[0];
 #pragma unroll
