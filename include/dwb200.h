@@ -161,6 +161,18 @@ size_t dw_attribute_split_workspace_size(int64_t n_samples, int64_t n);
 int dw_attribute_split(const dw_signal_t *sig, dw_interval_set_t *set, void *d_workspace,
                        size_t workspace_bytes, dw_stream_t stream);
 
+/* Replay estimator (energy.py:196-256) for n_ops operators [start, end) of a
+ * STEP ground truth: each op's power profile tiled `repeat` times, read by the
+ * delayed sampler every period_us with the per-read delays d_delays (the
+ * caller draws them: numpy PCG64 uniform(0.5, 1.5) x delay, the same stream
+ * for every op, energy.py:160-165), mid-window reads averaged (Python sum()).
+ * Out: d_watts[o] (steady power), d_joules[o] = watts * duration / 1e6.
+ * *d_bad = first op whose profile is empty (the reference's SignalError),
+ * INT64_MAX if none. */
+int dw_replay(const dw_signal_t *truth, const int64_t *d_op_start, const int64_t *d_op_end, int64_t n_ops,
+              int64_t repeat, int64_t period_us, const double *d_delays, int64_t n_delays, double *d_watts,
+              double *d_joules, int64_t *d_bad, dw_stream_t stream);
+
 /* Synchronise `stream` and copy the status block out of the workspace. Returns
  * status->code. */
 int dw_status(const void *d_workspace, dw_stream_t stream, dw_status_t *status);

@@ -118,6 +118,37 @@ def split(kind, ts, watts, span_hi, lo, hi):
     return out
 
 
+def replay_delays(n: int, delay_us: int, seed: int) -> np.ndarray:
+    """The sampler's per-sample delays (energy.py:160-165): a fresh numpy
+    PCG64 stream per call, uniform in [0.5, 1.5] x delay_us; zeros without
+    delay.  rng.uniform(a, b, size=n) equals n scalar draws."""
+    if not delay_us:
+        return np.zeros(max(n, 1))
+    rng = np.random.default_rng(seed)
+    return rng.uniform(0.5 * delay_us, 1.5 * delay_us, size=max(n, 1))
+
+
+def replay(ts, watts, span_hi, op_start, op_end, repeat=1000, period_us=40_000, delay_us=200_000, seed=0):
+    """replay_estimate restated for every operator (energy.py:196-256):
+    (watts, joules) per op."""
+    ts = np.ascontiguousarray(ts, dtype=np.int64)
+    watts = np.ascontiguousarray(watts, dtype=np.float64)
+    op_start = np.ascontiguousarray(op_start, dtype=np.int64)
+    op_end = np.ascontiguousarray(op_end, dtype=np.int64)
+    dmax = int((op_end - op_start).max()) if op_start.size else 0
+    delays = replay_delays(repeat * dmax // period_us + 2, delay_us, seed)
+    w_out = np.empty(op_start.shape[0])
+    j_out = np.empty(op_start.shape[0])
+    bad = ctypes.c_int64(-1)
+    rc = lib().dwo_replay(_p(ts), _p(watts), ctypes.c_int64(ts.shape[0]), ctypes.c_int64(int(span_hi)),
+                          _p(op_start), _p(op_end), ctypes.c_int64(op_start.shape[0]), ctypes.c_int64(repeat),
+                          ctypes.c_int64(period_us), _p(delays), ctypes.c_int64(delays.shape[0]), _p(w_out),
+                          _p(j_out), ctypes.byref(bad))
+    if rc:
+        raise OracleError(rc, bad.value)
+    return w_out, j_out
+
+
 def total_device(kind, ts, watts, span_hi=None) -> float:
     """The ledger total over the whole span under the device's definition."""
     ts = np.ascontiguousarray(ts, dtype=np.int64)

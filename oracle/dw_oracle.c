@@ -680,3 +680,79 @@ int dwo_split(int kind, const int64_t *ts, const double *w, int64_t n, int64_t s
     free(ev); free(x); free(c); free(es); free(P);
     return rc;
 }
+
+/* ------------------------------------------------------- replay estimator
+ * replay_estimate (energy.py:196-256) for every operator, restated: the op's
+ * truth profile tiled `repeat` times, read by the delayed sampler
+ * (energy.py:144-171; the delays are the numpy stream, drawn by the caller:
+ * every op restarts the same seeded stream, so one array serves all ops),
+ * mid-window samples averaged with Python's sum().  Truth: breakpoints
+ * ts/w with the last segment ending at span_hi.  Returns DW_OK or
+ * DW_E_EMPTY with *bad = the first op whose profile is empty (the reference's
+ * "sample_signal requires a ground-truth signal"). */
+static double replay_value(const int64_t *ts, const double *w, int64_t n, int64_t span_hi, int64_t start,
+                           int64_t d, int64_t repeat, int64_t i0, int64_t i1, int64_t p0s, int64_t ple,
+                           double x) {
+    /* tiled segments: tile k, truth segment i in [i0, i1]:
+       [k d + max(ts_i, start) - start, k d + min(end_i, start + d) - start) */
+    const double sr = (double)p0s, er = (double)((repeat - 1) * d + ple);
+    if (x < sr) x = sr;
+    if (x > er) x = er;
+    int64_t k = (int64_t)(x / (double)d);
+    if (k < 0) k = 0;
+    if (k > repeat - 1) k = repeat - 1;
+    while (k > 0 && (double)(k * d + p0s) > x) k--;
+    while (k < repeat - 1 && (double)((k + 1) * d + p0s) <= x) k++;
+    const int64_t base = k * d - start;
+    for (int64_t i = i0; i <= i1; i++) {  /* first containing segment */
+        int64_t s = ts[i] > start ? ts[i] : start;
+        int64_t e = i + 1 < n ? ts[i + 1] : span_hi;
+        if (e > start + d) e = start + d;
+        if ((double)(base + s) <= x && x < (double)(base + e)) return w[i];
+    }
+    return w[i1]; /* no containing segment: the last tiled segment's watts */
+}
+
+int dwo_replay(const int64_t *ts, const double *w, int64_t n, int64_t span_hi, const int64_t *op_start,
+               const int64_t *op_end, int64_t nops, int64_t repeat, int64_t period, const double *delays,
+               int64_t ndelays, double *watts_out, double *joules_out, int64_t *bad) {
+    for (int64_t o = 0; o < nops; o++) {
+        const int64_t start = op_start[o], end = op_end[o], d = end - start;
+        /* truth segments overlapping [start, end) */
+        int64_t i0 = -1, i1 = -1;
+        for (int64_t i = 0; i < n; i++) {
+            int64_t s = ts[i], e = i + 1 < n ? ts[i + 1] : span_hi;
+            int64_t lo = s > start ? s : start, hi = e < end ? e : end;
+            if (hi > lo) { if (i0 < 0) i0 = i; i1 = i; }
+        }
+        if (i0 < 0) { if (bad) *bad = o; return DW_E_EMPTY; }
+        const int64_t p0s = (ts[i0] > start ? ts[i0] : start) - start;
+        int64_t ple = (i1 + 1 < n ? ts[i1 + 1] : span_hi);
+        if (ple > end) ple = end;
+        ple -= start;
+        const int64_t sr = p0s, er = (repeat - 1) * d + ple;
+        const double total = (double)(repeat * d);
+        const double lo_m = 0.1 * total, hi_m = (1.0 - 0.1) * total;
+        py_sum_t mid, all;
+        memset(&mid, 0, sizeof(mid));
+        memset(&all, 0, sizeof(all));
+        int64_t nmid = 0, nall = 0, di = 0;
+        for (int64_t t = sr + period; t <= er; t += period) {
+            const double dl = di < ndelays ? delays[di] : 0.0;
+            di++;
+            const double v = replay_value(ts, w, n, span_hi, start, d, repeat, i0, i1, p0s, ple, (double)t - dl);
+            py_sum_add(&all, v); nall++;
+            if (lo_m <= (double)t && (double)t <= hi_m) { py_sum_add(&mid, v); nmid++; }
+        }
+        if (nall == 0) {  /* span shorter than one period: one read at the end */
+            const double dl = ndelays ? delays[0] : 0.0;
+            const double v = replay_value(ts, w, n, span_hi, start, d, repeat, i0, i1, p0s, ple, (double)er - dl);
+            py_sum_add(&all, v); nall++;
+            if (lo_m <= (double)er && (double)er <= hi_m) { py_sum_add(&mid, v); nmid++; }
+        }
+        const double wt = nmid ? py_sum_result(&mid) / (double)nmid : py_sum_result(&all) / (double)nall;
+        watts_out[o] = wt;
+        joules_out[o] = wt * (double)d / 1000000.0;
+    }
+    return DW_OK;
+}

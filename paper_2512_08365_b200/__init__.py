@@ -27,12 +27,15 @@ from .columns import TraceColumns  # noqa: F401
 from .energy import (  # noqa: F401
     EnergyLedger,
     PowerSignal,
+    ReplayEstimate,
     SignalError,
     build_ledger,
     ground_truth_signal,
     integrate,
     integrate_many,
+    integrate_split,
     mean_power,
+    replay_estimate,
     sample_signal,
     sampled_view,
 )

@@ -515,6 +515,143 @@ def _read_pair(cols, a, b, i):
     return int(x[i]), int(y[i])
 
 
+# ------------------------------------------------------------------ replay
+
+
+@dataclass(frozen=True)
+class ReplayEstimate:
+    op_id: str
+    watts: float
+    joules: float
+    repeat: int
+    samples_used: int
+
+
+def _sampler_delays(n: int, delay_us: int, seed: int) -> np.ndarray:
+    """The delayed sampler's per-sample delays (energy.py:160-165): every
+    replay restarts the seeded numpy stream, so one array serves all ops
+    (rng.uniform(a, b, size=n) draws exactly what n scalar calls draw)."""
+    if not delay_us:
+        return np.zeros(max(n, 1))
+    return np.random.default_rng(seed).uniform(0.5 * delay_us, 1.5 * delay_us, size=max(n, 1))
+
+
+def _replay_device(truth: PowerSignal, starts, ends, repeat, period_us, delay_us, seed):
+    """dw_replay over operators [starts, ends): (watts, joules) device tensors."""
+    dev = _native.device()
+    s_d = _to_dev(starts, torch.int64, dev).reshape(-1)
+    e_d = _to_dev(ends, torch.int64, dev).reshape(-1)
+    n = int(s_d.numel())
+    dmax = int((e_d - s_d).max().item()) if n else 0
+    delays = torch.from_numpy(_sampler_delays(repeat * dmax // period_us + 2, delay_us, seed)).to(dev)
+    watts = torch.empty(n, dtype=torch.float64, device=dev)
+    joules = torch.empty(n, dtype=torch.float64, device=dev)
+    bad = torch.empty(1, dtype=torch.int64, device=dev)
+    csig, keep = truth._c_signal()
+    L = _native.lib()
+    _native.check(L.dw_replay(ctypes.byref(csig), _native.ptr(s_d), _native.ptr(e_d), n, int(repeat),
+                              int(period_us), _native.ptr(delays), int(delays.numel()), _native.ptr(watts),
+                              _native.ptr(joules), _native.ptr(bad), _native.stream_handle()), "dw_replay")
+    b = int(bad.item())
+    if 0 <= b < (1 << 62):
+        raise SignalError("sample_signal requires a ground-truth signal")
+    return watts, joules
+
+
+def _replay_checks(cols: TraceColumns, repeat: int, first_op: int = 0) -> None:
+    """replay_estimate's argument errors in build_ledger's op order
+    (energy.py:227-230): an op without kernels, then repeat < 1."""
+    k_op = cols.k_op if cols.k_op is not None else np.zeros(0, dtype=np.int32)
+    k_op = k_op.cpu().numpy() if isinstance(k_op, torch.Tensor) else np.asarray(k_op)
+    has = np.zeros(cols.n_ops, dtype=bool)
+    has[k_op.astype(np.int64)] = True
+    missing = np.nonzero(~has[first_op:])[0]
+    first_missing = int(missing[0]) + first_op if missing.size else None
+    if first_missing == first_op:
+        oid = cols.op_ids[first_missing] if cols.op_ids is not None else f"op{first_missing}"
+        raise SignalError(f"operator {oid!r} launched no kernels; nothing to replay")
+    if repeat < 1:
+        raise SignalError("repeat must be >= 1")
+    if first_missing is not None:
+        oid = cols.op_ids[first_missing] if cols.op_ids is not None else f"op{first_missing}"
+        raise SignalError(f"operator {oid!r} launched no kernels; nothing to replay")
+
+
+def _replay_ledger(cols: TraceColumns, truth: PowerSignal, repeat, period_us, delay_us, seed) -> EnergyLedger:
+    """build_ledger(method="replay") (energy.py:306-311, 318-319): per-op
+    replay estimates, kernels at their op's steady watts, total = the ground
+    truth over the span, idle = max(total - sum, 0)."""
+    _replay_checks(cols, repeat)
+    cols.wait_ready()
+    tsig = PowerSignal.from_columns(cols.device("ts"), cols.device("watts"), truth._span_hi, "step")
+    watts, per_op = _replay_device(tsig, cols.device("op_start"), cols.device("op_end"), repeat, period_us,
+                                   delay_us, seed)
+    k_op = cols.device("k_op").to(torch.int64) if cols.n_kernels else None
+    kdur = (cols.device("k_end") - cols.device("k_start")).to(torch.float64)
+    # tensor / tensor: an IEEE division per element (a scalar divisor may be
+    # turned into a reciprocal multiply)
+    per_k = torch.div(watts[k_op] * kdur, torch.full_like(kdur, float(US_PER_S))) if cols.n_kernels else kdur
+    empty = cols.device("op_start")[:0]
+    totals = _span_total(tsig, empty)
+    op_total = _fx_sum(per_op)
+    return EnergyLedger(method="replay", per_kernel=JoulesView(cols.k_ids, per_k, "k"),
+                        per_operator=JoulesView(cols.op_ids, per_op, "op"),
+                        idle_joules=max(totals - op_total, 0.0), total_joules=totals, op_total=op_total)
+
+
+def _span_total(sig: PowerSignal, empty: torch.Tensor) -> float:
+    """The ledger total over the whole span (dw_ledger with no intervals)."""
+    L = _native.lib()
+    e = _native.IntervalSet(_native.ptr(empty), _native.ptr(empty), 0, 0, 1, 0)
+    csig, keep = sig._c_signal()
+    sizes = (ctypes.c_int64 * 2)(0, 0)
+    ws = _native.Workspace.get(L.dw_attribute_workspace_size(csig.n, sizes, 2))
+    stream = _native.stream_handle()
+    _native.check(L.dw_ledger(ctypes.byref(csig), ctypes.byref(e), ctypes.byref(e), ws.data_ptr(), ws.numel(),
+                              stream), "dw_ledger")
+    st = _native.Status()
+    L.dw_status(ws.data_ptr(), stream, ctypes.byref(st))
+    return float(st.totals[0])
+
+
+def replay_estimate(trace, op_id: str, repeat: int = DEFAULT_REPLAY_REPEAT,
+                    period_us: int = DEFAULT_SAMPLER_PERIOD_US, delay_us: int = DEFAULT_SAMPLER_DELAY_US,
+                    seed: int = 0) -> ReplayEstimate:
+    """Estimate one operator's steady power by replaying it back to back
+    (energy.py:208-256) -- the replay kernel on one operator."""
+    cols = TraceColumns.from_trace(trace)
+    ids = list(cols.op_ids) if cols.op_ids is not None else [f"op{i}" for i in range(cols.n_ops)]
+    try:
+        i = ids.index(op_id)
+    except ValueError:
+        raise KeyError(op_id) from None
+    k_op = cols.k_op.cpu().numpy() if isinstance(cols.k_op, torch.Tensor) else np.asarray(
+        cols.k_op if cols.k_op is not None else [], dtype=np.int64)
+    if not np.any(k_op == i):
+        raise SignalError(f"operator {op_id!r} launched no kernels; nothing to replay")
+    if repeat < 1:
+        raise SignalError("repeat must be >= 1")
+    truth = ground_truth_signal(cols)
+    tsig = PowerSignal.from_columns(cols.device("ts"), cols.device("watts"), truth._span_hi, "step")
+    lo, hi = int(_host(cols.op_start)[i]), int(_host(cols.op_end)[i])
+    watts, joules = _replay_device(tsig, np.array([lo]), np.array([hi]), repeat, period_us, delay_us, seed)
+    # samples used: the mid-window reads (energy.py:245-248)
+    ts = _host(cols.ts)
+    d = hi - lo
+    a = max(int(np.searchsorted(ts, lo, side="right")) - 1, 0)
+    b = int(np.searchsorted(ts, hi, side="left")) - 1
+    p0s = max(int(ts[a]), lo) - lo
+    seg_end_b = int(ts[b + 1]) if b + 1 < len(ts) else truth._span_hi
+    ple = min(seg_end_b, hi) - lo
+    sr, er = p0s, (repeat - 1) * d + ple
+    total = float(repeat * d)
+    lo_m, hi_m = 0.1 * total, (1.0 - 0.1) * total
+    t = np.arange(sr + period_us, er + 1, period_us, dtype=np.int64) if er >= sr + period_us else np.array([er])
+    used = int(np.count_nonzero((lo_m <= t) & (t <= hi_m))) or int(t.size)
+    return ReplayEstimate(op_id=op_id, watts=float(watts.item()), joules=float(joules.item()), repeat=repeat,
+                          samples_used=used)
+
+
 def _split_ledger(method: str, cols: TraceColumns, signal: PowerSignal, st) -> EnergyLedger:
     """Split-mode ledger: the compat pass above validated the intervals and
     integrated the span (total); here each set is split among its concurrently
@@ -574,8 +711,7 @@ def build_ledger(trace, method: str = "ground_truth",
                             op_total=float(st.totals[1]))
     truth = ground_truth_signal(cols)
     if method == "replay":
-        raise NotImplementedError(
-            "method='replay' (energy.py:196-256) is not on the device yet (SURVEY.md 8(f)2)")
+        return _replay_ledger(cols, truth, repeat, period_us, delay_us, seed)
     if method == "ground_truth":
         cols.wait_ready()
         signal = PowerSignal.from_columns(cols.device("ts"), cols.device("watts"),

@@ -8,6 +8,9 @@ records its outputs on seeded inputs into small fixtures under tests/golden/:
                              ``energy.integrate`` joules (src/energy.py:90-104)
 * ``integrate_linear.npz`` - random sample sets + intervals -> reference
                              ``energy._integrate_samples`` (src/energy.py:108-130)
+* ``replay.npz``           - reference ``build_ledger(method="replay")``
+                             (src/energy.py:196-256, 306-311) on the sampler
+                             demo trace and presets, several sampler settings
 * ``scenarios/*.npz``      - simulator presets + fuzz/null corpora: SoA columns
                              of both traces, reference ledgers
                              (src/energy.py:280-331), reference segment pairs
@@ -358,8 +361,38 @@ def trace_vectors(ref):
         json.dump(out, fh, indent=1, sort_keys=True)
 
 
+def replay_vectors(ref):
+    """Reference build_ledger(method="replay") (src/energy.py:196-256, 306-311)
+    on the sampler demo trace and the presets, for several sampler settings:
+    SoA columns + per-op / per-kernel joules + total / idle."""
+    out = {}
+    cases = [("demo", ref.simulate.sampler_demo_traces()[0])]
+    for preset in ("tf32_misconfig", "join_redundant", "attention_block"):
+        cases.append((preset, ref.simulate.generate(ref.simulate.preset(preset))[0]))
+    for i, m in enumerate(ref.simulate.fuzz(20260808, 4)):
+        cases.append((f"fuzz{i}", ref.simulate.generate(m)[1]))
+    settings = [("d", dict()), ("s2r100", dict(seed=2, repeat=100)),
+                ("nodelay", dict(delay_us=0, period_us=5000, repeat=50)),
+                ("fast", dict(period_us=1000, delay_us=300, repeat=7, seed=5))]
+    names = []
+    for name, tr in cases:
+        out.update(trace_columns(ref, tr, name))
+        for tag, kw in settings:
+            led = ref.energy.build_ledger(tr, method="replay", **kw)
+            out.update(ledger_columns(tr, led, f"{name}_{tag}"))
+            names.append(f"{name}:{tag}")
+    out["cases"] = np.array([c[0] for c in cases])
+    out["settings"] = np.array(json.dumps(settings))
+    return out
+
+
 def main():
     ref = _import_reference()
+    if "--replay" in sys.argv:
+        t0 = time.time()
+        np.savez_compressed(OUT / "replay.npz", **replay_vectors(ref))
+        print(f"replay done [{time.time() - t0:.1f}s]")
+        return
     if "--traces" in sys.argv:
         trace_vectors(ref)
         return

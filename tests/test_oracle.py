@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import oracle
-from conftest import load_scenario, pair_tuples, scenario_names
+from conftest import GOLDEN, load_scenario, pair_tuples, scenario_names
 
 
 def _nsegs_step(ts, span_hi, lo, hi):
@@ -186,3 +186,25 @@ def test_split_conserves_union_energy(kind):
     union = f(np.array(ulo), np.array(uhi)).sum()
     assert got.sum() == pytest.approx(union, rel=1e-9)
     assert np.all(got >= 0)
+
+
+# --------------------------------------------- replay estimator (golden)
+
+def _replay_cases():
+    import json
+    z = np.load(GOLDEN / "replay.npz")
+    settings = json.loads(str(z["settings"]))
+    for c in z["cases"]:
+        for tag, kw in settings:
+            yield str(c), tag, kw
+
+
+@pytest.mark.parametrize("case,tag,kw", list(_replay_cases()))
+def test_replay_oracle_bit_exact_vs_reference(case, tag, kw):
+    z = np.load(GOLDEN / "replay.npz")
+    ts, w, span = z[f"{case}_ts"], z[f"{case}_watts"], z[f"{case}_span"]
+    kw = {"repeat": 1000, "period_us": 40_000, "delay_us": 200_000, "seed": 0, **kw}
+    watts, joules = oracle.replay(ts, w, span[1], z[f"{case}_op_start"], z[f"{case}_op_end"], **kw)
+    np.testing.assert_array_equal(joules, z[f"{case}_{tag}_per_op"])
+    kdur = z[f"{case}_k_end"] - z[f"{case}_k_start"]
+    np.testing.assert_array_equal(watts[z[f"{case}_k_op"]] * kdur / 1_000_000, z[f"{case}_{tag}_per_k"])
