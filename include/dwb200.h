@@ -173,6 +173,14 @@ int dw_replay(const dw_signal_t *truth, const int64_t *d_op_start, const int64_t
               int64_t repeat, int64_t period_us, const double *d_delays, int64_t n_delays, double *d_watts,
               double *d_joules, int64_t *d_bad, dw_stream_t stream);
 
+/* Packed columns: a sorted int64 column stored
+ * as base + uint32 deltas (d_delta[0] is 0 or the offset of the first value)
+ * decodes to d_out[i] = base + sum(d_delta[0..i]); with d_dur, also
+ * d_end[i] = d_out[i] + d_dur[i] (interval ends from durations). */
+size_t dw_unpack_workspace_size(int64_t n);
+int dw_unpack_deltas(const uint32_t *d_delta, int64_t n, int64_t base, int64_t *d_out, const uint32_t *d_dur,
+                     int64_t *d_end, void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
+
 /* Synchronise `stream` and copy the status block out of the workspace. Returns
  * status->code. */
 int dw_status(const void *d_workspace, dw_stream_t stream, dw_status_t *status);

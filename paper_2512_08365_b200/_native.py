@@ -39,6 +39,7 @@ DW_DIRECT_MAX = 256
 EXPORTED = (
     "dw_attribute_workspace_size", "dw_attribute", "dw_ledger", "dw_status",
     "dw_attribute_split_workspace_size", "dw_attribute_split", "dw_attribute_window", "dw_fx_sum_exact", "dw_replay",
+    "dw_unpack_workspace_size", "dw_unpack_deltas",
     "dw_fx_sum_workspace_size", "dw_fx_sum", "dw_step_value_at", "dw_detect_pairs",
     "dw_rank_workspace_size", "dw_rank", "dw_join_workspace_size", "dw_join_diff",
     "dw_version", "dw_error_string", "dw_launch_count", "dw_kernel_timing", "dw_kernel_time_ms",
@@ -122,6 +123,9 @@ def lib():
                                           ctypes.POINTER(Window), c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
                                           ctypes.c_size_t, c_vp]
         L.dw_fx_sum_exact.argtypes = [c_vp, c_i64, c_vp, c_vp, ctypes.c_size_t, c_vp]
+        L.dw_unpack_workspace_size.restype = ctypes.c_size_t
+        L.dw_unpack_workspace_size.argtypes = [c_i64]
+        L.dw_unpack_deltas.argtypes = [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp]
         L.dw_replay.argtypes = [ctypes.POINTER(Signal), c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp,
                                 c_vp, c_vp]
         L.dw_attribute_split_workspace_size.restype = ctypes.c_size_t

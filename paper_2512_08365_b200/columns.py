@@ -206,3 +206,191 @@ class TraceColumns:
 
 _CACHE: dict = {}
 _CACHE_MAX = 32
+
+
+# ------------------------------------------------------------- packed columns
+
+
+class PackedColumns(TraceColumns):
+    """A trace whose sorted timestamp columns travel as 32-bit deltas and whose
+    interval ends travel as 32-bit durations.
+
+    Host bytes per sample 16 -> 12, per interval 16 -> 8: the host->HBM copy
+    bounds the end-to-end path, so this is what a deployment ships (and what
+    ``save_packed`` writes).  ``device(name)`` decodes on the GPU
+    (``dw_unpack_deltas``: one scan per column) and caches the full columns.
+    Host attributes: ``ts``/``op_start``/``k_start`` hold the uint32 deltas
+    (``*_base`` the first value), ``op_end``/``k_end`` the uint32 durations.
+    """
+
+    PACKED = ("ts", "op_start", "k_start")
+
+    def __init__(self, ts_base, ts_delta, watts, op_base, op_delta, op_dur, k_base, k_delta, k_dur,
+                 trace_end, k_op=None, op_sig=None, **kw):
+        super().__init__(ts=ts_delta, watts=watts, trace_end=int(trace_end), op_start=op_delta, op_end=op_dur,
+                         k_start=k_delta, k_end=k_dur, k_op=k_op, op_sig=op_sig, ops_sorted=True,
+                         kernels_sorted=True, **kw)
+        self.ts_base, self.op_start_base, self.k_start_base = int(ts_base), int(op_base), int(k_base)
+        self._first_last = None
+
+    def _first_last_ts(self) -> tuple[int, int]:
+        if "first_last" not in self._dev:
+            d = self.ts
+            if isinstance(d, torch.Tensor):  # uint32 deltas, possibly held in an int32 tensor
+                dd = d.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+            else:
+                dd = np.asarray(d).view(np.uint32).astype(np.int64)
+            last = self.ts_base + int(dd.sum())
+            first = self.ts_base + int(dd[0])
+            self._dev["first_last"] = (first, last)
+        return self._dev["first_last"]
+
+    def _raw(self, name):
+        src = getattr(self, name)
+        if isinstance(src, torch.Tensor):
+            return src
+        return torch.from_numpy(np.ascontiguousarray(src))
+
+    def device(self, name: str) -> torch.Tensor:
+        if name not in ("ts", "op_start", "op_end", "k_start", "k_end"):
+            return super().device(name)
+        dev = _native.device()
+        key = (name, dev.index)
+        t = self._dev.get(key)
+        if t is not None:
+            return t
+        base_name = {"op_end": "op_start", "k_end": "k_start"}.get(name, name)
+        delta = self._raw(base_name).to(dev, non_blocking=True)
+        n = int(delta.numel())
+        out = torch.empty(n, dtype=torch.int64, device=dev)
+        end = None
+        dur_name = {"op_start": "op_end", "k_start": "k_end"}.get(base_name)
+        if dur_name is not None:
+            dur = self._raw(dur_name).to(dev, non_blocking=True)
+            end = torch.empty(n, dtype=torch.int64, device=dev)
+        base = {"ts": self.ts_base, "op_start": self.op_start_base, "k_start": self.k_start_base}[base_name]
+        L = _native.lib()
+        ws = _native.Workspace.get(L.dw_unpack_workspace_size(n))
+        _native.check(L.dw_unpack_deltas(_native.ptr(delta.view(torch.int32)), n, base, _native.ptr(out),
+                                         _native.ptr(dur.view(torch.int32)) if end is not None else None,
+                                         _native.ptr(end), ws.data_ptr(), ws.numel(), _native.stream_handle()),
+                      "dw_unpack_deltas")
+        self._dev[(base_name, dev.index)] = out
+        if end is not None:
+            self._dev[(dur_name, dev.index)] = end
+        return self._dev[key]
+
+    def host(self, name: str) -> np.ndarray:
+        if name in ("ts", "op_start", "op_end", "k_start", "k_end"):
+            return self.device(name).cpu().numpy()
+        return super().host(name)
+
+    @property
+    def host_bytes(self) -> int:
+        """Bytes the hot columns occupy on the host (what crosses PCIe)."""
+        return sum(int(getattr(self, n).numel() * getattr(self, n).element_size()) if isinstance(
+            getattr(self, n), torch.Tensor) else int(getattr(self, n).nbytes)
+            for n in ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "op_sig") if getattr(self, n) is not None)
+
+
+def _deltas(x, what: str):
+    """(base, uint32 deltas) of a sorted int64 column (numpy or torch)."""
+    if isinstance(x, torch.Tensor):
+        if x.numel() == 0:
+            return 0, torch.zeros(0, dtype=torch.int32, device=x.device)
+        d = torch.empty_like(x)
+        d[0] = 0
+        d[1:] = x[1:] - x[:-1]
+        if bool((d < 0).any()) or bool((d > 0xFFFFFFFF).any()):
+            raise ValueError(f"{what}: not sorted, or a gap of 2^32 us or more -- cannot pack")
+        return int(x[0].item()), d.to(torch.int64).to(torch.int32)  # low 32 bits (uint32 stored in int32)
+    x = np.asarray(x, dtype=np.int64)
+    if x.size == 0:
+        return 0, np.zeros(0, dtype=np.uint32)
+    d = np.diff(x, prepend=x[0])
+    if (d < 0).any() or (d > 0xFFFFFFFF).any():
+        raise ValueError(f"{what}: not sorted, or a gap of 2^32 us or more -- cannot pack")
+    return int(x[0]), d.astype(np.uint32)
+
+
+def _durations(start, end, what: str):
+    if isinstance(start, torch.Tensor):
+        dur = end - start
+        if dur.numel() and (bool((dur < 0).any()) or bool((dur > 0xFFFFFFFF).any())):
+            raise ValueError(f"{what}: negative or >= 2^32 us durations -- cannot pack")
+        return dur.to(torch.int32)
+    dur = np.asarray(end, dtype=np.int64) - np.asarray(start, dtype=np.int64)
+    if dur.size and ((dur < 0).any() or (dur > 0xFFFFFFFF).any()):
+        raise ValueError(f"{what}: negative or >= 2^32 us durations -- cannot pack")
+    return dur.astype(np.uint32)
+
+
+def pack(cols: TraceColumns) -> PackedColumns:
+    """Packed form of a trace with sorted power, operator and kernel starts
+    (ValueError otherwise -- keep such traces unpacked).  Works on host or
+    device columns; the result lives where the input does."""
+    ts = cols.ts if not isinstance(cols.ts, torch.Tensor) else cols.ts
+    tb, td = _deltas(cols.ts, "power timestamps")
+    ob, od = _deltas(cols.op_start, "operator starts")
+    kb, kd = _deltas(cols.k_start, "kernel starts")
+    return PackedColumns(tb, td, cols.watts, ob, od, _durations(cols.op_start, cols.op_end, "operators"),
+                         kb, kd, _durations(cols.k_start, cols.k_end, "kernels"), cols.trace_end,
+                         k_op=cols.k_op, op_sig=cols.op_sig, op_ids=cols.op_ids, k_ids=cols.k_ids,
+                         op_names=cols.op_names, op_work=cols.op_work, op_rank=cols.op_rank)
+
+
+def save_packed(cols: TraceColumns, path) -> None:
+    """The packed columnar trace file (``*.dwc``): one JSON header line, then
+    every column's raw little-endian bytes, 64-byte aligned.  Columns only --
+    ids, names and tensors stay in the JSONL trace (trace_model.save_trace)."""
+    import json
+    pc = cols if isinstance(cols, PackedColumns) else pack(cols)
+    arrays = {}
+    for n in ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "k_op", "op_sig", "op_work"):
+        a = getattr(pc, n)
+        if a is None:
+            continue
+        a = a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+        if n in ("ts", "op_start", "op_end", "k_start", "k_end"):
+            a = a.view(np.uint32) if a.dtype in (np.int32, np.uint32) else a.astype(np.uint32)
+        arrays[n] = np.ascontiguousarray(a)
+    meta = {"format": "dwc", "version": 1, "trace_end": pc.trace_end, "ts_base": pc.ts_base,
+            "op_base": pc.op_start_base, "k_base": pc.k_start_base, "columns": {}}
+    off = 0
+    for n, a in arrays.items():
+        meta["columns"][n] = {"dtype": a.dtype.str, "n": int(a.shape[0]), "offset": off}
+        off += (a.nbytes + 63) & ~63
+    head = json.dumps(meta).encode() + b"\n"
+    pad = (-len(head)) % 64
+    with open(path, "wb") as fh:
+        fh.write(head + b" " * pad)
+        for n, a in arrays.items():
+            fh.write(a.tobytes())
+            fh.write(b"\0" * ((-a.nbytes) % 64))
+
+
+def load_packed(path, pin: bool = False) -> PackedColumns:
+    """Memory-map a ``*.dwc`` file (optionally copying it into pinned host
+    memory for asynchronous host->HBM transfers)."""
+    import json
+    with open(path, "rb") as fh:
+        head = fh.readline()
+    meta = json.loads(head)
+    if meta.get("format") != "dwc" or meta.get("version") != 1:
+        raise ValueError(f"{path}: not a dwc v1 file")
+    start = (len(head) + 63) & ~63
+    raw = np.memmap(path, dtype=np.uint8, mode="r")
+    cols = {}
+    for n, c in meta["columns"].items():
+        dt = np.dtype(c["dtype"])
+        a = raw[start + c["offset"]: start + c["offset"] + c["n"] * dt.itemsize].view(dt)
+        t = torch.from_numpy(np.array(a)) if pin else a
+        if pin:
+            t = t.pin_memory()
+        cols[n] = t
+    def as_i32(x):
+        return x.view(torch.int32) if isinstance(x, torch.Tensor) else x
+    return PackedColumns(meta["ts_base"], as_i32(cols["ts"]), cols["watts"], meta["op_base"], as_i32(cols["op_start"]),
+                         as_i32(cols["op_end"]), meta["k_base"], as_i32(cols["k_start"]), as_i32(cols["k_end"]),
+                         meta["trace_end"], k_op=cols.get("k_op"), op_sig=cols.get("op_sig"),
+                         op_work=cols.get("op_work"))
