@@ -153,9 +153,33 @@ __global__ void partition_kernel(AttrParams p) {
     } else if (b == p.ntiles) {
         r = n;
     } else {
-        int64_t key = p.ts[b * TILE];
+        // first k with a[k] >= key: interpolated guess (starts are spread over
+        // the span), gallop to a bracket, then bisect
+        const int64_t key = p.ts[b * TILE];
         const int64_t *a = p.start[j];
-        int64_t lo = 0, hi = n;
+        int64_t lo = 0, hi = n;  // a[lo-1] < key (or lo == 0), a[hi] >= key (or hi == n)
+        if (n > 0) {
+            const int64_t a0 = __ldg(a), an = __ldg(a + n - 1);
+            if (key <= a0) {
+                hi = 0;
+            } else if (key > an) {
+                lo = n;
+            } else {
+                const double f = (double)(key - a0) / (double)(an - a0);
+                int64_t g = (int64_t)(f * (double)(n - 1));
+                g = g < 0 ? 0 : (g > n - 1 ? n - 1 : g);
+                int64_t step = 1;
+                if (__ldg(a + g) < key) {  // a[g] < key: gallop up
+                    lo = g + 1;
+                    while (lo + step - 1 < n && __ldg(a + lo + step - 1) < key) { lo += step; step <<= 1; }
+                    hi = lo + step - 1 < n ? lo + step - 1 : n;
+                } else {                   // a[g] >= key: gallop down
+                    hi = g;
+                    while (hi - step >= 0 && __ldg(a + hi - step) >= key) { hi -= step; step <<= 1; }
+                    lo = hi - step + 1 > 0 ? hi - step + 1 : 0;
+                }
+            }
+        }
         while (lo < hi) {
             int64_t mid = lo + ((hi - lo) >> 1);
             if (__ldg(a + mid) < key) lo = mid + 1; else hi = mid;
@@ -1322,9 +1346,18 @@ __global__ void __launch_bounds__(SUM_THREADS) fx_sum_kernel(const double *x, in
     __shared__ unsigned long long red[SUM_THREADS / 32][2];
     __shared__ bool last;
     i128 acc = 0;
-    for (int64_t i = blockIdx.x * (int64_t)SUM_THREADS + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * SUM_THREADS)
-        acc += fx_from_double(__ldg(x + i), FX_JOULE_BITS);
+    constexpr int U = 8;  // loads in flight per thread
+    const int64_t stride = (int64_t)gridDim.x * SUM_THREADS;
+    for (int64_t i0 = blockIdx.x * (int64_t)SUM_THREADS + threadIdx.x; i0 < n; i0 += U * stride) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + (int64_t)u * stride;
+            v[u] = i < n ? __ldcs(x + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) acc += fx_from_double(v[u], FX_JOULE_BITS);
+    }
     acc = warp_sum_i128(acc);
     if ((threadIdx.x & 31) == 0) {
         I128Parts pp = split(acc);
