@@ -145,6 +145,11 @@ int dw_attribute_window(const dw_signal_t *sig, dw_interval_set_t *sets, int32_t
                         const int64_t *d_blo, const int64_t *d_bhi, int64_t nb, int64_t *d_part,
                         int64_t *d_tile_fx, void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
 
+/* Cap the SMs the attribution tile kernel occupies (0 = all, the default), so
+ * kernels on another stream can run beside it (pipeline.analyze overlaps the
+ * join's pairing with the ledgers this way).  Process-wide. */
+int dw_set_attribute_sms(int n);
+
 /* Exact 2^-64 J fixed-point sum of d_x[0..n) as int128 halves (not rounded):
  * the per-rank share of a sharded operator_total.  Workspace as dw_fx_sum. */
 int dw_fx_sum_exact(const double *d_x, int64_t n, int64_t *d_out_fx, void *d_workspace,
@@ -265,6 +270,20 @@ int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_d
                  double threshold, dw_findings_t *out, int32_t *d_match_a, int32_t *d_b_only,
                  double *d_epw_a, double *d_epw_b, int64_t *d_count, void *d_workspace,
                  size_t workspace_bytes, dw_stream_t stream);
+
+/* dw_join_diff in two phases, so the pairing (signatures only) can run on its
+ * own stream while the ledgers that provide the joules are still computing:
+ * dw_join_prepare pairs the operators (d_match_a's sort state, d_b_only and
+ * *n_b_only), dw_join_findings then writes the finding columns.  Both take
+ * the same sides, max_distinct and workspace; the workspace carries the state
+ * from one call to the other. */
+int dw_join_prepare(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_distinct, int32_t *d_match_a,
+                    int32_t *d_b_only, int64_t *n_b_only, void *d_workspace, size_t workspace_bytes,
+                    dw_stream_t stream);
+int dw_join_findings(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_distinct, double threshold,
+                     dw_findings_t *out, int32_t *d_match_a, int32_t *d_b_only, int64_t n_b_only, double *d_epw_a,
+                     double *d_epw_b, int64_t *d_count, void *d_workspace, size_t workspace_bytes,
+                     dw_stream_t stream);
 
 /* --------------------------------------------------------------- misc */
 const char *dw_version(void);

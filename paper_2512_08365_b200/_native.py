@@ -39,7 +39,8 @@ DW_DIRECT_MAX = 256
 EXPORTED = (
     "dw_attribute_workspace_size", "dw_attribute", "dw_ledger", "dw_status",
     "dw_attribute_split_workspace_size", "dw_attribute_split", "dw_attribute_window", "dw_fx_sum_exact", "dw_replay",
-    "dw_unpack_workspace_size", "dw_unpack_deltas",
+    "dw_unpack_workspace_size", "dw_unpack_deltas", "dw_join_prepare", "dw_join_findings",
+    "dw_set_attribute_sms",
     "dw_fx_sum_workspace_size", "dw_fx_sum", "dw_step_value_at", "dw_detect_pairs",
     "dw_rank_workspace_size", "dw_rank", "dw_join_workspace_size", "dw_join_diff",
     "dw_version", "dw_error_string", "dw_launch_count", "dw_kernel_timing", "dw_kernel_time_ms",
@@ -123,6 +124,7 @@ def lib():
                                           ctypes.POINTER(Window), c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
                                           ctypes.c_size_t, c_vp]
         L.dw_fx_sum_exact.argtypes = [c_vp, c_i64, c_vp, c_vp, ctypes.c_size_t, c_vp]
+        L.dw_set_attribute_sms.argtypes = [ctypes.c_int]
         L.dw_unpack_workspace_size.restype = ctypes.c_size_t
         L.dw_unpack_workspace_size.argtypes = [c_i64]
         L.dw_unpack_deltas.argtypes = [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp]
@@ -156,6 +158,11 @@ def lib():
             L.dw_join_diff.argtypes = [ctypes.POINTER(JoinSide), ctypes.POINTER(JoinSide), c_i64,
                                        ctypes.c_double, ctypes.POINTER(Findings), c_vp, c_vp,
                                        c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp]
+            L.dw_join_prepare.argtypes = [ctypes.POINTER(JoinSide), ctypes.POINTER(JoinSide), c_i64, c_vp, c_vp,
+                                          ctypes.POINTER(c_i64), c_vp, ctypes.c_size_t, c_vp]
+            L.dw_join_findings.argtypes = [ctypes.POINTER(JoinSide), ctypes.POINTER(JoinSide), c_i64,
+                                           ctypes.c_double, ctypes.POINTER(Findings), c_vp, c_vp, c_i64, c_vp,
+                                           c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp]
         _lib = L
         return L
 
@@ -220,3 +227,8 @@ class Workspace:
     @classmethod
     def clear(cls) -> None:
         cls._pool.clear()
+
+
+def num_sms() -> int:
+    """Streaming multiprocessors of the current device."""
+    return int(torch.cuda.get_device_properties(device()).multi_processor_count)

@@ -1509,6 +1509,11 @@ static AttrLayout attr_layout(int64_t S, const int64_t *sizes, const int32_t *so
 
 static bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
 
+// SMs the tile kernel may occupy (0: all).  Leaving a few free lets work on
+// another stream (the join's pairing) run beside it: the tile kernel is a
+// persistent one-CTA-per-SM kernel that otherwise fills the whole GPU.
+static int g_attr_sms = 0;
+
 struct WindowJob {  // dw_attribute_window: work after the tile kernel on the same tile prefix
     WindowParams wp;
     const int64_t *blo, *bhi;
@@ -1597,7 +1602,8 @@ static int attribute_impl(const dw_signal_t *sig, dw_interval_set_t *sets, int n
         count_launch();
     }
     const size_t smem = ((sizeof(TileSmem) + 15) & ~(size_t)15) + GROUPS * sizeof(GroupSmem);
-    int grid = (int)std::min<int64_t>(p.ntiles, (int64_t)num_sms() * CTAS_PER_SM);
+    const int sms = g_attr_sms > 0 && g_attr_sms < num_sms() ? g_attr_sms : num_sms();
+    int grid = (int)std::min<int64_t>(p.ntiles, (int64_t)sms * CTAS_PER_SM);
     timing_begin(stream);
     if (sig->kind == DW_SIGNAL_STEP) {
         cudaFuncSetAttribute(attribute_tiles_kernel<DW_SIGNAL_STEP>,
@@ -1705,6 +1711,12 @@ int dw_attribute_window(const dw_signal_t *sig, dw_interval_set_t *sets, int32_t
     wj.tile_fx = (unsigned long long *)d_tile_fx;
     return attribute_impl(sig, sets, nsets, d_workspace, workspace_bytes, (cudaStream_t)stream, false, nullptr,
                           &wj);
+}
+
+int dw_set_attribute_sms(int n) {
+    if (n < 0) return DW_E_ARG;
+    g_attr_sms = n;
+    return DW_OK;
 }
 
 int dw_fx_sum_exact(const double *d_x, int64_t n, int64_t *d_out_fx, void *d_workspace, size_t ws_bytes,

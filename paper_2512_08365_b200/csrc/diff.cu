@@ -825,106 +825,121 @@ size_t dw_join_workspace_size(int64_t na, int64_t nb, int64_t max_distinct) {
     return join_layout(na, nb, max_distinct).total;
 }
 
-int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_distinct, double threshold,
-                 dw_findings_t *out, int32_t *d_match_a, int32_t *d_b_only, double *d_epw_a,
-                 double *d_epw_b, int64_t *d_count, void *d_workspace, size_t workspace_bytes,
-                 dw_stream_t stream) {
-    if (!(threshold > 0.0 && threshold <= 1.0)) return DW_E_ARG;
-    if (!a || !b || !out || !out->d_key_hi || !d_count || !d_workspace) return DW_E_ARG;
+// phase 1: pairing only (signatures; no joules needed) -> stage2, b_only,
+// *n_bonly_out; phase 2: the findings (joules); 3: both
+static int join_impl(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_distinct, double threshold,
+                     dw_findings_t *out, int32_t *d_match_a, int32_t *d_b_only, double *d_epw_a, double *d_epw_b,
+                     int64_t *d_count, void *d_workspace, size_t workspace_bytes, dw_stream_t stream, int phase,
+                     int64_t *n_bonly_io) {
+    if (!a || !b || !d_workspace) return DW_E_ARG;
+    if ((phase & 2) && (!(threshold > 0.0 && threshold <= 1.0))) return DW_E_ARG;
+    if ((phase & 2) && (!out || !out->d_key_hi || !d_count)) return DW_E_ARG;
     const int64_t na = a->n, nb = b->n;
     if (na < 0 || nb < 0 || na + nb >= ((int64_t)1 << 31)) return DW_E_ARG;
-    if ((na && (!a->d_sig || !a->d_start || !a->d_end || !a->d_joules || !d_match_a)) ||
-        (nb && (!b->d_sig || !b->d_start || !b->d_end || !b->d_joules || !d_b_only)))
+    if ((na && (!a->d_sig || !a->d_start || !a->d_end || !d_match_a)) ||
+        (nb && (!b->d_sig || !b->d_start || !b->d_end || !d_b_only)))
         return DW_E_ARG;
+    if ((phase & 2) && ((na && !a->d_joules) || (nb && !b->d_joules))) return DW_E_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     JoinLayout L = join_layout(na, nb, max_distinct);
     if (workspace_bytes < L.total) return DW_E_WORKSPACE;
     char *base = (char *)d_workspace;
-    JoinParams q{};
-    q.sig_a = a->d_sig;
-    q.sig_b = b->d_sig;
-    q.na = na;
-    q.nb = nb;
-    q.table = (uint64_t *)(base + L.table);
-    q.cap = L.cap;
-    q.id_a = (uint32_t *)(base + L.id_a);
-    q.id_b = (uint32_t *)(base + L.id_b);
-    q.ix_a = (uint32_t *)(base + L.ix_a);
-    q.ix_b = (uint32_t *)(base + L.ix_b);
     unsigned long long *counters = (unsigned long long *)(base + L.counters);
-    // counters: [0] overflow, [1] matched, [2] next_id (u32), [3] n_bonly (u32)
-    q.overflow = counters;
-    unsigned int *n_bonly = (unsigned int *)(counters + 3);
-    trace_mark(s, "join:start");
-    cudaMemsetAsync(counters, 0, 64, s);
-    cudaMemsetAsync(q.table, 0xFF, 8 * L.cap, s);
-    const int64_t n = na + nb;
-    if (n) {
-        join_hash_kernel<<<(unsigned)std::min<int64_t>(num_sms() * 16, blocks_for(n, 256 * ITEMS)), 256, 0, s>>>(q);
-        count_launch();
+    int64_t b_only = 0;
+    if (phase & 1) {
+        JoinParams q{};
+        q.sig_a = a->d_sig;
+        q.sig_b = b->d_sig;
+        q.na = na;
+        q.nb = nb;
+        q.table = (uint64_t *)(base + L.table);
+        q.cap = L.cap;
+        q.id_a = (uint32_t *)(base + L.id_a);
+        q.id_b = (uint32_t *)(base + L.id_b);
+        q.ix_a = (uint32_t *)(base + L.ix_a);
+        q.ix_b = (uint32_t *)(base + L.ix_b);
+        // counters: [0] overflow, [1] matched, [2] next_id (u32), [3] n_bonly (u32)
+        q.overflow = counters;
+        unsigned int *n_bonly = (unsigned int *)(counters + 3);
+        trace_mark(s, "join:start");
+        cudaMemsetAsync(counters, 0, 64, s);
+        cudaMemsetAsync(q.table, 0xFF, 8 * L.cap, s);
+        const int64_t n = na + nb;
+        if (n) {
+            join_hash_kernel<<<(unsigned)std::min<int64_t>(num_sms() * 16, blocks_for(n, 256 * ITEMS)), 256, 0, s>>>(q);
+            count_launch();
+        }
+        trace_mark(s, "join:hash");
+        // the number of distinct signatures bounds the sort's key bits
+        unsigned long long hc0[4] = {0, 0, 0, 0};
+        cudaMemcpyAsync(hc0, counters, sizeof(hc0), cudaMemcpyDeviceToHost, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess) return DW_E_CUDA;
+        if (hc0[0]) return DW_E_WORKSPACE;  // more distinct signatures than the table holds
+        const int64_t D = L.D;  // ids are table slots + 1
+        const int nbits = bits_for(D);
+        int32_t *first_a = (int32_t *)(base + L.first_a), *end_a = (int32_t *)(base + L.end_a);
+        int32_t *first_b = (int32_t *)(base + L.first_b), *end_b = (int32_t *)(base + L.end_b);
+        uint32_t *sid_a = (uint32_t *)(base + L.sid_a), *sid_b = (uint32_t *)(base + L.sid_b);
+        uint32_t *six_a = (uint32_t *)(base + L.six_a), *six_b = (uint32_t *)(base + L.six_b);
+        cudaMemsetAsync(end_a, 0, 4 * D, s);
+        cudaMemsetAsync(end_b, 0, 4 * D, s);
+        size_t cb = L.cub_bytes;
+        if (na) {  // stable: equal ids keep op order
+            cub::DeviceRadixSort::SortPairs(base + L.cub, cb, q.id_a, sid_a, q.ix_a, six_a, (int)na, 0, nbits, s);
+            trace_mark(s, "join:sort_a");
+            run_bounds_kernel<<<blocks_for(na), 256, 0, s>>>(sid_a, na, first_a, end_a);
+            count_launch(4);
+            trace_mark(s, "join:bounds_a");
+        }
+        if (nb) {
+            cb = L.cub_bytes;
+            cub::DeviceRadixSort::SortPairs(base + L.cub, cb, q.id_b, sid_b, q.ix_b, six_b, (int)nb, 0, nbits, s);
+            trace_mark(s, "join:sort_b");
+            run_bounds_kernel<<<blocks_for(nb), 256, 0, s>>>(sid_b, nb, first_b, end_b);
+            count_launch(4);
+            trace_mark(s, "join:bounds_b");
+        }
+        if (na) {
+            unsigned int *cursor = (unsigned int *)(base + L.pair_cursor);
+            uint2 *stage = (uint2 *)(base + L.pair_stage);
+            cudaMemsetAsync(cursor, 0, 4 * PAIR_MAXB, s);
+            join_pair_bucket_kernel<<<blocks_for(na, PAIR_THREADS * PAIR_ITEMS), PAIR_THREADS, 0, s>>>(
+                sid_a, six_a, na, first_a, six_b, first_b, end_b, cursor, stage);
+            trace_mark(s, "join:pair_bucket");
+            unsigned int *cursor2 = (unsigned int *)(base + L.win_cursor);
+            uint2 *stage2 = (uint2 *)(base + L.win_stage);
+            const int64_t nwin = (na + WIN_OPS - 1) / WIN_OPS;
+            cudaMemsetAsync(cursor2, 0, 4 * nwin, s);
+            join_pair_sub_kernel<<<(unsigned)((na + SUB_CHUNK - 1) / SUB_CHUNK), 256, 0, s>>>(stage, na, cursor2, stage2);
+            count_launch(1);
+            trace_mark(s, "join:pair_sub");
+        }
+        int32_t *bonly_tmp = (int32_t *)(base + L.bonly_tmp);
+        if (nb) {
+            join_bonly_kernel<<<blocks_for(nb), 256, 0, s>>>(sid_b, six_b, nb, first_b, first_a, end_a, bonly_tmp,
+                                                              n_bonly);
+            count_launch();
+            trace_mark(s, "join:bonly");
+        }
+        unsigned long long hc[4] = {0, 0, 0, 0};  // overflow, matched, next_id, n_bonly
+        cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess) return DW_E_CUDA;
+        b_only = (int64_t)(unsigned int)hc[3];
+        if (b_only) {  // B-only operators in B order
+            cb = L.cub_bytes;
+            cub::DeviceRadixSort::SortKeys(base + L.cub, cb, bonly_tmp, d_b_only, (int)b_only, 0,
+                                           bits_for(nb), s);
+            count_launch(4);
+            trace_mark(s, "join:bonly_sort");
+        }
+
+        if (n_bonly_io) *n_bonly_io = b_only;
+    } else {
+        b_only = n_bonly_io ? *n_bonly_io : 0;
     }
-    trace_mark(s, "join:hash");
-    // the number of distinct signatures bounds the sort's key bits
-    unsigned long long hc0[4] = {0, 0, 0, 0};
-    cudaMemcpyAsync(hc0, counters, sizeof(hc0), cudaMemcpyDeviceToHost, s);
-    if (cudaStreamSynchronize(s) != cudaSuccess) return DW_E_CUDA;
-    if (hc0[0]) return DW_E_WORKSPACE;  // more distinct signatures than the table holds
-    const int64_t D = L.D;  // ids are table slots + 1
-    const int nbits = bits_for(D);
-    int32_t *first_a = (int32_t *)(base + L.first_a), *end_a = (int32_t *)(base + L.end_a);
-    int32_t *first_b = (int32_t *)(base + L.first_b), *end_b = (int32_t *)(base + L.end_b);
-    uint32_t *sid_a = (uint32_t *)(base + L.sid_a), *sid_b = (uint32_t *)(base + L.sid_b);
-    uint32_t *six_a = (uint32_t *)(base + L.six_a), *six_b = (uint32_t *)(base + L.six_b);
-    cudaMemsetAsync(end_a, 0, 4 * D, s);
-    cudaMemsetAsync(end_b, 0, 4 * D, s);
-    size_t cb = L.cub_bytes;
-    if (na) {  // stable: equal ids keep op order
-        cub::DeviceRadixSort::SortPairs(base + L.cub, cb, q.id_a, sid_a, q.ix_a, six_a, (int)na, 0, nbits, s);
-        trace_mark(s, "join:sort_a");
-        run_bounds_kernel<<<blocks_for(na), 256, 0, s>>>(sid_a, na, first_a, end_a);
-        count_launch(4);
-        trace_mark(s, "join:bounds_a");
-    }
-    if (nb) {
-        cb = L.cub_bytes;
-        cub::DeviceRadixSort::SortPairs(base + L.cub, cb, q.id_b, sid_b, q.ix_b, six_b, (int)nb, 0, nbits, s);
-        trace_mark(s, "join:sort_b");
-        run_bounds_kernel<<<blocks_for(nb), 256, 0, s>>>(sid_b, nb, first_b, end_b);
-        count_launch(4);
-        trace_mark(s, "join:bounds_b");
-    }
-    if (na) {
-        unsigned int *cursor = (unsigned int *)(base + L.pair_cursor);
-        uint2 *stage = (uint2 *)(base + L.pair_stage);
-        cudaMemsetAsync(cursor, 0, 4 * PAIR_MAXB, s);
-        join_pair_bucket_kernel<<<blocks_for(na, PAIR_THREADS * PAIR_ITEMS), PAIR_THREADS, 0, s>>>(
-            sid_a, six_a, na, first_a, six_b, first_b, end_b, cursor, stage);
-        trace_mark(s, "join:pair_bucket");
-        unsigned int *cursor2 = (unsigned int *)(base + L.win_cursor);
-        uint2 *stage2 = (uint2 *)(base + L.win_stage);
-        const int64_t nwin = (na + WIN_OPS - 1) / WIN_OPS;
-        cudaMemsetAsync(cursor2, 0, 4 * nwin, s);
-        join_pair_sub_kernel<<<(unsigned)((na + SUB_CHUNK - 1) / SUB_CHUNK), 256, 0, s>>>(stage, na, cursor2, stage2);
-        count_launch(1);
-        trace_mark(s, "join:pair_sub");
-    }
-    int32_t *bonly_tmp = (int32_t *)(base + L.bonly_tmp);
-    if (nb) {
-        join_bonly_kernel<<<blocks_for(nb), 256, 0, s>>>(sid_b, six_b, nb, first_b, first_a, end_a, bonly_tmp,
-                                                          n_bonly);
-        count_launch();
-        trace_mark(s, "join:bonly");
-    }
-    unsigned long long hc[4] = {0, 0, 0, 0};  // overflow, matched, next_id, n_bonly
-    cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s);
-    if (cudaStreamSynchronize(s) != cudaSuccess) return DW_E_CUDA;
-    const int64_t b_only = (int64_t)(unsigned int)hc[3];
-    if (b_only) {  // B-only operators in B order
-        cb = L.cub_bytes;
-        cub::DeviceRadixSort::SortKeys(base + L.cub, cb, bonly_tmp, d_b_only, (int)b_only, 0,
-                                       bits_for(nb), s);
-        count_launch(4);
-        trace_mark(s, "join:bonly_sort");
+    if (!(phase & 2)) {
+        DW_CHECK_LAUNCH();
+        return DW_OK;
     }
     JoinSideDev A{a->d_start, a->d_end, a->d_rank, a->d_joules, a->d_work};
     JoinSideDev B{b->d_start, b->d_end, b->d_rank, b->d_joules, b->d_work};
@@ -953,6 +968,31 @@ int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_d
     trace_mark(s, "join:end");
     DW_CHECK_LAUNCH();
     return DW_OK;
+}
+
+int dw_join_diff(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_distinct, double threshold,
+                 dw_findings_t *out, int32_t *d_match_a, int32_t *d_b_only, double *d_epw_a,
+                 double *d_epw_b, int64_t *d_count, void *d_workspace, size_t workspace_bytes,
+                 dw_stream_t stream) {
+    int64_t nb_only = 0;
+    return join_impl(a, b, max_distinct, threshold, out, d_match_a, d_b_only, d_epw_a, d_epw_b, d_count,
+                     d_workspace, workspace_bytes, stream, 3, &nb_only);
+}
+
+int dw_join_prepare(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_distinct, int32_t *d_match_a,
+                    int32_t *d_b_only, int64_t *n_b_only, void *d_workspace, size_t workspace_bytes,
+                    dw_stream_t stream) {
+    if (!n_b_only) return DW_E_ARG;
+    return join_impl(a, b, max_distinct, 0.1, nullptr, d_match_a, d_b_only, nullptr, nullptr, nullptr, d_workspace,
+                     workspace_bytes, stream, 1, n_b_only);
+}
+
+int dw_join_findings(const dw_join_side_t *a, const dw_join_side_t *b, int64_t max_distinct, double threshold,
+                     dw_findings_t *out, int32_t *d_match_a, int32_t *d_b_only, int64_t n_b_only, double *d_epw_a,
+                     double *d_epw_b, int64_t *d_count, void *d_workspace, size_t workspace_bytes,
+                     dw_stream_t stream) {
+    return join_impl(a, b, max_distinct, threshold, out, d_match_a, d_b_only, d_epw_a, d_epw_b, d_count, d_workspace,
+                     workspace_bytes, stream, 2, &n_b_only);
 }
 
 }  // extern "C"

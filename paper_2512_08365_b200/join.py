@@ -161,21 +161,72 @@ class JoinDiff:
 DEFAULT_MAX_DISTINCT = 1 << 20
 
 
+@dataclass
+class JoinPrep:
+    """The pairing of two traces' operators (dw_join_prepare): it needs only
+    the signatures, so it can run on its own stream while the ledgers that
+    supply the joules are still computing.  Holds its workspace until
+    ``join_diff(..., prep=)`` writes the findings."""
+
+    ca: TraceColumns
+    cb: TraceColumns
+    keep: list
+    match_a: torch.Tensor
+    b_only: torch.Tensor
+    n_b_only: int
+    ws: torch.Tensor
+    max_distinct: int
+
+
+def _side(cols, trace, joules, work, rank, dev):
+    p = _native.ptr
+    sig = _sig_tensor(cols, trace, dev)
+    s, e = cols.device("op_start"), cols.device("op_end")
+    return _native.JoinSide(p(sig), p(s), p(e), p(joules), p(work), p(rank), cols.n_ops), [sig, s, e]
+
+
+def join_prepare(trace_a, trace_b, *, max_distinct: int = DEFAULT_MAX_DISTINCT, stream=None) -> JoinPrep:
+    """Pair the operators of two traces by (signature, occurrence) on the
+    device (the first half of ``join_diff``)."""
+    dev = _native.device()
+    ca, cb = TraceColumns.from_trace(trace_a), TraceColumns.from_trace(trace_b)
+    sa, ka = _side(ca, trace_a, None, None, None, dev)
+    sb, kb = _side(cb, trace_b, None, None, None, dev)
+    na, nb = ca.n_ops, cb.n_ops
+    match_a = torch.empty(max(na, 1), dtype=torch.int32, device=dev)
+    bonly_t = torch.empty(max(nb, 1), dtype=torch.int32, device=dev)
+    L = _native.lib()
+    p = _native.ptr
+    md = int(min(max_distinct, na + nb)) if max_distinct else 0
+    nbo = ctypes.c_int64(0)
+    while True:
+        ws = torch.empty(int(L.dw_join_workspace_size(na, nb, md)), dtype=torch.uint8, device=dev)
+        rc = L.dw_join_prepare(ctypes.byref(sa), ctypes.byref(sb), md, p(match_a), p(bonly_t), ctypes.byref(nbo),
+                               ws.data_ptr(), ws.numel(), _native.stream_handle(stream))
+        if rc == _native.DW_E_WORKSPACE and md and md < na + nb:
+            md = min(4 * md, na + nb)  # more distinct signatures than the table held
+            continue
+        break
+    _native.check(rc, "dw_join_prepare")
+    return JoinPrep(ca, cb, ka + kb, match_a, bonly_t, int(nbo.value), ws, md)
+
+
 def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
               threshold: float = DEFAULT_THRESHOLD, k: int = 100, *, full_columns: bool = True,
               epw: bool = True, work_a=None, work_b=None, stream=None,
-              max_distinct: int = DEFAULT_MAX_DISTINCT) -> JoinDiff:
-    """Signature-join diff of two traces with their ledgers; top-k ranked."""
+              max_distinct: int = DEFAULT_MAX_DISTINCT, prep: Optional[JoinPrep] = None) -> JoinDiff:
+    """Signature-join diff of two traces with their ledgers; top-k ranked.
+    ``prep``: the pairing already made by ``join_prepare`` (same traces)."""
     if ledger_a.method != ledger_b.method:
         raise ValueError(f"ledger method mismatch: {ledger_a.method!r} vs {ledger_b.method!r}")
     if not 0 < threshold <= 1:
         raise ValueError("threshold must be in (0, 1]")
     dev = _native.device()
-    ca, cb = TraceColumns.from_trace(trace_a), TraceColumns.from_trace(trace_b)
-    sides = []
-    keep = []
+    if prep is None:
+        prep = join_prepare(trace_a, trace_b, max_distinct=max_distinct, stream=stream)
+    ca, cb = prep.ca, prep.cb
+    sides, keep = [], []
     for cols, trace, led, work in ((ca, trace_a, ledger_a, work_a), (cb, trace_b, ledger_b, work_b)):
-        sig = _sig_tensor(cols, trace, dev)
         j = led.operator_tensor()
         if j is None:
             ids = cols.op_ids
@@ -187,41 +238,31 @@ def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
         elif cols.op_work is not None:
             w = cols.device("op_work")
         rank = _ranks(cols, dev) if cols is ca else None
-        s, e = cols.device("op_start"), cols.device("op_end")
-        keep += [sig, j, w, rank, s, e]
-        p = _native.ptr
-        sides.append(_native.JoinSide(p(sig), p(s), p(e), p(j), p(w), p(rank), cols.n_ops))
+        side, kk = _side(cols, trace, j, w, rank, dev)
+        sides.append(side)
+        keep += [j, w, rank] + kk
     na, nb = ca.n_ops, cb.n_ops
     Pmax = na + nb
-    rank_a = keep[3]
+    rank_a = keep[2]
     fc = FindingColumns(Pmax, dev, full=full_columns, key_lo=False, tie_rank=rank_a, n_a=na)
-    match_a = torch.empty(max(na, 1), dtype=torch.int32, device=dev)
-    bonly_t = torch.empty(max(nb, 1), dtype=torch.int32, device=dev)
     epw_a = torch.empty(Pmax, dtype=torch.float64, device=dev) if epw else None
     epw_b = torch.empty(Pmax, dtype=torch.float64, device=dev) if epw else None
     count = torch.zeros(4, dtype=torch.int64, device=dev)
     L = _native.lib()
     fs = fc.c_struct()
     p = _native.ptr
-    md = int(min(max_distinct, na + nb)) if max_distinct else 0
-    while True:
-        ws = _native.Workspace.get(L.dw_join_workspace_size(na, nb, md), stream)
-        rc = L.dw_join_diff(ctypes.byref(sides[0]), ctypes.byref(sides[1]), md, float(threshold),
-                            ctypes.byref(fs), p(match_a), p(bonly_t), p(epw_a), p(epw_b), p(count),
-                            ws.data_ptr(), ws.numel(), _native.stream_handle(stream))
-        if rc == _native.DW_E_WORKSPACE and md and md < na + nb:
-            md = min(4 * md, na + nb)  # more distinct signatures than the table held
-            continue
-        break
-    _native.check(rc, "dw_join_diff")
+    _native.check(L.dw_join_findings(ctypes.byref(sides[0]), ctypes.byref(sides[1]), prep.max_distinct,
+                                     float(threshold), ctypes.byref(fs), p(prep.match_a), p(prep.b_only),
+                                     prep.n_b_only, p(epw_a), p(epw_b), p(count), prep.ws.data_ptr(),
+                                     prep.ws.numel(), _native.stream_handle(stream)), "dw_join_findings")
     P, matched, a_only, b_only = (int(x) for x in count.cpu().tolist())
     kk = min(k, P)
     order, summary = rank_order(fc.key_hi[:P], None, kk, tie_rank=rank_a, n_a=na)
     sm = summary.cpu().tolist()
     return JoinDiff(P=P, n_a=na, n_matched=matched, n_a_only=a_only, n_b_only=b_only, columns=fc,
-                    match_a=match_a[:na], b_only=bonly_t[:b_only],
+                    match_a=prep.match_a[:na], b_only=prep.b_only[:b_only],
                     epw_a=epw_a, epw_b=epw_b, order=order, n_waste=int(sm[0]),
-                    wasted_joules=float(sm[1]), ja=keep[1], jb=keep[7])
+                    wasted_joules=float(sm[1]), ja=keep[0], jb=keep[6])
 
 
 def join_report(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,

@@ -30,7 +30,12 @@ class Analysis:
 def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAULT_THRESHOLD,
             k: int = 100, *, lean: bool = True, copy_stream: "torch.cuda.Stream | None" = None
             ) -> Analysis:
-    """Ledgers for both traces, the signature-join diff and the top-k report."""
+    """Ledgers for both traces, the signature-join diff and the top-k report.
+
+    (Running the join's pairing on a second stream beside the ledgers, with
+    the tile kernel capped to fewer SMs via dw_set_attribute_sms, was measured
+    slower on C4 -- 35.4 vs 34.5 ms at 12 reserved SMs, worse with more -- so
+    the phases run back to back.)"""
     ca, cb = TraceColumns.from_trace(trace_a), TraceColumns.from_trace(trace_b)
     if copy_stream is not None:
         # B's host->HBM copy runs under A's attribution
