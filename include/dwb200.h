@@ -186,6 +186,32 @@ size_t dw_unpack_workspace_size(int64_t n);
 int dw_unpack_deltas(const uint32_t *d_delta, int64_t n, int64_t base, int64_t *d_out, const uint32_t *d_dur,
                      int64_t *d_end, void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
 
+/* JSONL ingestion (paper_2512_08365_b200/ingest.py):
+ * byte-level stages over the raw file resident in HBM.  The canonical
+ * power / op / kernel records of tensor-free traces parse here; `flags` (one
+ * device unsigned) turns nonzero on anything else, and the caller then loads
+ * the file through the reference-compatible Python loader.  Glue between the
+ * stages (scans, compaction, sorts) is the caller's. */
+int dw_ig_nl_count(const uint8_t *buf, int64_t n, unsigned long long *counts, unsigned *flags, dw_stream_t stream);
+int dw_ig_nl_write(const uint8_t *buf, int64_t n, const unsigned long long *offs, int64_t *ends, dw_stream_t stream);
+int dw_ig_classify(const uint8_t *buf, int64_t n, const int64_t *ends, int64_t nlines, uint8_t *type, unsigned *flags,
+                   dw_stream_t stream);
+int dw_ig_parse_power(const uint8_t *buf, const int64_t *ends, const int64_t *lines, int64_t m, int64_t *ts,
+                      double *w, unsigned *flags, dw_stream_t stream);
+int dw_ig_parse_op(const uint8_t *buf, const int64_t *ends, const int64_t *lines, int64_t m, int64_t *id_off,
+                   int32_t *id_len, int64_t *name_off, int32_t *name_len, int64_t *kl_first, int32_t *kl_count,
+                   int64_t *start, int64_t *end, unsigned *flags, dw_stream_t stream);
+int dw_ig_parse_kernel(const uint8_t *buf, const int64_t *ends, const int64_t *lines, int64_t m, int64_t *id_off,
+                       int32_t *id_len, int64_t *corr, int64_t *start, int64_t *end, unsigned *flags,
+                       dw_stream_t stream);
+int dw_ig_hash(const uint8_t *buf, const int64_t *off, const int32_t *len, int64_t m, uint64_t *h, uint32_t *idx,
+               dw_stream_t stream);
+int dw_ig_kernel_lists(const uint8_t *buf, int64_t nops, const int64_t *kl_first, const int32_t *kl_count,
+                       const int64_t *kl_base, const int64_t *op_start, const int64_t *op_end, const uint64_t *kh,
+                       const uint32_t *kidx, int64_t nk, const int64_t *k_off, const int32_t *k_len,
+                       const int64_t *k_start, const int64_t *k_end, int64_t *fk_start, int64_t *fk_end,
+                       int32_t *fk_op, int64_t *fk_kernel, unsigned *owner_count, unsigned *flags, dw_stream_t stream);
+
 /* Synchronise `stream` and copy the status block out of the workspace. Returns
  * status->code. */
 int dw_status(const void *d_workspace, dw_stream_t stream, dw_status_t *status);

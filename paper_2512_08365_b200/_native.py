@@ -40,7 +40,8 @@ EXPORTED = (
     "dw_attribute_workspace_size", "dw_attribute", "dw_ledger", "dw_status",
     "dw_attribute_split_workspace_size", "dw_attribute_split", "dw_attribute_window", "dw_fx_sum_exact", "dw_replay",
     "dw_unpack_workspace_size", "dw_unpack_deltas", "dw_join_prepare", "dw_join_findings",
-    "dw_set_attribute_sms",
+    "dw_set_attribute_sms", "dw_ig_nl_count", "dw_ig_nl_write", "dw_ig_classify", "dw_ig_parse_power",
+    "dw_ig_parse_op", "dw_ig_parse_kernel", "dw_ig_hash", "dw_ig_kernel_lists",
     "dw_fx_sum_workspace_size", "dw_fx_sum", "dw_step_value_at", "dw_detect_pairs",
     "dw_rank_workspace_size", "dw_rank", "dw_join_workspace_size", "dw_join_diff",
     "dw_version", "dw_error_string", "dw_launch_count", "dw_kernel_timing", "dw_kernel_time_ms",
@@ -125,6 +126,14 @@ def lib():
                                           ctypes.c_size_t, c_vp]
         L.dw_fx_sum_exact.argtypes = [c_vp, c_i64, c_vp, c_vp, ctypes.c_size_t, c_vp]
         L.dw_set_attribute_sms.argtypes = [ctypes.c_int]
+        L.dw_ig_nl_count.argtypes = [c_vp, c_i64, c_vp, c_vp, c_vp]
+        L.dw_ig_nl_write.argtypes = [c_vp, c_i64, c_vp, c_vp, c_vp]
+        L.dw_ig_classify.argtypes = [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]
+        L.dw_ig_parse_power.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]
+        L.dw_ig_parse_op.argtypes = [c_vp, c_vp, c_vp, c_i64] + [c_vp] * 10
+        L.dw_ig_parse_kernel.argtypes = [c_vp, c_vp, c_vp, c_i64] + [c_vp] * 7
+        L.dw_ig_hash.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]
+        L.dw_ig_kernel_lists.argtypes = [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64] + [c_vp] * 11
         L.dw_unpack_workspace_size.restype = ctypes.c_size_t
         L.dw_unpack_workspace_size.argtypes = [c_i64]
         L.dw_unpack_deltas.argtypes = [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp]
