@@ -378,12 +378,30 @@ __global__ void join_hash_kernel(JoinParams q) {
 }
 
 // runs of equal ids in a sorted id column -> first[id], end[id]
+constexpr int RB_ITEMS = 8;  // consecutive sorted positions per thread (two 16-byte loads)
+
 __global__ void run_bounds_kernel(const uint32_t *sorted, int64_t n, int32_t *first, int32_t *end) {
-    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    const uint32_t d = sorted[p];
-    if (p == 0 || sorted[p - 1] != d) first[d] = (int32_t)p;
-    if (p == n - 1 || sorted[p + 1] != d) end[d] = (int32_t)(p + 1);
+    const int64_t p0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * RB_ITEMS;
+    if (p0 >= n) return;
+    uint32_t v[RB_ITEMS + 2];
+    v[0] = p0 > 0 ? __ldg(sorted + p0 - 1) : 0xFFFFFFFFu;
+    if (p0 + RB_ITEMS <= n && (p0 & 3) == 0) {
+        const uint4 a = __ldcs(reinterpret_cast<const uint4 *>(sorted + p0));
+        const uint4 b = __ldcs(reinterpret_cast<const uint4 *>(sorted + p0 + 4));
+        v[1] = a.x; v[2] = a.y; v[3] = a.z; v[4] = a.w; v[5] = b.x; v[6] = b.y; v[7] = b.z; v[8] = b.w;
+    } else {
+#pragma unroll
+        for (int u = 0; u < RB_ITEMS; ++u) v[u + 1] = p0 + u < n ? __ldg(sorted + p0 + u) : 0xFFFFFFFFu;
+    }
+    v[RB_ITEMS + 1] = p0 + RB_ITEMS < n ? __ldg(sorted + p0 + RB_ITEMS) : 0xFFFFFFFFu;
+#pragma unroll
+    for (int u = 0; u < RB_ITEMS; ++u) {
+        const int64_t p = p0 + u;
+        if (p >= n) break;
+        const uint32_t d = v[u + 1];
+        if (p == 0 || v[u] != d) first[d] = (int32_t)p;
+        if (p == n - 1 || v[u + 2] != d) end[d] = (int32_t)(p + 1);
+    }
 }
 
 // The pairing in sorted order, written back to A order without a random
@@ -443,17 +461,22 @@ __global__ void __launch_bounds__(PAIR_THREADS) join_pair_bucket_kernel(
     }
 }
 
-// B operators beyond A's occurrence count of their signature: B-only
-__global__ void join_bonly_kernel(const uint32_t *db, const uint32_t *xb, int64_t nb, const int32_t *first_b,
+// B operators beyond A's occurrence count of their signature: B-only.  One
+// thread per signature id (table slot): the B-only ops of id d are the tail
+// [first_b + count_a, end_b) of its run in sorted B (few ids have any).
+__global__ void join_bonly_kernel(int64_t D, const uint32_t *xb, const int32_t *first_b, const int32_t *end_b,
                                   const int32_t *first_a, const int32_t *end_a, int32_t *b_only,
                                   unsigned int *n_bonly) {
-    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (q >= nb) return;
-    const uint32_t d = db[q];
-    const int32_t t = (int32_t)q - first_b[d];
+    const int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (d >= D) return;
+    const int32_t eb = end_b[d];
+    if (eb <= 0) return;
     const int32_t ea = end_a[d];
     const int32_t ca = ea > 0 ? ea - first_a[d] : 0;
-    if (t >= ca) b_only[atomicAdd(n_bonly, 1u)] = (int32_t)xb[q];
+    const int32_t fb = first_b[d];
+    if (fb + ca >= eb) return;
+    const unsigned base = atomicAdd(n_bonly, (unsigned)(eb - fb - ca));  // one reservation per id
+    for (int32_t q = fb + ca; q < eb; ++q) b_only[base + (q - fb - ca)] = (int32_t)xb[q];
 }
 
 struct JoinSideDev {
@@ -887,7 +910,7 @@ static int join_impl(const dw_join_side_t *a, const dw_join_side_t *b, int64_t m
         if (na) {  // stable: equal ids keep op order
             cub::DeviceRadixSort::SortPairs(base + L.cub, cb, q.id_a, sid_a, q.ix_a, six_a, (int)na, 0, nbits, s);
             trace_mark(s, "join:sort_a");
-            run_bounds_kernel<<<blocks_for(na), 256, 0, s>>>(sid_a, na, first_a, end_a);
+            run_bounds_kernel<<<blocks_for(na, 256 * RB_ITEMS), 256, 0, s>>>(sid_a, na, first_a, end_a);
             count_launch(4);
             trace_mark(s, "join:bounds_a");
         }
@@ -895,7 +918,7 @@ static int join_impl(const dw_join_side_t *a, const dw_join_side_t *b, int64_t m
             cb = L.cub_bytes;
             cub::DeviceRadixSort::SortPairs(base + L.cub, cb, q.id_b, sid_b, q.ix_b, six_b, (int)nb, 0, nbits, s);
             trace_mark(s, "join:sort_b");
-            run_bounds_kernel<<<blocks_for(nb), 256, 0, s>>>(sid_b, nb, first_b, end_b);
+            run_bounds_kernel<<<blocks_for(nb, 256 * RB_ITEMS), 256, 0, s>>>(sid_b, nb, first_b, end_b);
             count_launch(4);
             trace_mark(s, "join:bounds_b");
         }
@@ -916,8 +939,7 @@ static int join_impl(const dw_join_side_t *a, const dw_join_side_t *b, int64_t m
         }
         int32_t *bonly_tmp = (int32_t *)(base + L.bonly_tmp);
         if (nb) {
-            join_bonly_kernel<<<blocks_for(nb), 256, 0, s>>>(sid_b, six_b, nb, first_b, first_a, end_a, bonly_tmp,
-                                                              n_bonly);
+            join_bonly_kernel<<<blocks_for(D), 256, 0, s>>>(D, six_b, first_b, end_b, first_a, end_a, bonly_tmp, n_bonly);
             count_launch();
             trace_mark(s, "join:bonly");
         }

@@ -202,7 +202,7 @@ def _columns(ops: _Ops, cfg: SynthConfig, t0: int, n_samples: int, dev, prefix: 
     n = op_start.numel()
     return TraceColumns(ts=ts, watts=watts, trace_end=max(end, int(ts[-1].item())),
                         op_start=op_start, op_end=op_end, k_start=k_start, k_end=k_end,
-                        k_op=kop, op_sig=ops.sig, op_rank=torch.arange(n, device=dev),
+                        k_op=kop, op_sig=ops.sig,
                         ops_sorted=True, kernels_sorted=True)
 
 
@@ -262,6 +262,6 @@ def _make_pair_streams(cfg: SynthConfig, g, dev, t0: int):
         sides.append(TraceColumns(ts=ts, watts=watts, trace_end=max(end, int(ts[-1].item())),
                                   op_start=op_start[order], op_end=op_end[order],
                                   k_start=k_start, k_end=k_end, k_op=kop_new.to(torch.int32),
-                                  op_sig=sig[order], op_rank=torch.arange(order.numel(), device=dev),
+                                  op_sig=sig[order],
                                   ops_sorted=True, kernels_sorted=None))
     return sides[0], sides[1]
