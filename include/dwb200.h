@@ -202,8 +202,8 @@ int dw_ig_parse_op(const uint8_t *buf, const int64_t *ends, const int64_t *lines
                    int32_t *id_len, int64_t *name_off, int32_t *name_len, int64_t *kl_first, int32_t *kl_count,
                    int64_t *start, int64_t *end, unsigned *flags, dw_stream_t stream);
 int dw_ig_parse_kernel(const uint8_t *buf, const int64_t *ends, const int64_t *lines, int64_t m, int64_t *id_off,
-                       int32_t *id_len, int64_t *corr, int64_t *start, int64_t *end, unsigned *flags,
-                       dw_stream_t stream);
+                       int32_t *id_len, int64_t *name_off, int32_t *name_len, int64_t *corr, int64_t *start,
+                       int64_t *end, unsigned *flags, dw_stream_t stream);
 int dw_ig_hash(const uint8_t *buf, const int64_t *off, const int32_t *len, int64_t m, uint64_t *h, uint32_t *idx,
                dw_stream_t stream);
 int dw_ig_kernel_lists(const uint8_t *buf, int64_t nops, const int64_t *kl_first, const int32_t *kl_count,

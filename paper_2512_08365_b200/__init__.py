@@ -47,6 +47,13 @@ from .detect import (  # noqa: F401
     detect_waste,
     report,
 )
+from .diagnose import (  # noqa: F401
+    DiagnoseError,
+    classify,
+    classify_findings,
+    forced_gap_joules,
+    idle_baseline_watts,
+)
 from .join import join_diff, join_report, signature_of  # noqa: F401
 
 __version__ = "0.1.0"

@@ -131,7 +131,7 @@ def lib():
         L.dw_ig_classify.argtypes = [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]
         L.dw_ig_parse_power.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]
         L.dw_ig_parse_op.argtypes = [c_vp, c_vp, c_vp, c_i64] + [c_vp] * 10
-        L.dw_ig_parse_kernel.argtypes = [c_vp, c_vp, c_vp, c_i64] + [c_vp] * 7
+        L.dw_ig_parse_kernel.argtypes = [c_vp, c_vp, c_vp, c_i64] + [c_vp] * 9
         L.dw_ig_hash.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]
         L.dw_ig_kernel_lists.argtypes = [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64] + [c_vp] * 11
         L.dw_unpack_workspace_size.restype = ctypes.c_size_t

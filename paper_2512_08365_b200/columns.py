@@ -49,6 +49,7 @@ class TraceColumns:
     op_ids: Optional[Sequence[str]] = None
     k_ids: Optional[Sequence[str]] = None
     op_names: Optional[Sequence[str]] = None
+    k_names: Optional[Sequence[str]] = None   # kernel names, k_* row order (diagnosis)
     op_sig: object = None       # uint64[N] signature hash (join)
     op_work: object = None      # f64[N] useful work per op (join)
     op_rank: object = None      # int64[N] lexicographic rank of op ids
@@ -174,12 +175,13 @@ class TraceColumns:
         n = len(ops)
         op_start = np.fromiter((o.start for o in ops), dtype=np.int64, count=n)
         op_end = np.fromiter((o.end for o in ops), dtype=np.int64, count=n)
-        k_ids, k_start, k_end, k_op = [], [], [], []
+        k_ids, k_names, k_start, k_end, k_op = [], [], [], [], []
         kernels = trace.kernels
         for i, o in enumerate(ops):
             for kid in o.kernel_ids:
                 k = kernels[kid]
                 k_ids.append(kid)
+                k_names.append(k.kernel_name)
                 k_start.append(k.start)
                 k_end.append(k.end)
                 k_op.append(i)
@@ -194,7 +196,7 @@ class TraceColumns:
         cols = cls(ts=ts, watts=watts, trace_end=max(ends) if ends else 0, op_start=op_start,
                    op_end=op_end, k_start=k_start, k_end=k_end,
                    k_op=np.asarray(k_op, dtype=np.int32), op_ids=[o.op_id for o in ops],
-                   k_ids=k_ids, op_names=[o.op_name for o in ops])
+                   k_ids=k_ids, op_names=[o.op_name for o in ops], k_names=k_names)
         try:
             _CACHE[id(trace)] = (weakref.ref(trace), cols)
             while len(_CACHE) > _CACHE_MAX:

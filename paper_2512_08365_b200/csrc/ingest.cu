@@ -268,15 +268,15 @@ __global__ void parse_op_kernel(const uint8_t *buf, const int64_t *ends, const i
 }
 
 __global__ void parse_kernel_kernel(const uint8_t *buf, const int64_t *ends, const int64_t *lines, int64_t m,
-                                    int64_t *id_off, int32_t *id_len, int64_t *corr, int64_t *start, int64_t *end,
-                                    unsigned *flags) {
+                                    int64_t *id_off, int32_t *id_len, int64_t *name_off, int32_t *name_len,
+                                    int64_t *corr, int64_t *start, int64_t *end, unsigned *flags) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= m) return;
     const int64_t i = lines[k];
     const int64_t a = i == 0 ? 0 : ends[i - 1] + 1;
     Cur c{buf + a, buf + ends[i]};
-    int64_t io = 0, no, cr = 0, s = 0, e = 0, bf;
-    int32_t il = 0, nl, bc = 0;
+    int64_t io = 0, no = 0, cr = 0, s = 0, e = 0, bf;
+    int32_t il = 0, nl = 0, bc = 0;
     bool ok = c.lit("{\"type\":\"kernel\",\"kernel_id\":") && take_str(c, buf, io, il) &&
               c.lit(",\"kernel_name\":") && take_str(c, buf, no, nl) && c.lit(",\"correlation_id\":") &&
               c.int64v(cr) && c.lit(",\"start\":") && c.int64v(s) && c.lit(",\"end\":") && c.int64v(e) &&
@@ -285,7 +285,8 @@ __global__ void parse_kernel_kernel(const uint8_t *buf, const int64_t *ends, con
     ok = ok && c.lit("}") && c.at_end();
     if (!ok) atomicOr(flags, F_BAD_LINE);
     if (ok && (e <= s || bc == 0)) atomicOr(flags, F_INTERVAL);  // KernelEvent.validate
-    id_off[k] = io; id_len[k] = il; corr[k] = cr; start[k] = s; end[k] = e;
+    id_off[k] = io; id_len[k] = il; name_off[k] = no; name_len[k] = nl;
+    corr[k] = cr; start[k] = s; end[k] = e;
 }
 
 // 64-bit FNV-1a of a byte string
@@ -395,9 +396,10 @@ int dw_ig_parse_op(const uint8_t *buf, const int64_t *ends, const int64_t *lines
               end, flags);
 }
 int dw_ig_parse_kernel(const uint8_t *buf, const int64_t *ends, const int64_t *lines, int64_t m, int64_t *id_off,
-                       int32_t *id_len, int64_t *corr, int64_t *start, int64_t *end, unsigned *flags,
-                       dw_stream_t stream) {
-    IG_LAUNCH(parse_kernel_kernel, m, buf, ends, lines, m, id_off, id_len, corr, start, end, flags);
+                       int32_t *id_len, int64_t *name_off, int32_t *name_len, int64_t *corr, int64_t *start,
+                       int64_t *end, unsigned *flags, dw_stream_t stream) {
+    IG_LAUNCH(parse_kernel_kernel, m, buf, ends, lines, m, id_off, id_len, name_off, name_len, corr, start, end,
+              flags);
 }
 int dw_ig_hash(const uint8_t *buf, const int64_t *off, const int32_t *len, int64_t m, uint64_t *h, uint32_t *idx,
                dw_stream_t stream) {

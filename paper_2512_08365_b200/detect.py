@@ -8,18 +8,18 @@ ranking (``dw_rank``); the host only builds the CSR member lists, evaluates the
 boundary-tensor output rule (tensor snapshots live on the host) and
 materialises the findings.
 
-Category: the reference classifies each waste finding by calling into its
-diagnosis module (detect.py:137-172), which is outside this hot path
-(SURVEY.md 8(f)3).  ``detect_waste(..., classify=fn)`` accepts that function
-(e.g. the reference's ``diffwatt.detect.classify``); without one the category
-stays "unknown".
+Category: like the reference, every waste finding is classified
+(detect.py:127-128, 137-172) -- here in one batch (``diagnose.classify_findings``:
+one device integral launch for all forced gaps).  ``classify=fn`` substitutes a
+per-finding function (e.g. the reference's own ``diffwatt.detect.classify``),
+``classify=False`` skips the step and leaves "unknown".
 """
 
 from __future__ import annotations
 
 import ctypes
 from dataclasses import dataclass, field
-from typing import Callable, Optional, Sequence
+from typing import Optional, Sequence
 
 import numpy as np
 import torch
@@ -161,7 +161,7 @@ def tuple_rank(tuples) -> np.ndarray:
 def detect_waste(pairs: Sequence, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
                  threshold: float = DEFAULT_THRESHOLD, *, trace_a, trace_b,
                  output_diff: Optional[Sequence[float]] = None,
-                 classify: Optional[Callable] = None) -> list[WasteFinding]:
+                 classify=None) -> list[WasteFinding]:
     """One finding per subgraph pair; the higher-energy side is the suspect
     (detect.py:72-130)."""
     _check_args(ledger_a, ledger_b, threshold)
@@ -198,9 +198,14 @@ def detect_waste(pairs: Sequence, ledger_a: EnergyLedger, ledger_b: EnergyLedger
             verdict=VERDICTS[h["verdict"][i]], category="unknown",
             wasteful_side=SIDES[h["side"][i]], wasted_joules=float(h["wasted"][i]),
             informational=bool(h["informational"][i]))
-        if classify is not None and f.verdict == VERDICT_WASTE:
+        if callable(classify) and f.verdict == VERDICT_WASTE:
             f = WasteFinding(**{**f.__dict__, "category": classify(f, trace_a, trace_b)})
         findings.append(f)
+    if classify is None:
+        from .diagnose import classify_findings
+        cats = classify_findings(findings, trace_a, trace_b)
+        findings = [f if c == f.category else WasteFinding(**{**f.__dict__, "category": c})
+                    for f, c in zip(findings, cats)]
     return findings
 
 

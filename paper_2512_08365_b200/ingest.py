@@ -131,9 +131,9 @@ def _gpu_path(raw: np.ndarray):
         i64(nop), i64(nop)
     _native.check(L.dw_ig_parse_op(p(buf), p(ends), p(lines[L_OP]), nop, p(o_id), p(o_idl), p(o_nm), p(o_nml),
                                    p(o_klf), p(o_klc), p(o_s), p(o_e), p(flags), st), "dw_ig_parse_op")
-    k_id, k_idl, k_corr, k_s, k_e = i64(nk), i32(nk), i64(nk), i64(nk), i64(nk)
-    _native.check(L.dw_ig_parse_kernel(p(buf), p(ends), p(lines[L_KERNEL]), nk, p(k_id), p(k_idl), p(k_corr),
-                                       p(k_s), p(k_e), p(flags), st), "dw_ig_parse_kernel")
+    k_id, k_idl, k_nm, k_nml, k_corr, k_s, k_e = i64(nk), i32(nk), i64(nk), i32(nk), i64(nk), i64(nk), i64(nk)
+    _native.check(L.dw_ig_parse_kernel(p(buf), p(ends), p(lines[L_KERNEL]), nk, p(k_id), p(k_idl), p(k_nm),
+                                       p(k_nml), p(k_corr), p(k_s), p(k_e), p(flags), st), "dw_ig_parse_kernel")
     if int(flags.item()) or npw == 0:
         return None
     if npw > 1 and not bool((ts[1:] > ts[:-1]).all()):
@@ -180,6 +180,7 @@ def _gpu_path(raw: np.ndarray):
     cols = TraceColumns(ts=ts, watts=watts, trace_end=trace_end, op_start=o_s, op_end=o_e, k_start=fk_s,
                         k_end=fk_e, k_op=fk_op, op_ids=StrView(raw, h(o_id), h(o_idl)),
                         k_ids=StrView(raw, k_id_h[fk_k_h], k_idl_h[fk_k_h]),
-                        op_names=StrView(raw, h(o_nm), h(o_nml)))
+                        op_names=StrView(raw, h(o_nm), h(o_nml)),
+                        k_names=StrView(raw, h(k_nm)[fk_k_h], h(k_nml)[fk_k_h]))
     cols.header, cols.config, cols.loaded_by = header, config, "gpu"
     return cols

@@ -118,10 +118,13 @@ class JoinDiff:
         ib = torch.where(is_a, ma, bo)
         return ia, ib
 
-    def top_findings(self, cols_a: TraceColumns, cols_b: TraceColumns) -> list[WasteFinding]:
+    def top_findings(self, cols_a: TraceColumns, cols_b: TraceColumns, classify: bool = True,
+                     trace_a=None, trace_b=None) -> list[WasteFinding]:
         """Materialise the top-k findings (report order) as reference-style
         WasteFinding objects; columns not written by the join are gathered from
-        the ledgers on the device for these k rows only."""
+        the ledgers on the device for these k rows only.  Waste findings are
+        classified as detect_waste does (diagnose.classify_pairs; the trace
+        objects, when given, enable the program-model probe)."""
         idx = self.order
         c = self.columns
         ia_d, ib_d = self.pair_of(idx)
@@ -144,6 +147,14 @@ class JoinDiff:
                                                             "informational")}
         ia, ib = ia_d.cpu().numpy(), ib_d.cpu().numpy()
         name = lambda ids, i, p: (ids[i] if ids is not None else f"{p}{i}")  # noqa: E731
+        cats = ["unknown"] * len(ia)
+        waste = np.nonzero(h["verdict"] == VERDICTS.index(VERDICT_WASTE))[0]
+        if classify and waste.size:
+            from .diagnose import classify_pairs
+            got = classify_pairs(cols_a, cols_b, [SIDES[h["side"][r]] for r in waste], ia[waste], ib[waste],
+                                 trace_a, trace_b)
+            for r, c in zip(waste.tolist(), got):
+                cats[r] = c
         out = []
         for r in range(len(ia)):
             na = (name(cols_a.op_ids, int(ia[r]), "a"),) if ia[r] >= 0 else ()
@@ -152,7 +163,7 @@ class JoinDiff:
                 pair=SubgraphPair(nodes_a=na, nodes_b=nb), energy_a=float(ea[r]),
                 energy_b=float(eb[r]), energy_ratio=float(h["ratio"][r]),
                 latency_a=int(la[r]), latency_b=int(lb[r]),
-                output_rel_diff=0.0, verdict=VERDICTS[h["verdict"][r]], category="unknown",
+                output_rel_diff=0.0, verdict=VERDICTS[h["verdict"][r]], category=cats[r],
                 wasteful_side=SIDES[h["side"][r]], wasted_joules=float(h["wasted"][r]),
                 informational=bool(h["informational"][r])))
         return out
@@ -271,7 +282,8 @@ def join_report(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger
     wasted_joules / end_to_end_waste_pct cover every waste finding."""
     jd = join_diff(trace_a, trace_b, ledger_a, ledger_b, threshold, k)
     ca, cb = TraceColumns.from_trace(trace_a), TraceColumns.from_trace(trace_b)
-    top = jd.top_findings(ca, cb)
+    top = jd.top_findings(ca, cb, trace_a=None if isinstance(trace_a, TraceColumns) else trace_a,
+                          trace_b=None if isinstance(trace_b, TraceColumns) else trace_b)
     ineff = max(ledger_a.total_joules, ledger_b.total_joules)
     pct = jd.wasted_joules / ineff if ineff > 0 else 0.0
     rep = Report(findings=tuple(top), total_a=ledger_a.total_joules, total_b=ledger_b.total_joules,

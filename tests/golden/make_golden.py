@@ -386,8 +386,53 @@ def replay_vectors(ref):
     return out
 
 
+def classify_vectors(ref):
+    """Reference detect.classify (src/detect.py:137-172), which detect_waste
+    applies to every waste finding (:127-128), on the presets and a fuzz
+    corpus: the two traces as JSONL lines (the reference's own writer) and,
+    per finding in detect_waste order, (nodes_a, nodes_b, verdict, side,
+    category, forced_gap_joules of the wasteful side)."""
+    import tempfile
+
+    import diffwatt.diagnose as dg
+
+    def gaps(f, ta, tb):  # forced_gap_joules of the wasteful side (diagnose.py:372-387)
+        if f.verdict != "waste":
+            return None
+        tr, nodes = (ta, f.pair.nodes_a) if f.wasteful_side == "A" else (tb, f.pair.nodes_b)
+        return dg.forced_gap_joules(tr, list(nodes))
+
+    sim = ref.simulate
+    cases = [(p, sim.preset(p)) for p in ("tf32_misconfig", "join_redundant", "fused_api_misuse",
+                                           "layout_null", "attention_block")]
+    cases += [(f"fuzz_{i:02d}", m) for i, m in enumerate(sim.fuzz(20260808, 40))]
+    out = {}
+    tmp = Path(tempfile.mkdtemp())
+    for name, manifest in cases:
+        pa, pb = sim.write_scenario(manifest, str(tmp / name))
+        ta, tb = ref.tm.load_trace(pa), ref.tm.load_trace(pb)
+        la, lb = ref.energy.build_ledger(ta), ref.energy.build_ledger(tb)
+        g_a, g_b = ref.graph.build_graph(ta), ref.graph.build_graph(tb)
+        eq, _ = ref.sm.match_tensors(g_a, g_b)
+        res = ref.sm.recursive_match(g_a, g_b, eq)
+        fs = ref.detect.detect_waste(res.pairs, la, lb, 0.10, trace_a=ta, trace_b=tb)
+        out[name] = {
+            "a": open(pa).read().splitlines(), "b": open(pb).read().splitlines(),
+            "findings": [[list(f.pair.nodes_a), list(f.pair.nodes_b), f.verdict, f.wasteful_side,
+                          f.category, gaps(f, ta, tb)] for f in fs],
+        }
+    return out
+
+
 def main():
     ref = _import_reference()
+    if "--classify" in sys.argv:
+        t0 = time.time()
+        import gzip
+        with gzip.open(OUT / "classify.json.gz", "wt") as fh:
+            json.dump(classify_vectors(ref), fh, sort_keys=True)
+        print(f"classify done [{time.time() - t0:.1f}s]")
+        return
     if "--replay" in sys.argv:
         t0 = time.time()
         np.savez_compressed(OUT / "replay.npz", **replay_vectors(ref))

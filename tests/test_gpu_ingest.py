@@ -50,6 +50,7 @@ def _same(a: TraceColumns, b: TraceColumns):
     assert list(a.op_ids) == list(b.op_ids)
     assert list(a.k_ids) == list(b.k_ids)
     assert list(a.op_names) == list(b.op_names)
+    assert list(a.k_names) == list(b.k_names)
 
 
 def test_canonical_scale_trace_parses_on_device(tmp_path):
