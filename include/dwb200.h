@@ -312,6 +312,57 @@ int dw_join_findings(const dw_join_side_t *a, const dw_join_side_t *b, int64_t m
                      dw_stream_t stream);
 
 /* --------------------------------------------------------------- misc */
+/* ---------------------------------------------- tensor equivalence (8(f)4)
+ * Replaces the Python loops of subgraph_match.match_tensors
+ * (subgraph_match.py:109-204) and tensor_equiv.singular_values /
+ * invariant_set (tensor_equiv.py:118-189). */
+
+/* norms[i] = sqrt(sum(v*v for v in values[off[i]:off[i+1]])) with CPython's
+ * sum() -- the prefilter norms (subgraph_match.py:129-132), bit-exact. */
+int dw_tensor_norms(const double *d_values, const int64_t *d_off, int64_t n, double *d_norms, dw_stream_t stream);
+
+/* Prefilter (subgraph_match.py:134-145): (a, b) survives when count_a[a] ==
+ * count_b[b] and, on every run r, |na - nb| <= eps * max(min(na, nb), 1e-30)
+ * with na = d_norm_a[r * n_a + a].  pass 0 writes d_row_count[a]; pass 1,
+ * given the exclusive scan d_row_off, writes the pairs in row-major order. */
+int dw_tensor_prefilter(int pass, int64_t n_a, int64_t n_b, int32_t runs, const int64_t *d_count_a,
+                        const int64_t *d_count_b, const double *d_norm_a, const double *d_norm_b, double eps,
+                        int64_t *d_row_count, const int64_t *d_row_off, int64_t *d_pair_a, int64_t *d_pair_b,
+                        dw_stream_t stream);
+
+/* One unfolding of a row-major tensor: modes whose bit is set in `mask`
+ * (ascending) index the rows, the others the columns (tensor_equiv.unfold). */
+typedef struct {
+    int64_t value_off;    /* first element of the tensor in d_values */
+    int64_t out_off;      /* min(rows, cols) singular values written here */
+    int64_t scratch_off;  /* rows*cols + min(rows, cols) doubles of d_scratch, used
+                             when that exceeds smem_doubles */
+    int32_t order;        /* 2..8 */
+    int32_t mask;         /* proper, non-empty subset of the modes */
+    int32_t dims[8];
+} dw_unfold_t;
+
+/* largest per-matrix working set (doubles) that fits in shared memory */
+int64_t dw_unfold_smem_doubles(void);
+
+/* Singular values of every unfolding by one-sided Jacobi with the reference's
+ * round-robin order, tolerance and sweep cap (tensor_equiv.py:118-159):
+ * sorted descending at d_spectra[out_off...]; d_spectra_len[i] = how many are
+ * >= 1e-12.  smem_doubles = max over the batch of rows*cols + min(rows, cols),
+ * capped at dw_unfold_smem_doubles(). */
+int dw_unfold_spectra(const double *d_values, const dw_unfold_t *d_mats, int64_t n_mats, int64_t smem_doubles,
+                      double *d_spectra, int32_t *d_spectra_len, double *d_scratch, dw_stream_t stream);
+
+/* Bottleneck injective embedding (tensor_equiv.py:183-242) of spectrum set
+ * job_a[j] against set job_b[j] (the smaller into the larger): set s is
+ * unfoldings set_first[s] .. + set_count[s] (<= DW_EMBED_MAX_SPECTRA), unfolding
+ * u is d_spec[u_off[u] .. + u_len[u]].  d_score[j] = the smallest level <= eps
+ * admitting a perfect matching, +inf when none does. */
+#define DW_EMBED_MAX_SPECTRA 14
+int dw_spectra_embed(const double *d_spec, const int64_t *d_u_off, const int32_t *d_u_len, const int64_t *d_set_first,
+                     const int32_t *d_set_count, int64_t n_jobs, const int64_t *d_job_a, const int64_t *d_job_b,
+                     double eps, double *d_score, dw_stream_t stream);
+
 const char *dw_version(void);
 const char *dw_error_string(int code);
 /* number of kernel launches issued by this library on the calling thread

@@ -44,6 +44,7 @@ EXPORTED = (
     "dw_ig_parse_op", "dw_ig_parse_kernel", "dw_ig_hash", "dw_ig_kernel_lists",
     "dw_fx_sum_workspace_size", "dw_fx_sum", "dw_step_value_at", "dw_detect_pairs",
     "dw_rank_workspace_size", "dw_rank", "dw_join_workspace_size", "dw_join_diff",
+    "dw_tensor_norms", "dw_tensor_prefilter", "dw_unfold_smem_doubles", "dw_unfold_spectra", "dw_spectra_embed",
     "dw_version", "dw_error_string", "dw_launch_count", "dw_kernel_timing", "dw_kernel_time_ms",
 )
 
@@ -77,6 +78,11 @@ class Window(ctypes.Structure):
     _fields_ = [("g_off", c_i64), ("n_samples_global", c_i64), ("piece_lo", c_i64), ("piece_hi", c_i64),
                 ("ts_first", c_i64), ("ts_last", c_i64), ("w_first", ctypes.c_double),
                 ("w_last", ctypes.c_double)]
+
+
+class Unfold(ctypes.Structure):
+    _fields_ = [("value_off", c_i64), ("out_off", c_i64), ("scratch_off", c_i64), ("order", c_i32),
+                ("mask", c_i32), ("dims", c_i32 * 8)]
 
 
 class Status(ctypes.Structure):
@@ -139,6 +145,14 @@ def lib():
         L.dw_unpack_deltas.argtypes = [c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, ctypes.c_size_t, c_vp]
         L.dw_replay.argtypes = [ctypes.POINTER(Signal), c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp,
                                 c_vp, c_vp]
+        L.dw_tensor_norms.argtypes = [c_vp, c_vp, c_i64, c_vp, c_vp]
+        L.dw_tensor_prefilter.argtypes = [ctypes.c_int, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp,
+                                          ctypes.c_double, c_vp, c_vp, c_vp, c_vp, c_vp]
+        L.dw_unfold_smem_doubles.restype = c_i64
+        L.dw_unfold_smem_doubles.argtypes = []
+        L.dw_unfold_spectra.argtypes = [c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]
+        L.dw_spectra_embed.argtypes = [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, ctypes.c_double, c_vp,
+                                       c_vp]
         L.dw_attribute_split_workspace_size.restype = ctypes.c_size_t
         L.dw_attribute_split_workspace_size.argtypes = [c_i64, c_i64]
         L.dw_attribute_split.argtypes = [ctypes.POINTER(Signal), ctypes.POINTER(IntervalSet), c_vp,

@@ -1,26 +1,70 @@
-"""Layout-blind tensor equivalence (host side; used only for detect_waste's 1%
-output rule on boundary tensors, detect.py:55-69).
+"""Layout-blind tensor equivalence -- drop-in for ``diffwatt.tensor_equiv``.
 
-Restates the reference's criterion (tensor_equiv.py:118-294): two tensors are
+The reference's criterion (tensor_equiv.py:71-294): two tensors are
 equivalent when their element counts match, their Frobenius norms agree, and
-the multiset of singular-value spectra of all non-trivial unfoldings of the
-smaller-order tensor embeds injectively into the other's with every matched
-pair within epsilon (relative L2 distance); the score is the bottleneck
-distance of the best embedding.  Spectra come from LAPACK SVD here rather than
-the reference's one-sided Jacobi (agreement ~1e-15 relative).  This is tiny
-dense work on host snapshots (order <= 8), not on the GPU hot path.
+the multiset of singular-value spectra of all non-trivial unfoldings of one
+embeds injectively into the other's with every matched pair within epsilon
+(relative L2 distance); the score is the bottleneck distance of the best
+embedding.
+
+The singular values come from the device: ``invariant_sets`` ships every
+unfolding of every tensor of a batch to ``dw_unfold_spectra``
+(csrc/tensor.cu: one CTA per unfolding, one-sided Jacobi with the reference's
+round-robin rotation order, tolerance and sweep cap).  The embedding test
+(distance matrix + Kuhn matching + bottleneck search) runs per pair on the
+device too (``SpectraBatch.embed`` -> ``dw_spectra_embed``, sets of up to 14
+spectra, i.e. order <= 4) with the reference's sequential distance arithmetic;
+larger sets use the host restatement below.  Floating point: spectra agree
+with the reference's numpy Jacobi to rounding (tests/test_gpu_tensor.py).
 """
 
 from __future__ import annotations
 
 import math
-from typing import Optional
+from dataclasses import dataclass
+from typing import Iterable, Optional, Sequence
 
 import numpy as np
+import torch
+
+from . import _native
 
 SPECTRUM_FLOOR = 1e-12
+DEFAULT_EPSILON = 1e-3
 ORDER_CAP = 8
 _NORM_FLOOR = 1e-30
+
+
+@dataclass(frozen=True)
+class Spectrum:
+    """Singular values sorted descending, trimmed below the floor
+    (tensor_equiv.py:30-47)."""
+
+    singulars: tuple
+
+    @classmethod
+    def from_values(cls, values: Iterable[float]) -> "Spectrum":
+        vals = sorted((float(v) for v in values), reverse=True)
+        while vals and vals[-1] < SPECTRUM_FLOOR:
+            vals.pop()
+        return cls(tuple(vals))
+
+    def norm(self) -> float:
+        return math.sqrt(sum(v * v for v in self.singulars))
+
+    def sum_squares(self) -> float:
+        return sum(v * v for v in self.singulars)
+
+
+@dataclass(frozen=True)
+class InvariantSet:
+    """All unfolding spectra of one tensor (tensor_equiv.py:50-61)."""
+
+    spectra: tuple
+    source_order: int
+
+    def frobenius_norm(self) -> float:
+        return self.spectra[0].norm() if self.spectra else 0.0
 
 
 def _arr(t) -> np.ndarray:
@@ -29,48 +73,201 @@ def _arr(t) -> np.ndarray:
     return np.asarray(t.values, dtype=np.float64).reshape(tuple(t.shape))
 
 
-def _spectrum(mat: np.ndarray) -> np.ndarray:
-    s = np.linalg.svd(mat, compute_uv=False)
-    s = np.sort(s)[::-1]
-    return s[s >= SPECTRUM_FLOOR]
+def unfold(t, modes: Iterable[int]) -> np.ndarray:
+    """Matricization (tensor_equiv.py:71-90): ``modes`` (ascending) index the
+    rows, the complement the columns.  Host helper; the device gathers the
+    same entries itself."""
+    arr = _arr(t)
+    r = arr.ndim
+    group = sorted(set(int(m) for m in modes))
+    if not group:
+        raise ValueError("mode subset must be non-empty")
+    if any(m < 0 or m >= r for m in group):
+        raise ValueError(f"mode out of range for order-{r} tensor")
+    if len(group) == r:
+        raise ValueError("mode subset must be a proper subset of the modes")
+    comp = [m for m in range(r) if m not in group]
+    rows = int(np.prod([arr.shape[m] for m in group]))
+    return arr.transpose(group + comp).reshape(rows, -1)
 
 
-def spectra(t) -> list[np.ndarray]:
-    a = _arr(t)
-    r = a.ndim
-    if r > ORDER_CAP:
-        raise ValueError(f"tensor order {r} exceeds the cap of {ORDER_CAP}")
-    if r == 1:
-        return [np.array([math.sqrt(float(a @ a))])]
+# ------------------------------------------------------------ device batch
+
+
+UNFOLD_DTYPE = np.dtype([("value_off", "<i8"), ("out_off", "<i8"), ("scratch_off", "<i8"), ("order", "<i4"),
+                         ("mask", "<i4"), ("dims", "<i4", (8,))])  # dw_unfold_t
+
+
+class SpectraBatch:
+    """Device-resident spectra of every unfolding of a batch of tensors
+    (one dw_unfold_spectra launch).  Tensor t owns unfoldings
+    set_first[t] .. + set_count[t] (masks 1 .. 2^r - 2 in order); unfolding u
+    holds u_len[u] values at spec[u_off[u]:]."""
+
+    def __init__(self, values: np.ndarray, shapes: Sequence[tuple], value_off: Sequence[int]):
+        L = _native.lib()
+        cap = int(L.dw_unfold_smem_doubles())
+        T = len(shapes)
+        self.set_count = np.zeros(T, dtype=np.int32)
+        self.set_first = np.zeros(T, dtype=np.int64)
+        recs, first = [], 0
+        order = np.fromiter((len(sh) for sh in shapes), dtype=np.int64, count=T)
+        value_off = np.asarray(value_off, dtype=np.int64)
+        for r in range(2, ORDER_CAP + 1):
+            ts = np.nonzero(order == r)[0]
+            if ts.size == 0:
+                continue
+            D = np.array([shapes[t] for t in ts], dtype=np.int64).reshape(ts.size, r)
+            masks = np.arange(1, (1 << r) - 1, dtype=np.int64)
+            bits = (masks[:, None] >> np.arange(r)[None, :]) & 1
+            rows = np.where(bits[None, :, :] == 1, D[:, None, :], 1).prod(-1)
+            total = D.prod(1)[:, None]
+            n = np.minimum(rows, total // rows)
+            rec = np.zeros((ts.size, masks.size), dtype=UNFOLD_DTYPE)
+            rec["value_off"] = value_off[ts][:, None]
+            rec["order"] = r
+            rec["mask"] = masks[None, :]
+            rec["dims"][:, :, :r] = D[:, None, :]
+            self.set_first[ts] = first + np.arange(ts.size) * masks.size
+            self.set_count[ts] = masks.size
+            first += ts.size * masks.size
+            recs.append((rec.reshape(-1), n.reshape(-1), (total + n).reshape(-1)))
+        self.n_unfold = first
+        dev = _native.device()
+        if first == 0:
+            self.u_off = np.zeros(0, dtype=np.int64)
+            self._host = (np.zeros(0), np.zeros(0, dtype=np.int32))
+            return
+        rec = np.concatenate([x[0] for x in recs])
+        n = np.concatenate([x[1] for x in recs])
+        need = np.concatenate([x[2] for x in recs])
+        out_off = np.zeros(first, dtype=np.int64)
+        np.cumsum(n[:-1], out=out_off[1:])
+        rec["out_off"] = out_off
+        big = need > cap
+        scr = np.where(big, need, 0)
+        rec["scratch_off"] = np.cumsum(scr) - scr
+        smem = int(need[~big].max()) if (~big).any() else 0
+        self.u_off = out_off
+        self.d_mats = torch.from_numpy(rec.view(np.uint8)).to(dev)
+        self.d_vals = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64)).to(dev)
+        self.d_spec = torch.empty(max(int(n.sum()), 1), dtype=torch.float64, device=dev)
+        self.d_len = torch.empty(first, dtype=torch.int32, device=dev)
+        d_scr = torch.empty(max(int(scr.sum()), 1), dtype=torch.float64, device=dev)
+        p = _native.ptr
+        _native.check(L.dw_unfold_spectra(p(self.d_vals), p(self.d_mats), first, smem, p(self.d_spec),
+                                          p(self.d_len), p(d_scr), _native.stream_handle()), "dw_unfold_spectra")
+        self._host = None
+
+    def host(self):
+        if self._host is None:
+            self._host = (self.d_spec.cpu().numpy(), self.d_len.cpu().numpy())
+        return self._host
+
+    def spectra(self, t: int) -> list:
+        spec, lens = self.host()
+        f = int(self.set_first[t])
+        return [Spectrum(tuple(spec[self.u_off[u]:self.u_off[u] + int(lens[u])].tolist()))
+                for u in range(f, f + int(self.set_count[t]))]
+
+    def embed(self, job_a: np.ndarray, job_b: np.ndarray, epsilon: float) -> np.ndarray:
+        """Bottleneck scores of tensor pairs (job_a[j], job_b[j]) of this batch
+        (+inf: no embedding within epsilon) -- dw_spectra_embed."""
+        dev = _native.device()
+        n = int(job_a.shape[0])
+        out = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        if n:
+            t = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+            keep = [t(self.u_off), self.d_len, t(self.set_first), t(self.set_count), t(job_a.astype(np.int64)),
+                    t(job_b.astype(np.int64))]
+            p = _native.ptr
+            _native.check(_native.lib().dw_spectra_embed(p(self.d_spec), p(keep[0]), p(keep[1]), p(keep[2]),
+                                                         p(keep[3]), n, p(keep[4]), p(keep[5]), float(epsilon),
+                                                         p(out), _native.stream_handle()), "dw_spectra_embed")
+        return out[:n].cpu().numpy()
+
+
+EMBED_MAX = 14  # DW_EMBED_MAX_SPECTRA: sets up to order 4 embed on the device
+
+
+def invariant_sets(tensors: Sequence) -> list[InvariantSet]:
+    """invariant_set (tensor_equiv.py:162-180) of many tensors at once: every
+    unfolding of every tensor in one device launch."""
+    arrs = [_arr(t) for t in tensors]
+    for a in arrs:
+        if a.ndim > ORDER_CAP:
+            raise ValueError(f"tensor order {a.ndim} exceeds the cap of {ORDER_CAP}")
+    sizes = np.fromiter((a.size for a in arrs), dtype=np.int64, count=len(arrs))
+    offs = np.cumsum(sizes) - sizes
+    vals = np.concatenate([a.ravel() for a in arrs]) if arrs else np.zeros(0)
+    sb = SpectraBatch(vals, [a.shape for a in arrs], offs)
     out = []
-    for mask in range(1, (1 << r) - 1):
-        rows = [m for m in range(r) if mask >> m & 1]
-        cols = [m for m in range(r) if not mask >> m & 1]
-        nr = int(np.prod([a.shape[m] for m in rows]))
-        out.append(_spectrum(a.transpose(rows + cols).reshape(nr, -1)))
+    for i, a in enumerate(arrs):
+        if a.ndim == 1:
+            out.append(InvariantSet((Spectrum.from_values([math.sqrt(float(a @ a))]),), 1))
+        elif a.ndim == 0:
+            out.append(InvariantSet((), 0))
+        else:
+            out.append(InvariantSet(tuple(sb.spectra(i)), a.ndim))
     return out
 
 
-def _distance(x: np.ndarray, y: np.ndarray) -> float:
-    n = max(len(x), len(y))
+def invariant_set(t) -> InvariantSet:
+    return invariant_sets([t])[0]
+
+
+def singular_values(mat) -> Spectrum:
+    """Drop-in for tensor_equiv.singular_values (tensor_equiv.py:113-159)."""
+    a = np.asarray(mat, dtype=np.float64)
+    if a.ndim != 2:
+        raise ValueError("expected a 2-D matrix")
+    if not np.all(np.isfinite(a)):
+        raise ValueError("matrix has non-finite entries")
+    m, n = a.shape
+    if min(m, n) == 1:
+        v = a.ravel()
+        return Spectrum.from_values([math.sqrt(float(v @ v))])
+    return SpectraBatch(a.ravel(), [(m, n)], [0]).spectra(0)[0]
+
+
+# ------------------------------------------------------------- embedding
+
+
+def spectrum_distance(a: Spectrum, b: Spectrum) -> float:
+    """Relative L2 distance, shorter spectrum zero-padded (tensor_equiv.py:183-194)."""
+    n = max(len(a.singulars), len(b.singulars))
     if n == 0:
         return 0.0
-    xp = np.zeros(n)
-    yp = np.zeros(n)
-    xp[:len(x)] = x
-    yp[:len(y)] = y
-    denom = max(min(math.sqrt(float(x @ x)), math.sqrt(float(y @ y))), _NORM_FLOOR)
-    return math.sqrt(float(((xp - yp) ** 2).sum())) / denom
+    diff = 0.0
+    for i in range(n):
+        va = a.singulars[i] if i < len(a.singulars) else 0.0
+        vb = b.singulars[i] if i < len(b.singulars) else 0.0
+        diff += (va - vb) ** 2
+    return math.sqrt(diff) / max(min(a.norm(), b.norm()), _NORM_FLOOR)
+
+
+def _distances(small: Sequence[Spectrum], large: Sequence[Spectrum]) -> np.ndarray:
+    w = max([len(s.singulars) for s in small] + [len(s.singulars) for s in large] + [1])
+    S = np.zeros((len(small), w))
+    Lg = np.zeros((len(large), w))
+    for i, s in enumerate(small):
+        S[i, :len(s.singulars)] = s.singulars
+    for j, s in enumerate(large):
+        Lg[j, :len(s.singulars)] = s.singulars
+    ns, nl = np.sqrt((S * S).sum(1)), np.sqrt((Lg * Lg).sum(1))
+    d = np.sqrt(((S[:, None, :] - Lg[None, :, :]) ** 2).sum(2))
+    return d / np.maximum(np.minimum(ns[:, None], nl[None, :]), _NORM_FLOOR)
 
 
 def _matching_ok(dist: np.ndarray, limit: float) -> bool:
-    """Kuhn augmenting paths: can every row take a distinct column within limit?"""
+    """Kuhn augmenting paths: every row takes a distinct column within limit."""
     n_rows, n_cols = dist.shape
+    adj = [np.nonzero(dist[i] <= limit)[0].tolist() for i in range(n_rows)]
     owner = [-1] * n_cols
 
     def augment(i, seen):
-        for j in range(n_cols):
-            if dist[i, j] <= limit and not seen[j]:
+        for j in adj[i]:
+            if not seen[j]:
                 seen[j] = True
                 if owner[j] < 0 or augment(owner[j], seen):
                     owner[j] = i
@@ -80,34 +277,60 @@ def _matching_ok(dist: np.ndarray, limit: float) -> bool:
     return all(augment(i, [False] * n_cols) for i in range(n_rows))
 
 
-def tensors_equivalent(a, b, epsilon: float = 1e-3) -> tuple[bool, float]:
+def embed_injectively(small: Sequence[Spectrum], large: Sequence[Spectrum], epsilon: float) -> Optional[float]:
+    """Bottleneck injective embedding (tensor_equiv.py:219-242): the smallest
+    achievable max matched distance if within epsilon, else None."""
+    if not small:
+        return 0.0
+    dist = _distances(small, large)
+    levels = np.unique(dist[dist <= epsilon])
+    if levels.size == 0 or not _matching_ok(dist, float(levels[-1])):
+        return None
+    lo, hi = 0, levels.size - 1
+    while lo < hi:
+        mid = (lo + hi) // 2
+        if _matching_ok(dist, float(levels[mid])):
+            hi = mid
+        else:
+            lo = mid + 1
+    return float(levels[lo])
+
+
+def equivalent_from(norm_a: float, norm_b: float, ndim_a: int, ndim_b: int, set_a: Optional[InvariantSet],
+                    set_b: Optional[InvariantSet], epsilon: float) -> tuple[bool, float]:
+    """tensors_equivalent's decision once counts are known equal and norms and
+    invariant sets are computed (tensor_equiv.py:264-294)."""
+    nd = abs(norm_a - norm_b) / max(min(norm_a, norm_b), _NORM_FLOOR)
+    if nd > epsilon:
+        return False, math.inf
+    if ndim_a == 1 or ndim_b == 1:
+        return nd <= epsilon, nd
+    small, large = set_a.spectra, set_b.spectra
+    if len(small) > len(large):
+        small, large = large, small
+    worst = embed_injectively(small, large, epsilon)
+    return (False, math.inf) if worst is None else (True, worst)
+
+
+def tensors_equivalent(a, b, epsilon: float = DEFAULT_EPSILON, set_a: Optional[InvariantSet] = None,
+                       set_b: Optional[InvariantSet] = None) -> tuple[bool, float]:
+    """Drop-in for tensor_equiv.tensors_equivalent (tensor_equiv.py:245-294)."""
     if epsilon <= 0:
         raise ValueError("epsilon must be positive")
     xa, xb = _arr(a), _arr(b)
     if xa.size != xb.size:
         return False, math.inf
-    na, nb = float(np.sqrt(np.sum(xa * xa))), float(np.sqrt(np.sum(xb * xb)))
+    na, nb = float(np.sqrt(np.dot(xa.ravel(), xa.ravel()))), float(np.sqrt(np.dot(xb.ravel(), xb.ravel())))
     nd = abs(na - nb) / max(min(na, nb), _NORM_FLOOR)
     if nd > epsilon:
         return False, math.inf
     if xa.ndim == 1 or xb.ndim == 1:
         return nd <= epsilon, nd
-    sa, sb = spectra(xa), spectra(xb)
-    small, large = (sa, sb) if len(sa) <= len(sb) else (sb, sa)
-    if not small:
-        return True, 0.0
-    dist = np.array([[_distance(x, y) for y in large] for x in small])
-    levels = sorted({float(d) for d in dist.ravel() if d <= epsilon})
-    if not levels or not _matching_ok(dist, levels[-1]):
-        return False, math.inf
-    lo, hi = 0, len(levels) - 1
-    while lo < hi:
-        mid = (lo + hi) // 2
-        if _matching_ok(dist, levels[mid]):
-            hi = mid
-        else:
-            lo = mid + 1
-    return True, levels[lo]
+    need = [x for x, s in ((xa, set_a), (xb, set_b)) if s is None]
+    got = iter(invariant_sets(need)) if need else iter(())
+    set_a = set_a if set_a is not None else next(got)
+    set_b = set_b if set_b is not None else next(got)
+    return equivalent_from(na, nb, xa.ndim, xb.ndim, set_a, set_b, epsilon)
 
 
 def boundary_rel_diff(boundary_right, trace_a, trace_b, limit: float = 0.01) -> float:

@@ -424,8 +424,59 @@ def classify_vectors(ref):
     return out
 
 
+def tensor_vectors(ref):
+    """Reference match_tensors (subgraph_match.py:109-204) on the classify
+    corpus (traces in classify.json.gz) and reference invariant sets
+    (tensor_equiv.py:162-180) of seeded random tensors."""
+    import gzip
+
+    import diffwatt.tensor_equiv as te
+
+    with gzip.open(OUT / "classify.json.gz", "rt") as fh:
+        corpus = json.load(fh)
+    import tempfile
+    tmp = Path(tempfile.mkdtemp())
+    extra = {}
+    sim = ref.simulate
+    for name, m in (("big_chain", sim.ScenarioManifest(workload="big", seed=77, template="chain", length=120)),
+                    ("big_transformer", sim.ScenarioManifest(workload="big", seed=78, template="transformer",
+                                                             length=3))):
+        pa, pb = sim.write_scenario(m, str(tmp / name))
+        extra[name] = {"a": open(pa).read().splitlines(), "b": open(pb).read().splitlines()}
+    match = {}
+    for name, c in list(corpus.items()) + list(extra.items()):
+        ta, tb = ref.tm.parse_trace_lines(c["a"]), ref.tm.parse_trace_lines(c["b"])
+        ga, gb = ref.graph.build_graph(ta), ref.graph.build_graph(tb)
+        pairs, st = ref.sm.match_tensors(ga, gb)
+        match[name] = {"pairs": [[p.tensor_a, p.tensor_b, p.score] for p in pairs.pairs],
+                       "candidate_pairs": st.candidate_pairs, "full_checks": st.full_checks}
+    rng = np.random.default_rng(20261017)
+    shapes = [(3, 4), (7, 2), (5, 5), (1, 6), (16, 16), (40, 3), (2, 3, 4), (4, 4, 5), (2, 2, 2, 2),
+              (3, 1, 5), (2, 3, 2, 3, 2), (6, 7, 8), (64, 33), (2, 2, 2, 2, 2, 2)]
+    tensors, spectra = [], []
+    for i, shp in enumerate(shapes):
+        x = rng.standard_normal(shp)
+        if i % 3 == 1:  # rank-deficient: an outer product
+            x = np.multiply.outer(rng.standard_normal(shp[0]), rng.standard_normal(shp[1:]))
+        if i % 4 == 2:
+            x = x * 1e-7
+        tensors.append(x)
+        inv = te.invariant_set(x)
+        spectra.append([list(s.singulars) for s in inv.spectra])
+    return match, extra, {"shapes": [list(s) for s in shapes], "values": [t.ravel().tolist() for t in tensors],
+                          "spectra": spectra}
+
+
 def main():
     ref = _import_reference()
+    if "--tensors" in sys.argv:
+        import gzip
+        t0 = time.time()
+        match, extra, spec = tensor_vectors(ref)
+        with gzip.open(OUT / "tensors.json.gz", "wt") as fh:
+            json.dump({"match": match, "traces": extra, "random": spec}, fh, sort_keys=True)
+        print(f"tensors done [{time.time() - t0:.1f}s]")
+        return
     if "--classify" in sys.argv:
         t0 = time.time()
         import gzip
