@@ -336,11 +336,16 @@ def run_ours(args, rank: int, world: int, local: int):
                 return h
             hc = PackedColumns(pc.ts_base, pin(pc.ts), pin(pc.watts), pc.op_start_base, pin(pc.op_start),
                                pin(pc.op_end), pc.k_start_base, pin(pc.k_start), pin(pc.k_end), c.trace_end,
-                               op_sig=pin(pc.op_sig))
+                               op_sig=pin(pc.op_sig), watts_p0=pc.watts_p0)
             hc._dev["first_last"] = c._first_last_ts()
             pinned.append(hc)
             del pc
         h2d = sum(pc.host_bytes for pc in pinned)
+        pc0 = pinned[0]
+        host_format = (f"packed columns: ts deltas u{8 * pc0.ts.element_size()}, interval deltas/durations "
+                       f"u{8 * pc0.op_start.element_size()}/u{8 * pc0.op_end.element_size()} (ops) "
+                       f"u{8 * pc0.k_start.element_size()}/u{8 * pc0.k_end.element_size()} (kernels), watts "
+                       + ("9-digit decimal codes u32" if pc0.watts_p0 is not None else "f64") + ", sig u64")
         for c in (ca, cb):
             c._dev.clear()
         del ca, cb
@@ -353,17 +358,23 @@ def run_ours(args, rank: int, world: int, local: int):
             r = analyze(pinned[0], pinned[1], args.method, 0.10, args.k, copy_stream=copy_stream)
             return r
 
-        e2e_step()
+        for _ in range(max(3, args.warmup)):  # the first steps run ~50 % slower (allocator, pinned pages)
+            e2e_step()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.e2e_steps)]
         f0.record()
-        for _ in range(args.e2e_steps):
+        for i in range(args.e2e_steps):
             r = e2e_step()
+            marks[i].record()
         f1.record()
         torch.cuda.synchronize()
         e_ms = f0.elapsed_time(f1) / args.e2e_steps
+        if os.environ.get("DWB200_E2E_DEBUG"):
+            prev = [f0] + marks[:-1]
+            print("e2e steps ms:", [round(a.elapsed_time(b), 1) for a, b in zip(prev, marks)], file=sys.stderr)
         te = torch.tensor([e_ms], device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -372,7 +383,7 @@ def run_ours(args, rank: int, world: int, local: int):
         e2e = {"value": world * intervals / (float(te.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": float(te.item()),
-               "host_format": "packed columns (uint32 ts deltas, uint32 interval durations, f64 watts, u64 sig)",
+               "host_format": host_format,
                "overlap": "trace B H2D + decode under trace A attribution"}
 
     if rank != 0:

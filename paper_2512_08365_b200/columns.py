@@ -16,6 +16,7 @@ scale workloads can be constructed directly from device tensors.
 
 from __future__ import annotations
 
+import math
 import weakref
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -213,35 +214,47 @@ _CACHE_MAX = 32
 # ------------------------------------------------------------- packed columns
 
 
-class PackedColumns(TraceColumns):
-    """A trace whose sorted timestamp columns travel as 32-bit deltas and whose
-    interval ends travel as 32-bit durations.
+def _unsigned(d):
+    """int64 values of a 16/32-bit unsigned column held in a signed or
+    unsigned container (torch or numpy)."""
+    if isinstance(d, torch.Tensor):
+        mask = 0xFFFF if d.element_size() == 2 else 0xFFFFFFFF
+        return d.to(torch.int64) & mask
+    d = np.asarray(d)
+    return d.view(np.uint16 if d.itemsize == 2 else np.uint32).astype(np.int64)
 
-    Host bytes per sample 16 -> 12, per interval 16 -> 8: the host->HBM copy
-    bounds the end-to-end path, so this is what a deployment ships (and what
-    ``save_packed`` writes).  ``device(name)`` decodes on the GPU
-    (``dw_unpack_deltas``: one scan per column) and caches the full columns.
-    Host attributes: ``ts``/``op_start``/``k_start`` hold the uint32 deltas
-    (``*_base`` the first value), ``op_end``/``k_end`` the uint32 durations.
+
+class PackedColumns(TraceColumns):
+    """A trace whose sorted timestamp columns travel as deltas, whose interval
+    ends travel as durations and whose watts travel as 9-digit decimal codes
+    (DESIGN.md "packed columns").
+
+    Each delta / duration column is 16-bit when every value fits, else 32-bit;
+    watts are uint32 codes (``watts_p0`` set, ``dw_unpack_decimal``) when every
+    sample is a 9-significant-digit decimal -- the trace format's on-disk
+    precision (trace_model.py:63-65) -- else f64.  At C4: host bytes per
+    sample 16 -> 6, per interval 16 -> 4.  The host->HBM copy bounds the
+    end-to-end path, so this is what a deployment ships (and what
+    ``save_packed`` writes).  ``device(name)`` decodes on the GPU (one scan
+    per timestamp column, one pass for the watts) and caches the full columns.
+    Host attributes: ``ts``/``op_start``/``k_start`` hold the deltas (``*_base``
+    the first value), ``op_end``/``k_end`` the durations.
     """
 
     PACKED = ("ts", "op_start", "k_start")
 
     def __init__(self, ts_base, ts_delta, watts, op_base, op_delta, op_dur, k_base, k_delta, k_dur,
-                 trace_end, k_op=None, op_sig=None, **kw):
+                 trace_end, k_op=None, op_sig=None, watts_p0=None, **kw):
         super().__init__(ts=ts_delta, watts=watts, trace_end=int(trace_end), op_start=op_delta, op_end=op_dur,
                          k_start=k_delta, k_end=k_dur, k_op=k_op, op_sig=op_sig, ops_sorted=True,
                          kernels_sorted=True, **kw)
         self.ts_base, self.op_start_base, self.k_start_base = int(ts_base), int(op_base), int(k_base)
+        self.watts_p0 = None if watts_p0 is None else int(watts_p0)
         self._first_last = None
 
     def _first_last_ts(self) -> tuple[int, int]:
         if "first_last" not in self._dev:
-            d = self.ts
-            if isinstance(d, torch.Tensor):  # uint32 deltas, possibly held in an int32 tensor
-                dd = d.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
-            else:
-                dd = np.asarray(d).view(np.uint32).astype(np.int64)
+            dd = _unsigned(self.ts)
             last = self.ts_base + int(dd.sum())
             first = self.ts_base + int(dd[0])
             self._dev["first_last"] = (first, last)
@@ -251,9 +264,14 @@ class PackedColumns(TraceColumns):
         src = getattr(self, name)
         if isinstance(src, torch.Tensor):
             return src
-        return torch.from_numpy(np.ascontiguousarray(src))
+        a = np.ascontiguousarray(src)
+        if a.dtype in (np.uint16, np.uint32):  # same bits in the signed type torch handles everywhere
+            a = a.view(np.int16 if a.itemsize == 2 else np.int32)
+        return torch.from_numpy(a)
 
     def device(self, name: str) -> torch.Tensor:
+        if name == "watts" and self.watts_p0 is not None:
+            return self._device_watts()
         if name not in ("ts", "op_start", "op_end", "k_start", "k_end"):
             return super().device(name)
         dev = _native.device()
@@ -273,17 +291,31 @@ class PackedColumns(TraceColumns):
         base = {"ts": self.ts_base, "op_start": self.op_start_base, "k_start": self.k_start_base}[base_name]
         L = _native.lib()
         ws = _native.Workspace.get(L.dw_unpack_workspace_size(n))
-        _native.check(L.dw_unpack_deltas(_native.ptr(delta.view(torch.int32)), n, base, _native.ptr(out),
-                                         _native.ptr(dur.view(torch.int32)) if end is not None else None,
-                                         _native.ptr(end), ws.data_ptr(), ws.numel(), _native.stream_handle()),
-                      "dw_unpack_deltas")
+        _native.check(L.dw_unpack_deltas_w(_native.ptr(delta), delta.element_size(), n, base, _native.ptr(out),
+                                           _native.ptr(dur) if end is not None else None,
+                                           dur.element_size() if end is not None else 4, _native.ptr(end),
+                                           ws.data_ptr(), ws.numel(), _native.stream_handle()),
+                      "dw_unpack_deltas_w")
         self._dev[(base_name, dev.index)] = out
         if end is not None:
             self._dev[(dur_name, dev.index)] = end
         return self._dev[key]
 
+    def _device_watts(self) -> torch.Tensor:
+        dev = _native.device()
+        key = ("watts", dev.index)
+        t = self._dev.get(key)
+        if t is None:
+            code = self._raw("watts").to(dev, non_blocking=True)
+            t = torch.empty(code.numel(), dtype=torch.float64, device=dev)
+            _native.check(_native.lib().dw_unpack_decimal(_native.ptr(code), code.numel(), self.watts_p0,
+                                                          _native.ptr(t), _native.stream_handle()),
+                          "dw_unpack_decimal")
+            self._dev[key] = t
+        return t
+
     def host(self, name: str) -> np.ndarray:
-        if name in ("ts", "op_start", "op_end", "k_start", "k_end"):
+        if name in ("ts", "op_start", "op_end", "k_start", "k_end") or (name == "watts" and self.watts_p0 is not None):
             return self.device(name).cpu().numpy()
         return super().host(name)
 
@@ -295,49 +327,102 @@ class PackedColumns(TraceColumns):
             for n in ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "op_sig") if getattr(self, n) is not None)
 
 
+def _narrow(d, what: str):
+    """Unsigned 16-bit container when every value fits, else 32-bit (torch:
+    int16/int32 holding the bit patterns; numpy: uint16/uint32)."""
+    if isinstance(d, torch.Tensor):
+        if d.numel() and (bool((d < 0).any()) or bool((d > 0xFFFFFFFF).any())):
+            raise ValueError(f"{what} -- cannot pack")
+        if d.numel() == 0 or int(d.max().item()) <= 0xFFFF:
+            return torch.where(d >= 0x8000, d - 0x10000, d).to(torch.int16)
+        return torch.where(d >= 0x80000000, d - 0x100000000, d).to(torch.int32)
+    if d.size and ((d < 0).any() or (d > 0xFFFFFFFF).any()):
+        raise ValueError(f"{what} -- cannot pack")
+    return d.astype(np.uint16 if (d.size == 0 or d.max() <= 0xFFFF) else np.uint32)
+
+
 def _deltas(x, what: str):
-    """(base, uint32 deltas) of a sorted int64 column (numpy or torch)."""
+    """(base, deltas) of a sorted int64 column (numpy or torch)."""
     if isinstance(x, torch.Tensor):
         if x.numel() == 0:
-            return 0, torch.zeros(0, dtype=torch.int32, device=x.device)
+            return 0, torch.zeros(0, dtype=torch.int16, device=x.device)
         d = torch.empty_like(x)
         d[0] = 0
         d[1:] = x[1:] - x[:-1]
-        if bool((d < 0).any()) or bool((d > 0xFFFFFFFF).any()):
-            raise ValueError(f"{what}: not sorted, or a gap of 2^32 us or more -- cannot pack")
-        return int(x[0].item()), d.to(torch.int64).to(torch.int32)  # low 32 bits (uint32 stored in int32)
+        return int(x[0].item()), _narrow(d, f"{what}: not sorted, or a gap of 2^32 us or more")
     x = np.asarray(x, dtype=np.int64)
     if x.size == 0:
-        return 0, np.zeros(0, dtype=np.uint32)
-    d = np.diff(x, prepend=x[0])
-    if (d < 0).any() or (d > 0xFFFFFFFF).any():
-        raise ValueError(f"{what}: not sorted, or a gap of 2^32 us or more -- cannot pack")
-    return int(x[0]), d.astype(np.uint32)
+        return 0, np.zeros(0, dtype=np.uint16)
+    return int(x[0]), _narrow(np.diff(x, prepend=x[0]), f"{what}: not sorted, or a gap of 2^32 us or more")
 
 
 def _durations(start, end, what: str):
     if isinstance(start, torch.Tensor):
-        dur = end - start
-        if dur.numel() and (bool((dur < 0).any()) or bool((dur > 0xFFFFFFFF).any())):
-            raise ValueError(f"{what}: negative or >= 2^32 us durations -- cannot pack")
-        return dur.to(torch.int32)
+        return _narrow(end - start, f"{what}: negative or >= 2^32 us durations")
     dur = np.asarray(end, dtype=np.int64) - np.asarray(start, dtype=np.int64)
-    if dur.size and ((dur < 0).any() or (dur > 0xFFFFFFFF).any()):
-        raise ValueError(f"{what}: negative or >= 2^32 us durations -- cannot pack")
-    return dur.astype(np.uint32)
+    return _narrow(dur, f"{what}: negative or >= 2^32 us durations")
 
 
-def pack(cols: TraceColumns) -> PackedColumns:
+_M_LIMIT = 1 << 30
+
+
+def decimal_code(w):
+    """(p0, uint32 codes) encoding every watts value exactly as m * 10^-(p0+j)
+    (m < 2^30, j < 4; decoded by one correctly rounded IEEE operation, as
+    dw_unpack_decimal does), or None when some value is not such a decimal.
+    Works on numpy or torch (cuda) columns."""
+    is_t = isinstance(w, torch.Tensor)
+    n = int(w.numel() if is_t else np.asarray(w).size)
+    if n == 0:
+        return None
+    if is_t:
+        pos = w[w > 0]
+        if bool((w < 0).any()) or not bool(torch.isfinite(w).all()):
+            return None
+        top = float(pos.max().item()) if pos.numel() else 1.0
+    else:
+        w = np.asarray(w, dtype=np.float64)
+        if (w < 0).any() or not np.isfinite(w).all():
+            return None
+        top = float(w.max()) if (w > 0).any() else 1.0
+    p0 = 8 - int(math.floor(math.log10(top)))
+    p0 = max(-22, min(p0, 19))
+    lib = torch if is_t else np
+    code = None
+    done = lib.zeros_like(w, dtype=lib.bool) if is_t else np.zeros(n, dtype=bool)
+    out = (torch.zeros(n, dtype=torch.int64, device=w.device) if is_t else np.zeros(n, dtype=np.int64))
+    for j in range(4):
+        p = p0 + j
+        scale = 10.0 ** abs(p)
+        m = lib.round(w * scale) if p >= 0 else lib.round(w / scale)
+        if is_t:
+            sc = torch.full_like(w, scale)
+            back = torch.div(m, sc) if p >= 0 else m * sc
+        else:
+            back = m / scale if p >= 0 else m * scale
+        ok = (m >= 0) & (m < _M_LIMIT) & (back == w) & ~done
+        mi = m.to(torch.int64) if is_t else m.astype(np.int64)
+        out = lib.where(ok, mi | (j << 30), out)
+        done = done | ok
+    if not bool(done.all()):
+        return None
+    code = (torch.where(out >= 0x80000000, out - 0x100000000, out).to(torch.int32) if is_t
+            else out.astype(np.uint32))
+    return p0, code
+
+
+def pack(cols: TraceColumns, decimal: bool = True) -> PackedColumns:
     """Packed form of a trace with sorted power, operator and kernel starts
     (ValueError otherwise -- keep such traces unpacked).  Works on host or
     device columns; the result lives where the input does."""
-    ts = cols.ts if not isinstance(cols.ts, torch.Tensor) else cols.ts
     tb, td = _deltas(cols.ts, "power timestamps")
     ob, od = _deltas(cols.op_start, "operator starts")
     kb, kd = _deltas(cols.k_start, "kernel starts")
-    return PackedColumns(tb, td, cols.watts, ob, od, _durations(cols.op_start, cols.op_end, "operators"),
+    dec = decimal_code(cols.watts) if decimal else None
+    watts, p0 = (cols.watts, None) if dec is None else (dec[1], dec[0])
+    return PackedColumns(tb, td, watts, ob, od, _durations(cols.op_start, cols.op_end, "operators"),
                          kb, kd, _durations(cols.k_start, cols.k_end, "kernels"), cols.trace_end,
-                         k_op=cols.k_op, op_sig=cols.op_sig, op_ids=cols.op_ids, k_ids=cols.k_ids,
+                         k_op=cols.k_op, op_sig=cols.op_sig, watts_p0=p0, op_ids=cols.op_ids, k_ids=cols.k_ids,
                          op_names=cols.op_names, op_work=cols.op_work, op_rank=cols.op_rank)
 
 
@@ -353,11 +438,11 @@ def save_packed(cols: TraceColumns, path) -> None:
         if a is None:
             continue
         a = a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
-        if n in ("ts", "op_start", "op_end", "k_start", "k_end"):
-            a = a.view(np.uint32) if a.dtype in (np.int32, np.uint32) else a.astype(np.uint32)
+        if n in ("ts", "op_start", "op_end", "k_start", "k_end") or (n == "watts" and pc.watts_p0 is not None):
+            a = a.view(np.uint16 if a.itemsize == 2 else np.uint32)
         arrays[n] = np.ascontiguousarray(a)
-    meta = {"format": "dwc", "version": 1, "trace_end": pc.trace_end, "ts_base": pc.ts_base,
-            "op_base": pc.op_start_base, "k_base": pc.k_start_base, "columns": {}}
+    meta = {"format": "dwc", "version": 2, "trace_end": pc.trace_end, "ts_base": pc.ts_base,
+            "op_base": pc.op_start_base, "k_base": pc.k_start_base, "watts_p0": pc.watts_p0, "columns": {}}
     off = 0
     for n, a in arrays.items():
         meta["columns"][n] = {"dtype": a.dtype.str, "n": int(a.shape[0]), "offset": off}
@@ -378,8 +463,8 @@ def load_packed(path, pin: bool = False) -> PackedColumns:
     with open(path, "rb") as fh:
         head = fh.readline()
     meta = json.loads(head)
-    if meta.get("format") != "dwc" or meta.get("version") != 1:
-        raise ValueError(f"{path}: not a dwc v1 file")
+    if meta.get("format") != "dwc" or meta.get("version") not in (1, 2):
+        raise ValueError(f"{path}: not a dwc v1/v2 file")
     start = (len(head) + 63) & ~63
     raw = np.memmap(path, dtype=np.uint8, mode="r")
     cols = {}
@@ -390,9 +475,13 @@ def load_packed(path, pin: bool = False) -> PackedColumns:
         if pin:
             t = t.pin_memory()
         cols[n] = t
-    def as_i32(x):
-        return x.view(torch.int32) if isinstance(x, torch.Tensor) else x
-    return PackedColumns(meta["ts_base"], as_i32(cols["ts"]), cols["watts"], meta["op_base"], as_i32(cols["op_start"]),
-                         as_i32(cols["op_end"]), meta["k_base"], as_i32(cols["k_start"]), as_i32(cols["k_end"]),
-                         meta["trace_end"], k_op=cols.get("k_op"), op_sig=cols.get("op_sig"),
-                         op_work=cols.get("op_work"))
+    def as_signed(x):  # torch has no uint16/uint32 storage for these: same bits, signed view
+        if isinstance(x, torch.Tensor) and x.dtype in (torch.uint16, torch.uint32):
+            return x.view(torch.int16 if x.element_size() == 2 else torch.int32)
+        return x
+    p0 = meta.get("watts_p0")
+    return PackedColumns(meta["ts_base"], as_signed(cols["ts"]), as_signed(cols["watts"]) if p0 is not None
+                         else cols["watts"], meta["op_base"], as_signed(cols["op_start"]), as_signed(cols["op_end"]),
+                         meta["k_base"], as_signed(cols["k_start"]), as_signed(cols["k_end"]), meta["trace_end"],
+                         k_op=cols.get("k_op"), op_sig=cols.get("op_sig"), op_work=cols.get("op_work"),
+                         watts_p0=p0)

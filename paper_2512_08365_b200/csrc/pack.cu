@@ -15,23 +15,60 @@
 
 namespace dw {
 
+template <typename T>
 struct DeltaAt {  // value i of the scan input: base + d[0] at 0, d[i] after
-    const uint32_t *d;
+    const T *d;
     int64_t base;
     __host__ __device__ int64_t operator()(int64_t i) const { return i == 0 ? base + (int64_t)d[0] : (int64_t)d[i]; }
 };
 
-__global__ void add_duration_kernel(const int64_t *start, const uint32_t *dur, int64_t n, int64_t *end) {
+template <typename T>
+__global__ void add_duration_kernel(const int64_t *start, const T *dur, int64_t n, int64_t *end) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
         end[i] = __ldcs(start + i) + (int64_t)__ldcs(dur + i);
 }
 
-static size_t scan_bytes(int64_t n) {
+template <typename T>
+static size_t scan_bytes_t(int64_t n) {
     size_t b = 0;
-    auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), DeltaAt{nullptr, 0});
+    auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), DeltaAt<T>{nullptr, 0});
     cub::DeviceScan::InclusiveSum(nullptr, b, it, (int64_t *)nullptr, (int)std::max<int64_t>(n, 1));
     return b;
+}
+static size_t scan_bytes(int64_t n) { return std::max(scan_bytes_t<uint32_t>(n), scan_bytes_t<uint16_t>(n)); }
+
+template <typename T>
+static void scan_deltas(const void *delta, int64_t n, int64_t base, int64_t *out, void *ws, size_t bytes,
+                        cudaStream_t s) {
+    auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
+                                              DeltaAt<T>{(const T *)delta, base});
+    cub::DeviceScan::InclusiveSum(ws, bytes, it, out, (int)n, s);
+    count_launch(2);
+}
+
+template <typename T>
+static void add_durations(const int64_t *start, const void *dur, int64_t n, int64_t *end, cudaStream_t s) {
+    add_duration_kernel<T><<<(unsigned)std::min<int64_t>(num_sms() * 8, ceil_div(n, 256)), 256, 0, s>>>(
+        start, (const T *)dur, n, end);
+    count_launch();
+}
+
+// 9-significant-digit decimals (the trace format's on-disk precision,
+// trace_model.py:63-65): code = m | j << 30, value = m * 10^-(p0 + j) as ONE
+// correctly rounded IEEE operation -- the same double a decimal parse of
+// "m e-(p0+j)" yields, so the decode is exact.
+__constant__ double POW10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
+                                 1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
+
+__global__ void decimal_decode_kernel(const uint32_t *code, int64_t n, int32_t p0, double *out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint32_t c = __ldcs(code + i);
+        const double m = (double)(c & 0x3FFFFFFFu);
+        const int p = p0 + (int)(c >> 30);
+        __stcs(out + i, p >= 0 ? __ddiv_rn(m, POW10[p]) : __dmul_rn(m, POW10[-p]));
+    }
 }
 
 }  // namespace dw
@@ -42,19 +79,34 @@ extern "C" {
 
 size_t dw_unpack_workspace_size(int64_t n) { return scan_bytes(n) + 256; }
 
-int dw_unpack_deltas(const uint32_t *d_delta, int64_t n, int64_t base, int64_t *d_out, const uint32_t *d_dur,
-                     int64_t *d_end, void *d_workspace, size_t workspace_bytes, dw_stream_t stream) {
+int dw_unpack_deltas_w(const void *d_delta, int32_t delta_bytes, int64_t n, int64_t base, int64_t *d_out,
+                       const void *d_dur, int32_t dur_bytes, int64_t *d_end, void *d_workspace,
+                       size_t workspace_bytes, dw_stream_t stream) {
     if (n < 0 || (n && (!d_delta || !d_out)) || (d_dur && !d_end) || n >= ((int64_t)1 << 31)) return DW_E_ARG;
+    if ((delta_bytes != 2 && delta_bytes != 4) || (d_dur && dur_bytes != 2 && dur_bytes != 4)) return DW_E_ARG;
     if (n == 0) return DW_OK;
     if (!d_workspace || workspace_bytes < dw_unpack_workspace_size(n)) return DW_E_WORKSPACE;
     cudaStream_t s = (cudaStream_t)stream;
-    auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), DeltaAt{d_delta, base});
-    size_t b = workspace_bytes;
-    cub::DeviceScan::InclusiveSum(d_workspace, b, it, d_out, (int)n, s);
-    count_launch(2);
+    if (delta_bytes == 2) scan_deltas<uint16_t>(d_delta, n, base, d_out, d_workspace, workspace_bytes, s);
+    else scan_deltas<uint32_t>(d_delta, n, base, d_out, d_workspace, workspace_bytes, s);
     if (d_dur) {
-        add_duration_kernel<<<(unsigned)std::min<int64_t>(num_sms() * 8, ceil_div(n, 256)), 256, 0, s>>>(
-            d_out, d_dur, n, d_end);
+        if (dur_bytes == 2) add_durations<uint16_t>(d_out, d_dur, n, d_end, s);
+        else add_durations<uint32_t>(d_out, d_dur, n, d_end, s);
+    }
+    DW_CHECK_LAUNCH();
+    return DW_OK;
+}
+
+int dw_unpack_deltas(const uint32_t *d_delta, int64_t n, int64_t base, int64_t *d_out, const uint32_t *d_dur,
+                     int64_t *d_end, void *d_workspace, size_t workspace_bytes, dw_stream_t stream) {
+    return dw_unpack_deltas_w(d_delta, 4, n, base, d_out, d_dur, 4, d_end, d_workspace, workspace_bytes, stream);
+}
+
+int dw_unpack_decimal(const uint32_t *d_code, int64_t n, int32_t p0, double *d_out, dw_stream_t stream) {
+    if (n < 0 || (n && (!d_code || !d_out)) || p0 < -22 || p0 + 3 > 22) return DW_E_ARG;
+    if (n) {
+        decimal_decode_kernel<<<(unsigned)std::min<int64_t>(num_sms() * 8, ceil_div(n, 256)), 256, 0,
+                                (cudaStream_t)stream>>>(d_code, n, p0, d_out);
         count_launch();
     }
     DW_CHECK_LAUNCH();

@@ -130,6 +130,21 @@ def _truth_at(ts: torch.Tensor, k_start, k_end, kw, chunk=1 << 26) -> torch.Tens
     return out
 
 
+_POW10 = [10.0 ** k for k in range(23)]  # exact doubles
+
+
+def round9(w: torch.Tensor) -> torch.Tensor:
+    """Watts at the trace format's on-disk precision: 9 significant decimal
+    digits (trace_model.py:63-65, the reference writes every power sample
+    that way), as the double nearest each decimal (one IEEE division)."""
+    pos = w > 0
+    p = (8 - torch.floor(torch.log10(torch.where(pos, w, torch.ones_like(w))))).to(torch.int64).clamp(0, 22)
+    pw = torch.tensor(_POW10, dtype=torch.float64, device=w.device)[p]
+    m = torch.round(w * pw)
+    m = torch.where(m >= 1e9, torch.round(w * pw / 10.0) * 10.0, m)  # log10 landed one decade low
+    return torch.where(pos, torch.div(m, pw), w)
+
+
 def _power(op_end_max: int, t0: int, n_samples: int, k_start, k_end, kw, dev):
     span = max(op_end_max - t0, 1)
     if n_samples <= 0:
@@ -141,7 +156,7 @@ def _power(op_end_max: int, t0: int, n_samples: int, k_start, k_end, kw, dev):
     ts[-1] = t0 + span
     if period < 1:
         raise ValueError("more samples than microseconds in the span")
-    return ts, _truth_at(ts, k_start, k_end, kw)
+    return ts, _truth_at(ts, k_start, k_end, round9(kw))
 
 
 def _b_side(a: _Ops, cfg: SynthConfig, g: torch.Generator, dev) -> _Ops:

@@ -1,5 +1,5 @@
-"""Packed columns (uint32 deltas / durations, csrc/pack.cu): device decode is
-exact, and every result computed from a packed trace equals the unpacked
+"""Packed columns (16/32-bit deltas / durations, 9-digit decimal watts codes,
+csrc/pack.cu): device decode is exact, and every result computed from a packed trace equals the unpacked
 one; the .dwc file round-trips."""
 import numpy as np
 import pytest
@@ -17,7 +17,9 @@ def test_decode_exact_and_ledger_identical(tmp_path):
     cfg = synth.scaled(synth.CONFIGS["C4"], 50_000)
     a, b = synth.make_pair(cfg)
     p = pack(a)
-    for n in ("ts", "op_start", "op_end", "k_start", "k_end"):
+    assert p.watts_p0 is not None  # synthetic watts are at the format's 9-digit precision
+    assert p.ts.element_size() == 2 and p.k_end.element_size() == 2
+    for n in ("ts", "watts", "op_start", "op_end", "k_start", "k_end"):
         assert torch.equal(p.device(n), a.device(n)), n
     assert p.signal_span() == a.signal_span()
     la, lp = build_ledger(a, method="samples"), build_ledger(p, method="samples")
@@ -33,6 +35,14 @@ def test_decode_exact_and_ledger_identical(tmp_path):
     assert rp.report.wasted_joules == ra.report.wasted_joules
     assert [f.wasted_joules for f in rp.report.findings] == [f.wasted_joules for f in ra.report.findings]
     assert [f.pair for f in rp.report.findings] == [f.pair for f in ra.report.findings]
+    assert [f.category for f in rp.report.findings] == [f.category for f in ra.report.findings]
+    # the shipped host form carries no owner column: classification by containment
+    from paper_2512_08365_b200.columns import PackedColumns
+    bare = [PackedColumns(q.ts_base, q.ts, q.watts, q.op_start_base, q.op_start, q.op_end, q.k_start_base,
+                          q.k_start, q.k_end, q.trace_end, op_sig=q.op_sig, watts_p0=q.watts_p0) for q in (ha, hb)]
+    rb = analyze(bare[0], bare[1], "samples", 0.10, 20)
+    assert [f.category for f in rb.report.findings] == [f.category for f in ra.report.findings]
+    assert rb.report.wasted_joules == ra.report.wasted_joules
 
 
 def test_pack_rejects_unsorted():

@@ -1,10 +1,20 @@
 """Packed columnar trace files (columns.pack / save_packed / load_packed) on
-the host: the uint32 deltas and durations round-trip exactly, the span is
-preserved, and traces that cannot be packed are refused."""
+the host: the 16/32-bit deltas and durations and the decimal watts codes
+round-trip exactly, the span is preserved, and traces that cannot be packed
+are refused."""
 import numpy as np
 import pytest
 
-from paper_2512_08365_b200.columns import TraceColumns, load_packed, pack, save_packed
+from paper_2512_08365_b200.columns import TraceColumns, decimal_code, load_packed, pack, save_packed
+
+
+def _u(d):
+    d = np.asarray(d)
+    return d.view(np.uint16 if d.itemsize == 2 else np.uint32).astype(np.int64)
+
+
+def _round9(x):
+    return np.array([float(f"{v:.9g}") for v in x])
 
 
 def _cols(seed=0, n=5000, m=400):
@@ -24,13 +34,14 @@ def test_roundtrip(tmp_path):
     c = _cols()
     save_packed(c, tmp_path / "t.dwc")
     p = load_packed(tmp_path / "t.dwc")
-    dec = lambda base, d: base + np.cumsum(np.asarray(d).view(np.uint32).astype(np.int64))  # noqa: E731
+    dec = lambda base, d: base + np.cumsum(_u(d))  # noqa: E731
     np.testing.assert_array_equal(dec(p.ts_base, p.ts), c.ts)
+    assert p.watts_p0 is None  # uniform draws are not 9-digit decimals: f64 column
     np.testing.assert_array_equal(np.asarray(p.watts), c.watts)
     np.testing.assert_array_equal(dec(p.op_start_base, p.op_start), c.op_start)
-    np.testing.assert_array_equal(dec(p.op_start_base, p.op_start) + np.asarray(p.op_end).view(np.uint32),
-                                  c.op_end)
-    np.testing.assert_array_equal(dec(p.k_start_base, p.k_start) + np.asarray(p.k_end).view(np.uint32), c.k_end)
+    np.testing.assert_array_equal(dec(p.op_start_base, p.op_start) + _u(p.op_end), c.op_end)
+    np.testing.assert_array_equal(dec(p.k_start_base, p.k_start) + _u(p.k_end), c.k_end)
+    assert np.asarray(p.ts).itemsize == 2 and np.asarray(p.op_end).itemsize == 4  # narrowest width per column
     np.testing.assert_array_equal(np.asarray(p.op_sig), c.op_sig)
     np.testing.assert_array_equal(np.asarray(p.k_op), c.k_op)
     assert p.signal_span() == c.signal_span()
@@ -57,3 +68,30 @@ def test_unpackable_refused(mutate):
     bad = TraceColumns.from_arrays(ts, c.watts, c.op_start, en, c.k_start, c.k_end, c.k_op)
     with pytest.raises(ValueError):
         pack(bad)
+
+
+def _decode(p0, code):
+    code = np.asarray(code).view(np.uint32)
+    m = (code & 0x3FFFFFFF).astype(np.float64)
+    pw = p0 + (code >> 30).astype(np.int64)
+    return np.where(pw >= 0, m / 10.0 ** np.abs(pw), m * 10.0 ** np.abs(pw))
+
+
+def test_decimal_watts_roundtrip(tmp_path):
+    rng = np.random.default_rng(3)
+    w = _round9(np.concatenate([rng.uniform(50, 700, 3000), rng.uniform(1.0, 9.9, 100), [75.0, 0.0, 999.0]]))
+    p0, code = decimal_code(w)
+    np.testing.assert_array_equal(_decode(p0, code), w)
+    c = _cols()
+    c = TraceColumns.from_arrays(c.ts[:w.size], w, c.op_start[:10], c.op_end[:10], c.k_start[:20], c.k_end[:20],
+                                 c.k_op[:20])
+    save_packed(c, tmp_path / "d.dwc")
+    p = load_packed(tmp_path / "d.dwc")
+    assert p.watts_p0 == p0
+    np.testing.assert_array_equal(_decode(p.watts_p0, p.watts), w)
+
+
+def test_non_decimal_watts_stay_f64():
+    assert decimal_code(np.array([1.0 / 3.0, 2.0])) is None
+    assert decimal_code(np.array([-1.0])) is None
+    assert decimal_code(np.array([np.nan])) is None
