@@ -80,11 +80,6 @@ class Window(ctypes.Structure):
                 ("w_last", ctypes.c_double)]
 
 
-class Unfold(ctypes.Structure):
-    _fields_ = [("value_off", c_i64), ("out_off", c_i64), ("scratch_off", c_i64), ("order", c_i32),
-                ("mask", c_i32), ("dims", c_i32 * 8)]
-
-
 class Status(ctypes.Structure):
     _fields_ = [("code", c_i32), ("bad_set", c_i32), ("bad_index", c_i64 * DW_MAX_SETS),
                 ("order_index", c_i64), ("unsorted_index", c_i64 * DW_MAX_SETS),

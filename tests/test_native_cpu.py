@@ -39,3 +39,17 @@ def test_no_cpu_fallback_without_gpu():
                                        np.array([0]), np.array([5]))
     with pytest.raises(_native.NativeUnavailable):
         dw.build_ledger(cols)
+
+
+def test_unfold_descriptor_layout_matches_header():
+    """tensor_equiv.UNFOLD_DTYPE mirrors dw_unfold_t (include/dwb200.h)."""
+    from paper_2512_08365_b200.tensor_equiv import UNFOLD_DTYPE
+    assert UNFOLD_DTYPE.itemsize == 64
+    assert [UNFOLD_DTYPE.fields[n][1] for n in ("value_off", "out_off", "scratch_off", "order", "mask", "dims")] \
+        == [0, 8, 16, 24, 28, 32]
+    hdr = (Path(__file__).resolve().parent.parent / "include" / "dwb200.h").read_text()
+    body = hdr[hdr.index("typedef struct {\n    int64_t value_off;"):hdr.index("} dw_unfold_t;")]
+    fields = re.findall(r"^\s*(int64_t|int32_t)\s+(\w+)(\[8\])?;", body, flags=re.M)
+    assert [(t, n) for t, n, _ in fields] == [("int64_t", "value_off"), ("int64_t", "out_off"),
+                                             ("int64_t", "scratch_off"), ("int32_t", "order"),
+                                             ("int32_t", "mask"), ("int32_t", "dims")]
