@@ -108,3 +108,25 @@ def test_forced_gaps_without_owner_column():
     np.testing.assert_array_equal(ea, eb)
     np.testing.assert_array_equal(ra, rb)
     assert ra.size >= len(ops)
+
+
+def test_kernelless_waste_finding_raises_like_reference():
+    """Same op names, no forced gaps, no kernels on either side: the reference's
+    analyze_segment_pair raises DiagnoseError (diagnose.py:292-293)."""
+    from paper_2512_08365_b200.detect import SubgraphPair, WasteFinding
+    from paper_2512_08365_b200.trace_model import OperatorEvent, PowerSample, Trace, TraceHeader
+
+    def mk():
+        op = OperatorEvent("o", "matmul", (), (), (), 5, 5)
+        return Trace(TraceHeader(1, "s", "w", 0), {}, (op,), {}, (PowerSample(0, 1.0), PowerSample(10, 2.0)),
+                     (), None, {})
+    ta, tb = mk(), mk()
+    f = WasteFinding(pair=SubgraphPair(("o",), ("o",)), energy_a=1.0, energy_b=0.5, energy_ratio=2.0,
+                     latency_a=0, latency_b=0, output_rel_diff=0.0, verdict="waste", category="unknown",
+                     wasteful_side="A", wasted_joules=0.5, informational=False)
+    with pytest.raises(dg.DiagnoseError):
+        dg.classify_findings([f], ta, tb)
+    # the same pair as columns (no program model): same error
+    with pytest.raises(dg.DiagnoseError):
+        dg.classify_pairs(TraceColumns.from_trace(ta), TraceColumns.from_trace(tb), ["A"], np.array([0]),
+                          np.array([0]))

@@ -153,3 +153,34 @@ def test_order5_sets_embed_on_host():
     oeq, os_ = ot.equivalent(x, np.transpose(x, (4, 3, 2, 1, 0)))
     assert eq and oeq
     assert s == pytest.approx(os_, abs=1e-12)
+
+
+def _trace_with(tensors_a, tensors_b):
+    """Minimal reference-style traces whose tensors are graph inputs of one op."""
+    from paper_2512_08365_b200.trace_model import (OperatorEvent, PowerSample, TensorSnapshot, Trace,
+                                                   TraceHeader)
+
+    def mk(tensors):
+        snaps = {tid: (TensorSnapshot(tid, tuple(x.shape), tuple(float(v) for v in x.ravel())),)
+                 for tid, x in tensors.items()}
+        op = OperatorEvent("op0", "f", tuple(sorted(tensors)), (), (), 0, 10)
+        return Trace(TraceHeader(1, "s", "w", 0), snaps, (op,), {}, (PowerSample(0, 1.0),), (), None, {})
+    return mk(tensors_a), mk(tensors_b)
+
+
+def test_match_tensors_edge_cases():
+    rng = np.random.default_rng(8)
+    x = rng.standard_normal((2, 3, 4))
+    ta, tb = _trace_with({"a": x, "v": np.arange(5.0)}, {"b": np.transpose(x, (2, 0, 1)), "w": np.arange(5.0)})
+    pairs, st = tm.match_tensors(ta, tb)
+    assert [(p.tensor_a, p.tensor_b) for p in pairs.pairs] == [("a", "b"), ("v", "w")]
+    assert st.candidate_pairs == 2 and st.full_checks == 2
+    # no tensors at all
+    ea, eb = _trace_with({}, {})
+    pairs, st = tm.match_tensors(ea, eb)
+    assert len(pairs) == 0 and st.candidate_pairs == 0
+    # order above the cap raises once that pair is compared, as the reference does
+    big = rng.standard_normal((1,) * 9)
+    ba, bb = _trace_with({"a": big}, {"b": big})
+    with pytest.raises(ValueError):
+        tm.match_tensors(ba, bb)
