@@ -140,7 +140,24 @@ __global__ void status_init_kernel(DevStatus *st) {
 }
 
 // ------------------------------------------------------------ K1 partition
-__global__ void partition_kernel(AttrParams p) {
+// Every PIDX_STRIDE-th interval start of each set: a ~1 MB index the
+// partition searches first (L2-resident), so each tile boundary costs a
+// handful of DRAM sectors instead of a full-depth search over the starts.
+constexpr int64_t PIDX_STRIDE = 1024;
+
+struct PartIndex {
+    int64_t *p[DW_MAX_SETS];
+};
+
+__global__ void partition_index_kernel(AttrParams p, PartIndex idx, int nsets) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (int j = 0; j < nsets; ++j) {
+        const int64_t m = ceil_div(p.n[j], PIDX_STRIDE);
+        if (i < m) idx.p[j][i] = __ldg(p.start[j] + i * PIDX_STRIDE);
+    }
+}
+
+__global__ void partition_kernel(AttrParams p, PartIndex idx) {
     int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     int64_t nb = p.ntiles + 1;
     if (b >= nb * p.nsets) return;
@@ -153,38 +170,24 @@ __global__ void partition_kernel(AttrParams p) {
     } else if (b == p.ntiles) {
         r = n;
     } else {
-        // first k with a[k] >= key: interpolated guess (starts are spread over
-        // the span), gallop to a bracket, then bisect
+        // first k with a[k] >= key: bisect the sampled index (cached), then
+        // the PIDX_STRIDE-wide bracket of the starts it leaves
         const int64_t key = p.ts[b * TILE];
         const int64_t *a = p.start[j];
-        int64_t lo = 0, hi = n;  // a[lo-1] < key (or lo == 0), a[hi] >= key (or hi == n)
-        if (n > 0) {
-            const int64_t a0 = __ldg(a), an = __ldg(a + n - 1);
-            if (key <= a0) {
-                hi = 0;
-            } else if (key > an) {
-                lo = n;
-            } else {
-                const double f = (double)(key - a0) / (double)(an - a0);
-                int64_t g = (int64_t)(f * (double)(n - 1));
-                g = g < 0 ? 0 : (g > n - 1 ? n - 1 : g);
-                int64_t step = 1;
-                if (__ldg(a + g) < key) {  // a[g] < key: gallop up
-                    lo = g + 1;
-                    while (lo + step - 1 < n && __ldg(a + lo + step - 1) < key) { lo += step; step <<= 1; }
-                    hi = lo + step - 1 < n ? lo + step - 1 : n;
-                } else {                   // a[g] >= key: gallop down
-                    hi = g;
-                    while (hi - step >= 0 && __ldg(a + hi - step) >= key) { hi -= step; step <<= 1; }
-                    lo = hi - step + 1 > 0 ? hi - step + 1 : 0;
-                }
-            }
-        }
+        const int64_t *ix = idx.p[j];
+        int64_t lo = 0, hi = ceil_div(n, PIDX_STRIDE);  // first index entry >= key
         while (lo < hi) {
-            int64_t mid = lo + ((hi - lo) >> 1);
-            if (__ldg(a + mid) < key) lo = mid + 1; else hi = mid;
+            const int64_t mid = lo + ((hi - lo) >> 1);
+            if (__ldg(ix + mid) < key) lo = mid + 1; else hi = mid;
         }
-        r = lo;
+        // a[(lo-1)*STRIDE] < key (lo > 0), a[lo*STRIDE] >= key (if in range)
+        int64_t l2 = lo > 0 ? (lo - 1) * PIDX_STRIDE + 1 : 0;
+        int64_t h2 = lo * PIDX_STRIDE < n ? lo * PIDX_STRIDE : n;
+        while (l2 < h2) {
+            const int64_t mid = l2 + ((h2 - l2) >> 1);
+            if (__ldg(a + mid) < key) l2 = mid + 1; else h2 = mid;
+        }
+        r = l2;
     }
     const_cast<int64_t *>(p.first)[j * nb + b] = r;
 }
@@ -1460,6 +1463,7 @@ static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct AttrLayout {
     size_t status, first, tile_sum, prefix, scan_part, long_list, sum_partials, sum_done, sum_out;
+    size_t pidx[DW_MAX_SETS];
     size_t sort_keys[DW_MAX_SETS], sort_perm[DW_MAX_SETS], sort_end[DW_MAX_SETS],
         sort_iota[DW_MAX_SETS];
     size_t cub_tmp, cub_bytes, total;
@@ -1489,6 +1493,10 @@ static AttrLayout attr_layout(int64_t S, const int64_t *sizes, const int32_t *so
     L.sum_partials = off; off += align_up(16 * (size_t)SUM_BLOCKS);
     L.sum_done = off; off += align_up(16);
     L.sum_out = off; off += align_up(16);
+    for (int j = 0; j < nsets; ++j) {
+        L.pidx[j] = off;
+        off += align_up(8 * (size_t)(ceil_div(sizes[j], PIDX_STRIDE) + 1));
+    }
     size_t cub = 0;
     for (int j = 0; j < nsets; ++j) {
         if (sorted && sorted[j]) continue;
@@ -1598,7 +1606,17 @@ static int attribute_impl(const dw_signal_t *sig, dw_interval_set_t *sets, int n
 
     const int64_t nb = (p.ntiles + 1) * (int64_t)nsets;
     if (nb > 0) {
-        partition_kernel<<<(unsigned)ceil_div(nb, 256), 256, 0, stream>>>(p);
+        PartIndex pix{};
+        int64_t mmax = 0;
+        for (int j = 0; j < nsets; ++j) {
+            pix.p[j] = (int64_t *)(base + L.pidx[j]);
+            mmax = std::max<int64_t>(mmax, ceil_div(p.n[j], PIDX_STRIDE));
+        }
+        if (mmax > 0) {
+            partition_index_kernel<<<(unsigned)ceil_div(mmax, 256), 256, 0, stream>>>(p, pix, nsets);
+            count_launch();
+        }
+        partition_kernel<<<(unsigned)ceil_div(nb, 256), 256, 0, stream>>>(p, pix);
         count_launch();
     }
     const size_t smem = ((sizeof(TileSmem) + 15) & ~(size_t)15) + GROUPS * sizeof(GroupSmem);
