@@ -1379,12 +1379,23 @@ __global__ void __launch_bounds__(SUM_THREADS) fx_sum_kernel(const double *x, in
         last = ticket == gridDim.x - 1;
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
-        __threadfence();
+    if (!last) return;
+    // the last block sums the per-block partials with all its threads (L2
+    // loads, independent), not one thread's chain of dependent round trips
+    __threadfence();
+    i128 part = 0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += SUM_THREADS)
+        part += join(__ldcg(partials + 2 * b), __ldcg(partials + 2 * b + 1));
+    part = warp_sum_i128(part);
+    if ((threadIdx.x & 31) == 0) {
+        I128Parts pp = split(part);
+        red[threadIdx.x >> 5][0] = pp.lo;
+        red[threadIdx.x >> 5][1] = pp.hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
         i128 s = 0;
-        for (unsigned b = 0; b < gridDim.x; ++b)
-            s += join(((volatile unsigned long long *)partials)[2 * b],
-                      ((volatile unsigned long long *)partials)[2 * b + 1]);
+        for (int k = 0; k < SUM_THREADS / 32; ++k) s += join(red[k][0], red[k][1]);
         if (out) *out = fx_to_double(s, FX_JOULE_BITS);
         if (out_fx) {
             const I128Parts pp = split(s);

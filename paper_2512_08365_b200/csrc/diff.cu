@@ -283,14 +283,31 @@ __global__ void waste_sum_kernel(const uint64_t *khi, int64_t P, unsigned long l
         last = atomicAdd(done, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
-        __threadfence();
+    if (!last) return;
+    // the last block sums the partials with all its threads (independent L2 loads)
+    __threadfence();
+    i128 ps = 0;
+    unsigned long long pc = 0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+        ps += join(__ldcg(partials + 3 * b), __ldcg(partials + 3 * b + 1));
+        pc += __ldcg(partials + 3 * b + 2);
+    }
+    ps = warp_sum_i128(ps);
+    for (int o = 16; o > 0; o >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, o);
+    __syncthreads();  // red is reused
+    if ((threadIdx.x & 31) == 0) {
+        I128Parts q = split(ps);
+        red[threadIdx.x >> 5][0] = q.lo;
+        red[threadIdx.x >> 5][1] = q.hi;
+        red[threadIdx.x >> 5][2] = pc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
         i128 s = 0;
         unsigned long long c = 0;
-        volatile unsigned long long *pp = partials;
-        for (unsigned b = 0; b < gridDim.x; ++b) {
-            s += join(pp[3 * b], pp[3 * b + 1]);
-            c += pp[3 * b + 2];
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+            s += join(red[w][0], red[w][1]);
+            c += red[w][2];
         }
         summary[0] = (double)c;
         summary[1] = fx_to_double(s, FX_JOULE_BITS);
