@@ -336,16 +336,20 @@ def run_ours(args, rank: int, world: int, local: int):
                 return h
             hc = PackedColumns(pc.ts_base, pin(pc.ts), pin(pc.watts), pc.op_start_base, pin(pc.op_start),
                                pin(pc.op_end), pc.k_start_base, pin(pc.k_start), pin(pc.k_end), c.trace_end,
-                               op_sig=pin(pc.op_sig), watts_p0=pc.watts_p0)
+                               op_sig=pin(pc.op_sig), watts_p0=pc.watts_p0, ts_bias=pc.ts_bias,
+                               op_sig_dict=pin(pc.op_sig_dict) if pc.op_sig_dict is not None else None)
             hc._dev["first_last"] = c._first_last_ts()
             pinned.append(hc)
             del pc
         h2d = sum(pc.host_bytes for pc in pinned)
         pc0 = pinned[0]
-        host_format = (f"packed columns: ts deltas u{8 * pc0.ts.element_size()}, interval deltas/durations "
-                       f"u{8 * pc0.op_start.element_size()}/u{8 * pc0.op_end.element_size()} (ops) "
+        tsw = pc0.ts.element_size()
+        host_format = (f"packed columns: ts deltas {'biased i8' if tsw == 1 else f'u{8 * tsw}'}, interval "
+                       f"deltas/durations u{8 * pc0.op_start.element_size()}/u{8 * pc0.op_end.element_size()} (ops) "
                        f"u{8 * pc0.k_start.element_size()}/u{8 * pc0.k_end.element_size()} (kernels), watts "
-                       + ("9-digit decimal codes u32" if pc0.watts_p0 is not None else "f64") + ", sig u64")
+                       + ("9-digit decimal codes u32" if pc0.watts_p0 is not None else "f64")
+                       + (f", sig dictionary + u{8 * pc0.op_sig.element_size()} codes" if pc0.op_sig_dict is not None
+                          else ", sig u64"))
         for c in (ca, cb):
             c._dev.clear()
         del ca, cb

@@ -185,11 +185,17 @@ int dw_replay(const dw_signal_t *truth, const int64_t *d_op_start, const int64_t
 size_t dw_unpack_workspace_size(int64_t n);
 int dw_unpack_deltas(const uint32_t *d_delta, int64_t n, int64_t base, int64_t *d_out, const uint32_t *d_dur,
                      int64_t *d_end, void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
-/* Same with 16- or 32-bit deltas / durations (delta_bytes, dur_bytes = 2 or 4):
- * the packer picks the narrowest width the column's gaps fit. */
-int dw_unpack_deltas_w(const void *d_delta, int32_t delta_bytes, int64_t n, int64_t base, int64_t *d_out,
-                       const void *d_dur, int32_t dur_bytes, int64_t *d_end, void *d_workspace,
+/* Same with narrow columns: deltas of delta_bytes = 1 (int8, value =
+ * delta_bias + d[i]), 2 or 4 (unsigned, value = delta_bias + d[i]); durations
+ * of dur_bytes = 2 or 4.  d[0] is ignored: the first value is `base`.  The
+ * packer picks the narrowest width the column fits. */
+int dw_unpack_deltas_w(const void *d_delta, int32_t delta_bytes, int64_t delta_bias, int64_t n, int64_t base,
+                       int64_t *d_out, const void *d_dur, int32_t dur_bytes, int64_t *d_end, void *d_workspace,
                        size_t workspace_bytes, dw_stream_t stream);
+/* Dictionary-coded 64-bit column (operator signatures): d_out[i] =
+ * d_dict[code[i]], codes of code_bytes = 2 or 4. */
+int dw_unpack_dict(const uint64_t *d_dict, const void *d_code, int32_t code_bytes, int64_t n, uint64_t *d_out,
+                   dw_stream_t stream);
 /* Watts stored as 9-significant-digit decimals (the trace format's on-disk
  * precision, trace_model.py:63-65): code = m | j << 30 (m < 2^30, j < 4),
  * d_out[i] = m * 10^-(p0 + j), one correctly rounded IEEE operation -- the

@@ -244,17 +244,25 @@ class PackedColumns(TraceColumns):
     PACKED = ("ts", "op_start", "k_start")
 
     def __init__(self, ts_base, ts_delta, watts, op_base, op_delta, op_dur, k_base, k_delta, k_dur,
-                 trace_end, k_op=None, op_sig=None, watts_p0=None, **kw):
+                 trace_end, k_op=None, op_sig=None, watts_p0=None, ts_bias=0, op_sig_dict=None, **kw):
         super().__init__(ts=ts_delta, watts=watts, trace_end=int(trace_end), op_start=op_delta, op_end=op_dur,
                          k_start=k_delta, k_end=k_dur, k_op=k_op, op_sig=op_sig, ops_sorted=True,
                          kernels_sorted=True, **kw)
         self.ts_base, self.op_start_base, self.k_start_base = int(ts_base), int(op_base), int(k_base)
         self.watts_p0 = None if watts_p0 is None else int(watts_p0)
+        self.ts_bias = int(ts_bias)          # int8 ts deltas: delta = ts_bias + code
+        self.op_sig_dict = op_sig_dict       # op_sig holds u16/u32 codes into this u64 dictionary
         self._first_last = None
 
     def _first_last_ts(self) -> tuple[int, int]:
         if "first_last" not in self._dev:
-            dd = _unsigned(self.ts)
+            t = self.ts
+            if (t.element_size() if isinstance(t, torch.Tensor) else np.asarray(t).itemsize) == 1:
+                dd = (t.to(torch.int64) if isinstance(t, torch.Tensor) else np.asarray(t).astype(np.int64)) \
+                    + self.ts_bias  # biased int8 deltas
+                dd[0] = 0
+            else:
+                dd = _unsigned(t)
             last = self.ts_base + int(dd.sum())
             first = self.ts_base + int(dd[0])
             self._dev["first_last"] = (first, last)
@@ -272,6 +280,8 @@ class PackedColumns(TraceColumns):
     def device(self, name: str) -> torch.Tensor:
         if name == "watts" and self.watts_p0 is not None:
             return self._device_watts()
+        if name == "op_sig" and self.op_sig_dict is not None:
+            return self._device_sig()
         if name not in ("ts", "op_start", "op_end", "k_start", "k_end"):
             return super().device(name)
         dev = _native.device()
@@ -291,7 +301,8 @@ class PackedColumns(TraceColumns):
         base = {"ts": self.ts_base, "op_start": self.op_start_base, "k_start": self.k_start_base}[base_name]
         L = _native.lib()
         ws = _native.Workspace.get(L.dw_unpack_workspace_size(n))
-        _native.check(L.dw_unpack_deltas_w(_native.ptr(delta), delta.element_size(), n, base, _native.ptr(out),
+        bias = self.ts_bias if base_name == "ts" else 0
+        _native.check(L.dw_unpack_deltas_w(_native.ptr(delta), delta.element_size(), bias, n, base, _native.ptr(out),
                                            _native.ptr(dur) if end is not None else None,
                                            dur.element_size() if end is not None else 4, _native.ptr(end),
                                            ws.data_ptr(), ws.numel(), _native.stream_handle()),
@@ -314,17 +325,35 @@ class PackedColumns(TraceColumns):
             self._dev[key] = t
         return t
 
+    def _device_sig(self) -> torch.Tensor:
+        dev = _native.device()
+        key = ("op_sig", dev.index)
+        t = self._dev.get(key)
+        if t is None:
+            code = self._raw("op_sig").to(dev, non_blocking=True)
+            d = self.op_sig_dict
+            d = (d if isinstance(d, torch.Tensor) else torch.from_numpy(np.asarray(d).view(np.int64))).to(
+                dev, non_blocking=True)
+            t = torch.empty(code.numel(), dtype=torch.int64, device=dev)
+            _native.check(_native.lib().dw_unpack_dict(_native.ptr(d), _native.ptr(code), code.element_size(),
+                                                       code.numel(), _native.ptr(t), _native.stream_handle()),
+                          "dw_unpack_dict")
+            self._dev[key] = t
+        return t
+
     def host(self, name: str) -> np.ndarray:
-        if name in ("ts", "op_start", "op_end", "k_start", "k_end") or (name == "watts" and self.watts_p0 is not None):
+        if name in ("ts", "op_start", "op_end", "k_start", "k_end") or (name == "watts" and self.watts_p0 is not None) \
+                or (name == "op_sig" and self.op_sig_dict is not None):
             return self.device(name).cpu().numpy()
         return super().host(name)
 
     @property
     def host_bytes(self) -> int:
         """Bytes the hot columns occupy on the host (what crosses PCIe)."""
-        return sum(int(getattr(self, n).numel() * getattr(self, n).element_size()) if isinstance(
-            getattr(self, n), torch.Tensor) else int(getattr(self, n).nbytes)
-            for n in ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "op_sig") if getattr(self, n) is not None)
+        def nb(a):
+            return int(a.numel() * a.element_size()) if isinstance(a, torch.Tensor) else int(np.asarray(a).nbytes)
+        cols = [getattr(self, n) for n in ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "op_sig")]
+        return sum(nb(a) for a in cols + [self.op_sig_dict] if a is not None)
 
 
 def _narrow(d, what: str):
@@ -354,6 +383,50 @@ def _deltas(x, what: str):
     if x.size == 0:
         return 0, np.zeros(0, dtype=np.uint16)
     return int(x[0]), _narrow(np.diff(x, prepend=x[0]), f"{what}: not sorted, or a gap of 2^32 us or more")
+
+
+def _ts_deltas(x, what: str):
+    """(base, bias, deltas) of the power timestamps: biased int8 when every
+    delta after the first lies within 127 of the midpoint (a regular sampling
+    clock with jitter), else as _deltas."""
+    base, d = _deltas(x, what)
+    n = int(d.shape[0])
+    if n < 2:
+        return base, 0, d
+    full = _unsigned(d)
+    tail = full[1:]
+    lo, hi = (int(tail.min().item()), int(tail.max().item())) if isinstance(tail, torch.Tensor) else \
+        (int(tail.min()), int(tail.max()))
+    if hi - lo > 255:
+        return base, 0, d
+    bias = (lo + hi + 1) // 2
+    code = full - bias
+    if isinstance(code, torch.Tensor):
+        code[0] = 0
+        return base, bias, code.to(torch.int8)
+    code[0] = 0
+    return base, bias, code.astype(np.int8)
+
+
+def _sig_dict(sig):
+    """(dictionary u64, codes u16/u32) of the signature column when it has at
+    most 2^32 distinct values (it has ~1e6 at C4), else None."""
+    if sig is None:
+        return None
+    if isinstance(sig, torch.Tensor):
+        if sig.numel() == 0:
+            return None
+        uniq, inv = torch.unique(sig, return_inverse=True)
+        if uniq.numel() > 0x7FFFFFFF:
+            return None
+        code = inv.to(torch.int16) if uniq.numel() <= 0x7FFF else inv.to(torch.int32)
+        return uniq, code
+    a = np.asarray(sig)
+    if a.size == 0:
+        return None
+    uniq, inv = np.unique(a, return_inverse=True)
+    code = inv.astype(np.uint16) if uniq.size <= 0xFFFF else inv.astype(np.uint32)
+    return uniq, code
 
 
 def _durations(start, end, what: str):
@@ -415,15 +488,18 @@ def pack(cols: TraceColumns, decimal: bool = True) -> PackedColumns:
     """Packed form of a trace with sorted power, operator and kernel starts
     (ValueError otherwise -- keep such traces unpacked).  Works on host or
     device columns; the result lives where the input does."""
-    tb, td = _deltas(cols.ts, "power timestamps")
+    tb, tbias, td = _ts_deltas(cols.ts, "power timestamps")
     ob, od = _deltas(cols.op_start, "operator starts")
     kb, kd = _deltas(cols.k_start, "kernel starts")
     dec = decimal_code(cols.watts) if decimal else None
     watts, p0 = (cols.watts, None) if dec is None else (dec[1], dec[0])
+    sd = _sig_dict(cols.op_sig)
+    sig, sig_dict = (cols.op_sig, None) if sd is None else (sd[1], sd[0])
     return PackedColumns(tb, td, watts, ob, od, _durations(cols.op_start, cols.op_end, "operators"),
                          kb, kd, _durations(cols.k_start, cols.k_end, "kernels"), cols.trace_end,
-                         k_op=cols.k_op, op_sig=cols.op_sig, watts_p0=p0, op_ids=cols.op_ids, k_ids=cols.k_ids,
-                         op_names=cols.op_names, op_work=cols.op_work, op_rank=cols.op_rank)
+                         k_op=cols.k_op, op_sig=sig, watts_p0=p0, ts_bias=tbias, op_sig_dict=sig_dict,
+                         op_ids=cols.op_ids, k_ids=cols.k_ids, op_names=cols.op_names, op_work=cols.op_work,
+                         op_rank=cols.op_rank)
 
 
 def save_packed(cols: TraceColumns, path) -> None:
@@ -433,16 +509,19 @@ def save_packed(cols: TraceColumns, path) -> None:
     import json
     pc = cols if isinstance(cols, PackedColumns) else pack(cols)
     arrays = {}
-    for n in ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "k_op", "op_sig", "op_work"):
+    for n in ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "k_op", "op_sig", "op_sig_dict", "op_work"):
         a = getattr(pc, n)
         if a is None:
             continue
         a = a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
-        if n in ("ts", "op_start", "op_end", "k_start", "k_end") or (n == "watts" and pc.watts_p0 is not None):
+        coded = n in ("op_start", "op_end", "k_start", "k_end") or (n == "ts" and a.itemsize > 1) or \
+            (n == "watts" and pc.watts_p0 is not None) or (n == "op_sig" and pc.op_sig_dict is not None)
+        if coded:
             a = a.view(np.uint16 if a.itemsize == 2 else np.uint32)
         arrays[n] = np.ascontiguousarray(a)
     meta = {"format": "dwc", "version": 2, "trace_end": pc.trace_end, "ts_base": pc.ts_base,
-            "op_base": pc.op_start_base, "k_base": pc.k_start_base, "watts_p0": pc.watts_p0, "columns": {}}
+            "op_base": pc.op_start_base, "k_base": pc.k_start_base, "watts_p0": pc.watts_p0,
+            "ts_bias": pc.ts_bias, "columns": {}}
     off = 0
     for n, a in arrays.items():
         meta["columns"][n] = {"dtype": a.dtype.str, "n": int(a.shape[0]), "offset": off}
@@ -480,8 +559,11 @@ def load_packed(path, pin: bool = False) -> PackedColumns:
             return x.view(torch.int16 if x.element_size() == 2 else torch.int32)
         return x
     p0 = meta.get("watts_p0")
+    sig_dict = cols.get("op_sig_dict")
+    sig = cols.get("op_sig")
     return PackedColumns(meta["ts_base"], as_signed(cols["ts"]), as_signed(cols["watts"]) if p0 is not None
                          else cols["watts"], meta["op_base"], as_signed(cols["op_start"]), as_signed(cols["op_end"]),
                          meta["k_base"], as_signed(cols["k_start"]), as_signed(cols["k_end"]), meta["trace_end"],
-                         k_op=cols.get("k_op"), op_sig=cols.get("op_sig"), op_work=cols.get("op_work"),
-                         watts_p0=p0)
+                         k_op=cols.get("k_op"), op_sig=as_signed(sig) if sig_dict is not None else sig,
+                         op_work=cols.get("op_work"), watts_p0=p0, ts_bias=meta.get("ts_bias", 0),
+                         op_sig_dict=sig_dict)

@@ -16,10 +16,10 @@
 namespace dw {
 
 template <typename T>
-struct DeltaAt {  // value i of the scan input: base + d[0] at 0, d[i] after
+struct DeltaAt {  // value i of the scan input: base at 0, bias + d[i] after
     const T *d;
-    int64_t base;
-    __host__ __device__ int64_t operator()(int64_t i) const { return i == 0 ? base + (int64_t)d[0] : (int64_t)d[i]; }
+    int64_t base, bias;
+    __host__ __device__ int64_t operator()(int64_t i) const { return i == 0 ? base : bias + (int64_t)d[i]; }
 };
 
 template <typename T>
@@ -32,17 +32,19 @@ __global__ void add_duration_kernel(const int64_t *start, const T *dur, int64_t 
 template <typename T>
 static size_t scan_bytes_t(int64_t n) {
     size_t b = 0;
-    auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), DeltaAt<T>{nullptr, 0});
+    auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), DeltaAt<T>{nullptr, 0, 0});
     cub::DeviceScan::InclusiveSum(nullptr, b, it, (int64_t *)nullptr, (int)std::max<int64_t>(n, 1));
     return b;
 }
-static size_t scan_bytes(int64_t n) { return std::max(scan_bytes_t<uint32_t>(n), scan_bytes_t<uint16_t>(n)); }
+static size_t scan_bytes(int64_t n) {
+    return std::max(std::max(scan_bytes_t<uint32_t>(n), scan_bytes_t<uint16_t>(n)), scan_bytes_t<int8_t>(n));
+}
 
 template <typename T>
-static void scan_deltas(const void *delta, int64_t n, int64_t base, int64_t *out, void *ws, size_t bytes,
-                        cudaStream_t s) {
+static void scan_deltas(const void *delta, int64_t n, int64_t base, int64_t bias, int64_t *out, void *ws,
+                        size_t bytes, cudaStream_t s) {
     auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
-                                              DeltaAt<T>{(const T *)delta, base});
+                                              DeltaAt<T>{(const T *)delta, base, bias});
     cub::DeviceScan::InclusiveSum(ws, bytes, it, out, (int)n, s);
     count_launch(2);
 }
@@ -60,6 +62,13 @@ static void add_durations(const int64_t *start, const void *dur, int64_t n, int6
 // "m e-(p0+j)" yields, so the decode is exact.
 __constant__ double POW10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
                                  1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
+
+template <typename T>
+__global__ void dict_decode_kernel(const uint64_t *dict, const T *code, int64_t n, uint64_t *out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+        __stcs(out + i, __ldg(dict + __ldcs(code + i)));
+}
 
 __global__ void decimal_decode_kernel(const uint32_t *code, int64_t n, int32_t p0, double *out) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -79,16 +88,20 @@ extern "C" {
 
 size_t dw_unpack_workspace_size(int64_t n) { return scan_bytes(n) + 256; }
 
-int dw_unpack_deltas_w(const void *d_delta, int32_t delta_bytes, int64_t n, int64_t base, int64_t *d_out,
-                       const void *d_dur, int32_t dur_bytes, int64_t *d_end, void *d_workspace,
+int dw_unpack_deltas_w(const void *d_delta, int32_t delta_bytes, int64_t delta_bias, int64_t n, int64_t base,
+                       int64_t *d_out, const void *d_dur, int32_t dur_bytes, int64_t *d_end, void *d_workspace,
                        size_t workspace_bytes, dw_stream_t stream) {
     if (n < 0 || (n && (!d_delta || !d_out)) || (d_dur && !d_end) || n >= ((int64_t)1 << 31)) return DW_E_ARG;
-    if ((delta_bytes != 2 && delta_bytes != 4) || (d_dur && dur_bytes != 2 && dur_bytes != 4)) return DW_E_ARG;
+    if ((delta_bytes != 1 && delta_bytes != 2 && delta_bytes != 4) ||
+        (d_dur && dur_bytes != 2 && dur_bytes != 4))
+        return DW_E_ARG;
     if (n == 0) return DW_OK;
     if (!d_workspace || workspace_bytes < dw_unpack_workspace_size(n)) return DW_E_WORKSPACE;
     cudaStream_t s = (cudaStream_t)stream;
-    if (delta_bytes == 2) scan_deltas<uint16_t>(d_delta, n, base, d_out, d_workspace, workspace_bytes, s);
-    else scan_deltas<uint32_t>(d_delta, n, base, d_out, d_workspace, workspace_bytes, s);
+    if (delta_bytes == 1) scan_deltas<int8_t>(d_delta, n, base, delta_bias, d_out, d_workspace, workspace_bytes, s);
+    else if (delta_bytes == 2)
+        scan_deltas<uint16_t>(d_delta, n, base, delta_bias, d_out, d_workspace, workspace_bytes, s);
+    else scan_deltas<uint32_t>(d_delta, n, base, delta_bias, d_out, d_workspace, workspace_bytes, s);
     if (d_dur) {
         if (dur_bytes == 2) add_durations<uint16_t>(d_out, d_dur, n, d_end, s);
         else add_durations<uint32_t>(d_out, d_dur, n, d_end, s);
@@ -97,9 +110,26 @@ int dw_unpack_deltas_w(const void *d_delta, int32_t delta_bytes, int64_t n, int6
     return DW_OK;
 }
 
+int dw_unpack_dict(const uint64_t *d_dict, const void *d_code, int32_t code_bytes, int64_t n, uint64_t *d_out,
+                   dw_stream_t stream) {
+    if (n < 0 || (n && (!d_dict || !d_code || !d_out)) || (code_bytes != 2 && code_bytes != 4)) return DW_E_ARG;
+    if (n) {
+        const unsigned grid = (unsigned)std::min<int64_t>(num_sms() * 8, ceil_div(n, 256));
+        if (code_bytes == 2)
+            dict_decode_kernel<uint16_t><<<grid, 256, 0, (cudaStream_t)stream>>>(d_dict, (const uint16_t *)d_code,
+                                                                                 n, d_out);
+        else
+            dict_decode_kernel<uint32_t><<<grid, 256, 0, (cudaStream_t)stream>>>(d_dict, (const uint32_t *)d_code,
+                                                                                 n, d_out);
+        count_launch();
+    }
+    DW_CHECK_LAUNCH();
+    return DW_OK;
+}
+
 int dw_unpack_deltas(const uint32_t *d_delta, int64_t n, int64_t base, int64_t *d_out, const uint32_t *d_dur,
                      int64_t *d_end, void *d_workspace, size_t workspace_bytes, dw_stream_t stream) {
-    return dw_unpack_deltas_w(d_delta, 4, n, base, d_out, d_dur, 4, d_end, d_workspace, workspace_bytes, stream);
+    return dw_unpack_deltas_w(d_delta, 4, 0, n, base, d_out, d_dur, 4, d_end, d_workspace, workspace_bytes, stream);
 }
 
 int dw_unpack_decimal(const uint32_t *d_code, int64_t n, int32_t p0, double *d_out, dw_stream_t stream) {

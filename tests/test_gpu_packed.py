@@ -18,8 +18,9 @@ def test_decode_exact_and_ledger_identical(tmp_path):
     a, b = synth.make_pair(cfg)
     p = pack(a)
     assert p.watts_p0 is not None  # synthetic watts are at the format's 9-digit precision
-    assert p.ts.element_size() == 2 and p.k_end.element_size() == 2
-    for n in ("ts", "watts", "op_start", "op_end", "k_start", "k_end"):
+    assert p.ts.element_size() == 1 and p.k_end.element_size() == 2  # regular clock: int8 ts deltas
+    assert p.op_sig_dict is not None
+    for n in ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "op_sig"):
         assert torch.equal(p.device(n), a.device(n)), n
     assert p.signal_span() == a.signal_span()
     la, lp = build_ledger(a, method="samples"), build_ledger(p, method="samples")
@@ -39,7 +40,8 @@ def test_decode_exact_and_ledger_identical(tmp_path):
     # the shipped host form carries no owner column: classification by containment
     from paper_2512_08365_b200.columns import PackedColumns
     bare = [PackedColumns(q.ts_base, q.ts, q.watts, q.op_start_base, q.op_start, q.op_end, q.k_start_base,
-                          q.k_start, q.k_end, q.trace_end, op_sig=q.op_sig, watts_p0=q.watts_p0) for q in (ha, hb)]
+                          q.k_start, q.k_end, q.trace_end, op_sig=q.op_sig, watts_p0=q.watts_p0, ts_bias=q.ts_bias,
+                          op_sig_dict=q.op_sig_dict) for q in (ha, hb)]
     rb = analyze(bare[0], bare[1], "samples", 0.10, 20)
     assert [f.category for f in rb.report.findings] == [f.category for f in ra.report.findings]
     assert rb.report.wasted_joules == ra.report.wasted_joules

@@ -42,7 +42,7 @@ def test_roundtrip(tmp_path):
     np.testing.assert_array_equal(dec(p.op_start_base, p.op_start) + _u(p.op_end), c.op_end)
     np.testing.assert_array_equal(dec(p.k_start_base, p.k_start) + _u(p.k_end), c.k_end)
     assert np.asarray(p.ts).itemsize == 2 and np.asarray(p.op_end).itemsize == 4  # narrowest width per column
-    np.testing.assert_array_equal(np.asarray(p.op_sig), c.op_sig)
+    np.testing.assert_array_equal(np.asarray(p.op_sig_dict)[_u(p.op_sig)], c.op_sig)  # dictionary-coded
     np.testing.assert_array_equal(np.asarray(p.k_op), c.k_op)
     assert p.signal_span() == c.signal_span()
     assert p.n_power == c.n_power and p.n_ops == c.n_ops and p.n_kernels == c.n_kernels
@@ -95,3 +95,25 @@ def test_non_decimal_watts_stay_f64():
     assert decimal_code(np.array([1.0 / 3.0, 2.0])) is None
     assert decimal_code(np.array([-1.0])) is None
     assert decimal_code(np.array([np.nan])) is None
+
+
+def test_regular_clock_ts_pack_to_int8(tmp_path):
+    """A sampling clock with jitter: biased int8 deltas; signatures as a
+    dictionary + 16-bit codes."""
+    rng = np.random.default_rng(5)
+    ts = (10**9 + np.cumsum(160 + rng.integers(-40, 41, size=5000))).astype(np.int64)
+    sig = rng.integers(0, 300, size=50).astype(np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+    st = np.sort(rng.integers(ts[0], ts[-1] - 1000, size=50))
+    c = TraceColumns.from_arrays(ts, np.full(5000, 75.0), st, st + 100, op_sig=sig)
+    for p in (pack(c), None):
+        if p is None:
+            save_packed(c, tmp_path / "r.dwc")
+            p = load_packed(tmp_path / "r.dwc")
+        t = np.asarray(p.ts)
+        assert t.dtype == np.int8
+        d = t.astype(np.int64) + p.ts_bias
+        d[0] = 0
+        np.testing.assert_array_equal(p.ts_base + np.cumsum(d), ts)
+        assert np.asarray(p.op_sig).itemsize == 2
+        np.testing.assert_array_equal(np.asarray(p.op_sig_dict)[_u(p.op_sig)], sig)
+        assert p.signal_span() == c.signal_span()
