@@ -70,13 +70,27 @@ __global__ void dict_decode_kernel(const uint64_t *dict, const T *code, int64_t 
         __stcs(out + i, __ldg(dict + __ldcs(code + i)));
 }
 
+// correctly rounded 1/10^p: with Markstein's final FMA step the quotient
+// m / 10^p equals IEEE division for every m < 2^30 and p <= 22 (exhaustive:
+// scripts/micro/dec_check.cu, 0 mismatches over 23 x 2^30), at a fraction of
+// __ddiv_rn's instructions.
+__constant__ double RCP10[23] = {1.0, 0.1, 0.01, 0.001, 0.0001, 1e-05, 1e-06, 1e-07, 1e-08, 1e-09, 1e-10, 1e-11, 1e-12, 1e-13, 1e-14, 1e-15, 1e-16, 1e-17, 1e-18, 1e-19, 1e-20, 1e-21, 1e-22};
+
 __global__ void decimal_decode_kernel(const uint32_t *code, int64_t n, int32_t p0, double *out) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
         const uint32_t c = __ldcs(code + i);
         const double m = (double)(c & 0x3FFFFFFFu);
         const int p = p0 + (int)(c >> 30);
-        __stcs(out + i, p >= 0 ? __ddiv_rn(m, POW10[p]) : __dmul_rn(m, POW10[-p]));
+        double v;
+        if (p >= 0) {
+            const double y = RCP10[p], d = POW10[p];
+            const double q = __dmul_rn(m, y);
+            v = __fma_rn(__fma_rn(-q, d, m), y, q);
+        } else {
+            v = __dmul_rn(m, POW10[-p]);
+        }
+        __stcs(out + i, v);
     }
 }
 
