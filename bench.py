@@ -362,7 +362,7 @@ def run_ours(args, rank: int, world: int, local: int):
             r = analyze(pinned[0], pinned[1], args.method, 0.10, args.k, copy_stream=copy_stream)
             return r
 
-        for _ in range(max(3, args.warmup)):  # the first steps run ~50 % slower (allocator, pinned pages)
+        for _ in range(max(5, args.warmup)):  # the first steps run up to 50 % slower (allocator, pinned pages)
             e2e_step()
         torch.cuda.synchronize()
         if world > 1:

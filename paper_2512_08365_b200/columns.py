@@ -111,10 +111,10 @@ class TraceColumns:
 
     HOT = ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "op_sig")
 
-    def prefetch(self, stream: "torch.cuda.Stream", names=HOT) -> None:
+    def prefetch(self, stream: "torch.cuda.Stream", names=HOT) -> "torch.cuda.Event":
         """Start the host->HBM copies of ``names`` on ``stream`` (pinned host
         buffers copy asynchronously); later device() calls on another stream
-        wait for them."""
+        wait for them (``wait_ready``, or the returned event)."""
         dev = _native.device()
         with torch.cuda.stream(stream):
             for n in names:
@@ -123,6 +123,7 @@ class TraceColumns:
             ev = torch.cuda.Event()
             ev.record(stream)
         self._dev["__ready__"] = ev
+        return ev
 
     def wait_ready(self) -> None:
         ev = self._dev.pop("__ready__", None)
@@ -268,6 +269,29 @@ class PackedColumns(TraceColumns):
             self._dev["first_last"] = (first, last)
         return self._dev["first_last"]
 
+    def _staged(self, name, dev):
+        """The packed column in HBM: staged by prefetch(), else copied now."""
+        t = self._dev.pop(("raw", name, dev.index), None)
+        return t if t is not None else self._raw(name).to(dev, non_blocking=True)
+
+    def prefetch(self, stream: "torch.cuda.Stream", names=TraceColumns.HOT) -> "torch.cuda.Event":
+        """All host->HBM copies of ``names`` first (event ``copied``), then the
+        decodes, on ``stream``: a copy queued behind this one (another trace)
+        waits for the transfers only, not for the decodes."""
+        dev = _native.device()
+        raw = {"op_end": "op_start", "k_end": "k_start"}
+        with torch.cuda.stream(stream):
+            for n in names:
+                for m in (n, {"op_start": "op_end", "k_start": "k_end"}.get(n), raw.get(n)):
+                    if m is None or getattr(self, m) is None or (m, dev.index) in self._dev \
+                            or ("raw", m, dev.index) in self._dev:
+                        continue
+                    self._dev[("raw", m, dev.index)] = self._raw(m).to(dev, non_blocking=True)
+            copied = torch.cuda.Event()
+            copied.record(stream)
+        self.copied = copied
+        return super().prefetch(stream, names)
+
     def _raw(self, name):
         src = getattr(self, name)
         if isinstance(src, torch.Tensor):
@@ -290,13 +314,13 @@ class PackedColumns(TraceColumns):
         if t is not None:
             return t
         base_name = {"op_end": "op_start", "k_end": "k_start"}.get(name, name)
-        delta = self._raw(base_name).to(dev, non_blocking=True)
+        delta = self._staged(base_name, dev)
         n = int(delta.numel())
         out = torch.empty(n, dtype=torch.int64, device=dev)
         end = None
         dur_name = {"op_start": "op_end", "k_start": "k_end"}.get(base_name)
         if dur_name is not None:
-            dur = self._raw(dur_name).to(dev, non_blocking=True)
+            dur = self._staged(dur_name, dev)
             end = torch.empty(n, dtype=torch.int64, device=dev)
         base = {"ts": self.ts_base, "op_start": self.op_start_base, "k_start": self.k_start_base}[base_name]
         L = _native.lib()
@@ -317,7 +341,7 @@ class PackedColumns(TraceColumns):
         key = ("watts", dev.index)
         t = self._dev.get(key)
         if t is None:
-            code = self._raw("watts").to(dev, non_blocking=True)
+            code = self._staged("watts", dev)
             t = torch.empty(code.numel(), dtype=torch.float64, device=dev)
             _native.check(_native.lib().dw_unpack_decimal(_native.ptr(code), code.numel(), self.watts_p0,
                                                           _native.ptr(t), _native.stream_handle()),
@@ -330,7 +354,7 @@ class PackedColumns(TraceColumns):
         key = ("op_sig", dev.index)
         t = self._dev.get(key)
         if t is None:
-            code = self._raw("op_sig").to(dev, non_blocking=True)
+            code = self._staged("op_sig", dev)
             d = self.op_sig_dict
             d = (d if isinstance(d, torch.Tensor) else torch.from_numpy(np.asarray(d).view(np.int64))).to(
                 dev, non_blocking=True)

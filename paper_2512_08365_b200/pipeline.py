@@ -16,7 +16,7 @@ from . import _native
 from .columns import TraceColumns
 from .detect import DEFAULT_THRESHOLD, Report
 from .energy import EnergyLedger, build_ledger
-from .join import JoinDiff, join_diff
+from .join import JoinDiff, join_diff, join_prepare
 
 
 @dataclass
@@ -35,15 +35,28 @@ def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAUL
     (Running the join's pairing on a second stream beside the ledgers, with
     the tile kernel capped to fewer SMs via dw_set_attribute_sms, was measured
     slower on C4 -- 35.4 vs 34.5 ms at 12 reserved SMs, worse with more -- so
-    the phases run back to back.)"""
+    the phases run back to back.)
+
+    With ``copy_stream`` (host-resident inputs): B's host->HBM copy runs on
+    that stream after A's, under A's attribution, B's signature columns first, so the
+    pairing (``join_prepare``, signatures only) runs while the rest of B is
+    still crossing PCIe; only B's ledger and the findings remain after the
+    last byte lands."""
     ca, cb = TraceColumns.from_trace(trace_a), TraceColumns.from_trace(trace_b)
+    prep = None
     if copy_stream is not None:
-        # B's host->HBM copy runs under A's attribution
-        ca.prefetch(torch.cuda.current_stream())
+        a_ready = ca.prefetch(torch.cuda.current_stream())
+        # B's copies queue behind A's transfers (not its decodes): concurrent
+        # copies would share PCIe and delay A to the end of the transfer
+        copy_stream.wait_event(getattr(ca, "copied", None) or a_ready)
+        sig_ready = cb.prefetch(copy_stream, names=("op_sig", "op_start", "op_end"))
         cb.prefetch(copy_stream)
     la = build_ledger(ca, method=method)
+    if copy_stream is not None:
+        torch.cuda.current_stream().wait_event(sig_ready)
+        prep = join_prepare(ca, cb)
     lb = build_ledger(cb, method=method)
-    jd = join_diff(ca, cb, la, lb, threshold, k, full_columns=not lean, epw=not lean)
+    jd = join_diff(ca, cb, la, lb, threshold, k, full_columns=not lean, epw=not lean, prep=prep)
     top = jd.top_findings(ca, cb)
     ineff = max(la.total_joules, lb.total_joules)
     pct = jd.wasted_joules / ineff if ineff > 0 else 0.0
