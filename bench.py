@@ -315,7 +315,9 @@ def run_ours(args, rank: int, world: int, local: int):
     e2e_skip = None
     if not args.no_e2e:
         import psutil
-        need = 12 * samples + 8 * intervals + 8 * (ca.n_ops + cb.n_ops)  # packed columns, this rank
+        # packed columns of this rank (worst case: 16-bit ts deltas, 32-bit
+        # watts codes, 16-bit interval deltas + durations, 32-bit sig codes)
+        need = 6 * samples + 4 * intervals + 4 * (ca.n_ops + cb.n_ops)
         local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
         avail = psutil.virtual_memory().available
         if need * local_world > 0.75 * avail:
