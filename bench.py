@@ -311,26 +311,26 @@ def run_ours(args, rank: int, world: int, local: int):
 
     # ---- e2e through the public API from pinned host buffers
     e2e = None
-    # pinned host memory the e2e leg needs on this box (all local ranks share it)
     e2e_skip = None
     if not args.no_e2e:
+        del res, la, lb, jd
+        # the host holds what a deployment ships: packed columns
+        # (columns.PackedColumns) in pinned memory.  Pack on the device first:
+        # the exact host bytes decide whether this box's memory holds every
+        # local rank's copy (all local ranks share it).
         import psutil
-        # packed columns of this rank (worst case: 16-bit ts deltas, 32-bit
-        # watts codes, 16-bit interval deltas + durations, 32-bit sig codes)
-        need = 6 * samples + 4 * intervals + 4 * (ca.n_ops + cb.n_ops)
+        from paper_2512_08365_b200.columns import PackedColumns, pack
+        packed = [pack(c) for c in (ca, cb)]
+        need = sum(pc.host_bytes for pc in packed)
         local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
         avail = psutil.virtual_memory().available
         if need * local_world > 0.75 * avail:
             e2e_skip = (f"host memory: {local_world} ranks x {need / 1e9:.1f} GB pinned > 75% of "
                         f"{avail / 1e9:.0f} GB available")
+            del packed
     if not args.no_e2e and e2e_skip is None:
-        del res, la, lb, jd
-        # the host holds what a deployment ships: packed columns (uint32 time
-        # deltas / durations, columns.PackedColumns) in pinned memory
-        from paper_2512_08365_b200.columns import PackedColumns, pack
         pinned = []
-        for c in (ca, cb):
-            pc = pack(c)
+        for c, pc in zip((ca, cb), packed):
 
             def pin(t):  # straight into pinned memory: no pageable staging copy
                 h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
@@ -342,7 +342,7 @@ def run_ours(args, rank: int, world: int, local: int):
                                op_sig_dict=pin(pc.op_sig_dict) if pc.op_sig_dict is not None else None)
             hc._dev["first_last"] = c._first_last_ts()
             pinned.append(hc)
-            del pc
+        del packed, pc
         h2d = sum(pc.host_bytes for pc in pinned)
         pc0 = pinned[0]
         tsw = pc0.ts.element_size()
