@@ -53,3 +53,24 @@ def test_unfold_descriptor_layout_matches_header():
     assert [(t, n) for t, n, _ in fields] == [("int64_t", "value_off"), ("int64_t", "out_off"),
                                              ("int64_t", "scratch_off"), ("int32_t", "order"),
                                              ("int32_t", "mask"), ("int32_t", "dims")]
+
+
+def test_new_entry_points_reject_bad_arguments_before_touching_the_device():
+    """Argument validation of the 8(f) entry points runs on the host: bad sizes
+    and widths return DW_E_ARG (no CUDA call is made, so this runs without a
+    GPU)."""
+    L = ctypes.CDLL(str(_native.LIB_PATH))
+    E_ARG = _native.DW_E_ARG
+    i64 = ctypes.c_int64
+    assert L.dw_tensor_norms(None, None, i64(-1), None, None) == E_ARG
+    assert L.dw_tensor_prefilter(2, i64(1), i64(1), 1, None, None, None, None, ctypes.c_double(1e-3), None, None,
+                                 None, None, None) == E_ARG
+    assert L.dw_unfold_spectra(None, None, i64(-1), i64(0), None, None, None, None) == E_ARG
+    assert L.dw_unfold_spectra(None, None, i64(0), i64(1 << 40), None, None, None, None) == E_ARG
+    assert L.dw_spectra_embed(None, None, None, None, None, i64(-1), None, None, ctypes.c_double(1e-3), None,
+                              None) == E_ARG
+    assert L.dw_unpack_deltas_w(None, 3, i64(0), i64(5), i64(0), None, None, 4, None, None, ctypes.c_size_t(0),
+                                None) == E_ARG
+    assert L.dw_unpack_dict(None, None, 1, i64(4), None, None) == E_ARG
+    assert L.dw_unpack_decimal(None, i64(-1), 6, None, None) == E_ARG
+    assert L.dw_unpack_decimal(None, i64(0), 30, None, None) == E_ARG
