@@ -379,6 +379,31 @@ int dw_spectra_embed(const double *d_spec, const int64_t *d_u_off, const int32_t
                      const int32_t *d_set_count, int64_t n_jobs, const int64_t *d_job_a, const int64_t *d_job_b,
                      double eps, double *d_score, dw_stream_t stream);
 
+/* ------------------------------------------- time-window join exchange (8(e))
+ * Replaces shard.py's pack + sort-by-destination + NCCL all-to-all of the
+ * sharded signature join (the reference has no multi-GPU path; SURVEY.md
+ * 8(e)) with one kernel storing records straight into the receivers' buffers
+ * through CUDA IPC mappings (P2P over NVLink/NVSwitch). */
+#define DW_MAX_PEERS 64
+#define DW_XCH_MAX_WIDTH 8
+#define DW_IPC_HANDLE_BYTES 64
+
+/* d_counts[d] = number of records (one per operator, d_sig[i]) bound for rank
+ * d = ((sig ^ (sig >> 31)) & 0x7FFFFFFF) % world. */
+int dw_exchange_count(const int64_t *d_sig, int64_t n, int32_t world, uint64_t *d_counts, dw_stream_t stream);
+/* Record i (the width int64 columns cols[0..width-1] at row i) is stored at
+ * d_peer[d] + (base[d] + slot) * width for its destination d, slot a
+ * per-destination counter (d_cursor[world], reset here).  cols, d_peer and
+ * base are HOST arrays of device pointers / offsets. */
+int dw_exchange_scatter(const int64_t *const *cols, int32_t width, const int64_t *d_sig, int64_t n, int32_t world,
+                        int64_t *const *d_peer, const int64_t *base, uint64_t *d_cursor, dw_stream_t stream);
+/* CUDA IPC plumbing for the receive buffers (64-byte handles).  A buffer
+ * inside a larger allocation exports the allocation's handle plus its byte
+ * offset; the opener adds the offset to what dw_ipc_open returns. */
+int dw_ipc_handle(const void *d_ptr, void *handle_out, int64_t *offset_out);
+int dw_ipc_open(const void *handle, void **d_ptr_out);
+int dw_ipc_close(void *d_ptr);
+
 const char *dw_version(void);
 const char *dw_error_string(int code);
 /* number of kernel launches issued by this library on the calling thread

@@ -45,6 +45,7 @@ EXPORTED = (
     "dw_ig_parse_op", "dw_ig_parse_kernel", "dw_ig_hash", "dw_ig_kernel_lists",
     "dw_fx_sum_workspace_size", "dw_fx_sum", "dw_step_value_at", "dw_detect_pairs",
     "dw_rank_workspace_size", "dw_rank", "dw_join_workspace_size", "dw_join_diff",
+    "dw_exchange_count", "dw_exchange_scatter", "dw_ipc_handle", "dw_ipc_open", "dw_ipc_close",
     "dw_tensor_norms", "dw_tensor_prefilter", "dw_unfold_smem_doubles", "dw_unfold_spectra", "dw_spectra_embed",
     "dw_version", "dw_error_string", "dw_launch_count", "dw_kernel_timing", "dw_kernel_time_ms",
 )
@@ -146,6 +147,11 @@ def lib():
         L.dw_replay.argtypes = [ctypes.POINTER(Signal), c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp,
                                 c_vp, c_vp]
         L.dw_tensor_norms.argtypes = [c_vp, c_vp, c_i64, c_vp, c_vp]
+        L.dw_exchange_count.argtypes = [c_vp, c_i64, c_i32, c_vp, c_vp]
+        L.dw_exchange_scatter.argtypes = [c_vp, c_i32, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]
+        L.dw_ipc_handle.argtypes = [c_vp, c_vp, c_vp]
+        L.dw_ipc_open.argtypes = [c_vp, ctypes.POINTER(c_vp)]
+        L.dw_ipc_close.argtypes = [c_vp]
         L.dw_tensor_prefilter.argtypes = [ctypes.c_int, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp,
                                           ctypes.c_double, c_vp, c_vp, c_vp, c_vp, c_vp]
         L.dw_unfold_smem_doubles.restype = c_i64

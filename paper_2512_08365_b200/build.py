@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libdwb200.so"
-SOURCES = ["capi.cu", "attribute.cu", "split.cu", "replay.cu", "diff.cu", "pack.cu", "ingest.cu", "tensor.cu"]
+SOURCES = ["capi.cu", "attribute.cu", "split.cu", "replay.cu", "diff.cu", "pack.cu", "ingest.cu", "tensor.cu", "exchange.cu"]
 HEADERS = ["dw_common.cuh"]
 
 NVCC_FLAGS = [
@@ -73,7 +73,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> Path
         objs.append(str(obj))
     tmp = OUT_DIR / (lib.name + ".tmp")
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
-           *objs, "-lcudart"]
+           *objs, "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

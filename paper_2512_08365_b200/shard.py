@@ -78,13 +78,68 @@ def plan(n_samples: int, world: int, kind: str) -> list[Window]:
 
 
 class Comm:
-    """The two collectives the sharded path needs, over torch.distributed."""
+    """The collectives the sharded path needs, over torch.distributed; with
+    ``p2p`` (every rank on this node, CUDA tensors) the join's record exchange
+    is one kernel storing into the peers' buffers (``exchange``)."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, p2p: Optional[bool] = None):
+        import os
         import torch.distributed as dist
         self.dist, self.group = dist, group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        if p2p is None:  # CUDA IPC reaches only the ranks of this node
+            p2p = (torch.cuda.is_available() and os.environ.get("DWB200_P2P", "1") != "0"
+                   and int(os.environ.get("LOCAL_WORLD_SIZE", self.world)) == self.world)
+        self.p2p = bool(p2p)
+
+    def exchange(self, o: "ShardOps", with_rank: bool) -> torch.Tensor:
+        """The records of ``o`` bound for this rank from every rank (rows of
+        idx, sig, start, end, joules bits[, rank]): one sizing pass, the count
+        matrix swapped, receive buffers shared over CUDA IPC, then ONE kernel
+        (dw_exchange_scatter) stores every record straight into its
+        receiver's buffer -- the pack, sort and all-to-all of the NCCL path
+        fused, over NVLink peer memory."""
+        L, p = _native.lib(), _native.ptr
+        dev = o.sig.device
+        st = _native.stream_handle()
+        world, me = self.world, self.rank
+        width = 6 if with_rank else 5
+        n = int(o.sig.numel())
+        counts = torch.empty(world, dtype=torch.int64, device=dev)
+        _native.check(L.dw_exchange_count(p(o.sig), n, world, p(counts), st), "dw_exchange_count")
+        mat = self.all_gather_object(counts.cpu().tolist())  # mat[src][dst]
+        recv_n = sum(mat[s][me] for s in range(world))
+        recv = torch.empty(max(recv_n, 1) * width, dtype=torch.int64, device=dev)
+        handle = (ctypes.c_char * 64)()
+        off = ctypes.c_int64(0)
+        _native.check(L.dw_ipc_handle(p(recv), handle, ctypes.byref(off)), "dw_ipc_handle")
+        shared = self.all_gather_object((bytes(handle), int(off.value)))
+        peers, opened = [], []
+        try:
+            for d in range(world):
+                if d == me:
+                    peers.append(p(recv))
+                    continue
+                ptr = ctypes.c_void_p()
+                _native.check(L.dw_ipc_open(shared[d][0], ctypes.byref(ptr)), "dw_ipc_open")
+                opened.append(ptr)
+                peers.append(ptr.value + shared[d][1])
+            base = [sum(mat[s][d] for s in range(me)) for d in range(world)]
+            cols = [o.idx, o.sig, o.start, o.end, o.joules.view(torch.int64)] + ([o.rank] if with_rank else [])
+            cols = [c.contiguous() for c in cols]
+            cursor = torch.empty(world, dtype=torch.int64, device=dev)
+            col_ptrs = (ctypes.c_void_p * width)(*[p(c) for c in cols])
+            peer_ptrs = (ctypes.c_void_p * world)(*peers)
+            base_arr = (ctypes.c_int64 * world)(*base)
+            _native.check(L.dw_exchange_scatter(col_ptrs, width, p(o.sig), n, world, peer_ptrs, base_arr, p(cursor),
+                                                st), "dw_exchange_scatter")
+            torch.cuda.current_stream().synchronize()  # this rank's stores have landed
+            self.dist.barrier(group=self.group)        # ... and every other rank's
+        finally:
+            for ptr in opened:
+                L.dw_ipc_close(ptr)
+        return recv[:recv_n * width].view(-1, width)
 
     def all_gather_object(self, obj):
         out = [None] * self.world
@@ -522,9 +577,12 @@ def sharded_join(A: ShardOps, B: ShardOps, n_a: int, comm: Comm, threshold: floa
     of their signature meets in global op order -- so the local join pairs
     exactly as the one-GPU join.  Local top-k candidates carry global finding
     numbers and merge over the ranks (dist.merge_order)."""
-    from .dist import merge_order
-    a = _unpack(comm.all_to_all(_partition(A, comm.world, True)), 6)
-    b = _unpack(comm.all_to_all(_partition(B, comm.world, False)), 5)
+    if getattr(comm, "p2p", False) and A.sig.is_cuda:
+        a = _unpack([comm.exchange(A, True)], 6)
+        b = _unpack([comm.exchange(B, False)], 5)
+    else:
+        a = _unpack(comm.all_to_all(_partition(A, comm.world, True)), 6)
+        b = _unpack(comm.all_to_all(_partition(B, comm.world, False)), 5)
     jd, ca, cb = _local_join(a, b, threshold, k)
     part, tie = _local_part(jd, ca, cb, a, b)
     b_only_sorted = sorted(x for lst in comm.all_gather_object(part.b_only_global) for x in lst)
