@@ -409,7 +409,8 @@ def run_ours(args, rank: int, world: int, local: int):
                                f"{cfg.n_samples} power samples per trace",
                    "method": args.method, "intervals_per_pair": intervals,
                    "samples_per_pair": samples, "findings": P, "top_k": args.k,
-                   "l2": "inputs (~44 GB/pair) >> 126 MB L2; no flush needed",
+                   "l2": (f"inputs (~{(16 * samples + 24 * intervals) / 1e9:.1f} GB/pair read per step) >> "
+                          f"126 MB L2; no flush needed"),
                    "parallelism": f"pair-per-rank x{world}"},
         "samples_per_s": world * samples / (ms_max / 1e3),
         "attribution_ms": (t1 - t0) * 1e3, "diff_latency_ms": (t2 - t1) * 1e3,
