@@ -405,7 +405,7 @@ def classify_vectors(ref):
     sim = ref.simulate
     cases = [(p, sim.preset(p)) for p in ("tf32_misconfig", "join_redundant", "fused_api_misuse",
                                            "layout_null", "attention_block")]
-    cases += [(f"fuzz_{i:02d}", m) for i, m in enumerate(sim.fuzz(20260808, 40))]
+    cases += [(f"fuzz_{i:03d}", m) for i, m in enumerate(sim.fuzz(20260808, 120))]
     out = {}
     tmp = Path(tempfile.mkdtemp())
     for name, manifest in cases:
