@@ -133,19 +133,27 @@ class JoinDiff:
 
         def pick(name, fallback):
             t = getattr(c, name)
-            return (t[idx] if t is not None else fallback()).cpu().numpy()
+            return t[idx] if t is not None else fallback()
 
         zero_f = torch.zeros((), dtype=torch.float64, device=idx.device)
         zero_i = torch.zeros((), dtype=torch.int64, device=idx.device)
-        ea = pick("energy_a", lambda: torch.where(has_a, self.ja[ia_c], zero_f))
-        eb = pick("energy_b", lambda: torch.where(has_b, self.jb[ib_c], zero_f))
-        la = pick("latency_a", lambda: torch.where(
-            has_a, cols_a.device("op_end")[ia_c] - cols_a.device("op_start")[ia_c], zero_i))
-        lb = pick("latency_b", lambda: torch.where(
-            has_b, cols_b.device("op_end")[ib_c] - cols_b.device("op_start")[ib_c], zero_i))
-        h = {n: getattr(c, n)[idx].cpu().numpy() for n in ("ratio", "wasted", "verdict", "side",
-                                                            "informational")}
-        ia, ib = ia_d.cpu().numpy(), ib_d.cpu().numpy()
+        # every column of the k rows in two device tensors: two D2H copies
+        fcols = torch.stack([
+            pick("energy_a", lambda: torch.where(has_a, self.ja[ia_c], zero_f)),
+            pick("energy_b", lambda: torch.where(has_b, self.jb[ib_c], zero_f)),
+            c.ratio[idx], c.wasted[idx]]).cpu().numpy()
+        icols = torch.stack([
+            pick("latency_a", lambda: torch.where(
+                has_a, cols_a.device("op_end")[ia_c] - cols_a.device("op_start")[ia_c], zero_i)),
+            pick("latency_b", lambda: torch.where(
+                has_b, cols_b.device("op_end")[ib_c] - cols_b.device("op_start")[ib_c], zero_i)),
+            c.verdict[idx].to(torch.int64), c.side[idx].to(torch.int64), c.informational[idx].to(torch.int64),
+            ia_d, ib_d]).cpu().numpy()
+        ea, eb = fcols[0], fcols[1]
+        la, lb = icols[0], icols[1]
+        h = {"ratio": fcols[2], "wasted": fcols[3], "verdict": icols[2], "side": icols[3],
+             "informational": icols[4]}
+        ia, ib = icols[5], icols[6]
         name = lambda ids, i, p: (ids[i] if ids is not None else f"{p}{i}")  # noqa: E731
         cats = ["unknown"] * len(ia)
         waste = np.nonzero(h["verdict"] == VERDICTS.index(VERDICT_WASTE))[0]
