@@ -1341,6 +1341,7 @@ __global__ void tile_range_kernel(AttrParams p, int64_t t0, int64_t t1, unsigned
 
 // ------------------------------------------------------- K5 sums / finalize
 constexpr int SUM_THREADS = 512;
+constexpr int SUM_BLOCKS = 1024;  // partial slots in the workspace
 // Exact fixed-point sum (2^-64 J) with the last-block-done pattern.
 __global__ void __launch_bounds__(SUM_THREADS) fx_sum_kernel(const double *x, int64_t n,
                                                              unsigned long long *partials,
@@ -1404,6 +1405,17 @@ __global__ void __launch_bounds__(SUM_THREADS) fx_sum_kernel(const double *x, in
         }
         *done = 0;  // reusable
     }
+}
+
+// One resident wave: every block of the sum is on an SM at once (no tail
+// wave), capped at SUM_BLOCKS partials.
+static unsigned sum_grid(int64_t n) {
+    static int per_sm = 0;
+    if (!per_sm && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fx_sum_kernel, SUM_THREADS, 0) !=
+                       cudaSuccess)
+        per_sm = 1;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(SUM_BLOCKS, (int64_t)num_sms() * per_sm),
+                                                            ceil_div(n, SUM_THREADS)));
 }
 
 // total over the whole span + idle (energy.py:318-324)
@@ -1480,7 +1492,6 @@ struct AttrLayout {
     size_t cub_tmp, cub_bytes, total;
 };
 
-constexpr int SUM_BLOCKS = 1024;
 
 static size_t cub_sort_bytes(int64_t n) {
     size_t bytes = 0;
@@ -1677,7 +1688,7 @@ static int attribute_impl(const dw_signal_t *sig, dw_interval_set_t *sets, int n
         double *op_total = nullptr;
         if (ops_for_total && ops_for_total->n > 0) {
             op_total = (double *)(base + L.sum_out);
-            unsigned blocks = (unsigned)std::min<int64_t>(SUM_BLOCKS, ceil_div(ops_for_total->n, SUM_THREADS));
+            unsigned blocks = sum_grid(ops_for_total->n);
             cudaMemsetAsync(base + L.sum_done, 0, 16, stream);
             fx_sum_kernel<<<blocks, SUM_THREADS, 0, stream>>>(
                 ops_for_total->d_joules, ops_for_total->n, (unsigned long long *)(base + L.sum_partials),
@@ -1758,7 +1769,7 @@ int dw_fx_sum_exact(const double *d_x, int64_t n, int64_t *d_out_fx, void *d_wor
         return DW_OK;
     }
     char *base = (char *)d_workspace;
-    unsigned blocks = (unsigned)std::min<int64_t>(SUM_BLOCKS, ceil_div(n, SUM_THREADS));
+    unsigned blocks = sum_grid(n);
     unsigned int *done = (unsigned int *)(base + 16 * (size_t)SUM_BLOCKS);
     cudaMemsetAsync(done, 0, 16, s);
     fx_sum_kernel<<<blocks, SUM_THREADS, 0, s>>>(d_x, n, (unsigned long long *)base, done, nullptr,
@@ -1814,7 +1825,7 @@ int dw_fx_sum(const double *d_x, int64_t n, double *d_out, void *d_workspace, si
         DW_CHECK_LAUNCH();
         return DW_OK;
     }
-    unsigned blocks = (unsigned)std::min<int64_t>(SUM_BLOCKS, ceil_div(n, SUM_THREADS));
+    unsigned blocks = sum_grid(n);
     unsigned int *done = (unsigned int *)(base + 16 * (size_t)SUM_BLOCKS);
     cudaMemsetAsync(done, 0, 16, s);
     fx_sum_kernel<<<blocks, SUM_THREADS, 0, s>>>(d_x, n, (unsigned long long *)base, done, d_out);
