@@ -691,7 +691,13 @@ static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, const 
     if (summary) {
         cudaMemsetAsync(base + L.done, 0, 16, s);
         if (P > 0) {
-            waste_sum_kernel<<<(unsigned)std::min<int64_t>(1024, blocks_for(P)), 256, 0, s>>>(
+            static int per_sm = 0;  // one resident wave (no tail), at most 1024 partials
+            if (!per_sm && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, waste_sum_kernel, 256, 0) !=
+                               cudaSuccess)
+                per_sm = 1;
+            const int64_t wgrid = std::min<int64_t>(std::min<int64_t>(1024, (int64_t)num_sms() * per_sm),
+                                                    blocks_for(P));
+            waste_sum_kernel<<<(unsigned)wgrid, 256, 0, s>>>(
                 khi, P, (unsigned long long *)(base + L.partials), (unsigned int *)(base + L.done),
                 summary);
             count_launch();
