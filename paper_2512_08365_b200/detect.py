@@ -80,6 +80,7 @@ class FindingColumns:
     ALL = ("energy_a", "energy_b", "ratio", "wasted", "latency_a", "latency_b", "verdict", "side",
            "informational")
     LEAN = ("ratio", "wasted", "verdict", "side", "informational")
+    KEYS = ("key_hi",)  # the ranking key only: every other column is derived for the top-k rows
 
     def __init__(self, P: int, dev, full: bool = True, columns=None, key_lo: bool = True,
                  tie_rank=None, n_a: int = 0):
@@ -113,6 +114,25 @@ class FindingColumns:
                 t = t[idx]
             out[n] = t.cpu().numpy()
         return out
+
+
+def judge(ea: float, eb: float, la: int, lb: int, out_diff: float, threshold: float) -> tuple:
+    """One pair's (ratio, wasted, verdict, side, informational), detect.py:93-126
+    -- the host twin of csrc/diff.cu judge() (same IEEE operations)."""
+    high, low = (ea, eb) if ea >= eb else (eb, ea)
+    if high == low:
+        ratio, side = 1.0, "-"
+    else:
+        ratio = high / low if low > 0 else float("inf")
+        side = "A" if ea > eb else "B"
+    if ratio >= 1.0 + threshold:
+        eff, ineff = (lb, la) if side == "A" else (la, lb)
+        verdict = VERDICT_WASTE if (float(eff) <= LATENCY_SLACK * float(ineff) and
+                                    out_diff <= OUTPUT_DIFF_LIMIT) else VERDICT_TRADEOFF
+    else:
+        verdict = VERDICT_BELOW
+    info = verdict == VERDICT_BELOW and ratio >= 1.0 + THRESHOLD_FLOOR
+    return ratio, high - low, verdict, side, info
 
 
 def _check_args(ledger_a, ledger_b, threshold):

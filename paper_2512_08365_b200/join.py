@@ -33,7 +33,7 @@ import torch
 from . import _native
 from .columns import TraceColumns
 from .detect import (DEFAULT_THRESHOLD, SIDES, VERDICT_WASTE, VERDICTS, FindingColumns,
-                     Report, SubgraphPair, WasteFinding, rank_order)
+                     Report, SubgraphPair, WasteFinding, judge, rank_order)
 from .energy import EnergyLedger
 
 
@@ -106,6 +106,7 @@ class JoinDiff:
     wasted_joules: float         # exact sum over all waste findings
     ja: Optional[torch.Tensor] = None    # operator joules of A / B (for lean columns)
     jb: Optional[torch.Tensor] = None
+    threshold: float = DEFAULT_THRESHOLD
 
     def pair_of(self, f: torch.Tensor):
         """(A op, B op) of findings f (device tensors; -1 on an empty side)."""
@@ -138,22 +139,34 @@ class JoinDiff:
         zero_f = torch.zeros((), dtype=torch.float64, device=idx.device)
         zero_i = torch.zeros((), dtype=torch.int64, device=idx.device)
         # every column of the k rows in two device tensors: two D2H copies
-        fcols = torch.stack([
-            pick("energy_a", lambda: torch.where(has_a, self.ja[ia_c], zero_f)),
-            pick("energy_b", lambda: torch.where(has_b, self.jb[ib_c], zero_f)),
-            c.ratio[idx], c.wasted[idx]]).cpu().numpy()
-        icols = torch.stack([
-            pick("latency_a", lambda: torch.where(
-                has_a, cols_a.device("op_end")[ia_c] - cols_a.device("op_start")[ia_c], zero_i)),
-            pick("latency_b", lambda: torch.where(
-                has_b, cols_b.device("op_end")[ib_c] - cols_b.device("op_start")[ib_c], zero_i)),
-            c.verdict[idx].to(torch.int64), c.side[idx].to(torch.int64), c.informational[idx].to(torch.int64),
-            ia_d, ib_d]).cpu().numpy()
+        keys_only = c.ratio is None
+        fl = [pick("energy_a", lambda: torch.where(has_a, self.ja[ia_c], zero_f)),
+              pick("energy_b", lambda: torch.where(has_b, self.jb[ib_c], zero_f))]
+        if not keys_only:
+            fl += [c.ratio[idx], c.wasted[idx]]
+        fcols = torch.stack(fl).cpu().numpy()
+        il = [pick("latency_a", lambda: torch.where(
+                  has_a, cols_a.device("op_end")[ia_c] - cols_a.device("op_start")[ia_c], zero_i)),
+              pick("latency_b", lambda: torch.where(
+                  has_b, cols_b.device("op_end")[ib_c] - cols_b.device("op_start")[ib_c], zero_i)),
+              ia_d, ib_d]
+        if not keys_only:
+            il += [c.verdict[idx].to(torch.int64), c.side[idx].to(torch.int64),
+                   c.informational[idx].to(torch.int64)]
+        icols = torch.stack(il).cpu().numpy()
         ea, eb = fcols[0], fcols[1]
         la, lb = icols[0], icols[1]
-        h = {"ratio": fcols[2], "wasted": fcols[3], "verdict": icols[2], "side": icols[3],
-             "informational": icols[4]}
-        ia, ib = icols[5], icols[6]
+        ia, ib = icols[2], icols[3]
+        if keys_only:  # the k rows' verdicts on the host, as the device computed them for all
+            rows = [judge(float(ea[r]), float(eb[r]), int(la[r]), int(lb[r]), 0.0, self.threshold)
+                    for r in range(len(ia))]
+            h = {"ratio": np.array([x[0] for x in rows]), "wasted": np.array([x[1] for x in rows]),
+                 "verdict": np.array([VERDICTS.index(x[2]) for x in rows], dtype=np.int64),
+                 "side": np.array([SIDES.index(x[3]) for x in rows], dtype=np.int64),
+                 "informational": np.array([x[4] for x in rows], dtype=bool)}
+        else:
+            h = {"ratio": fcols[2], "wasted": fcols[3], "verdict": icols[4], "side": icols[5],
+                 "informational": icols[6]}
         name = lambda ids, i, p: (ids[i] if ids is not None else f"{p}{i}")  # noqa: E731
         cats = ["unknown"] * len(ia)
         waste = np.nonzero(h["verdict"] == VERDICTS.index(VERDICT_WASTE))[0]
@@ -233,7 +246,8 @@ def join_prepare(trace_a, trace_b, *, max_distinct: int = DEFAULT_MAX_DISTINCT, 
 def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
               threshold: float = DEFAULT_THRESHOLD, k: int = 100, *, full_columns: bool = True,
               epw: bool = True, work_a=None, work_b=None, stream=None,
-              max_distinct: int = DEFAULT_MAX_DISTINCT, prep: Optional[JoinPrep] = None) -> JoinDiff:
+              max_distinct: int = DEFAULT_MAX_DISTINCT, prep: Optional[JoinPrep] = None,
+              columns: Optional[Sequence[str]] = None) -> JoinDiff:
     """Signature-join diff of two traces with their ledgers; top-k ranked.
     ``prep``: the pairing already made by ``join_prepare`` (same traces)."""
     if ledger_a.method != ledger_b.method:
@@ -263,7 +277,7 @@ def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
     na, nb = ca.n_ops, cb.n_ops
     Pmax = na + nb
     rank_a = keep[2]
-    fc = FindingColumns(Pmax, dev, full=full_columns, key_lo=False, tie_rank=rank_a, n_a=na)
+    fc = FindingColumns(Pmax, dev, full=full_columns, columns=columns, key_lo=False, tie_rank=rank_a, n_a=na)
     epw_a = torch.empty(Pmax, dtype=torch.float64, device=dev) if epw else None
     epw_b = torch.empty(Pmax, dtype=torch.float64, device=dev) if epw else None
     count = torch.zeros(4, dtype=torch.int64, device=dev)
@@ -281,7 +295,7 @@ def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
     return JoinDiff(P=P, n_a=na, n_matched=matched, n_a_only=a_only, n_b_only=b_only, columns=fc,
                     match_a=prep.match_a[:na], b_only=prep.b_only[:b_only],
                     epw_a=epw_a, epw_b=epw_b, order=order, n_waste=int(sm[0]),
-                    wasted_joules=float(sm[1]), ja=keep[0], jb=keep[6])
+                    wasted_joules=float(sm[1]), ja=keep[0], jb=keep[6], threshold=float(threshold))
 
 
 def join_report(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,

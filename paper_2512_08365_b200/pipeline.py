@@ -14,7 +14,7 @@ import torch
 
 from . import _native
 from .columns import TraceColumns
-from .detect import DEFAULT_THRESHOLD, Report
+from .detect import DEFAULT_THRESHOLD, FindingColumns, Report
 from .energy import EnergyLedger, build_ledger
 from .join import JoinDiff, join_diff, join_prepare
 
@@ -56,7 +56,8 @@ def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAUL
         torch.cuda.current_stream().wait_event(sig_ready)
         prep = join_prepare(ca, cb)
     lb = build_ledger(cb, method=method)
-    jd = join_diff(ca, cb, la, lb, threshold, k, full_columns=not lean, epw=not lean, prep=prep)
+    jd = join_diff(ca, cb, la, lb, threshold, k, full_columns=not lean, epw=not lean, prep=prep,
+                   columns=FindingColumns.KEYS if lean else None)
     top = jd.top_findings(ca, cb)
     ineff = max(la.total_joules, lb.total_joules)
     pct = jd.wasted_joules / ineff if ineff > 0 else 0.0

@@ -156,3 +156,18 @@ def test_config1_detect_and_report_golden():
     pos = {id(f): i for i, f in enumerate(fs)}
     np.testing.assert_array_equal([pos[id(f)] for f in doc.findings], sc["det10_rank"])
     assert doc.wasted_joules == sc["det10_report"][2]
+
+
+@pytest.mark.parametrize("theta", [0.10, 0.05])
+def test_keys_only_join_gives_the_same_top_findings(theta):
+    """analyze()'s lean join writes only the ranking key; the top-k rows'
+    ratio / verdict / side / informational / wasted are then derived on the
+    host (detect.judge) and must equal the device columns."""
+    from paper_2512_08365_b200.detect import FindingColumns
+    ca, cb = synth.make_pair(synth.scaled(synth.CONFIGS["C4"], 80_000))
+    la, lb = build_ledger(ca, method="samples"), build_ledger(cb, method="samples")
+    full = join_diff(ca, cb, la, lb, theta, k=300)
+    keys = join_diff(ca, cb, la, lb, theta, k=300, full_columns=False, epw=False, columns=FindingColumns.KEYS)
+    assert keys.columns.ratio is None and keys.columns.verdict is None
+    assert (keys.P, keys.n_waste, keys.wasted_joules) == (full.P, full.n_waste, full.wasted_joules)
+    assert keys.top_findings(ca, cb) == full.top_findings(ca, cb)
