@@ -4,6 +4,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2512_08365_b200 import synth, build_ledger, _native
 from paper_2512_08365_b200.join import join_diff
+from paper_2512_08365_b200.detect import FindingColumns
 name = sys.argv[1] if len(sys.argv) > 1 else "C4"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 a, b = synth.make_pair(name)
@@ -12,7 +13,8 @@ torch.cuda.synchronize()
 for it in range(iters):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter(); e0.record()
-    jd = join_diff(a, b, la, lb, 0.10, 100, full_columns=False, epw=False)
+    cols = FindingColumns.KEYS if "keys" in sys.argv else None
+    jd = join_diff(a, b, la, lb, 0.10, 100, full_columns=False, epw=False, columns=cols)
     top = jd.top_findings(a, b)
     e1.record(); torch.cuda.synchronize(); t1 = time.perf_counter()
     if it == iters - 1 and hasattr(_native.lib(), "dw_trace_report"):
