@@ -339,14 +339,18 @@ def run_ours(args, rank: int, world: int, local: int):
             hc = PackedColumns(pc.ts_base, pin(pc.ts), pin(pc.watts), pc.op_start_base, pin(pc.op_start),
                                pin(pc.op_end), pc.k_start_base, pin(pc.k_start), pin(pc.k_end), c.trace_end,
                                op_sig=pin(pc.op_sig), watts_p0=pc.watts_p0, ts_bias=pc.ts_bias,
-                               op_sig_dict=pin(pc.op_sig_dict) if pc.op_sig_dict is not None else None)
+                               op_sig_dict=pin(pc.op_sig_dict) if pc.op_sig_dict is not None else None,
+                               ts_bits=pc.ts_bits, n_power=pc.n_power,
+                               ts_last=pc._ts_last if pc.ts_bits is not None else None)
             hc._dev["first_last"] = c._first_last_ts()
             pinned.append(hc)
         del packed, pc
         h2d = sum(pc.host_bytes for pc in pinned)
         pc0 = pinned[0]
         tsw = pc0.ts.element_size()
-        host_format = (f"packed columns: ts deltas {'biased i8' if tsw == 1 else f'u{8 * tsw}'}, interval "
+        tsf = (f"{pc0.ts_bits}-bit packed" if pc0.ts_bits is not None else
+               ("biased i8" if tsw == 1 else f"u{8 * tsw}"))
+        host_format = (f"packed columns: ts deltas {tsf}, interval "
                        f"deltas/durations u{8 * pc0.op_start.element_size()}/u{8 * pc0.op_end.element_size()} (ops) "
                        f"u{8 * pc0.k_start.element_size()}/u{8 * pc0.k_end.element_size()} (kernels), watts "
                        + ("9-digit decimal codes u32" if pc0.watts_p0 is not None else "f64")

@@ -192,6 +192,13 @@ int dw_unpack_deltas(const uint32_t *d_delta, int64_t n, int64_t base, int64_t *
 int dw_unpack_deltas_w(const void *d_delta, int32_t delta_bytes, int64_t delta_bias, int64_t n, int64_t base,
                        int64_t *d_out, const void *d_dur, int32_t dur_bytes, int64_t *d_end, void *d_workspace,
                        size_t workspace_bytes, dw_stream_t stream);
+/* Sorted timestamps from bit-packed deltas: field i (width bits, 1..32, at
+ * bit i*width of the little-endian 32-bit words; one padding word after the
+ * last) holds delta_i - bias; d_out[0] = base, d_out[i] = d_out[i-1] + bias +
+ * field i.  A regular sampling clock with a few us of jitter packs its
+ * timestamps into 1-4 bits each. */
+int dw_unpack_bits(const uint32_t *d_words, int32_t width, int64_t bias, int64_t n, int64_t base, int64_t *d_out,
+                   void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
 /* Dictionary-coded 64-bit column (operator signatures): d_out[i] =
  * d_dict[code[i]], codes of code_bytes = 2 or 4. */
 int dw_unpack_dict(const uint64_t *d_dict, const void *d_code, int32_t code_bytes, int64_t n, uint64_t *d_out,

@@ -245,14 +245,23 @@ class PackedColumns(TraceColumns):
     PACKED = ("ts", "op_start", "k_start")
 
     def __init__(self, ts_base, ts_delta, watts, op_base, op_delta, op_dur, k_base, k_delta, k_dur,
-                 trace_end, k_op=None, op_sig=None, watts_p0=None, ts_bias=0, op_sig_dict=None, **kw):
+                 trace_end, k_op=None, op_sig=None, watts_p0=None, ts_bias=0, op_sig_dict=None,
+                 ts_bits=None, n_power=None, ts_last=None, **kw):
         super().__init__(ts=ts_delta, watts=watts, trace_end=int(trace_end), op_start=op_delta, op_end=op_dur,
                          k_start=k_delta, k_end=k_dur, k_op=k_op, op_sig=op_sig, ops_sorted=True,
                          kernels_sorted=True, **kw)
         self.ts_base, self.op_start_base, self.k_start_base = int(ts_base), int(op_base), int(k_base)
         self.watts_p0 = None if watts_p0 is None else int(watts_p0)
-        self.ts_bias = int(ts_bias)          # int8 ts deltas: delta = ts_bias + code
+        self.ts_bias = int(ts_bias)          # int8 / bit-packed ts deltas: delta = ts_bias + code
         self.op_sig_dict = op_sig_dict       # op_sig holds u16/u32 codes into this u64 dictionary
+        self.ts_bits = None if ts_bits is None else int(ts_bits)  # ts holds bit-packed 32-bit words
+        if self.ts_bits is not None:
+            self._n_power, self._ts_last = int(n_power), int(ts_last)
+            self._dev["first_last"] = (self.ts_base, self._ts_last)
+
+    @property
+    def n_power(self) -> int:
+        return self._n_power if self.ts_bits is not None else super().n_power
         self._first_last = None
 
     def _first_last_ts(self) -> tuple[int, int]:
@@ -326,6 +335,14 @@ class PackedColumns(TraceColumns):
         L = _native.lib()
         ws = _native.Workspace.get(L.dw_unpack_workspace_size(n))
         bias = self.ts_bias if base_name == "ts" else 0
+        if base_name == "ts" and self.ts_bits is not None:
+            n = self._n_power
+            out = torch.empty(n, dtype=torch.int64, device=dev)
+            ws = _native.Workspace.get(L.dw_unpack_workspace_size(n))
+            _native.check(L.dw_unpack_bits(_native.ptr(delta), self.ts_bits, bias, n, base, _native.ptr(out),
+                                           ws.data_ptr(), ws.numel(), _native.stream_handle()), "dw_unpack_bits")
+            self._dev[("ts", dev.index)] = out
+            return out
         _native.check(L.dw_unpack_deltas_w(_native.ptr(delta), delta.element_size(), bias, n, base, _native.ptr(out),
                                            _native.ptr(dur) if end is not None else None,
                                            dur.element_size() if end is not None else 4, _native.ptr(end),
@@ -432,6 +449,46 @@ def _ts_deltas(x, what: str):
     return base, bias, code.astype(np.int8)
 
 
+def _bitpack(x, max_width: int = 8):
+    """(base, bias, width, words) of a sorted timestamp column whose deltas
+    after the first span at most 2^max_width - 1 (a regular sampling clock),
+    else None: field i = delta_i - bias in width bits at bit i*width of
+    little-endian 32-bit words, one padding word after (dw_unpack_bits)."""
+    is_t = isinstance(x, torch.Tensor)
+    n = int(x.shape[0])
+    if n < 2:
+        return None
+    d = (x[1:] - x[:-1]) if is_t else np.diff(np.asarray(x, dtype=np.int64))
+    lo, hi = (int(d.min().item()), int(d.max().item())) if is_t else (int(d.min()), int(d.max()))
+    if lo < 0:
+        return None
+    width = max(1, (hi - lo).bit_length())
+    if width > max_width:
+        return None
+    nwords = (n * width + 31) // 32 + 1
+    if is_t:
+        f = torch.zeros(n, dtype=torch.int64, device=x.device)
+        f[1:] = d - lo
+        bit = torch.arange(n, dtype=torch.int64, device=x.device) * width
+        k, sh = bit >> 5, bit & 31
+        words = torch.zeros(nwords, dtype=torch.int64, device=x.device)
+        words.index_add_(0, k, (f << sh) & 0xFFFFFFFF)  # disjoint bit fields: add == or
+        words.index_add_(0, k + 1, f >> (32 - sh))
+        words = torch.where(words >= 0x80000000, words - 0x100000000, words).to(torch.int32)
+        base = int(x[0].item())
+    else:
+        f = np.zeros(n, dtype=np.int64)
+        f[1:] = d - lo
+        bit = np.arange(n, dtype=np.int64) * width
+        k, sh = bit >> 5, bit & 31
+        words = np.zeros(nwords, dtype=np.int64)
+        np.add.at(words, k, (f << sh) & 0xFFFFFFFF)
+        np.add.at(words, k + 1, f >> (32 - sh))
+        words = words.astype(np.uint32)
+        base = int(np.asarray(x)[0])
+    return base, lo, width, words
+
+
 def _sig_dict(sig):
     """(dictionary u64, codes u16/u32) of the signature column when it has at
     most 2^32 distinct values (it has ~1e6 at C4), else None."""
@@ -512,7 +569,13 @@ def pack(cols: TraceColumns, decimal: bool = True) -> PackedColumns:
     """Packed form of a trace with sorted power, operator and kernel starts
     (ValueError otherwise -- keep such traces unpacked).  Works on host or
     device columns; the result lives where the input does."""
-    tb, tbias, td = _ts_deltas(cols.ts, "power timestamps")
+    bits = _bitpack(cols.ts)
+    if bits is not None:
+        tb, tbias, twidth, td = bits
+        tlast = int(cols.ts[-1].item()) if isinstance(cols.ts, torch.Tensor) else int(np.asarray(cols.ts)[-1])
+    else:
+        tb, tbias, td = _ts_deltas(cols.ts, "power timestamps")
+        twidth, tlast = None, None
     ob, od = _deltas(cols.op_start, "operator starts")
     kb, kd = _deltas(cols.k_start, "kernel starts")
     dec = decimal_code(cols.watts) if decimal else None
@@ -522,6 +585,7 @@ def pack(cols: TraceColumns, decimal: bool = True) -> PackedColumns:
     return PackedColumns(tb, td, watts, ob, od, _durations(cols.op_start, cols.op_end, "operators"),
                          kb, kd, _durations(cols.k_start, cols.k_end, "kernels"), cols.trace_end,
                          k_op=cols.k_op, op_sig=sig, watts_p0=p0, ts_bias=tbias, op_sig_dict=sig_dict,
+                         ts_bits=twidth, n_power=cols.n_power, ts_last=tlast,
                          op_ids=cols.op_ids, k_ids=cols.k_ids, op_names=cols.op_names, op_work=cols.op_work,
                          op_rank=cols.op_rank)
 
@@ -539,13 +603,15 @@ def save_packed(cols: TraceColumns, path) -> None:
             continue
         a = a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
         coded = n in ("op_start", "op_end", "k_start", "k_end") or (n == "ts" and a.itemsize > 1) or \
+            (n == "ts" and pc.ts_bits is not None) or \
             (n == "watts" and pc.watts_p0 is not None) or (n == "op_sig" and pc.op_sig_dict is not None)
         if coded:
             a = a.view(np.uint16 if a.itemsize == 2 else np.uint32)
         arrays[n] = np.ascontiguousarray(a)
     meta = {"format": "dwc", "version": 2, "trace_end": pc.trace_end, "ts_base": pc.ts_base,
             "op_base": pc.op_start_base, "k_base": pc.k_start_base, "watts_p0": pc.watts_p0,
-            "ts_bias": pc.ts_bias, "columns": {}}
+            "ts_bias": pc.ts_bias, "ts_bits": pc.ts_bits, "n_power": pc.n_power,
+            "ts_last": pc._ts_last if pc.ts_bits is not None else None, "columns": {}}
     off = 0
     for n, a in arrays.items():
         meta["columns"][n] = {"dtype": a.dtype.str, "n": int(a.shape[0]), "offset": off}
@@ -590,4 +656,5 @@ def load_packed(path, pin: bool = False) -> PackedColumns:
                          meta["k_base"], as_signed(cols["k_start"]), as_signed(cols["k_end"]), meta["trace_end"],
                          k_op=cols.get("k_op"), op_sig=as_signed(sig) if sig_dict is not None else sig,
                          op_work=cols.get("op_work"), watts_p0=p0, ts_bias=meta.get("ts_bias", 0),
-                         op_sig_dict=sig_dict)
+                         op_sig_dict=sig_dict, ts_bits=meta.get("ts_bits"), n_power=meta.get("n_power"),
+                         ts_last=meta.get("ts_last"))

@@ -22,6 +22,23 @@ struct DeltaAt {  // value i of the scan input: base at 0, bias + d[i] after
     __host__ __device__ int64_t operator()(int64_t i) const { return i == 0 ? base : bias + (int64_t)d[i]; }
 };
 
+// value i of a bit-packed delta column: base at 0, bias + the width-bit field
+// i after (fields little-endian in 32-bit words; the words array carries one
+// padding word so the 64-bit window never reads past it)
+struct BitsAt {
+    const uint32_t *w;
+    int width;
+    int64_t base, bias;
+    __host__ __device__ int64_t operator()(int64_t i) const {
+        if (i == 0) return base;
+        const int64_t bit = i * (int64_t)width;
+        const int64_t k = bit >> 5;
+        const uint64_t win = (uint64_t)w[k] | ((uint64_t)w[k + 1] << 32);
+        const uint64_t mask = width == 64 ? ~0ULL : ((1ULL << width) - 1ULL);
+        return bias + (int64_t)((win >> (bit & 31)) & mask);
+    }
+};
+
 template <typename T>
 __global__ void add_duration_kernel(const int64_t *start, const T *dur, int64_t n, int64_t *end) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -36,8 +53,16 @@ static size_t scan_bytes_t(int64_t n) {
     cub::DeviceScan::InclusiveSum(nullptr, b, it, (int64_t *)nullptr, (int)std::max<int64_t>(n, 1));
     return b;
 }
+static size_t scan_bytes_bits(int64_t n) {
+    size_t b = 0;
+    auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), BitsAt{nullptr, 1, 0, 0});
+    cub::DeviceScan::InclusiveSum(nullptr, b, it, (int64_t *)nullptr, (int)std::max<int64_t>(n, 1));
+    return b;
+}
+
 static size_t scan_bytes(int64_t n) {
-    return std::max(std::max(scan_bytes_t<uint32_t>(n), scan_bytes_t<uint16_t>(n)), scan_bytes_t<int8_t>(n));
+    return std::max(std::max(std::max(scan_bytes_t<uint32_t>(n), scan_bytes_t<uint16_t>(n)), scan_bytes_t<int8_t>(n)),
+                    scan_bytes_bits(n));
 }
 
 template <typename T>
@@ -120,6 +145,20 @@ int dw_unpack_deltas_w(const void *d_delta, int32_t delta_bytes, int64_t delta_b
         if (dur_bytes == 2) add_durations<uint16_t>(d_out, d_dur, n, d_end, s);
         else add_durations<uint32_t>(d_out, d_dur, n, d_end, s);
     }
+    DW_CHECK_LAUNCH();
+    return DW_OK;
+}
+
+int dw_unpack_bits(const uint32_t *d_words, int32_t width, int64_t bias, int64_t n, int64_t base, int64_t *d_out,
+                   void *d_workspace, size_t workspace_bytes, dw_stream_t stream) {
+    if (n < 0 || width < 1 || width > 32 || (n && (!d_words || !d_out)) || n >= ((int64_t)1 << 31)) return DW_E_ARG;
+    if (n == 0) return DW_OK;
+    if (!d_workspace || workspace_bytes < dw_unpack_workspace_size(n)) return DW_E_WORKSPACE;
+    auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
+                                              BitsAt{d_words, width, base, bias});
+    size_t b = workspace_bytes;
+    cub::DeviceScan::InclusiveSum(d_workspace, b, it, d_out, (int)n, (cudaStream_t)stream);
+    count_launch(2);
     DW_CHECK_LAUNCH();
     return DW_OK;
 }

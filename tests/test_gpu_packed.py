@@ -18,7 +18,7 @@ def test_decode_exact_and_ledger_identical(tmp_path):
     a, b = synth.make_pair(cfg)
     p = pack(a)
     assert p.watts_p0 is not None  # synthetic watts are at the format's 9-digit precision
-    assert p.ts.element_size() == 1 and p.k_end.element_size() == 2  # regular clock: int8 ts deltas
+    assert p.ts_bits == 1 and p.k_end.element_size() == 2  # regular clock: 1-bit ts deltas
     assert p.op_sig_dict is not None
     for n in ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "op_sig"):
         assert torch.equal(p.device(n), a.device(n)), n
@@ -41,7 +41,8 @@ def test_decode_exact_and_ledger_identical(tmp_path):
     from paper_2512_08365_b200.columns import PackedColumns
     bare = [PackedColumns(q.ts_base, q.ts, q.watts, q.op_start_base, q.op_start, q.op_end, q.k_start_base,
                           q.k_start, q.k_end, q.trace_end, op_sig=q.op_sig, watts_p0=q.watts_p0, ts_bias=q.ts_bias,
-                          op_sig_dict=q.op_sig_dict) for q in (ha, hb)]
+                          op_sig_dict=q.op_sig_dict, ts_bits=q.ts_bits, n_power=q.n_power,
+                          ts_last=q._ts_last) for q in (ha, hb)]
     rb = analyze(bare[0], bare[1], "samples", 0.10, 20)
     assert [f.category for f in rb.report.findings] == [f.category for f in ra.report.findings]
     assert rb.report.wasted_joules == ra.report.wasted_joules
@@ -53,3 +54,18 @@ def test_pack_rejects_unsorted():
     c = TraceColumns.from_arrays(ts, np.ones(3), np.array([1]), np.array([2]))
     with pytest.raises(ValueError):
         pack(c)
+
+
+@pytest.mark.parametrize("jitter", [0, 1, 3, 17, 100])
+def test_bit_packed_timestamps_decode_exactly(jitter):
+    """dw_unpack_bits: widths 1..8, fields crossing 32-bit word boundaries."""
+    from paper_2512_08365_b200.columns import TraceColumns
+    g = torch.Generator().manual_seed(jitter)
+    n = 300_001
+    d = 160 + torch.randint(-jitter, jitter + 1, (n,), generator=g) if jitter else torch.full((n,), 160)
+    ts = (10**12 + torch.cumsum(d, 0)).to(torch.int64)
+    c = TraceColumns.from_arrays(ts.numpy(), np.full(n, 75.0), np.array([int(ts[3])]), np.array([int(ts[9])]))
+    p = pack(c)
+    assert p.ts_bits is not None and p.ts_bits <= 8
+    assert torch.equal(p.device("ts").cpu(), ts)
+    assert p.signal_span() == c.signal_span()

@@ -97,9 +97,19 @@ def test_non_decimal_watts_stay_f64():
     assert decimal_code(np.array([np.nan])) is None
 
 
-def test_regular_clock_ts_pack_to_int8(tmp_path):
-    """A sampling clock with jitter: biased int8 deltas; signatures as a
-    dictionary + 16-bit codes."""
+def _unbits(base, bias, width, words, n):
+    w = np.asarray(words).view(np.uint32).astype(np.uint64)
+    i = np.arange(1, n, dtype=np.int64)
+    bit = i * width
+    k = bit >> 5
+    win = w[k] | (w[k + 1] << np.uint64(32))
+    f = ((win >> (bit & 31).astype(np.uint64)) & np.uint64((1 << width) - 1)).astype(np.int64)
+    return base + np.concatenate([[0], np.cumsum(bias + f)])
+
+
+def test_regular_clock_ts_bit_packed(tmp_path):
+    """A sampling clock with jitter: bit-packed deltas (7 bits here);
+    signatures as a dictionary + 16-bit codes."""
     rng = np.random.default_rng(5)
     ts = (10**9 + np.cumsum(160 + rng.integers(-40, 41, size=5000))).astype(np.int64)
     sig = rng.integers(0, 300, size=50).astype(np.uint64) * np.uint64(0x9E3779B97F4A7C15)
@@ -109,11 +119,8 @@ def test_regular_clock_ts_pack_to_int8(tmp_path):
         if p is None:
             save_packed(c, tmp_path / "r.dwc")
             p = load_packed(tmp_path / "r.dwc")
-        t = np.asarray(p.ts)
-        assert t.dtype == np.int8
-        d = t.astype(np.int64) + p.ts_bias
-        d[0] = 0
-        np.testing.assert_array_equal(p.ts_base + np.cumsum(d), ts)
+        assert p.ts_bits == 7 and p.n_power == ts.size
+        np.testing.assert_array_equal(_unbits(p.ts_base, p.ts_bias, p.ts_bits, p.ts, ts.size), ts)
         assert np.asarray(p.op_sig).itemsize == 2
         np.testing.assert_array_equal(np.asarray(p.op_sig_dict)[_u(p.op_sig)], sig)
         assert p.signal_span() == c.signal_span()
