@@ -341,7 +341,8 @@ def run_ours(args, rank: int, world: int, local: int):
                                op_sig=pin(pc.op_sig), watts_p0=pc.watts_p0, ts_bias=pc.ts_bias,
                                op_sig_dict=pin(pc.op_sig_dict) if pc.op_sig_dict is not None else None,
                                ts_bits=pc.ts_bits, n_power=pc.n_power,
-                               ts_last=pc._ts_last if pc.ts_bits is not None else None)
+                               ts_last=pc._ts_last if pc.ts_bits is not None else None,
+                               iv_bits=pc.iv_bits, n_ops=pc.n_ops, n_kernels=pc.n_kernels)
             hc._dev["first_last"] = c._first_last_ts()
             pinned.append(hc)
         del packed, pc
@@ -350,9 +351,12 @@ def run_ours(args, rank: int, world: int, local: int):
         tsw = pc0.ts.element_size()
         tsf = (f"{pc0.ts_bits}-bit packed" if pc0.ts_bits is not None else
                ("biased i8" if tsw == 1 else f"u{8 * tsw}"))
-        host_format = (f"packed columns: ts deltas {tsf}, interval "
-                       f"deltas/durations u{8 * pc0.op_start.element_size()}/u{8 * pc0.op_end.element_size()} (ops) "
-                       f"u{8 * pc0.k_start.element_size()}/u{8 * pc0.k_end.element_size()} (kernels), watts "
+        def ivf(a, b):
+            if a in pc0.iv_bits:
+                return f"{pc0.iv_bits[a][0]}/{pc0.iv_bits[b][0]}-bit packed"
+            return f"u{8 * getattr(pc0, a).element_size()}/u{8 * getattr(pc0, b).element_size()}"
+        host_format = (f"packed columns: ts deltas {tsf}, interval deltas/durations "
+                       f"{ivf('op_start', 'op_end')} (ops) {ivf('k_start', 'k_end')} (kernels), watts "
                        + ("9-digit decimal codes u32" if pc0.watts_p0 is not None else "f64")
                        + (f", sig dictionary + u{8 * pc0.op_sig.element_size()} codes" if pc0.op_sig_dict is not None
                           else ", sig u64"))

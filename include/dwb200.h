@@ -199,6 +199,10 @@ int dw_unpack_deltas_w(const void *d_delta, int32_t delta_bytes, int64_t delta_b
  * timestamps into 1-4 bits each. */
 int dw_unpack_bits(const uint32_t *d_words, int32_t width, int64_t bias, int64_t n, int64_t base, int64_t *d_out,
                    void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
+/* Interval ends from bit-packed durations: d_end[i] = d_start[i] + bias +
+ * field i (same field layout as dw_unpack_bits; field 0 counts). */
+int dw_unpack_bits_dur(const int64_t *d_start, const uint32_t *d_words, int32_t width, int64_t bias, int64_t n,
+                       int64_t *d_end, dw_stream_t stream);
 /* Dictionary-coded 64-bit column (operator signatures): d_out[i] =
  * d_dict[code[i]], codes of code_bytes = 2 or 4. */
 int dw_unpack_dict(const uint64_t *d_dict, const void *d_code, int32_t code_bytes, int64_t n, uint64_t *d_out,

@@ -246,7 +246,7 @@ class PackedColumns(TraceColumns):
 
     def __init__(self, ts_base, ts_delta, watts, op_base, op_delta, op_dur, k_base, k_delta, k_dur,
                  trace_end, k_op=None, op_sig=None, watts_p0=None, ts_bias=0, op_sig_dict=None,
-                 ts_bits=None, n_power=None, ts_last=None, **kw):
+                 ts_bits=None, n_power=None, ts_last=None, iv_bits=None, n_ops=None, n_kernels=None, **kw):
         super().__init__(ts=ts_delta, watts=watts, trace_end=int(trace_end), op_start=op_delta, op_end=op_dur,
                          k_start=k_delta, k_end=k_dur, k_op=k_op, op_sig=op_sig, ops_sorted=True,
                          kernels_sorted=True, **kw)
@@ -258,10 +258,23 @@ class PackedColumns(TraceColumns):
         if self.ts_bits is not None:
             self._n_power, self._ts_last = int(n_power), int(ts_last)
             self._dev["first_last"] = (self.ts_base, self._ts_last)
+        # bit-packed interval columns: name -> (width, bias); op_start / k_start
+        # hold packed deltas, op_end / k_end packed durations
+        self.iv_bits = dict(iv_bits or {})
+        self._n_ops = None if n_ops is None else int(n_ops)
+        self._n_kernels = None if n_kernels is None else int(n_kernels)
 
     @property
     def n_power(self) -> int:
         return self._n_power if self.ts_bits is not None else super().n_power
+
+    @property
+    def n_ops(self) -> int:
+        return self._n_ops if "op_start" in self.iv_bits else super().n_ops
+
+    @property
+    def n_kernels(self) -> int:
+        return self._n_kernels if "k_start" in self.iv_bits else super().n_kernels
         self._first_last = None
 
     def _first_last_ts(self) -> tuple[int, int]:
@@ -324,16 +337,11 @@ class PackedColumns(TraceColumns):
             return t
         base_name = {"op_end": "op_start", "k_end": "k_start"}.get(name, name)
         delta = self._staged(base_name, dev)
-        n = int(delta.numel())
-        out = torch.empty(n, dtype=torch.int64, device=dev)
-        end = None
         dur_name = {"op_start": "op_end", "k_start": "k_end"}.get(base_name)
-        if dur_name is not None:
-            dur = self._staged(dur_name, dev)
-            end = torch.empty(n, dtype=torch.int64, device=dev)
+        dur = self._staged(dur_name, dev) if dur_name is not None else None
+        end = dur  # placeholder: decoded ends are allocated by the branch that fills them
         base = {"ts": self.ts_base, "op_start": self.op_start_base, "k_start": self.k_start_base}[base_name]
         L = _native.lib()
-        ws = _native.Workspace.get(L.dw_unpack_workspace_size(n))
         bias = self.ts_bias if base_name == "ts" else 0
         if base_name == "ts" and self.ts_bits is not None:
             n = self._n_power
@@ -343,6 +351,25 @@ class PackedColumns(TraceColumns):
                                            ws.data_ptr(), ws.numel(), _native.stream_handle()), "dw_unpack_bits")
             self._dev[("ts", dev.index)] = out
             return out
+        if base_name in self.iv_bits:
+            n = self._n_ops if base_name == "op_start" else self._n_kernels
+            out = torch.empty(n, dtype=torch.int64, device=dev)
+            ws = _native.Workspace.get(L.dw_unpack_workspace_size(n))
+            w, b = self.iv_bits[base_name]
+            _native.check(L.dw_unpack_bits(_native.ptr(delta), w, b, n, base, _native.ptr(out), ws.data_ptr(),
+                                           ws.numel(), _native.stream_handle()), "dw_unpack_bits")
+            self._dev[(base_name, dev.index)] = out
+            if end is not None:
+                end = torch.empty(n, dtype=torch.int64, device=dev)
+                wd, bd = self.iv_bits[dur_name]
+                _native.check(L.dw_unpack_bits_dur(_native.ptr(out), _native.ptr(dur), wd, bd, n, _native.ptr(end),
+                                                   _native.stream_handle()), "dw_unpack_bits_dur")
+                self._dev[(dur_name, dev.index)] = end
+            return self._dev[key]
+        n = int(delta.numel())
+        out = torch.empty(n, dtype=torch.int64, device=dev)
+        end = torch.empty(n, dtype=torch.int64, device=dev) if dur is not None else None
+        ws = _native.Workspace.get(L.dw_unpack_workspace_size(n))
         _native.check(L.dw_unpack_deltas_w(_native.ptr(delta), delta.element_size(), bias, n, base, _native.ptr(out),
                                            _native.ptr(dur) if end is not None else None,
                                            dur.element_size() if end is not None else 4, _native.ptr(end),
@@ -449,44 +476,56 @@ def _ts_deltas(x, what: str):
     return base, bias, code.astype(np.int8)
 
 
-def _bitpack(x, max_width: int = 8):
-    """(base, bias, width, words) of a sorted timestamp column whose deltas
-    after the first span at most 2^max_width - 1 (a regular sampling clock),
-    else None: field i = delta_i - bias in width bits at bit i*width of
-    little-endian 32-bit words, one padding word after (dw_unpack_bits)."""
-    is_t = isinstance(x, torch.Tensor)
-    n = int(x.shape[0])
-    if n < 2:
+def _bitfields(v, max_width: int):
+    """(bias, width, words) packing every element of a non-negative-spread
+    int64 vector as v - min(v) in the fewest bits (<= max_width), little-endian
+    in 32-bit words plus one padding word; None if the spread needs more."""
+    is_t = isinstance(v, torch.Tensor)
+    n = int(v.shape[0])
+    if n == 0:
         return None
-    d = (x[1:] - x[:-1]) if is_t else np.diff(np.asarray(x, dtype=np.int64))
-    lo, hi = (int(d.min().item()), int(d.max().item())) if is_t else (int(d.min()), int(d.max()))
-    if lo < 0:
-        return None
+    lo, hi = (int(v.min().item()), int(v.max().item())) if is_t else (int(v.min()), int(v.max()))
     width = max(1, (hi - lo).bit_length())
     if width > max_width:
         return None
     nwords = (n * width + 31) // 32 + 1
     if is_t:
-        f = torch.zeros(n, dtype=torch.int64, device=x.device)
-        f[1:] = d - lo
-        bit = torch.arange(n, dtype=torch.int64, device=x.device) * width
+        f = v - lo
+        bit = torch.arange(n, dtype=torch.int64, device=v.device) * width
         k, sh = bit >> 5, bit & 31
-        words = torch.zeros(nwords, dtype=torch.int64, device=x.device)
+        words = torch.zeros(nwords, dtype=torch.int64, device=v.device)
         words.index_add_(0, k, (f << sh) & 0xFFFFFFFF)  # disjoint bit fields: add == or
         words.index_add_(0, k + 1, f >> (32 - sh))
         words = torch.where(words >= 0x80000000, words - 0x100000000, words).to(torch.int32)
-        base = int(x[0].item())
     else:
-        f = np.zeros(n, dtype=np.int64)
-        f[1:] = d - lo
+        f = np.asarray(v, dtype=np.int64) - lo
         bit = np.arange(n, dtype=np.int64) * width
         k, sh = bit >> 5, bit & 31
         words = np.zeros(nwords, dtype=np.int64)
         np.add.at(words, k, (f << sh) & 0xFFFFFFFF)
         np.add.at(words, k + 1, f >> (32 - sh))
         words = words.astype(np.uint32)
-        base = int(np.asarray(x)[0])
-    return base, lo, width, words
+    return lo, width, words
+
+
+def _bitpack(x, max_width: int = 8):
+    """(base, bias, width, words) of a sorted column whose deltas after the
+    first spread at most 2^max_width - 1 (e.g. a regular sampling clock), else
+    None: field i = delta_i - bias (field 0 unused), decoded by dw_unpack_bits."""
+    is_t = isinstance(x, torch.Tensor)
+    n = int(x.shape[0])
+    if n < 2:
+        return None
+    d = (x[1:] - x[:-1]) if is_t else np.diff(np.asarray(x, dtype=np.int64))
+    if (bool((d < 0).any()) if is_t else bool((d < 0).any())):
+        return None
+    lo = int(d.min().item()) if is_t else int(d.min())
+    full = torch.cat([d.new_full((1,), lo), d]) if is_t else np.concatenate([[lo], d])
+    packed = _bitfields(full, max_width)
+    if packed is None:
+        return None
+    base = int(x[0].item()) if is_t else int(np.asarray(x)[0])
+    return base, packed[0], packed[1], packed[2]
 
 
 def _sig_dict(sig):
@@ -578,14 +617,31 @@ def pack(cols: TraceColumns, decimal: bool = True) -> PackedColumns:
         twidth, tlast = None, None
     ob, od = _deltas(cols.op_start, "operator starts")
     kb, kd = _deltas(cols.k_start, "kernel starts")
+    o_dur = _durations(cols.op_start, cols.op_end, "operators")
+    k_dur = _durations(cols.k_start, cols.k_end, "kernels")
+    # narrower still: bit-pack interval deltas / durations whose spread needs <= 15 bits
+    iv_bits = {}
+    for sname, ename, start, end in (("op_start", "op_end", cols.op_start, cols.op_end),
+                                     ("k_start", "k_end", cols.k_start, cols.k_end)):
+        sp = _bitpack(start, 15)
+        dp = _bitfields(end - start if isinstance(start, torch.Tensor) else
+                        np.asarray(end, dtype=np.int64) - np.asarray(start, dtype=np.int64), 15) \
+            if sp is not None else None
+        if sp is not None and dp is not None:
+            iv_bits[sname] = (sp[2], sp[1])
+            iv_bits[ename] = (dp[1], dp[0])
+            if sname == "op_start":
+                ob, od, o_dur = sp[0], sp[3], dp[2]
+            else:
+                kb, kd, k_dur = sp[0], sp[3], dp[2]
     dec = decimal_code(cols.watts) if decimal else None
     watts, p0 = (cols.watts, None) if dec is None else (dec[1], dec[0])
     sd = _sig_dict(cols.op_sig)
     sig, sig_dict = (cols.op_sig, None) if sd is None else (sd[1], sd[0])
-    return PackedColumns(tb, td, watts, ob, od, _durations(cols.op_start, cols.op_end, "operators"),
-                         kb, kd, _durations(cols.k_start, cols.k_end, "kernels"), cols.trace_end,
+    return PackedColumns(tb, td, watts, ob, od, o_dur, kb, kd, k_dur, cols.trace_end,
                          k_op=cols.k_op, op_sig=sig, watts_p0=p0, ts_bias=tbias, op_sig_dict=sig_dict,
-                         ts_bits=twidth, n_power=cols.n_power, ts_last=tlast,
+                         ts_bits=twidth, n_power=cols.n_power, ts_last=tlast, iv_bits=iv_bits,
+                         n_ops=cols.n_ops, n_kernels=cols.n_kernels,
                          op_ids=cols.op_ids, k_ids=cols.k_ids, op_names=cols.op_names, op_work=cols.op_work,
                          op_rank=cols.op_rank)
 
@@ -603,6 +659,7 @@ def save_packed(cols: TraceColumns, path) -> None:
             continue
         a = a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
         coded = n in ("op_start", "op_end", "k_start", "k_end") or (n == "ts" and a.itemsize > 1) or \
+            n in pc.iv_bits or \
             (n == "ts" and pc.ts_bits is not None) or \
             (n == "watts" and pc.watts_p0 is not None) or (n == "op_sig" and pc.op_sig_dict is not None)
         if coded:
@@ -611,7 +668,9 @@ def save_packed(cols: TraceColumns, path) -> None:
     meta = {"format": "dwc", "version": 2, "trace_end": pc.trace_end, "ts_base": pc.ts_base,
             "op_base": pc.op_start_base, "k_base": pc.k_start_base, "watts_p0": pc.watts_p0,
             "ts_bias": pc.ts_bias, "ts_bits": pc.ts_bits, "n_power": pc.n_power,
-            "ts_last": pc._ts_last if pc.ts_bits is not None else None, "columns": {}}
+            "ts_last": pc._ts_last if pc.ts_bits is not None else None,
+            "iv_bits": {k: list(v) for k, v in pc.iv_bits.items()}, "n_ops": pc.n_ops, "n_kernels": pc.n_kernels,
+            "columns": {}}
     off = 0
     for n, a in arrays.items():
         meta["columns"][n] = {"dtype": a.dtype.str, "n": int(a.shape[0]), "offset": off}
@@ -657,4 +716,5 @@ def load_packed(path, pin: bool = False) -> PackedColumns:
                          k_op=cols.get("k_op"), op_sig=as_signed(sig) if sig_dict is not None else sig,
                          op_work=cols.get("op_work"), watts_p0=p0, ts_bias=meta.get("ts_bias", 0),
                          op_sig_dict=sig_dict, ts_bits=meta.get("ts_bits"), n_power=meta.get("n_power"),
-                         ts_last=meta.get("ts_last"))
+                         ts_last=meta.get("ts_last"), iv_bits={k: tuple(v) for k, v in meta.get("iv_bits", {}).items()},
+                         n_ops=meta.get("n_ops"), n_kernels=meta.get("n_kernels"))

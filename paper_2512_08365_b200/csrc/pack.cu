@@ -39,6 +39,19 @@ struct BitsAt {
     }
 };
 
+// end[i] = start[i] + bias + field i (bit-packed durations; field 0 counts)
+__global__ void add_bits_duration_kernel(const int64_t *start, const uint32_t *w, int width, int64_t bias, int64_t n,
+                                         int64_t *end) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const uint64_t mask = (1ULL << width) - 1ULL;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int64_t bit = i * (int64_t)width;
+        const int64_t k = bit >> 5;
+        const uint64_t win = (uint64_t)__ldg(w + k) | ((uint64_t)__ldg(w + k + 1) << 32);
+        end[i] = __ldcs(start + i) + bias + (int64_t)((win >> (bit & 31)) & mask);
+    }
+}
+
 template <typename T>
 __global__ void add_duration_kernel(const int64_t *start, const T *dur, int64_t n, int64_t *end) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -159,6 +172,18 @@ int dw_unpack_bits(const uint32_t *d_words, int32_t width, int64_t bias, int64_t
     size_t b = workspace_bytes;
     cub::DeviceScan::InclusiveSum(d_workspace, b, it, d_out, (int)n, (cudaStream_t)stream);
     count_launch(2);
+    DW_CHECK_LAUNCH();
+    return DW_OK;
+}
+
+int dw_unpack_bits_dur(const int64_t *d_start, const uint32_t *d_words, int32_t width, int64_t bias, int64_t n,
+                       int64_t *d_end, dw_stream_t stream) {
+    if (n < 0 || width < 1 || width > 32 || (n && (!d_start || !d_words || !d_end))) return DW_E_ARG;
+    if (n) {
+        add_bits_duration_kernel<<<(unsigned)std::min<int64_t>(num_sms() * 8, ceil_div(n, 256)), 256, 0,
+                                   (cudaStream_t)stream>>>(d_start, d_words, width, bias, n, d_end);
+        count_launch();
+    }
     DW_CHECK_LAUNCH();
     return DW_OK;
 }
