@@ -203,6 +203,10 @@ int dw_unpack_bits(const uint32_t *d_words, int32_t width, int64_t bias, int64_t
  * field i (same field layout as dw_unpack_bits; field 0 counts). */
 int dw_unpack_bits_dur(const int64_t *d_start, const uint32_t *d_words, int32_t width, int64_t bias, int64_t n,
                        int64_t *d_end, dw_stream_t stream);
+/* Dictionary codes bit-packed (width bits each, dw_unpack_bits layout):
+ * d_out[i] = d_dict[field i]. */
+int dw_unpack_dict_bits(const uint64_t *d_dict, const uint32_t *d_words, int32_t width, int64_t n, uint64_t *d_out,
+                        dw_stream_t stream);
 /* Dictionary-coded 64-bit column (operator signatures): d_out[i] =
  * d_dict[code[i]], codes of code_bytes = 2 or 4. */
 int dw_unpack_dict(const uint64_t *d_dict, const void *d_code, int32_t code_bytes, int64_t n, uint64_t *d_out,

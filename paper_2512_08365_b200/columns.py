@@ -246,7 +246,8 @@ class PackedColumns(TraceColumns):
 
     def __init__(self, ts_base, ts_delta, watts, op_base, op_delta, op_dur, k_base, k_delta, k_dur,
                  trace_end, k_op=None, op_sig=None, watts_p0=None, ts_bias=0, op_sig_dict=None,
-                 ts_bits=None, n_power=None, ts_last=None, iv_bits=None, n_ops=None, n_kernels=None, **kw):
+                 ts_bits=None, n_power=None, ts_last=None, iv_bits=None, n_ops=None, n_kernels=None,
+                 sig_bits=None, **kw):
         super().__init__(ts=ts_delta, watts=watts, trace_end=int(trace_end), op_start=op_delta, op_end=op_dur,
                          k_start=k_delta, k_end=k_dur, k_op=k_op, op_sig=op_sig, ops_sorted=True,
                          kernels_sorted=True, **kw)
@@ -261,6 +262,7 @@ class PackedColumns(TraceColumns):
         # bit-packed interval columns: name -> (width, bias); op_start / k_start
         # hold packed deltas, op_end / k_end packed durations
         self.iv_bits = dict(iv_bits or {})
+        self.sig_bits = None if sig_bits is None else int(sig_bits)  # op_sig: bit-packed dictionary codes
         self._n_ops = None if n_ops is None else int(n_ops)
         self._n_kernels = None if n_kernels is None else int(n_kernels)
 
@@ -402,10 +404,16 @@ class PackedColumns(TraceColumns):
             d = self.op_sig_dict
             d = (d if isinstance(d, torch.Tensor) else torch.from_numpy(np.asarray(d).view(np.int64))).to(
                 dev, non_blocking=True)
-            t = torch.empty(code.numel(), dtype=torch.int64, device=dev)
-            _native.check(_native.lib().dw_unpack_dict(_native.ptr(d), _native.ptr(code), code.element_size(),
-                                                       code.numel(), _native.ptr(t), _native.stream_handle()),
-                          "dw_unpack_dict")
+            if self.sig_bits is not None:
+                t = torch.empty(self.n_ops, dtype=torch.int64, device=dev)
+                _native.check(_native.lib().dw_unpack_dict_bits(_native.ptr(d), _native.ptr(code), self.sig_bits,
+                                                                self.n_ops, _native.ptr(t), _native.stream_handle()),
+                              "dw_unpack_dict_bits")
+            else:
+                t = torch.empty(code.numel(), dtype=torch.int64, device=dev)
+                _native.check(_native.lib().dw_unpack_dict(_native.ptr(d), _native.ptr(code), code.element_size(),
+                                                           code.numel(), _native.ptr(t), _native.stream_handle()),
+                              "dw_unpack_dict")
             self._dev[key] = t
         return t
 
@@ -638,10 +646,18 @@ def pack(cols: TraceColumns, decimal: bool = True) -> PackedColumns:
     watts, p0 = (cols.watts, None) if dec is None else (dec[1], dec[0])
     sd = _sig_dict(cols.op_sig)
     sig, sig_dict = (cols.op_sig, None) if sd is None else (sd[1], sd[0])
+    sig_bits = None
+    if sd is not None:
+        codes = sd[1].to(torch.int64) if isinstance(sd[1], torch.Tensor) else np.asarray(sd[1], dtype=np.int64)
+        width = max(1, (int(sd[0].shape[0]) - 1).bit_length())
+        if width < 8 * (sd[1].element_size() if isinstance(sd[1], torch.Tensor) else sd[1].itemsize):
+            packed = _bitfields(codes - 0, 32)  # codes start at 0: bias 0 unless code 0 is absent
+            if packed is not None and packed[0] == 0 and packed[1] <= width:
+                sig, sig_bits = packed[2], packed[1]
     return PackedColumns(tb, td, watts, ob, od, o_dur, kb, kd, k_dur, cols.trace_end,
                          k_op=cols.k_op, op_sig=sig, watts_p0=p0, ts_bias=tbias, op_sig_dict=sig_dict,
                          ts_bits=twidth, n_power=cols.n_power, ts_last=tlast, iv_bits=iv_bits,
-                         n_ops=cols.n_ops, n_kernels=cols.n_kernels,
+                         n_ops=cols.n_ops, n_kernels=cols.n_kernels, sig_bits=sig_bits,
                          op_ids=cols.op_ids, k_ids=cols.k_ids, op_names=cols.op_names, op_work=cols.op_work,
                          op_rank=cols.op_rank)
 
@@ -659,7 +675,7 @@ def save_packed(cols: TraceColumns, path) -> None:
             continue
         a = a.cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
         coded = n in ("op_start", "op_end", "k_start", "k_end") or (n == "ts" and a.itemsize > 1) or \
-            n in pc.iv_bits or \
+            n in pc.iv_bits or (n == "op_sig" and pc.sig_bits is not None) or \
             (n == "ts" and pc.ts_bits is not None) or \
             (n == "watts" and pc.watts_p0 is not None) or (n == "op_sig" and pc.op_sig_dict is not None)
         if coded:
@@ -670,6 +686,7 @@ def save_packed(cols: TraceColumns, path) -> None:
             "ts_bias": pc.ts_bias, "ts_bits": pc.ts_bits, "n_power": pc.n_power,
             "ts_last": pc._ts_last if pc.ts_bits is not None else None,
             "iv_bits": {k: list(v) for k, v in pc.iv_bits.items()}, "n_ops": pc.n_ops, "n_kernels": pc.n_kernels,
+            "sig_bits": pc.sig_bits,
             "columns": {}}
     off = 0
     for n, a in arrays.items():
@@ -717,4 +734,4 @@ def load_packed(path, pin: bool = False) -> PackedColumns:
                          op_work=cols.get("op_work"), watts_p0=p0, ts_bias=meta.get("ts_bias", 0),
                          op_sig_dict=sig_dict, ts_bits=meta.get("ts_bits"), n_power=meta.get("n_power"),
                          ts_last=meta.get("ts_last"), iv_bits={k: tuple(v) for k, v in meta.get("iv_bits", {}).items()},
-                         n_ops=meta.get("n_ops"), n_kernels=meta.get("n_kernels"))
+                         n_ops=meta.get("n_ops"), n_kernels=meta.get("n_kernels"), sig_bits=meta.get("sig_bits"))

@@ -101,6 +101,18 @@ static void add_durations(const int64_t *start, const void *dur, int64_t n, int6
 __constant__ double POW10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
                                  1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
 
+__global__ void dict_bits_decode_kernel(const uint64_t *dict, const uint32_t *w, int width, int64_t n,
+                                        uint64_t *out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const uint64_t mask = (1ULL << width) - 1ULL;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int64_t bit = i * (int64_t)width;
+        const int64_t k = bit >> 5;
+        const uint64_t win = (uint64_t)__ldg(w + k) | ((uint64_t)__ldg(w + k + 1) << 32);
+        __stcs(out + i, __ldg(dict + ((win >> (bit & 31)) & mask)));
+    }
+}
+
 template <typename T>
 __global__ void dict_decode_kernel(const uint64_t *dict, const T *code, int64_t n, uint64_t *out) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -182,6 +194,18 @@ int dw_unpack_bits_dur(const int64_t *d_start, const uint32_t *d_words, int32_t 
     if (n) {
         add_bits_duration_kernel<<<(unsigned)std::min<int64_t>(num_sms() * 8, ceil_div(n, 256)), 256, 0,
                                    (cudaStream_t)stream>>>(d_start, d_words, width, bias, n, d_end);
+        count_launch();
+    }
+    DW_CHECK_LAUNCH();
+    return DW_OK;
+}
+
+int dw_unpack_dict_bits(const uint64_t *d_dict, const uint32_t *d_words, int32_t width, int64_t n, uint64_t *d_out,
+                        dw_stream_t stream) {
+    if (n < 0 || width < 1 || width > 32 || (n && (!d_dict || !d_words || !d_out))) return DW_E_ARG;
+    if (n) {
+        dict_bits_decode_kernel<<<(unsigned)std::min<int64_t>(num_sms() * 8, ceil_div(n, 256)), 256, 0,
+                                  (cudaStream_t)stream>>>(d_dict, d_words, width, n, d_out);
         count_launch();
     }
     DW_CHECK_LAUNCH();

@@ -20,7 +20,7 @@ def test_decode_exact_and_ledger_identical(tmp_path):
     assert p.watts_p0 is not None  # synthetic watts are at the format's 9-digit precision
     assert p.ts_bits == 1  # regular clock: 1-bit ts deltas
     assert set(p.iv_bits) == {"op_start", "op_end", "k_start", "k_end"}  # bit-packed intervals
-    assert p.op_sig_dict is not None
+    assert p.op_sig_dict is not None and p.sig_bits is not None
     for n in ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "op_sig"):
         assert torch.equal(p.device(n), a.device(n)), n
     assert p.signal_span() == a.signal_span()
@@ -43,7 +43,8 @@ def test_decode_exact_and_ledger_identical(tmp_path):
     bare = [PackedColumns(q.ts_base, q.ts, q.watts, q.op_start_base, q.op_start, q.op_end, q.k_start_base,
                           q.k_start, q.k_end, q.trace_end, op_sig=q.op_sig, watts_p0=q.watts_p0, ts_bias=q.ts_bias,
                           op_sig_dict=q.op_sig_dict, ts_bits=q.ts_bits, n_power=q.n_power,
-                          ts_last=q._ts_last, iv_bits=q.iv_bits, n_ops=q.n_ops, n_kernels=q.n_kernels)
+                          ts_last=q._ts_last, iv_bits=q.iv_bits, n_ops=q.n_ops, n_kernels=q.n_kernels,
+                          sig_bits=q.sig_bits)
             for q in (ha, hb)]
     rb = analyze(bare[0], bare[1], "samples", 0.10, 20)
     assert [f.category for f in rb.report.findings] == [f.category for f in ra.report.findings]

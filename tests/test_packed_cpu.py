@@ -42,7 +42,7 @@ def test_roundtrip(tmp_path):
     np.testing.assert_array_equal(dec(p.op_start_base, p.op_start) + _u(p.op_end), c.op_end)
     np.testing.assert_array_equal(dec(p.k_start_base, p.k_start) + _u(p.k_end), c.k_end)
     assert np.asarray(p.ts).itemsize == 2 and np.asarray(p.op_end).itemsize == 4  # narrowest width per column
-    np.testing.assert_array_equal(np.asarray(p.op_sig_dict)[_u(p.op_sig)], c.op_sig)  # dictionary-coded
+    np.testing.assert_array_equal(np.asarray(p.op_sig_dict)[_fields(p.op_sig, p.sig_bits, c.n_ops)], c.op_sig)
     np.testing.assert_array_equal(np.asarray(p.k_op), c.k_op)
     assert p.signal_span() == c.signal_span()
     assert p.n_power == c.n_power and p.n_ops == c.n_ops and p.n_kernels == c.n_kernels
@@ -97,6 +97,14 @@ def test_non_decimal_watts_stay_f64():
     assert decimal_code(np.array([np.nan])) is None
 
 
+def _fields(words, width, n):
+    w = np.asarray(words).view(np.uint32).astype(np.uint64)
+    bit = np.arange(n, dtype=np.int64) * width
+    k = bit >> 5
+    win = w[k] | (w[k + 1] << np.uint64(32))
+    return ((win >> (bit & 31).astype(np.uint64)) & np.uint64((1 << width) - 1)).astype(np.int64)
+
+
 def _unbits(base, bias, width, words, n):
     w = np.asarray(words).view(np.uint32).astype(np.uint64)
     i = np.arange(1, n, dtype=np.int64)
@@ -121,6 +129,6 @@ def test_regular_clock_ts_bit_packed(tmp_path):
             p = load_packed(tmp_path / "r.dwc")
         assert p.ts_bits == 7 and p.n_power == ts.size
         np.testing.assert_array_equal(_unbits(p.ts_base, p.ts_bias, p.ts_bits, p.ts, ts.size), ts)
-        assert np.asarray(p.op_sig).itemsize == 2
-        np.testing.assert_array_equal(np.asarray(p.op_sig_dict)[_u(p.op_sig)], sig)
+        assert p.sig_bits is not None and p.sig_bits <= 9  # < 300 distinct signatures
+        np.testing.assert_array_equal(np.asarray(p.op_sig_dict)[_fields(p.op_sig, p.sig_bits, sig.size)], sig)
         assert p.signal_span() == c.signal_span()
