@@ -298,23 +298,48 @@ class PackedColumns(TraceColumns):
         t = self._dev.pop(("raw", name, dev.index), None)
         return t if t is not None else self._raw(name).to(dev, non_blocking=True)
 
-    def prefetch(self, stream: "torch.cuda.Stream", names=TraceColumns.HOT) -> "torch.cuda.Event":
+    def prefetch(self, stream: "torch.cuda.Stream", names=TraceColumns.HOT,
+                 decode_stream: "torch.cuda.Stream | None" = None) -> "torch.cuda.Event":
         """All host->HBM copies of ``names`` first (event ``copied``), then the
-        decodes, on ``stream``: a copy queued behind this one (another trace)
-        waits for the transfers only, not for the decodes."""
+        decodes: a copy queued behind this one (another trace) waits for the
+        transfers only.  With ``decode_stream`` each column decodes there as
+        soon as its own transfer has landed, under the transfers after it."""
         dev = _native.device()
         raw = {"op_end": "op_start", "k_end": "k_start"}
+        groups = []
         with torch.cuda.stream(stream):
             for n in names:
+                staged = []
                 for m in (n, {"op_start": "op_end", "k_start": "k_end"}.get(n), raw.get(n)):
                     if m is None or getattr(self, m) is None or (m, dev.index) in self._dev \
                             or ("raw", m, dev.index) in self._dev:
                         continue
-                    self._dev[("raw", m, dev.index)] = self._raw(m).to(dev, non_blocking=True)
+                    t = self._raw(m).to(dev, non_blocking=True)
+                    self._dev[("raw", m, dev.index)] = t
+                    staged.append(t)
+                if decode_stream is not None:
+                    ev = None
+                    if staged:
+                        ev = torch.cuda.Event()
+                        ev.record(stream)
+                    groups.append((n, ev, staged))
             copied = torch.cuda.Event()
             copied.record(stream)
         self.copied = copied
-        return super().prefetch(stream, names)
+        if decode_stream is None:
+            return super().prefetch(stream, names)
+        with torch.cuda.stream(decode_stream):
+            for n, ev, staged in groups:
+                if ev is not None:
+                    decode_stream.wait_event(ev)  # this column's transfer only
+                for t in staged:  # allocated on the copy stream, read on the decode stream
+                    t.record_stream(decode_stream)
+                if getattr(self, n) is not None:
+                    self.device(n)
+            ready = torch.cuda.Event()
+            ready.record(decode_stream)
+        self._dev["__ready__"] = ready
+        return ready
 
     def _raw(self, name):
         src = getattr(self, name)

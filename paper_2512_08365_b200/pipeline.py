@@ -27,6 +27,16 @@ class Analysis:
     join: JoinDiff
 
 
+_DECODE_STREAMS: dict = {}
+
+
+def _decode_stream() -> "torch.cuda.Stream":
+    dev = torch.cuda.current_device()
+    if dev not in _DECODE_STREAMS:
+        _DECODE_STREAMS[dev] = torch.cuda.Stream()
+    return _DECODE_STREAMS[dev]
+
+
 def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAULT_THRESHOLD,
             k: int = 100, *, lean: bool = True, copy_stream: "torch.cuda.Stream | None" = None
             ) -> Analysis:
@@ -50,7 +60,10 @@ def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAUL
         # copies would share PCIe and delay A to the end of the transfer
         copy_stream.wait_event(getattr(ca, "copied", None) or a_ready)
         sig_ready = cb.prefetch(copy_stream, names=("op_sig", "op_start", "op_end"))
-        cb.prefetch(copy_stream)
+        # the rest of B decodes column by column on a side stream as it lands
+        # (by then A's attribution and the pairing are done), so only the last
+        # column's decode trails the last byte
+        cb.prefetch(copy_stream, names=("ts", "watts", "k_start", "k_end"), decode_stream=_decode_stream())
     la = build_ledger(ca, method=method)
     if copy_stream is not None:
         torch.cuda.current_stream().wait_event(sig_ready)
