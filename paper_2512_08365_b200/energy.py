@@ -560,13 +560,18 @@ def _replay_device(truth: PowerSignal, starts, ends, repeat, period_us, delay_us
 
 def _replay_checks(cols: TraceColumns, repeat: int, first_op: int = 0) -> None:
     """replay_estimate's argument errors in build_ledger's op order
-    (energy.py:227-230): an op without kernels, then repeat < 1."""
-    k_op = cols.k_op if cols.k_op is not None else np.zeros(0, dtype=np.int32)
-    k_op = k_op.cpu().numpy() if isinstance(k_op, torch.Tensor) else np.asarray(k_op)
-    has = np.zeros(cols.n_ops, dtype=bool)
-    has[k_op.astype(np.int64)] = True
-    missing = np.nonzero(~has[first_op:])[0]
-    first_missing = int(missing[0]) + first_op if missing.size else None
+    (energy.py:227-230): an op without kernels, then repeat < 1.  The
+    kernel-less scan runs on the device (one scatter, one reduction)."""
+    n = cols.n_ops - first_op
+    first_missing = None
+    if n > 0:
+        dev = _native.device()
+        has = torch.zeros(cols.n_ops, dtype=torch.bool, device=dev)
+        if cols.n_kernels and cols.k_op is not None:
+            has[cols.device("k_op").to(torch.int64)] = True
+        miss = ~has[first_op:]
+        if bool(miss.any().item()):
+            first_missing = int(torch.argmax(miss.to(torch.int8)).item()) + first_op
     if first_missing == first_op:
         oid = cols.op_ids[first_missing] if cols.op_ids is not None else f"op{first_missing}"
         raise SignalError(f"operator {oid!r} launched no kernels; nothing to replay")
