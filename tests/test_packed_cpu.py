@@ -132,3 +132,27 @@ def test_regular_clock_ts_bit_packed(tmp_path):
         assert p.sig_bits is not None and p.sig_bits <= 9  # < 300 distinct signatures
         np.testing.assert_array_equal(np.asarray(p.op_sig_dict)[_fields(p.op_sig, p.sig_bits, sig.size)], sig)
         assert p.signal_span() == c.signal_span()
+
+
+@pytest.mark.parametrize("spread", [0, 1, 2, 3, 31, 32, 255, 4095, 32767])
+def test_bitfields_roundtrip_every_width(spread):
+    """_bitfields packs v - min(v) in bit_length(spread) bits (at least 1),
+    fields straddling 32-bit words included; torch and numpy agree."""
+    import torch
+    from paper_2512_08365_b200.columns import _bitfields
+    rng = np.random.default_rng(spread)
+    v = 1000 + rng.integers(0, spread + 1, size=4097)
+    v[0], v[-1] = 1000, 1000 + spread
+    lo, width, words = _bitfields(v, 15)
+    assert lo == 1000 and width == max(1, spread.bit_length())
+    np.testing.assert_array_equal(_fields(words, width, v.size) + lo, v)
+    lo_t, width_t, words_t = _bitfields(torch.from_numpy(v), 15)
+    assert (lo_t, width_t) == (lo, width)
+    np.testing.assert_array_equal(words_t.numpy().view(np.uint32), words)
+
+
+def test_bitfields_refuse_wide_spreads():
+    from paper_2512_08365_b200.columns import _bitfields, _bitpack
+    assert _bitfields(np.array([0, 1 << 15]), 15) is None
+    assert _bitpack(np.array([5, 3])) is None          # a negative delta: not sorted
+    assert _bitpack(np.array([7])) is None             # fewer than two samples
