@@ -72,3 +72,20 @@ def test_bit_packed_timestamps_decode_exactly(jitter):
     assert p.ts_bits is not None and p.ts_bits <= 8
     assert torch.equal(p.device("ts").cpu(), ts)
     assert p.signal_span() == c.signal_span()
+
+
+@pytest.mark.parametrize("spread", [0, 1, 7, 200, 4095, 32000])
+def test_bit_packed_intervals_decode_exactly(spread):
+    """dw_unpack_bits + dw_unpack_bits_dur on interval columns of every width."""
+    from paper_2512_08365_b200.columns import TraceColumns
+    rng = np.random.default_rng(spread + 1)
+    n = 200_003
+    st = 10**9 + np.cumsum(rng.integers(50, 51 + spread, size=n)).astype(np.int64)
+    en = st + rng.integers(3, 4 + spread, size=n)
+    ts = np.arange(st[0] - 100, en.max() + 1000, 997, dtype=np.int64)
+    c = TraceColumns.from_arrays(ts, np.full(ts.size, 75.0), st, en, st, en, np.arange(n, dtype=np.int32))
+    p = pack(c)
+    assert {"op_start", "op_end", "k_start", "k_end"} <= set(p.iv_bits)
+    for name in ("op_start", "op_end", "k_start", "k_end"):
+        assert torch.equal(p.device(name).cpu(), torch.from_numpy(c.host(name))), name
+    assert p.n_ops == n and p.n_kernels == n
