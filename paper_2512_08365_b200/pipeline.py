@@ -42,16 +42,21 @@ def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAUL
             ) -> Analysis:
     """Ledgers for both traces, the signature-join diff and the top-k report.
 
+    ``lean`` (default): the join writes only each finding's ranking key (the
+    top-k rows' ratio / verdict / side / informational / wasted are derived
+    on the host, equal to the device's); ``lean=False`` keeps every finding
+    column on the device (``Analysis.join.columns``) plus energy-per-work.
+
     (Running the join's pairing on a second stream beside the ledgers, with
     the tile kernel capped to fewer SMs via dw_set_attribute_sms, was measured
     slower on C4 -- 35.4 vs 34.5 ms at 12 reserved SMs, worse with more -- so
     the phases run back to back.)
 
     With ``copy_stream`` (host-resident inputs): B's host->HBM copy runs on
-    that stream after A's, under A's attribution, B's signature columns first, so the
-    pairing (``join_prepare``, signatures only) runs while the rest of B is
-    still crossing PCIe; only B's ledger and the findings remain after the
-    last byte lands."""
+    that stream after A's, under A's attribution, B's signature and operator
+    columns first, so the pairing (``join_prepare``) runs while the rest of B
+    is still crossing PCIe, and B's later columns decode on a side stream as
+    each lands; only B's ledger and the findings remain after the last byte."""
     ca, cb = TraceColumns.from_trace(trace_a), TraceColumns.from_trace(trace_b)
     prep = None
     if copy_stream is not None:
