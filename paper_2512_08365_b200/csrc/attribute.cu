@@ -480,6 +480,10 @@ __device__ __forceinline__ void tile_intervals(const AttrParams &p, const TileSm
 #define DW_CHUNK 512
 #endif
 constexpr int CHUNK = DW_CHUNK;  // intervals per phase-1/phase-2 round
+#ifndef DW_FOLD_UNROLL
+#define DW_FOLD_UNROLL 4
+#endif
+constexpr int FOLD_UNROLL = DW_FOLD_UNROLL;
 
 // item meta: q (chunk index, 10 bits) | s (first interior term, 11 bits) << 10 |
 //            cnt (interior terms, 9 bits) << 21 | has_last << 30
@@ -733,7 +737,7 @@ __device__ void tile_intervals_two_pass(const AttrParams &p, TileSmem &sm, Group
             const int j = (int)(mt >> 30);
             double tot = so.F0[q];
             const double *tp = term + s;
-#pragma unroll 4
+#pragma unroll FOLD_UNROLL
             for (int u = 0; u < cnt; ++u) tot = __dadd_rn(tot, tp[u]);
             if ((mt >> 29) & 1u) tot = __dadd_rn(tot, so.L[q]);
             const int64_t k = ckq[j] + q;
