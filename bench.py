@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--method", default="samples", choices=("samples", "ground_truth"))
     ap.add_argument("--k", type=int, default=100)
+    ap.add_argument("--summation", default="exact", choices=("exact", "reference"),
+                    help="how each interval's pieces are summed (energy.build_ledger): the exact "
+                         "fixed-point sum (default, the scale path) or the reference's sequential order")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-ops", type=int, default=2_000_000)
@@ -192,6 +195,21 @@ def c_sig(c):
     return np.ascontiguousarray(s).view(np.uint64)
 
 
+def host_cpu() -> dict:
+    """The host's CPU model (lscpu "Model name", from /proc/cpuinfo) and
+    logical core count, reported beside every CPU number."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.lower().startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 def cpu_baseline(args, steps: int = 1) -> dict:
     import oracle
     ca, cb = cpu_sample(args.config, args.cpu_sample_ops)
@@ -202,6 +220,7 @@ def cpu_baseline(args, steps: int = 1) -> dict:
         cpu_step(ca, cb, args.method, args.k)
     dt = (time.perf_counter() - t0) / steps
     return {"value": intervals / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "port",
+            **host_cpu(),
             "sample": (f"{args.config} distribution scaled to {ca.n_ops}+{cb.n_ops} ops, "
                        f"{ca.n_power}+{cb.n_power} samples (pair); oracle/dw_oracle.c "
                        f"reference-order sums, {oracle.num_threads()} threads"),
@@ -228,7 +247,7 @@ def run_reference(args, rank: int, world: int):
         "data": "synthetic",
         "config": {"workload": f"{args.config} (bounded CPU sample)", "method": args.method,
                    "ops_per_trace": ca.n_ops, "samples_per_trace": ca.n_power},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "port",
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.num_threads(), "kind": "port", **host_cpu(),
                          "sample": f"{ca.n_ops}+{cb.n_ops} ops, {ca.n_power}+{cb.n_power} samples"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -261,7 +280,7 @@ def run_ours(args, rank: int, world: int, local: int):
     samples = ca.n_power + cb.n_power
 
     def step():
-        res = analyze(ca, cb, args.method, 0.10, args.k)
+        res = analyze(ca, cb, args.method, 0.10, args.k, summation=args.summation)
         if world > 1:  # corpus top-k: merge every rank's k candidates over NCCL
             jd = res.join
             f = jd.order
@@ -276,6 +295,7 @@ def run_ours(args, rank: int, world: int, local: int):
     if world > 1:
         dist.barrier()
     L.dw_kernel_time_ms(1)
+    L.dw_kernel_timed_count(1)
     L.dw_kernel_timing(1)
     _native.launch_count(reset=True)
     with ClockSampler(local) as clocks:
@@ -288,7 +308,8 @@ def run_ours(args, rank: int, world: int, local: int):
         torch.cuda.synchronize()
     L.dw_kernel_timing(0)
     launches = _native.launch_count(reset=True)
-    kern_ms = L.dw_kernel_time_ms(1) / (2 * args.steps)  # per tile-kernel launch
+    n_timed = int(L.dw_kernel_timed_count(1))
+    kern_ms = L.dw_kernel_time_ms(1) / max(n_timed, 1)  # per tile-kernel launch (every launch timed)
     ms = e0.elapsed_time(e1) / args.steps
     t = torch.tensor([ms], device=dev)
     if world > 1:
@@ -300,8 +321,8 @@ def run_ours(args, rank: int, world: int, local: int):
     from paper_2512_08365_b200.join import join_diff
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    la = build_ledger(ca, method=args.method)
-    lb = build_ledger(cb, method=args.method)
+    la = build_ledger(ca, method=args.method, summation=args.summation)
+    lb = build_ledger(cb, method=args.method, summation=args.summation)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     jd = join_diff(ca, cb, la, lb, 0.10, args.k, full_columns=False, epw=False)
@@ -371,7 +392,8 @@ def run_ours(args, rank: int, world: int, local: int):
         def e2e_step():
             for pc in pinned:
                 pc.drop_device()
-            r = analyze(pinned[0], pinned[1], args.method, 0.10, args.k, copy_stream=copy_stream)
+            r = analyze(pinned[0], pinned[1], args.method, 0.10, args.k, copy_stream=copy_stream,
+                        summation=args.summation)
             return r
 
         for _ in range(max(5, args.warmup)):  # the first steps run up to 50 % slower (allocator, pinned pages)
@@ -417,7 +439,7 @@ def run_ours(args, rank: int, world: int, local: int):
         "data": "synthetic",
         "config": {"workload": f"{args.config}: trace pair, {cfg.n_ops} ops and "
                                f"{cfg.n_samples} power samples per trace",
-                   "method": args.method, "intervals_per_pair": intervals,
+                   "method": args.method, "summation": args.summation, "intervals_per_pair": intervals,
                    "samples_per_pair": samples, "findings": P, "top_k": args.k,
                    "l2": (f"inputs (~{(16 * samples + 24 * intervals) / 1e9:.1f} GB/pair read per step) >> "
                           f"126 MB L2; no flush needed"),

@@ -62,10 +62,24 @@ typedef struct CUstream_st *dw_stream_t; /* == cudaStream_t */
 #ifndef DW_DIRECT_MAX
 #define DW_DIRECT_MAX 256
 #endif
+/* How an interval's pieces are summed (dw_signal_t.sum_mode):
+ *  DW_SUM_REFERENCE  the reference's sequential fp64 sum for intervals of at
+ *                    most DW_DIRECT_MAX pieces (bit-identical to
+ *                    energy.integrate), the exact sum below for longer ones;
+ *  DW_SUM_EXACT      every interval as the exact sum of its pieces, each
+ *                    rounded to 2^-40 W*us, rounded once to a double and
+ *                    divided by 1e6.  Integer addition is associative, so the
+ *                    result does not depend on how the device groups the
+ *                    pieces (window prefixes, whole tiles); it differs from
+ *                    the reference's sum by a few ulps.  Same
+ *                    pieces, same values in both modes for every interval
+ *                    longer than DW_DIRECT_MAX pieces and for the span total
+ *                    of a signal with more than DW_DIRECT_MAX pieces. */
+#define DW_SUM_REFERENCE 0
+#define DW_SUM_EXACT 1
 /* Tiling of the attribution kernel.  Whole tiles enter long-interval sums as
- * fp64 tile sums reduced in a fixed order (per-thread sums of term pairs
- * strided over DW_TILE_THREADS threads, warp xor-butterfly, warps in order), converted to
- * fixed point; the CPU oracle mirrors that order (oracle/dw_oracle.c). */
+ * exact fixed-point tile sums (int128 sums of the rounded pieces), so any
+ * grouping gives the oracle's value (oracle/dw_oracle.c fx_range). */
 #define DW_TILE 1024
 #ifndef DW_TILE_THREADS
 #define DW_TILE_THREADS 192
@@ -80,6 +94,8 @@ typedef struct {
                         (energy.py:80); LINEAR: ignored, the span is [ts[0], ts[n-1]] */
     int32_t kind;    /* DW_SIGNAL_STEP | DW_SIGNAL_LINEAR */
     int32_t validate_order; /* 1: check ts strictly increasing (DW_E_ORDER) */
+    int32_t sum_mode; /* DW_SUM_REFERENCE (0, default) | DW_SUM_EXACT (1) */
+    int32_t pad;
 } dw_signal_t;
 
 typedef struct {
@@ -426,9 +442,12 @@ const char *dw_error_string(int code);
 int64_t dw_launch_count(int reset);
 /* Profiling hook for bench.py's roofline: when enabled, CUDA events bracket
  * every attribution tile-kernel launch on its stream; dw_kernel_time_ms
- * synchronises them and returns the summed device time. */
+ * synchronises them and returns the summed device time, and
+ * dw_kernel_timed_count the number of launches that time covers (every
+ * launch: a full event ring is folded into the sum, never dropped). */
 int dw_kernel_timing(int enable);
 double dw_kernel_time_ms(int reset);
+int64_t dw_kernel_timed_count(int reset);
 
 #ifdef __cplusplus
 }

@@ -25,7 +25,8 @@ _LIB = _HERE / "libdw_oracle.so"
 _lib = None
 
 MODE_REFERENCE = 0  # sequential fp64 sum for every interval (the reference's arithmetic)
-MODE_DEVICE = 1     # the GPU's definition: sequential <= DW_DIRECT_MAX segments, exact fixed point above
+MODE_DEVICE = 1     # the GPU's reference-order mode: sequential <= DW_DIRECT_MAX segments, exact fixed point above
+MODE_EXACT = 2      # the GPU's exact mode (summation="exact"): every interval as the exact fixed-point sum of its pieces
 
 DW_DIRECT_MAX = 256
 
@@ -47,6 +48,7 @@ def lib():
         _lib.dwo_fx_sum.restype = ctypes.c_double
         _lib.dwo_py_sum.restype = ctypes.c_double
         _lib.dwo_total_device.restype = ctypes.c_double
+        _lib.dwo_total_device_mode.restype = ctypes.c_double
     return _lib
 
 
@@ -149,13 +151,15 @@ def replay(ts, watts, span_hi, op_start, op_end, repeat=1000, period_us=40_000, 
     return w_out, j_out
 
 
-def total_device(kind, ts, watts, span_hi=None) -> float:
-    """The ledger total over the whole span under the device's definition."""
+def total_device(kind, ts, watts, span_hi=None, exact: bool = False) -> float:
+    """The ledger total over the whole span under the device's definition
+    (``exact``: the DW_SUM_EXACT mode's)."""
     ts = np.ascontiguousarray(ts, dtype=np.int64)
     watts = np.ascontiguousarray(watts, dtype=np.float64)
-    return float(lib().dwo_total_device(ctypes.c_int(0 if kind == "step" else 1), _p(ts), _p(watts),
-                                        ctypes.c_int64(ts.shape[0]),
-                                        ctypes.c_int64(int(span_hi) if span_hi is not None else 0)))
+    return float(lib().dwo_total_device_mode(ctypes.c_int(0 if kind == "step" else 1), _p(ts), _p(watts),
+                                             ctypes.c_int64(ts.shape[0]),
+                                             ctypes.c_int64(int(span_hi) if span_hi is not None else 0),
+                                             ctypes.c_int(1 if exact else 0)))
 
 
 def fx_sum(x) -> float:
@@ -180,8 +184,8 @@ def ledger(kind, ts, watts, span_hi, op_start, op_end, k_start, k_end, mode=MODE
         span = (int(ts[0]), int(ts[-1]))
     per_op = f(op_start, op_end)
     per_k = f(k_start, k_end)
-    if mode == MODE_DEVICE:
-        total = total_device(kind, ts, watts, span_hi)
+    if mode in (MODE_DEVICE, MODE_EXACT):
+        total = total_device(kind, ts, watts, span_hi, exact=mode == MODE_EXACT)
     else:
         total = float(f(np.array([span[0]]), np.array([span[1]]))[0])
     op_total = py_sum(per_op) if mode == MODE_REFERENCE else fx_sum(per_op)

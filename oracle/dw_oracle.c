@@ -225,54 +225,21 @@ static double step_direct(const int64_t *ts, const double *w, int64_t n, int64_t
     return total / US_PER_S;
 }
 
-/* ---- the device's long-interval definition (MODE_DEVICE) ----
- * Whole tiles of DW_TILE terms enter as fp64 tile sums reduced in the GPU's
- * fixed order: thread t of DW_TILE_THREADS sums the term pairs (2t, 2t+1),
- * (2t + 2*THREADS, 2t + 2*THREADS + 1), ... sequentially; each warp
- * combines its 32 lanes by an xor butterfly (lane 0's value); the warp
- * results are added in warp order.  Partial tiles and edge
- * terms enter term by term.  Everything meets in exact fixed point. */
+/* ---- the device's fixed-point definition (MODE_DEVICE long intervals,
+ * MODE_EXACT every interval) ----
+ * The interval's pieces (the reference's own decomposition: edge pieces with
+ * the interpolated endpoint values, interior pieces between samples) are each
+ * rounded to 2^-40 W*us and summed exactly (int128); the sum is rounded once
+ * to a double and divided by 1e6.  Integer addition is associative, so the
+ * GPU may group the pieces any way it likes (window prefixes, whole-tile
+ * sums) and still return exactly this value. */
 typedef double (*term_fn)(const void *ctx, int64_t i);
 
-static double tile_sum(term_fn term, const void *ctx, int64_t t0, int64_t t1) {
-    double red[DW_TILE_THREADS / 32];
-    for (int w = 0; w < DW_TILE_THREADS / 32; w++) {
-        double v[32];
-        for (int l = 0; l < 32; l++) {
-            double acc = 0.0;
-            for (int64_t r = t0 + 2 * (w * 32 + l); r < t1; r += 2 * DW_TILE_THREADS) {
-                acc += term(ctx, r);
-                if (r + 1 < t1) acc += term(ctx, r + 1);
-            }
-            v[l] = acc;
-        }
-        for (int off = 16; off > 0; off >>= 1) {
-            double nv[32];
-            for (int l = 0; l < 32; l++) nv[l] = v[l] + v[l ^ off];
-            memcpy(v, nv, sizeof(v));
-        }
-        red[w] = v[0];
-    }
-    double s = red[0];
-    for (int w = 1; w < DW_TILE_THREADS / 32; w++) s += red[w];
-    return s;
-}
-
-/* exact sum of terms [j0, j1] under the tile decomposition */
+/* exact sum of terms [j0, j1] */
 static i128 fx_range(term_fn term, const void *ctx, int64_t nterms, int64_t j0, int64_t j1) {
+    (void)nterms;
     i128 acc = 0;
-    if (j1 < j0) return 0;
-    int64_t ta = j0 / DW_TILE, tb = j1 / DW_TILE;
-    if (ta == tb) {
-        for (int64_t i = j0; i <= j1; i++) acc += q_term(term(ctx, i));
-        return acc;
-    }
-    for (int64_t i = j0; i < (ta + 1) * DW_TILE; i++) acc += q_term(term(ctx, i));
-    for (int64_t t = ta + 1; t < tb; t++) {
-        int64_t e = (t + 1) * DW_TILE < nterms ? (t + 1) * DW_TILE : nterms;
-        acc += q_term(tile_sum(term, ctx, t * DW_TILE, e));
-    }
-    for (int64_t i = tb * DW_TILE; i <= j1; i++) acc += q_term(term(ctx, i));
+    for (int64_t i = j0; i <= j1; i++) acc += q_term(term(ctx, i));
     return acc;
 }
 
@@ -295,6 +262,23 @@ static double step_fx(const int64_t *ts, const double *w, int64_t n, int64_t spa
     return term_to_joules(acc);
 }
 
+/* MODE_EXACT, step: every interval as the exact sum of its pieces.  Pieces
+ * as the device's exact path takes them: none for hi == lo; one
+ * w[a]*(hi-lo) inside a single segment; else the first partial segment, the
+ * whole interior segments and the last partial segment. */
+static double step_exact(const int64_t *ts, const double *w, int64_t n, int64_t span_hi,
+                         int64_t lo, int64_t hi) {
+    if (hi <= lo) return 0.0;
+    sig_ctx c = {ts, w, n, span_hi};
+    int64_t a = upper_bound64(ts, n, lo) - 1;
+    int64_t b = lower_bound64(ts, n, hi) - 1;
+    if (a == b) return term_to_joules(q_term(w[a] * (double)(hi - lo)));
+    i128 acc = fx_range(step_term, &c, n, a + 1, b - 1);
+    acc += q_term(w[a] * (double)(ts[a + 1] - lo));
+    acc += q_term(w[b] * (double)(hi - ts[b]));
+    return term_to_joules(acc);
+}
+
 /* the ledger total over the whole span, device definition */
 double dwo_total_device(int kind, const int64_t *ts, const double *w, int64_t n, int64_t span_hi);
 
@@ -306,7 +290,9 @@ typedef struct {
 static void step_range(void *ctx, int64_t k0, int64_t k1) {
     iv_job *j = (iv_job *)ctx;
     for (int64_t k = k0; k < k1; k++) {
-        if (j->mode == 1 && step_nseg(j->ts, j->n, j->lo[k], j->hi[k]) > DW_DIRECT_MAX)
+        if (j->mode == 2)
+            j->out[k] = step_exact(j->ts, j->w, j->n, j->span_hi, j->lo[k], j->hi[k]);
+        else if (j->mode == 1 && step_nseg(j->ts, j->n, j->lo[k], j->hi[k]) > DW_DIRECT_MAX)
             j->out[k] = step_fx(j->ts, j->w, j->n, j->span_hi, j->lo[k], j->hi[k]);
         else
             j->out[k] = step_direct(j->ts, j->w, j->n, j->span_hi, j->lo[k], j->hi[k]);
@@ -314,8 +300,10 @@ static void step_range(void *ctx, int64_t k0, int64_t k1) {
 }
 
 /* mode: 0 = reference-literal sequential sum for every interval;
- *       1 = the GPU's definition: sequential for <= DW_DIRECT_MAX segments,
- *           exact fixed point above.
+ *       1 = the GPU's reference-order mode: sequential for <= DW_DIRECT_MAX
+ *           segments, exact fixed point above;
+ *       2 = the GPU's exact mode (DW_SUM_EXACT): exact fixed point for every
+ *           interval.
  * Returns DW_OK, or the error code of the first bad interval (*bad = index). */
 int dwo_integrate_step(const int64_t *ts, const double *w, int64_t n, int64_t span_hi,
                        const int64_t *lo, const int64_t *hi, int64_t m, double *out,
@@ -380,7 +368,11 @@ static double lin_fx(const int64_t *ts, const double *w, int64_t n, int64_t lo, 
 
 static double lin_integrate(const int64_t *ts, const double *w, int64_t n, int64_t lo,
                             int64_t hi, int fx) {
-    if (fx) return lin_fx(ts, w, n, lo, hi);
+    if (fx) {
+        /* one piece [lo, hi] when no sample lies strictly inside */
+        if (lin_npieces(ts, n, lo, hi) == 1) return term_to_joules(q_term(lin_term(ts, w, n, lo, hi)));
+        return lin_fx(ts, w, n, lo, hi);
+    }
     int64_t first = upper_bound64(ts, n, lo); /* first ts > lo */
     int64_t last = lower_bound64(ts, n, hi);  /* first ts >= hi */
     int64_t prev = lo;
@@ -400,7 +392,7 @@ static double lin_integrate(const int64_t *ts, const double *w, int64_t n, int64
 static void lin_range(void *ctx, int64_t k0, int64_t k1) {
     iv_job *j = (iv_job *)ctx;
     for (int64_t k = k0; k < k1; k++) {
-        int fx = j->mode == 1 && lin_npieces(j->ts, j->n, j->lo[k], j->hi[k]) > DW_DIRECT_MAX;
+        int fx = j->mode == 2 || (j->mode == 1 && lin_npieces(j->ts, j->n, j->lo[k], j->hi[k]) > DW_DIRECT_MAX);
         j->out[k] = lin_integrate(j->ts, j->w, j->n, j->lo[k], j->hi[k], fx);
     }
 }
@@ -597,20 +589,23 @@ int dwo_join(const uint64_t *sig_a, int64_t na, const uint64_t *sig_b, int64_t n
 }
 
 
-double dwo_total_device(int kind, const int64_t *ts, const double *w, int64_t n, int64_t span_hi) {
+/* exact: 1 = DW_SUM_EXACT (every span as the exact sum of its pieces); 0 =
+ * reference order (the literal sequential sum up to DW_DIRECT_MAX pieces). */
+double dwo_total_device_mode(int kind, const int64_t *ts, const double *w, int64_t n, int64_t span_hi,
+                             int exact) {
     sig_ctx c = {ts, w, n, span_hi};
     int64_t nterms = kind == 0 ? n : (n > 1 ? n - 1 : 1);
-    if (nterms <= DW_DIRECT_MAX) {
+    if (nterms <= DW_DIRECT_MAX && !exact) {
         int64_t lo = ts[0], hi = kind == 0 ? span_hi : ts[n - 1];
         if (kind == 0) return step_direct(ts, w, n, span_hi, lo, hi);
         return lin_integrate(ts, w, n, lo, hi, 0);
     }
-    i128 acc = 0;
-    for (int64_t t = 0; t * DW_TILE < nterms; t++) {
-        int64_t e = (t + 1) * DW_TILE < nterms ? (t + 1) * DW_TILE : nterms;
-        acc += q_term(tile_sum(kind == 0 ? step_term : lin_piece_term, &c, t * DW_TILE, e));
-    }
-    return term_to_joules(acc);
+    if (kind != 0 && n == 1) return 0.0;
+    return term_to_joules(fx_range(kind == 0 ? step_term : lin_piece_term, &c, nterms, 0, nterms - 1));
+}
+
+double dwo_total_device(int kind, const int64_t *ts, const double *w, int64_t n, int64_t span_hi) {
+    return dwo_total_device_mode(kind, ts, w, n, span_hi, 0);
 }
 
 /* ---------------------------------------------------- overlap split (G1)

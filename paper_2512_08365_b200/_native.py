@@ -49,6 +49,7 @@ EXPORTED = (
     "dw_exchange_count", "dw_exchange_scatter", "dw_ipc_handle", "dw_ipc_open", "dw_ipc_close",
     "dw_tensor_norms", "dw_tensor_prefilter", "dw_unfold_smem_doubles", "dw_unfold_spectra", "dw_spectra_embed",
     "dw_version", "dw_error_string", "dw_launch_count", "dw_kernel_timing", "dw_kernel_time_ms",
+    "dw_kernel_timed_count",
 )
 
 
@@ -69,7 +70,10 @@ c_vp = ctypes.c_void_p
 
 class Signal(ctypes.Structure):
     _fields_ = [("d_ts", c_vp), ("d_watts", c_vp), ("n", c_i64), ("span_hi", c_i64),
-                ("kind", c_i32), ("validate_order", c_i32)]
+                ("kind", c_i32), ("validate_order", c_i32), ("sum_mode", c_i32), ("pad", c_i32)]
+
+
+SUM_REFERENCE, SUM_EXACT = 0, 1  # dw_signal_t.sum_mode
 
 
 class IntervalSet(ctypes.Structure):
@@ -179,6 +183,8 @@ def lib():
         L.dw_kernel_timing.argtypes = [ctypes.c_int]
         L.dw_kernel_time_ms.restype = ctypes.c_double
         L.dw_kernel_time_ms.argtypes = [ctypes.c_int]
+        L.dw_kernel_timed_count.restype = c_i64
+        L.dw_kernel_timed_count.argtypes = [ctypes.c_int]
         if hasattr(L, "dw_detect_pairs"):
             L.dw_detect_pairs.argtypes = [c_i64] + [c_vp] * 12 + [ctypes.c_double,
                                                                   ctypes.POINTER(Findings), c_vp]

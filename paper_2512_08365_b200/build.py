@@ -58,15 +58,21 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> Path
     if not variant and not force and not _stale():
         return LIB
     OUT_DIR.mkdir(exist_ok=True)
-    objs = []
-    log = []
+    jobs = []
     for src in SOURCES:
         if not (CSRC / src).exists():
             continue
         obj = OUT_DIR / (Path(src).stem + variant + ".o")
         cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", str(PKG.parent / "include"), "-c", str(CSRC / src),
                "-o", str(obj)]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        jobs.append((src, obj, cmd))
+    # the translation units are independent: compile them side by side
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(lambda j: subprocess.run(j[2], capture_output=True, text=True), jobs))
+    objs = []
+    log = []
+    for (src, obj, _), r in zip(jobs, results):
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")

@@ -27,6 +27,19 @@ import torch
 from . import _native
 
 
+def synthetic_id(prefix: str, i: int, n: int) -> str:
+    """Name of item ``i`` of ``n`` in columns that carry no ids: zero-padded to
+    the width of ``n - 1``, so lexicographic order (the report's nodes_a
+    tie-break, detect.py:263-266) equals index order.  Every view of such
+    columns (ledgers, detect, join findings, diagnosis) uses this name."""
+    return f"{prefix}{i:0{len(str(max(n - 1, 0)))}d}"
+
+
+def synthetic_ids(prefix: str, n: int) -> list:
+    w = len(str(max(n - 1, 0)))
+    return [f"{prefix}{i:0{w}d}" for i in range(n)]
+
+
 def _np_i64(x):
     return np.ascontiguousarray(np.asarray(x, dtype=np.int64))
 

@@ -76,7 +76,7 @@ struct AttrParams {
     int32_t kind;
     int32_t nsets;
     int32_t validate_order;
-    int32_t pad;
+    int32_t sum_mode;            // DW_SUM_REFERENCE | DW_SUM_EXACT
     const int64_t *start[DW_MAX_SETS];
     const int64_t *end[DW_MAX_SETS];
     double *out[DW_MAX_SETS];
@@ -84,8 +84,8 @@ struct AttrParams {
     int64_t n[DW_MAX_SETS];
     int32_t check_sorted[DW_MAX_SETS];
     const int64_t *first;        // [nsets][ntiles + 1]
-    double *tile_sum;            // [ntiles] fp64 tile sums (fixed reduction tree)
-    unsigned long long *prefix;  // [ntiles + 1][2] exact int128 prefix of q(tile_sum)
+    unsigned long long *tile_fx; // [ntiles][2] exact int128 tile sums: sum of q(piece) over the tile
+    unsigned long long *prefix;  // [ntiles + 1][2] exact int128 prefix of the tile sums
     unsigned long long *scan_part; // [nblocks][2] scan partials
     unsigned long long *long_list;
     DevStatus *st;
@@ -494,7 +494,7 @@ struct __align__(16) GroupSmem {  // private to one consumer group
     double F0[CHUNK];    // first piece (0.0 + first piece for the trapezoid)
     double L[CHUNK];     // last piece
     uint32_t meta[CHUNK];
-    double red[NCW];
+    unsigned long long red[NCW][2];
     int64_t kq[2][DW_MAX_SETS];  // per chunk parity, per set: interval index = kq + chunk index
     int4 desc[2][DW_MAX_SETS];   // per chunk parity, per set: smem base, staged limit, first staged slot
     int next_it;              // the group's claimed next tile (sequence position)
@@ -840,15 +840,15 @@ __device__ __forceinline__ void producer(const AttrParams &p, TileSmem &sm, int6
 }
 
 // Terms of pieces r, r+1 for r = r0 + 2*ctid + 2*ATTR_THREADS*k, r < rend,
-// stored to term[] (when non-null); returns this thread's partial of the tile
-// sum over pieces < e1, added in that order (the fixed order oracle/
-// dw_oracle.c tile_sum() restates).  Linear pieces use v(x) of energy.py:
-// 115-124 (w0 / wl at the signal's first / last sample, window indices rz0 /
-// rzS; elsewhere the interior form w[x-1] + (w[x] - w[x-1])).
+// stored to term[] (when non-null); returns this thread's exact share of the
+// tile sum (q(piece) over its pieces < e1, int128; any grouping gives the
+// same total).  Linear pieces use v(x) of energy.py:115-124 (w0 / wl at the
+// signal's first / last sample, window indices rz0 / rzS; elsewhere the
+// interior form w[x-1] + (w[x] - w[x-1])).
 template <int KIND, typename WIDTH>
-__device__ __forceinline__ double pair_terms(const double *w, const WIDTH &width, int r0, int rend, int e1,
-                                             int rz0, int rzS, double w0, double wl, double *term, int ctid) {
-    double acc = 0.0;
+__device__ __forceinline__ i128 pair_terms(const double *w, const WIDTH &width, int r0, int rend, int e1,
+                                           int rz0, int rzS, double w0, double wl, double *term, int ctid) {
+    i128 acc = 0;
     for (int r = r0 + 2 * ctid; r < rend; r += 2 * ATTR_THREADS) {
         const double2 wr = *reinterpret_cast<const double2 *>(w + r);  // w[r], w[r+1]
         const double d0 = (double)width(r), d1 = (double)width(r + 1);
@@ -869,10 +869,30 @@ __device__ __forceinline__ double pair_terms(const double *w, const WIDTH &width
             if (r + 1 < rend) *reinterpret_cast<double2 *>(term + r) = make_double2(t0, t1);
             else term[r] = t0;
         }
-        if (r < e1) acc = __dadd_rn(acc, t0);
-        if (r + 1 < e1) acc = __dadd_rn(acc, t1);
+        if (r < e1) acc += q40(t0);
+        if (r + 1 < e1) acc += q40(t1);
     }
     return acc;
+}
+
+// exact int128 tile sum from each thread's share: warp sums to red[], then
+// one thread adds the warps (after the group barrier that follows)
+__device__ __forceinline__ void tile_fx_partial(i128 acc, unsigned long long (*red)[2], int ctid) {
+    acc = warp_sum_i128(acc);
+    if ((ctid & 31) == 0) {
+        const I128Parts pp = split(acc);
+        red[ctid >> 5][0] = pp.lo;
+        red[ctid >> 5][1] = pp.hi;
+    }
+}
+template <int NW>
+__device__ __forceinline__ void tile_fx_store(const unsigned long long (*red)[2], unsigned long long *out) {
+    i128 t = 0;
+#pragma unroll
+    for (int k = 0; k < NW; ++k) t += join(red[k][0], red[k][1]);
+    const I128Parts pp = split(t);
+    out[0] = pp.lo;
+    out[1] = pp.hi;
 }
 
 struct Width32 {
@@ -981,10 +1001,8 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_tiles_kernel(AttrParams
             // (b) interior terms of pieces r0 .. last-1 into the stage's ts slots
             // (phase 1 searches ts32 from here on), (c) the tile-sum partials
             double *term = reinterpret_cast<double *>(const_cast<int64_t *>(s_ts));
-            double acc = pair_terms<KIND>(s_w, Width32{gs.ts32}, r0, last, e1, rz0, rzS, cx.w0, cx.wl, term, ctid);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-            if ((ctid & 31) == 0) gs.red[ctid >> 5] = acc;
+            const i128 acc = pair_terms<KIND>(s_w, Width32{gs.ts32}, r0, last, e1, rz0, rzS, cx.w0, cx.wl, term, ctid);
+            tile_fx_partial(acc, gs.red, ctid);
             PROF(2);
             if (M.c[DW_MAX_SETS] == 0) consumer_sync(g);  // no intervals: red must still be visible
 #ifdef DW_EXP_PASSA_ONLY
@@ -992,31 +1010,261 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_tiles_kernel(AttrParams
 #else
             tile_intervals_two_pass<KIND>(p, sm, gs, stage, tile, cx, ctid, g, prof_t);
 #endif
-            if (ctid == 0) {
-                double t = gs.red[0];
-#pragma unroll
-                for (int k = 1; k < NCW; ++k) t = __dadd_rn(t, gs.red[k]);
-                p.tile_sum[tile] = t;
-            }
+            if (ctid == 0) tile_fx_store<NCW>(gs.red, p.tile_fx + 2 * tile);
         } else {
-            double acc = pair_terms<KIND>(s_w, Width64{s_ts}, r0, e1, e1, rz0, rzS, cx.w0, cx.wl,
-                                          (double *)nullptr, ctid);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-            if ((ctid & 31) == 0) gs.red[ctid >> 5] = acc;
+            const i128 acc = pair_terms<KIND>(s_w, Width64{s_ts}, r0, e1, e1, rz0, rzS, cx.w0, cx.wl,
+                                              (double *)nullptr, ctid);
+            tile_fx_partial(acc, gs.red, ctid);
             consumer_sync(g);
             if (ctid == 0) gs.next_it = atomicAdd(&sm.claim, 1);  // every thread has read it
-            if (ctid == 0) {
-                double t = gs.red[0];
-#pragma unroll
-                for (int k = 1; k < NCW; ++k) t = __dadd_rn(t, gs.red[k]);
-                p.tile_sum[tile] = t;
-            }
+            if (ctid == 0) tile_fx_store<NCW>(gs.red, p.tile_fx + 2 * tile);
             Ts64 a64{s_ts, base};
             tile_intervals<KIND>(p, sm, stage, a64, s_w, tile, (int64_t)INT64_MAX, cx, ctid);
             consumer_sync(g);
         }
         if (ctid == 0) mbar_arrive(&sm.empty[stage]);
+    }
+}
+
+// ------------------------------------------------ K2x exact-sum tile kernel
+// DW_SUM_EXACT (every interval = the exact sum of its pieces rounded to
+// 2^-40 W*us, rounded once).  Same producer and stage ring as K2; per tile a
+// consumer group:
+//   pass B  one thread per XPER consecutive pieces of the window: the window's
+//           32-bit relative timestamps, each piece's term and its fixed-point
+//           value q (two instructions for |term| < 2^23 W*us), the thread's
+//           share of the exact tile sum, and a warp scan of the q's (mod 2^64);
+//   (group barrier)
+//           the exclusive window prefix P[r] = sum of q over pieces < r, stored
+//           into the stage's timestamp slots (mod 2^64);
+//   (group barrier)
+//   items   one thread per interval: locate its first piece and piece count
+//           (the phase-1 search), its two edge pieces, and
+//           q(first) + (P[s + cnt] - P[s]) + q(last) -- O(1) whatever the
+//           length.  The modular difference is exact whenever the interval's
+//           true sum is below 2^63 units; the bound (hi - lo) * max|w| <= 8e6
+//           W*us guarantees it (|v| <= max|w| for every value the pieces use),
+//           and intervals beyond the bound or DW_DIRECT_MAX pieces go to K4,
+//           which sums the same pieces in int128.
+// Each warp releases the stage on its own (empty barrier count = NCW): no
+// barrier at the end of a tile; the 32-bit timestamps are double buffered.
+constexpr int XPER = (WIN + ATTR_THREADS - 1) / ATTR_THREADS;  // pieces per thread in pass B
+constexpr double X_BOUND = 8.0e6;  // W*us: |sum of an interval's q| < 2^63 below it
+
+struct __align__(16) GroupSmemX {
+    uint32_t ts32[2][WIN];
+    unsigned long long red[NCW][2];  // warp shares of the exact tile sum
+    unsigned long long wtot[NCW];    // warp totals of the q scan (mod 2^64)
+    uint32_t wmax[NCW];              // warp max of |w| (high word, rounded up)
+    int next_it;
+};
+
+// |x| rounded up to its high 32 bits: a monotone u32 bound (non-negative doubles
+// order as their bit patterns)
+__device__ __forceinline__ uint32_t abs_hi_up(double x) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(x));
+    const uint32_t h = (uint32_t)(b >> 32);
+    return h == 0x7FF00000u ? h : h + ((uint32_t)b != 0u);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    TileSmem &sm = *reinterpret_cast<TileSmem *>(smem_raw);
+    GroupSmemX *groups =
+        reinterpret_cast<GroupSmemX *>(smem_raw + ((sizeof(TileSmem) + 15) & ~(size_t)15));
+    const int tid = threadIdx.x;
+    if ((int64_t)blockIdx.x >= p.ntiles) return;
+
+    const int64_t S = p.S;
+    TileCtx cx;
+    cx.ts0 = __ldg(p.ts);
+    cx.tsl = __ldg(p.ts + S - 1);
+    cx.w0 = __ldg(p.w);
+    cx.wl = __ldg(p.w + S - 1);
+    cx.span_lo = cx.ts0;
+    cx.span_hi = KIND == DW_SIGNAL_STEP ? p.span_hi : cx.tsl;
+    const int64_t nterms = KIND == DW_SIGNAL_STEP ? S : S - 1;
+
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&sm.full[s], 1);
+            mbar_init(&sm.empty[s], NCW);  // one arrival per consumer warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid < GROUPS) groups[tid].next_it = tid;
+    if (tid == 0) sm.claim = GROUPS;
+    __syncthreads();
+
+    if (tid >= GROUPS * ATTR_THREADS) {
+        producer(p, sm, cx.span_hi, (tid - GROUPS * ATTR_THREADS) >> 5);
+        return;
+    }
+    const int g = tid / ATTR_THREADS;
+    const int ctid = tid - g * ATTR_THREADS;
+    const int lane = ctid & 31, warp = ctid >> 5;
+    GroupSmemX &gs = groups[g];
+    int par = 0;
+    for (;; par ^= 1) {
+        const int it = gs.next_it;
+        const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+        if (tile >= p.ntiles) break;
+        const int stage = it % STAGES;
+        mbar_wait(&sm.full[stage], (uint32_t)((it / STAGES) & 1));
+        const StageMeta &M = sm.meta[stage];
+        const int64_t wb = M.wb;
+        const int cnt = M.cnt;
+        int64_t *s_ts = sm.ts[stage];
+        const double *s_w = sm.w[stage];
+        const int64_t base = s_ts[0];
+        const int last = (wb + cnt == S) ? cnt : cnt - 1;  // last valid timestamp slot
+        const bool wide = (s_ts[last] - base) >= (int64_t)0xFFFFFFF0LL;
+        const int r0 = (int)(tile * TILE - wb);
+        const int r1 = (int)(min((tile + 1) * TILE, S) - wb);
+        const int e1 = (int)(min((tile + 1) * TILE, nterms) - wb);
+        const int rz0 = wb == 0 ? 0 : -1000;
+        const int rzS = (S - 1 - wb) < (int64_t)WIN ? (int)(S - 1 - wb) : -1000;
+        {
+            const int64_t dt = s_ts[r1 < last ? r1 : last] - s_ts[r0];
+            cx.scale = dt > 0 ? (float)(r1 - r0) / (float)dt : 0.0f;
+        }
+        cx.base = base;
+        uint32_t *ts32 = gs.ts32[par];
+
+        // ---- pass B: pieces rb .. rb + XPER - 1 of the window
+        const int rb = ctid * XPER;
+        long long q[XPER];
+        unsigned long long run = 0;
+        i128 tfx = 0;
+        uint32_t wm = 0;
+        {
+            int64_t t0 = rb <= last ? s_ts[rb] : 0;
+            // v(rb) for the linear pieces (window slot 0 has no left neighbour:
+            // its piece lies before the tile and is never used)
+            double wprev = s_w[rb > 0 ? rb - 1 : 0];
+            double wcur = rb < cnt ? s_w[rb] : 0.0;
+            double vcur = rb == rz0 ? cx.w0 : (rb == rzS ? cx.wl : __dadd_rn(wprev, __dsub_rn(wcur, wprev)));
+#pragma unroll
+            for (int i = 0; i < XPER; ++i) {
+                const int r = rb + i;
+                q[i] = 0;
+                if (r <= last) ts32[r] = (uint32_t)(t0 - base);
+                if (r < cnt) wm = max(wm, abs_hi_up(wcur));
+                if (r < last) {
+                    const int64_t t1 = s_ts[r + 1];
+                    const int64_t wd = t1 - t0;
+                    double term;
+                    if (KIND == DW_SIGNAL_STEP) {
+                        term = __dmul_rn(wcur, (double)wd);
+                        wcur = r + 1 < cnt ? s_w[r + 1] : 0.0;
+                    } else {
+                        const double wnext = s_w[r + 1];
+                        const double vnext = r + 1 == rzS ? cx.wl : __dadd_rn(wcur, __dsub_rn(wnext, wcur));
+                        term = __dmul_rn(__dmul_rn(0.5, __dadd_rn(vcur, vnext)), (double)wd);
+                        vcur = vnext;
+                        wcur = wnext;
+                    }
+                    long long qq;
+                    const bool fast = q40_fast(term, qq);
+                    q[i] = fast ? qq : 0;  // a huge piece: its intervals fail the bound
+                    if (r >= r0 && r < e1) tfx += fast ? (i128)qq : q_term(term);
+                    run += (unsigned long long)q[i];
+                    if (p.validate_order && r >= r0 && r < r1 && wb + r + 1 < S && wd <= 0)
+                        atomic_min_index(&p.st->order_index, wb + r);
+                    t0 = t1;
+                }
+            }
+        }
+        // warp inclusive scan of the per-thread sums (mod 2^64)
+        unsigned long long inc = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        wm = __reduce_max_sync(0xffffffffu, wm);
+        tile_fx_partial(tfx, gs.red, ctid);
+        if (lane == 31) gs.wtot[warp] = inc;
+        if (lane == 0) gs.wmax[warp] = wm;
+        consumer_sync(g);
+        if (ctid == 0) {
+            gs.next_it = atomicAdd(&sm.claim, 1);  // every thread has read it
+            tile_fx_store<NCW>(gs.red, p.tile_fx + 2 * tile);
+        }
+        // ---- the exclusive window prefix into the stage's timestamp slots
+        {
+            unsigned long long pre = inc - run;
+            uint32_t wmx = 0;
+#pragma unroll
+            for (int k = 0; k < NCW; ++k) {
+                if (k < warp) pre += gs.wtot[k];
+                wmx = max(wmx, gs.wmax[k]);
+            }
+            wm = wmx;
+            unsigned long long *P = reinterpret_cast<unsigned long long *>(s_ts);
+#pragma unroll
+            for (int i = 0; i < XPER; ++i) {
+                const int r = rb + i;
+                if (r <= last) P[r] = pre;
+                pre += (unsigned long long)q[i];
+            }
+        }
+        consumer_sync(g);
+        const double wmaxd = __longlong_as_double((long long)((unsigned long long)wm << 32));
+        const unsigned long long *P = reinterpret_cast<const unsigned long long *>(s_ts);
+
+        // ---- items: one interval per thread
+        const int64_t total = M.c[DW_MAX_SETS];
+        const int64_t *s_lo = sm.iv_lo[stage], *s_hi = sm.iv_hi[stage];
+        for (int64_t v = ctid; v < total; v += ATTR_THREADS) {
+            const int j = (v >= M.c[1]) + (v >= M.c[2]) + (v >= M.c[3]);
+            const int64_t k = v - M.c[j] + M.f0[j];
+            const int64_t idx = k - M.a0[j];
+            const bool staged = idx < M.copied[j];
+            int64_t glo, ghi;
+            if (staged) {
+                glo = s_lo[M.pool[j] + idx];
+                ghi = s_hi[M.pool[j] + idx];
+            } else {
+                glo = __ldg(p.start[j] + k);
+                ghi = __ldg(p.end[j] + k);
+            }
+            if (p.check_sorted[j] && k > 0) {
+                const int64_t prev = (staged && idx > 0) ? s_lo[M.pool[j] + idx - 1] : __ldg(p.start[j] + k - 1);
+                if (prev > glo) atomic_min_index(&p.st->unsorted_index[j], k);
+            }
+            if (ghi < glo || glo < cx.span_lo || ghi > cx.span_hi) {
+                report_bad(p, j, k);
+                continue;
+            }
+            bool ok = !wide && __dmul_rn((double)(ghi - glo), wmaxd) <= X_BOUND;
+            double J = 0.0;
+            if (ok) {
+                const uint32_t lo = (uint32_t)(glo - base);
+                const int64_t dh = ghi - base;
+                const uint32_t hi = dh > 0xFFFFFFFFLL ? 0xFFFFFFFFu : (uint32_t)dh;
+                double F0, L;
+                int s0, n, lst;
+                ok = phase1_item<KIND>(ts32, s_w, r0, r1, cnt, lo, hi, glo <= cx.ts0, glo >= cx.tsl, ghi <= cx.ts0,
+                                       ghi >= cx.tsl, cx, F0, L, s0, n, lst);
+                long long qf = 0, ql = 0;
+                ok = ok && q40_fast(F0, qf) && (!lst || q40_fast(L, ql));
+                if (ok) {
+                    const long long tq = qf + (lst ? ql : 0LL) + (long long)(P[s0 + n] - P[s0]);
+                    J = div_1e6(__dmul_rn((double)tq, 9.094947017729282379150390625e-13));  // * 2^-40
+                }
+            }
+            if (!ok) {
+                push_long(p, j, k);
+            } else {
+                const int64_t oidx = p.perm[j] ? __ldg(p.perm[j] + k) : k;
+                p.out[j][oidx] = J;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.empty[stage]);
     }
 }
 
@@ -1069,7 +1317,7 @@ __device__ __forceinline__ i128 thread_chunk(const AttrParams &p, int64_t b0, i1
 #pragma unroll
     for (int k = 0; k < SCAN_PER_THREAD; ++k) {
         int64_t b = b0 + k;
-        i128 v = b < p.ntiles ? q_term(p.tile_sum[b]) : (i128)0;
+        i128 v = b < p.ntiles ? join(p.tile_fx[2 * b], p.tile_fx[2 * b + 1]) : (i128)0;
         if (vals) vals[k] = v;
         sum += v;
     }
@@ -1149,14 +1397,14 @@ __device__ __forceinline__ double term_global(const AttrParams &p, int64_t i) {
 }
 
 // exact sum of terms [j0, j1] (inclusive): partial tiles term by term, whole
-// tiles through the int128 prefix of their fp64 sums; whole warp participates
+// tiles through the int128 prefix of the exact tile sums; whole warp participates
 template <int KIND>
 __device__ i128 range_sum(const AttrParams &p, int64_t j0, int64_t j1) {
     const int lane = threadIdx.x & 31;
     if (j1 < j0) return 0;
     auto span_sum = [&](int64_t a, int64_t b) -> i128 {
         i128 acc = 0;
-        for (int64_t i = a + lane; i <= b; i += 32) acc += q_term(term_global<KIND>(p, i));
+        for (int64_t i = a + lane; i <= b; i += 32) acc += q40(term_global<KIND>(p, i));
         return warp_sum_i128(acc);
     };
     const int64_t ta = j0 / TILE, tb = j1 / TILE;
@@ -1429,7 +1677,7 @@ __global__ void ledger_finalize_kernel(AttrParams p, const double *op_total) {
     const int64_t S = p.S;
     const int64_t nterms = KIND == DW_SIGNAL_STEP ? S : (S > 1 ? S - 1 : 1);
     double total;
-    if (nterms <= DIRECT) {
+    if (nterms <= DIRECT && p.sum_mode != DW_SUM_EXACT) {
         // reference-literal sequential sum over the span
         auto TS = [&](int64_t g) -> int64_t { return g < S ? p.ts[g] : p.span_hi; };
         auto W = [&](int64_t g) -> double { return p.w[g]; };
@@ -1512,7 +1760,7 @@ static AttrLayout attr_layout(int64_t S, const int64_t *sizes, const int32_t *so
     size_t off = 0;
     L.status = off; off += align_up(STATUS_BYTES);
     L.first = off; off += align_up(sizeof(int64_t) * (size_t)(ntiles + 1) * DW_MAX_SETS);
-    L.tile_sum = off; off += align_up(8 * (size_t)(ntiles + 1));
+    L.tile_sum = off; off += align_up(16 * (size_t)(ntiles + 1));
     L.prefix = off; off += align_up(16 * (size_t)(ntiles + 2));
     L.scan_part = off; off += align_up(16 * (size_t)(ceil_div(ntiles, SCAN_CHUNK) + 1));
     L.long_list = off; off += align_up(8 * (size_t)(nint + 1));
@@ -1594,8 +1842,9 @@ static int attribute_impl(const dw_signal_t *sig, dw_interval_set_t *sets, int n
     p.kind = sig->kind;
     p.nsets = nsets;
     p.validate_order = sig->validate_order;
+    p.sum_mode = sig->sum_mode == DW_SUM_EXACT ? DW_SUM_EXACT : DW_SUM_REFERENCE;
     p.first = (const int64_t *)(base + L.first);
-    p.tile_sum = (double *)(base + L.tile_sum);
+    p.tile_fx = (unsigned long long *)(base + L.tile_sum);
     p.scan_part = (unsigned long long *)(base + L.scan_part);
     p.prefix = (unsigned long long *)(base + L.prefix);
     p.long_list = (unsigned long long *)(base + L.long_list);
@@ -1648,8 +1897,19 @@ static int attribute_impl(const dw_signal_t *sig, dw_interval_set_t *sets, int n
     const size_t smem = ((sizeof(TileSmem) + 15) & ~(size_t)15) + GROUPS * sizeof(GroupSmem);
     const int sms = g_attr_sms > 0 && g_attr_sms < num_sms() ? g_attr_sms : num_sms();
     int grid = (int)std::min<int64_t>(p.ntiles, (int64_t)sms * CTAS_PER_SM);
+    const size_t smem_x = ((sizeof(TileSmem) + 15) & ~(size_t)15) + GROUPS * sizeof(GroupSmemX);
     timing_begin(stream);
-    if (sig->kind == DW_SIGNAL_STEP) {
+    if (p.sum_mode == DW_SUM_EXACT) {
+        if (sig->kind == DW_SIGNAL_STEP) {
+            cudaFuncSetAttribute(attribute_exact_kernel<DW_SIGNAL_STEP>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x);
+            attribute_exact_kernel<DW_SIGNAL_STEP><<<grid, KTHREADS, smem_x, stream>>>(p);
+        } else {
+            cudaFuncSetAttribute(attribute_exact_kernel<DW_SIGNAL_LINEAR>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x);
+            attribute_exact_kernel<DW_SIGNAL_LINEAR><<<grid, KTHREADS, smem_x, stream>>>(p);
+        }
+    } else if (sig->kind == DW_SIGNAL_STEP) {
         cudaFuncSetAttribute(attribute_tiles_kernel<DW_SIGNAL_STEP>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attribute_tiles_kernel<DW_SIGNAL_STEP><<<grid, KTHREADS, smem, stream>>>(p);

@@ -9,24 +9,40 @@ namespace dw {
 
 static thread_local int64_t g_launches = 0;
 static thread_local int g_timing = 0;
-static thread_local cudaEvent_t g_ev[2 * 64];
+constexpr int TIMING_RING = 1024;
+static thread_local cudaEvent_t g_ev[2 * TIMING_RING];
 static thread_local int g_nev = 0;
 static thread_local double g_pending_ms = 0.0;
+static thread_local int64_t g_timed = 0;  // launches timed since the last reset
 
 void count_launch(int n) { g_launches += n; }
 
+// fold the recorded event pairs into g_pending_ms (waits for the last one)
+static void timing_drain() {
+    for (int i = 0; i < g_nev; ++i) {
+        float ms = 0.f;
+        cudaEventSynchronize(g_ev[2 * i + 1]);
+        cudaEventElapsedTime(&ms, g_ev[2 * i], g_ev[2 * i + 1]);
+        g_pending_ms += ms;
+    }
+    g_nev = 0;
+}
+
 // Events around the attribution tile kernel (bench.py's roofline timing).
+// Every launch is timed: a full ring is drained (one host wait on an event
+// recorded ~1000 launches earlier) rather than dropping launches.
 void timing_begin(cudaStream_t s) {
     if (!g_timing) return;
-    if (g_nev >= 64) return;
+    if (g_nev >= TIMING_RING) timing_drain();
     cudaEvent_t *e = &g_ev[2 * g_nev];
     if (!e[0]) { cudaEventCreate(&e[0]); cudaEventCreate(&e[1]); }
     cudaEventRecord(e[0], s);
 }
 void timing_end(cudaStream_t s) {
-    if (!g_timing || g_nev >= 64) return;
+    if (!g_timing) return;
     cudaEventRecord(g_ev[2 * g_nev + 1], s);
     ++g_nev;
+    ++g_timed;
 }
 
 // Phase trace (diagnostic): with DWB200_TRACE set, trace_mark() records a
@@ -86,16 +102,16 @@ int dw_kernel_timing(int enable) {
 
 double dw_kernel_time_ms(int reset) {
     using namespace dw;
-    double total = g_pending_ms;
-    for (int i = 0; i < g_nev; ++i) {
-        float ms = 0.f;
-        cudaEventSynchronize(g_ev[2 * i + 1]);
-        cudaEventElapsedTime(&ms, g_ev[2 * i], g_ev[2 * i + 1]);
-        total += ms;
-    }
-    g_nev = 0;
-    g_pending_ms = reset ? 0.0 : total;
+    timing_drain();
+    const double total = g_pending_ms;
+    if (reset) g_pending_ms = 0.0;
     return total;
+}
+
+int64_t dw_kernel_timed_count(int reset) {
+    const int64_t n = dw::g_timed;
+    if (reset) dw::g_timed = 0;
+    return n;
 }
 
 void dw_trace_report(void) {

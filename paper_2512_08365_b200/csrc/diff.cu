@@ -989,6 +989,9 @@ static int join_impl(const dw_join_side_t *a, const dw_join_side_t *b, int64_t m
     JoinSideDev A{a->d_start, a->d_end, a->d_rank, a->d_joules, a->d_work};
     JoinSideDev B{b->d_start, b->d_end, b->d_rank, b->d_joules, b->d_work};
     FindCols o = cols_of(out);
+    // the matched count is this phase's own: a JoinPrep may be reused (other
+    // threshold or ledgers), so it restarts from zero on every call
+    cudaMemsetAsync(counters + 1, 0, sizeof(unsigned long long), s);
     if (na) {
         const uint2 *stage2 = (const uint2 *)(base + L.win_stage);
         const int64_t nwin = (na + WIN_OPS - 1) / WIN_OPS;

@@ -99,6 +99,19 @@ __host__ __device__ __forceinline__ double fx_to_double(i128 v, int scale) {
 
 __host__ __device__ __forceinline__ i128 q_term(double x) { return fx_from_double(x, FX_TERM_BITS); }
 
+// q_term for |x| < 2^23 (|x * 2^40| < 2^63) in two instructions: the scaling
+// by 2^40 is exact and cvt.rni rounds half to even, as fx_from_double does.
+constexpr double Q40_FAST_LIMIT = 8388608.0;  // 2^23 W*us
+__device__ __forceinline__ bool q40_fast(double x, long long &q) {
+    if (!(fabs(x) < Q40_FAST_LIMIT)) return false;
+    q = __double2ll_rn(__dmul_rn(x, 1099511627776.0));
+    return true;
+}
+__device__ __forceinline__ i128 q40(double x) {
+    long long q;
+    return q40_fast(x, q) ? (i128)q : q_term(x);
+}
+
 __host__ __device__ __forceinline__ double term_fx_to_joules(i128 v) {
     return fx_to_double(v, FX_TERM_BITS) / US_PER_S;
 }

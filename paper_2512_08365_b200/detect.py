@@ -26,7 +26,7 @@ import torch
 
 from . import _native
 from .energy import EnergyLedger
-from .columns import TraceColumns
+from .columns import TraceColumns, synthetic_id, synthetic_ids
 from .tensor_equiv import boundary_rel_diff
 
 DEFAULT_THRESHOLD = 0.10
@@ -146,7 +146,7 @@ def _op_columns(trace, ledger, dev):
     """(op index by id, joules, start, end) of one trace, joules in the ledger's
     op order (which is the trace's op order for ledgers built here)."""
     cols = TraceColumns.from_trace(trace)
-    ids = cols.op_ids if cols.op_ids is not None else [f"op{i}" for i in range(cols.n_ops)]
+    ids = cols.op_ids if cols.op_ids is not None else synthetic_ids("op", cols.n_ops)
     index = {o: i for i, o in enumerate(ids)}
     jt = ledger.operator_tensor() if isinstance(ledger, EnergyLedger) else None
     if jt is None or jt.numel() != len(ids) or list(ledger.per_operator) != list(ids):

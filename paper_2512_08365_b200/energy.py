@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .columns import TraceColumns
+from .columns import TraceColumns, synthetic_id, synthetic_ids
 from .trace_model import OperatorEvent, PowerSample, Trace
 
 US_PER_S = 1_000_000
@@ -180,11 +180,27 @@ class PowerSignal:
             self._dev[key] = (_to_dev(self._ts, torch.int64, dev), _to_dev(self._w, torch.float64, dev))
         return self._dev[key]
 
-    def _c_signal(self, validate_order=False) -> tuple:
+    def _c_signal(self, validate_order=False, summation: str = "reference") -> tuple:
         ts_d, w_d = self._device()
         sig = _native.Signal(ts_d.data_ptr(), w_d.data_ptr(), int(ts_d.numel()),
-                             int(self._span_hi), int(self._kind), 1 if validate_order else 0)
+                             int(self._span_hi), int(self._kind), 1 if validate_order else 0,
+                             _sum_mode(summation), 0)
         return sig, (ts_d, w_d)
+
+
+SUMMATIONS = ("reference", "exact")
+
+
+def _sum_mode(summation: str) -> int:
+    """dw_signal_t.sum_mode of a summation name (include/dwb200.h):
+    "reference" -- the reference's own sequential fp64 sum for intervals of
+    up to DW_DIRECT_MAX pieces (bit-identical to energy.integrate), exact
+    fixed point beyond; "exact" -- every interval as the exact sum of its
+    pieces rounded to 2^-40 W*us, rounded once (deterministic, independent of
+    how the device groups the pieces, within a few ulps of the reference)."""
+    if summation not in SUMMATIONS:
+        raise ValueError(f"unknown summation {summation!r}")
+    return _native.SUM_EXACT if summation == "exact" else _native.SUM_REFERENCE
 
 
 def _host(a):
@@ -229,9 +245,10 @@ def _raise_interval_error(lo: int, hi: int, span: tuple[int, int]):
     raise SignalError(f"interval [{lo},{hi}] outside signal span [{span[0]},{span[1]}]")
 
 
-def integrate_many(signal: PowerSignal, lo, hi) -> torch.Tensor:
+def integrate_many(signal: PowerSignal, lo, hi, summation: str = "reference") -> torch.Tensor:
     """Joules for many intervals at once (device tensor out).  Errors follow
-    the reference: the first invalid interval raises SignalError."""
+    the reference: the first invalid interval raises SignalError.
+    ``summation``: see ``_sum_mode``."""
     if signal._kind is None or len(signal) == 0:
         raise SignalError("empty power signal")
     dev = _native.device()
@@ -241,7 +258,7 @@ def integrate_many(signal: PowerSignal, lo, hi) -> torch.Tensor:
     sorted_ = bool(lo_d.numel() < 2 or bool((lo_d[1:] >= lo_d[:-1]).all().item()))
     iset = _native.IntervalSet(_native.ptr(lo_d), _native.ptr(hi_d), lo_d.numel(),
                                _native.ptr(out), 1 if sorted_ else 0, 0)
-    csig, keep = signal._c_signal()
+    csig, keep = signal._c_signal(summation=summation)
     sizes = (ctypes.c_int64 * 1)(lo_d.numel())
     L = _native.lib()
     nbytes = L.dw_attribute_workspace_size(csig.n, sizes, 1)
@@ -393,7 +410,7 @@ class JoulesView(Mapping):
         return self._host
 
     def _id(self, i: int) -> str:
-        return self._ids[i] if self._ids is not None else f"{self._prefix}{i}"
+        return self._ids[i] if self._ids is not None else synthetic_id(self._prefix, i, len(self))
 
     def _idx(self):
         if self._index is None:
@@ -401,7 +418,7 @@ class JoulesView(Mapping):
             if self._ids is not None:
                 self._index = {k: i for i, k in enumerate(self._ids)}
             else:
-                self._index = {f"{self._prefix}{i}": i for i in range(n)}
+                self._index = {k: i for i, k in enumerate(synthetic_ids(self._prefix, n))}
         return self._index
 
     def __getitem__(self, key):
@@ -410,7 +427,7 @@ class JoulesView(Mapping):
     def __iter__(self):
         if self._ids is not None:
             return iter(self._ids)
-        return (f"{self._prefix}{i}" for i in range(len(self)))
+        return iter(synthetic_ids(self._prefix, len(self)))
 
     def __len__(self):
         return int(self._dev.numel())
@@ -460,7 +477,7 @@ class EnergyLedger:
         return getattr(self.per_kernel, "tensor", None)
 
 
-def _run_ledger(cols: TraceColumns, sig: PowerSignal, validate_order: bool):
+def _run_ledger(cols: TraceColumns, sig: PowerSignal, validate_order: bool, summation: str = "reference"):
     """dw_ledger on the device; returns (per_op, per_k, total, op_total, idle)."""
     dev = _native.device()
     L = _native.lib()
@@ -472,7 +489,7 @@ def _run_ledger(cols: TraceColumns, sig: PowerSignal, validate_order: bool):
                               _native.ptr(per_op), 1 if cols.ops_sorted else 0, 0)
     kers = _native.IntervalSet(_native.ptr(k_s), _native.ptr(k_e), cols.n_kernels,
                                _native.ptr(per_k), 1 if cols.kernels_sorted else 0, 0)
-    csig, keep = sig._c_signal(validate_order)
+    csig, keep = sig._c_signal(validate_order, summation)
     sizes = (ctypes.c_int64 * 2)(cols.n_ops, cols.n_kernels)
     nbytes = L.dw_attribute_workspace_size(csig.n, sizes, 2)
     ws = _native.Workspace.get(nbytes)
@@ -558,6 +575,28 @@ def _replay_device(truth: PowerSignal, starts, ends, repeat, period_us, delay_us
     return watts, joules
 
 
+def _kernel_owners(cols: TraceColumns) -> torch.Tensor:
+    """Owning operator of every kernel (device int64).  From ``k_op`` when the
+    columns carry it; otherwise (packed columns ship none) by containment,
+    which is exact when operators are sorted and pairwise disjoint and
+    kernels sorted, since every kernel lies inside its owner (the trace
+    validation, trace_model.py:529-540).  Anything else raises."""
+    if cols.k_op is not None:
+        return cols.device("k_op").to(torch.int64)
+    s, e = cols.device("op_start"), cols.device("op_end")
+    ks, ke = cols.device("k_start"), cols.device("k_end")
+    ok = bool(s.numel()) and cols.ops_sorted and cols.kernels_sorted and (
+        s.numel() < 2 or bool((s[1:] >= e[:-1]).all().item()))
+    if ok:
+        own = torch.searchsorted(s, ks, right=True) - 1
+        oc = own.clamp(min=0)
+        ok = bool(((own >= 0) & (ks >= s[oc]) & (ke <= e[oc])).all().item())
+    if not ok:
+        raise ValueError("replay needs each kernel's operator: the columns carry no k_op and the "
+                         "kernels are not contained in sorted, disjoint operators")
+    return own
+
+
 def _replay_checks(cols: TraceColumns, repeat: int, first_op: int = 0) -> None:
     """replay_estimate's argument errors in build_ledger's op order
     (energy.py:227-230): an op without kernels, then repeat < 1.  The
@@ -567,18 +606,18 @@ def _replay_checks(cols: TraceColumns, repeat: int, first_op: int = 0) -> None:
     if n > 0:
         dev = _native.device()
         has = torch.zeros(cols.n_ops, dtype=torch.bool, device=dev)
-        if cols.n_kernels and cols.k_op is not None:
-            has[cols.device("k_op").to(torch.int64)] = True
+        if cols.n_kernels:
+            has[_kernel_owners(cols)] = True
         miss = ~has[first_op:]
         if bool(miss.any().item()):
             first_missing = int(torch.argmax(miss.to(torch.int8)).item()) + first_op
     if first_missing == first_op:
-        oid = cols.op_ids[first_missing] if cols.op_ids is not None else f"op{first_missing}"
+        oid = cols.op_ids[first_missing] if cols.op_ids is not None else synthetic_id("op", first_missing, cols.n_ops)
         raise SignalError(f"operator {oid!r} launched no kernels; nothing to replay")
     if repeat < 1:
         raise SignalError("repeat must be >= 1")
     if first_missing is not None:
-        oid = cols.op_ids[first_missing] if cols.op_ids is not None else f"op{first_missing}"
+        oid = cols.op_ids[first_missing] if cols.op_ids is not None else synthetic_id("op", first_missing, cols.n_ops)
         raise SignalError(f"operator {oid!r} launched no kernels; nothing to replay")
 
 
@@ -591,7 +630,7 @@ def _replay_ledger(cols: TraceColumns, truth: PowerSignal, repeat, period_us, de
     tsig = PowerSignal.from_columns(cols.device("ts"), cols.device("watts"), truth._span_hi, "step")
     watts, per_op = _replay_device(tsig, cols.device("op_start"), cols.device("op_end"), repeat, period_us,
                                    delay_us, seed)
-    k_op = cols.device("k_op").to(torch.int64) if cols.n_kernels else None
+    k_op = _kernel_owners(cols) if cols.n_kernels else None
     kdur = (cols.device("k_end") - cols.device("k_start")).to(torch.float64)
     # tensor / tensor: an IEEE division per element (a scalar divisor may be
     # turned into a reciprocal multiply)
@@ -625,7 +664,7 @@ def replay_estimate(trace, op_id: str, repeat: int = DEFAULT_REPLAY_REPEAT,
     """Estimate one operator's steady power by replaying it back to back
     (energy.py:208-256) -- the replay kernel on one operator."""
     cols = TraceColumns.from_trace(trace)
-    ids = list(cols.op_ids) if cols.op_ids is not None else [f"op{i}" for i in range(cols.n_ops)]
+    ids = list(cols.op_ids) if cols.op_ids is not None else synthetic_ids("op", cols.n_ops)
     try:
         i = ids.index(op_id)
     except ValueError:
@@ -682,8 +721,15 @@ def _fx_sum(x: torch.Tensor) -> float:
 def build_ledger(trace, method: str = "ground_truth",
                  period_us: int = DEFAULT_SAMPLER_PERIOD_US,
                  delay_us: int = DEFAULT_SAMPLER_DELAY_US, repeat: int = DEFAULT_REPLAY_REPEAT,
-                 seed: int = 0, validate_order: bool = False, overlap: str = "compat") -> EnergyLedger:
+                 seed: int = 0, validate_order: bool = False, overlap: str = "compat",
+                 summation: str = "reference") -> EnergyLedger:
     """Attribute energy to kernels and operators (energy.py:280-331).
+
+    ``summation="reference"`` (default) sums each interval's pieces in the
+    reference's order (bit-identical to energy.integrate up to DW_DIRECT_MAX
+    pieces); ``summation="exact"`` sums them exactly in fixed point and
+    rounds once -- the scale path's mode (pipeline.analyze, bench.py), within
+    a few ulps of the reference and bit-identical to the oracle's MODE_EXACT.
 
     ``overlap="compat"`` (default) is the reference: every interval gets the
     full signal over its span.  ``overlap="split"`` divides the power among
@@ -698,6 +744,7 @@ def build_ledger(trace, method: str = "ground_truth",
         raise ValueError(f"unknown energy method {method!r}")
     if overlap not in ("compat", "split"):
         raise ValueError(f"unknown overlap mode {overlap!r}")
+    _sum_mode(summation)
     cols = TraceColumns.from_trace(trace)
     if method == "samples":
         if cols.n_power == 0:
@@ -706,7 +753,7 @@ def build_ledger(trace, method: str = "ground_truth",
         first, last = cols._first_last_ts()
         signal = PowerSignal.from_columns(cols.device("ts"), cols.device("watts"), kind="linear")
         signal._span_hi = last
-        per_op, per_k, st = _run_ledger(cols, signal, validate_order)
+        per_op, per_k, st = _run_ledger(cols, signal, validate_order, summation)
         _raise_ledger_errors(cols, st, signal.span())
         if overlap == "split":
             return _split_ledger(method, cols, signal, st)
@@ -723,7 +770,7 @@ def build_ledger(trace, method: str = "ground_truth",
                                           truth._span_hi, "step")
     else:
         signal = sampled_view(cols, period_us, delay_us, seed)
-    per_op, per_k, st = _run_ledger(cols, signal, validate_order)
+    per_op, per_k, st = _run_ledger(cols, signal, validate_order, summation)
     _raise_ledger_errors(cols, st, truth.span())
     if overlap == "split":
         return _split_ledger(method, cols, signal, st)

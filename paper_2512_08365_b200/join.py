@@ -31,7 +31,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .columns import TraceColumns
+from .columns import TraceColumns, synthetic_id, synthetic_ids
 from .detect import (DEFAULT_THRESHOLD, SIDES, VERDICT_WASTE, VERDICTS, FindingColumns,
                      Report, SubgraphPair, WasteFinding, judge, rank_order)
 from .energy import EnergyLedger
@@ -83,6 +83,27 @@ def _ranks(cols: TraceColumns, dev) -> Optional[torch.Tensor]:
     rank[np.asarray(order, dtype=np.int64)] = np.arange(len(order), dtype=np.int64)
     cols.op_rank = rank
     return cols.device("op_rank")
+
+
+def _ledger_joules(cols: TraceColumns, led: EnergyLedger, dev) -> torch.Tensor:
+    """The ledger's operator joules in ``cols``' operator order.  The device
+    column is used as is only when it belongs to these columns (same length,
+    same op ids in the same order); otherwise it is rebuilt by id, so a ledger
+    of other columns can never be read out of bounds or misattributed."""
+    j = led.operator_tensor()
+    per = led.per_operator
+    ids = cols.op_ids
+    if j is not None and j.numel() == cols.n_ops:
+        own = getattr(per, "_ids", None)
+        if ids is None and own is None:
+            return j
+        if ids is not None and own is not None and (own is ids or list(own) == list(ids)):
+            return j
+    if ids is None:
+        ids = synthetic_ids("op", cols.n_ops)
+    if len(per) != len(ids):
+        raise ValueError(f"ledger has {len(per)} operators, the trace {len(ids)}")
+    return torch.tensor([float(per[o]) for o in ids], dtype=torch.float64, device=dev)
 
 
 @dataclass
@@ -167,7 +188,7 @@ class JoinDiff:
         else:
             h = {"ratio": fcols[2], "wasted": fcols[3], "verdict": icols[4], "side": icols[5],
                  "informational": icols[6]}
-        name = lambda ids, i, p: (ids[i] if ids is not None else f"{p}{i}")  # noqa: E731
+        name = lambda ids, i, n: (ids[i] if ids is not None else synthetic_id("op", i, n))  # noqa: E731
         cats = ["unknown"] * len(ia)
         waste = np.nonzero(h["verdict"] == VERDICTS.index(VERDICT_WASTE))[0]
         if classify and waste.size:
@@ -178,8 +199,8 @@ class JoinDiff:
                 cats[r] = c
         out = []
         for r in range(len(ia)):
-            na = (name(cols_a.op_ids, int(ia[r]), "a"),) if ia[r] >= 0 else ()
-            nb = (name(cols_b.op_ids, int(ib[r]), "b"),) if ib[r] >= 0 else ()
+            na = (name(cols_a.op_ids, int(ia[r]), cols_a.n_ops),) if ia[r] >= 0 else ()
+            nb = (name(cols_b.op_ids, int(ib[r]), cols_b.n_ops),) if ib[r] >= 0 else ()
             out.append(WasteFinding(
                 pair=SubgraphPair(nodes_a=na, nodes_b=nb), energy_a=float(ea[r]),
                 energy_b=float(eb[r]), energy_ratio=float(h["ratio"][r]),
@@ -260,16 +281,15 @@ def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
     ca, cb = prep.ca, prep.cb
     sides, keep = [], []
     for cols, trace, led, work in ((ca, trace_a, ledger_a, work_a), (cb, trace_b, ledger_b, work_b)):
-        j = led.operator_tensor()
-        if j is None:
-            ids = cols.op_ids
-            j = torch.tensor([float(led.per_operator[o]) for o in ids], dtype=torch.float64, device=dev)
+        j = _ledger_joules(cols, led, dev)
         w = None
         if work is not None:
             w = work if isinstance(work, torch.Tensor) else torch.as_tensor(work, dtype=torch.float64)
-            w = w.to(dev)
+            w = w.to(device=dev, dtype=torch.float64).reshape(-1)
         elif cols.op_work is not None:
             w = cols.device("op_work")
+        if w is not None and w.numel() != cols.n_ops:
+            raise ValueError(f"work column has {w.numel()} entries for {cols.n_ops} operators")
         rank = _ranks(cols, dev) if cols is ca else None
         side, kk = _side(cols, trace, j, w, rank, dev)
         sides.append(side)

@@ -38,9 +38,13 @@ def _decode_stream() -> "torch.cuda.Stream":
 
 
 def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAULT_THRESHOLD,
-            k: int = 100, *, lean: bool = True, copy_stream: "torch.cuda.Stream | None" = None
-            ) -> Analysis:
+            k: int = 100, *, lean: bool = True, copy_stream: "torch.cuda.Stream | None" = None,
+            summation: str = "exact") -> Analysis:
     """Ledgers for both traces, the signature-join diff and the top-k report.
+
+    ``summation`` (default "exact"): how the ledgers sum each interval's
+    pieces (energy.build_ledger) -- the exact fixed-point sum, the scale
+    path's definition; "reference" for the reference's sequential order.
 
     ``lean`` (default): the join writes only each finding's ranking key (the
     top-k rows' ratio / verdict / side / informational / wasted are derived
@@ -69,11 +73,11 @@ def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAUL
         # (by then A's attribution and the pairing are done), so only the last
         # column's decode trails the last byte
         cb.prefetch(copy_stream, names=("ts", "watts", "k_start", "k_end"), decode_stream=_decode_stream())
-    la = build_ledger(ca, method=method)
+    la = build_ledger(ca, method=method, summation=summation)
     if copy_stream is not None:
         torch.cuda.current_stream().wait_event(sig_ready)
         prep = join_prepare(ca, cb)
-    lb = build_ledger(cb, method=method)
+    lb = build_ledger(cb, method=method, summation=summation)
     jd = join_diff(ca, cb, la, lb, threshold, k, full_columns=not lean, epw=not lean, prep=prep,
                    columns=FindingColumns.KEYS if lean else None)
     top = jd.top_findings(ca, cb)

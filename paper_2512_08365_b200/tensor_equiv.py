@@ -247,16 +247,11 @@ def spectrum_distance(a: Spectrum, b: Spectrum) -> float:
 
 
 def _distances(small: Sequence[Spectrum], large: Sequence[Spectrum]) -> np.ndarray:
-    w = max([len(s.singulars) for s in small] + [len(s.singulars) for s in large] + [1])
-    S = np.zeros((len(small), w))
-    Lg = np.zeros((len(large), w))
-    for i, s in enumerate(small):
-        S[i, :len(s.singulars)] = s.singulars
-    for j, s in enumerate(large):
-        Lg[j, :len(s.singulars)] = s.singulars
-    ns, nl = np.sqrt((S * S).sum(1)), np.sqrt((Lg * Lg).sum(1))
-    d = np.sqrt(((S[:, None, :] - Lg[None, :, :]) ** 2).sum(2))
-    return d / np.maximum(np.minimum(ns[:, None], nl[None, :]), _NORM_FLOOR)
+    """The reference's distance matrix (tensor_equiv.py:225-226): every entry
+    through spectrum_distance, i.e. the same sequential arithmetic and the same
+    norms, so a score at the epsilon / 1% boundary decides as it does there."""
+    return np.array([[spectrum_distance(s, l) for l in large] for s in small], dtype=np.float64).reshape(
+        len(small), len(large))
 
 
 def _matching_ok(dist: np.ndarray, limit: float) -> bool:
@@ -320,7 +315,9 @@ def tensors_equivalent(a, b, epsilon: float = DEFAULT_EPSILON, set_a: Optional[I
     xa, xb = _arr(a), _arr(b)
     if xa.size != xb.size:
         return False, math.inf
-    na, nb = float(np.sqrt(np.dot(xa.ravel(), xa.ravel()))), float(np.sqrt(np.dot(xb.ravel(), xb.ravel())))
+    # the reference's Frobenius norms, same numpy reduction (tensor_equiv.py:275-276)
+    na = float(np.sqrt(np.einsum("i,i->", xa.ravel(), xa.ravel())))
+    nb = float(np.sqrt(np.einsum("i,i->", xb.ravel(), xb.ravel())))
     nd = abs(na - nb) / max(min(na, nb), _NORM_FLOOR)
     if nd > epsilon:
         return False, math.inf

@@ -224,3 +224,156 @@ def test_config1_golden():
         lin = build_ledger(cols, method="sampled", period_us=1_000, delay_us=0)
         np.testing.assert_array_equal(lin.per_operator.array()[:500], sc[f"s1_{side}_per_op500"])
         np.testing.assert_array_equal(lin.per_kernel.array()[:500], sc[f"s1_{side}_per_k500"])
+
+
+# ------------------------------------------------- summation="exact" (DW_SUM_EXACT)
+# Every interval is the exact sum of its pieces rounded to 2^-40 W*us, rounded
+# once: bit-identical to the oracle's MODE_EXACT, within a few ulps of the
+# reference's sequential sums (tolerance 1e-12 relative here; the north star
+# asks 1e-6).
+
+
+@pytest.mark.parametrize("seed,S,n,max_len", [(11, 300_000, 200_000, 3000), (12, 2_000_001, 500_000, 40_000),
+                                              (13, 5000, 100_000, 100)])
+def test_exact_step_vs_oracle(seed, S, n, max_len):
+    ts, w, span_hi, lo, hi = _random_case(seed, S, n, max_len)
+    sig = PowerSignal.from_columns(ts, w, span_hi, "step")
+    got = E.integrate_many(sig, lo, hi, summation="exact").cpu().numpy()
+    np.testing.assert_array_equal(got, oracle.integrate_step(ts, w, span_hi, lo, hi, oracle.MODE_EXACT))
+    ref = oracle.integrate_step(ts, w, span_hi, lo, hi, oracle.MODE_REFERENCE)
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-300)
+
+
+@pytest.mark.parametrize("seed,S,n,max_len", [(14, 300_000, 200_000, 3000), (15, 1_000_003, 300_000, 20_000)])
+def test_exact_linear_vs_oracle(seed, S, n, max_len):
+    ts, w, span_hi, lo, hi = _random_case(seed, S, n, max_len)
+    hi = np.minimum(hi, ts[-1])
+    lo = np.minimum(lo, hi)
+    sig = PowerSignal.from_columns(ts, w, kind="linear")
+    got = E.integrate_many(sig, lo, hi, summation="exact").cpu().numpy()
+    np.testing.assert_array_equal(got, oracle.integrate_linear(ts, w, lo, hi, oracle.MODE_EXACT))
+    ref = oracle.integrate_linear(ts, w, lo, hi, oracle.MODE_REFERENCE)
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-300)
+
+
+def test_exact_golden_vectors(golden_step, golden_linear):
+    for ts, w, span_hi, lo, hi, ref in _signals(golden_step, True):
+        got = E.integrate_many(PowerSignal.from_columns(ts, w, span_hi, "step"), lo, hi, summation="exact")
+        got = got.cpu().numpy()
+        np.testing.assert_array_equal(got, oracle.integrate_step(ts, w, span_hi, lo, hi, oracle.MODE_EXACT))
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-300)
+    for ts, w, _, lo, hi, ref in _signals(golden_linear, False):
+        got = E.integrate_many(PowerSignal.from_columns(ts, w, kind="linear"), lo, hi, summation="exact")
+        got = got.cpu().numpy()
+        np.testing.assert_array_equal(got, oracle.integrate_linear(ts, w, lo, hi, oracle.MODE_EXACT))
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-300)
+
+
+@pytest.mark.parametrize("name", ["preset_tf32_misconfig", "preset_join_redundant", "fuzz_00", "cfg1"])
+def test_exact_ledger_golden(name):
+    sc = load_scenario(name)
+    for side in ("a", "b"):
+        cols = _cols(sc, side)
+        led = build_ledger(cols, summation="exact")
+        np.testing.assert_allclose(led.per_operator.array(), sc[f"gt_{side}_per_op"], rtol=1e-12, atol=1e-300)
+        np.testing.assert_allclose(led.per_kernel.array(), sc[f"gt_{side}_per_k"], rtol=1e-12, atol=1e-300)
+        ts, w = cols.host("ts"), cols.host("watts")
+        span_hi = cols.signal_span()[1]
+        po, pk, total, idle = oracle.ledger("step", ts, w, span_hi, cols.host("op_start"), cols.host("op_end"),
+                                            cols.host("k_start"), cols.host("k_end"), oracle.MODE_EXACT)
+        np.testing.assert_array_equal(led.per_operator.array(), po)
+        np.testing.assert_array_equal(led.per_kernel.array(), pk)
+        assert led.total_joules == total
+        assert led.idle_joules == idle
+        assert led.total_joules == pytest.approx(sc[f"gt_{side}_total_idle"][0], rel=1e-12)
+
+
+def _wide_case(seed, kind):
+    """Timestamps with gaps of more than 2^32 us (tile windows too wide for
+    32-bit offsets: the kernels' int64 branch) between dense runs."""
+    rng = np.random.default_rng(seed)
+    gaps = rng.integers(1, 400, size=60_000)
+    gaps[rng.integers(0, gaps.size, size=25)] = (1 << 32) + rng.integers(0, 1 << 20, size=25)
+    ts = np.cumsum(gaps).astype(np.int64)
+    w = rng.uniform(0.001, 2.0, size=ts.size)  # small watts: long gaps stay within the term range
+    span_hi = int(ts[-1]) + 7
+    top = span_hi if kind == "step" else int(ts[-1])
+    lo = np.sort(rng.integers(ts[0], top, size=20_000))
+    hi = np.minimum(lo + rng.integers(0, 3000, size=lo.size), top)
+    # some intervals across a wide gap
+    k = rng.integers(0, ts.size - 2, size=200)
+    lo2, hi2 = ts[k] + 1, np.minimum(ts[k + 2] - 1, top)
+    lo = np.concatenate([lo, np.minimum(lo2, hi2)])
+    hi = np.concatenate([hi, hi2])
+    o = np.argsort(lo, kind="stable")
+    return ts, w, span_hi, lo[o], hi[o]
+
+
+@pytest.mark.parametrize("summation,mode", [("reference", oracle.MODE_DEVICE), ("exact", oracle.MODE_EXACT)])
+@pytest.mark.parametrize("kind", ["step", "linear"])
+def test_wide_windows(kind, summation, mode):
+    """Windows spanning >= 2^32 us take the int64 path (attribute.cu 'wide')."""
+    ts, w, span_hi, lo, hi = _wide_case(31, kind)
+    if kind == "step":
+        got = E.integrate_many(PowerSignal.from_columns(ts, w, span_hi, "step"), lo, hi, summation=summation)
+        want = oracle.integrate_step(ts, w, span_hi, lo, hi, mode)
+        ref = oracle.integrate_step(ts, w, span_hi, lo, hi, oracle.MODE_REFERENCE)
+    else:
+        got = E.integrate_many(PowerSignal.from_columns(ts, w, kind="linear"), lo, hi, summation=summation)
+        want = oracle.integrate_linear(ts, w, lo, hi, mode)
+        ref = oracle.integrate_linear(ts, w, lo, hi, oracle.MODE_REFERENCE)
+    got = got.cpu().numpy()
+    np.testing.assert_array_equal(got, want)
+    np.testing.assert_allclose(got, ref, rtol=1e-11, atol=1e-300)
+
+
+@pytest.mark.parametrize("kind", ["step", "linear"])
+def test_exact_huge_pieces_take_the_long_path(kind):
+    """Pieces above 2^23 W*us (beyond the two-instruction rounding) and
+    intervals whose bound exceeds the 64-bit window prefix go through the
+    int128 long-interval kernel: still the oracle's MODE_EXACT bit for bit."""
+    rng = np.random.default_rng(5)
+    ts = np.cumsum(rng.integers(1, 50_000, size=40_000)).astype(np.int64)
+    w = rng.uniform(1.0, 1500.0, size=ts.size)
+    span_hi = int(ts[-1]) + 3
+    top = span_hi if kind == "step" else int(ts[-1])
+    lo = np.sort(rng.integers(ts[0], top, size=30_000))
+    hi = np.minimum(lo + rng.integers(0, 200_000, size=lo.size), top)
+    if kind == "step":
+        got = E.integrate_many(PowerSignal.from_columns(ts, w, span_hi, "step"), lo, hi, summation="exact")
+        want = oracle.integrate_step(ts, w, span_hi, lo, hi, oracle.MODE_EXACT)
+    else:
+        got = E.integrate_many(PowerSignal.from_columns(ts, w, kind="linear"), lo, hi, summation="exact")
+        want = oracle.integrate_linear(ts, w, lo, hi, oracle.MODE_EXACT)
+    np.testing.assert_array_equal(got.cpu().numpy(), want)
+
+
+def test_exact_ledger_total_and_idle():
+    ts, w, span_hi, lo, hi = _random_case(18, 200_000, 20_000, 500)
+    cols = TraceColumns.from_arrays(ts, w, lo, hi, trace_end=span_hi - 1)
+    led = build_ledger(cols, summation="exact")
+    sh = cols.signal_span()[1]
+    assert led.total_joules == oracle.total_device("step", ts, w, sh, exact=True)
+    assert led.operator_total() == oracle.fx_sum(led.per_operator.array())
+    assert led.idle_joules == max(led.total_joules - led.operator_total(), 0.0)
+    ref = build_ledger(cols)  # the long span total is the same exact sum in both modes
+    assert led.total_joules == ref.total_joules
+
+
+def test_mean_power_matches_reference_rule():
+    """mean_power (energy.py:133-137): integrate * 1e6 / (hi - lo); 0 for an
+    empty or reversed interval; errors as integrate."""
+    sig = PowerSignal(segments=((0, 5000, 100.0), (5000, 10000, 300.0)))
+    assert E.mean_power(sig, (0, 10000)) == 2.0 * 1e6 / 10000
+    assert E.mean_power(sig, (0, 5000)) == 100.0
+    assert E.mean_power(sig, (7000, 7000)) == 0.0
+    assert E.mean_power(sig, (7000, 6000)) == 0.0
+    with pytest.raises(SignalError, match="outside"):
+        E.mean_power(sig, (0, 10001))
+    rng = np.random.default_rng(3)
+    ts = np.cumsum(rng.integers(1, 300, size=5000)).astype(np.int64)
+    w = rng.uniform(50, 700, size=ts.size)
+    lin = PowerSignal.from_columns(ts, w, kind="linear")
+    for lo, hi in ((int(ts[10]) + 3, int(ts[400]) - 1), (int(ts[0]), int(ts[-1]))):
+        j = oracle.integrate_linear(ts, w, [lo], [hi], oracle.MODE_DEVICE)[0]
+        assert E.mean_power(lin, (lo, hi)) == j * 1e6 / (hi - lo)
