@@ -29,6 +29,7 @@
 //                         partial first/last tiles + prefix difference
 //   K5 fx_sum / finalize  operator_total (exact sum) and total / idle
 #include <algorithm>
+#include <type_traits>
 
 #include <cub/cub.cuh>
 
@@ -218,16 +219,20 @@ struct StageMeta {
     int32_t cnt;                // samples in the window
 };
 
-struct __align__(16) TileSmem {  // the stage ring, shared by the producer and every group
-    int64_t ts[STAGES][WIN];
-    double w[STAGES][WIN];
-    int64_t iv_lo[STAGES][IV_POOL];
-    int64_t iv_hi[STAGES][IV_POOL];
-    StageMeta meta[STAGES];
-    uint64_t full[STAGES];
-    uint64_t empty[STAGES];
+template <int NST, int NWIN>
+struct __align__(16) TileSmemT {  // the stage ring, shared by the producer and every group
+    static constexpr int kStages = NST;
+    static constexpr int kWin = NWIN;
+    int64_t ts[NST][NWIN];
+    double w[NST][NWIN];
+    int64_t iv_lo[NST][IV_POOL];
+    int64_t iv_hi[NST][IV_POOL];
+    StageMeta meta[NST];
+    uint64_t full[NST];
+    uint64_t empty[NST];
     int claim;                  // next position of this CTA's tile sequence to hand to a group
 };
+using TileSmem = TileSmemT<STAGES, WIN>;
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -238,10 +243,11 @@ __device__ __forceinline__ void consumer_sync(int g) {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(ATTR_THREADS) : "memory");
 }
 
+template <int HALO = DIRECT>
 __device__ __forceinline__ void tile_window(int64_t tile, int64_t S, int64_t &wb, int64_t &we) {
     wb = tile * TILE - 2;
     if (wb < 0) wb = 0;
-    we = (tile + 1) * TILE + DIRECT + 2;  // keeps the steady-state window even (16-B TMA)
+    we = (tile + 1) * TILE + HALO + 2;  // keeps the steady-state window even (16-B TMA)
     if (we > S) we = S;
 }
 
@@ -577,20 +583,20 @@ __device__ __forceinline__ int find_le(const uint32_t *ts, int r0, int r1, uint3
 // pieces and interior count.  Returns false when it spans more than DIRECT
 // pieces (the fixed-point path takes it).  Branch-free apart from the
 // search fallbacks.
-template <int KIND>
+template <int KIND, int CAP = DIRECT>
 __device__ __forceinline__ bool phase1_item(const uint32_t *ts, const double *w, int r0, int r1, int cnt_win,
                                             uint32_t lo, uint32_t hi, bool lo_first, bool lo_last,
                                             bool hi_first, bool hi_last, const TileCtx &cx, double &F0,
                                             double &L, int &s, int &cnt, int &last) {
     const int a = find_le(ts, r0, r1, lo, ts[r0], r0, cx.scale);
-    const int lim = min(a + DIRECT + 1, cnt_win);
+    const int lim = min(a + CAP + 1, cnt_win);
     const uint32_t ta = ts[a], ta1 = ts[a + 1];
     s = a + 1;
     if (KIND == DW_SIGNAL_STEP) {
         // energy.py:99-104, zero-overlap segments skipped; b = last segment start < hi
         const int b = hi > lo ? find_le(ts, a, lim, hi - 1, ts[a], a, cx.scale) : a;
         const int n = hi > lo ? b - a + 1 : 0;  // segments
-        if (n > DIRECT) return false;
+        if (n > CAP) return false;
         const double wa = w[a];
         F0 = n == 0 ? 0.0 : __dmul_rn(wa, (double)((n == 1 ? hi : ta1) - lo));
         L = __dmul_rn(w[b], (double)(hi - ts[b]));
@@ -601,7 +607,7 @@ __device__ __forceinline__ bool phase1_item(const uint32_t *ts, const double *w,
         // energy.py:108-130: points [lo] + {ts in (lo, hi)} + [hi]; b = last sample < hi
         const int b = ta < hi ? find_le(ts, a, lim, hi - 1, ta, a, cx.scale) : a - 1;
         const int m = b - a;  // -1 only when hi == lo == ts[a]
-        if (m + 1 > DIRECT) return false;  // pieces = m + 1
+        if (m + 1 > CAP) return false;  // pieces = m + 1
         // v(lo), v(hi): first bracketing pair (energy.py:115-124)
         const int il = ta == lo && a > 0 ? a - 1 : a;  // (a == 0: lo is the first sample, vlo = w0)
         const double wl0 = w[il], wl1 = w[il + 1];
@@ -755,7 +761,9 @@ __device__ void tile_intervals_two_pass(const AttrParams &p, TileSmem &sm, Group
 // 32 of its tiles are fetched at once (one global-load latency per 32 tiles)
 // and handed out by shuffles; lane 0 waits for the slot, lays out the stage
 // and arms the barrier, and the bulk copies are issued by separate lanes.
-__device__ __forceinline__ void producer(const AttrParams &p, TileSmem &sm, int64_t span_hi, int pw) {
+template <typename SM, int HALO = DIRECT>
+__device__ __forceinline__ void producer(const AttrParams &p, SM &sm, int64_t span_hi, int pw) {
+    constexpr int NST = SM::kStages;
     const int64_t S = p.S;
     const int lane = threadIdx.x & 31;
     const int64_t nb = p.ntiles + 1;
@@ -778,10 +786,10 @@ __device__ __forceinline__ void producer(const AttrParams &p, TileSmem &sm, int6
             const int64_t tile = (int64_t)blockIdx.x + (int64_t)it * gridDim.x;
             if (tile >= p.ntiles) break;
             if (lane == u) {
-                const int stage = it % STAGES;
+                const int stage = it % NST;
                 StageMeta &M = sm.meta[stage];
                 int64_t wb, we;
-                tile_window(tile, S, wb, we);
+                tile_window<HALO>(tile, S, wb, we);
                 const int cnt = (int)(we - wb);
                 const int even = cnt & ~1;
                 uint32_t bytes = 2u * 8u * (uint32_t)even;
@@ -802,7 +810,7 @@ __device__ __forceinline__ void producer(const AttrParams &p, TileSmem &sm, int6
                     bytes += 2u * 8u * (uint32_t)m;
                 }
                 PROF(8);
-                if (it >= STAGES) mbar_wait(&sm.empty[stage], (uint32_t)(((it / STAGES) - 1) & 1));
+                if (it >= NST) mbar_wait(&sm.empty[stage], (uint32_t)(((it / NST) - 1) & 1));
                 PROF(7);
                 fence_proxy_async();
                 M.wb = wb;
@@ -1028,8 +1036,10 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_tiles_kernel(AttrParams
 
 // ------------------------------------------------ K2x exact-sum tile kernel
 // DW_SUM_EXACT (every interval = the exact sum of its pieces rounded to
-// 2^-40 W*us, rounded once).  Same producer and stage ring as K2; per tile a
-// consumer group:
+// 2^-40 W*us, rounded once).  Same producer as K2, with a shorter window halo
+// (XHALO pieces: longer intervals take K4) so the ring holds XSTAGES stages:
+// every consumer group holds one stage while it works, and the ring keeps
+// XSTAGES - GROUPS tiles in flight ahead of them.  Per tile a consumer group:
 //   pass B  one thread per XPER consecutive pieces of the window: the window's
 //           32-bit relative timestamps, each piece's term and its fixed-point
 //           value q (two instructions for |term| < 2^23 W*us), the thread's
@@ -1044,15 +1054,26 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_tiles_kernel(AttrParams
 //           length.  The modular difference is exact whenever the interval's
 //           true sum is below 2^63 units; the bound (hi - lo) * max|w| <= 8e6
 //           W*us guarantees it (|v| <= max|w| for every value the pieces use),
-//           and intervals beyond the bound or DW_DIRECT_MAX pieces go to K4,
-//           which sums the same pieces in int128.
+//           and intervals beyond the bound or XHALO pieces go to K4, which
+//           sums the same pieces in int128.
 // Each warp releases the stage on its own (empty barrier count = NCW): no
 // barrier at the end of a tile; the 32-bit timestamps are double buffered.
-constexpr int XPER = (WIN + ATTR_THREADS - 1) / ATTR_THREADS;  // pieces per thread in pass B
+#ifndef DW_XHALO
+#define DW_XHALO 64
+#endif
+#ifndef DW_XSTAGES
+#define DW_XSTAGES 7
+#endif
+constexpr int XHALO = DW_XHALO;                          // window halo = piece cap of the exact kernel
+constexpr int XSTAGES = DW_XSTAGES;
+constexpr int WINX = TILE + XHALO + 6;
+constexpr int XPER = (WINX + ATTR_THREADS - 1) / ATTR_THREADS;  // pieces per thread in pass B
 constexpr double X_BOUND = 8.0e6;  // W*us: |sum of an interval's q| < 2^63 below it
+using TileSmemX = TileSmemT<XSTAGES, WINX>;
+static_assert(GROUPS < XSTAGES, "claims in flight must span fewer positions than the ring");
 
 struct __align__(16) GroupSmemX {
-    uint32_t ts32[2][WIN];
+    uint32_t ts32[2][WINX];
     unsigned long long red[NCW][2];  // warp shares of the exact tile sum
     unsigned long long wtot[NCW];    // warp totals of the q scan (mod 2^64)
     uint32_t wmax[NCW];              // warp max of |w| (high word, rounded up)
@@ -1064,15 +1085,15 @@ struct __align__(16) GroupSmemX {
 __device__ __forceinline__ uint32_t abs_hi_up(double x) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(x));
     const uint32_t h = (uint32_t)(b >> 32);
-    return h == 0x7FF00000u ? h : h + ((uint32_t)b != 0u);
+    return h >= 0x7FF00000u ? 0x7FF00000u : h + ((uint32_t)b != 0u);
 }
 
 template <int KIND>
 __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    TileSmem &sm = *reinterpret_cast<TileSmem *>(smem_raw);
+    TileSmemX &sm = *reinterpret_cast<TileSmemX *>(smem_raw);
     GroupSmemX *groups =
-        reinterpret_cast<GroupSmemX *>(smem_raw + ((sizeof(TileSmem) + 15) & ~(size_t)15));
+        reinterpret_cast<GroupSmemX *>(smem_raw + ((sizeof(TileSmemX) + 15) & ~(size_t)15));
     const int tid = threadIdx.x;
     if ((int64_t)blockIdx.x >= p.ntiles) return;
 
@@ -1088,7 +1109,7 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
 
     if (tid == 0) {
 #pragma unroll
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < XSTAGES; ++s) {
             mbar_init(&sm.full[s], 1);
             mbar_init(&sm.empty[s], NCW);  // one arrival per consumer warp
         }
@@ -1099,20 +1120,21 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
     __syncthreads();
 
     if (tid >= GROUPS * ATTR_THREADS) {
-        producer(p, sm, cx.span_hi, (tid - GROUPS * ATTR_THREADS) >> 5);
+        producer<TileSmemX, XHALO>(p, sm, cx.span_hi, (tid - GROUPS * ATTR_THREADS) >> 5);
         return;
     }
     const int g = tid / ATTR_THREADS;
     const int ctid = tid - g * ATTR_THREADS;
     const int lane = ctid & 31, warp = ctid >> 5;
     GroupSmemX &gs = groups[g];
+    const int rb = ctid * XPER;  // this thread's first piece of every window
     int par = 0;
     for (;; par ^= 1) {
         const int it = gs.next_it;
         const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
         if (tile >= p.ntiles) break;
-        const int stage = it % STAGES;
-        mbar_wait(&sm.full[stage], (uint32_t)((it / STAGES) & 1));
+        const int stage = it % XSTAGES;
+        mbar_wait(&sm.full[stage], (uint32_t)((it / XSTAGES) & 1));
         const StageMeta &M = sm.meta[stage];
         const int64_t wb = M.wb;
         const int cnt = M.cnt;
@@ -1125,57 +1147,64 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
         const int r1 = (int)(min((tile + 1) * TILE, S) - wb);
         const int e1 = (int)(min((tile + 1) * TILE, nterms) - wb);
         const int rz0 = wb == 0 ? 0 : -1000;
-        const int rzS = (S - 1 - wb) < (int64_t)WIN ? (int)(S - 1 - wb) : -1000;
+        const int rzS = (S - 1 - wb) < (int64_t)WINX ? (int)(S - 1 - wb) : -1000;
         {
             const int64_t dt = s_ts[r1 < last ? r1 : last] - s_ts[r0];
             cx.scale = dt > 0 ? (float)(r1 - r0) / (float)dt : 0.0f;
         }
         cx.base = base;
         uint32_t *ts32 = gs.ts32[par];
+        if (p.validate_order) {  // strictly increasing power timestamps (int64 compare)
+            for (int r = r0 + ctid; r < r1 && wb + r + 1 < S; r += ATTR_THREADS)
+                if (s_ts[r + 1] <= s_ts[r]) atomic_min_index(&p.st->order_index, wb + r);
+        }
 
         // ---- pass B: pieces rb .. rb + XPER - 1 of the window
-        const int rb = ctid * XPER;
         long long q[XPER];
         unsigned long long run = 0;
         i128 tfx = 0;
-        uint32_t wm = 0;
+        double wmd = 0.0;
         {
             int64_t t0 = rb <= last ? s_ts[rb] : 0;
             // v(rb) for the linear pieces (window slot 0 has no left neighbour:
             // its piece lies before the tile and is never used)
-            double wprev = s_w[rb > 0 ? rb - 1 : 0];
+            const double wprev = s_w[rb > 0 ? rb - 1 : 0];
             double wcur = rb < cnt ? s_w[rb] : 0.0;
             double vcur = rb == rz0 ? cx.w0 : (rb == rzS ? cx.wl : __dadd_rn(wprev, __dsub_rn(wcur, wprev)));
+            const bool all_in = rb >= r0 && rb + XPER <= e1;  // every piece of this thread in the tile
+            auto body = [&](auto checked) {
+                constexpr bool C = decltype(checked)::value;
 #pragma unroll
-            for (int i = 0; i < XPER; ++i) {
-                const int r = rb + i;
-                q[i] = 0;
-                if (r <= last) ts32[r] = (uint32_t)(t0 - base);
-                if (r < cnt) wm = max(wm, abs_hi_up(wcur));
-                if (r < last) {
-                    const int64_t t1 = s_ts[r + 1];
-                    const int64_t wd = t1 - t0;
-                    double term;
-                    if (KIND == DW_SIGNAL_STEP) {
-                        term = __dmul_rn(wcur, (double)wd);
-                        wcur = r + 1 < cnt ? s_w[r + 1] : 0.0;
-                    } else {
-                        const double wnext = s_w[r + 1];
-                        const double vnext = r + 1 == rzS ? cx.wl : __dadd_rn(wcur, __dsub_rn(wnext, wcur));
-                        term = __dmul_rn(__dmul_rn(0.5, __dadd_rn(vcur, vnext)), (double)wd);
-                        vcur = vnext;
-                        wcur = wnext;
+                for (int i = 0; i < XPER; ++i) {
+                    const int r = rb + i;
+                    q[i] = 0;
+                    if (!C || r <= last) ts32[r] = (uint32_t)(t0 - base);
+                    if (!C || r < cnt) wmd = fmax(wmd, fabs(wcur));
+                    if (!C || r < last) {
+                        const int64_t t1 = s_ts[r + 1];
+                        const double wd = (double)(t1 - t0);
+                        double term;
+                        if (KIND == DW_SIGNAL_STEP) {
+                            term = __dmul_rn(wcur, wd);
+                            wcur = (!C || r + 1 < cnt) ? s_w[r + 1] : 0.0;
+                        } else {
+                            const double wnext = s_w[r + 1];
+                            const double vnext = r + 1 == rzS ? cx.wl : __dadd_rn(wcur, __dsub_rn(wnext, wcur));
+                            term = __dmul_rn(__dmul_rn(0.5, __dadd_rn(vcur, vnext)), wd);
+                            vcur = vnext;
+                            wcur = wnext;
+                        }
+                        long long qq;
+                        const bool fast = q40_fast(term, qq);
+                        q[i] = fast ? qq : 0;  // a huge piece: its intervals fail the bound
+                        if (all_in || (r >= r0 && r < e1)) tfx += fast ? (i128)qq : q_term(term);
+                        run += (unsigned long long)q[i];
+                        t0 = t1;
                     }
-                    long long qq;
-                    const bool fast = q40_fast(term, qq);
-                    q[i] = fast ? qq : 0;  // a huge piece: its intervals fail the bound
-                    if (r >= r0 && r < e1) tfx += fast ? (i128)qq : q_term(term);
-                    run += (unsigned long long)q[i];
-                    if (p.validate_order && r >= r0 && r < r1 && wb + r + 1 < S && wd <= 0)
-                        atomic_min_index(&p.st->order_index, wb + r);
-                    t0 = t1;
                 }
-            }
+            };
+            if (rb + XPER <= last && rb + XPER < cnt) body(std::false_type{});
+            else body(std::true_type{});
         }
         // warp inclusive scan of the per-thread sums (mod 2^64)
         unsigned long long inc = run;
@@ -1184,7 +1213,7 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
             const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += y;
         }
-        wm = __reduce_max_sync(0xffffffffu, wm);
+        const uint32_t wm = __reduce_max_sync(0xffffffffu, abs_hi_up(wmd));
         tile_fx_partial(tfx, gs.red, ctid);
         if (lane == 31) gs.wtot[warp] = inc;
         if (lane == 0) gs.wmax[warp] = wm;
@@ -1194,15 +1223,14 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
             tile_fx_store<NCW>(gs.red, p.tile_fx + 2 * tile);
         }
         // ---- the exclusive window prefix into the stage's timestamp slots
+        uint32_t wmx = 0;
         {
             unsigned long long pre = inc - run;
-            uint32_t wmx = 0;
 #pragma unroll
             for (int k = 0; k < NCW; ++k) {
                 if (k < warp) pre += gs.wtot[k];
                 wmx = max(wmx, gs.wmax[k]);
             }
-            wm = wmx;
             unsigned long long *P = reinterpret_cast<unsigned long long *>(s_ts);
 #pragma unroll
             for (int i = 0; i < XPER; ++i) {
@@ -1212,27 +1240,42 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
             }
         }
         consumer_sync(g);
-        const double wmaxd = __longlong_as_double((long long)((unsigned long long)wm << 32));
+        const double wmaxd = __longlong_as_double((long long)((unsigned long long)wmx << 32));
         const unsigned long long *P = reinterpret_cast<const unsigned long long *>(s_ts);
 
-        // ---- items: one interval per thread
+        // ---- items: one interval per thread.  Per-set descriptors in
+        // registers: item v of set j is interval v + kq[j], staged at
+        // s_lo[v + sx[j]] when v < lim[j].
         const int64_t total = M.c[DW_MAX_SETS];
+        const int64_t c1 = M.c[1], c2 = M.c[2], c3 = M.c[3];
+        int64_t kq[DW_MAX_SETS], sx[DW_MAX_SETS], lim[DW_MAX_SETS], pl[DW_MAX_SETS];
+#pragma unroll
+        for (int j = 0; j < DW_MAX_SETS; ++j) {
+            pl[j] = M.pool[j];
+            kq[j] = M.f0[j] - M.c[j];
+            sx[j] = M.pool[j] - M.a0[j] + kq[j];
+            lim[j] = M.a0[j] + M.copied[j] - kq[j];
+        }
         const int64_t *s_lo = sm.iv_lo[stage], *s_hi = sm.iv_hi[stage];
+        // register selects (a dynamic index would put the arrays in local memory)
+        auto pick = [](const int64_t (&a)[DW_MAX_SETS], int j) -> int64_t {
+            return j == 0 ? a[0] : (j == 1 ? a[1] : (j == 2 ? a[2] : a[3]));
+        };
         for (int64_t v = ctid; v < total; v += ATTR_THREADS) {
-            const int j = (v >= M.c[1]) + (v >= M.c[2]) + (v >= M.c[3]);
-            const int64_t k = v - M.c[j] + M.f0[j];
-            const int64_t idx = k - M.a0[j];
-            const bool staged = idx < M.copied[j];
+            const int j = (v >= c1) + (v >= c2) + (v >= c3);
+            const int64_t k = v + pick(kq, j);
+            const bool staged = v < pick(lim, j);
+            const int64_t si = v + pick(sx, j);
             int64_t glo, ghi;
             if (staged) {
-                glo = s_lo[M.pool[j] + idx];
-                ghi = s_hi[M.pool[j] + idx];
+                glo = s_lo[si];
+                ghi = s_hi[si];
             } else {
                 glo = __ldg(p.start[j] + k);
                 ghi = __ldg(p.end[j] + k);
             }
             if (p.check_sorted[j] && k > 0) {
-                const int64_t prev = (staged && idx > 0) ? s_lo[M.pool[j] + idx - 1] : __ldg(p.start[j] + k - 1);
+                const int64_t prev = (staged && si > pick(pl, j)) ? s_lo[si - 1] : __ldg(p.start[j] + k - 1);
                 if (prev > glo) atomic_min_index(&p.st->unsorted_index[j], k);
             }
             if (ghi < glo || glo < cx.span_lo || ghi > cx.span_hi) {
@@ -1247,8 +1290,8 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
                 const uint32_t hi = dh > 0xFFFFFFFFLL ? 0xFFFFFFFFu : (uint32_t)dh;
                 double F0, L;
                 int s0, n, lst;
-                ok = phase1_item<KIND>(ts32, s_w, r0, r1, cnt, lo, hi, glo <= cx.ts0, glo >= cx.tsl, ghi <= cx.ts0,
-                                       ghi >= cx.tsl, cx, F0, L, s0, n, lst);
+                ok = phase1_item<KIND, XHALO>(ts32, s_w, r0, r1, cnt, lo, hi, glo <= cx.ts0, glo >= cx.tsl,
+                                              ghi <= cx.ts0, ghi >= cx.tsl, cx, F0, L, s0, n, lst);
                 long long qf = 0, ql = 0;
                 ok = ok && q40_fast(F0, qf) && (!lst || q40_fast(L, ql));
                 if (ok) {
@@ -1897,7 +1940,7 @@ static int attribute_impl(const dw_signal_t *sig, dw_interval_set_t *sets, int n
     const size_t smem = ((sizeof(TileSmem) + 15) & ~(size_t)15) + GROUPS * sizeof(GroupSmem);
     const int sms = g_attr_sms > 0 && g_attr_sms < num_sms() ? g_attr_sms : num_sms();
     int grid = (int)std::min<int64_t>(p.ntiles, (int64_t)sms * CTAS_PER_SM);
-    const size_t smem_x = ((sizeof(TileSmem) + 15) & ~(size_t)15) + GROUPS * sizeof(GroupSmemX);
+    const size_t smem_x = ((sizeof(TileSmemX) + 15) & ~(size_t)15) + GROUPS * sizeof(GroupSmemX);
     timing_begin(stream);
     if (p.sum_mode == DW_SUM_EXACT) {
         if (sig->kind == DW_SIGNAL_STEP) {

@@ -8,6 +8,7 @@ from paper_2512_08365_b200.energy import PowerSignal, _run_ledger
 name = sys.argv[1] if len(sys.argv) > 1 else "C4"
 kind = sys.argv[2] if len(sys.argv) > 2 else "step"
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+summation = sys.argv[4] if len(sys.argv) > 4 else "reference"
 t = time.time()
 a, b = synth.make_pair(name)
 torch.cuda.synchronize()
@@ -21,10 +22,10 @@ bytes_alg = 16 * a.n_power + 24 * (a.n_ops + a.n_kernels)
 for it in range(iters):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    per_op, per_k, st = _run_ledger(a, sig, False)
+    per_op, per_k, st = _run_ledger(a, sig, False, summation)
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    print(f"ledger {kind}: {ms:.3f} ms  {bytes_alg/ms/1e6:.1f} GB/s alg  long={st.long_intervals} code={st.code} total={st.totals[0]:.6e}", flush=True)
+    print(f"ledger {kind} {summation}: {ms:.3f} ms  {bytes_alg/ms/1e6:.1f} GB/s alg  long={st.long_intervals} code={st.code} total={st.totals[0]:.6e}", flush=True)
 L = _native.lib()
 if hasattr(L, "dw_phase_prof"):
     import ctypes

@@ -230,7 +230,11 @@ def test_config1_golden():
 # Every interval is the exact sum of its pieces rounded to 2^-40 W*us, rounded
 # once: bit-identical to the oracle's MODE_EXACT, within a few ulps of the
 # reference's sequential sums (tolerance 1e-12 relative here; the north star
-# asks 1e-6).
+# asks 1e-6).  Each piece is rounded to 2^-40 W*us, so an interval's absolute
+# error is at most (pieces / 2) * 2^-40 W*us = pieces * 4.5e-19 J: EXACT_ATOL
+# covers intervals of up to ~200 pieces whose energy is too small for the
+# relative bar (below ~1e-4 J the quantum dominates 1e-12 relative).
+EXACT_ATOL = 1e-16  # J
 
 
 @pytest.mark.parametrize("seed,S,n,max_len", [(11, 300_000, 200_000, 3000), (12, 2_000_001, 500_000, 40_000),
@@ -241,7 +245,7 @@ def test_exact_step_vs_oracle(seed, S, n, max_len):
     got = E.integrate_many(sig, lo, hi, summation="exact").cpu().numpy()
     np.testing.assert_array_equal(got, oracle.integrate_step(ts, w, span_hi, lo, hi, oracle.MODE_EXACT))
     ref = oracle.integrate_step(ts, w, span_hi, lo, hi, oracle.MODE_REFERENCE)
-    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-300)
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=EXACT_ATOL)
 
 
 @pytest.mark.parametrize("seed,S,n,max_len", [(14, 300_000, 200_000, 3000), (15, 1_000_003, 300_000, 20_000)])
@@ -253,7 +257,7 @@ def test_exact_linear_vs_oracle(seed, S, n, max_len):
     got = E.integrate_many(sig, lo, hi, summation="exact").cpu().numpy()
     np.testing.assert_array_equal(got, oracle.integrate_linear(ts, w, lo, hi, oracle.MODE_EXACT))
     ref = oracle.integrate_linear(ts, w, lo, hi, oracle.MODE_REFERENCE)
-    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-300)
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=EXACT_ATOL)
 
 
 def test_exact_golden_vectors(golden_step, golden_linear):
@@ -261,12 +265,12 @@ def test_exact_golden_vectors(golden_step, golden_linear):
         got = E.integrate_many(PowerSignal.from_columns(ts, w, span_hi, "step"), lo, hi, summation="exact")
         got = got.cpu().numpy()
         np.testing.assert_array_equal(got, oracle.integrate_step(ts, w, span_hi, lo, hi, oracle.MODE_EXACT))
-        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-300)
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=EXACT_ATOL)
     for ts, w, _, lo, hi, ref in _signals(golden_linear, False):
         got = E.integrate_many(PowerSignal.from_columns(ts, w, kind="linear"), lo, hi, summation="exact")
         got = got.cpu().numpy()
         np.testing.assert_array_equal(got, oracle.integrate_linear(ts, w, lo, hi, oracle.MODE_EXACT))
-        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-300)
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=EXACT_ATOL)
 
 
 @pytest.mark.parametrize("name", ["preset_tf32_misconfig", "preset_join_redundant", "fuzz_00", "cfg1"])
@@ -275,8 +279,8 @@ def test_exact_ledger_golden(name):
     for side in ("a", "b"):
         cols = _cols(sc, side)
         led = build_ledger(cols, summation="exact")
-        np.testing.assert_allclose(led.per_operator.array(), sc[f"gt_{side}_per_op"], rtol=1e-12, atol=1e-300)
-        np.testing.assert_allclose(led.per_kernel.array(), sc[f"gt_{side}_per_k"], rtol=1e-12, atol=1e-300)
+        np.testing.assert_allclose(led.per_operator.array(), sc[f"gt_{side}_per_op"], rtol=1e-12, atol=EXACT_ATOL)
+        np.testing.assert_allclose(led.per_kernel.array(), sc[f"gt_{side}_per_k"], rtol=1e-12, atol=EXACT_ATOL)
         ts, w = cols.host("ts"), cols.host("watts")
         span_hi = cols.signal_span()[1]
         po, pk, total, idle = oracle.ledger("step", ts, w, span_hi, cols.host("op_start"), cols.host("op_end"),
