@@ -1135,6 +1135,13 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
         if (tile >= p.ntiles) break;
         const int stage = it % XSTAGES;
         mbar_wait(&sm.full[stage], (uint32_t)((it / XSTAGES) & 1));
+#ifdef DW_SKIP_CONSUMERS
+        consumer_sync(g);
+        if (ctid == 0) gs.next_it = atomicAdd(&sm.claim, 1);
+        consumer_sync(g);
+        if (lane == 0) mbar_arrive(&sm.empty[stage]);
+        continue;
+#endif
         const StageMeta &M = sm.meta[stage];
         const int64_t wb = M.wb;
         const int cnt = M.cnt;
@@ -1257,6 +1264,9 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
             lim[j] = M.a0[j] + M.copied[j] - kq[j];
         }
         const int64_t *s_lo = sm.iv_lo[stage], *s_hi = sm.iv_hi[stage];
+#ifdef DW_X_NO_ITEMS
+        if (total >= 0) { __syncwarp(); if (lane == 0) mbar_arrive(&sm.empty[stage]); continue; }
+#endif
         // register selects (a dynamic index would put the arrays in local memory)
         auto pick = [](const int64_t (&a)[DW_MAX_SETS], int j) -> int64_t {
             return j == 0 ? a[0] : (j == 1 ? a[1] : (j == 2 ? a[2] : a[3]));
@@ -1493,14 +1503,27 @@ __global__ void __launch_bounds__(256) long_intervals_kernel(AttrParams p) {
         if (KIND == DW_SIGNAL_STEP) {
             int64_t a = upper_bound_g(p.ts, S, lo) - 1;
             int64_t b = lower_bound_g(p.ts, S, hi) - 1;
-            acc = range_sum<KIND>(p, a + 1, b - 1);
-            if (lane == 0) {
-                acc += q_term(__dmul_rn(W(a), (double)(TS(a + 1) - lo)));
-                acc += q_term(__dmul_rn(W(b), (double)(min(TS(b + 1), hi) - TS(b))));
+            if (hi <= lo || a >= b) {  // no piece, or one piece inside segment a (exact mode's wide windows)
+                acc = (lane == 0 && hi > lo) ? q_term(__dmul_rn(W(a), (double)(hi - lo))) : (i128)0;
+            } else {
+                acc = range_sum<KIND>(p, a + 1, b - 1);
+                if (lane == 0) {
+                    acc += q_term(__dmul_rn(W(a), (double)(TS(a + 1) - lo)));
+                    acc += q_term(__dmul_rn(W(b), (double)(min(TS(b + 1), hi) - TS(b))));
+                }
             }
         } else {
             int64_t first = upper_bound_g(p.ts, S, lo);
             int64_t last = lower_bound_g(p.ts, S, hi);
+            if (last <= first) {  // no sample strictly inside: the one piece [lo, hi]
+                acc = 0;
+                if (lane == 0) {
+                    const double vlo = lin_value_at(lo, (first > 0 && TS(first - 1) == lo) ? first - 1 : first, TS(0),
+                                                    TS(S - 1), W(0), W(S - 1), TS, W);
+                    const double vh = lin_value_at(hi, last, TS(0), TS(S - 1), W(0), W(S - 1), TS, W);
+                    acc = q_term(lin_piece(vlo, vh, hi - lo));
+                }
+            } else {
             acc = range_sum<KIND>(p, first, last - 2);
             if (lane == 0) {
                 int64_t lbj = (first > 0 && TS(first - 1) == lo) ? first - 1 : first;
@@ -1510,6 +1533,7 @@ __global__ void __launch_bounds__(256) long_intervals_kernel(AttrParams p) {
                 double vl = lin_sample_value(last - 1, S, TS, W);
                 double vh = lin_value_at(hi, last, TS(0), TS(S - 1), W(0), W(S - 1), TS, W);
                 acc += q_term(lin_piece(vl, vh, hi - TS(last - 1)));
+            }
             }
         }
         if (lane == 0) {
