@@ -1072,22 +1072,59 @@ constexpr double X_BOUND = 8.0e6;  // W*us: |sum of an interval's q| < 2^63 belo
 using TileSmemX = TileSmemT<XSTAGES, WINX>;
 static_assert(GROUPS < XSTAGES, "claims in flight must span fewer positions than the ring");
 
+// Per-set item descriptor of one tile (group smem, double buffered by tile
+// parity): item v of set j (v in [c_j, c_{j+1}): the tile's items of all sets
+// concatenated) is interval kq + v; its [start, end) sits at stage slot v + sx
+// when v < lim; its joules go to out[v] (out pre-offset by kq; perm: the set
+// was sorted on the device, so results scatter through p.perm).
+struct __align__(16) SetDescX {
+    double *out;
+    int64_t kq;
+    int sx, lim, pool, flags;  // flags: 1 check sorted, 2 perm
+};
+
 struct __align__(16) GroupSmemX {
     uint32_t ts32[2][WINX];
-    unsigned long long red[NCW][2];  // warp shares of the exact tile sum
+    SetDescX desc[2][DW_MAX_SETS];
     unsigned long long wtot[NCW];    // warp totals of the q scan (mod 2^64)
-    uint32_t wmax[NCW];              // warp max of |w| (high word, rounded up)
+    long long red[NCW][4];           // warp shares of the exact tile sum: 21-bit limb sums + int128 spill
+    uint32_t wmax[NCW];              // warp max of the high word of |w|
     int next_it;
 };
 
-// |x| rounded up to its high 32 bits: a monotone u32 bound (non-negative doubles
-// order as their bit patterns)
-__device__ __forceinline__ uint32_t abs_hi_up(double x) {
-    const unsigned long long b = (unsigned long long)__double_as_longlong(fabs(x));
-    const uint32_t h = (uint32_t)(b >> 32);
-    return h >= 0x7FF00000u ? 0x7FF00000u : h + ((uint32_t)b != 0u);
+// Interior value v(x) of a linear signal at window slot r (energy.py:115-124:
+// w[r-1] + 1.0 * (w[r] - w[r-1]); the signal's first / last sample hold w0 /
+// wl; rz0 / rzS are their window slots or out of range).
+__device__ __forceinline__ double lin_v(const double *w, int r, int rz0, int rzS, double w0, double wl) {
+    const double wa = w[r > 0 ? r - 1 : 0];
+    const double v = __dadd_rn(wa, __dsub_rn(w[r], wa));
+    return r == rz0 ? w0 : (r == rzS ? wl : v);
 }
 
+__device__ __forceinline__ uint32_t abs_hi(double x) { return (uint32_t)__double2hiint(x) & 0x7FFFFFFFu; }
+
+// Exact per-interval sum with O(1) work per interval.  Per tile a consumer
+// group:
+//   pass B  one thread per XPER consecutive pieces from the tile's first
+//           sample r0: 32-bit relative timestamps (for the searches), each
+//           piece's doubled term t2 = (v_r + v_r+1) * width (linear) or
+//           2 * w_r * width (step) and q = rni(t2 * 2^39) -- bit for bit
+//           q40(term), as 0.5 * x is exact -- the thread's running sum of q
+//           (mod 2^64), its exact share of the tile sum (int64 for pieces
+//           below 2^20 W*us; int128 term by term otherwise) and max |w|.
+//           Threads whose pieces are all interior, in range and narrow take
+//           a 32-bit body with no per-piece conditions.
+//   (group barrier)
+//           the exclusive window prefix P[r] = sum of q over pieces < r (mod
+//           2^64) into the stage's timestamp slots;
+//   (group barrier)
+//   items   one thread per interval: its first piece a and last piece b by
+//           guessed search, the two edge pieces (interpolated endpoint values,
+//           exact divisions) and q(F0) + (P[b] - P[a+1]) + q(L).  The modular
+//           difference is exact: (hi - lo) * max|w| <= X_BOUND W*us bounds the
+//           interval's sum below 2^63 units and every piece inside it below
+//           2^23 W*us.  Longer or larger intervals go to K4 (int128 there).
+// Every warp releases the stage on its own.
 template <int KIND>
 __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -1127,7 +1164,6 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
     const int ctid = tid - g * ATTR_THREADS;
     const int lane = ctid & 31, warp = ctid >> 5;
     GroupSmemX &gs = groups[g];
-    const int rb = ctid * XPER;  // this thread's first piece of every window
     int par = 0;
     for (;; par ^= 1) {
         const int it = gs.next_it;
@@ -1148,70 +1184,111 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
         int64_t *s_ts = sm.ts[stage];
         const double *s_w = sm.w[stage];
         const int64_t base = s_ts[0];
-        const int last = (wb + cnt == S) ? cnt : cnt - 1;  // last valid timestamp slot
+        const int last = (KIND == DW_SIGNAL_STEP && wb + cnt == S) ? cnt : cnt - 1;  // last timestamp slot
         const bool wide = (s_ts[last] - base) >= (int64_t)0xFFFFFFF0LL;
-        const int r0 = (int)(tile * TILE - wb);
-        const int r1 = (int)(min((tile + 1) * TILE, S) - wb);
-        const int e1 = (int)(min((tile + 1) * TILE, nterms) - wb);
+        const int64_t t0g = tile * TILE;
+        const int r0 = (int)(t0g - wb);
+        const int r1 = (int)((t0g + TILE < S ? t0g + TILE : S) - wb);
+        const int e1 = (int)((t0g + TILE < nterms ? t0g + TILE : nterms) - wb);
         const int rz0 = wb == 0 ? 0 : -1000;
         const int rzS = (S - 1 - wb) < (int64_t)WINX ? (int)(S - 1 - wb) : -1000;
         {
             const int64_t dt = s_ts[r1 < last ? r1 : last] - s_ts[r0];
-            cx.scale = dt > 0 ? (float)(r1 - r0) / (float)dt : 0.0f;
+            cx.scale = dt > 0 ? __fdividef((float)(r1 - r0), (float)dt) : 0.0f;
         }
-        cx.base = base;
         uint32_t *ts32 = gs.ts32[par];
-        if (p.validate_order) {  // strictly increasing power timestamps (int64 compare)
-            for (int r = r0 + ctid; r < r1 && wb + r + 1 < S; r += ATTR_THREADS)
-                if (s_ts[r + 1] <= s_ts[r]) atomic_min_index(&p.st->order_index, wb + r);
+        if (ctid < DW_MAX_SETS) {  // this tile's set descriptors
+            const int j = ctid;
+            SetDescX d;
+            d.kq = M.f0[j] - M.c[j];
+            const bool perm = j < p.nsets && p.perm[j] != nullptr;
+            d.out = j < p.nsets && !perm ? p.out[j] + d.kq : nullptr;
+            d.sx = (int)(M.pool[j] - M.a0[j] + d.kq);
+            d.lim = (int)(M.a0[j] + M.copied[j] - d.kq);
+            d.pool = M.pool[j];
+            d.flags = (j < p.nsets && p.check_sorted[j] ? 1 : 0) | (perm ? 2 : 0);
+            gs.desc[par][j] = d;
         }
 
-        // ---- pass B: pieces rb .. rb + XPER - 1 of the window
+        // ---- pass B: pieces rb .. rb + XPER - 1 (r < last)
+        const int rb = r0 + ctid * XPER;
         long long q[XPER];
         unsigned long long run = 0;
-        i128 tfx = 0;
-        double wmd = 0.0;
-        {
-            int64_t t0 = rb <= last ? s_ts[rb] : 0;
-            // v(rb) for the linear pieces (window slot 0 has no left neighbour:
-            // its piece lies before the tile and is never used)
-            const double wprev = s_w[rb > 0 ? rb - 1 : 0];
-            double wcur = rb < cnt ? s_w[rb] : 0.0;
-            double vcur = rb == rz0 ? cx.w0 : (rb == rzS ? cx.wl : __dadd_rn(wprev, __dsub_rn(wcur, wprev)));
-            const bool all_in = rb >= r0 && rb + XPER <= e1;  // every piece of this thread in the tile
-            auto body = [&](auto checked) {
-                constexpr bool C = decltype(checked)::value;
+        long long tin = 0;    // exact share of the tile sum (pieces [r0, e1)), int64 part
+        i128 tbig = 0;        // ... and its int128 part (huge pieces)
+        uint32_t hmax = 0;
+        bool big = false, bad = false;
+        const bool fastb = !wide && rb + XPER <= last && rb + XPER < cnt && !(rzS > rb && rzS <= rb + XPER) &&
+                           (rb + XPER <= e1 || rb >= e1);
+        if (fastb) {
+            const uint32_t b32 = (uint32_t)base;
+            int64_t t0 = s_ts[rb];
+            double wcur = s_w[rb];
+            double vcur = KIND == DW_SIGNAL_LINEAR ? lin_v(s_w, rb, rz0, rzS, cx.w0, cx.wl) : 0.0;
+            hmax = abs_hi(wcur);
 #pragma unroll
-                for (int i = 0; i < XPER; ++i) {
-                    const int r = rb + i;
-                    q[i] = 0;
-                    if (!C || r <= last) ts32[r] = (uint32_t)(t0 - base);
-                    if (!C || r < cnt) wmd = fmax(wmd, fabs(wcur));
-                    if (!C || r < last) {
-                        const int64_t t1 = s_ts[r + 1];
-                        const double wd = (double)(t1 - t0);
-                        double term;
-                        if (KIND == DW_SIGNAL_STEP) {
-                            term = __dmul_rn(wcur, wd);
-                            wcur = (!C || r + 1 < cnt) ? s_w[r + 1] : 0.0;
-                        } else {
-                            const double wnext = s_w[r + 1];
-                            const double vnext = r + 1 == rzS ? cx.wl : __dadd_rn(wcur, __dsub_rn(wnext, wcur));
-                            term = __dmul_rn(__dmul_rn(0.5, __dadd_rn(vcur, vnext)), wd);
-                            vcur = vnext;
-                            wcur = wnext;
-                        }
-                        long long qq;
-                        const bool fast = q40_fast(term, qq);
-                        q[i] = fast ? qq : 0;  // a huge piece: its intervals fail the bound
-                        if (all_in || (r >= r0 && r < e1)) tfx += fast ? (i128)qq : q_term(term);
-                        run += (unsigned long long)q[i];
-                        t0 = t1;
-                    }
+            for (int i = 0; i < XPER; ++i) {
+                const int r = rb + i;
+                ts32[r] = (uint32_t)t0 - b32;
+                const int64_t t1 = s_ts[r + 1];
+                bad |= t1 <= t0;
+                const double wd = (double)((uint32_t)t1 - (uint32_t)t0);
+                const double wnext = s_w[r + 1];
+                double t2;
+                if (KIND == DW_SIGNAL_STEP) {
+                    t2 = __dmul_rn(__dadd_rn(wcur, wcur), wd);
+                } else {
+                    const double vnext = __dadd_rn(wcur, __dsub_rn(wnext, wcur));
+                    t2 = __dmul_rn(__dadd_rn(vcur, vnext), wd);
+                    vcur = vnext;
                 }
-            };
-            if (rb + XPER <= last && rb + XPER < cnt) body(std::false_type{});
-            else body(std::true_type{});
+                hmax = max(hmax, abs_hi(wnext));
+                wcur = wnext;
+                big |= !(fabs(t2) < 2097152.0);  // 2^21: |q| < 2^60, the share of XPER pieces fits int64
+                q[i] = __double2ll_rn(__dmul_rn(t2, 549755813888.0));  // * 2^39
+                run += (unsigned long long)q[i];
+                t0 = t1;
+            }
+            if (rb < e1) tin = (long long)run;
+        } else {
+#pragma unroll
+            for (int i = 0; i < XPER; ++i) {
+                const int r = rb + i;
+                q[i] = 0;
+                if (!wide && r <= last) ts32[r] = (uint32_t)(s_ts[r] - base);
+                if (r < last) {
+                    const int64_t t0 = s_ts[r], t1 = s_ts[r + 1];
+                    bad |= t1 <= t0;
+                    const int64_t width = t1 - t0;
+                    double t2;
+                    if (KIND == DW_SIGNAL_STEP) {
+                        const double wv = s_w[r];
+                        hmax = max(hmax, abs_hi(wv));
+                        t2 = __dmul_rn(__dadd_rn(wv, wv), (double)width);
+                    } else {
+                        hmax = max(hmax, max(abs_hi(s_w[r]), abs_hi(s_w[r + 1])));
+                        t2 = __dmul_rn(__dadd_rn(lin_v(s_w, r, rz0, rzS, cx.w0, cx.wl),
+                                                 lin_v(s_w, r + 1, rz0, rzS, cx.w0, cx.wl)), (double)width);
+                    }
+                    q[i] = __double2ll_rn(__dmul_rn(t2, 549755813888.0));
+                    run += (unsigned long long)q[i];
+                    if (r < e1) tbig += q40(__dmul_rn(t2, 0.5));
+                }
+            }
+        }
+        if (big) {  // a piece of 2^20 W*us or more: this thread's share term by term in int128
+            tin = 0;
+            for (int i = 0; i < XPER; ++i) {
+                const int r = rb + i;
+                if (r >= e1) break;
+                const double wd = (double)(s_ts[r + 1] - s_ts[r]);
+                const double term = KIND == DW_SIGNAL_STEP
+                                        ? __dmul_rn(s_w[r], wd)
+                                        : __dmul_rn(__dmul_rn(0.5, __dadd_rn(lin_v(s_w, r, rz0, rzS, cx.w0, cx.wl),
+                                                                             lin_v(s_w, r + 1, rz0, rzS, cx.w0, cx.wl))),
+                                                    wd);
+                tbig += q40(term);
+            }
         }
         // warp inclusive scan of the per-thread sums (mod 2^64)
         unsigned long long inc = run;
@@ -1220,100 +1297,157 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
             const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += y;
         }
-        const uint32_t wm = __reduce_max_sync(0xffffffffu, abs_hi_up(wmd));
-        tile_fx_partial(tfx, gs.red, ctid);
+        const uint32_t wm = __reduce_max_sync(0xffffffffu, hmax);
+        // the warp's exact share of the tile sum: int64 shares as three 21-bit
+        // limb sums (32-bit reductions), int128 spills (rare) by shuffles
+        {
+            const int l0 = __reduce_add_sync(0xffffffffu, (int)(tin & 0x1FFFFF));
+            const int l1 = __reduce_add_sync(0xffffffffu, (int)((tin >> 21) & 0x1FFFFF));
+            const int l2 = __reduce_add_sync(0xffffffffu, (int)(tin >> 42));
+            i128 spill = 0;
+            if (__any_sync(0xffffffffu, tbig != 0)) spill = warp_sum_i128(tbig);
+            if (lane == 0) {
+                const i128 t = (i128)l0 + ((i128)l1 << 21) + ((i128)l2 << 42) + spill;
+                const I128Parts pp = split(t);
+                gs.red[warp][0] = (long long)pp.lo;
+                gs.red[warp][1] = (long long)pp.hi;
+                gs.wmax[warp] = wm;
+            }
+        }
         if (lane == 31) gs.wtot[warp] = inc;
-        if (lane == 0) gs.wmax[warp] = wm;
+        if (p.validate_order && bad) {  // strictly increasing power timestamps: the first offender
+            for (int i = 0; i < XPER; ++i) {
+                const int r = rb + i;
+                if (r < r1 && wb + r + 1 < S && r < last && s_ts[r + 1] <= s_ts[r])
+                    atomic_min_index(&p.st->order_index, wb + r);
+            }
+        }
         consumer_sync(g);
         if (ctid == 0) {
             gs.next_it = atomicAdd(&sm.claim, 1);  // every thread has read it
-            tile_fx_store<NCW>(gs.red, p.tile_fx + 2 * tile);
+            i128 t = 0;
+#pragma unroll
+            for (int k = 0; k < NCW; ++k) t += join((uint64_t)gs.red[k][0], (uint64_t)gs.red[k][1]);
+            const I128Parts pp = split(t);
+            p.tile_fx[2 * tile] = pp.lo;
+            p.tile_fx[2 * tile + 1] = pp.hi;
         }
         // ---- the exclusive window prefix into the stage's timestamp slots
-        uint32_t wmx = 0;
+        uint32_t wmx_hi = 0;
         {
             unsigned long long pre = inc - run;
 #pragma unroll
             for (int k = 0; k < NCW; ++k) {
                 if (k < warp) pre += gs.wtot[k];
-                wmx = max(wmx, gs.wmax[k]);
+                wmx_hi = max(wmx_hi, gs.wmax[k]);
             }
             unsigned long long *P = reinterpret_cast<unsigned long long *>(s_ts);
+            if (fastb) {
 #pragma unroll
-            for (int i = 0; i < XPER; ++i) {
-                const int r = rb + i;
-                if (r <= last) P[r] = pre;
-                pre += (unsigned long long)q[i];
+                for (int i = 0; i < XPER; ++i) {
+                    P[rb + i] = pre;
+                    pre += (unsigned long long)q[i];
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < XPER; ++i) {
+                    if (rb + i <= last) P[rb + i] = pre;
+                    pre += (unsigned long long)q[i];
+                }
             }
         }
         consumer_sync(g);
-        const double wmaxd = __longlong_as_double((long long)((unsigned long long)wmx << 32));
         const unsigned long long *P = reinterpret_cast<const unsigned long long *>(s_ts);
+        // max |w| over the window, rounded up (NaN / inf: every bound test fails)
+        const double wmx = __hiloint2double((int)(wmx_hi + 1u), 0);
 
-        // ---- items: one interval per thread.  Per-set descriptors in
-        // registers: item v of set j is interval v + kq[j], staged at
-        // s_lo[v + sx[j]] when v < lim[j].
-        const int64_t total = M.c[DW_MAX_SETS];
-        const int64_t c1 = M.c[1], c2 = M.c[2], c3 = M.c[3];
-        int64_t kq[DW_MAX_SETS], sx[DW_MAX_SETS], lim[DW_MAX_SETS], pl[DW_MAX_SETS];
-#pragma unroll
-        for (int j = 0; j < DW_MAX_SETS; ++j) {
-            pl[j] = M.pool[j];
-            kq[j] = M.f0[j] - M.c[j];
-            sx[j] = M.pool[j] - M.a0[j] + kq[j];
-            lim[j] = M.a0[j] + M.copied[j] - kq[j];
-        }
+        // ---- items: one interval per thread
+        const int total = (int)M.c[DW_MAX_SETS];
+        const int c1 = (int)M.c[1], c2 = (int)M.c[2], c3 = (int)M.c[3];
         const int64_t *s_lo = sm.iv_lo[stage], *s_hi = sm.iv_hi[stage];
+        const SetDescX *dsc = gs.desc[par];
+        const bool first_tile = wb == 0;
+        const uint32_t tr0 = ts32[r0];
 #ifdef DW_X_NO_ITEMS
         if (total >= 0) { __syncwarp(); if (lane == 0) mbar_arrive(&sm.empty[stage]); continue; }
 #endif
-        // register selects (a dynamic index would put the arrays in local memory)
-        auto pick = [](const int64_t (&a)[DW_MAX_SETS], int j) -> int64_t {
-            return j == 0 ? a[0] : (j == 1 ? a[1] : (j == 2 ? a[2] : a[3]));
-        };
-        for (int64_t v = ctid; v < total; v += ATTR_THREADS) {
+        for (int v = ctid; v < total; v += ATTR_THREADS) {
             const int j = (v >= c1) + (v >= c2) + (v >= c3);
-            const int64_t k = v + pick(kq, j);
-            const bool staged = v < pick(lim, j);
-            const int64_t si = v + pick(sx, j);
+            const SetDescX d = dsc[j];
+            const int slot = v + d.sx;
             int64_t glo, ghi;
+            const bool staged = v < d.lim;
             if (staged) {
-                glo = s_lo[si];
-                ghi = s_hi[si];
-            } else {
-                glo = __ldg(p.start[j] + k);
-                ghi = __ldg(p.end[j] + k);
+                glo = s_lo[slot];
+                ghi = s_hi[slot];
+            } else {  // beyond the staged pool (rare)
+                glo = __ldg(p.start[j] + d.kq + v);
+                ghi = __ldg(p.end[j] + d.kq + v);
             }
-            if (p.check_sorted[j] && k > 0) {
-                const int64_t prev = (staged && si > pick(pl, j)) ? s_lo[si - 1] : __ldg(p.start[j] + k - 1);
+            if (d.flags & 1) {  // a set flagged sorted must be sorted by start
+                const int64_t k = d.kq + v;
+                const int64_t prev = (staged && slot > d.pool) ? s_lo[slot - 1]
+                                                               : (k > 0 ? __ldg(p.start[j] + k - 1) : glo);
                 if (prev > glo) atomic_min_index(&p.st->unsorted_index[j], k);
             }
-            if (ghi < glo || glo < cx.span_lo || ghi > cx.span_hi) {
-                report_bad(p, j, k);
+            if (ghi < glo || ghi > cx.span_hi || (first_tile && glo < cx.span_lo)) {
+                report_bad(p, j, d.kq + v);
                 continue;
             }
-            bool ok = !wide && __dmul_rn((double)(ghi - glo), wmaxd) <= X_BOUND;
+            const int64_t dh = ghi - base;
+            bool ok = !wide && dh <= (int64_t)0xFFFFFFFFLL && __dmul_rn((double)(ghi - glo), wmx) <= X_BOUND;
             double J = 0.0;
             if (ok) {
-                const uint32_t lo = (uint32_t)(glo - base);
-                const int64_t dh = ghi - base;
-                const uint32_t hi = dh > 0xFFFFFFFFLL ? 0xFFFFFFFFu : (uint32_t)dh;
-                double F0, L;
-                int s0, n, lst;
-                ok = phase1_item<KIND, XHALO>(ts32, s_w, r0, r1, cnt, lo, hi, glo <= cx.ts0, glo >= cx.tsl,
-                                              ghi <= cx.ts0, ghi >= cx.tsl, cx, F0, L, s0, n, lst);
-                long long qf = 0, ql = 0;
-                ok = ok && q40_fast(F0, qf) && (!lst || q40_fast(L, ql));
-                if (ok) {
-                    const long long tq = qf + (lst ? ql : 0LL) + (long long)(P[s0 + n] - P[s0]);
-                    J = div_1e6(__dmul_rn((double)tq, 9.094947017729282379150390625e-13));  // * 2^-40
+                const uint32_t lo = (uint32_t)glo - (uint32_t)base;
+                const uint32_t hi = (uint32_t)dh;
+                const int a = find_le(ts32, r0, r1, lo, tr0, r0, cx.scale);
+                const uint32_t ta = ts32[a], ta1 = ts32[a + 1];
+                const int lim = min(a + XHALO + 1, cnt);
+                double F2, L2;
+                int b;
+                bool one;
+                if (KIND == DW_SIGNAL_STEP) {
+                    // pieces: none (hi == lo); w[a]*(hi-lo) inside one segment;
+                    // else first partial + whole interior + last partial segment
+                    b = hi > lo ? find_le(ts32, a, lim, hi - 1, ta, a, cx.scale) : a;
+                    ok = b - a < XHALO;  // segments b - a + 1 <= XHALO
+                    const double wa = s_w[a];
+                    one = b == a;
+                    F2 = __dmul_rn(__dadd_rn(wa, wa), (double)((one ? hi : ta1) - lo));
+                    const double wbv = s_w[b];
+                    L2 = __dmul_rn(__dadd_rn(wbv, wbv), (double)(hi - ts32[b]));
+                } else {
+                    // pieces [lo, ts] .. [ts, hi] (energy.py:108-130); b = last sample < hi
+                    b = ta < hi ? find_le(ts32, a, lim, hi - 1, ta, a, cx.scale) : a - 1;
+                    const int m = b - a;  // -1 only when hi == lo == ts[a]
+                    ok = m < XHALO;       // pieces m + 1 <= XHALO
+                    const int il = ta == lo && a > 0 ? a - 1 : a;  // first bracketing pair (energy.py:115-124)
+                    const double wl0 = s_w[il], wl1 = s_w[il + 1];
+                    const uint32_t tl0 = ts32[il];
+                    const double vlo_i = __dadd_rn(wl0, __dmul_rn(div_u32(lo - tl0, ts32[il + 1] - tl0), __dsub_rn(wl1, wl0)));
+                    const double vlo = glo <= cx.ts0 ? cx.w0 : (glo >= cx.tsl ? cx.wl : vlo_i);
+                    const double wh0 = s_w[b], wh1 = s_w[b + 1];
+                    const uint32_t th0 = ts32[b];
+                    const double vhi_i = __dadd_rn(wh0, __dmul_rn(div_u32(hi - th0, ts32[b + 1] - th0), __dsub_rn(wh1, wh0)));
+                    const double vhi = ghi <= cx.ts0 ? cx.w0 : (ghi >= cx.tsl ? cx.wl : vhi_i);
+                    one = m <= 0;  // one piece [lo, hi]
+                    const double wa = s_w[a];
+                    const double vn = one ? vhi : __dadd_rn(wa, __dsub_rn(s_w[a + 1], wa));
+                    F2 = __dmul_rn(__dadd_rn(vlo, vn), (double)((one ? hi : ta1) - lo));
+                    const double wbm = s_w[b > 0 ? b - 1 : 0];
+                    L2 = __dmul_rn(__dadd_rn(__dadd_rn(wbm, __dsub_rn(wh0, wbm)), vhi), (double)(hi - th0));
                 }
+                // |F2|, |L2| < 2^24 follow from the bound: rni is exact in int64
+                long long tq = __double2ll_rn(__dmul_rn(F2, 549755813888.0));
+                if (!one) tq += __double2ll_rn(__dmul_rn(L2, 549755813888.0)) + (long long)(P[b] - P[a + 1]);
+                J = div_1e6(__dmul_rn((double)tq, 9.094947017729282379150390625e-13));  // * 2^-40
             }
             if (!ok) {
-                push_long(p, j, k);
+                push_long(p, j, d.kq + v);
+            } else if (!(d.flags & 2)) {
+                d.out[v] = J;
             } else {
-                const int64_t oidx = p.perm[j] ? __ldg(p.perm[j] + k) : k;
-                p.out[j][oidx] = J;
+                p.out[j][__ldg(p.perm[j] + d.kq + v)] = J;
             }
         }
         __syncwarp();
