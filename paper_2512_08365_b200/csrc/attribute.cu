@@ -1087,9 +1087,9 @@ struct __align__(16) GroupSmemX {
     uint32_t ts32[2][WINX];
     SetDescX desc[2][DW_MAX_SETS];
     unsigned long long wtot[NCW];    // warp totals of the q scan (mod 2^64)
-    long long red[NCW][4];           // warp shares of the exact tile sum: 21-bit limb sums + int128 spill
+    long long red[2][NCW][2];        // warp shares of the exact tile sum (by tile parity)
     uint32_t wmax[NCW];              // warp max of the high word of |w|
-    int next_it;
+    int next_it[2];                  // claimed next tile, by parity (claimed during pass B)
 };
 
 // Interior value v(x) of a linear signal at window slot r (energy.py:115-124:
@@ -1152,7 +1152,7 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (tid < GROUPS) groups[tid].next_it = tid;
+    if (tid < GROUPS) groups[tid].next_it[0] = tid;
     if (tid == 0) sm.claim = GROUPS;
     __syncthreads();
 
@@ -1166,14 +1166,14 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
     GroupSmemX &gs = groups[g];
     int par = 0;
     for (;; par ^= 1) {
-        const int it = gs.next_it;
+        const int it = gs.next_it[par];
         const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
         if (tile >= p.ntiles) break;
         const int stage = it % XSTAGES;
         mbar_wait(&sm.full[stage], (uint32_t)((it / XSTAGES) & 1));
 #ifdef DW_SKIP_CONSUMERS
         consumer_sync(g);
-        if (ctid == 0) gs.next_it = atomicAdd(&sm.claim, 1);
+        if (ctid == 0) gs.next_it[par ^ 1] = atomicAdd(&sm.claim, 1);
         consumer_sync(g);
         if (lane == 0) mbar_arrive(&sm.empty[stage]);
         continue;
@@ -1210,6 +1210,8 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
             gs.desc[par][j] = d;
         }
 
+        // the group's next tile, claimed early (read after this tile's barriers)
+        if (ctid == 32) gs.next_it[par ^ 1] = atomicAdd(&sm.claim, 1);
         // ---- pass B: pieces rb .. rb + XPER - 1 (r < last)
         const int rb = r0 + ctid * XPER;
         long long q[XPER];
@@ -1309,8 +1311,8 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
             if (lane == 0) {
                 const i128 t = (i128)l0 + ((i128)l1 << 21) + ((i128)l2 << 42) + spill;
                 const I128Parts pp = split(t);
-                gs.red[warp][0] = (long long)pp.lo;
-                gs.red[warp][1] = (long long)pp.hi;
+                gs.red[par][warp][0] = (long long)pp.lo;
+                gs.red[par][warp][1] = (long long)pp.hi;
                 gs.wmax[warp] = wm;
             }
         }
@@ -1323,15 +1325,6 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
             }
         }
         consumer_sync(g);
-        if (ctid == 0) {
-            gs.next_it = atomicAdd(&sm.claim, 1);  // every thread has read it
-            i128 t = 0;
-#pragma unroll
-            for (int k = 0; k < NCW; ++k) t += join((uint64_t)gs.red[k][0], (uint64_t)gs.red[k][1]);
-            const I128Parts pp = split(t);
-            p.tile_fx[2 * tile] = pp.lo;
-            p.tile_fx[2 * tile + 1] = pp.hi;
-        }
         // ---- the exclusive window prefix into the stage's timestamp slots
         uint32_t wmx_hi = 0;
         {
@@ -1358,6 +1351,14 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
         }
         consumer_sync(g);
         const unsigned long long *P = reinterpret_cast<const unsigned long long *>(s_ts);
+        if (ctid == 32) {  // the exact tile sum (its shares are double buffered)
+            i128 t = 0;
+#pragma unroll
+            for (int k = 0; k < NCW; ++k) t += join((uint64_t)gs.red[par][k][0], (uint64_t)gs.red[par][k][1]);
+            const I128Parts pp = split(t);
+            p.tile_fx[2 * tile] = pp.lo;
+            p.tile_fx[2 * tile + 1] = pp.hi;
+        }
         // max |w| over the window, rounded up (NaN / inf: every bound test fails)
         const double wmx = __hiloint2double((int)(wmx_hi + 1u), 0);
 
