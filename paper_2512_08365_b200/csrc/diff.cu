@@ -617,6 +617,565 @@ __global__ void join_findings_b_kernel(int64_t na, int64_t n_bonly, const int32_
     if (epw_b) epw_b[f] = div_or_same(eb, B.work, j);
 }
 
+// ---------------------------------------------------- K5' bucketed join (no sort)
+// The pairing needs, per signature, its A ops and its B ops in op order; the
+// t-th A occurrence pairs with the t-th B occurrence.  Instead of a full radix
+// sort by signature id, the ops are partitioned ONCE by signature bucket (a
+// range of JB_SPB table slots) with a stable scatter, and one CTA per bucket
+// ranks the occurrences of its few hundred signatures in shared memory:
+//   jb_hash      per op: table slot of its signature (as K5), plus the per-tile
+//                histogram of the bucket id's low 6-bit digit;
+//   jb_pass<1>, jb_hist2, jb_pass<2>
+//                two stable partition passes (LSD radix, 6-bit digits of the
+//                12-bit bucket id), each with its tile x digit count matrix
+//                scanned digit-major (jb_colsum / jb_base / jb_apply): the ops
+//                end up grouped by bucket, in op order inside a bucket, as
+//                (slot << 32 | op index);
+//   jb_bounds    each bucket's range (binary search of the grouped column);
+//   jb_bucket    per bucket: B's occurrences ranked per slot the same way and
+//                laid out by (slot, occurrence); A's occurrences ranked and
+//                paired with B's t-th occurrence; the pairs go straight into
+//                the A-window stage of K5's findings pass; B ops beyond A's
+//                count of their signature set a bit of the B-only bitmap;
+//   jb_bonly_*   the bitmap compacted into the B-only list, in B order.
+constexpr int JB_NB = 2048;             // signature buckets (+1 for the all-ones signature)
+constexpr int JB_NBB = JB_NB + 1;       // bucket ids < 2^12: two 6-bit digits
+constexpr int JB_SPB_MAX = 2048;        // table slots per bucket: cap <= JB_NB * JB_SPB_MAX
+constexpr int JB_THREADS = 512;         // 16 warps
+constexpr int JB_WARPS = JB_THREADS / 32;
+constexpr int JB_DIG = 64;              // radix of the two partition passes
+constexpr int JB_T1 = 8192;             // ops per tile, hash + pass 1
+constexpr int JB_T2 = 8192;             // ops per tile, pass 2 (16 per thread; JB_T1 == JB_T2)
+constexpr int JB_SEG = 256;             // tile segments of a matrix scan
+
+struct JbSide {
+    const uint64_t *sig;
+    int64_t n;
+    uint32_t *slot;            // [n] table slot of each op's signature (cap: the all-ones signature)
+    uint32_t *mat1, *mat2;     // [ntile][JB_DIG] digit counts -> output offsets, passes 1 / 2
+    uint32_t *part;            // [JB_SEG][JB_DIG] scan scratch
+    unsigned long long *tmp;   // [n] after pass 1: (slot << 32 | op index), by low digit
+    unsigned long long *scat;  // [n] after pass 2: by bucket, op order kept inside a bucket
+    uint32_t *bstart;          // [JB_NBB + 1] first position of each bucket in scat
+};
+
+struct JbParams {
+    JbSide s[2];
+    int64_t nt1[2], nt2[2];    // tiles per side, passes 1 / 2
+    uint64_t *table;
+    int64_t cap;
+    int shift;                 // bucket = slot >> shift
+    unsigned long long *overflow;
+};
+
+__device__ __forceinline__ uint32_t jb_slot(const JbParams &q, uint64_t s) {
+    if (s == EMPTY) return (uint32_t)q.cap;  // its own bucket (JB_NB)
+    const uint64_t mask = (uint64_t)q.cap - 1;
+    uint64_t h = mix64(s) & mask;
+    for (int64_t probe = 0; probe < q.cap; ++probe) {
+        uint64_t k = q.table[h];
+        if (k == EMPTY) k = atomicCAS((unsigned long long *)&q.table[h], EMPTY, s);
+        if (k == EMPTY || k == s) return (uint32_t)h;
+        h = (h + 1) & mask;
+    }
+    atomicAdd(q.overflow, 1ULL);
+    return (uint32_t)q.cap;
+}
+
+// grid: tiles of side 0 then side 1 (per pass)
+__device__ __forceinline__ int jb_side_of(const int64_t *nt, int64_t &t) {
+    t = blockIdx.x;
+    if (t < nt[0]) return 0;
+    t -= nt[0];
+    return 1;
+}
+
+__global__ void __launch_bounds__(JB_THREADS) jb_hash_kernel(JbParams q) {
+    __shared__ unsigned int h[JB_DIG];
+    int64_t t;
+    const int side = jb_side_of(q.nt1, t);
+    const JbSide &S = q.s[side];
+    if (threadIdx.x < JB_DIG) h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t i0 = t * JB_T1, i1 = min(i0 + JB_T1, S.n);
+    for (int64_t base = i0 + threadIdx.x; base < i1; base += (int64_t)JB_THREADS * ITEMS) {
+        uint64_t sg[ITEMS];
+#pragma unroll
+        for (int u = 0; u < ITEMS; ++u) {
+            const int64_t i = base + (int64_t)u * JB_THREADS;
+            sg[u] = i < i1 ? __ldcs(S.sig + i) : EMPTY;
+        }
+#pragma unroll
+        for (int u = 0; u < ITEMS; ++u) {
+            const int64_t i = base + (int64_t)u * JB_THREADS;
+            if (i >= i1) continue;
+            const uint32_t sl = jb_slot(q, sg[u]);
+            S.slot[i] = sl;
+            atomicAdd(&h[(sl >> q.shift) & (JB_DIG - 1)], 1u);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < JB_DIG) S.mat1[t * JB_DIG + threadIdx.x] = h[threadIdx.x];
+}
+
+// Digit-major exclusive scan of a [ntile][JB_DIG] count matrix, in place:
+// segment sums, then (one block per side) digit totals, digit bases and
+// segment bases, then the segments' running sums.
+__global__ void jb_colsum_kernel(JbParams q, int pass) {
+    const int side = blockIdx.y;
+    const JbSide &S = q.s[side];
+    uint32_t *mat = pass == 1 ? S.mat1 : S.mat2;
+    const int64_t nt = pass == 1 ? q.nt1[side] : q.nt2[side];
+    const int d = threadIdx.x & (JB_DIG - 1);
+    const int seg = blockIdx.x * (blockDim.x / JB_DIG) + threadIdx.x / JB_DIG;
+    if (seg >= JB_SEG) return;
+    const int64_t per = ceil_div(nt, JB_SEG);
+    const int64_t t0 = seg * per, t1 = min(t0 + per, nt);
+    uint32_t sum = 0;
+    for (int64_t t = t0; t < t1; ++t) sum += mat[t * JB_DIG + d];
+    S.part[seg * JB_DIG + d] = sum;
+}
+
+__global__ void __launch_bounds__(JB_DIG) jb_base_kernel(JbParams q) {
+    const JbSide &S = q.s[blockIdx.x];
+    const int d = threadIdx.x;  // one thread per digit
+    uint32_t tot = 0;
+    for (int seg = 0; seg < JB_SEG; ++seg) tot += S.part[seg * JB_DIG + d];
+    // exclusive scan of the 64 digit totals (two warps)
+    __shared__ uint32_t ws[2];
+    const int lane = d & 31, warp = d >> 5;
+    uint32_t x = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    uint32_t run = (warp ? ws[0] : 0) + x - tot;
+    for (int seg = 0; seg < JB_SEG; ++seg) {
+        const uint32_t v = S.part[seg * JB_DIG + d];
+        S.part[seg * JB_DIG + d] = run;
+        run += v;
+    }
+}
+
+__global__ void jb_apply_kernel(JbParams q, int pass) {
+    const int side = blockIdx.y;
+    const JbSide &S = q.s[side];
+    uint32_t *mat = pass == 1 ? S.mat1 : S.mat2;
+    const int64_t nt = pass == 1 ? q.nt1[side] : q.nt2[side];
+    const int d = threadIdx.x & (JB_DIG - 1);
+    const int seg = blockIdx.x * (blockDim.x / JB_DIG) + threadIdx.x / JB_DIG;
+    if (seg >= JB_SEG) return;
+    const int64_t per = ceil_div(nt, JB_SEG);
+    const int64_t t0 = seg * per, t1 = min(t0 + per, nt);
+    uint32_t run = S.part[seg * JB_DIG + d];
+    for (int64_t t = t0; t < t1; ++t) {
+        const uint32_t v = mat[t * JB_DIG + d];
+        mat[t * JB_DIG + d] = run;
+        run += v;
+    }
+}
+
+// Stable rank of equal keys inside one 32-item step of a warp: each lane ORs
+// its bit into the warp-private mask of its key; the mask read back is the
+// lanes holding that key (CUB onesweep's atomic-OR match); the masks are
+// cleared for the next step.  (The bucket kernel's slot ranking.)
+__device__ __forceinline__ unsigned jb_peers(uint32_t *bins, uint32_t key, bool valid) {
+    const int lane = threadIdx.x & 31;
+    if (valid) atomicOr(&bins[key], 1u << lane);
+    __syncwarp();
+    const unsigned peers = valid ? bins[key] : 0u;
+    __syncwarp();
+    if (valid) bins[key] = 0u;
+    __syncwarp();
+    return peers;
+}
+
+// Warp multisplit on a 6-bit digit with no shared memory: six ballots give,
+// for every digit, the lanes holding it (the AND of the bit masks); lane l
+// keeps the warp's running counts of digits l and l + 32 in registers, and a
+// lane reads its digit's count from the owner with one shuffle.
+struct Split6 {
+    unsigned m[6];
+    __device__ __forceinline__ void vote(uint32_t d, bool valid) {
+        const unsigned v = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int b = 0; b < 6; ++b) m[b] = __ballot_sync(0xffffffffu, (d >> b) & 1u) & v;
+        m0 = v;
+    }
+    __device__ __forceinline__ unsigned lanes_of(uint32_t d) const {
+        unsigned r = m0;
+#pragma unroll
+        for (int b = 0; b < 6; ++b) r &= ((d >> b) & 1u) ? m[b] : ~m[b];
+        return r;
+    }
+    unsigned m0;
+};
+
+// One stable partition pass by a 6-bit digit of the bucket id (tile of
+// JB_T2 ops, 16 per thread).  Each warp owns a contiguous stretch of the
+// tile: counts per digit (Split6), a scan over the tile (digit-major, warps
+// in order inside a digit), then in op order every op's rank among equal
+// digits against the warp's running counts; the ops are laid out by digit in
+// shared memory and written out in runs (coalesced), at the tile's offset of
+// each digit from the scanned count matrix.
+template <int PASS>
+__global__ void __launch_bounds__(JB_THREADS, 2) jb_pass_kernel(JbParams q) {
+    constexpr int STEPS = JB_T2 / JB_THREADS;  // ops per lane
+    extern __shared__ __align__(16) unsigned char jb_smem[];
+    unsigned long long *lay = reinterpret_cast<unsigned long long *>(jb_smem);  // [JB_T2]
+    __shared__ uint32_t cnt[JB_WARPS][JB_DIG];
+    __shared__ uint32_t lstart[JB_DIG], gstart[JB_DIG], half0;
+    int64_t t;
+    const int side = jb_side_of(q.nt2, t);
+    const JbSide &S = q.s[side];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t t0 = t * JB_T2;
+    const int nt = (int)min((int64_t)JB_T2, S.n - t0);
+    const int64_t w0 = t0 + (int64_t)warp * (STEPS * 32);
+    const int dshift = 32 + q.shift + (PASS == 1 ? 0 : 6);
+    unsigned long long e[STEPS];  // (slot << 32 | op index)
+#pragma unroll
+    for (int k = 0; k < STEPS; ++k) {
+        const int64_t i = w0 + k * 32 + lane;
+        if (PASS == 1)
+            e[k] = i < S.n ? ((unsigned long long)__ldcs(S.slot + i) << 32) | (unsigned long long)(uint32_t)i
+                           : ~0ULL;
+        else
+            e[k] = i < S.n ? __ldcs(S.tmp + i) : ~0ULL;
+    }
+    // counts of digits lane and lane + 32 over this warp's stretch
+    uint32_t c_lo = 0, c_hi = 0;
+#pragma unroll
+    for (int k = 0; k < STEPS; ++k) {
+        Split6 sp;
+        sp.vote((uint32_t)(e[k] >> dshift) & (JB_DIG - 1), e[k] != ~0ULL);
+        c_lo += __popc(sp.lanes_of((uint32_t)lane));
+        c_hi += __popc(sp.lanes_of((uint32_t)lane + 32));
+    }
+    cnt[warp][lane] = c_lo;
+    cnt[warp][lane + 32] = c_hi;
+    __syncthreads();
+    if (warp < 2) {  // digit d = threadIdx.x: tile total, its start inside the tile (two 32-digit halves)
+        const int d = threadIdx.x;
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < JB_WARPS; ++w) tot += cnt[w][d];
+        uint32_t x = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        lstart[d] = x - tot;
+        if (d == 31) half0 = x;
+        gstart[d] = (PASS == 1 ? S.mat1 : S.mat2)[t * JB_DIG + d];
+    }
+    __syncthreads();
+    if (warp < 2) {  // digit starts, and each warp's base inside its digits
+        const int d = threadIdx.x;
+        uint32_t run = lstart[d] + (d >= 32 ? half0 : 0);
+        lstart[d] = run;
+#pragma unroll
+        for (int w = 0; w < JB_WARPS; ++w) {
+            const uint32_t c = cnt[w][d];
+            cnt[w][d] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    c_lo = cnt[warp][lane];
+    c_hi = cnt[warp][lane + 32];
+#pragma unroll
+    for (int k = 0; k < STEPS; ++k) {
+        const bool valid = e[k] != ~0ULL;
+        const uint32_t d = (uint32_t)(e[k] >> dshift) & (JB_DIG - 1);
+        Split6 sp;
+        sp.vote(d, valid);
+        const unsigned peers = sp.lanes_of(d);
+        const uint32_t lo = __shfl_sync(0xffffffffu, c_lo, d & 31), hi = __shfl_sync(0xffffffffu, c_hi, d & 31);
+        if (valid) lay[(d & 32 ? hi : lo) + __popc(peers & ((1u << lane) - 1u))] = e[k];
+        c_lo += __popc(sp.lanes_of((uint32_t)lane));
+        c_hi += __popc(sp.lanes_of((uint32_t)lane + 32));
+    }
+    __syncthreads();
+    unsigned long long *dst = PASS == 1 ? S.tmp : S.scat;
+#pragma unroll 4
+    for (int x = threadIdx.x; x < nt; x += JB_THREADS) {  // runs per digit: consecutive threads, consecutive positions
+        const unsigned long long v = lay[x];
+        const uint32_t d = (uint32_t)(v >> dshift) & (JB_DIG - 1);
+        dst[gstart[d] + (x - lstart[d])] = v;
+    }
+}
+
+// histogram of pass 2's digit over pass 1's output, per pass-2 tile
+__global__ void __launch_bounds__(256) jb_hist2_kernel(JbParams q) {
+    __shared__ unsigned int h[JB_DIG];
+    int64_t t;
+    const int side = jb_side_of(q.nt2, t);
+    const JbSide &S = q.s[side];
+    if (threadIdx.x < JB_DIG) h[threadIdx.x] = 0;
+    __syncthreads();
+    const int64_t i0 = t * JB_T2, i1 = min(i0 + JB_T2, S.n);
+    const int dshift = 32 + q.shift + 6;
+    for (int64_t i = i0 + threadIdx.x; i < i1; i += 256)
+        atomicAdd(&h[(uint32_t)(__ldcs(S.tmp + i) >> dshift) & (JB_DIG - 1)], 1u);
+    __syncthreads();
+    if (threadIdx.x < JB_DIG) S.mat2[t * JB_DIG + threadIdx.x] = h[threadIdx.x];
+}
+
+// bucket boundaries in the partitioned column (sorted by bucket): one thread per bucket
+__global__ void jb_bounds_kernel(JbParams q) {
+    const int side = blockIdx.y;
+    const JbSide &S = q.s[side];
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > JB_NBB) return;
+    int64_t lo = 0, hi = S.n;  // first position with bucket >= b
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if ((uint32_t)(__ldg(S.scat + mid) >> (32 + q.shift)) < (uint32_t)b) lo = mid + 1; else hi = mid;
+    }
+    S.bstart[b] = (uint32_t)lo;
+}
+
+// A warp's walk of [s0, s1) in order, 32 items per step, JB_PF steps of
+// loads issued together (independent loads in flight) before they are used.
+constexpr int JB_PF = 8;
+template <typename F>
+__device__ __forceinline__ void jb_walk(const unsigned long long *src, uint32_t s0, uint32_t s1, F &&f) {
+    const int lane = threadIdx.x & 31;
+    for (uint32_t c = s0; c < s1; c += 32 * JB_PF) {
+        unsigned long long e[JB_PF];
+#pragma unroll
+        for (int k = 0; k < JB_PF; ++k) {
+            const uint32_t x = c + k * 32 + lane;
+            e[k] = x < s1 ? __ldcg(src + x) : 0ULL;
+        }
+#pragma unroll
+        for (int k = 0; k < JB_PF; ++k) f(e[k], c + k * 32 + lane < s1);
+    }
+}
+
+struct JbBucketOut {
+    uint32_t *bsorted;           // [nb] B ops laid out by (bucket, slot, occurrence)
+    unsigned int *cursor;        // [PAIR_MAXB] A-stage bucket fill
+    uint2 *stage;                // A-stage (i, partner) by i >> PAIR_BSH
+    uint32_t *bonly_bits;        // [ceil(nb / 32)]
+};
+
+// dynamic smem: cw[JB_WARPS][spb] + bins[JB_WARPS][spb] (u32) + totA, totB, startB [spb] + sbh[PAIR_MAXB]
+__global__ void __launch_bounds__(JB_THREADS) jb_bucket_kernel(JbParams q, JbBucketOut o) {
+    extern __shared__ __align__(16) unsigned char jb_smem[];
+    const int spb = 1 << q.shift;
+    uint32_t *cw = reinterpret_cast<uint32_t *>(jb_smem);
+    uint32_t *binw = cw + JB_WARPS * spb;  // this warp's masks: binw + warp * spb
+    uint32_t *totA = binw + JB_WARPS * spb;
+    uint32_t *totB = totA + spb;
+    uint32_t *startB = totB + spb;
+    unsigned int *sbh = startB + spb;
+    __shared__ uint32_t wsum[JB_WARPS];
+    const int b = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const JbSide &A = q.s[0], &B = q.s[1];
+    const uint32_t a0 = A.bstart[b], a1 = A.bstart[b + 1];
+    const uint32_t b0 = B.bstart[b], b1 = B.bstart[b + 1];
+    const int nslot = b == JB_NB ? 1 : spb;
+    const uint32_t smask = (uint32_t)spb - 1u;
+    for (int k = threadIdx.x; k < JB_WARPS * spb; k += JB_THREADS) binw[k] = 0;
+    // this warp's contiguous segment of [lo, hi)
+    auto seg = [&](uint32_t lo, uint32_t hi, uint32_t &s0, uint32_t &s1) {
+        const uint32_t per = (hi - lo + JB_WARPS - 1) / JB_WARPS;
+        s0 = min(lo + warp * per, hi);
+        s1 = min(s0 + per, hi);
+    };
+    // per-warp counts of the slots over [lo, hi) -> cross-warp exclusive bases, totals
+    auto count_pass = [&](const unsigned long long *src, uint32_t lo, uint32_t hi, uint32_t *tot, bool stage_hist) {
+        for (int k = threadIdx.x; k < JB_WARPS * spb; k += JB_THREADS) cw[k] = 0;
+        if (stage_hist)
+            for (int k = threadIdx.x; k < PAIR_MAXB; k += JB_THREADS) sbh[k] = 0;
+        __syncthreads();
+        uint32_t s0, s1;
+        seg(lo, hi, s0, s1);
+        uint32_t *mc = cw + warp * spb;
+        jb_walk(src, s0, s1, [&](unsigned long long e, bool valid) {
+            if (!valid) return;
+            atomicAdd(&mc[(uint32_t)(e >> 32) & smask], 1u);
+            if (stage_hist) atomicAdd(&sbh[(uint32_t)e >> PAIR_BSH], 1u);
+        });
+        __syncthreads();
+        for (int s = threadIdx.x; s < nslot; s += JB_THREADS) {
+            uint32_t run = 0;
+#pragma unroll
+            for (int w = 0; w < JB_WARPS; ++w) {
+                const uint32_t c = cw[w * spb + s];
+                cw[w * spb + s] = run;
+                run += c;
+            }
+            tot[s] = run;
+        }
+        __syncthreads();
+    };
+    // ---- B: occurrences by slot, laid out at bsorted[b0 + startB[s] + occ]
+    count_pass(B.scat, b0, b1, totB, false);
+    {  // startB = exclusive scan of totB over the slots
+        uint32_t carry = 0;
+        for (int c = 0; c < nslot; c += JB_THREADS) {
+            const int s = c + threadIdx.x;
+            const uint32_t v = s < nslot ? totB[s] : 0;
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) wsum[warp] = x;
+            __syncthreads();
+            uint32_t wb = 0, all = 0;
+#pragma unroll
+            for (int w = 0; w < JB_WARPS; ++w) {
+                const uint32_t ws = wsum[w];
+                if (w < warp) wb += ws;
+                all += ws;
+            }
+            if (s < nslot) startB[s] = carry + wb + x - v;
+            carry += all;
+            __syncthreads();
+        }
+    }
+    {
+        uint32_t s0, s1;
+        seg(b0, b1, s0, s1);
+        uint32_t *mc = cw + warp * spb;
+        jb_walk(B.scat, s0, s1, [&](unsigned long long e, bool valid) {
+            const uint32_t sl = (uint32_t)(e >> 32) & smask;
+            const unsigned peers = jb_peers(binw + warp * spb, sl, valid);
+            const int below = __popc(peers & ((1u << lane) - 1u));
+            const uint32_t occ = valid ? mc[sl] + below : 0;
+            __syncwarp();
+            if (valid && below == 0) mc[sl] += __popc(peers);
+            __syncwarp();
+            if (valid) o.bsorted[b0 + startB[sl] + occ] = (uint32_t)e;
+        });
+    }
+    __syncthreads();  // bsorted of this bucket complete (block-visible)
+    // ---- A: occurrences by slot, paired with B's t-th occurrence
+    count_pass(A.scat, a0, a1, totA, true);
+    for (int k = threadIdx.x; k < PAIR_MAXB; k += JB_THREADS)  // reserve this bucket's A-stage ranges
+        if (sbh[k]) sbh[k] = atomicAdd(o.cursor + k, sbh[k]);
+    for (int s = threadIdx.x; s < nslot; s += JB_THREADS) {  // B occurrences beyond A's count: B-only
+        for (uint32_t t = totA[s]; t < totB[s]; ++t) {
+            const uint32_t j = o.bsorted[b0 + startB[s] + t];
+            atomicOr(o.bonly_bits + (j >> 5), 1u << (j & 31));
+        }
+    }
+    __syncthreads();
+    {
+        uint32_t s0, s1;
+        seg(a0, a1, s0, s1);
+        uint32_t *mc = cw + warp * spb;
+        jb_walk(A.scat, s0, s1, [&](unsigned long long e, bool valid) {
+            const uint32_t sl = (uint32_t)(e >> 32) & smask, i = (uint32_t)e;
+            const unsigned peers = jb_peers(binw + warp * spb, sl, valid);
+            const int below = __popc(peers & ((1u << lane) - 1u));
+            const uint32_t occ = valid ? mc[sl] + below : 0;
+            __syncwarp();
+            if (valid && below == 0) mc[sl] += __popc(peers);
+            __syncwarp();
+            if (valid) {
+                const int32_t j = occ < totB[sl] ? (int32_t)o.bsorted[b0 + startB[sl] + occ] : -1;
+                const unsigned pos = atomicAdd(&sbh[i >> PAIR_BSH], 1u);
+                o.stage[((int64_t)(i >> PAIR_BSH) << PAIR_BSH) + pos] = make_uint2(i, (uint32_t)j);
+            }
+        });
+    }
+}
+
+// B-only list from the bitmap, in B order: per-block popcounts, their scan, writes
+constexpr int BO_WORDS = 2048;  // bitmap words per block (8 per thread)
+__global__ void __launch_bounds__(256) bonly_count_kernel(const uint32_t *bits, int64_t nw, uint32_t *bsum) {
+    uint32_t c = 0;
+    const int64_t w0 = (int64_t)blockIdx.x * BO_WORDS;
+    for (int k = threadIdx.x; k < BO_WORDS; k += 256) c += w0 + k < nw ? __popc(bits[w0 + k]) : 0;
+    c = __reduce_add_sync(0xffffffffu, c);
+    __shared__ uint32_t s[8];
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < 8; ++w) t += s[w];
+        bsum[blockIdx.x] = t;
+    }
+}
+__global__ void __launch_bounds__(1024) bonly_scan_kernel(uint32_t *bsum, int64_t nblk, unsigned int *total) {
+    __shared__ uint32_t carry;
+    __shared__ uint32_t ws[32];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t c = 0; c < nblk; c += 1024) {
+        const int64_t k = c + threadIdx.x;
+        const uint32_t v = k < nblk ? bsum[k] : 0;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) ws[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = ws[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            ws[lane] = w;
+        }
+        __syncthreads();
+        if (k < nblk) bsum[k] = carry + (warp ? ws[warp - 1] : 0) + x - v;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += ws[31];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+__global__ void __launch_bounds__(256) bonly_write_kernel(const uint32_t *bits, int64_t nw, const uint32_t *bsum,
+                                                          int32_t *out) {
+    // each thread owns 8 consecutive words; thread order = word order
+    const int64_t w0 = (int64_t)blockIdx.x * BO_WORDS + threadIdx.x * 8;
+    uint32_t wv[8];
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        wv[k] = w0 + k < nw ? bits[w0 + k] : 0u;
+        c += __popc(wv[k]);
+    }
+    __shared__ uint32_t ws[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) ws[warp] = x;
+    __syncthreads();
+    uint32_t base = bsum[blockIdx.x] + x - c;
+    for (int w = 0; w < warp; ++w) base += ws[w];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        uint32_t m = wv[k];
+        while (m) {
+            const int bit = __ffs(m) - 1;
+            m &= m - 1;
+            out[base++] = (int32_t)(((w0 + k) << 5) + bit);
+        }
+    }
+}
+
 // ================================================================ host side
 static size_t au(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -782,7 +1341,12 @@ struct JoinLayout {
     size_t table, counters, id_a, id_b, ix_a, ix_b, sid_a, sid_b, six_a, six_b, first_a, end_a,
         first_b, end_b,
         bonly_tmp, pair_stage, pair_cursor, win_stage, win_cursor, cub, cub_bytes, total;
-    int64_t cap, D;
+    // bucketed join (jb): tile x bucket matrices, segment sums, bucket starts,
+    // scattered ops, B by (slot, occurrence), B-only bitmap and block sums
+    size_t mat_a, mat_b, mat2_a, mat2_b, part_a, part_b, bst_a, bst_b, tmp_a, tmp_b, scat_a, scat_b, bsorted,
+        bbits, bsum;
+    int64_t cap, D, nt1_a, nt1_b, nt2_a, nt2_b, nw, nblk;
+    bool jb;
 };
 
 static int64_t pow2_at_least(int64_t x) {
@@ -791,16 +1355,49 @@ static int64_t pow2_at_least(int64_t x) {
     return p;
 }
 
+// The bucketed join handles tables of up to JB_NB * JB_SPB_MAX slots (2M
+// distinct signatures); larger ones take the sort-based path.
 static JoinLayout join_layout(int64_t na, int64_t nb, int64_t max_distinct) {
     JoinLayout L{};
     if (max_distinct <= 0 || max_distinct > na + nb) max_distinct = na + nb;
-    L.cap = pow2_at_least(std::max<int64_t>(1024, 2 * max_distinct));
+    L.cap = pow2_at_least(std::max<int64_t>(4096, 2 * max_distinct));
+    L.jb = L.cap <= (int64_t)JB_NB * JB_SPB_MAX;
     L.D = L.cap + 2;  // ids are table slots + 1; 0 reserved
     size_t off = 0;
     L.table = off; off += au(8 * L.cap);
     L.counters = off; off += au(64);
     L.id_a = off; off += au(4 * na);
     L.id_b = off; off += au(4 * nb);
+    L.bonly_tmp = off; off += au(4 * std::max<int64_t>(nb, 1));
+    L.pair_stage = off; off += au(8 * std::max<int64_t>(na, 1));
+    L.pair_cursor = off; off += au(4 * PAIR_MAXB);
+    L.win_stage = off; off += au(8 * std::max<int64_t>(na, 1));
+    L.win_cursor = off; off += au(4 * ((std::max<int64_t>(na, 1) + WIN_OPS - 1) / WIN_OPS));
+    if (L.jb) {
+        L.nt1_a = ceil_div(na, JB_T1);
+        L.nt1_b = ceil_div(nb, JB_T1);
+        L.nt2_a = ceil_div(na, JB_T2);
+        L.nt2_b = ceil_div(nb, JB_T2);
+        L.mat_a = off; off += au(4 * JB_DIG * L.nt1_a);
+        L.mat_b = off; off += au(4 * JB_DIG * L.nt1_b);
+        L.mat2_a = off; off += au(4 * JB_DIG * L.nt2_a);
+        L.mat2_b = off; off += au(4 * JB_DIG * L.nt2_b);
+        L.part_a = off; off += au(4 * JB_SEG * JB_DIG);
+        L.part_b = off; off += au(4 * JB_SEG * JB_DIG);
+        L.bst_a = off; off += au(4 * (JB_NBB + 1));
+        L.bst_b = off; off += au(4 * (JB_NBB + 1));
+        L.tmp_a = off; off += au(8 * na);
+        L.tmp_b = off; off += au(8 * nb);
+        L.scat_a = off; off += au(8 * na);
+        L.scat_b = off; off += au(8 * nb);
+        L.bsorted = off; off += au(4 * nb);
+        L.nw = ceil_div(std::max<int64_t>(nb, 1), 32);
+        L.nblk = ceil_div(L.nw, BO_WORDS);
+        L.bbits = off; off += au(4 * L.nw);
+        L.bsum = off; off += au(4 * L.nblk);
+        L.total = off;
+        return L;
+    }
     L.ix_a = off; off += au(4 * na);
     L.ix_b = off; off += au(4 * nb);
     L.sid_a = off; off += au(4 * na);
@@ -811,11 +1408,6 @@ static JoinLayout join_layout(int64_t na, int64_t nb, int64_t max_distinct) {
     L.end_a = off; off += au(4 * L.D);
     L.first_b = off; off += au(4 * L.D);
     L.end_b = off; off += au(4 * L.D);
-    L.bonly_tmp = off; off += au(4 * std::max<int64_t>(nb, 1));
-    L.pair_stage = off; off += au(8 * std::max<int64_t>(na, 1));
-    L.pair_cursor = off; off += au(4 * PAIR_MAXB);
-    L.win_stage = off; off += au(8 * std::max<int64_t>(na, 1));
-    L.win_cursor = off; off += au(4 * ((std::max<int64_t>(na, 1) + WIN_OPS - 1) / WIN_OPS));
     size_t c1 = 0, c2 = 0;
     const int64_t nmax = std::max<int64_t>(std::max(na, nb), 1);
     cub::DeviceRadixSort::SortPairs(nullptr, c1, (const uint32_t *)nullptr, (uint32_t *)nullptr,
@@ -827,6 +1419,106 @@ static JoinLayout join_layout(int64_t na, int64_t nb, int64_t max_distinct) {
     off += au(L.cub_bytes);
     L.total = off;
     return L;
+}
+
+static int log2_exact(int64_t x) {
+    int b = 0;
+    while (((int64_t)1 << b) < x) ++b;
+    return b;
+}
+
+// phase 1 of the bucketed join: pairs into the A stage (by i >> PAIR_BSH), the
+// B-only list; returns the B-only count through *n_bonly (host)
+static int jb_pairing(const dw_join_side_t *a, const dw_join_side_t *b, const JoinLayout &L, char *base,
+                      int32_t *d_b_only, int64_t *n_bonly, cudaStream_t s) {
+    const int64_t na = a->n, nb = b->n;
+    unsigned long long *counters = (unsigned long long *)(base + L.counters);
+    JbParams q{};
+    q.table = (uint64_t *)(base + L.table);
+    q.cap = L.cap;
+    q.shift = log2_exact(L.cap / JB_NB);
+    q.overflow = counters;
+    const int64_t n2[2] = {na, nb};
+    const uint64_t *sig[2] = {a->d_sig, b->d_sig};
+    const size_t slot_off[2] = {L.id_a, L.id_b}, mat[2] = {L.mat_a, L.mat_b}, mat2[2] = {L.mat2_a, L.mat2_b},
+                 part[2] = {L.part_a, L.part_b}, bst[2] = {L.bst_a, L.bst_b}, tmp[2] = {L.tmp_a, L.tmp_b},
+                 scat[2] = {L.scat_a, L.scat_b};
+    q.nt1[0] = L.nt1_a;
+    q.nt1[1] = L.nt1_b;
+    q.nt2[0] = L.nt2_a;
+    q.nt2[1] = L.nt2_b;
+    for (int k = 0; k < 2; ++k) {
+        q.s[k].sig = sig[k];
+        q.s[k].n = n2[k];
+        q.s[k].slot = (uint32_t *)(base + slot_off[k]);
+        q.s[k].mat1 = (uint32_t *)(base + mat[k]);
+        q.s[k].mat2 = (uint32_t *)(base + mat2[k]);
+        q.s[k].part = (uint32_t *)(base + part[k]);
+        q.s[k].bstart = (uint32_t *)(base + bst[k]);
+        q.s[k].tmp = (unsigned long long *)(base + tmp[k]);
+        q.s[k].scat = (unsigned long long *)(base + scat[k]);
+    }
+    trace_mark(s, "join:start");
+    cudaMemsetAsync(counters, 0, 64, s);
+    cudaMemsetAsync(q.table, 0xFF, 8 * L.cap, s);
+    const unsigned tiles1 = (unsigned)(L.nt1_a + L.nt1_b), tiles2 = (unsigned)(L.nt2_a + L.nt2_b);
+    const dim3 sg(JB_SEG * JB_DIG / 256, 2);
+    cudaFuncSetAttribute(jb_pass_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * JB_T2);
+    cudaFuncSetAttribute(jb_pass_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * JB_T2);
+    if (tiles1) {
+        jb_hash_kernel<<<tiles1, JB_THREADS, 0, s>>>(q);
+        jb_colsum_kernel<<<sg, 256, 0, s>>>(q, 1);
+        jb_base_kernel<<<2, JB_DIG, 0, s>>>(q);
+        jb_apply_kernel<<<sg, 256, 0, s>>>(q, 1);
+        jb_pass_kernel<1><<<tiles1, JB_THREADS, 8 * JB_T2, s>>>(q);
+        jb_hist2_kernel<<<tiles2, 256, 0, s>>>(q);
+        jb_colsum_kernel<<<sg, 256, 0, s>>>(q, 2);
+        jb_base_kernel<<<2, JB_DIG, 0, s>>>(q);
+        jb_apply_kernel<<<sg, 256, 0, s>>>(q, 2);
+        jb_pass_kernel<2><<<tiles2, JB_THREADS, 8 * JB_T2, s>>>(q);
+        count_launch(10);
+    }
+    jb_bounds_kernel<<<dim3((JB_NBB + 1 + 255) / 256, 2), 256, 0, s>>>(q);
+    count_launch();
+    trace_mark(s, "join:partition");
+    JbBucketOut o{};
+    o.bsorted = (uint32_t *)(base + L.bsorted);
+    o.cursor = (unsigned int *)(base + L.pair_cursor);
+    o.stage = (uint2 *)(base + L.pair_stage);
+    o.bonly_bits = (uint32_t *)(base + L.bbits);
+    cudaMemsetAsync(o.cursor, 0, 4 * PAIR_MAXB, s);
+    cudaMemsetAsync(o.bonly_bits, 0, 4 * L.nw, s);
+    const int spb = 1 << q.shift;
+    const size_t smem_b = 4 * ((size_t)(2 * JB_WARPS + 3) * spb + PAIR_MAXB);
+    cudaFuncSetAttribute(jb_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
+    jb_bucket_kernel<<<JB_NBB, JB_THREADS, smem_b, s>>>(q, o);
+    count_launch();
+    trace_mark(s, "join:bucket");
+    if (na) {
+        unsigned int *cursor2 = (unsigned int *)(base + L.win_cursor);
+        uint2 *stage2 = (uint2 *)(base + L.win_stage);
+        const int64_t nwin = (na + WIN_OPS - 1) / WIN_OPS;
+        cudaMemsetAsync(cursor2, 0, 4 * nwin, s);
+        join_pair_sub_kernel<<<(unsigned)((na + SUB_CHUNK - 1) / SUB_CHUNK), 256, 0, s>>>(o.stage, na, cursor2,
+                                                                                           stage2);
+        count_launch();
+        trace_mark(s, "join:pair_sub");
+    }
+    unsigned int *n_bo = (unsigned int *)(counters + 3);
+    if (nb) {
+        uint32_t *bsum = (uint32_t *)(base + L.bsum);
+        bonly_count_kernel<<<(unsigned)L.nblk, 256, 0, s>>>(o.bonly_bits, L.nw, bsum);
+        bonly_scan_kernel<<<1, 1024, 0, s>>>(bsum, L.nblk, n_bo);
+        bonly_write_kernel<<<(unsigned)L.nblk, 256, 0, s>>>(o.bonly_bits, L.nw, bsum, d_b_only);
+        count_launch(3);
+        trace_mark(s, "join:bonly");
+    }
+    unsigned long long hc[4] = {0, 0, 0, 0};  // overflow, matched, -, n_bonly
+    cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return DW_E_CUDA;
+    if (hc[0]) return DW_E_WORKSPACE;  // more distinct signatures than the table holds
+    *n_bonly = (int64_t)(unsigned int)hc[3];
+    return DW_OK;
 }
 
 static int bits_for(int64_t D) {
@@ -892,7 +1584,11 @@ static int join_impl(const dw_join_side_t *a, const dw_join_side_t *b, int64_t m
     char *base = (char *)d_workspace;
     unsigned long long *counters = (unsigned long long *)(base + L.counters);
     int64_t b_only = 0;
-    if (phase & 1) {
+    if ((phase & 1) && L.jb) {
+        const int rc = jb_pairing(a, b, L, base, d_b_only, &b_only, s);
+        if (rc != DW_OK) return rc;
+        if (n_bonly_io) *n_bonly_io = b_only;
+    } else if (phase & 1) {
         JoinParams q{};
         q.sig_a = a->d_sig;
         q.sig_b = b->d_sig;
