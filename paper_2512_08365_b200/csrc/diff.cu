@@ -778,19 +778,17 @@ __global__ void jb_apply_kernel(JbParams q, int pass) {
     }
 }
 
-// Stable rank of equal keys inside one 32-item step of a warp: each lane ORs
-// its bit into the warp-private mask of its key; the mask read back is the
-// lanes holding that key (CUB onesweep's atomic-OR match); the masks are
-// cleared for the next step.  (The bucket kernel's slot ranking.)
-__device__ __forceinline__ unsigned jb_peers(uint32_t *bins, uint32_t key, bool valid) {
-    const int lane = threadIdx.x & 31;
-    if (valid) atomicOr(&bins[key], 1u << lane);
-    __syncwarp();
-    const unsigned peers = valid ? bins[key] : 0u;
-    __syncwarp();
-    if (valid) bins[key] = 0u;
-    __syncwarp();
-    return peers;
+// The lanes of a warp step holding the same key (< 2^NB), from NB ballots.
+template <int NB>
+__device__ __forceinline__ unsigned jb_vote_peers(uint32_t key, bool valid) {
+    unsigned r = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const bool on = (key >> b) & 1u;
+        const unsigned m = __ballot_sync(0xffffffffu, on);
+        r &= on ? m : ~m;
+    }
+    return valid ? r : 0u;
 }
 
 // Warp multisplit on a 6-bit digit with no shared memory: six ballots give,
@@ -965,13 +963,12 @@ struct JbBucketOut {
     uint32_t *bonly_bits;        // [ceil(nb / 32)]
 };
 
-// dynamic smem: cw[JB_WARPS][spb] + bins[JB_WARPS][spb] (u32) + totA, totB, startB [spb] + sbh[PAIR_MAXB]
+// dynamic smem: cw[JB_WARPS][spb] (u32) + totA, totB, startB [spb] + sbh[PAIR_MAXB]
 __global__ void __launch_bounds__(JB_THREADS) jb_bucket_kernel(JbParams q, JbBucketOut o) {
     extern __shared__ __align__(16) unsigned char jb_smem[];
     const int spb = 1 << q.shift;
     uint32_t *cw = reinterpret_cast<uint32_t *>(jb_smem);
-    uint32_t *binw = cw + JB_WARPS * spb;  // this warp's masks: binw + warp * spb
-    uint32_t *totA = binw + JB_WARPS * spb;
+    uint32_t *totA = cw + JB_WARPS * spb;
     uint32_t *totB = totA + spb;
     uint32_t *startB = totB + spb;
     unsigned int *sbh = startB + spb;
@@ -983,7 +980,6 @@ __global__ void __launch_bounds__(JB_THREADS) jb_bucket_kernel(JbParams q, JbBuc
     const uint32_t b0 = B.bstart[b], b1 = B.bstart[b + 1];
     const int nslot = b == JB_NB ? 1 : spb;
     const uint32_t smask = (uint32_t)spb - 1u;
-    for (int k = threadIdx.x; k < JB_WARPS * spb; k += JB_THREADS) binw[k] = 0;
     // this warp's contiguous segment of [lo, hi)
     auto seg = [&](uint32_t lo, uint32_t hi, uint32_t &s0, uint32_t &s1) {
         const uint32_t per = (hi - lo + JB_WARPS - 1) / JB_WARPS;
@@ -1050,7 +1046,7 @@ __global__ void __launch_bounds__(JB_THREADS) jb_bucket_kernel(JbParams q, JbBuc
         uint32_t *mc = cw + warp * spb;
         jb_walk(B.scat, s0, s1, [&](unsigned long long e, bool valid) {
             const uint32_t sl = (uint32_t)(e >> 32) & smask;
-            const unsigned peers = jb_peers(binw + warp * spb, sl, valid);
+            const unsigned peers = jb_vote_peers<11>(sl, valid);
             const int below = __popc(peers & ((1u << lane) - 1u));
             const uint32_t occ = valid ? mc[sl] + below : 0;
             __syncwarp();
@@ -1077,7 +1073,7 @@ __global__ void __launch_bounds__(JB_THREADS) jb_bucket_kernel(JbParams q, JbBuc
         uint32_t *mc = cw + warp * spb;
         jb_walk(A.scat, s0, s1, [&](unsigned long long e, bool valid) {
             const uint32_t sl = (uint32_t)(e >> 32) & smask, i = (uint32_t)e;
-            const unsigned peers = jb_peers(binw + warp * spb, sl, valid);
+            const unsigned peers = jb_vote_peers<11>(sl, valid);
             const int below = __popc(peers & ((1u << lane) - 1u));
             const uint32_t occ = valid ? mc[sl] + below : 0;
             __syncwarp();
@@ -1489,7 +1485,7 @@ static int jb_pairing(const dw_join_side_t *a, const dw_join_side_t *b, const Jo
     cudaMemsetAsync(o.cursor, 0, 4 * PAIR_MAXB, s);
     cudaMemsetAsync(o.bonly_bits, 0, 4 * L.nw, s);
     const int spb = 1 << q.shift;
-    const size_t smem_b = 4 * ((size_t)(2 * JB_WARPS + 3) * spb + PAIR_MAXB);
+    const size_t smem_b = 4 * ((size_t)(JB_WARPS + 3) * spb + PAIR_MAXB);
     cudaFuncSetAttribute(jb_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
     jb_bucket_kernel<<<JB_NBB, JB_THREADS, smem_b, s>>>(q, o);
     count_launch();
