@@ -293,6 +293,11 @@ typedef struct {
     uint64_t *d_key_hi, *d_key_lo;   /* [P] ranking key */
     const int64_t *d_tie_rank;       /* implicit key_lo: A-op id ranks (NULL = index) */
     int64_t n_a;                     /* implicit key_lo: number of A-op findings */
+    /* the differential columns (north star (3)); each may be NULL */
+    double *d_delta_e;               /* [P] e_b - e_a (J) */
+    int64_t *d_delta_t;              /* [P] latency_b - latency_a (us) */
+    double *d_epw_ratio;             /* [P] (e_b / work_b) / (e_a / work_a), IEEE (x/0 = inf, 0/0 = NaN);
+                                        work = 1 per op without a work column */
 } dw_findings_t;
 
 /* detect_waste over CSR segment pairs (reference SubgraphPair lists).

@@ -97,7 +97,8 @@ class Findings(ctypes.Structure):
     _fields_ = [("d_energy_a", c_vp), ("d_energy_b", c_vp), ("d_ratio", c_vp),
                 ("d_latency_a", c_vp), ("d_latency_b", c_vp), ("d_verdict", c_vp),
                 ("d_side", c_vp), ("d_informational", c_vp), ("d_wasted", c_vp),
-                ("d_key_hi", c_vp), ("d_key_lo", c_vp), ("d_tie_rank", c_vp), ("n_a", c_i64)]
+                ("d_key_hi", c_vp), ("d_key_lo", c_vp), ("d_tie_rank", c_vp), ("n_a", c_i64),
+                ("d_delta_e", c_vp), ("d_delta_t", c_vp), ("d_epw_ratio", c_vp)]
 
 
 class JoinSide(ctypes.Structure):

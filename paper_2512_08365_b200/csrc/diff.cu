@@ -76,11 +76,17 @@ struct FindCols {
     int64_t *la, *lb;
     int8_t *verdict, *side, *info;
     uint64_t *khi, *klo;
+    double *de, *epwr;
+    int64_t *dt;
 };
 
+// epw_a / epw_b: joules per unit of work of each side (= joules without work)
 __device__ __forceinline__ void store_finding(const FindCols &o, int64_t f, double ea, double eb,
                                               int64_t la, int64_t lb, const Verdict &v,
-                                              int64_t tie) {
+                                              int64_t tie, double epw_a, double epw_b) {
+    if (o.de) o.de[f] = __dsub_rn(eb, ea);
+    if (o.dt) o.dt[f] = lb - la;
+    if (o.epwr) o.epwr[f] = __ddiv_rn(epw_b, epw_a);
     if (o.ea) o.ea[f] = ea;
     if (o.eb) o.eb[f] = eb;
     if (o.ratio) o.ratio[f] = v.ratio;
@@ -107,6 +113,9 @@ static FindCols cols_of(const dw_findings_t *f) {
     c.info = f->d_informational;
     c.khi = f->d_key_hi;
     c.klo = f->d_key_lo;
+    c.de = f->d_delta_e;
+    c.dt = f->d_delta_t;
+    c.epwr = f->d_epw_ratio;
     return c;
 }
 
@@ -141,7 +150,7 @@ __global__ void detect_pairs_kernel(int64_t P, const int64_t *off_a, const int32
     const int64_t lb = b1 > b0 ? emax - smin : 0;
     const double e_a = su_a.result(), e_b = su_b.result();
     const Verdict v = judge(e_a, e_b, la, lb, out_diff ? out_diff[p] : 0.0, threshold);
-    store_finding(o, p, e_a, e_b, la, lb, v, tie ? tie[p] : 0);
+    store_finding(o, p, e_a, e_b, la, lb, v, tie ? tie[p] : 0, e_a, e_b);
 }
 
 // ------------------------------------------------------------------ K6 rank
@@ -591,9 +600,11 @@ __global__ void __launch_bounds__(WF_THREADS) join_window_findings_kernel(
             const int64_t i = i0 + q;
             match_a[i] = j[u];
             const Verdict v = judge(ea[u], eb[u], la[u], lb[u], 0.0, threshold);
-            store_finding(o, i, ea[u], eb[u], la[u], lb[u], v, tie[u]);
-            if (epw_a) epw_a[i] = div_or_same(ea[u], A.work, i);
-            if (epw_b) epw_b[i] = j[u] >= 0 ? div_or_same(eb[u], B.work, j[u]) : 0.0;
+            const double pa = div_or_same(ea[u], A.work, i);
+            const double pb = j[u] >= 0 ? div_or_same(eb[u], B.work, j[u]) : 0.0;
+            store_finding(o, i, ea[u], eb[u], la[u], lb[u], v, tie[u], pa, pb);
+            if (epw_a) epw_a[i] = pa;
+            if (epw_b) epw_b[i] = pb;
             cnt += j[u] >= 0;
         }
     }
@@ -612,9 +623,10 @@ __global__ void join_findings_b_kernel(int64_t na, int64_t n_bonly, const int32_
     const double eb = B.joules[j];
     const int64_t lb = B.end[j] - B.start[j];
     const Verdict v = judge(0.0, eb, 0, lb, 0.0, threshold);
-    store_finding(o, f, 0.0, eb, 0, lb, v, -1);  // nodes_a == () sorts first
+    const double pb = div_or_same(eb, B.work, j);
+    store_finding(o, f, 0.0, eb, 0, lb, v, -1, 0.0, pb);  // nodes_a == () sorts first
     if (epw_a) epw_a[f] = 0.0;
-    if (epw_b) epw_b[f] = div_or_same(eb, B.work, j);
+    if (epw_b) epw_b[f] = pb;
 }
 
 // ---------------------------------------------------- K5' bucketed join (no sort)

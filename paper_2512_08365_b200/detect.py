@@ -78,9 +78,12 @@ class FindingColumns:
     selects which optional columns are written (the ranking keys always are)."""
 
     ALL = ("energy_a", "energy_b", "ratio", "wasted", "latency_a", "latency_b", "verdict", "side",
-           "informational")
+           "informational", "delta_e", "delta_t", "epw_ratio")
     LEAN = ("ratio", "wasted", "verdict", "side", "informational")
     KEYS = ("key_hi",)  # the ranking key only: every other column is derived for the top-k rows
+    # the differential output of the north star (3): energy and time deltas and the
+    # energy-per-useful-work ratio per pair, plus the ranking key (32 B per finding)
+    DELTAS = ("delta_e", "delta_t", "epw_ratio")
 
     def __init__(self, P: int, dev, full: bool = True, columns=None, key_lo: bool = True,
                  tie_rank=None, n_a: int = 0):
@@ -88,7 +91,8 @@ class FindingColumns:
         self.tie_rank, self.n_a = tie_rank, n_a
         types = {"energy_a": torch.float64, "energy_b": torch.float64, "ratio": torch.float64,
                  "wasted": torch.float64, "latency_a": torch.int64, "latency_b": torch.int64,
-                 "verdict": torch.int8, "side": torch.int8, "informational": torch.int8}
+                 "verdict": torch.int8, "side": torch.int8, "informational": torch.int8,
+                 "delta_e": torch.float64, "delta_t": torch.int64, "epw_ratio": torch.float64}
         self.P = P
         self.key_hi = torch.empty(P, dtype=torch.int64, device=dev)
         self.key_lo = torch.empty(P, dtype=torch.int64, device=dev) if key_lo else None
@@ -100,11 +104,11 @@ class FindingColumns:
         return _native.Findings(p(self.energy_a), p(self.energy_b), p(self.ratio),
                                 p(self.latency_a), p(self.latency_b), p(self.verdict),
                                 p(self.side), p(self.informational), p(self.wasted),
-                                p(self.key_hi), p(self.key_lo), p(self.tie_rank), int(self.n_a))
+                                p(self.key_hi), p(self.key_lo), p(self.tie_rank), int(self.n_a),
+                                p(self.delta_e), p(self.delta_t), p(self.epw_ratio))
 
     def host(self, idx=None) -> dict:
-        names = ("energy_a", "energy_b", "ratio", "wasted", "latency_a", "latency_b", "verdict",
-                 "side", "informational")
+        names = self.ALL
         out = {}
         for n in names:
             t = getattr(self, n)

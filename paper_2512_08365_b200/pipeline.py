@@ -46,10 +46,12 @@ def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAUL
     pieces (energy.build_ledger) -- the exact fixed-point sum, the scale
     path's definition; "reference" for the reference's sequential order.
 
-    ``lean`` (default): the join writes only each finding's ranking key (the
-    top-k rows' ratio / verdict / side / informational / wasted are derived
-    on the host, equal to the device's); ``lean=False`` keeps every finding
-    column on the device (``Analysis.join.columns``) plus energy-per-work.
+    ``lean`` (default): the join writes each finding's differential columns
+    -- energy delta, time delta, energy-per-useful-work ratio (north star
+    (3)) -- and its ranking key (the top-k rows' ratio / verdict / side /
+    informational / wasted are derived on the host, equal to the device's);
+    ``lean=False`` keeps every finding column on the device
+    (``Analysis.join.columns``) plus per-side energy-per-work.
 
     (Running the join's pairing on a second stream beside the ledgers, with
     the tile kernel capped to fewer SMs via dw_set_attribute_sms, was measured
@@ -79,7 +81,7 @@ def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAUL
         prep = join_prepare(ca, cb)
     lb = build_ledger(cb, method=method, summation=summation)
     jd = join_diff(ca, cb, la, lb, threshold, k, full_columns=not lean, epw=not lean, prep=prep,
-                   columns=FindingColumns.KEYS if lean else None)
+                   columns=FindingColumns.DELTAS if lean else None)
     top = jd.top_findings(ca, cb)
     ineff = max(la.total_joules, lb.total_joules)
     pct = jd.wasted_joules / ineff if ineff > 0 else 0.0

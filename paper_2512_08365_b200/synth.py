@@ -13,7 +13,8 @@ signature drawn from a 64-name Zipf vocabulary x 16 shape buckets x 2 dtypes x
 watts, m ~ U(0.02, 0.5)  (misconfiguration-like), (ii) 0.1% extra operators
 inserted (redundant) and (iii) 0.1% operators renamed (api-misuse).  The power
 column is the step ground truth read every ``span/S`` us (delay 0), so S is
-exact.  Everything is a pure function of (config, seed).
+exact; C4 / C5 jitter each read by up to a quarter period (an irregular,
+host-polled meter: 7-bit timestamp deltas instead of a 1-bit regular clock).  Everything is a pure function of (config, seed).
 """
 
 from __future__ import annotations
@@ -41,13 +42,14 @@ class SynthConfig:
     watt_frac: float = 0.01       # fraction of signatures with inflated watts on B
     insert_frac: float = 0.001
     rename_frac: float = 0.001
+    jitter: float = 0.0           # sample-clock jitter, fraction of the period (NVML-like irregular reads)
 
 
 CONFIGS = {
     "C2": SynthConfig("C2", 1_000_000, 0, seed=2, kmax=3, kdur=(5, 500), gap=20),
     "C3": SynthConfig("C3", 10_000_000, 0, seed=3, kmax=3, kdur=(5, 2000), gap=20, streams=4),
-    "C4": SynthConfig("C4", 100_000_000, 1_000_000_000, seed=4, kmax=2, kdur=(20, 3000), gap=200),
-    "C5": SynthConfig("C5", 6_250_000, 62_500_000, seed=5000, kmax=2, kdur=(20, 3000), gap=200),
+    "C4": SynthConfig("C4", 100_000_000, 1_000_000_000, seed=4, kmax=2, kdur=(20, 3000), gap=200, jitter=0.25),
+    "C5": SynthConfig("C5", 6_250_000, 62_500_000, seed=5000, kmax=2, kdur=(20, 3000), gap=200, jitter=0.25),
 }
 
 
@@ -145,14 +147,24 @@ def round9(w: torch.Tensor) -> torch.Tensor:
     return torch.where(pos, torch.div(m, pw), w)
 
 
-def _power(op_end_max: int, t0: int, n_samples: int, k_start, k_end, kw, dev):
+def _power(op_end_max: int, t0: int, n_samples: int, k_start, k_end, kw, dev, jitter: float = 0.0,
+           seed: int = 0):
     span = max(op_end_max - t0, 1)
     if n_samples <= 0:
         n_samples = max(2, span // 100)  # 10 kHz
     # samples at t0 + floor(i * span / (S-1)): the last one lands on the trace
-    # end, so a sampled (trapezoid) view covers every interval
+    # end, so a sampled (trapezoid) view covers every interval.  With jitter J
+    # each interior read moves by up to +-J periods (J < 1/2 keeps the clock
+    # strictly increasing): a power meter polled by a host thread.
     period = span / (n_samples - 1)
-    ts = t0 + torch.floor(torch.arange(n_samples, device=dev, dtype=torch.float64) * period).to(torch.int64)
+    x = torch.arange(n_samples, device=dev, dtype=torch.float64)
+    if jitter > 0:
+        assert jitter < 0.5
+        gj = torch.Generator(device=dev)
+        gj.manual_seed(seed)
+        x += (2.0 * torch.rand(n_samples, device=dev, dtype=torch.float64, generator=gj) - 1.0) * jitter
+    ts = t0 + torch.floor(x * period).to(torch.int64)
+    ts[0] = t0
     ts[-1] = t0 + span
     if period < 1:
         raise ValueError("more samples than microseconds in the span")
@@ -213,7 +225,8 @@ def _b_side(a: _Ops, cfg: SynthConfig, g: torch.Generator, dev) -> _Ops:
 def _columns(ops: _Ops, cfg: SynthConfig, t0: int, n_samples: int, dev, prefix: str) -> TraceColumns:
     op_start, op_end, k_start, k_end, kop = _layout(ops, t0, dev)
     end = int(op_end[-1].item())
-    ts, watts = _power(end, t0, n_samples, k_start, k_end, ops.kw, dev)
+    ts, watts = _power(end, t0, n_samples, k_start, k_end, ops.kw, dev, cfg.jitter,
+                       cfg.seed * 2 + (prefix == "b"))
     n = op_start.numel()
     return TraceColumns(ts=ts, watts=watts, trace_end=max(end, int(ts[-1].item())),
                         op_start=op_start, op_end=op_end, k_start=k_start, k_end=k_end,

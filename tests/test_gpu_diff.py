@@ -171,3 +171,43 @@ def test_keys_only_join_gives_the_same_top_findings(theta):
     assert keys.columns.ratio is None and keys.columns.verdict is None
     assert (keys.P, keys.n_waste, keys.wasted_joules) == (full.P, full.n_waste, full.wasted_joules)
     assert keys.top_findings(ca, cb) == full.top_findings(ca, cb)
+
+
+@pytest.mark.parametrize("with_work", [False, True])
+def test_join_differential_columns(with_work):
+    """North star (3): per finding the energy delta e_b - e_a, the time delta
+    lat_b - lat_a and the energy-per-useful-work ratio (e_b / work_b) /
+    (e_a / work_a) (IEEE: a B-only finding has e_a = 0 -> inf).  Bit-exact
+    against numpy over the oracle's pairing; the lean columns analyze() writes
+    (FindingColumns.DELTAS) equal the full set's."""
+    from paper_2512_08365_b200.detect import FindingColumns
+    ca, cb = synth.make_pair(synth.scaled(synth.CONFIGS["C2"], 60_000))
+    la, lb = build_ledger(ca), build_ledger(cb)
+    ja, jb = la.per_operator.array(), lb.per_operator.array()
+    rng = np.random.default_rng(7)
+    wa = rng.uniform(0.5, 4.0, size=ca.n_ops) if with_work else None
+    wb = rng.uniform(0.5, 4.0, size=cb.n_ops) if with_work else None
+    full = join_diff(ca, cb, la, lb, 0.10, k=50, work_a=wa, work_b=wb)
+    lean = join_diff(ca, cb, la, lb, 0.10, k=50, work_a=wa, work_b=wb, full_columns=False, epw=False,
+                     columns=FindingColumns.DELTAS)
+    ma, mb, b_only, d, _ = _join_oracle(ca, cb, ja, jb, 0.10)
+    na = len(ma)
+    ib = np.concatenate([ma, b_only])
+    ia = np.concatenate([np.arange(na), np.full(len(b_only), -1)])
+    ea = np.where(ia >= 0, ja[np.maximum(ia, 0)], 0.0)
+    eb = np.where(ib >= 0, jb[np.maximum(ib, 0)], 0.0)
+    lat = lambda c, k: np.where(k >= 0, (c.host("op_end") - c.host("op_start"))[np.maximum(k, 0)], 0)
+    work_a = wa if with_work else np.ones(ca.n_ops)
+    work_b = wb if with_work else np.ones(cb.n_ops)
+    pa = np.where(ia >= 0, ea / work_a[np.maximum(ia, 0)] if with_work else ea, 0.0)
+    pb = np.where(ib >= 0, eb / work_b[np.maximum(ib, 0)] if with_work else eb, 0.0)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ratio = pb / pa
+    for jd in (full, lean):
+        h = jd.columns.host()
+        P = jd.P
+        np.testing.assert_array_equal(h["delta_e"][:P], eb - ea)
+        np.testing.assert_array_equal(h["delta_t"][:P], lat(cb, ib) - lat(ca, ia))
+        np.testing.assert_array_equal(h["epw_ratio"][:P], ratio)
+        np.testing.assert_array_equal(jd.order.cpu().numpy(), full.order.cpu().numpy())
+    assert np.isinf(full.columns.host()["epw_ratio"][na:full.P]).all()  # B-only: nothing on A

@@ -18,7 +18,10 @@ def test_decode_exact_and_ledger_identical(tmp_path):
     a, b = synth.make_pair(cfg)
     p = pack(a)
     assert p.watts_p0 is not None  # synthetic watts are at the format's 9-digit precision
-    assert p.ts_bits == 1  # regular clock: 1-bit ts deltas
+    assert p.ts_bits is not None and 6 <= p.ts_bits <= 8  # C4's jittered clock: 7-bit ts deltas
+    from dataclasses import replace
+    regular = pack(synth.make_pair(replace(cfg, jitter=0.0))[0])
+    assert regular.ts_bits == 1  # a regular clock packs to 1-bit deltas
     assert set(p.iv_bits) == {"op_start", "op_end", "k_start", "k_end"}  # bit-packed intervals
     assert p.op_sig_dict is not None and p.sig_bits is not None
     for n in ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "op_sig"):
