@@ -2,10 +2,13 @@
 """Benchmark of the Magneton/diffwatt hot path on B200 (one JSON line).
 
 A step = attribution of both traces of a pair (per-operator and per-kernel
-joules, trapezoid over the trace's 10 kHz power samples) + the signature-join
-differential diff + the top-k ranked report on the host: the BASELINE config 4
-workload (100M operators / 1e9 power samples per trace) on
-one B200, generated in HBM from a fixed seed.
+joules, trapezoid over the trace's power samples) + the signature-join
+differential diff (per finding: energy delta, time delta, energy-per-work
+ratio and ranking key) + the top-k ranked report on the host: the BASELINE
+config 4 workload (100M operators / 1e9 power samples per trace, SURVEY.md
+8(d) C4) on one B200, generated in HBM from a fixed seed.  After the timed
+runs the same path runs on the CPU baseline's sample and is compared with the
+oracle ("parity").
 
   value  operator intervals (ops + kernels, both traces) attributed per second,
          inputs resident in HBM (inputs >> 126 MB L2, so no flush is needed)
@@ -159,18 +162,22 @@ def cpu_sample(cfg_name: str, n_ops: int, seed_shift: int = 0):
     return ca, cb
 
 
-def cpu_step(ca, cb, method: str, k: int):
+def cpu_step(ca, cb, method: str, k: int, mode=None):
     """The reference hot path restated in C (oracle/, pthreads over all host
-    cores): ledger of both traces, signature join, detect rule, report order."""
+    cores): ledger of both traces, signature join, detect rule, report order.
+    ``mode``: the oracle's summation (default the reference's sequential
+    sums; oracle.MODE_EXACT restates summation="exact")."""
     import numpy as np
     import oracle
+    if mode is None:
+        mode = oracle.MODE_REFERENCE
     kind = "linear" if method == "samples" else "step"
     out = []
     for c in (ca, cb):
         ts, w = c.host("ts"), c.host("watts")
         span_hi = None if kind == "linear" else c.signal_span()[1]
         out.append(oracle.ledger(kind, ts, w, span_hi, c.host("op_start"), c.host("op_end"),
-                                 c.host("k_start"), c.host("k_end")))
+                                 c.host("k_start"), c.host("k_end"), mode))
     ja, jb = out[0][0], out[1][0]
     sig_a = c_sig(ca)
     sig_b = c_sig(cb)
@@ -186,7 +193,52 @@ def cpu_step(ca, cb, method: str, k: int):
                       cb.host("op_start"), cb.host("op_end"), None, 0.10)
     tie = np.concatenate([np.arange(na) + 1, np.zeros(len(b_only), dtype=np.int64)])
     order = oracle.rank(d["verdict"], d["wasted"], tie)
-    return order[:k]
+    waste = d["verdict"] == 2
+    return {"ledgers": out, "match_a": ma, "b_only": b_only, "order": order[:k],
+            "n_waste": int(waste.sum()), "wasted": oracle.fx_sum(d["wasted"][waste])}
+
+
+def parity_record(args, dev) -> dict:
+    """The GPU path (pipeline.analyze, this run's summation) against the CPU
+    oracle on the exact sample cpu_baseline times: ledgers, pairing, top-k
+    order, waste count and wasted joules bit for bit under the same summation
+    definition, and the per-operator joules against the reference's own
+    sequential sums within the north star's 1e-6 relative."""
+    import numpy as np
+    import oracle
+    from paper_2512_08365_b200.pipeline import analyze
+    ca, cb = cpu_sample(args.config, args.cpu_sample_ops)
+    mode = oracle.MODE_EXACT if args.summation == "exact" else oracle.MODE_DEVICE
+    ref = cpu_step(ca, cb, args.method, args.k, mode)
+    res = analyze(ca, cb, args.method, 0.10, args.k, summation=args.summation)
+    led_eq = True
+    for led, (po, pk, total, idle) in zip((res.ledger_a, res.ledger_b), ref["ledgers"]):
+        led_eq &= bool(np.array_equal(led.per_operator.array(), po) and np.array_equal(led.per_kernel.array(), pk)
+                       and led.total_joules == total and led.idle_joules == idle)
+    jd = res.join
+    join_eq = bool(np.array_equal(jd.match_a.cpu().numpy(), ref["match_a"]) and
+                   np.array_equal(jd.b_only.cpu().numpy(), ref["b_only"]))
+    topk_eq = bool(np.array_equal(jd.order.cpu().numpy(), ref["order"]))
+    # the reference's sequential sums (MODE_REFERENCE) per operator
+    kind = "linear" if args.method == "samples" else "step"
+    rel = 0.0
+    for c, led in ((ca, res.ledger_a), (cb, res.ledger_b)):
+        f = oracle.integrate_linear if kind == "linear" else None
+        lo, hi = c.host("op_start"), c.host("op_end")
+        want = (f(c.host("ts"), c.host("watts"), lo, hi, oracle.MODE_REFERENCE) if f else
+                oracle.integrate_step(c.host("ts"), c.host("watts"), c.signal_span()[1], lo, hi,
+                                      oracle.MODE_REFERENCE))
+        got = led.per_operator.array()
+        nz = want != 0
+        rel = max(rel, float(np.max(np.abs(got[nz] - want[nz]) / np.abs(want[nz]))) if nz.any() else 0.0)
+    out = {"sample": f"{args.config} distribution, {ca.n_ops}+{cb.n_ops} ops, {ca.n_power}+{cb.n_power} samples",
+           "oracle_mode": {oracle.MODE_EXACT: "MODE_EXACT", oracle.MODE_DEVICE: "MODE_DEVICE"}[mode],
+           "ledgers_bit_exact": led_eq, "pairing_bit_exact": join_eq, "topk_order_equal": topk_eq,
+           "n_waste_equal": jd.n_waste == ref["n_waste"], "wasted_joules_equal": jd.wasted_joules == ref["wasted"],
+           "max_rel_err_vs_reference_sums": rel, "tolerance": 1e-6}
+    out["pass"] = bool(led_eq and join_eq and topk_eq and out["n_waste_equal"] and out["wasted_joules_equal"]
+                       and rel <= 1e-6)
+    return out
 
 
 def c_sig(c):
@@ -325,7 +377,8 @@ def run_ours(args, rank: int, world: int, local: int):
     lb = build_ledger(cb, method=args.method, summation=args.summation)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
-    jd = join_diff(ca, cb, la, lb, 0.10, args.k, full_columns=False, epw=False)
+    from paper_2512_08365_b200.detect import FindingColumns
+    jd = join_diff(ca, cb, la, lb, 0.10, args.k, full_columns=False, epw=False, columns=FindingColumns.DELTAS)
     jd.top_findings(ca, cb)
     t2 = time.perf_counter()
     P = res.join.P
@@ -460,6 +513,10 @@ def run_ours(args, rank: int, world: int, local: int):
             line["cpu_baseline"] = cpu_baseline(args)
         except Exception as exc:  # noqa: BLE001 - the baseline must not hide the GPU line
             line["cpu_baseline"] = {"error": repr(exc)}
+        try:
+            line["parity"] = parity_record(args, dev)
+        except Exception as exc:  # noqa: BLE001
+            line["parity"] = {"error": repr(exc), "pass": False}
     print(json.dumps(line), flush=True)
 
 
