@@ -137,7 +137,10 @@ __global__ void status_init_kernel(DevStatus *st) {
         st->order_index = (unsigned long long)NONE;
         st->long_count = 0;
     }
-    if (t < 4) st->totals[t] = 0.0;
+    if (t < 4) {
+        st->totals[t] = 0.0;
+        st->pad[t] = 0;  // every byte of the block defined (dw_status copies all of it)
+    }
 }
 
 // ------------------------------------------------------------ K1 partition

@@ -233,6 +233,13 @@ def detect_waste(pairs: Sequence, ledger_a: EnergyLedger, ledger_b: EnergyLedger
     return findings
 
 
+def classify(finding: WasteFinding, trace_a, trace_b) -> str:
+    """Category of one waste finding (detect.py:137-172); the batched rule is
+    `diagnose.classify_findings`."""
+    from .diagnose import classify as _classify
+    return _classify(finding, trace_a, trace_b)
+
+
 # ----------------------------------------------------------------- report
 
 
