@@ -582,6 +582,21 @@ __device__ __forceinline__ int find_le(const uint32_t *ts, int r0, int r1, uint3
     return lo;
 }
 
+// find_le with a wider first probe: the four timestamps around the
+// interpolated guess (independent loads), which settle a guess off by one
+// either way -- a jittered clock's usual miss -- without the gallop.
+__device__ __forceinline__ int find_le4(const uint32_t *ts, int r0, int r1, uint32_t key, uint32_t kref,
+                                        int gref, float scale) {
+    if (r1 - r0 >= 4) {
+        const float off = (float)(key - kref) * scale;
+        int g = off >= (float)(r1 - 2 - gref) ? r1 - 2 : gref + (int)off;
+        g = g < r0 + 1 ? r0 + 1 : g;  // g - 1 >= r0, g + 1 <= r1 - 1
+        const uint32_t tm = ts[g - 1], t0 = ts[g], t1 = ts[g + 1], t2 = ts[g + 2 < r1 ? g + 2 : g + 1];
+        if (tm <= key && (g + 2 >= r1 || t2 > key)) return g - 1 + (t0 <= key) + (t1 <= key);
+    }
+    return find_le(ts, r0, r1, key, kref, gref, scale);
+}
+
 // Phase 1 for one interval (window-relative lo <= hi, lo in the tile): edge
 // pieces and interior count.  Returns false when it spans more than DIRECT
 // pieces (the fixed-point path takes it).  Branch-free apart from the
@@ -1070,7 +1085,8 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_tiles_kernel(AttrParams
 constexpr int XHALO = DW_XHALO;                          // window halo = piece cap of the exact kernel
 constexpr int XSTAGES = DW_XSTAGES;
 constexpr int WINX = TILE + XHALO + 6;
-constexpr int XPER = (WINX + ATTR_THREADS - 1) / ATTR_THREADS;  // pieces per thread in pass B
+constexpr int XPER = (((WINX + ATTR_THREADS - 1) / ATTR_THREADS) + 1) & ~1;  // pieces per thread in pass B (even)
+static_assert(XPER % 2 == 0 && TILE % 2 == 0, "pass B's 16-byte shared-memory accesses need even XPER");
 constexpr double X_BOUND = 8.0e6;  // W*us: |sum of an interval's q| < 2^63 below it
 using TileSmemX = TileSmemT<XSTAGES, WINX>;
 static_assert(GROUPS < XSTAGES, "claims in flight must span fewer positions than the ring");
@@ -1226,19 +1242,42 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
         const bool fastb = !wide && rb + XPER <= last && rb + XPER < cnt && !(rzS > rb && rzS <= rb + XPER) &&
                            (rb + XPER <= e1 || rb >= e1);
         if (fastb) {
+            // the thread's XPER + 1 timestamps and watts (and w[rb - 1] for
+            // v(rb)) as 16-byte loads: rb is even, so every pair is aligned,
+            // and lanes XPER * 8 bytes apart hit distinct banks per quarter warp
             const uint32_t b32 = (uint32_t)base;
-            int64_t t0 = s_ts[rb];
-            double wcur = s_w[rb];
-            double vcur = KIND == DW_SIGNAL_LINEAR ? lin_v(s_w, rb, rz0, rzS, cx.w0, cx.wl) : 0.0;
+            int64_t tv[XPER + 2];
+            double wv[XPER + 4];  // wv[i] = w[rb - 2 + i]
+#pragma unroll
+            for (int i = 0; i < XPER; i += 2) {
+                const longlong2 t2v = *reinterpret_cast<const longlong2 *>(s_ts + rb + i);
+                tv[i] = t2v.x;
+                tv[i + 1] = t2v.y;
+            }
+            tv[XPER] = s_ts[rb + XPER];
+#pragma unroll
+            for (int i = (KIND == DW_SIGNAL_LINEAR ? 0 : 2); i < XPER + 2; i += 2) {
+                const double2 w2v = *reinterpret_cast<const double2 *>(s_w + rb - 2 + i);
+                wv[i] = w2v.x;
+                wv[i + 1] = w2v.y;
+            }
+            wv[XPER + 2] = s_w[rb + XPER];
+            int64_t t0 = tv[0];
+            double wcur = wv[2];
+            double vcur = 0.0;
+            if (KIND == DW_SIGNAL_LINEAR)
+                vcur = rb == rz0 ? cx.w0 : (rb == rzS ? cx.wl : __dadd_rn(wv[1], __dsub_rn(wcur, wv[1])));
             hmax = abs_hi(wcur);
 #pragma unroll
+            for (int i = 0; i < XPER; i += 2)  // 32-bit window timestamps, two per store
+                *reinterpret_cast<uint2 *>(ts32 + rb + i) =
+                    make_uint2((uint32_t)tv[i] - b32, (uint32_t)tv[i + 1] - b32);
+#pragma unroll
             for (int i = 0; i < XPER; ++i) {
-                const int r = rb + i;
-                ts32[r] = (uint32_t)t0 - b32;
-                const int64_t t1 = s_ts[r + 1];
+                const int64_t t1 = tv[i + 1];
                 bad |= t1 <= t0;
                 const double wd = (double)((uint32_t)t1 - (uint32_t)t0);
-                const double wnext = s_w[r + 1];
+                const double wnext = wv[i + 3];
                 double t2;
                 if (KIND == DW_SIGNAL_STEP) {
                     t2 = __dmul_rn(__dadd_rn(wcur, wcur), wd);
@@ -1340,9 +1379,10 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
             unsigned long long *P = reinterpret_cast<unsigned long long *>(s_ts);
             if (fastb) {
 #pragma unroll
-                for (int i = 0; i < XPER; ++i) {
-                    P[rb + i] = pre;
-                    pre += (unsigned long long)q[i];
+                for (int i = 0; i < XPER; i += 2) {  // 16-byte stores (rb even)
+                    const unsigned long long p1 = pre + (unsigned long long)q[i];
+                    *reinterpret_cast<ulonglong2 *>(P + rb + i) = make_ulonglong2(pre, p1);
+                    pre = p1 + (unsigned long long)q[i + 1];
                 }
             } else {
 #pragma unroll
@@ -1404,7 +1444,7 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
             if (ok) {
                 const uint32_t lo = (uint32_t)glo - (uint32_t)base;
                 const uint32_t hi = (uint32_t)dh;
-                const int a = find_le(ts32, r0, r1, lo, tr0, r0, cx.scale);
+                const int a = find_le4(ts32, r0, r1, lo, tr0, r0, cx.scale);
                 const uint32_t ta = ts32[a], ta1 = ts32[a + 1];
                 const int lim = min(a + XHALO + 1, cnt);
                 double F2, L2;
@@ -1413,7 +1453,7 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
                 if (KIND == DW_SIGNAL_STEP) {
                     // pieces: none (hi == lo); w[a]*(hi-lo) inside one segment;
                     // else first partial + whole interior + last partial segment
-                    b = hi > lo ? find_le(ts32, a, lim, hi - 1, ta, a, cx.scale) : a;
+                    b = hi > lo ? find_le4(ts32, a, lim, hi - 1, ta, a, cx.scale) : a;
                     ok = b - a < XHALO;  // segments b - a + 1 <= XHALO
                     const double wa = s_w[a];
                     one = b == a;
@@ -1422,7 +1462,7 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
                     L2 = __dmul_rn(__dadd_rn(wbv, wbv), (double)(hi - ts32[b]));
                 } else {
                     // pieces [lo, ts] .. [ts, hi] (energy.py:108-130); b = last sample < hi
-                    b = ta < hi ? find_le(ts32, a, lim, hi - 1, ta, a, cx.scale) : a - 1;
+                    b = ta < hi ? find_le4(ts32, a, lim, hi - 1, ta, a, cx.scale) : a - 1;
                     const int m = b - a;  // -1 only when hi == lo == ts[a]
                     ok = m < XHALO;       // pieces m + 1 <= XHALO
                     const int il = ta == lo && a > 0 ? a - 1 : a;  // first bracketing pair (energy.py:115-124)
