@@ -208,7 +208,7 @@ constexpr int NCW = ATTR_WARPS;              // warps per consumer group
 constexpr int NPROD = 1;                     // producer warps
 constexpr int KTHREADS = GROUPS * ATTR_THREADS + 32 * NPROD;
 #ifndef DW_IV_POOL
-#define DW_IV_POOL 512
+#define DW_IV_POOL 384
 #endif
 constexpr int IV_POOL = DW_IV_POOL;          // staged intervals per stage (all sets)
 
@@ -1080,7 +1080,7 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_tiles_kernel(AttrParams
 #define DW_XHALO 64
 #endif
 #ifndef DW_XSTAGES
-#define DW_XSTAGES 7
+#define DW_XSTAGES 8
 #endif
 constexpr int XHALO = DW_XHALO;                          // window halo = piece cap of the exact kernel
 constexpr int XSTAGES = DW_XSTAGES;
