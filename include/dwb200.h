@@ -14,6 +14,7 @@
  *   dw_step_value_at    PowerSignal.value_at (the sampler's read) energy.py:57-66
  *   dw_detect_pairs     detect.detect_waste per-pair rule         detect.py:72-130
  *   dw_rank             detect.report ordering                    detect.py:256-278
+ *   dw_rank_segmented   report ordering of every pair of a corpus    detect.py:256-278
  *   dw_join_diff        signature hash-join + deltas + verdicts   (new)
  *
  * Conventions
@@ -320,6 +321,23 @@ int dw_detect_pairs(int64_t P, const int64_t *d_off_a, const int32_t *d_mem_a,
 size_t dw_rank_workspace_size(int64_t P, int64_t k);
 int dw_rank(int64_t P, const dw_findings_t *f, int64_t k, int64_t *d_order, double *d_summary,
             void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
+
+/* Segmented top-k: the report order of many finding sets in one
+ * call -- one segment per trace pair of a corpus (report() per pair,
+ * detect.py:256-278).  Segment i's keys are as in dw_findings_t (d_key_lo NULL:
+ * implied by the join numbering, d_tie_rank / n_a).  Writes, per segment, the
+ * min(k, P_i) best finding indices into d_order[i * k ...] (rest -1), and
+ * {n_waste, wasted_joules (exact), P_i, 0} into d_summary[4 * i ...] (may be
+ * NULL).  k <= 8192. */
+typedef struct {
+    const uint64_t *d_key_hi, *d_key_lo;
+    const int64_t *d_tie_rank;
+    int64_t n_a;
+    int64_t P;
+} dw_rank_segment_t;
+size_t dw_rank_segmented_workspace_size(int32_t nseg, int64_t k);
+int dw_rank_segmented(const dw_rank_segment_t *segs, int32_t nseg, int64_t k, int64_t *d_order,
+                      double *d_summary, void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
 
 /* Signature hash-join diff.  Operators of A and B
  * are keyed by (sig, occurrence in op order); equal keys pair up, unmatched

@@ -45,7 +45,8 @@ EXPORTED = (
     "dw_set_attribute_sms", "dw_ig_nl_count", "dw_ig_nl_write", "dw_ig_classify", "dw_ig_parse_power",
     "dw_ig_parse_op", "dw_ig_parse_kernel", "dw_ig_hash", "dw_ig_kernel_lists",
     "dw_fx_sum_workspace_size", "dw_fx_sum", "dw_step_value_at", "dw_detect_pairs",
-    "dw_rank_workspace_size", "dw_rank", "dw_join_workspace_size", "dw_join_diff",
+    "dw_rank_workspace_size", "dw_rank", "dw_rank_segmented_workspace_size", "dw_rank_segmented",
+    "dw_join_workspace_size", "dw_join_diff",
     "dw_exchange_count", "dw_exchange_scatter", "dw_ipc_handle", "dw_ipc_open", "dw_ipc_close",
     "dw_tensor_norms", "dw_tensor_prefilter", "dw_unfold_smem_doubles", "dw_unfold_spectra", "dw_spectra_embed",
     "dw_version", "dw_error_string", "dw_launch_count", "dw_kernel_timing", "dw_kernel_time_ms",
@@ -99,6 +100,10 @@ class Findings(ctypes.Structure):
                 ("d_side", c_vp), ("d_informational", c_vp), ("d_wasted", c_vp),
                 ("d_key_hi", c_vp), ("d_key_lo", c_vp), ("d_tie_rank", c_vp), ("n_a", c_i64),
                 ("d_delta_e", c_vp), ("d_delta_t", c_vp), ("d_epw_ratio", c_vp)]
+
+
+class RankSegment(ctypes.Structure):
+    _fields_ = [("d_key_hi", c_vp), ("d_key_lo", c_vp), ("d_tie_rank", c_vp), ("n_a", c_i64), ("P", c_i64)]
 
 
 class JoinSide(ctypes.Structure):
@@ -193,6 +198,10 @@ def lib():
             L.dw_rank_workspace_size.argtypes = [c_i64, c_i64]
             L.dw_rank.argtypes = [c_i64, ctypes.POINTER(Findings), c_i64, c_vp, c_vp, c_vp,
                                   ctypes.c_size_t, c_vp]
+            L.dw_rank_segmented_workspace_size.restype = ctypes.c_size_t
+            L.dw_rank_segmented_workspace_size.argtypes = [c_i32, c_i64]
+            L.dw_rank_segmented.argtypes = [ctypes.POINTER(RankSegment), c_i32, c_i64, c_vp, c_vp, c_vp,
+                                            ctypes.c_size_t, c_vp]
             L.dw_join_workspace_size.restype = ctypes.c_size_t
             L.dw_join_workspace_size.argtypes = [c_i64, c_i64, c_i64]
             L.dw_join_diff.argtypes = [ctypes.POINTER(JoinSide), ctypes.POINTER(JoinSide), c_i64,

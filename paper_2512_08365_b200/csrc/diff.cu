@@ -13,6 +13,7 @@
 //                     histogram, compaction of the candidates, CUB sort of the
 //                     (few) candidates.  Also the exact wasted-joules sum.
 #include <algorithm>
+#include <vector>
 
 #include <cub/cub.cuh>
 
@@ -1532,6 +1533,237 @@ static int bits_for(int64_t D) {
     return b;
 }
 
+
+// ------------------------------------------------ K6s segmented top-k
+// The report order of many finding sets at once (one segment per trace pair
+// of a corpus): every launch covers all segments (grid.y =
+// segment), each with its own radix-select state, so a corpus of S pairs takes
+// the same few launches as one pair.  Per segment: the exact waste sum, the
+// threshold digit by digit until the keys above it fit SEG_SORT_MAX, their
+// compaction, and a bitonic sort in shared memory (no library sort).
+constexpr int SEG_SORT_MAX = 8192;   // candidates per segment (24 B each in shared memory)
+constexpr int SEG_SORT_THREADS = 1024;
+constexpr int SEG_BLOCK = 512;
+
+struct SegDesc {
+    const uint64_t *khi, *klo;
+    const int64_t *tie_rank;
+    int64_t n_a, P, k;
+};
+
+struct SegState {
+    uint64_t phi, plo, mhi, mlo, thr_hi, thr_lo;
+    int64_t need;
+    int32_t pos, done;
+};
+
+__device__ __forceinline__ uint64_t seg_lo(const SegDesc &d, int64_t i) {
+    if (d.klo) return d.klo[i];
+    const int64_t tie = i < d.n_a ? (d.tie_rank ? d.tie_rank[i] : i) : -1;
+    return key_lo(tie, i);
+}
+
+__global__ void seg_init_kernel(const SegDesc *segs, int nseg, SegState *st, unsigned *hist, unsigned *cand_n,
+                                unsigned *pending) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s == 0) *pending = 0;
+    if (s >= nseg) return;
+    SegState z{};
+    z.need = segs[s].k;
+    z.pos = 128 - HIST_BITS;
+    z.done = segs[s].k == 0;  // nothing to rank
+    st[s] = z;
+    cand_n[s] = 0;
+    for (int b = 0; b < HIST_BINS; ++b) hist[s * HIST_BINS + b] = 0;
+}
+
+// exact n_waste and wasted sum per segment: block partials, then one block per segment
+__global__ void __launch_bounds__(256) seg_waste_kernel(const SegDesc *segs, unsigned long long *partials) {
+    const int s = blockIdx.y;
+    const SegDesc d = segs[s];
+    i128 acc = 0;
+    unsigned long long cnt = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.P; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = d.khi[i];
+        if (k >> 63) {
+            acc += fx_from_double(__longlong_as_double((long long)(k & 0x7FFFFFFFFFFFFFFFULL)), FX_JOULE_BITS);
+            ++cnt;
+        }
+    }
+    acc = warp_sum_i128(acc);
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    __shared__ unsigned long long red[8][3];
+    if ((threadIdx.x & 31) == 0) {
+        const I128Parts q = split(acc);
+        red[threadIdx.x >> 5][0] = q.lo;
+        red[threadIdx.x >> 5][1] = q.hi;
+        red[threadIdx.x >> 5][2] = cnt;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        i128 t = 0;
+        unsigned long long c = 0;
+        for (int w = 0; w < 8; ++w) {
+            t += join(red[w][0], red[w][1]);
+            c += red[w][2];
+        }
+        const I128Parts q = split(t);
+        unsigned long long *o = partials + 3 * ((int64_t)s * gridDim.x + blockIdx.x);
+        o[0] = q.lo;
+        o[1] = q.hi;
+        o[2] = c;
+    }
+}
+
+__global__ void seg_waste_final_kernel(const SegDesc *segs, const unsigned long long *partials, int nblk,
+                                       double *summary) {
+    const int s = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    i128 t = 0;
+    unsigned long long c = 0;
+    for (int b = 0; b < nblk; ++b) {
+        const unsigned long long *o = partials + 3 * ((int64_t)s * nblk + b);
+        t += join(o[0], o[1]);
+        c += o[2];
+    }
+    summary[4 * s + 0] = (double)c;
+    summary[4 * s + 1] = fx_to_double(t, FX_JOULE_BITS);
+    summary[4 * s + 2] = (double)segs[s].P;
+    summary[4 * s + 3] = 0.0;
+}
+
+__global__ void __launch_bounds__(SEG_BLOCK) seg_hist_kernel(const SegDesc *segs, const SegState *st,
+                                                              unsigned *hist) {
+    const int s = blockIdx.y;
+    const SegState g = st[s];
+    if (g.done) return;
+    const SegDesc d = segs[s];
+    __shared__ unsigned h[HIST_BINS];
+    for (int b = threadIdx.x; b < HIST_BINS; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    const bool need_lo = g.pos < 64 || g.mlo;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.P; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t hi = d.khi[i];
+        if ((hi & g.mhi) != g.phi) continue;
+        const uint64_t lo = need_lo ? seg_lo(d, i) : 0;
+        if ((lo & g.mlo) != g.plo) continue;
+        atomicAdd(&h[digit128(hi, lo, g.pos)], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < HIST_BINS; b += blockDim.x)
+        if (h[b]) atomicAdd(&hist[s * HIST_BINS + b], h[b]);
+}
+
+// one warp per segment: the bin holding the need-th largest key; either the
+// keys >= the threshold fit the candidate buffer (done) or the next digit
+__global__ void seg_select_kernel(const SegDesc *segs, SegState *st, unsigned *hist, int64_t cap,
+                                  unsigned *pending) {
+    const int s = blockIdx.x;
+    SegState g = st[s];
+    if (g.done) return;
+    unsigned *h = hist + s * HIST_BINS;
+    if (threadIdx.x == 0) {
+        int64_t above = 0;
+        int b = HIST_BINS - 1;
+        for (; b > 0; --b) {
+            if (above + (int64_t)h[b] >= g.need) break;
+            above += h[b];
+        }
+        const uint64_t dig = (uint64_t)b;
+        if (g.pos >= 64) {
+            g.thr_hi = g.phi | (dig << (g.pos - 64));
+            g.thr_lo = 0;
+        } else {
+            g.thr_hi = g.phi;
+            g.thr_lo = g.plo | (dig << g.pos);
+        }
+        // keys >= the threshold: those above the prefix (counted in earlier
+        // digits), the bins above b, and bin b
+        const int64_t cand = (segs[s].k - g.need) + above + (int64_t)h[b];
+        if (g.pos == 0 || cand <= cap) {
+            g.done = 1;
+        } else {
+            g.need -= above;
+            g.phi = g.thr_hi;
+            g.plo = g.thr_lo;
+            if (g.pos >= 64) g.mhi |= ((uint64_t)(HIST_BINS - 1)) << (g.pos - 64);
+            else g.mlo |= ((uint64_t)(HIST_BINS - 1)) << g.pos;
+            g.pos -= HIST_BITS;
+            atomicAdd(pending, 1u);
+        }
+        st[s] = g;
+    }
+    __syncwarp();
+    for (int b = threadIdx.x; b < HIST_BINS; b += 32) h[b] = 0;
+}
+
+__global__ void __launch_bounds__(256) seg_compact_kernel(const SegDesc *segs, const SegState *st, int64_t cap,
+                                                          uint64_t *chi, uint64_t *clo, int64_t *cidx,
+                                                          unsigned *cand_n) {
+    const int s = blockIdx.y;
+    const SegDesc d = segs[s];
+    if (d.k == 0) return;
+    const uint64_t th = st[s].thr_hi, tl = st[s].thr_lo;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.P; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t hi = d.khi[i];
+        if (hi < th) continue;
+        const uint64_t lo = seg_lo(d, i);
+        if (hi == th && lo < tl) continue;
+        const unsigned slot = atomicAdd(&cand_n[s], 1u);
+        if ((int64_t)slot < cap) {
+            const int64_t o = (int64_t)s * cap + slot;
+            chi[o] = hi;
+            clo[o] = lo;
+            cidx[o] = i;
+        }
+    }
+}
+
+// one CTA per segment: bitonic sort of the candidates, descending (hi, lo)
+// (keys are distinct: lo carries the finding index), best k indices out
+__global__ void __launch_bounds__(SEG_SORT_THREADS) seg_sort_kernel(const SegDesc *segs, int64_t cap,
+                                                                    const uint64_t *chi, const uint64_t *clo,
+                                                                    const int64_t *cidx, const unsigned *cand_n,
+                                                                    int64_t k, int64_t *order, int *overflow) {
+    extern __shared__ __align__(16) unsigned char seg_smem[];
+    const int s = blockIdx.x;
+    int n = (int)min((int64_t)cand_n[s], cap);
+    if ((int64_t)cand_n[s] > cap && threadIdx.x == 0) atomicOr(overflow, 1);
+    int m = 1;
+    while (m < n) m <<= 1;
+    uint64_t *sh = reinterpret_cast<uint64_t *>(seg_smem);
+    uint64_t *sl = sh + m;
+    int64_t *si = reinterpret_cast<int64_t *>(sl + m);
+    for (int x = threadIdx.x; x < m; x += blockDim.x) {
+        const bool in = x < n;
+        const int64_t o = (int64_t)s * cap + x;
+        sh[x] = in ? chi[o] : 0;
+        sl[x] = in ? clo[o] : 0;
+        si[x] = in ? cidx[o] : -1;
+    }
+    __syncthreads();
+    for (int size = 2; size <= m; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int x = threadIdx.x; x < m; x += blockDim.x) {
+                const int y = x ^ stride;
+                if (y > x) {
+                    const bool desc = (x & size) == 0;  // descending runs first: the whole array ends descending
+                    const bool less = sh[x] < sh[y] || (sh[x] == sh[y] && sl[x] < sl[y]);
+                    if (less == desc) {
+                        const uint64_t th = sh[x], tl = sl[x];
+                        const int64_t ti = si[x];
+                        sh[x] = sh[y]; sl[x] = sl[y]; si[x] = si[y];
+                        sh[y] = th; sl[y] = tl; si[y] = ti;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    const int64_t ks = segs[s].k;
+    for (int64_t x = threadIdx.x; x < k; x += blockDim.x) order[(int64_t)s * k + x] = x < ks && x < n ? si[x] : -1;
+}
+
 }  // namespace dw
 
 using namespace dw;
@@ -1742,6 +1974,94 @@ int dw_join_findings(const dw_join_side_t *a, const dw_join_side_t *b, int64_t m
                      dw_stream_t stream) {
     return join_impl(a, b, max_distinct, threshold, out, d_match_a, d_b_only, d_epw_a, d_epw_b, d_count, d_workspace,
                      workspace_bytes, stream, 2, &n_b_only);
+}
+
+
+size_t dw_rank_segmented_workspace_size(int32_t nseg, int64_t k) {
+    if (nseg < 0) return 0;
+    const int64_t cap = SEG_SORT_MAX;
+    (void)k;
+    size_t off = 0;
+    off += au(sizeof(SegDesc) * (size_t)std::max(nseg, 1));
+    off += au(sizeof(SegState) * (size_t)std::max(nseg, 1));
+    off += au(4 * (size_t)HIST_BINS * std::max(nseg, 1));
+    off += au(64);                                     // pending, overflow
+    off += au(4 * (size_t)std::max(nseg, 1));          // cand_n
+    off += au(24 * (size_t)cap * std::max(nseg, 1));   // candidates
+    off += au(24 * (size_t)1024 * std::max(nseg, 1));  // waste partials (<= 1024 blocks per segment)
+    return off;
+}
+
+int dw_rank_segmented(const dw_rank_segment_t *segs, int32_t nseg, int64_t k, int64_t *d_order,
+                      double *d_summary, void *d_workspace, size_t workspace_bytes, dw_stream_t stream) {
+    if (nseg < 0 || k < 0 || k > SEG_SORT_MAX || (nseg && !segs) || !d_workspace) return DW_E_ARG;
+    if (nseg == 0) return DW_OK;
+    if (workspace_bytes < dw_rank_segmented_workspace_size(nseg, k)) return DW_E_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t cap = SEG_SORT_MAX;
+    std::vector<SegDesc> h(nseg);
+    int64_t pmax = 0;
+    for (int i = 0; i < nseg; ++i) {
+        const dw_rank_segment_t &g = segs[i];
+        if (g.P < 0 || (g.P && !g.d_key_hi)) return DW_E_ARG;
+        h[i] = SegDesc{g.d_key_hi, g.d_key_lo, g.d_tie_rank, g.n_a, g.P, std::min(k, g.P)};
+        pmax = std::max(pmax, g.P);
+    }
+    if (k && !d_order) return DW_E_ARG;
+    char *base = (char *)d_workspace;
+    size_t off = 0;
+    SegDesc *d_segs = (SegDesc *)(base + off); off += au(sizeof(SegDesc) * nseg);
+    SegState *st = (SegState *)(base + off); off += au(sizeof(SegState) * nseg);
+    unsigned *hist = (unsigned *)(base + off); off += au(4 * (size_t)HIST_BINS * nseg);
+    unsigned *flags = (unsigned *)(base + off); off += au(64);
+    unsigned *cand_n = (unsigned *)(base + off); off += au(4 * (size_t)nseg);
+    uint64_t *chi = (uint64_t *)(base + off);
+    uint64_t *clo = chi + cap * nseg;
+    int64_t *cidx = (int64_t *)(clo + cap * nseg);
+    off += au(24 * (size_t)cap * nseg);
+    unsigned long long *partials = (unsigned long long *)(base + off);
+    cudaMemcpyAsync(d_segs, h.data(), sizeof(SegDesc) * nseg, cudaMemcpyHostToDevice, s);
+    // blocks per segment: about num_sms * 8 blocks in all, <= 1024 per segment
+    const int64_t want = std::max<int64_t>(1, (int64_t)num_sms() * 8 / nseg);
+    const unsigned bps = (unsigned)std::max<int64_t>(1, std::min<int64_t>({want, 1024, blocks_for(pmax, SEG_BLOCK)}));
+    seg_init_kernel<<<(nseg + 255) / 256, 256, 0, s>>>(d_segs, nseg, st, hist, cand_n, flags);
+    cudaMemsetAsync(flags, 0, 64, s);
+    count_launch();
+    if (d_summary) {
+        seg_waste_kernel<<<dim3(bps, nseg), 256, 0, s>>>(d_segs, partials);
+        seg_waste_final_kernel<<<nseg, 32, 0, s>>>(d_segs, partials, (int)bps, d_summary);
+        count_launch(2);
+    }
+    if (k == 0) {
+        DW_CHECK_LAUNCH();
+        return DW_OK;
+    }
+    for (int round = 0; round < 128 / HIST_BITS; ++round) {
+        seg_hist_kernel<<<dim3(bps, nseg), SEG_BLOCK, 0, s>>>(d_segs, st, hist);
+        seg_select_kernel<<<nseg, 32, 0, s>>>(d_segs, st, hist, cap, flags);
+        count_launch(2);
+        unsigned pending = 0;
+        cudaMemcpyAsync(&pending, flags, 4, cudaMemcpyDeviceToHost, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess) return DW_E_CUDA;
+        if (!pending) break;
+        cudaMemsetAsync(flags, 0, 4, s);
+    }
+    seg_compact_kernel<<<dim3(bps, nseg), 256, 0, s>>>(d_segs, st, cap, chi, clo, cidx, cand_n);
+    const size_t smem = 24 * (size_t)cap;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(seg_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    seg_sort_kernel<<<nseg, SEG_SORT_THREADS, smem, s>>>(d_segs, cap, chi, clo, cidx, cand_n, k, d_order,
+                                                          (int *)(flags + 1));
+    count_launch(2);
+    int overflow = 0;
+    cudaMemcpyAsync(&overflow, flags + 1, 4, cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return DW_E_CUDA;
+    if (overflow) return DW_E_WORKSPACE;  // massive ties at a threshold key (cannot happen: keys are distinct)
+    DW_CHECK_LAUNCH();
+    return DW_OK;
 }
 
 }  // extern "C"

@@ -348,6 +348,32 @@ def rank_order(key_hi: torch.Tensor, key_lo: Optional[torch.Tensor], k: int, tie
     return order[:k], summary
 
 
+def rank_order_segmented(segments: Sequence, k: int):
+    """Report order of many finding sets in one call (dw_rank_segmented, the
+    segmented top-k of a corpus: one segment per trace pair).  ``segments``:
+    (key_hi, key_lo or None, tie_rank or None, n_a) per segment, as
+    ``rank_order`` takes them.  Returns (order [S, k] int64 with -1 past a
+    segment's P, summary [S, 4] {n_waste, wasted_joules, P, 0}), both device
+    tensors; segment i equals ``rank_order`` of segment i alone."""
+    dev = _native.device()
+    segs = list(segments)
+    S = len(segs)
+    arr = (_native.RankSegment * max(S, 1))()
+    keep = []
+    for i, (hi, lo, tie, n_a) in enumerate(segs):
+        arr[i] = _native.RankSegment(_native.ptr(hi), _native.ptr(lo), _native.ptr(tie), int(n_a),
+                                     int(hi.numel()))
+        keep += [hi, lo, tie]
+    L = _native.lib()
+    ws = _native.Workspace.get(L.dw_rank_segmented_workspace_size(S, k))
+    order = torch.full((max(S, 1), max(k, 1)), -1, dtype=torch.int64, device=dev)
+    summary = torch.zeros((max(S, 1), 4), dtype=torch.float64, device=dev)
+    rc = L.dw_rank_segmented(arr, S, int(k), _native.ptr(order), _native.ptr(summary), ws.data_ptr(),
+                             ws.numel(), _native.stream_handle())
+    _native.check(rc, "dw_rank_segmented")
+    return order[:S, :k], summary[:S]
+
+
 def report(findings: Sequence[WasteFinding], ledger_a: EnergyLedger, ledger_b: EnergyLedger,
            threshold: float = DEFAULT_THRESHOLD) -> Report:
     """Machine-readable report plus human summary, ranked by wasted joules
