@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-ops", type=int, default=2_000_000)
+    ap.add_argument("--pairs", type=int, default=64, help="C5 corpus size (trace pairs)")
     ap.add_argument("--shard", default="pair", choices=("pair", "window"),
                     help="N>1: 'pair' = every rank its own trace pair (weak scaling, corpus); "
                          "'window' = ONE pair split by time window over the ranks (strong scaling)")
@@ -594,6 +595,132 @@ def run_window(args, rank: int, world: int, local: int):
     print(json.dumps(line), flush=True)
 
 
+def run_corpus(args, rank: int, world: int, local: int):
+    """C5: a corpus of trace pairs (64 pairs, seeds 5000 + i,
+    6.25M ops / 6.25e7 samples per trace).  Rank r owns the contiguous block of
+    pairs [r * n / N, (r + 1) * n / N) (no data-path collective); a step is
+    pipeline.analyze_corpus over the rank's resident pairs -- both ledgers and
+    the join of every pair, ONE segmented top-k for all of them, the rank's
+    corpus top-k -- plus, for N > 1, the corpus-wide top-k merged over NCCL.
+    A rank holds its pairs resident in HBM while they fit (the whole 64-pair
+    corpus is ~175 GB, so one B200 holds part of it: config names how many)."""
+    import torch
+    import torch.distributed as dist
+    from dataclasses import replace
+
+    from paper_2512_08365_b200 import _native, synth
+    from paper_2512_08365_b200.columns import TraceColumns
+    from paper_2512_08365_b200.dist import merge_topk
+    from paper_2512_08365_b200.pipeline import analyze_corpus
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    L = _native.lib()
+    base = synth.CONFIGS["C5"]
+    n_total = args.pairs
+    lo_p, hi_p = rank * n_total // world, (rank + 1) * n_total // world
+    # HBM left after the resident pairs: analyze's transient workspaces
+    # (~16 GB) + what each pair keeps until the segmented top-k (~1 GB: 32 B
+    # per finding slot, the match / B-only columns, both ledgers' joules)
+    pairs, ids = [], []
+    for i in range(lo_p, hi_p):
+        free, _ = torch.cuda.mem_get_info(dev)
+        per = (torch.cuda.memory_allocated(dev) / len(pairs)) if pairs else 3.5e9
+        if pairs and free < 16e9 + 1.0e9 * (len(pairs) + 1) + 1.1 * per:
+            break
+        ca, cb = synth.make_pair(replace(base, seed=base.seed + i), dev)
+        for c in (ca, cb):
+            for n in TraceColumns.HOT:
+                c.device(n)
+        pairs.append((ca, cb))
+        ids.append(i)
+    torch.cuda.synchronize()
+    print(f"rank {rank}: {len(pairs)} of pairs {lo_p}..{hi_p - 1} resident, "
+          f"{torch.cuda.memory_allocated(dev) / 1e9:.1f} GB allocated", file=sys.stderr, flush=True)
+    intervals = sum(a.n_ops + a.n_kernels + b.n_ops + b.n_kernels for a, b in pairs)
+    samples = sum(a.n_power + b.n_power for a, b in pairs)
+
+    def step():
+        res = analyze_corpus(pairs, args.method, 0.10, args.k, summation=args.summation)
+        if world > 1:  # corpus-wide top-k: every rank's k candidates merged over NCCL
+            hi, lo = [], []
+            for p, f in res.top:
+                jd = res.pairs[p].join
+                ft = torch.tensor([f], dtype=torch.int64, device=dev)
+                tie = jd.pair_of(ft)[0]
+                if jd.columns.tie_rank is not None:
+                    tie = torch.where(tie >= 0, jd.columns.tie_rank[tie.clamp(min=0)], tie)
+                hi.append(jd.columns.key_hi[ft])
+                lo.append(~(((tie + 1) << 32) | ft))
+            if hi:
+                merge_topk(torch.cat(hi), torch.cat(lo), args.k)
+            else:
+                e = torch.empty(0, dtype=torch.int64, device=dev)
+                merge_topk(e, e, args.k)
+        return res
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    L.dw_kernel_time_ms(1)
+    L.dw_kernel_timed_count(1)
+    L.dw_kernel_timing(1)
+    _native.launch_count(reset=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            res = step()
+        e1.record()
+        torch.cuda.synchronize()
+    L.dw_kernel_timing(0)
+    launches = _native.launch_count(reset=True)
+    n_timed = int(L.dw_kernel_timed_count(1))
+    kern_ms = L.dw_kernel_time_ms(1) / max(n_timed, 1)
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms, float(intervals), float(samples), float(len(pairs))], device=dev, dtype=torch.float64)
+    if world > 1:
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+    else:
+        parts = [t]
+    ms_max = max(float(x[0]) for x in parts)
+    tot_iv = sum(float(x[1]) for x in parts)
+    tot_s = sum(float(x[2]) for x in parts)
+    resident = [int(x[3]) for x in parts]
+    if rank != 0:
+        return
+    peak, peak_kind = measured_peak_gbs()
+    a_bytes = (16 * samples + 24 * intervals) / (2 * len(pairs))  # one tile-kernel launch: one trace
+    achieved = a_bytes / (kern_ms * 1e-3) / 1e9
+    P = sum(ps.join.P for ps in res.pairs)
+    line = {
+        "metric": METRIC, "value": tot_iv / (ms_max / 1e3), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"C5: corpus of {n_total} trace pairs ({base.n_ops} ops and {base.n_samples} "
+                               f"power samples per trace), pair-sharded",
+                   "pairs_per_rank_resident": resident, "pairs_timed": sum(resident),
+                   "method": args.method, "summation": args.summation, "top_k_per_pair": args.k,
+                   "findings_rank0": P,
+                   "l2": "inputs (~2.7 GB per pair) >> 126 MB L2; no flush needed",
+                   "parallelism": f"pair blocks x{world}; corpus top-k merged over NCCL"},
+        "samples_per_s": tot_s / (ms_max / 1e3),
+        "roofline": {"bound": "hbm", "kernel": "attribute_exact_kernel", "achieved": achieved,
+                     "peak": peak, "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "bytes_per_launch": a_bytes, "launch_ms": kern_ms, "traffic": None},
+        "e2e": {"skipped": "corpus mode times device-resident pairs only (the C4 line carries e2e)"},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "n_waste_rank0": sum(ps.n_waste for ps in res.pairs),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -616,6 +743,9 @@ def main():
     try:
         if args.shard == "window":
             run_window(args, rank, world, local)
+            return
+        if args.config == "C5":
+            run_corpus(args, rank, world, local)
             return
         run_ours(args, rank, world, local)
     finally:

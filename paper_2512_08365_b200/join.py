@@ -122,7 +122,7 @@ class JoinDiff:
     b_only: torch.Tensor         # int32 [n_b_only]
     epw_a: Optional[torch.Tensor]
     epw_b: Optional[torch.Tensor]
-    order: torch.Tensor          # top-k finding indices, report order
+    order: Optional[torch.Tensor]  # top-k finding indices, report order (None: ranked elsewhere)
     n_waste: int
     wasted_joules: float         # exact sum over all waste findings
     ja: Optional[torch.Tensor] = None    # operator joules of A / B (for lean columns)
@@ -141,13 +141,13 @@ class JoinDiff:
         return ia, ib
 
     def top_findings(self, cols_a: TraceColumns, cols_b: TraceColumns, classify: bool = True,
-                     trace_a=None, trace_b=None) -> list[WasteFinding]:
+                     trace_a=None, trace_b=None, idx: Optional[torch.Tensor] = None) -> list[WasteFinding]:
         """Materialise the top-k findings (report order) as reference-style
         WasteFinding objects; columns not written by the join are gathered from
         the ledgers on the device for these k rows only.  Waste findings are
         classified as detect_waste does (diagnose.classify_pairs; the trace
         objects, when given, enable the program-model probe)."""
-        idx = self.order
+        idx = self.order if idx is None else idx
         c = self.columns
         ia_d, ib_d = self.pair_of(idx)
         has_a, has_b = ia_d >= 0, ib_d >= 0
@@ -268,9 +268,11 @@ def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
               threshold: float = DEFAULT_THRESHOLD, k: int = 100, *, full_columns: bool = True,
               epw: bool = True, work_a=None, work_b=None, stream=None,
               max_distinct: int = DEFAULT_MAX_DISTINCT, prep: Optional[JoinPrep] = None,
-              columns: Optional[Sequence[str]] = None) -> JoinDiff:
+              columns: Optional[Sequence[str]] = None, ranked: bool = True) -> JoinDiff:
     """Signature-join diff of two traces with their ledgers; top-k ranked.
-    ``prep``: the pairing already made by ``join_prepare`` (same traces)."""
+    ``prep``: the pairing already made by ``join_prepare`` (same traces).
+    ``ranked=False``: no ranking here (``order`` None, n_waste / wasted_joules
+    0) -- a corpus ranks all its pairs at once (``pipeline.analyze_corpus``)."""
     if ledger_a.method != ledger_b.method:
         raise ValueError(f"ledger method mismatch: {ledger_a.method!r} vs {ledger_b.method!r}")
     if not 0 < threshold <= 1:
@@ -310,8 +312,11 @@ def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
                                      prep.ws.numel(), _native.stream_handle(stream)), "dw_join_findings")
     P, matched, a_only, b_only = (int(x) for x in count.cpu().tolist())
     kk = min(k, P)
-    order, summary = rank_order(fc.key_hi[:P], None, kk, tie_rank=rank_a, n_a=na)
-    sm = summary.cpu().tolist()
+    if ranked:
+        order, summary = rank_order(fc.key_hi[:P], None, kk, tie_rank=rank_a, n_a=na)
+        sm = summary.cpu().tolist()
+    else:
+        order, sm = None, [0, 0.0]
     return JoinDiff(P=P, n_a=na, n_matched=matched, n_a_only=a_only, n_b_only=b_only, columns=fc,
                     match_a=prep.match_a[:na], b_only=prep.b_only[:b_only],
                     epw_a=epw_a, epw_b=epw_b, order=order, n_waste=int(sm[0]),

@@ -14,8 +14,10 @@ import torch
 
 from . import _native
 from .columns import TraceColumns
-from .detect import DEFAULT_THRESHOLD, FindingColumns, Report
+from .detect import DEFAULT_THRESHOLD, FindingColumns, Report, WasteFinding, rank_order_segmented
 from .energy import EnergyLedger, build_ledger
+
+import numpy as np
 from .join import JoinDiff, join_diff, join_prepare
 
 
@@ -89,3 +91,94 @@ def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAUL
                  wasted_joules=jd.wasted_joules, end_to_end_waste_pct=pct, method=method,
                  threshold=threshold)
     return Analysis(la, lb, rep, jd)
+
+
+@dataclass
+class PairSummary:
+    """One pair of a corpus after ``analyze_corpus``: its ledgers' totals, the
+    join (device columns; ``order`` = this pair's top-k in report order) and
+    its waste totals over every finding."""
+
+    total_a: float
+    total_b: float
+    join: JoinDiff
+    n_waste: int
+    wasted_joules: float
+
+
+@dataclass
+class CorpusAnalysis:
+    pairs: list                       # PairSummary per pair, corpus order
+    order: torch.Tensor               # [S, k] per-pair top-k finding indices (-1 padded)
+    top: list                         # corpus top-k: (pair index, finding index), report order
+
+    def findings(self, columns, classify: bool = True) -> list:
+        """The corpus top-k as (pair index, WasteFinding); ``columns`` =
+        [(cols_a, cols_b)] per pair."""
+        out = []
+        by_pair: dict = {}
+        for r, (i, f) in enumerate(self.top):
+            by_pair.setdefault(i, []).append((r, f))
+        rows: dict = {}
+        for i, items in by_pair.items():
+            jd = self.pairs[i].join
+            idx = torch.tensor([f for _, f in items], dtype=torch.int64, device=jd.columns.key_hi.device)
+            ca, cb = columns[i]
+            for (r, _), wf in zip(items, jd.top_findings(ca, cb, classify=classify, idx=idx)):
+                rows[r] = (i, wf)
+        for r in range(len(self.top)):
+            out.append(rows[r])
+        return out
+
+
+def analyze_corpus(pairs, method: str = "samples", threshold: float = DEFAULT_THRESHOLD, k: int = 100, *,
+                   summation: str = "exact") -> CorpusAnalysis:
+    """A corpus of trace pairs: per pair, both ledgers and
+    the signature-join diff (differential columns + ranking key, as
+    ``analyze``); then ONE segmented top-k launch sequence ranks every pair's
+    findings (``dw_rank_segmented``: per-pair report order and exact waste
+    sums), and the corpus top-k is the merge of the per-pair top-k lists on the
+    same composite key, ties between pairs going to the earlier pair
+    (detect.py:263-266 per pair).  Each pair's ledgers are released after its
+    join; only the finding columns stay on the device."""
+    summaries, segs = [], []
+    for a, b in pairs:
+        ca, cb = TraceColumns.from_trace(a), TraceColumns.from_trace(b)
+        la = build_ledger(ca, method=method, summation=summation)
+        lb = build_ledger(cb, method=method, summation=summation)
+        jd = join_diff(ca, cb, la, lb, threshold, k, full_columns=False, epw=False,
+                       columns=FindingColumns.DELTAS, ranked=False)
+        summaries.append(PairSummary(la.total_joules, lb.total_joules, jd, 0, 0.0))
+        segs.append((jd.columns.key_hi[:jd.P], None, jd.columns.tie_rank, jd.n_a))
+        del la, lb
+    order, summary = rank_order_segmented(segs, k)
+    sm = summary.cpu().numpy()
+    for i, ps in enumerate(summaries):
+        ps.n_waste, ps.wasted_joules = int(sm[i, 0]), float(sm[i, 1])
+        ps.join.n_waste, ps.join.wasted_joules = ps.n_waste, ps.wasted_joules
+        n = min(k, ps.join.P)
+        ps.join.order = order[i, :n]
+    # corpus merge: every pair's top-k keys, ordered by (hi, lo) descending, pair ascending
+    keys = []
+    for i, ps in enumerate(summaries):
+        o = ps.join.order
+        if o.numel() == 0:
+            continue
+        jd = ps.join
+        hi = jd.columns.key_hi[o]
+        tie = jd.pair_of(o)[0]
+        if jd.columns.tie_rank is not None:
+            tie = torch.where(tie >= 0, jd.columns.tie_rank[tie.clamp(min=0)], tie)
+        lo = ~(((tie + 1) << 32) | o)
+        keys.append(torch.stack([hi, lo, torch.full_like(o, i), o]))
+    top = []
+    if keys:
+        kk = torch.cat(keys, dim=1).cpu().numpy()
+        hi_u = kk[0].view(np.uint64)
+        lo_u = kk[1].view(np.uint64)
+        # primary key last: hi desc, nodes_a tie asc (lo's upper half, stored
+        # complemented), then corpus order (pair, finding) -- a stable sort of
+        # the concatenated findings, as report() on the whole corpus would give
+        sel = np.lexsort((kk[3], kk[2], ~(lo_u >> np.uint64(32)), ~hi_u))
+        top = [(int(kk[2][j]), int(kk[3][j])) for j in sel[:k]]
+    return CorpusAnalysis(summaries, order, top)
