@@ -536,13 +536,7 @@ def run_window(args, rank: int, world: int, local: int):
     cfg = synth.CONFIGS[args.config]
     ca, cb = synth.make_pair(cfg)
     kind = "linear" if args.method == "samples" else "step"
-    comm = shard.Comm() if world > 1 else None
-    if comm is None:
-        class _One:
-            rank, world = 0, 1
-            all_gather_object = staticmethod(lambda o: [o])
-            all_to_all = staticmethod(lambda ts: ts)
-        comm = _One()
+    comm = shard.Comm() if world > 1 else shard.LocalComm()
     win_a = shard.plan(ca.n_power, world, kind)[rank]
     win_b = shard.plan(cb.n_power, world, kind)[rank]
     ia, ib = shard.rank_inputs(ca, kind, win_a), shard.rank_inputs(cb, kind, win_b)

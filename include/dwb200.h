@@ -451,6 +451,17 @@ int dw_exchange_count(const int64_t *d_sig, int64_t n, int32_t world, uint64_t *
  * base are HOST arrays of device pointers / offsets. */
 int dw_exchange_scatter(const int64_t *const *cols, int32_t width, const int64_t *d_sig, int64_t n, int32_t world,
                         int64_t *const *d_peer, const int64_t *base, uint64_t *d_cursor, dw_stream_t stream);
+/* Arrival flags of a persistent receive buffer: after its scatter, a sender
+ * stores `epoch` into slot [me] of every receiver's flag array
+ * (d_peer_flags[d]: receiver d's array, IPC-mapped; system-scope release after
+ * a system fence); dw_exchange_wait holds the receiver's stream until every
+ * sender's slot of d_flags[world] reaches `epoch` (device-side; *d_timeout
+ * set to 1 if a sender never signals within ~20 s).  d_peer_flags is a HOST
+ * array of device pointers. */
+int dw_exchange_signal(uint64_t *const *d_peer_flags, int32_t world, int32_t me, uint64_t epoch,
+                       dw_stream_t stream);
+int dw_exchange_wait(const uint64_t *d_flags, int32_t world, uint64_t epoch, int32_t *d_timeout,
+                     dw_stream_t stream);
 /* CUDA IPC plumbing for the receive buffers (64-byte handles).  A buffer
  * inside a larger allocation exports the allocation's handle plus its byte
  * offset; the opener adds the offset to what dw_ipc_open returns. */

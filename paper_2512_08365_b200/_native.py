@@ -47,7 +47,8 @@ EXPORTED = (
     "dw_fx_sum_workspace_size", "dw_fx_sum", "dw_step_value_at", "dw_detect_pairs",
     "dw_rank_workspace_size", "dw_rank", "dw_rank_segmented_workspace_size", "dw_rank_segmented",
     "dw_join_workspace_size", "dw_join_diff",
-    "dw_exchange_count", "dw_exchange_scatter", "dw_ipc_handle", "dw_ipc_open", "dw_ipc_close",
+    "dw_exchange_count", "dw_exchange_scatter", "dw_exchange_signal", "dw_exchange_wait",
+    "dw_ipc_handle", "dw_ipc_open", "dw_ipc_close",
     "dw_tensor_norms", "dw_tensor_prefilter", "dw_unfold_smem_doubles", "dw_unfold_spectra", "dw_spectra_embed",
     "dw_version", "dw_error_string", "dw_launch_count", "dw_kernel_timing", "dw_kernel_time_ms",
     "dw_kernel_timed_count",
@@ -163,6 +164,8 @@ def lib():
         L.dw_tensor_norms.argtypes = [c_vp, c_vp, c_i64, c_vp, c_vp]
         L.dw_exchange_count.argtypes = [c_vp, c_i64, c_i32, c_vp, c_vp]
         L.dw_exchange_scatter.argtypes = [c_vp, c_i32, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]
+        L.dw_exchange_signal.argtypes = [c_vp, c_i32, c_i32, ctypes.c_uint64, c_vp]
+        L.dw_exchange_wait.argtypes = [c_vp, c_i32, ctypes.c_uint64, c_vp, c_vp]
         L.dw_ipc_handle.argtypes = [c_vp, c_vp, c_vp]
         L.dw_ipc_open.argtypes = [c_vp, ctypes.POINTER(c_vp)]
         L.dw_ipc_close.argtypes = [c_vp]

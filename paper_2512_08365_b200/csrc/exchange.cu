@@ -69,6 +69,42 @@ __global__ void exchange_scatter_kernel(XchCols x, int width, const int64_t *sig
     }
 }
 
+
+// Arrival flags of the persistent mailbox (shard.Comm): after its scatter a
+// sender publishes the exchange's epoch into slot [me] of every receiver's
+// flag array (system-scope release, after a system fence, so its P2P record
+// stores are visible first); a receiver's stream waits on the device until
+// every sender's slot holds the epoch -- no host sync, no barrier.
+struct XchFlags {
+    unsigned long long *peer[DW_MAX_PEERS];
+};
+
+__global__ void exchange_signal_kernel(XchFlags f, int world, int me, unsigned long long epoch) {
+    __threadfence_system();
+    for (int d = threadIdx.x; d < world; d += blockDim.x) {
+        unsigned long long *slot = f.peer[d] + me;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot), "l"(epoch) : "memory");
+    }
+}
+
+__global__ void exchange_wait_kernel(const unsigned long long *flags, int world, unsigned long long epoch,
+                                     int *timeout) {
+    for (int s = threadIdx.x; s < world; s += blockDim.x) {
+        const long long t0 = clock64();
+        for (;;) {
+            unsigned long long v;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + s) : "memory");
+            if (v >= epoch) break;
+            if (clock64() - t0 > (long long)40000000000LL) {  // ~20 s at 2 GHz: a peer never signalled
+                atomicExch(timeout, 1);
+                break;
+            }
+            __nanosleep(256);
+        }
+    }
+    __threadfence_system();
+}
+
 }  // namespace dw
 
 using namespace dw;
@@ -109,6 +145,31 @@ int dw_exchange_scatter(const int64_t *const *cols, int32_t width, const int64_t
                                   XCH_THREADS, 0, s>>>(x, width, d_sig, n, world, (unsigned long long *)d_cursor);
         count_launch();
     }
+    DW_CHECK_LAUNCH();
+    return DW_OK;
+}
+
+
+int dw_exchange_signal(uint64_t *const *d_peer_flags, int32_t world, int32_t me, uint64_t epoch,
+                       dw_stream_t stream) {
+    if (world < 1 || world > DW_MAX_PEERS || me < 0 || me >= world || !d_peer_flags) return DW_E_ARG;
+    XchFlags f{};
+    for (int d = 0; d < world; ++d) {
+        if (!d_peer_flags[d]) return DW_E_ARG;
+        f.peer[d] = (unsigned long long *)d_peer_flags[d];
+    }
+    exchange_signal_kernel<<<1, 64, 0, (cudaStream_t)stream>>>(f, world, me, (unsigned long long)epoch);
+    count_launch();
+    DW_CHECK_LAUNCH();
+    return DW_OK;
+}
+
+int dw_exchange_wait(const uint64_t *d_flags, int32_t world, uint64_t epoch, int32_t *d_timeout,
+                     dw_stream_t stream) {
+    if (world < 1 || world > DW_MAX_PEERS || !d_flags || !d_timeout) return DW_E_ARG;
+    exchange_wait_kernel<<<1, 64, 0, (cudaStream_t)stream>>>((const unsigned long long *)d_flags, world,
+                                                             (unsigned long long)epoch, (int *)d_timeout);
+    count_launch();
     DW_CHECK_LAUNCH();
     return DW_OK;
 }

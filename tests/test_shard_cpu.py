@@ -102,7 +102,9 @@ def test_global_merge_matches_one_ranking():
         bits = wasted[mine].view(np.uint64) & np.uint64(0x7FFFFFFFFFFFFFFF)
         hi = (bits | ((verdict[mine] == 2).astype(np.uint64) << np.uint64(63))).view(np.int64)
         lo = (~(((tie[mine] + 1).astype(np.uint64) << np.uint64(32)) | mine.astype(np.uint64))).view(np.int64)
-        rows = [(int(f),) for f in mine]
-        gathered.append((torch.from_numpy(hi), torch.from_numpy(lo), rows, 0, 0, 0))
+        rows_i = torch.zeros(len(mine), 7, dtype=torch.int64)
+        rows_i[:, 0] = torch.from_numpy(mine)
+        gathered.append((torch.from_numpy(hi), torch.from_numpy(lo), rows_i,
+                         torch.zeros(len(mine), 4, dtype=torch.float64), torch.zeros(4, dtype=torch.int64)))
     res = shard._merge(gathered, 60)
     assert [r[0] for r in res.top] == want
