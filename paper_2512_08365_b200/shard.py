@@ -19,11 +19,13 @@ samples and every interval (operator or kernel) whose start falls in it.
     totals    ledger total = exact sum of every rank's owned whole-tile sums;
               operator_total = exact sum of every rank's 2^-64 J share.
 
-The exchanges are small (crossing intervals are at most the concurrency at
-each window edge) and go through ``Comm`` -- torch.distributed (NCCL on GPU,
-gloo on CPU) or an in-process loopback that runs the ranks one after the other
-(single-GPU parity tests).  The signature join of a sharded pair partitions
-operators by signature hash with one all-to-all (``sharded_join``).
+The exchanges are small tensor all-gathers (crossing intervals are at most
+the concurrency at each window edge) through ``Comm`` -- torch.distributed
+(NCCL on GPU, gloo on CPU) -- or an in-process loopback that runs the ranks
+one after the other (single-GPU parity tests).  The signature join of a
+sharded pair partitions operators by signature hash: one fused peer-memory
+scatter into persistent receive buffers (``Comm.exchange``) or one NCCL
+all-to-all (``sharded_join``).
 """
 
 from __future__ import annotations
