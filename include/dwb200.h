@@ -246,12 +246,22 @@ int dw_ig_classify(const uint8_t *buf, int64_t n, const int64_t *ends, int64_t n
                    dw_stream_t stream);
 int dw_ig_parse_power(const uint8_t *buf, const int64_t *ends, const int64_t *lines, int64_t m, int64_t *ts,
                       double *w, unsigned *flags, dw_stream_t stream);
+/* tl_off / tl_len (may both be NULL): [2m] byte spans of each op's
+ * input_tensor_ids and output_tensor_ids JSON lists (the host validates them
+ * against the tensor records); NULL flags any tensor reference instead. */
 int dw_ig_parse_op(const uint8_t *buf, const int64_t *ends, const int64_t *lines, int64_t m, int64_t *id_off,
                    int32_t *id_len, int64_t *name_off, int32_t *name_len, int64_t *kl_first, int32_t *kl_count,
-                   int64_t *start, int64_t *end, unsigned *flags, dw_stream_t stream);
+                   int64_t *start, int64_t *end, int64_t *tl_off, int32_t *tl_len, unsigned *flags,
+                   dw_stream_t stream);
 int dw_ig_parse_kernel(const uint8_t *buf, const int64_t *ends, const int64_t *lines, int64_t m, int64_t *id_off,
                        int32_t *id_len, int64_t *name_off, int32_t *name_len, int64_t *corr, int64_t *start,
                        int64_t *end, unsigned *flags, dw_stream_t stream);
+/* Word w (bytes 8w .. 8w+7) of each id span as a big-endian uint64, zero past
+ * the id's end: sorting ids by these words, last word first (stable), gives
+ * their byte-string order -- the op-id ranks of the report tie-break
+ * (detect.py:265, nodes_a) computed at ingest. */
+int dw_ig_id_words(const uint8_t *buf, const int64_t *off, const int32_t *len, int64_t m, int32_t w,
+                   uint64_t *out, dw_stream_t stream);
 int dw_ig_hash(const uint8_t *buf, const int64_t *off, const int32_t *len, int64_t m, uint64_t *h, uint32_t *idx,
                dw_stream_t stream);
 int dw_ig_kernel_lists(const uint8_t *buf, int64_t nops, const int64_t *kl_first, const int32_t *kl_count,

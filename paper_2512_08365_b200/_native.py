@@ -43,7 +43,7 @@ EXPORTED = (
     "dw_unpack_dict", "dw_unpack_bits", "dw_unpack_bits_dur", "dw_unpack_dict_bits",
     "dw_join_prepare", "dw_join_findings",
     "dw_set_attribute_sms", "dw_ig_nl_count", "dw_ig_nl_write", "dw_ig_classify", "dw_ig_parse_power",
-    "dw_ig_parse_op", "dw_ig_parse_kernel", "dw_ig_hash", "dw_ig_kernel_lists",
+    "dw_ig_parse_op", "dw_ig_parse_kernel", "dw_ig_hash", "dw_ig_id_words", "dw_ig_kernel_lists",
     "dw_fx_sum_workspace_size", "dw_fx_sum", "dw_step_value_at", "dw_detect_pairs",
     "dw_rank_workspace_size", "dw_rank", "dw_rank_segmented_workspace_size", "dw_rank_segmented",
     "dw_join_workspace_size", "dw_join_diff",
@@ -145,9 +145,10 @@ def lib():
         L.dw_ig_nl_write.argtypes = [c_vp, c_i64, c_vp, c_vp, c_vp]
         L.dw_ig_classify.argtypes = [c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]
         L.dw_ig_parse_power.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp]
-        L.dw_ig_parse_op.argtypes = [c_vp, c_vp, c_vp, c_i64] + [c_vp] * 10
+        L.dw_ig_parse_op.argtypes = [c_vp, c_vp, c_vp, c_i64] + [c_vp] * 12
         L.dw_ig_parse_kernel.argtypes = [c_vp, c_vp, c_vp, c_i64] + [c_vp] * 9
         L.dw_ig_hash.argtypes = [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]
+        L.dw_ig_id_words.argtypes = [c_vp, c_vp, c_vp, c_i64, c_i32, c_vp, c_vp]
         L.dw_ig_kernel_lists.argtypes = [c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64] + [c_vp] * 11
         L.dw_unpack_workspace_size.restype = ctypes.c_size_t
         L.dw_unpack_workspace_size.argtypes = [c_i64]

@@ -221,8 +221,7 @@ __global__ void classify_kernel(const uint8_t *buf, int64_t n, const int64_t *en
     else if (c.lit("{\"type\":\"power\",")) t = L_POWER;
     else if (c.lit("{\"type\":\"op\",")) t = L_OP;
     else if (c.lit("{\"type\":\"kernel\",")) t = L_KERNEL;
-    else if (c.lit("{\"type\":\"tensor\",")) { t = L_OTHER; atomicOr(flags, F_TENSOR); }
-    else t = L_OTHER;
+    else t = L_OTHER;  // header, config, tensor, progmodel, blocktrace: decoded on the host
     type[i] = t;
 }
 
@@ -247,7 +246,7 @@ __global__ void parse_power_kernel(const uint8_t *buf, const int64_t *ends, cons
 __global__ void parse_op_kernel(const uint8_t *buf, const int64_t *ends, const int64_t *lines, int64_t m,
                                 int64_t *id_off, int32_t *id_len, int64_t *name_off, int32_t *name_len,
                                 int64_t *kl_first, int32_t *kl_count, int64_t *start, int64_t *end,
-                                unsigned *flags) {
+                                int64_t *tl_off, int32_t *tl_len, unsigned *flags) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= m) return;
     const int64_t i = lines[k];
@@ -255,13 +254,23 @@ __global__ void parse_op_kernel(const uint8_t *buf, const int64_t *ends, const i
     Cur c{buf + a, buf + ends[i]};
     int64_t io = 0, no = 0, kf = 0, s = 0, e = 0, dummy;
     int32_t il = 0, nl = 0, kc = 0, nin = 0, nout = 0;
+    const uint8_t *lin = nullptr, *lout = nullptr, *lend = nullptr;
     bool ok = c.lit("{\"type\":\"op\",\"op_id\":") && take_str(c, buf, io, il) && c.lit(",\"op_name\":") &&
-              take_str(c, buf, no, nl) && c.lit(",\"input_tensor_ids\":") && take_str_list(c, buf, nin, dummy) &&
-              c.lit(",\"output_tensor_ids\":") && take_str_list(c, buf, nout, dummy) &&
+              take_str(c, buf, no, nl) && c.lit(",\"input_tensor_ids\":") && (lin = c.p, true) &&
+              take_str_list(c, buf, nin, dummy) && c.lit(",\"output_tensor_ids\":") && (lout = c.p, true) &&
+              take_str_list(c, buf, nout, dummy) && (lend = c.p, true) &&
               c.lit(",\"kernel_ids\":") && take_str_list(c, buf, kc, kf) && c.lit(",\"start\":") && c.int64v(s) &&
               c.lit(",\"end\":") && c.int64v(e) && c.lit("}") && c.at_end();
     if (!ok) atomicOr(flags, F_BAD_LINE);
-    if (ok && (nin || nout)) atomicOr(flags, F_TENSOR);  // tensor references: the Python path validates them
+    // tensor references: without span outputs the Python path validates them;
+    // with them the host checks them against the trace's tensor records
+    if (ok && (nin || nout) && !tl_off) atomicOr(flags, F_TENSOR);
+    if (tl_off) {  // the two lists' JSON text: [input list] then [output list], back to back
+        tl_off[2 * k] = ok ? lin - buf : 0;
+        tl_len[2 * k] = ok ? (int32_t)(lout - lin - (int)sizeof(",\"output_tensor_ids\":") + 1) : 0;
+        tl_off[2 * k + 1] = ok ? lout - buf : 0;
+        tl_len[2 * k + 1] = ok ? (int32_t)(lend - lout) : 0;
+    }
     if (ok && e < s) atomicOr(flags, F_INTERVAL);          // OperatorEvent.validate
     id_off[k] = io; id_len[k] = il; name_off[k] = no; name_len[k] = nl;
     kl_first[k] = kf; kl_count[k] = kc; start[k] = s; end[k] = e;
@@ -287,6 +296,23 @@ __global__ void parse_kernel_kernel(const uint8_t *buf, const int64_t *ends, con
     if (ok && (e <= s || bc == 0)) atomicOr(flags, F_INTERVAL);  // KernelEvent.validate
     id_off[k] = io; id_len[k] = il; name_off[k] = no; name_len[k] = nl;
     corr[k] = cr; start[k] = s; end[k] = e;
+}
+
+// word w of each id as a big-endian 64-bit integer, zero padded past its end:
+// unsigned order of the words, most significant first = byte-string order
+__global__ void id_words_kernel(const uint8_t *buf, const int64_t *off, const int32_t *len, int64_t m, int w,
+                                uint64_t *out) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const int32_t n = len[k];
+    const uint8_t *s = buf + off[k];
+    uint64_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const int32_t i = 8 * w + b;
+        v = (v << 8) | (i < n ? (uint64_t)s[i] : 0ULL);
+    }
+    out[k] = v;
 }
 
 // 64-bit FNV-1a of a byte string
@@ -391,15 +417,22 @@ int dw_ig_parse_power(const uint8_t *buf, const int64_t *ends, const int64_t *li
 }
 int dw_ig_parse_op(const uint8_t *buf, const int64_t *ends, const int64_t *lines, int64_t m, int64_t *id_off,
                    int32_t *id_len, int64_t *name_off, int32_t *name_len, int64_t *kl_first, int32_t *kl_count,
-                   int64_t *start, int64_t *end, unsigned *flags, dw_stream_t stream) {
+                   int64_t *start, int64_t *end, int64_t *tl_off, int32_t *tl_len, unsigned *flags,
+                   dw_stream_t stream) {
+    if ((tl_off == nullptr) != (tl_len == nullptr)) return DW_E_ARG;
     IG_LAUNCH(parse_op_kernel, m, buf, ends, lines, m, id_off, id_len, name_off, name_len, kl_first, kl_count, start,
-              end, flags);
+              end, tl_off, tl_len, flags);
 }
 int dw_ig_parse_kernel(const uint8_t *buf, const int64_t *ends, const int64_t *lines, int64_t m, int64_t *id_off,
                        int32_t *id_len, int64_t *name_off, int32_t *name_len, int64_t *corr, int64_t *start,
                        int64_t *end, unsigned *flags, dw_stream_t stream) {
     IG_LAUNCH(parse_kernel_kernel, m, buf, ends, lines, m, id_off, id_len, name_off, name_len, corr, start, end,
               flags);
+}
+int dw_ig_id_words(const uint8_t *buf, const int64_t *off, const int32_t *len, int64_t m, int32_t w,
+                   uint64_t *out, dw_stream_t stream) {
+    if (w < 0) return DW_E_ARG;
+    IG_LAUNCH(id_words_kernel, m, buf, off, len, m, w, out);
 }
 int dw_ig_hash(const uint8_t *buf, const int64_t *off, const int32_t *len, int64_t m, uint64_t *h, uint32_t *idx,
                dw_stream_t stream) {

@@ -78,10 +78,15 @@ def _ranks(cols: TraceColumns, dev) -> Optional[torch.Tensor]:
         return cols.device("op_rank")
     if cols.op_ids is None:
         return None
-    order = sorted(range(len(cols.op_ids)), key=lambda i: cols.op_ids[i])
-    rank = np.empty(len(order), dtype=np.int64)
-    rank[np.asarray(order, dtype=np.int64)] = np.arange(len(order), dtype=np.int64)
-    cols.op_rank = rank
+    # ids from the Python loader: their UTF-8 bytes (byte order = str order)
+    # ranked on the device, as ingest does for files it parses
+    from .ingest import id_ranks
+    enc = [str(x).encode("utf-8") for x in cols.op_ids]
+    lens = np.fromiter((len(e) for e in enc), dtype=np.int64, count=len(enc))
+    offs = np.concatenate([[0], np.cumsum(lens)[:-1]]) if len(enc) else np.zeros(0, dtype=np.int64)
+    buf = torch.from_numpy(np.frombuffer(b"".join(enc) or b"\0", dtype=np.uint8).copy()).to(dev)
+    cols.op_rank = id_ranks(buf, torch.from_numpy(offs.astype(np.int64)).to(dev),
+                            torch.from_numpy(lens.astype(np.int32)).to(dev))
     return cols.device("op_rank")
 
 

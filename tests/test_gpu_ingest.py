@@ -61,6 +61,7 @@ def test_canonical_scale_trace_parses_on_device(tmp_path):
     assert got.loaded_by == "gpu"
     _same(got, TraceColumns.from_trace(load_trace(str(path))))
     assert got.header == tr.header and got.config == {"idle_watts": 75.0}
+    _same_ranks(got, [o.op_id for o in tr.operators])
 
 
 def test_no_trailing_newline_and_blank_lines(tmp_path):
@@ -73,13 +74,74 @@ def test_no_trailing_newline_and_blank_lines(tmp_path):
 
 
 @pytest.mark.parametrize("name", ["tf32_misconfig", "join_redundant"])
-def test_reference_traces_take_the_python_path(name):
-    """Golden reference traces carry tensors: loaded by the Python path."""
+def test_reference_traces_with_tensors_parse_on_device(name):
+    """Golden reference traces carry tensor snapshots (and a program model):
+    power / op / kernel records still parse on the device, only the other
+    records are decoded on the host, and the operator-tensor rules hold."""
     for side in ("trace_a", "trace_b"):
         path = GOLDEN / "traces" / name / f"{side}.jsonl"
         got = load_columns(path)
-        assert got.loaded_by == "python"
-        _same(got, TraceColumns.from_trace(load_trace(str(path))))
+        assert got.loaded_by == "gpu"
+        ref = load_trace(str(path))
+        _same(got, TraceColumns.from_trace(ref))
+        assert got.tensors == ref.tensors and got.progmodel == ref.progmodel
+        assert tuple(got.blocktraces) == tuple(ref.blocktraces)
+        assert got.op_tensors == [(o.input_tensor_ids, o.output_tensor_ids) for o in ref.operators]
+        _same_ranks(got, [o.op_id for o in ref.operators])
+
+
+def _same_ranks(cols, ids):
+    want = np.empty(len(ids), dtype=np.int64)
+    want[np.array(sorted(range(len(ids)), key=lambda i: ids[i]), dtype=np.int64)] = np.arange(len(ids))
+    np.testing.assert_array_equal(cols.device("op_rank").cpu().numpy(), want)
+
+
+def test_op_id_ranks_at_ingest(tmp_path):
+    """Lexicographic op-id ranks (the report's nodes_a tie-break) on the
+    device: ids of different lengths, shared prefixes, multi-word ids."""
+    tr = _synthetic_trace(500, seed=9)
+    rng = np.random.default_rng(9)
+    names = [f"{'x' * int(rng.integers(0, 20))}{rng.integers(0, 10**6)}" + ("_long_suffix" * int(rng.integers(0, 3)))
+             for _ in tr.operators]
+    names = [f"{n}#{i}" for i, n in enumerate(names)]  # unique
+    ops = tuple(OperatorEvent(n, o.op_name, (), (), o.kernel_ids, o.start, o.end) for n, o in zip(names, tr.operators))
+    tr = Trace(tr.header, {}, ops, tr.kernels, tr.power, (), None, tr.config)
+    path = tmp_path / "t.jsonl"
+    path.write_text("\n".join(trace_to_lines(tr)) + "\n")
+    got = load_columns(path)
+    assert got.loaded_by == "gpu"
+    ids = [o.op_id for o in load_trace(str(path)).operators]
+    _same_ranks(got, ids)
+
+
+def _tensor_mutations():
+    return {
+        "missing_tensor": lambda L: [x for i, x in enumerate(L)
+                                     if i != [j for j, y in enumerate(L) if '"type":"tensor"' in y][0]],
+        "two_producers": lambda L: _two_producers(L),
+    }
+
+
+def _two_producers(L):
+    ops = [i for i, x in enumerate(L) if '"type":"op"' in x]
+    L = list(L)
+    a, b = json.loads(L[ops[0]]), json.loads(L[ops[1]])
+    b["output_tensor_ids"] = list(a["output_tensor_ids"])
+    L[ops[1]] = json.dumps(b, separators=(",", ":"))
+    return L
+
+
+@pytest.mark.parametrize("mut", list(_tensor_mutations()))
+def test_tensor_rule_violations_raise_the_reference_error(tmp_path, mut):
+    src = (GOLDEN / "traces" / "join_redundant" / "trace_a.jsonl").read_text().splitlines()
+    lines = _tensor_mutations()[mut](src)
+    path = tmp_path / "t.jsonl"
+    path.write_text("\n".join(lines) + "\n")
+    with pytest.raises(Exception) as want:
+        load_trace(str(path))
+    with pytest.raises(type(want.value)) as got:
+        load_columns(path)
+    assert str(got.value) == str(want.value)
 
 
 def _mutations():
