@@ -1194,7 +1194,7 @@ constexpr int64_t CAND_MIN = 1 << 16;
 
 struct RankLayout {
     size_t hist, sel, cand_n, cand_hi, cand_lo, cand_idx, tmp_hi, tmp_lo, tmp_idx, tmp_idx2,
-        partials, done, cub, cub_bytes, total;
+        partials, done, seg, seg_bytes, cub, cub_bytes, total;
     int64_t cap;
 };
 
@@ -1217,6 +1217,8 @@ static RankLayout rank_layout(int64_t P, int64_t k) {
     L.tmp_idx2 = off; off += au(8 * cap);
     L.partials = off; off += au(24 * 1024);
     L.done = off; off += au(16);
+    L.seg_bytes = dw_rank_segmented_workspace_size(1, std::min<int64_t>(k, 8192));
+    L.seg = off; off += au(L.seg_bytes);
     size_t c1 = 0;
     cub::DeviceRadixSort::SortPairsDescending(nullptr, c1, (const uint64_t *)nullptr, (uint64_t *)nullptr,
                                               (const int64_t *)nullptr, (int64_t *)nullptr, (int)cap);
@@ -1336,9 +1338,21 @@ static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, const 
     if ((int64_t)nc > L.cap) return DW_E_WORKSPACE;  // massive ties at the threshold key
     if ((int64_t)nc < k) return DW_E_ARG;             // cannot happen
     trace_mark(s, "rank:compact");
-    sort_candidates(base, L, (int64_t)nc, s);
+    if (k <= 8192) {
+        // the k best of the candidates: the segmented top-k on the candidate
+        // keys (a few small radix passes, then a shared-memory bitonic sort --
+        // no library sort), mapped back to finding indices
+        dw_rank_segment_t seg{r.cand_hi, r.cand_lo, nullptr, 0, (int64_t)nc};
+        int64_t *pos = (int64_t *)(base + L.tmp_idx2);
+        const int rc = dw_rank_segmented(&seg, 1, k, pos, nullptr, base + L.seg, L.seg_bytes, s);
+        if (rc != DW_OK) return rc;
+        gather_i64_kernel<<<blocks_for(k), 256, 0, s>>>(r.cand_idx, pos, k, order);
+        count_launch();
+    } else {
+        sort_candidates(base, L, (int64_t)nc, s);
+        cudaMemcpyAsync(order, base + L.tmp_idx, 8 * k, cudaMemcpyDeviceToDevice, s);
+    }
     trace_mark(s, "rank:sort");
-    cudaMemcpyAsync(order, base + L.tmp_idx, 8 * k, cudaMemcpyDeviceToDevice, s);
     DW_CHECK_LAUNCH();
     return DW_OK;
 }
