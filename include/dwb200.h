@@ -479,6 +479,18 @@ int dw_ipc_handle(const void *d_ptr, void *handle_out, int64_t *offset_out);
 int dw_ipc_open(const void *handle, void **d_ptr_out);
 int dw_ipc_close(void *d_ptr);
 
+/* ------------------------------------------- misconfiguration probe (8(f)3)
+ * Batched kernel-name alignment of analyze_segment_pair (diagnose.py:203-224):
+ * per problem p, the token sequences a = d_tok_a[d_off_a[p] .. d_off_a[p+1])
+ * and b (same for B) -- kernel names interned to integers -- are aligned on
+ * their longest common subsequence with the reference's tie rule (on a
+ * mismatch skip a's element when table[i+1][j] >= table[i][j+1]); matched
+ * positions get flag 1 in d_match_a / d_match_b (indexed like the tokens).
+ * d_tab: int32 scratch, problem p's (n+1)(m+1) table at d_tab_off[p]. */
+int dw_lcs_matched(const int32_t *d_tok_a, const int64_t *d_off_a, const int32_t *d_tok_b, const int64_t *d_off_b,
+                   int64_t nprob, const int64_t *d_tab_off, int32_t *d_tab, uint8_t *d_match_a, uint8_t *d_match_b,
+                   dw_stream_t stream);
+
 const char *dw_version(void);
 const char *dw_error_string(int code);
 /* number of kernel launches issued by this library on the calling thread

@@ -50,7 +50,7 @@ EXPORTED = (
     "dw_exchange_count", "dw_exchange_scatter", "dw_exchange_signal", "dw_exchange_wait",
     "dw_ipc_handle", "dw_ipc_open", "dw_ipc_close",
     "dw_tensor_norms", "dw_tensor_prefilter", "dw_unfold_smem_doubles", "dw_unfold_spectra", "dw_spectra_embed",
-    "dw_version", "dw_error_string", "dw_launch_count", "dw_kernel_timing", "dw_kernel_time_ms",
+    "dw_lcs_matched", "dw_version", "dw_error_string", "dw_launch_count", "dw_kernel_timing", "dw_kernel_time_ms",
     "dw_kernel_timed_count",
 )
 
@@ -185,6 +185,7 @@ def lib():
         L.dw_fx_sum_workspace_size.argtypes = [c_i64]
         L.dw_fx_sum.argtypes = [c_vp, c_i64, c_vp, c_vp, ctypes.c_size_t, c_vp]
         L.dw_step_value_at.argtypes = [ctypes.POINTER(Signal), c_vp, c_i64, c_vp, c_vp]
+        L.dw_lcs_matched.argtypes = [c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]
         L.dw_version.restype = ctypes.c_char_p
         L.dw_error_string.restype = ctypes.c_char_p
         L.dw_error_string.argtypes = [ctypes.c_int]

@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libdwb200.so"
-SOURCES = ["capi.cu", "attribute.cu", "split.cu", "replay.cu", "diff.cu", "pack.cu", "ingest.cu", "tensor.cu", "exchange.cu"]
+SOURCES = ["capi.cu", "attribute.cu", "split.cu", "replay.cu", "diff.cu", "pack.cu", "ingest.cu", "tensor.cu", "exchange.cu", "align.cu"]
 HEADERS = ["dw_common.cuh"]
 
 NVCC_FLAGS = [

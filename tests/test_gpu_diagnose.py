@@ -130,3 +130,20 @@ def test_kernelless_waste_finding_raises_like_reference():
     with pytest.raises(dg.DiagnoseError):
         dg.classify_pairs(TraceColumns.from_trace(ta), TraceColumns.from_trace(tb), ["A"], np.array([0]),
                           np.array([0]))
+
+
+def test_batched_lcs_alignment_matches_host_rule():
+    """csrc/align.cu (one launch for many findings) == the reference's
+    table-walk tie rule (diagnose.py:203-224, restated by _lcs_matched) on
+    random kernel-name sequences, empty ones included."""
+    import random
+    from paper_2512_08365_b200.diagnose import _lcs_matched, lcs_matched_batch
+    rng = random.Random(5)
+    probs = []
+    for _ in range(400):
+        na, nb = rng.randint(0, 30), rng.randint(0, 30)
+        alpha = [f"k{i}" for i in range(rng.randint(1, 6))]
+        probs.append(([rng.choice(alpha) for _ in range(na)], [rng.choice(alpha) for _ in range(nb)]))
+    got = lcs_matched_batch(probs)
+    for (a, b), g in zip(probs, got):
+        assert g == _lcs_matched(a, b)
