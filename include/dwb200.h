@@ -81,7 +81,9 @@ typedef struct CUstream_st *dw_stream_t; /* == cudaStream_t */
 /* Tiling of the attribution kernel.  Whole tiles enter long-interval sums as
  * exact fixed-point tile sums (int128 sums of the rounded pieces), so any
  * grouping gives the oracle's value (oracle/dw_oracle.c fx_range). */
+#ifndef DW_TILE
 #define DW_TILE 1024
+#endif
 #ifndef DW_TILE_THREADS
 #define DW_TILE_THREADS 192
 #endif
