@@ -205,7 +205,10 @@ __global__ void partition_kernel(AttrParams p, PartIndex idx) {
 // NCW consumer warps wait on `full`, integrate, and release the stage through
 // `empty`.  No consumer ever waits on a global load in the common case.
 constexpr int NCW = ATTR_WARPS;              // warps per consumer group
-constexpr int NPROD = 1;                     // producer warps
+#ifndef DW_NPROD
+#define DW_NPROD 1
+#endif
+constexpr int NPROD = DW_NPROD;              // producer warps
 constexpr int KTHREADS = GROUPS * ATTR_THREADS + 32 * NPROD;
 #ifndef DW_IV_POOL
 #define DW_IV_POOL 384
