@@ -522,35 +522,55 @@ def run_ours(args, rank: int, world: int, local: int):
 
 
 def run_window(args, rank: int, world: int, local: int):
-    """One trace pair time-window-sharded over the ranks:
-    each rank attributes its window of both traces, crossing intervals and
-    totals combine exactly, and the signature join runs hash-partitioned
-    after one all-to-all.  Strong scaling: the work per step is one pair."""
+    """Trace pairs time-window-sharded over the ranks: each
+    rank attributes its window of both traces, crossing intervals and totals
+    combine exactly, and the signature join runs hash-partitioned after one
+    exchange.  Strong scaling: the work per step is fixed.  C4: one pair;
+    C5: the corpus's pairs (as many as one GPU holds resident), each sharded
+    over every rank."""
     import torch
     import torch.distributed as dist
+    from dataclasses import replace
 
     from paper_2512_08365_b200 import _native, shard, synth
 
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     _native.lib()
-    cfg = synth.CONFIGS[args.config]
-    ca, cb = synth.make_pair(cfg)
     kind = "linear" if args.method == "samples" else "step"
     comm = shard.Comm() if world > 1 else shard.LocalComm()
-    win_a = shard.plan(ca.n_power, world, kind)[rank]
-    win_b = shard.plan(cb.n_power, world, kind)[rank]
-    ia, ib = shard.rank_inputs(ca, kind, win_a), shard.rank_inputs(cb, kind, win_b)
-    for c in (ca, cb):
-        for n in ("op_sig", "op_start", "op_end"):
-            c.device(n)
+    cfg = synth.CONFIGS[args.config]
+    n_pairs = args.pairs if args.config == "C5" else 1
+    pairs = []
+    for i in range(n_pairs):
+        if pairs:
+            free, _ = torch.cuda.mem_get_info(dev)
+            per = torch.cuda.memory_allocated(dev) / len(pairs)
+            if free < 16e9 + 1.0e9 * (len(pairs) + 1) + 1.1 * per:
+                break
+        ca, cb = synth.make_pair(replace(cfg, seed=cfg.seed + i) if n_pairs > 1 else cfg, dev)
+        ia = shard.rank_inputs(ca, kind, shard.plan(ca.n_power, world, kind)[rank])
+        ib = shard.rank_inputs(cb, kind, shard.plan(cb.n_power, world, kind)[rank])
+        for c in (ca, cb):
+            for n in ("op_sig", "op_start", "op_end"):
+                c.device(n)
+        pairs.append((ca, cb, ia, ib))
+    n_res = torch.tensor([len(pairs)], device=dev if args.dist_backend == "nccl" else "cpu")
+    if world > 1:  # every rank shards the same pairs
+        dist.all_reduce(n_res, op=dist.ReduceOp.MIN)
+    pairs = pairs[: int(n_res.item())]
     torch.cuda.synchronize()
-    intervals = ca.n_ops + ca.n_kernels + cb.n_ops + cb.n_kernels
+    intervals = sum(a.n_ops + a.n_kernels + b.n_ops + b.n_kernels for a, b, _, _ in pairs)
+    samples = sum(a.n_power + b.n_power for a, b, _, _ in pairs)
 
     def step():
-        la = shard.sharded_ledger(ca, kind, comm, inputs=ia)
-        lb = shard.sharded_ledger(cb, kind, comm, inputs=ib)
-        return shard.sharded_join(shard.shard_ops(ca, la, True), shard.shard_ops(cb, lb, False), ca.n_ops, comm,
-                                  0.10, args.k)
+        out = []
+        for ca, cb, ia, ib in pairs:
+            la = shard.sharded_ledger(ca, kind, comm, inputs=ia)
+            lb = shard.sharded_ledger(cb, kind, comm, inputs=ib)
+            out.append(shard.sharded_join(shard.shard_ops(ca, la, True), shard.shard_ops(cb, lb, False), ca.n_ops,
+                                          comm, 0.10, args.k))
+        return out
 
     for _ in range(args.warmup):
         res = step()
@@ -574,17 +594,19 @@ def run_window(args, rank: int, world: int, local: int):
     ms_max = float(t.item())
     if rank != 0:
         return
+    what = (f"ONE trace pair, {cfg.n_ops} ops and {pairs[0][0].n_power} power samples per trace" if n_pairs == 1
+            else f"{len(pairs)} of the corpus's {n_pairs} trace pairs ({cfg.n_ops} ops and {cfg.n_samples} power "
+                 f"samples per trace), each")
     line = {
         "metric": METRIC, "value": intervals / (ms_max / 1e3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config}: ONE trace pair, {cfg.n_ops} ops and {ca.n_power} power samples "
-                               f"per trace, time-window sharded", "method": args.method,
-                   "intervals_per_pair": intervals, "findings": res.P, "top_k": args.k,
-                   "parallelism": f"time-window x{world} ({args.dist_backend})"},
-        "samples_per_s": (ca.n_power + cb.n_power) / (ms_max / 1e3),
+        "config": {"workload": f"{args.config}: {what} time-window sharded", "method": args.method,
+                   "pairs": len(pairs), "intervals_per_step": intervals, "findings": sum(r.P for r in res),
+                   "top_k": args.k, "parallelism": f"time-window x{world} ({args.dist_backend})"},
+        "samples_per_s": samples / (ms_max / 1e3),
         "gpu_launches": launches, "clocks": clocks.summary(),
-        "n_waste": res.n_waste, "wasted_joules": res.wasted_joules,
+        "n_waste": sum(r.n_waste for r in res), "wasted_joules": sum(r.wasted_joules for r in res),
     }
     print(json.dumps(line), flush=True)
 
