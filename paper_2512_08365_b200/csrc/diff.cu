@@ -522,12 +522,18 @@ __device__ __forceinline__ double div_or_same(double e, const double *work, int6
 // window's partners out in shared memory, then walks the window's A ops in
 // order -- coalesced match_a writes, coalesced A-side reads, the verdict, and
 // coalesced finding columns -- with only the B-side reads random.
+#ifndef DW_WF_MINB
+#define DW_WF_MINB 1
+#endif
+#ifndef DW_SUB_MINB
+#define DW_SUB_MINB 4
+#endif
 constexpr int WIN_BSH = 14;
 constexpr int WIN_OPS = 1 << WIN_BSH;
 constexpr int SUB_CHUNK = 4096;  // divides 1 << PAIR_BSH: a chunk never straddles buckets
 constexpr int WF_THREADS = 512;
 
-__global__ void __launch_bounds__(256) join_pair_sub_kernel(const uint2 *stage, int64_t na, unsigned int *cursor2,
+__global__ void __launch_bounds__(256, DW_SUB_MINB) join_pair_sub_kernel(const uint2 *stage, int64_t na, unsigned int *cursor2,
                                                             uint2 *stage2) {
     constexpr int NSUB = 1 << (PAIR_BSH - WIN_BSH);
     __shared__ int hist[NSUB];
@@ -558,7 +564,10 @@ __global__ void __launch_bounds__(256) join_pair_sub_kernel(const uint2 *stage, 
     }
 }
 
-__global__ void __launch_bounds__(WF_THREADS) join_window_findings_kernel(
+// (one 512-thread CTA per SM: capping it at 64 registers for two CTAs spills
+// and measured slower, 1.96 -> 2.12 ms; join_pair_sub at 4 CTAs per SM
+// instead of 3: 0.71 -> 0.49 ms)
+__global__ void __launch_bounds__(WF_THREADS, DW_WF_MINB) join_window_findings_kernel(
     const uint2 *stage2, int64_t na, int32_t *match_a, JoinSideDev A, JoinSideDev B, double threshold, FindCols o,
     double *epw_a, double *epw_b, unsigned long long *n_matched) {
     extern __shared__ int32_t jw[];  // [WIN_OPS]
@@ -1944,6 +1953,7 @@ static int join_impl(const dw_join_side_t *a, const dw_join_side_t *b, int64_t m
         const int64_t nwin = (na + WIN_OPS - 1) / WIN_OPS;
         const size_t smem = 4 * (size_t)WIN_OPS;
         cudaFuncSetAttribute(join_window_findings_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(join_window_findings_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         join_window_findings_kernel<<<(unsigned)nwin, WF_THREADS, smem, s>>>(stage2, na, d_match_a, A, B, threshold,
                                                                             o, d_epw_a, d_epw_b, counters + 1);
         count_launch();
