@@ -523,7 +523,7 @@ __device__ __forceinline__ double div_or_same(double e, const double *work, int6
 // order -- coalesced match_a writes, coalesced A-side reads, the verdict, and
 // coalesced finding columns -- with only the B-side reads random.
 #ifndef DW_WF_MINB
-#define DW_WF_MINB 1
+#define DW_WF_MINB 2
 #endif
 #ifndef DW_SUB_MINB
 #define DW_SUB_MINB 4
@@ -564,8 +564,10 @@ __global__ void __launch_bounds__(256, DW_SUB_MINB) join_pair_sub_kernel(const u
     }
 }
 
-// (one 512-thread CTA per SM: capping it at 64 registers for two CTAs spills
-// and measured slower, 1.96 -> 2.12 ms; join_pair_sub at 4 CTAs per SM
+// (join_window_findings: two 512-thread CTAs per SM with one finding per
+// thread per step -- the kernel waits on the B-side loads, so warps in
+// flight beat unrolled independent loads: U=4 at 1 CTA/SM 1.96 ms, U=2 at 2
+// 1.89, U=1 at 2 1.82 ms; U=1 at 3 2.15.  join_pair_sub at 4 CTAs per SM
 // instead of 3: 0.71 -> 0.49 ms)
 __global__ void __launch_bounds__(WF_THREADS, DW_WF_MINB) join_window_findings_kernel(
     const uint2 *stage2, int64_t na, int32_t *match_a, JoinSideDev A, JoinSideDev B, double threshold, FindCols o,
@@ -578,7 +580,10 @@ __global__ void __launch_bounds__(WF_THREADS, DW_WF_MINB) join_window_findings_k
         jw[e.x - (uint32_t)i0] = (int32_t)e.y;
     }
     __syncthreads();
-    constexpr int U = 4;
+#ifndef DW_WF_U
+#define DW_WF_U 1
+#endif
+    constexpr int U = DW_WF_U;
     unsigned cnt = 0;
     for (int q0 = threadIdx.x; q0 < n; q0 += WF_THREADS * U) {
         int32_t j[U];
