@@ -671,8 +671,23 @@ constexpr int JB_SPB_MAX = 2048;        // table slots per bucket: cap <= JB_NB 
 constexpr int JB_THREADS = 512;         // 16 warps
 constexpr int JB_WARPS = JB_THREADS / 32;
 constexpr int JB_DIG = 64;              // radix of the two partition passes
-constexpr int JB_T1 = 8192;             // ops per tile, hash + pass 1
-constexpr int JB_T2 = 8192;             // ops per tile, pass 2 (16 per thread; JB_T1 == JB_T2)
+#ifndef DW_JB_T
+#define DW_JB_T 4096
+#endif
+#ifndef DW_JB_PT
+#define DW_JB_PT 256
+#endif
+#ifndef DW_JB_PMINB
+#define DW_JB_PMINB 3
+#endif
+constexpr int JB_T1 = DW_JB_T;          // ops per tile, hash + pass 1
+constexpr int JB_T2 = DW_JB_T;          // ops per tile, pass 2 (JB_T1 == JB_T2)
+constexpr int JB_PT = DW_JB_PT;         // threads of a partition pass (16 ops per thread)
+// measured (C4 passes 1 + 2): 8192-op tiles x 512 threads at 2 CTAs/SM 2.21 ms;
+// 4096 x 256 at 4 CTAs 1.93, at 3 (85 registers) 1.70, at 2 2.08; 2048 x 128
+// at 8 CTAs 1.84 (+ larger count matrices); 8192 x 1024 2.61
+constexpr int JB_PW = JB_PT / 32;
+static_assert(JB_T2 % (2 * JB_PT) == 0, "partition pass: an even number of ops per lane");
 constexpr int JB_SEG = 256;             // tile segments of a matrix scan
 
 struct JbSide {
@@ -840,11 +855,11 @@ __device__ __forceinline__ unsigned jb_peers(uint32_t key, bool valid) {
 // (coalesced), at the tile's offset of each digit from the scanned count
 // matrix.
 template <int PASS>
-__global__ void __launch_bounds__(JB_THREADS, 2) jb_pass_kernel(JbParams q) {
-    constexpr int STEPS = JB_T2 / JB_THREADS;  // ops per lane
+__global__ void __launch_bounds__(JB_PT, DW_JB_PMINB) jb_pass_kernel(JbParams q) {
+    constexpr int STEPS = JB_T2 / JB_PT;  // ops per lane
     extern __shared__ __align__(16) unsigned char jb_smem[];
     unsigned long long *lay = reinterpret_cast<unsigned long long *>(jb_smem);  // [JB_T2]
-    __shared__ uint32_t cnt[JB_WARPS][JB_DIG];
+    __shared__ uint32_t cnt[JB_PW][JB_DIG];
     __shared__ uint32_t lstart[JB_DIG], gstart[JB_DIG], half0;
     int64_t t;
     const int side = jb_side_of(q.nt2, t);
@@ -892,7 +907,7 @@ __global__ void __launch_bounds__(JB_THREADS, 2) jb_pass_kernel(JbParams q) {
         const int d = threadIdx.x;
         uint32_t tot = 0;
 #pragma unroll
-        for (int w = 0; w < JB_WARPS; ++w) tot += cnt[w][d];
+        for (int w = 0; w < JB_PW; ++w) tot += cnt[w][d];
         uint32_t x = tot;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -909,7 +924,7 @@ __global__ void __launch_bounds__(JB_THREADS, 2) jb_pass_kernel(JbParams q) {
         uint32_t run = lstart[d] + (d >= 32 ? half0 : 0);
         lstart[d] = run;
 #pragma unroll
-        for (int w = 0; w < JB_WARPS; ++w) {
+        for (int w = 0; w < JB_PW; ++w) {
             const uint32_t c = cnt[w][d];
             cnt[w][d] = run;
             run += c;
@@ -925,7 +940,7 @@ __global__ void __launch_bounds__(JB_THREADS, 2) jb_pass_kernel(JbParams q) {
     __syncthreads();
     unsigned long long *dst = PASS == 1 ? S.tmp : S.scat;
 #pragma unroll 4
-    for (int x = threadIdx.x; x < nt; x += JB_THREADS) {  // runs per digit: consecutive threads, consecutive positions
+    for (int x = threadIdx.x; x < nt; x += JB_PT) {  // runs per digit: consecutive threads, consecutive positions
         const unsigned long long v = lay[x];
         const uint32_t d = (uint32_t)(v >> dshift) & (JB_DIG - 1);
         dst[gstart[d] + (x - lstart[d])] = v;
@@ -1504,12 +1519,12 @@ static int jb_pairing(const dw_join_side_t *a, const dw_join_side_t *b, const Jo
         jb_colsum_kernel<<<sg, 256, 0, s>>>(q, 1);
         jb_base_kernel<<<2, JB_DIG, 0, s>>>(q);
         jb_apply_kernel<<<sg, 256, 0, s>>>(q, 1);
-        jb_pass_kernel<1><<<tiles1, JB_THREADS, 8 * JB_T2, s>>>(q);
+        jb_pass_kernel<1><<<tiles1, JB_PT, 8 * JB_T2, s>>>(q);
         jb_hist2_kernel<<<tiles2, 256, 0, s>>>(q);
         jb_colsum_kernel<<<sg, 256, 0, s>>>(q, 2);
         jb_base_kernel<<<2, JB_DIG, 0, s>>>(q);
         jb_apply_kernel<<<sg, 256, 0, s>>>(q, 2);
-        jb_pass_kernel<2><<<tiles2, JB_THREADS, 8 * JB_T2, s>>>(q);
+        jb_pass_kernel<2><<<tiles2, JB_PT, 8 * JB_T2, s>>>(q);
         count_launch(10);
     }
     jb_bounds_kernel<<<dim3((JB_NBB + 1 + 255) / 256, 2), 256, 0, s>>>(q);
