@@ -669,6 +669,11 @@ constexpr int JB_NB = 2048;             // signature buckets (+1 for the all-one
 constexpr int JB_NBB = JB_NB + 1;       // bucket ids < 2^12: two 6-bit digits
 constexpr int JB_SPB_MAX = 2048;        // table slots per bucket: cap <= JB_NB * JB_SPB_MAX
 constexpr int JB_THREADS = 512;         // 16 warps
+#ifndef DW_JB_BT
+#define DW_JB_BT 512
+#endif
+constexpr int JB_BT = DW_JB_BT;         // threads of the bucket kernel
+constexpr int JB_BW = JB_BT / 32;
 constexpr int JB_WARPS = JB_THREADS / 32;
 constexpr int JB_DIG = 64;              // radix of the two partition passes
 #ifndef DW_JB_T
@@ -1002,16 +1007,16 @@ struct JbBucketOut {
     uint32_t *bonly_bits;        // [ceil(nb / 32)]
 };
 
-// dynamic smem: cw[JB_WARPS][spb] (u32) + totA, totB, startB [spb] + sbh[PAIR_MAXB]
-__global__ void __launch_bounds__(JB_THREADS) jb_bucket_kernel(JbParams q, JbBucketOut o) {
+// dynamic smem: cw[JB_BW][spb] (u32) + totA, totB, startB [spb] + sbh[PAIR_MAXB]
+__global__ void __launch_bounds__(JB_BT) jb_bucket_kernel(JbParams q, JbBucketOut o) {
     extern __shared__ __align__(16) unsigned char jb_smem[];
     const int spb = 1 << q.shift;
     uint32_t *cw = reinterpret_cast<uint32_t *>(jb_smem);
-    uint32_t *totA = cw + JB_WARPS * spb;
+    uint32_t *totA = cw + JB_BW * spb;
     uint32_t *totB = totA + spb;
     uint32_t *startB = totB + spb;
     unsigned int *sbh = startB + spb;
-    __shared__ uint32_t wsum[JB_WARPS];
+    __shared__ uint32_t wsum[JB_BW];
     const int b = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const JbSide &A = q.s[0], &B = q.s[1];
@@ -1021,15 +1026,15 @@ __global__ void __launch_bounds__(JB_THREADS) jb_bucket_kernel(JbParams q, JbBuc
     const uint32_t smask = (uint32_t)spb - 1u;
     // this warp's contiguous segment of [lo, hi)
     auto seg = [&](uint32_t lo, uint32_t hi, uint32_t &s0, uint32_t &s1) {
-        const uint32_t per = (hi - lo + JB_WARPS - 1) / JB_WARPS;
+        const uint32_t per = (hi - lo + JB_BW - 1) / JB_BW;
         s0 = min(lo + warp * per, hi);
         s1 = min(s0 + per, hi);
     };
     // per-warp counts of the slots over [lo, hi) -> cross-warp exclusive bases, totals
     auto count_pass = [&](const unsigned long long *src, uint32_t lo, uint32_t hi, uint32_t *tot, bool stage_hist) {
-        for (int k = threadIdx.x; k < JB_WARPS * spb; k += JB_THREADS) cw[k] = 0;
+        for (int k = threadIdx.x; k < JB_BW * spb; k += JB_BT) cw[k] = 0;
         if (stage_hist)
-            for (int k = threadIdx.x; k < PAIR_MAXB; k += JB_THREADS) sbh[k] = 0;
+            for (int k = threadIdx.x; k < PAIR_MAXB; k += JB_BT) sbh[k] = 0;
         __syncthreads();
         uint32_t s0, s1;
         seg(lo, hi, s0, s1);
@@ -1040,10 +1045,10 @@ __global__ void __launch_bounds__(JB_THREADS) jb_bucket_kernel(JbParams q, JbBuc
             if (stage_hist) atomicAdd(&sbh[(uint32_t)e >> PAIR_BSH], 1u);
         });
         __syncthreads();
-        for (int s = threadIdx.x; s < nslot; s += JB_THREADS) {
+        for (int s = threadIdx.x; s < nslot; s += JB_BT) {
             uint32_t run = 0;
 #pragma unroll
-            for (int w = 0; w < JB_WARPS; ++w) {
+            for (int w = 0; w < JB_BW; ++w) {
                 const uint32_t c = cw[w * spb + s];
                 cw[w * spb + s] = run;
                 run += c;
@@ -1056,7 +1061,7 @@ __global__ void __launch_bounds__(JB_THREADS) jb_bucket_kernel(JbParams q, JbBuc
     count_pass(B.scat, b0, b1, totB, false);
     {  // startB = exclusive scan of totB over the slots
         uint32_t carry = 0;
-        for (int c = 0; c < nslot; c += JB_THREADS) {
+        for (int c = 0; c < nslot; c += JB_BT) {
             const int s = c + threadIdx.x;
             const uint32_t v = s < nslot ? totB[s] : 0;
             uint32_t x = v;
@@ -1069,7 +1074,7 @@ __global__ void __launch_bounds__(JB_THREADS) jb_bucket_kernel(JbParams q, JbBuc
             __syncthreads();
             uint32_t wb = 0, all = 0;
 #pragma unroll
-            for (int w = 0; w < JB_WARPS; ++w) {
+            for (int w = 0; w < JB_BW; ++w) {
                 const uint32_t ws = wsum[w];
                 if (w < warp) wb += ws;
                 all += ws;
@@ -1097,9 +1102,9 @@ __global__ void __launch_bounds__(JB_THREADS) jb_bucket_kernel(JbParams q, JbBuc
     __syncthreads();  // bsorted of this bucket complete (block-visible)
     // ---- A: occurrences by slot, paired with B's t-th occurrence
     count_pass(A.scat, a0, a1, totA, true);
-    for (int k = threadIdx.x; k < PAIR_MAXB; k += JB_THREADS)  // reserve this bucket's A-stage ranges
+    for (int k = threadIdx.x; k < PAIR_MAXB; k += JB_BT)  // reserve this bucket's A-stage ranges
         if (sbh[k]) sbh[k] = atomicAdd(o.cursor + k, sbh[k]);
-    for (int s = threadIdx.x; s < nslot; s += JB_THREADS) {  // B occurrences beyond A's count: B-only
+    for (int s = threadIdx.x; s < nslot; s += JB_BT) {  // B occurrences beyond A's count: B-only
         for (uint32_t t = totA[s]; t < totB[s]; ++t) {
             const uint32_t j = o.bsorted[b0 + startB[s] + t];
             atomicOr(o.bonly_bits + (j >> 5), 1u << (j & 31));
@@ -1538,9 +1543,9 @@ static int jb_pairing(const dw_join_side_t *a, const dw_join_side_t *b, const Jo
     cudaMemsetAsync(o.cursor, 0, 4 * PAIR_MAXB, s);
     cudaMemsetAsync(o.bonly_bits, 0, 4 * L.nw, s);
     const int spb = 1 << q.shift;
-    const size_t smem_b = 4 * ((size_t)(JB_WARPS + 3) * spb + PAIR_MAXB);
+    const size_t smem_b = 4 * ((size_t)(JB_BW + 3) * spb + PAIR_MAXB);
     cudaFuncSetAttribute(jb_bucket_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_b);
-    jb_bucket_kernel<<<JB_NBB, JB_THREADS, smem_b, s>>>(q, o);
+    jb_bucket_kernel<<<JB_NBB, JB_BT, smem_b, s>>>(q, o);
     count_launch();
     trace_mark(s, "join:bucket");
     if (na) {
