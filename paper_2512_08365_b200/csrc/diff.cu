@@ -161,7 +161,7 @@ struct RankParams {
     int64_t n_a;
     int64_t P, k;
     unsigned int *hist;        // [HIST_BINS]
-    unsigned long long *sel;   // [2]: bin, count strictly above the bin
+    unsigned long long *sel;   // [3]: bin, count strictly above the bin, count in the bin
     unsigned long long *cand_n;
     uint64_t *cand_hi, *cand_lo;
     int64_t *cand_idx;
@@ -213,6 +213,7 @@ __global__ void rank_select_kernel(RankParams r, int64_t need) {
     }
     r.sel[0] = (unsigned long long)b;
     r.sel[1] = (unsigned long long)above;
+    r.sel[2] = (unsigned long long)r.hist[b];  // keys in the selected bin (one read-back for all three)
 }
 
 // copy every key >= (thr_hi, thr_lo) into the candidate buffer
@@ -1341,11 +1342,10 @@ static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, const 
         rank_select_kernel<<<1, 32, 0, s>>>(r, need);
         count_launch(2);
         trace_mark(s, "rank:digit");
-        unsigned long long sel[2];
+        unsigned long long sel[3];
         cudaMemcpyAsync(sel, r.sel, sizeof(sel), cudaMemcpyDeviceToHost, s);
         if (cudaStreamSynchronize(s) != cudaSuccess) return DW_E_CUDA;
-        unsigned int in_bin = 0;
-        cudaMemcpy(&in_bin, r.hist + sel[0], 4, cudaMemcpyDeviceToHost);
+        const unsigned long long in_bin = sel[2];
         const uint64_t dig = sel[0];
         if (pos >= 64) {
             thr_hi = phi | (dig << (pos - 64));
