@@ -13,7 +13,7 @@ torch.cuda.synchronize()
 for it in range(iters):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter(); e0.record()
-    cols = FindingColumns.KEYS if "keys" in sys.argv else None
+    cols = FindingColumns.KEYS if "keys" in sys.argv else (FindingColumns.DELTAS if "deltas" in sys.argv else None)
     jd = join_diff(a, b, la, lb, 0.10, 100, full_columns=False, epw=False, columns=cols)
     top = jd.top_findings(a, b)
     e1.record(); torch.cuda.synchronize(); t1 = time.perf_counter()
