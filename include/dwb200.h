@@ -351,6 +351,14 @@ size_t dw_rank_segmented_workspace_size(int32_t nseg, int64_t k);
 int dw_rank_segmented(const dw_rank_segment_t *segs, int32_t nseg, int64_t k, int64_t *d_order,
                       double *d_summary, void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
 
+/* The report rows of a join's top-k (d_order[k], join numbering) for the host:
+ * d_out[6][k] int64 = A op, B op (-1 when empty), latency_a, latency_b, and
+ * the joules of each side as f64 bits (0 when empty). */
+int dw_topk_rows(const int64_t *d_order, int64_t k, int64_t n_a, const int32_t *d_match_a, const int32_t *d_b_only,
+                 const double *d_joules_a, const double *d_joules_b, const int64_t *d_start_a,
+                 const int64_t *d_end_a, const int64_t *d_start_b, const int64_t *d_end_b, int64_t *d_out,
+                 dw_stream_t stream);
+
 /* Signature hash-join diff.  Operators of A and B
  * are keyed by (sig, occurrence in op order); equal keys pair up, unmatched
  * operators become one-sided findings.  Findings are numbered: A ops in order

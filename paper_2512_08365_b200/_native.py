@@ -45,7 +45,7 @@ EXPORTED = (
     "dw_set_attribute_sms", "dw_ig_nl_count", "dw_ig_nl_write", "dw_ig_classify", "dw_ig_parse_power",
     "dw_ig_parse_op", "dw_ig_parse_kernel", "dw_ig_hash", "dw_ig_id_words", "dw_ig_kernel_lists",
     "dw_fx_sum_workspace_size", "dw_fx_sum", "dw_step_value_at", "dw_detect_pairs",
-    "dw_rank_workspace_size", "dw_rank", "dw_rank_segmented_workspace_size", "dw_rank_segmented",
+    "dw_rank_workspace_size", "dw_rank", "dw_rank_segmented_workspace_size", "dw_rank_segmented", "dw_topk_rows",
     "dw_join_workspace_size", "dw_join_diff",
     "dw_exchange_count", "dw_exchange_scatter", "dw_exchange_signal", "dw_exchange_wait",
     "dw_ipc_handle", "dw_ipc_open", "dw_ipc_close",
@@ -203,6 +203,7 @@ def lib():
             L.dw_rank_workspace_size.argtypes = [c_i64, c_i64]
             L.dw_rank.argtypes = [c_i64, ctypes.POINTER(Findings), c_i64, c_vp, c_vp, c_vp,
                                   ctypes.c_size_t, c_vp]
+            L.dw_topk_rows.argtypes = [c_vp, c_i64, c_i64] + [c_vp] * 9 + [c_vp]
             L.dw_rank_segmented_workspace_size.restype = ctypes.c_size_t
             L.dw_rank_segmented_workspace_size.argtypes = [c_i32, c_i64]
             L.dw_rank_segmented.argtypes = [ctypes.POINTER(RankSegment), c_i32, c_i64, c_vp, c_vp, c_vp,

@@ -1812,6 +1812,33 @@ __global__ void __launch_bounds__(SEG_SORT_THREADS) seg_sort_kernel(const SegDes
     for (int64_t x = threadIdx.x; x < k; x += blockDim.x) order[(int64_t)s * k + x] = x < ks && x < n ? si[x] : -1;
 }
 
+
+// The top-k rows of a join for the host report, in one launch: per row r of
+// the report order, its A / B operators (join numbering: f < n_a is A op f
+// with partner match_a[f]; else the B-only op b_only[f - n_a]), their joules
+// and latencies.  out[6][k] (int64; joules as their f64 bits): ia, ib, la,
+// lb, ea, eb -- one device->host copy instead of a dozen gathers.
+__global__ void topk_rows_kernel(const int64_t *order, int64_t k, int64_t n_a, const int32_t *match_a,
+                                 const int32_t *b_only, const double *ja, const double *jb, const int64_t *sa,
+                                 const int64_t *ea, const int64_t *sb, const int64_t *eb, int64_t *out) {
+    const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r >= k) return;
+    const int64_t f = order[r];
+    int64_t ia = -1, ib = -1;
+    if (f >= 0 && f < n_a) {
+        ia = f;
+        ib = match_a[f];
+    } else if (f >= n_a) {
+        ib = b_only[f - n_a];
+    }
+    out[r] = ia;
+    out[k + r] = ib;
+    out[2 * k + r] = ia >= 0 ? ea[ia] - sa[ia] : 0;
+    out[3 * k + r] = ib >= 0 ? eb[ib] - sb[ib] : 0;
+    out[4 * k + r] = __double_as_longlong(ia >= 0 ? ja[ia] : 0.0);
+    out[5 * k + r] = __double_as_longlong(ib >= 0 ? jb[ib] : 0.0);
+}
+
 }  // namespace dw
 
 using namespace dw;
@@ -2109,6 +2136,22 @@ int dw_rank_segmented(const dw_rank_segment_t *segs, int32_t nseg, int64_t k, in
     cudaMemcpyAsync(&overflow, flags + 1, 4, cudaMemcpyDeviceToHost, s);
     if (cudaStreamSynchronize(s) != cudaSuccess) return DW_E_CUDA;
     if (overflow) return DW_E_WORKSPACE;  // massive ties at a threshold key (cannot happen: keys are distinct)
+    DW_CHECK_LAUNCH();
+    return DW_OK;
+}
+
+
+int dw_topk_rows(const int64_t *d_order, int64_t k, int64_t n_a, const int32_t *d_match_a, const int32_t *d_b_only,
+                 const double *d_joules_a, const double *d_joules_b, const int64_t *d_start_a,
+                 const int64_t *d_end_a, const int64_t *d_start_b, const int64_t *d_end_b, int64_t *d_out,
+                 dw_stream_t stream) {
+    if (k < 0 || n_a < 0 || (k && (!d_order || !d_out))) return DW_E_ARG;
+    if (k) {
+        topk_rows_kernel<<<(unsigned)ceil_div(k, 128), 128, 0, (cudaStream_t)stream>>>(
+            d_order, k, n_a, d_match_a, d_b_only, d_joules_a, d_joules_b, d_start_a, d_end_a, d_start_b, d_end_b,
+            d_out);
+        count_launch();
+    }
     DW_CHECK_LAUNCH();
     return DW_OK;
 }

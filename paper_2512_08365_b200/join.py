@@ -145,6 +145,25 @@ class JoinDiff:
         ib = torch.where(is_a, ma, bo)
         return ia, ib
 
+    def _top_lean(self, cols_a, cols_b, classify, trace_a, trace_b, idx) -> list[WasteFinding]:
+        """top_findings for lean joins (no per-finding verdict columns): the
+        k rows' operators, joules and latencies in one device gather
+        (dw_topk_rows) and one copy; verdicts on the host with the device's
+        rule (judge)."""
+        k = int(idx.numel())
+        dev = idx.device
+        out = torch.empty((6, max(k, 1)), dtype=torch.int64, device=dev)
+        p = _native.ptr
+        o = idx.contiguous()
+        _native.check(_native.lib().dw_topk_rows(
+            p(o), k, self.n_a, p(self.match_a), p(self.b_only), p(self.ja), p(self.jb),
+            p(cols_a.device("op_start")), p(cols_a.device("op_end")), p(cols_b.device("op_start")),
+            p(cols_b.device("op_end")), p(out), _native.stream_handle()), "dw_topk_rows")
+        h = out[:, :k].cpu().numpy()
+        ia, ib, la, lb = h[0], h[1], h[2], h[3]
+        ea, eb = h[4].view(np.float64), h[5].view(np.float64)
+        return self._rows(cols_a, cols_b, classify, trace_a, trace_b, ia, ib, ea, eb, la, lb, None)
+
     def top_findings(self, cols_a: TraceColumns, cols_b: TraceColumns, classify: bool = True,
                      trace_a=None, trace_b=None, idx: Optional[torch.Tensor] = None) -> list[WasteFinding]:
         """Materialise the top-k findings (report order) as reference-style
@@ -154,6 +173,8 @@ class JoinDiff:
         objects, when given, enable the program-model probe)."""
         idx = self.order if idx is None else idx
         c = self.columns
+        if c.ratio is None and c.energy_a is None and c.latency_a is None and self.ja is not None:
+            return self._top_lean(cols_a, cols_b, classify, trace_a, trace_b, idx)
         ia_d, ib_d = self.pair_of(idx)
         has_a, has_b = ia_d >= 0, ib_d >= 0
         ia_c, ib_c = ia_d.clamp(min=0), ib_d.clamp(min=0)
@@ -183,16 +204,20 @@ class JoinDiff:
         ea, eb = fcols[0], fcols[1]
         la, lb = icols[0], icols[1]
         ia, ib = icols[2], icols[3]
-        if keys_only:  # the k rows' verdicts on the host, as the device computed them for all
+        h = None if keys_only else {"ratio": fcols[2], "wasted": fcols[3], "verdict": icols[4],
+                                    "side": icols[5], "informational": icols[6]}
+        return self._rows(cols_a, cols_b, classify, trace_a, trace_b, ia, ib, ea, eb, la, lb, h)
+
+    def _rows(self, cols_a, cols_b, classify, trace_a, trace_b, ia, ib, ea, eb, la, lb, h) -> list[WasteFinding]:
+        """WasteFinding rows from the k rows' columns; ``h`` None: the verdict
+        columns derived on the host with the device's rule (judge)."""
+        if h is None:  # the k rows' verdicts on the host, as the device computed them for all
             rows = [judge(float(ea[r]), float(eb[r]), int(la[r]), int(lb[r]), 0.0, self.threshold)
                     for r in range(len(ia))]
             h = {"ratio": np.array([x[0] for x in rows]), "wasted": np.array([x[1] for x in rows]),
                  "verdict": np.array([VERDICTS.index(x[2]) for x in rows], dtype=np.int64),
                  "side": np.array([SIDES.index(x[3]) for x in rows], dtype=np.int64),
                  "informational": np.array([x[4] for x in rows], dtype=bool)}
-        else:
-            h = {"ratio": fcols[2], "wasted": fcols[3], "verdict": icols[4], "side": icols[5],
-                 "informational": icols[6]}
         name = lambda ids, i, n: (ids[i] if ids is not None else synthetic_id("op", i, n))  # noqa: E731
         cats = ["unknown"] * len(ia)
         waste = np.nonzero(h["verdict"] == VERDICTS.index(VERDICT_WASTE))[0]
