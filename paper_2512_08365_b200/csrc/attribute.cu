@@ -1051,7 +1051,10 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_tiles_kernel(AttrParams
             tile_intervals<KIND>(p, sm, stage, a64, s_w, tile, (int64_t)INT64_MAX, cx, ctid);
             consumer_sync(g);
         }
-        if (ctid == 0) mbar_arrive(&sm.empty[stage]);
+        if (ctid == 0) {  // the group's stage reads / term writes before the producer's next bulk copy
+            fence_proxy_async();
+            mbar_arrive(&sm.empty[stage]);
+        }
     }
 }
 
@@ -1497,6 +1500,11 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
                 p.out[j][__ldg(p.perm[j] + d.kq + v)] = J;
             }
         }
+        // release the stage: every lane's reads (and its pass-B writes of P
+        // into the stage) ordered before the producer's next bulk copy into it
+        // -- a generic->async proxy fence per lane, warp sync, then the
+        // release-arrive the producer acquires
+        fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.empty[stage]);
     }
