@@ -150,31 +150,35 @@ def _gpu_path(raw: np.ndarray):
     k_id, k_idl, k_nm, k_nml, k_corr, k_s, k_e = i64(nk), i32(nk), i64(nk), i32(nk), i64(nk), i64(nk), i64(nk)
     _native.check(L.dw_ig_parse_kernel(p(buf), p(ends), p(lines[L_KERNEL]), nk, p(k_id), p(k_idl), p(k_nm),
                                        p(k_nml), p(k_corr), p(k_s), p(k_e), p(flags), st), "dw_ig_parse_kernel")
-    if int(flags.item()) or npw == 0:
+    if npw == 0:
         return _fallback()
-    if npw > 1 and not bool((ts[1:] > ts[:-1]).all()):
-        return _fallback()  # power samples must be strictly increasing
-    # unique ids (sorted 64-bit hashes; any equal pair goes to the Python path)
+    # the device checks, read back together (one synchronisation): parse flags,
+    # power order, unique op / kernel ids (sorted 64-bit hashes: any equal pair
+    # goes to the Python path), unique correlation ids, one owner per kernel
     def hashes(off, ln, m):
         h = torch.empty(m, dtype=torch.int64, device=dev)
         idx = torch.empty(m, dtype=torch.int32, device=dev)
         _native.check(L.dw_ig_hash(p(buf), p(off), p(ln), m, p(h), p(idx), st), "dw_ig_hash")
         hs, order = torch.sort(h ^ torch.iinfo(torch.int64).min)  # unsigned order
         return hs ^ torch.iinfo(torch.int64).min, idx[order]
-    if nop:
-        oh, _ = hashes(o_id, o_idl, nop)
-        if nop > 1 and bool((oh[1:] == oh[:-1]).any()):
-            return _fallback()
+
+    def dup(sorted_vals):
+        return (sorted_vals[1:] == sorted_vals[:-1]).any() if sorted_vals.numel() > 1 else no
+
+    no = torch.zeros((), dtype=torch.bool, device=dev)
+    oh = hashes(o_id, o_idl, nop)[0] if nop else i64(0)
     kh, kidx = hashes(k_id, k_idl, nk) if nk else (i64(0), i32(0))
-    if nk > 1 and bool((kh[1:] == kh[:-1]).any()):
-        return _fallback()
-    if nk > 1:
-        cs = torch.sort(k_corr).values
-        if bool((cs[1:] == cs[:-1]).any()):
-            return _fallback()  # correlation_id values must be unique per launch
+    o_klc64 = o_klc.to(torch.int64)
+    checks = torch.stack([flags.reshape(()).to(torch.int64),
+                          ((ts[1:] <= ts[:-1]).any() if npw > 1 else no).to(torch.int64),
+                          dup(oh).to(torch.int64), dup(kh).to(torch.int64),
+                          dup(torch.sort(k_corr).values if nk > 1 else k_corr).to(torch.int64),
+                          o_klc64.sum() if nop else torch.zeros((), dtype=torch.int64, device=dev)]).cpu().tolist()
+    bad_flags, bad_order, dup_op, dup_k, dup_corr, ne = checks
+    if bad_flags or bad_order or dup_op or dup_k or dup_corr:
+        return _fallback()  # order / duplicate ids / correlation ids: the Python path raises
     # kernels flattened in op.kernel_ids order (build_ledger's iteration order)
-    kl_base = torch.cumsum(o_klc.to(torch.int64), 0) - o_klc.to(torch.int64)
-    ne = int(o_klc.to(torch.int64).sum().item()) if nop else 0
+    kl_base = torch.cumsum(o_klc64, 0) - o_klc64
     if ne != nk:
         return _fallback()  # some kernel is not launched by exactly one operator
     fk_s, fk_e, fk_op, fk_k = i64(ne), i64(ne), i32(ne), i64(ne)
@@ -182,15 +186,18 @@ def _gpu_path(raw: np.ndarray):
     _native.check(L.dw_ig_kernel_lists(p(buf), nop, p(o_klf), p(o_klc), p(kl_base), p(o_s), p(o_e), p(kh),
                                        p(kidx), nk, p(k_id), p(k_idl), p(k_s), p(k_e), p(fk_s), p(fk_e), p(fk_op),
                                        p(fk_k), p(owner), p(flags), st), "dw_ig_kernel_lists")
-    if int(flags.item()) or (nk and not bool((owner[:nk] == 1).all())):
-        return _fallback()
     # Trace.span_us (trace_model.py:307-314): every timestamp of the trace
     parts = [ts.max()]
     if nop:
         parts += [o_e.max(), o_s.max()]
     if nk:
         parts += [k_e.max(), k_s.max()]
-    trace_end = int(torch.stack(parts).max().item())
+    tail = torch.stack([flags.reshape(()).to(torch.int64),
+                        ((owner[:nk] != 1).any() if nk else no).to(torch.int64),
+                        torch.stack(parts).max()]).cpu().tolist()
+    if tail[0] or tail[1]:
+        return _fallback()
+    trace_end = int(tail[2])
     h = lambda t: t.cpu().numpy()  # noqa: E731
     k_id_h, k_idl_h, fk_k_h = h(k_id), h(k_idl), h(fk_k)
     cols = TraceColumns(ts=ts, watts=watts, trace_end=trace_end, op_start=o_s, op_end=o_e, k_start=fk_s,
