@@ -395,15 +395,45 @@ def run_ours(args, rank: int, world: int, local: int):
         # local rank's copy (all local ranks share it).
         import psutil
         from paper_2512_08365_b200.columns import PackedColumns, pack
-        packed = [pack(c) for c in (ca, cb)]
-        need = sum(pc.host_bytes for pc in packed)
+        try:
+            packed = [pack(c) for c in (ca, cb)]
+            need = sum(pc.host_bytes for pc in packed)
+        except ValueError as exc:  # e.g. overlapping streams (C3): kernel starts not sorted
+            packed, pack_refusal = None, str(exc)
+            need = sum(getattr(c, n).numel() * getattr(c, n).element_size() for c in (ca, cb)
+                       for n in TraceColumns.HOT + ("k_op",) if getattr(c, n, None) is not None)
         local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
         avail = psutil.virtual_memory().available
         if need * local_world > 0.75 * avail:
             e2e_skip = (f"host memory: {local_world} ranks x {need / 1e9:.1f} GB pinned > 75% of "
                         f"{avail / 1e9:.0f} GB available")
             del packed
-    if not args.no_e2e and e2e_skip is None:
+    if not args.no_e2e and e2e_skip is None and packed is None:
+        # the trace does not pack: pinned unpacked columns
+        def pin(t):
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t)
+            return h
+        pinned = []
+        for c in (ca, cb):
+            hc = TraceColumns(ts=pin(c.device("ts")), watts=pin(c.device("watts")), trace_end=c.trace_end,
+                              op_start=pin(c.device("op_start")), op_end=pin(c.device("op_end")),
+                              k_start=pin(c.device("k_start")), k_end=pin(c.device("k_end")),
+                              op_sig=pin(c.device("op_sig")), ops_sorted=c.ops_sorted,
+                              kernels_sorted=c.kernels_sorted,
+                              k_op=pin(c.device("k_op")) if c.k_op is not None else None)
+            hc._dev["first_last"] = c._first_last_ts()
+            hc.host_bytes = sum(getattr(hc, n).numel() * getattr(hc, n).element_size()
+                                for n in TraceColumns.HOT + ("k_op",) if getattr(hc, n) is not None)
+            pinned.append(hc)
+        h2d = sum(hc.host_bytes for hc in pinned)
+        host_format = f"unpacked columns (int64 / f64 / u64; {pack_refusal})"
+        for c in (ca, cb):
+            c._dev.clear()
+        del ca, cb
+        torch.cuda.empty_cache()
+        copy_stream = torch.cuda.Stream()
+    elif not args.no_e2e and e2e_skip is None:
         pinned = []
         for c, pc in zip((ca, cb), packed):
 
@@ -443,6 +473,7 @@ def run_ours(args, rank: int, world: int, local: int):
         torch.cuda.empty_cache()
         copy_stream = torch.cuda.Stream()
 
+    if not args.no_e2e and e2e_skip is None:
         def e2e_step():
             for pc in pinned:
                 pc.drop_device()

@@ -124,10 +124,12 @@ class TraceColumns:
 
     HOT = ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "op_sig")
 
-    def prefetch(self, stream: "torch.cuda.Stream", names=HOT) -> "torch.cuda.Event":
+    def prefetch(self, stream: "torch.cuda.Stream", names=HOT,
+                 decode_stream: "torch.cuda.Stream | None" = None) -> "torch.cuda.Event":
         """Start the host->HBM copies of ``names`` on ``stream`` (pinned host
         buffers copy asynchronously); later device() calls on another stream
-        wait for them (``wait_ready``, or the returned event)."""
+        wait for them (``wait_ready``, or the returned event).  Unpacked
+        columns need no decode (``decode_stream`` is for PackedColumns)."""
         dev = _native.device()
         with torch.cuda.stream(stream):
             for n in names:
