@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample-ops", type=int, default=2_000_000)
     ap.add_argument("--pairs", type=int, default=64, help="C5 corpus size (trace pairs)")
+    ap.add_argument("--overlap", default="compat", choices=("compat", "split"),
+                    help="energy.build_ledger overlap mode (split: power shared among concurrent intervals)")
     ap.add_argument("--shard", default="pair", choices=("pair", "window"),
                     help="N>1: 'pair' = every rank its own trace pair (weak scaling, corpus); "
                          "'window' = ONE pair split by time window over the ranks (strong scaling)")
@@ -333,7 +335,7 @@ def run_ours(args, rank: int, world: int, local: int):
     samples = ca.n_power + cb.n_power
 
     def step():
-        res = analyze(ca, cb, args.method, 0.10, args.k, summation=args.summation)
+        res = analyze(ca, cb, args.method, 0.10, args.k, summation=args.summation, overlap=args.overlap)
         if world > 1:  # corpus top-k: merge every rank's k candidates over NCCL
             jd = res.join
             f = jd.order
@@ -374,8 +376,8 @@ def run_ours(args, rank: int, world: int, local: int):
     from paper_2512_08365_b200.join import join_diff
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    la = build_ledger(ca, method=args.method, summation=args.summation)
-    lb = build_ledger(cb, method=args.method, summation=args.summation)
+    la = build_ledger(ca, method=args.method, summation=args.summation, overlap=args.overlap)
+    lb = build_ledger(cb, method=args.method, summation=args.summation, overlap=args.overlap)
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     from paper_2512_08365_b200.detect import FindingColumns
@@ -478,7 +480,7 @@ def run_ours(args, rank: int, world: int, local: int):
             for pc in pinned:
                 pc.drop_device()
             r = analyze(pinned[0], pinned[1], args.method, 0.10, args.k, copy_stream=copy_stream,
-                        summation=args.summation)
+                        summation=args.summation, overlap=args.overlap)
             return r
 
         for _ in range(max(5, args.warmup)):  # the first steps run up to 50 % slower (allocator, pinned pages)
@@ -524,7 +526,8 @@ def run_ours(args, rank: int, world: int, local: int):
         "data": "synthetic",
         "config": {"workload": f"{args.config}: trace pair, {cfg.n_ops} ops and "
                                f"{cfg.n_samples} power samples per trace",
-                   "method": args.method, "summation": args.summation, "intervals_per_pair": intervals,
+                   "method": args.method, "summation": args.summation, "overlap": args.overlap,
+                   "intervals_per_pair": intervals,
                    "samples_per_pair": samples, "findings": P, "top_k": args.k,
                    "l2": (f"inputs (~{(16 * samples + 24 * intervals) / 1e9:.1f} GB/pair read per step) >> "
                           f"126 MB L2; no flush needed"),
@@ -546,7 +549,8 @@ def run_ours(args, rank: int, world: int, local: int):
         except Exception as exc:  # noqa: BLE001 - the baseline must not hide the GPU line
             line["cpu_baseline"] = {"error": repr(exc)}
         try:
-            line["parity"] = parity_record(args, dev)
+            line["parity"] = (parity_record(args, dev) if args.overlap == "compat" else
+                              {"skipped": "split ledgers: pinned to the oracle's dwo_split by tests/test_gpu_split.py"})
         except Exception as exc:  # noqa: BLE001
             line["parity"] = {"error": repr(exc), "pass": False}
     print(json.dumps(line), flush=True)

@@ -41,8 +41,10 @@ def _decode_stream() -> "torch.cuda.Stream":
 
 def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAULT_THRESHOLD,
             k: int = 100, *, lean: bool = True, copy_stream: "torch.cuda.Stream | None" = None,
-            summation: str = "exact") -> Analysis:
+            summation: str = "exact", overlap: str = "compat") -> Analysis:
     """Ledgers for both traces, the signature-join diff and the top-k report.
+
+    ``overlap`` ("compat" or "split"): energy.build_ledger's overlap mode.
 
     ``summation`` (default "exact"): how the ledgers sum each interval's
     pieces (energy.build_ledger) -- the exact fixed-point sum, the scale
@@ -77,11 +79,11 @@ def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAUL
         # (by then A's attribution and the pairing are done), so only the last
         # column's decode trails the last byte
         cb.prefetch(copy_stream, names=("ts", "watts", "k_start", "k_end"), decode_stream=_decode_stream())
-    la = build_ledger(ca, method=method, summation=summation)
+    la = build_ledger(ca, method=method, summation=summation, overlap=overlap)
     if copy_stream is not None:
         torch.cuda.current_stream().wait_event(sig_ready)
         prep = join_prepare(ca, cb)
-    lb = build_ledger(cb, method=method, summation=summation)
+    lb = build_ledger(cb, method=method, summation=summation, overlap=overlap)
     jd = join_diff(ca, cb, la, lb, threshold, k, full_columns=not lean, epw=not lean, prep=prep,
                    columns=FindingColumns.DELTAS if lean else None)
     top = jd.top_findings(ca, cb)
