@@ -55,6 +55,7 @@ from .diagnose import (  # noqa: F401
     idle_baseline_watts,
 )
 from .join import join_diff, join_report, signature_of  # noqa: F401
+from .pipeline import analyze, analyze_corpus  # noqa: F401
 from .tensor_equiv import invariant_set, invariant_sets, singular_values, tensors_equivalent  # noqa: F401
 from .tensor_match import MatchStats, TensorPair, TensorPairSet, match_tensors  # noqa: F401
 
