@@ -598,7 +598,7 @@ __global__ void __launch_bounds__(WF_THREADS, DW_WF_MINB) join_window_findings_k
             j[u] = in ? jw[q] : -1;
             ea[u] = in ? __ldcs(A.joules + i) : 0.0;
             la[u] = in ? __ldcs(A.end + i) - __ldcs(A.start + i) : 0;
-            tie[u] = in && A.rank ? __ldcs(A.rank + i) : i;
+            tie[u] = in && A.rank && o.klo ? __ldcs(A.rank + i) : i;  // only a stored low key needs the rank
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
