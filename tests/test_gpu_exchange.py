@@ -45,12 +45,20 @@ def _worker(rank: int, world: int, port: int, n: int, out_path: str):
         order_g = torch.argsort(got[:, 0])
         order_w = torch.argsort(want[:, 0])
         ok &= got.shape == want.shape and torch.equal(got[order_g], want[order_w])
+    # a call larger than the mailbox (65536 rows at first): every rank re-creates
+    # its receive buffer, re-maps the peers', and the epochs keep counting
+    big = 150_000
+    got = comm.exchange(_ops(rank, big + 7 * rank, True), True).cpu()
+    want = torch.cat([shard._partition(_ops(s, big + 7 * s, True), world, True)[rank].reshape(-1, 6).cpu()
+                      for s in range(world)])
+    ok &= got.shape == want.shape and torch.equal(got[torch.argsort(got[:, 0])], want[torch.argsort(want[:, 0])])
     # empty sender on one rank
     e = _ops(rank, 0 if rank == 1 else 500, False)
     got = comm.exchange(e, False)
     total = torch.tensor([got.shape[0]])
     dist.all_reduce(total)
     ok &= int(total.item()) == (0 if world == 1 else 500)
+    comm.close()
     with open(f"{out_path}.{rank}", "w") as fh:
         fh.write("ok" if ok else "mismatch")
     dist.barrier()
