@@ -276,6 +276,15 @@ int dw_ig_kernel_lists(const uint8_t *buf, int64_t nops, const int64_t *kl_first
  * status->code. */
 int dw_status(const void *d_workspace, dw_stream_t stream, dw_status_t *status);
 
+/* The same read split in two, so a caller can queue more work before it
+ * waits: dw_status_copy queues the copy of the workspace's DW_STATUS_BYTES
+ * status block into h_block (pinned host memory; no synchronisation), and
+ * dw_status_decode turns that copy -- once the stream has passed the copy --
+ * into the status struct (same result and return code as dw_status). */
+#define DW_STATUS_BYTES 256
+int dw_status_copy(const void *d_workspace, void *h_block, dw_stream_t stream);
+int dw_status_decode(const void *h_block, dw_status_t *status);
+
 /* Exact (2^-64 J fixed point) sum of d_x[0..n) rounded once -> *d_out. */
 size_t dw_fx_sum_workspace_size(int64_t n);
 int dw_fx_sum(const double *d_x, int64_t n, double *d_out, void *d_workspace,

@@ -33,11 +33,12 @@ DW_E_UNSORTED = -8
 DW_SIGNAL_STEP = 0
 DW_SIGNAL_LINEAR = 1
 DW_MAX_SETS = 4
+DW_STATUS_BYTES = 256  # include/dwb200.h
 DW_DIRECT_MAX = 256
 
 # every symbol include/dwb200.h declares (tests check the .so exports them all)
 EXPORTED = (
-    "dw_attribute_workspace_size", "dw_attribute", "dw_ledger", "dw_status",
+    "dw_attribute_workspace_size", "dw_attribute", "dw_ledger", "dw_status", "dw_status_copy", "dw_status_decode",
     "dw_attribute_split_workspace_size", "dw_attribute_split", "dw_attribute_window", "dw_fx_sum_exact", "dw_replay",
     "dw_unpack_workspace_size", "dw_unpack_deltas", "dw_unpack_deltas_w", "dw_unpack_decimal",
     "dw_unpack_dict", "dw_unpack_bits", "dw_unpack_bits_dur", "dw_unpack_dict_bits",
@@ -136,6 +137,8 @@ def lib():
         L.dw_ledger.argtypes = [ctypes.POINTER(Signal), ctypes.POINTER(IntervalSet),
                                 ctypes.POINTER(IntervalSet), c_vp, ctypes.c_size_t, c_vp]
         L.dw_status.argtypes = [c_vp, c_vp, ctypes.POINTER(Status)]
+        L.dw_status_copy.argtypes = [c_vp, c_vp, c_vp]
+        L.dw_status_decode.argtypes = [c_vp, ctypes.POINTER(Status)]
         L.dw_attribute_window.argtypes = [ctypes.POINTER(Signal), ctypes.POINTER(IntervalSet), c_i32,
                                           ctypes.POINTER(Window), c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
                                           ctypes.c_size_t, c_vp]

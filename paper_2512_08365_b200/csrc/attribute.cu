@@ -28,6 +28,7 @@
 //   K4 long_intervals     one warp per long interval: exact fixed-point sum of
 //                         partial first/last tiles + prefix difference
 //   K5 fx_sum / finalize  operator_total (exact sum) and total / idle
+#include <cstring>
 #include <algorithm>
 #include <type_traits>
 
@@ -1421,7 +1422,17 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
 #ifdef DW_X_NO_ITEMS
         if (total >= 0) { __syncwarp(); if (lane == 0) mbar_arrive(&sm.empty[stage]); continue; }
 #endif
-        for (int v = ctid; v < total; v += ATTR_THREADS) {
+#ifndef DW_ITEM_SPREAD
+#define DW_ITEM_SPREAD 1
+#endif
+        // the last, partial round of items spread over DW_ITEM_SPREAD warps
+        // (1: lanes of the first warps, as full rounds)
+        constexpr int SPK = DW_ITEM_SPREAD;
+        const int vlast = ctid / (32 * SPK) * (32 * SPK) + lane * SPK + warp % SPK;
+        const int tfull = total - total % ATTR_THREADS;
+        for (int v0 = 0; v0 < total; v0 += ATTR_THREADS) {
+            const int v = v0 + (SPK > 1 && v0 == tfull ? vlast : ctid);
+            if (v >= total) break;
             const int j = (v >= c1) + (v >= c2) + (v >= c3);
             const SetDescX d = dsc[j];
             const int slot = v + d.sx;
@@ -2299,13 +2310,26 @@ int dw_fx_sum_exact(const double *d_x, int64_t n, int64_t *d_out_fx, void *d_wor
     return DW_OK;
 }
 
+static_assert(STATUS_BYTES == DW_STATUS_BYTES, "status block size");
+
+int dw_status_copy(const void *d_workspace, void *h_block, dw_stream_t stream) {
+    if (!d_workspace || !h_block) return DW_E_ARG;
+    return cudaMemcpyAsync(h_block, d_workspace, sizeof(DevStatus), cudaMemcpyDeviceToHost,
+                           (cudaStream_t)stream) == cudaSuccess ? DW_OK : DW_E_CUDA;
+}
+
 int dw_status(const void *d_workspace, dw_stream_t stream, dw_status_t *out) {
     if (!d_workspace || !out) return DW_E_ARG;
     DevStatus st;
-    if (cudaMemcpyAsync(&st, d_workspace, sizeof(st), cudaMemcpyDeviceToHost,
-                        (cudaStream_t)stream) != cudaSuccess)
-        return DW_E_CUDA;
+    if (dw_status_copy(d_workspace, &st, stream) != DW_OK) return DW_E_CUDA;
     if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return DW_E_CUDA;
+    return dw_status_decode(&st, out);
+}
+
+int dw_status_decode(const void *h_block, dw_status_t *out) {
+    if (!h_block || !out) return DW_E_ARG;
+    DevStatus st;
+    memcpy(&st, h_block, sizeof(st));
     auto idx = [](unsigned long long v) -> int64_t {
         return v == (unsigned long long)NONE ? -1 : (int64_t)v;
     };

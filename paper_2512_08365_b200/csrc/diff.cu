@@ -628,6 +628,15 @@ __global__ void __launch_bounds__(WF_THREADS, DW_WF_MINB) join_window_findings_k
     if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(n_matched, (unsigned long long)cnt);
 }
 
+__global__ void join_count_kernel(const unsigned long long *matched, int64_t na, int64_t b_only, int64_t *cnt) {
+    if (threadIdx.x != 0) return;
+    const int64_t m = (int64_t)*matched;
+    cnt[0] = na + b_only;
+    cnt[1] = m;
+    cnt[2] = na - m;
+    cnt[3] = b_only;
+}
+
 // B-only findings: numbered na + position in B order
 __global__ void join_findings_b_kernel(int64_t na, int64_t n_bonly, const int32_t *b_only,
                                        JoinSideDev B, double threshold, FindCols o, double *epw_a,
@@ -2016,12 +2025,9 @@ static int join_impl(const dw_join_side_t *a, const dw_join_side_t *b, int64_t m
                                                                    d_epw_a, d_epw_b);
         count_launch();
     }
-    unsigned long long matched = 0;
-    cudaMemcpyAsync(&matched, counters + 1, 8, cudaMemcpyDeviceToHost, s);
-    if (cudaStreamSynchronize(s) != cudaSuccess) return DW_E_CUDA;
-    const int64_t cnt[4] = {na + b_only, (int64_t)matched, na - (int64_t)matched, b_only};
-    cudaMemcpyAsync(d_count, cnt, sizeof(cnt), cudaMemcpyHostToDevice, s);
-    cudaStreamSynchronize(s);
+    // {P, matched, A-only, B-only} written on the device: no host round trip
+    join_count_kernel<<<1, 32, 0, s>>>(counters + 1, na, b_only, d_count);
+    count_launch();
     trace_mark(s, "join:end");
     DW_CHECK_LAUNCH();
     return DW_OK;

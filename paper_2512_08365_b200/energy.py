@@ -61,7 +61,7 @@ class PowerSignal:
     """
 
     __slots__ = ("_ts", "_w", "_span_hi", "_kind", "period_us", "delay_us", "_segments",
-                 "_samples", "_dev")
+                 "_samples", "_dev", "_first")
 
     def __init__(self, segments=(), samples=(), period_us=None, delay_us=None):
         self.period_us = period_us
@@ -69,6 +69,7 @@ class PowerSignal:
         self._segments = tuple(segments) if segments else ()
         self._samples = tuple(samples) if samples else ()
         self._dev = {}
+        self._first = None
         if self._segments:
             self._kind = _native.DW_SIGNAL_STEP
             ts, w = [], []
@@ -99,23 +100,26 @@ class PowerSignal:
 
     @classmethod
     def from_columns(cls, ts, watts, span_hi=None, kind="step", period_us=None,
-                     delay_us=None) -> "PowerSignal":
+                     delay_us=None, first=None) -> "PowerSignal":
         """A signal over existing arrays (numpy or CUDA tensors): ``kind="step"``
         takes breakpoints ts with the last segment ending at ``span_hi``;
-        ``kind="linear"`` takes samples."""
+        ``kind="linear"`` takes samples (``span_hi``, when given, is their last
+        timestamp).  ``first``: ts[0] when the caller knows it (no device read)."""
         sig = cls.__new__(cls)
         sig.period_us, sig.delay_us = period_us, delay_us
         sig._segments = None
         sig._samples = None
         sig._dev = {}
         sig._ts, sig._w = ts, watts
+        sig._first = None if first is None else int(first)
         if kind == "step":
             sig._kind = _native.DW_SIGNAL_STEP
             sig._span_hi = int(span_hi)
         else:
             sig._kind = _native.DW_SIGNAL_LINEAR
-            last = ts[-1].item() if isinstance(ts, torch.Tensor) else ts[-1]
-            sig._span_hi = int(last)
+            if span_hi is None:
+                span_hi = ts[-1].item() if isinstance(ts, torch.Tensor) else ts[-1]
+            sig._span_hi = int(span_hi)
         return sig
 
     # reference fields, materialised lazily
@@ -151,7 +155,10 @@ class PowerSignal:
     def span(self) -> tuple[int, int]:
         if self._kind is None or len(self) == 0:
             raise SignalError("empty power signal")
-        first = self._ts[0].item() if isinstance(self._ts, torch.Tensor) else self._ts[0]
+        first = getattr(self, "_first", None)
+        if first is None:
+            first = self._ts[0].item() if isinstance(self._ts, torch.Tensor) else self._ts[0]
+            self._first = int(first)
         return int(first), int(self._span_hi)
 
     def value_at(self, t_us: float) -> float:
@@ -477,8 +484,29 @@ class EnergyLedger:
         return getattr(self.per_kernel, "tensor", None)
 
 
-def _run_ledger(cols: TraceColumns, sig: PowerSignal, validate_order: bool, summation: str = "reference"):
-    """dw_ledger on the device; returns (per_op, per_k, total, op_total, idle)."""
+class _PendingStatus:
+    """A ledger's status block read in two steps (dw_status_copy now,
+    dw_status_decode when needed), so the next launches queue before the host
+    waits for this one."""
+
+    def __init__(self, ws: torch.Tensor, stream):
+        L = _native.lib()
+        self.host = torch.empty(_native.DW_STATUS_BYTES, dtype=torch.uint8, pin_memory=True)
+        _native.check(L.dw_status_copy(ws.data_ptr(), self.host.data_ptr(), stream), "dw_status_copy")
+        self.done = torch.cuda.Event()
+        self.done.record()
+
+    def result(self):
+        self.done.synchronize()
+        st = _native.Status()
+        _native.lib().dw_status_decode(self.host.data_ptr(), ctypes.byref(st))
+        return st
+
+
+def _run_ledger(cols: TraceColumns, sig: PowerSignal, validate_order: bool, summation: str = "reference",
+                defer: bool = False):
+    """dw_ledger on the device; returns (per_op, per_k, status) -- with
+    ``defer`` the status as a _PendingStatus (read later)."""
     dev = _native.device()
     L = _native.lib()
     op_s, op_e = cols.device("op_start"), cols.device("op_end")
@@ -496,6 +524,8 @@ def _run_ledger(cols: TraceColumns, sig: PowerSignal, validate_order: bool, summ
     stream = _native.stream_handle()
     _native.check(L.dw_ledger(ctypes.byref(csig), ctypes.byref(ops), ctypes.byref(kers),
                               ws.data_ptr(), ws.numel(), stream), "dw_ledger")
+    if defer:
+        return per_op, per_k, _PendingStatus(ws, stream)
     st = _native.Status()
     L.dw_status(ws.data_ptr(), stream, ctypes.byref(st))
     return per_op, per_k, st
@@ -503,7 +533,8 @@ def _run_ledger(cols: TraceColumns, sig: PowerSignal, validate_order: bool, summ
 
 def _raise_ledger_errors(cols: TraceColumns, st, span):
     """First failing interval in build_ledger's iteration order (op, then its
-    kernels; energy.py:305-316) raises the reference's SignalError."""
+    kernels; energy.py:305-316) raises the reference's SignalError.  ``span``:
+    the signal's span, or a callable returning it (read only on an error)."""
     if st.order_index >= 0:
         from .trace_model import TraceError
         raise TraceError("power samples must be strictly increasing in timestamp")
@@ -522,7 +553,7 @@ def _raise_ledger_errors(cols: TraceColumns, st, span):
         lo, hi = _read_pair(cols, "op_start", "op_end", bad_op)
     else:
         lo, hi = _read_pair(cols, "k_start", "k_end", bad_k)
-    _raise_interval_error(lo, hi, span)
+    _raise_interval_error(lo, hi, span() if callable(span) else span)
 
 
 def _read_pair(cols, a, b, i):
@@ -740,6 +771,18 @@ def build_ledger(trace, method: str = "ground_truth",
     TraceColumns.  Gaps between kernels inside an operator's interval go to the
     operator; gaps between operators go to ``idle``.
     """
+    return _begin_ledger(trace, method, period_us, delay_us, repeat, seed, validate_order, overlap,
+                         summation)()
+
+
+def _begin_ledger(trace, method="ground_truth", period_us=DEFAULT_SAMPLER_PERIOD_US,
+                  delay_us=DEFAULT_SAMPLER_DELAY_US, repeat=DEFAULT_REPLAY_REPEAT, seed=0,
+                  validate_order=False, overlap="compat", summation="reference"):
+    """build_ledger in two halves: the launches now, then a callable that
+    waits for the status, raises build_ledger's errors (same order: the
+    argument checks here, the data errors in the callable) and returns the
+    EnergyLedger.  pipeline.analyze launches both traces' ledgers before it
+    waits for either."""
     if method not in METHODS and method not in EXTRA_METHODS:
         raise ValueError(f"unknown energy method {method!r}")
     if overlap not in ("compat", "split"):
@@ -751,32 +794,34 @@ def build_ledger(trace, method: str = "ground_truth",
             raise SignalError("trace carries no power records")
         cols.wait_ready()
         first, last = cols._first_last_ts()
-        signal = PowerSignal.from_columns(cols.device("ts"), cols.device("watts"), kind="linear")
-        signal._span_hi = last
-        per_op, per_k, st = _run_ledger(cols, signal, validate_order, summation)
-        _raise_ledger_errors(cols, st, signal.span())
-        if overlap == "split":
-            return _split_ledger(method, cols, signal, st)
-        return EnergyLedger(method=method, per_kernel=JoulesView(cols.k_ids, per_k, "k"),
-                            per_operator=JoulesView(cols.op_ids, per_op, "op"),
-                            idle_joules=float(st.totals[2]), total_joules=float(st.totals[0]),
-                            op_total=float(st.totals[1]))
+        signal = PowerSignal.from_columns(cols.device("ts"), cols.device("watts"), span_hi=last, kind="linear",
+                                          first=first)
+        return _finish_ledger(method, cols, signal, signal.span, overlap,
+                              _run_ledger(cols, signal, validate_order, summation, defer=True))
     truth = ground_truth_signal(cols)
     if method == "replay":
-        return _replay_ledger(cols, truth, repeat, period_us, delay_us, seed)
+        led = _replay_ledger(cols, truth, repeat, period_us, delay_us, seed)
+        return lambda: led
     if method == "ground_truth":
         cols.wait_ready()
         signal = PowerSignal.from_columns(cols.device("ts"), cols.device("watts"),
                                           truth._span_hi, "step")
     else:
         signal = sampled_view(cols, period_us, delay_us, seed)
-    per_op, per_k, st = _run_ledger(cols, signal, validate_order, summation)
-    _raise_ledger_errors(cols, st, truth.span())
-    if overlap == "split":
-        return _split_ledger(method, cols, signal, st)
-    total, op_total, idle = st.totals[0], st.totals[1], st.totals[2]
-    return EnergyLedger(method=method,
-                        per_kernel=JoulesView(cols.k_ids, per_k, "k"),
-                        per_operator=JoulesView(cols.op_ids, per_op, "op"),
-                        idle_joules=float(idle), total_joules=float(total),
-                        op_total=float(op_total))
+    return _finish_ledger(method, cols, signal, truth.span(), overlap,
+                          _run_ledger(cols, signal, validate_order, summation, defer=True))
+
+
+def _finish_ledger(method, cols, signal, span, overlap, launched):
+    per_op, per_k, pending = launched
+
+    def finish() -> EnergyLedger:
+        st = pending.result()
+        _raise_ledger_errors(cols, st, span)
+        if overlap == "split":
+            return _split_ledger(method, cols, signal, st)
+        return EnergyLedger(method=method, per_kernel=JoulesView(cols.k_ids, per_k, "k"),
+                            per_operator=JoulesView(cols.op_ids, per_op, "op"),
+                            idle_joules=float(st.totals[2]), total_joules=float(st.totals[0]),
+                            op_total=float(st.totals[1]))
+    return finish

@@ -340,13 +340,18 @@ def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
                                      float(threshold), ctypes.byref(fs), p(prep.match_a), p(prep.b_only),
                                      prep.n_b_only, p(epw_a), p(epw_b), p(count), prep.ws.data_ptr(),
                                      prep.ws.numel(), _native.stream_handle(stream)), "dw_join_findings")
-    P, matched, a_only, b_only = (int(x) for x in count.cpu().tolist())
+    P = na + prep.n_b_only  # the counts are read back with the rank's summary (one transfer)
     kk = min(k, P)
     if ranked:
         order, summary = rank_order(fc.key_hi[:P], None, kk, tie_rank=rank_a, n_a=na)
-        sm = summary.cpu().tolist()
+        both = torch.cat([count, summary.reshape(-1).view(torch.int64)]).cpu()
+        cnt, sm = both[:4].tolist(), both[4:].view(torch.float64).tolist()
     else:
         order, sm = None, [0, 0.0]
+        cnt = count.cpu().tolist()
+    P2, matched, a_only, b_only = (int(x) for x in cnt)
+    if P2 != P:
+        raise RuntimeError(f"internal: join counted {P2} findings, expected {P}")
     return JoinDiff(P=P, n_a=na, n_matched=matched, n_a_only=a_only, n_b_only=b_only, columns=fc,
                     match_a=prep.match_a[:na], b_only=prep.b_only[:b_only],
                     epw_a=epw_a, epw_b=epw_b, order=order, n_waste=int(sm[0]),

@@ -15,7 +15,7 @@ import torch
 from . import _native
 from .columns import TraceColumns
 from .detect import DEFAULT_THRESHOLD, FindingColumns, Report, WasteFinding, rank_order_segmented
-from .energy import EnergyLedger, build_ledger
+from .energy import EnergyLedger, _begin_ledger, build_ledger
 
 import numpy as np
 from .join import JoinDiff, join_diff, join_prepare
@@ -79,11 +79,16 @@ def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAUL
         # (by then A's attribution and the pairing are done), so only the last
         # column's decode trails the last byte
         cb.prefetch(copy_stream, names=("ts", "watts", "k_start", "k_end"), decode_stream=_decode_stream())
-    la = build_ledger(ca, method=method, summation=summation, overlap=overlap)
+    # both ledgers and the pairing queue before the host waits on any of
+    # them (build_ledger's status read deferred; errors raised A first)
+    fa = _begin_ledger(ca, method=method, summation=summation, overlap=overlap)
     if copy_stream is not None:
         torch.cuda.current_stream().wait_event(sig_ready)
         prep = join_prepare(ca, cb)
-    lb = build_ledger(cb, method=method, summation=summation, overlap=overlap)
+    fb = _begin_ledger(cb, method=method, summation=summation, overlap=overlap)
+    if prep is None:
+        prep = join_prepare(ca, cb)
+    la, lb = fa(), fb()
     jd = join_diff(ca, cb, la, lb, threshold, k, full_columns=not lean, epw=not lean, prep=prep,
                    columns=FindingColumns.DELTAS if lean else None)
     top = jd.top_findings(ca, cb)
@@ -146,10 +151,12 @@ def analyze_corpus(pairs, method: str = "samples", threshold: float = DEFAULT_TH
     summaries, segs = [], []
     for a, b in pairs:
         ca, cb = TraceColumns.from_trace(a), TraceColumns.from_trace(b)
-        la = build_ledger(ca, method=method, summation=summation)
-        lb = build_ledger(cb, method=method, summation=summation)
+        fa = _begin_ledger(ca, method=method, summation=summation)
+        fb = _begin_ledger(cb, method=method, summation=summation)
+        prep = join_prepare(ca, cb)
+        la, lb = fa(), fb()
         jd = join_diff(ca, cb, la, lb, threshold, k, full_columns=False, epw=False,
-                       columns=FindingColumns.DELTAS, ranked=False)
+                       columns=FindingColumns.DELTAS, ranked=False, prep=prep)
         summaries.append(PairSummary(la.total_joules, lb.total_joules, jd, 0, 0.0))
         segs.append((jd.columns.key_hi[:jd.P], None, jd.columns.tie_rank, jd.n_a))
         del la, lb
