@@ -246,11 +246,18 @@ __global__ void iota64_kernel(int64_t *a, int64_t n) {
     if (i < n) a[i] = i;
 }
 
-// n_waste, exact wasted sum over waste findings, n
+// n_waste, exact wasted sum over waste findings, n; with hist, also the
+// rank's first-digit histogram (the top HIST_BITS of key_hi; one read of the
+// key column for both)
 __global__ void waste_sum_kernel(const uint64_t *khi, int64_t P, unsigned long long *partials,
-                                 unsigned int *done, double *summary) {
+                                 unsigned int *done, double *summary, unsigned int *hist) {
     __shared__ unsigned long long red[8][3];
+    __shared__ unsigned int h[HIST_BINS];
     __shared__ bool last;
+    if (hist) {
+        for (int b = threadIdx.x; b < HIST_BINS; b += blockDim.x) h[b] = 0;
+        __syncthreads();
+    }
     i128 acc = 0;
     unsigned long long cnt = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
@@ -260,6 +267,11 @@ __global__ void waste_sum_kernel(const uint64_t *khi, int64_t P, unsigned long l
         for (int u = 0; u < 4; ++u) {
             const int64_t i = b + (int64_t)u * blockDim.x;
             k[u] = i < P ? khi[i] : 0;
+        }
+        if (hist) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (b + (int64_t)u * blockDim.x < P) atomicAdd(&h[k[u] >> (64 - HIST_BITS)], 1u);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -279,6 +291,9 @@ __global__ void waste_sum_kernel(const uint64_t *khi, int64_t P, unsigned long l
         red[threadIdx.x >> 5][2] = cnt;
     }
     __syncthreads();
+    if (hist)
+        for (int b = threadIdx.x; b < HIST_BINS; b += blockDim.x)
+            if (h[b]) atomicAdd(&hist[b], h[b]);
     if (threadIdx.x == 0) {
         i128 s = 0;
         unsigned long long c = 0;
@@ -1299,6 +1314,9 @@ static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, const 
     if (ws_bytes < L.total) return DW_E_WORKSPACE;
     char *base = (char *)ws;
     trace_mark(s, "rank:start");
+    // the first digit's histogram comes with the waste sum (one read of the keys)
+    const bool fused_hist = summary && P > 0 && k > 0;
+    if (fused_hist) cudaMemsetAsync(base + L.hist, 0, 4 * HIST_BINS, s);
     if (summary) {
         cudaMemsetAsync(base + L.done, 0, 16, s);
         if (P > 0) {
@@ -1310,7 +1328,7 @@ static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, const 
                                                     blocks_for(P));
             waste_sum_kernel<<<(unsigned)wgrid, 256, 0, s>>>(
                 khi, P, (unsigned long long *)(base + L.partials), (unsigned int *)(base + L.done),
-                summary);
+                summary, fused_hist ? (unsigned int *)(base + L.hist) : nullptr);
             count_launch();
         } else {
             cudaMemsetAsync(summary, 0, 3 * sizeof(double), s);
@@ -1346,10 +1364,13 @@ static int rank_impl(int64_t P, const uint64_t *khi, const uint64_t *klo, const 
         r.plo = plo;
         r.mhi = mhi;
         r.mlo = mlo;
-        cudaMemsetAsync(r.hist, 0, 4 * HIST_BINS, s);
-        rank_hist_kernel<<<grid, 512, 0, s>>>(r);
+        if (!(fused_hist && pos == 128 - HIST_BITS)) {
+            cudaMemsetAsync(r.hist, 0, 4 * HIST_BINS, s);
+            rank_hist_kernel<<<grid, 512, 0, s>>>(r);
+            count_launch();
+        }
         rank_select_kernel<<<1, 32, 0, s>>>(r, need);
-        count_launch(2);
+        count_launch();
         trace_mark(s, "rank:digit");
         unsigned long long sel[3];
         cudaMemcpyAsync(sel, r.sel, sizeof(sel), cudaMemcpyDeviceToHost, s);

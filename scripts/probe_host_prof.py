@@ -13,10 +13,18 @@ for c in (a, b):
 for _ in range(3):
     analyze(a, b)
 torch.cuda.synchronize()
+import time
+N = 5
+t0 = time.perf_counter()
+for _ in range(N):
+    analyze(a, b)
+torch.cuda.synchronize()
+print(f"wall per step {1e3 * (time.perf_counter() - t0) / N:.3f} ms")
 pr = cProfile.Profile()
 pr.enable()
-analyze(a, b)
+for _ in range(N):
+    analyze(a, b)
 torch.cuda.synchronize()
 pr.disable()
 st = pstats.Stats(pr)
-st.sort_stats("tottime").print_stats(25)
+st.sort_stats("tottime").print_stats(45)
