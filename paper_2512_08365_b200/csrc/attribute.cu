@@ -1152,7 +1152,11 @@ __device__ __forceinline__ uint32_t abs_hi(double x) { return (uint32_t)__double
 //           2^23 W*us.  Longer or larger intervals go to K4 (int128 there).
 // Every warp releases the stage on its own.
 template <int KIND>
+#ifdef DW_X_MAXNREG
+__global__ void __maxnreg__(DW_X_MAXNREG) attribute_exact_kernel(AttrParams p) {
+#else
 __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams p) {
+#endif
     extern __shared__ __align__(128) unsigned char smem_raw[];
     TileSmemX &sm = *reinterpret_cast<TileSmemX *>(smem_raw);
     GroupSmemX *groups =
