@@ -450,7 +450,8 @@ def run_ours(args, rank: int, world: int, local: int):
                                ts_bits=pc.ts_bits, n_power=pc.n_power,
                                ts_last=pc._ts_last if pc.ts_bits is not None else None,
                                iv_bits=pc.iv_bits, n_ops=pc.n_ops, n_kernels=pc.n_kernels,
-                               sig_bits=pc.sig_bits)
+                               sig_bits=pc.sig_bits,
+                               watts_rep=pin(pc.watts_rep) if pc.watts_rep is not None else None)
             hc._dev["first_last"] = c._first_last_ts()
             pinned.append(hc)
         del packed, pc
@@ -465,7 +466,9 @@ def run_ours(args, rank: int, world: int, local: int):
             return f"u{8 * getattr(pc0, a).element_size()}/u{8 * getattr(pc0, b).element_size()}"
         host_format = (f"packed columns: ts deltas {tsf}, interval deltas/durations "
                        f"{ivf('op_start', 'op_end')} (ops) {ivf('k_start', 'k_end')} (kernels), watts "
-                       + ("9-digit decimal codes u32" if pc0.watts_p0 is not None else "f64")
+                       + (("run-coded 9-digit decimal codes (change bitmap + u32 code per change, "
+                           f"{pc0.watts.numel() / pc0.n_power:.3f} codes/sample)" if pc0.watts_rep is not None
+                           else "9-digit decimal codes u32") if pc0.watts_p0 is not None else "f64")
                        + ((f", sig dictionary + {pc0.sig_bits}-bit codes" if pc0.sig_bits is not None else
                            f", sig dictionary + u{8 * pc0.op_sig.element_size()} codes")
                           if pc0.op_sig_dict is not None else ", sig u64"))

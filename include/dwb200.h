@@ -236,6 +236,15 @@ int dw_unpack_dict(const uint64_t *d_dict, const void *d_code, int32_t code_byte
  * double a parse of the decimal text yields. */
 int dw_unpack_decimal(const uint32_t *d_code, int64_t n, int32_t p0, double *d_out, dw_stream_t stream);
 
+/* The same codes run-coded: a power meter read faster than it updates
+ * repeats its last value, so only the samples that carry a new code store
+ * one.  d_rep[(n + 31) / 32] is a bitmap, bit i % 32 of word i / 32 set when
+ * sample i carries a new code (bit 0 must be set); d_code holds those codes in
+ * sample order.  d_out[i] = the decoded code of the last new sample <= i. */
+size_t dw_unpack_decimal_rep_workspace_size(int64_t n);
+int dw_unpack_decimal_rep(const uint32_t *d_code, const uint32_t *d_rep, int64_t n, int32_t p0, double *d_out,
+                          void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
+
 /* JSONL ingestion (paper_2512_08365_b200/ingest.py):
  * byte-level stages over the raw file resident in HBM.  The canonical
  * power / op / kernel records of tensor-free traces parse here; `flags` (one

@@ -262,12 +262,17 @@ class PackedColumns(TraceColumns):
     def __init__(self, ts_base, ts_delta, watts, op_base, op_delta, op_dur, k_base, k_delta, k_dur,
                  trace_end, k_op=None, op_sig=None, watts_p0=None, ts_bias=0, op_sig_dict=None,
                  ts_bits=None, n_power=None, ts_last=None, iv_bits=None, n_ops=None, n_kernels=None,
-                 sig_bits=None, **kw):
+                 sig_bits=None, watts_rep=None, **kw):
         super().__init__(ts=ts_delta, watts=watts, trace_end=int(trace_end), op_start=op_delta, op_end=op_dur,
                          k_start=k_delta, k_end=k_dur, k_op=k_op, op_sig=op_sig, ops_sorted=True,
                          kernels_sorted=True, **kw)
         self.ts_base, self.op_start_base, self.k_start_base = int(ts_base), int(op_base), int(k_base)
         self.watts_p0 = None if watts_p0 is None else int(watts_p0)
+        # run-coded watts: bitmap of the samples carrying a new code (u32
+        # words); ``watts`` then holds those samples' codes only
+        self.watts_rep = watts_rep
+        if watts_rep is not None and self.watts_p0 is None:
+            raise ValueError("run-coded watts need decimal codes (watts_p0)")
         self.ts_bias = int(ts_bias)          # int8 / bit-packed ts deltas: delta = ts_bias + code
         self.op_sig_dict = op_sig_dict       # op_sig holds u16/u32 codes into this u64 dictionary
         self.ts_bits = None if ts_bits is None else int(ts_bits)  # ts holds bit-packed 32-bit words
@@ -325,7 +330,7 @@ class PackedColumns(TraceColumns):
         with torch.cuda.stream(stream):
             for n in names:
                 staged = []
-                for m in (n, {"op_start": "op_end", "k_start": "k_end"}.get(n), raw.get(n)):
+                for m in (n, {"op_start": "op_end", "k_start": "k_end", "watts": "watts_rep"}.get(n), raw.get(n)):
                     if m is None or getattr(self, m) is None or (m, dev.index) in self._dev \
                             or ("raw", m, dev.index) in self._dev:
                         continue
@@ -428,10 +433,23 @@ class PackedColumns(TraceColumns):
         t = self._dev.get(key)
         if t is None:
             code = self._staged("watts", dev)
-            t = torch.empty(code.numel(), dtype=torch.float64, device=dev)
-            _native.check(_native.lib().dw_unpack_decimal(_native.ptr(code), code.numel(), self.watts_p0,
-                                                          _native.ptr(t), _native.stream_handle()),
-                          "dw_unpack_decimal")
+            L = _native.lib()
+            if self.watts_rep is not None:  # run-coded: one code per change
+                n = self.n_power
+                bits = self._staged("watts_rep", dev)
+                if bits.numel() != (n + 31) // 32:
+                    raise ValueError(f"watts_rep: {bits.numel()} words for {n} samples")
+                t = torch.empty(n, dtype=torch.float64, device=dev)
+                ws = _native.Workspace.get(L.dw_unpack_decimal_rep_workspace_size(n))
+                _native.check(L.dw_unpack_decimal_rep(_native.ptr(code), _native.ptr(bits), n, self.watts_p0,
+                                                      _native.ptr(t), ws.data_ptr(), ws.numel(),
+                                                      _native.stream_handle()), "dw_unpack_decimal_rep")
+            else:
+                if code.numel() != self.n_power:
+                    raise ValueError(f"watts: {code.numel()} codes for {self.n_power} samples")
+                t = torch.empty(code.numel(), dtype=torch.float64, device=dev)
+                _native.check(L.dw_unpack_decimal(_native.ptr(code), code.numel(), self.watts_p0,
+                                                  _native.ptr(t), _native.stream_handle()), "dw_unpack_decimal")
             self._dev[key] = t
         return t
 
@@ -469,7 +487,7 @@ class PackedColumns(TraceColumns):
         def nb(a):
             return int(a.numel() * a.element_size()) if isinstance(a, torch.Tensor) else int(np.asarray(a).nbytes)
         cols = [getattr(self, n) for n in ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "op_sig")]
-        return sum(nb(a) for a in cols + [self.op_sig_dict] if a is not None)
+        return sum(nb(a) for a in cols + [self.op_sig_dict, self.watts_rep] if a is not None)
 
 
 def _narrow(d, what: str):
@@ -652,7 +670,48 @@ def decimal_code(w):
     return p0, code
 
 
-def pack(cols: TraceColumns, decimal: bool = True) -> PackedColumns:
+_REP_CHUNK = 1 << 26
+
+
+def rep_code(code):
+    """Run-code a column of decimal codes: (bitmap words u32 -- bit i set when
+    sample i's code differs from sample i-1's, bit 0 always --, the codes of
+    those samples), or None when that is not at least a quarter smaller.
+    numpy or torch (device columns are coded in chunks of 2^26 samples)."""
+    is_t = isinstance(code, torch.Tensor)
+    n = int(code.numel() if is_t else np.asarray(code).size)
+    if n < 64:
+        return None
+    if not is_t:
+        c = np.asarray(code)
+        new = np.empty(n, dtype=bool)
+        new[0] = True
+        np.not_equal(c[1:], c[:-1], out=new[1:])
+        m = int(new.sum())
+        if 4 * m + 4 * ((n + 31) // 32) > 3 * n:
+            return None
+        words = np.packbits(np.concatenate([new, np.zeros((-n) % 32, dtype=bool)]), bitorder="little").view(np.uint32)
+        return words, c[new]
+    new = torch.empty(n, dtype=torch.bool, device=code.device)
+    new[0] = True
+    torch.ne(code[1:], code[:-1], out=new[1:])
+    m = int(new.sum().item())
+    if 4 * m + 4 * ((n + 31) // 32) > 3 * n:
+        return None
+    nw = (n + 31) // 32
+    words = torch.empty(nw, dtype=torch.int32, device=code.device)
+    shifts = torch.arange(32, dtype=torch.int64, device=code.device)
+    for w0 in range(0, nw, _REP_CHUNK // 32):
+        w1 = min(w0 + _REP_CHUNK // 32, nw)
+        b = new[32 * w0: min(32 * w1, n)].to(torch.int64)
+        if b.numel() < 32 * (w1 - w0):
+            b = torch.cat([b, b.new_zeros(32 * (w1 - w0) - b.numel())])
+        v = (b.view(-1, 32) << shifts).sum(1)
+        words[w0:w1] = torch.where(v >= 0x80000000, v - 0x100000000, v).to(torch.int32)
+    return words, code[new]
+
+
+def pack(cols: TraceColumns, decimal: bool = True, runs: bool = True) -> PackedColumns:
     """Packed form of a trace with sorted power, operator and kernel starts
     (ValueError otherwise -- keep such traces unpacked).  Works on host or
     device columns; the result lives where the input does."""
@@ -684,6 +743,10 @@ def pack(cols: TraceColumns, decimal: bool = True) -> PackedColumns:
                 kb, kd, k_dur = sp[0], sp[3], dp[2]
     dec = decimal_code(cols.watts) if decimal else None
     watts, p0 = (cols.watts, None) if dec is None else (dec[1], dec[0])
+    rc = rep_code(watts) if dec is not None and runs else None
+    watts_rep = None
+    if rc is not None:
+        watts_rep, watts = rc
     sd = _sig_dict(cols.op_sig)
     sig, sig_dict = (cols.op_sig, None) if sd is None else (sd[1], sd[0])
     sig_bits = None
@@ -697,7 +760,7 @@ def pack(cols: TraceColumns, decimal: bool = True) -> PackedColumns:
     return PackedColumns(tb, td, watts, ob, od, o_dur, kb, kd, k_dur, cols.trace_end,
                          k_op=cols.k_op, op_sig=sig, watts_p0=p0, ts_bias=tbias, op_sig_dict=sig_dict,
                          ts_bits=twidth, n_power=cols.n_power, ts_last=tlast, iv_bits=iv_bits,
-                         n_ops=cols.n_ops, n_kernels=cols.n_kernels, sig_bits=sig_bits,
+                         n_ops=cols.n_ops, n_kernels=cols.n_kernels, sig_bits=sig_bits, watts_rep=watts_rep,
                          op_ids=cols.op_ids, k_ids=cols.k_ids, op_names=cols.op_names, op_work=cols.op_work,
                          op_rank=cols.op_rank)
 
@@ -709,7 +772,8 @@ def save_packed(cols: TraceColumns, path) -> None:
     import json
     pc = cols if isinstance(cols, PackedColumns) else pack(cols)
     arrays = {}
-    for n in ("ts", "watts", "op_start", "op_end", "k_start", "k_end", "k_op", "op_sig", "op_sig_dict", "op_work"):
+    for n in ("ts", "watts", "watts_rep", "op_start", "op_end", "k_start", "k_end", "k_op", "op_sig", "op_sig_dict",
+              "op_work"):
         a = getattr(pc, n)
         if a is None:
             continue
@@ -717,7 +781,8 @@ def save_packed(cols: TraceColumns, path) -> None:
         coded = n in ("op_start", "op_end", "k_start", "k_end") or (n == "ts" and a.itemsize > 1) or \
             n in pc.iv_bits or (n == "op_sig" and pc.sig_bits is not None) or \
             (n == "ts" and pc.ts_bits is not None) or \
-            (n == "watts" and pc.watts_p0 is not None) or (n == "op_sig" and pc.op_sig_dict is not None)
+            (n == "watts" and pc.watts_p0 is not None) or (n == "op_sig" and pc.op_sig_dict is not None) or \
+            n == "watts_rep"
         if coded:
             a = a.view(np.uint16 if a.itemsize == 2 else np.uint32)
         arrays[n] = np.ascontiguousarray(a)
@@ -726,7 +791,7 @@ def save_packed(cols: TraceColumns, path) -> None:
             "ts_bias": pc.ts_bias, "ts_bits": pc.ts_bits, "n_power": pc.n_power,
             "ts_last": pc._ts_last if pc.ts_bits is not None else None,
             "iv_bits": {k: list(v) for k, v in pc.iv_bits.items()}, "n_ops": pc.n_ops, "n_kernels": pc.n_kernels,
-            "sig_bits": pc.sig_bits,
+            "sig_bits": pc.sig_bits, "watts_rep": pc.watts_rep is not None,
             "columns": {}}
     off = 0
     for n, a in arrays.items():
@@ -774,4 +839,5 @@ def load_packed(path, pin: bool = False) -> PackedColumns:
                          op_work=cols.get("op_work"), watts_p0=p0, ts_bias=meta.get("ts_bias", 0),
                          op_sig_dict=sig_dict, ts_bits=meta.get("ts_bits"), n_power=meta.get("n_power"),
                          ts_last=meta.get("ts_last"), iv_bits={k: tuple(v) for k, v in meta.get("iv_bits", {}).items()},
-                         n_ops=meta.get("n_ops"), n_kernels=meta.get("n_kernels"), sig_bits=meta.get("sig_bits"))
+                         n_ops=meta.get("n_ops"), n_kernels=meta.get("n_kernels"), sig_bits=meta.get("sig_bits"),
+                         watts_rep=as_signed(cols["watts_rep"]) if meta.get("watts_rep") else None)

@@ -126,21 +126,106 @@ __global__ void dict_decode_kernel(const uint64_t *dict, const T *code, int64_t 
 // __ddiv_rn's instructions.
 __constant__ double RCP10[23] = {1.0, 0.1, 0.01, 0.001, 0.0001, 1e-05, 1e-06, 1e-07, 1e-08, 1e-09, 1e-10, 1e-11, 1e-12, 1e-13, 1e-14, 1e-15, 1e-16, 1e-17, 1e-18, 1e-19, 1e-20, 1e-21, 1e-22};
 
+__device__ __forceinline__ double decimal_value(uint32_t c, int32_t p0) {
+    const double m = (double)(c & 0x3FFFFFFFu);
+    const int p = p0 + (int)(c >> 30);
+    if (p >= 0) {
+        const double y = RCP10[p], d = POW10[p];
+        const double q = __dmul_rn(m, y);
+        return __fma_rn(__fma_rn(-q, d, m), y, q);
+    }
+    return __dmul_rn(m, POW10[-p]);
+}
+
 __global__ void decimal_decode_kernel(const uint32_t *code, int64_t n, int32_t p0, double *out) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-        const uint32_t c = __ldcs(code + i);
-        const double m = (double)(c & 0x3FFFFFFFu);
-        const int p = p0 + (int)(c >> 30);
-        double v;
-        if (p >= 0) {
-            const double y = RCP10[p], d = POW10[p];
-            const double q = __dmul_rn(m, y);
-            v = __fma_rn(__fma_rn(-q, d, m), y, q);
-        } else {
-            v = __dmul_rn(m, POW10[-p]);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+        __stcs(out + i, decimal_value(__ldcs(code + i), p0));
+}
+
+// ---- run-coded watts: a bitmap marks the samples that carry a new code (bit
+// i of word i / 32; sample 0 always does), the codes of those samples only.
+// Sample s takes code[popcount of the bitmap over [0, s]] - 1].  Three
+// passes: new codes per block of REP_WORDS words, their exclusive scan (one
+// block), then the decode: each warp takes 32 words (1024 samples) and writes
+// 32 coalesced rows of 32 samples.
+constexpr int REP_WORDS = 1024;  // bitmap words per block (32768 samples)
+
+__global__ void __launch_bounds__(256) rep_count_kernel(const uint32_t *rep, int64_t nwords,
+                                                        unsigned long long *bsum) {
+    __shared__ unsigned ws[8];
+    const int64_t w0 = blockIdx.x * (int64_t)REP_WORDS;
+    unsigned c = 0;
+    for (int k = threadIdx.x; k < REP_WORDS; k += 256)
+        if (w0 + k < nwords) c += __popc(__ldg(rep + w0 + k));
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < 8; ++w) t += ws[w];
+        bsum[blockIdx.x] = t;
+    }
+}
+
+// exclusive scan of nb block counts, in place (one block of 1024 threads)
+__global__ void __launch_bounds__(1024) rep_scan_kernel(unsigned long long *bsum, int64_t nb) {
+    __shared__ unsigned long long wt[32];
+    __shared__ unsigned long long carry;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < nb; c0 += 1024) {
+        const int64_t i = c0 + threadIdx.x;
+        const unsigned long long v = i < nb ? bsum[i] : 0;
+        unsigned long long x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
-        __stcs(out + i, v);
+        if (lane == 31) wt[warp] = x;
+        __syncthreads();
+        unsigned long long off = carry;
+        for (int w = 0; w < warp; ++w) off += wt[w];
+        if (i < nb) bsum[i] = off + x - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = off + x;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(1024) rep_decode_kernel(const uint32_t *code, const uint32_t *rep, int64_t n,
+                                                          int32_t p0, const unsigned long long *bpre,
+                                                          double *out) {
+    __shared__ unsigned wt[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t nwords = (n + 31) >> 5;
+    const int64_t wfirst = blockIdx.x * (int64_t)REP_WORDS + warp * 32;  // this warp's first word
+    const uint32_t word = wfirst + lane < nwords ? __ldcs(rep + wfirst + lane) : 0u;
+    const unsigned pc = __popc(word);
+    unsigned inc = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) wt[warp] = inc;
+    __syncthreads();
+    const unsigned off = __reduce_add_sync(0xffffffffu, lane < warp ? wt[lane] : 0u);
+    const int64_t base = (int64_t)bpre[blockIdx.x] + off - 1;  // new codes before this warp, minus one
+    const unsigned exc = inc - pc;
+    const uint32_t upto = 0xFFFFFFFFu >> (31 - lane);  // bits 0 .. lane
+#pragma unroll 4
+    for (int k = 0; k < 32; ++k) {
+        const uint32_t wk = __shfl_sync(0xffffffffu, word, k);
+        const unsigned ek = __shfl_sync(0xffffffffu, exc, k);
+        const int64_t smp = ((wfirst + k) << 5) + lane;
+        if (smp < n) {
+            int64_t idx = base + ek + __popc(wk & upto);
+            idx = idx < 0 ? 0 : idx;  // only a bitmap without bit 0 (invalid input)
+            __stcs(out + smp, decimal_value(__ldg(code + idx), p0));
+        }
     }
 }
 
@@ -232,6 +317,27 @@ int dw_unpack_dict(const uint64_t *d_dict, const void *d_code, int32_t code_byte
 int dw_unpack_deltas(const uint32_t *d_delta, int64_t n, int64_t base, int64_t *d_out, const uint32_t *d_dur,
                      int64_t *d_end, void *d_workspace, size_t workspace_bytes, dw_stream_t stream) {
     return dw_unpack_deltas_w(d_delta, 4, 0, n, base, d_out, d_dur, 4, d_end, d_workspace, workspace_bytes, stream);
+}
+
+size_t dw_unpack_decimal_rep_workspace_size(int64_t n) {
+    const int64_t nwords = (std::max<int64_t>(n, 0) + 31) >> 5;
+    return 8 * (size_t)(ceil_div(nwords, REP_WORDS) + 1) + 256;
+}
+
+int dw_unpack_decimal_rep(const uint32_t *d_code, const uint32_t *d_rep, int64_t n, int32_t p0, double *d_out,
+                          void *d_workspace, size_t workspace_bytes, dw_stream_t stream) {
+    if (n < 0 || (n && (!d_code || !d_rep || !d_out)) || p0 < -22 || p0 + 3 > 22) return DW_E_ARG;
+    if (n == 0) return DW_OK;
+    if (!d_workspace || workspace_bytes < dw_unpack_decimal_rep_workspace_size(n)) return DW_E_WORKSPACE;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nwords = (n + 31) >> 5, nb = ceil_div(nwords, REP_WORDS);
+    unsigned long long *bsum = (unsigned long long *)d_workspace;
+    rep_count_kernel<<<(unsigned)nb, 256, 0, s>>>(d_rep, nwords, bsum);
+    rep_scan_kernel<<<1, 1024, 0, s>>>(bsum, nb);
+    rep_decode_kernel<<<(unsigned)nb, 1024, 0, s>>>(d_code, d_rep, n, p0, bsum, d_out);
+    count_launch(3);
+    DW_CHECK_LAUNCH();
+    return DW_OK;
 }
 
 int dw_unpack_decimal(const uint32_t *d_code, int64_t n, int32_t p0, double *d_out, dw_stream_t stream) {

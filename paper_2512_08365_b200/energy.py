@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import _native
-from .columns import TraceColumns, synthetic_id, synthetic_ids
+from .columns import PackedColumns, TraceColumns, synthetic_id, synthetic_ids
 from .trace_model import OperatorEvent, PowerSample, Trace
 
 US_PER_S = 1_000_000
@@ -239,8 +239,9 @@ def ground_truth_signal(trace) -> PowerSignal:
     if cols.n_power == 0:
         raise SignalError("trace carries no power records")
     _, span_hi = cols.signal_span()
-    sig = PowerSignal.from_columns(cols.ts, cols.watts, span_hi, "step")
-    return sig
+    if isinstance(cols, PackedColumns):  # host columns hold codes: the decoded device columns
+        return PowerSignal.from_columns(cols.device("ts"), cols.device("watts"), span_hi, "step")
+    return PowerSignal.from_columns(cols.ts, cols.watts, span_hi, "step")
 
 
 # ----------------------------------------------------------------- integrate

@@ -26,7 +26,7 @@ for c in (ca, cb):
                        ts_bits=pc.ts_bits, n_power=pc.n_power,
                        ts_last=pc._ts_last if pc.ts_bits is not None else None,
                                iv_bits=pc.iv_bits, n_ops=pc.n_ops, n_kernels=pc.n_kernels,
-                               sig_bits=pc.sig_bits)
+                               sig_bits=pc.sig_bits, watts_rep=None if pc.watts_rep is None else pin(pc.watts_rep))
     hc._dev["first_last"] = c._first_last_ts()
     pinned.append(hc)
 for c in (ca, cb):
@@ -70,7 +70,8 @@ for p in pinned:
                       p.k_start_base, p.k_start.cuda(), p.k_end.cuda(), p.trace_end, op_sig=p.op_sig.cuda(),
                       watts_p0=p.watts_p0, ts_bias=p.ts_bias, op_sig_dict=p.op_sig_dict,
                       ts_bits=p.ts_bits, n_power=p.n_power, ts_last=p._ts_last if p.ts_bits is not None else None,
-                      iv_bits=p.iv_bits, n_ops=p.n_ops, n_kernels=p.n_kernels, sig_bits=p.sig_bits)
+                      iv_bits=p.iv_bits, n_ops=p.n_ops, n_kernels=p.n_kernels, sig_bits=p.sig_bits,
+                      watts_rep=None if p.watts_rep is None else p.watts_rep.cuda())
     q._dev["first_last"] = p._dev["first_last"]
     dev_packed.append(q)
 for it in range(3):

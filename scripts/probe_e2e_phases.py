@@ -25,7 +25,7 @@ for c in (ca, cb):
                        ts_bits=pc.ts_bits, n_power=pc.n_power,
                        ts_last=pc._ts_last if pc.ts_bits is not None else None,
                                iv_bits=pc.iv_bits, n_ops=pc.n_ops, n_kernels=pc.n_kernels,
-                               sig_bits=pc.sig_bits)
+                               sig_bits=pc.sig_bits, watts_rep=None if pc.watts_rep is None else pin(pc.watts_rep))
     hc._dev["first_last"] = c._first_last_ts()
     pinned.append(hc)
 for c in (ca, cb):

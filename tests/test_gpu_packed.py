@@ -47,7 +47,7 @@ def test_decode_exact_and_ledger_identical(tmp_path):
                           q.k_start, q.k_end, q.trace_end, op_sig=q.op_sig, watts_p0=q.watts_p0, ts_bias=q.ts_bias,
                           op_sig_dict=q.op_sig_dict, ts_bits=q.ts_bits, n_power=q.n_power,
                           ts_last=q._ts_last, iv_bits=q.iv_bits, n_ops=q.n_ops, n_kernels=q.n_kernels,
-                          sig_bits=q.sig_bits)
+                          sig_bits=q.sig_bits, watts_rep=q.watts_rep)
             for q in (ha, hb)]
     rb = analyze(bare[0], bare[1], "samples", 0.10, 20)
     assert [f.category for f in rb.report.findings] == [f.category for f in ra.report.findings]
@@ -92,3 +92,66 @@ def test_bit_packed_intervals_decode_exactly(spread):
     for name in ("op_start", "op_end", "k_start", "k_end"):
         assert torch.equal(p.device(name).cpu(), torch.from_numpy(c.host(name))), name
     assert p.n_ops == n and p.n_kernels == n
+
+
+@pytest.mark.parametrize("n,maxrun", [(1, 1), (33, 3), (100_003, 9), (1_000_000, 1), (2_500_017, 40)])
+def test_run_coded_watts_decode_exactly(n, maxrun):
+    """dw_unpack_decimal_rep: the change bitmap's prefix counts across words,
+    warps and blocks (32768 samples each); ragged tails; runs of one sample
+    (a code per sample) and long runs."""
+    from paper_2512_08365_b200 import _native
+    from paper_2512_08365_b200.columns import decimal_code
+    rng = np.random.default_rng(n)
+    runs = rng.integers(1, maxrun + 1, size=n)
+    vals = np.round(rng.uniform(1.0, 900.0, size=n), 3)
+    w = np.repeat(vals, runs)[:n]
+    p0, code = decimal_code(w)
+    new = np.ones(n, dtype=bool)
+    new[1:] = code[1:] != code[:-1]
+    words = np.packbits(np.concatenate([new, np.zeros((-n) % 32, dtype=bool)]), bitorder="little").view(np.uint32)
+    dev = torch.device("cuda")
+    d_code = torch.from_numpy(code[new].view(np.int32)).to(dev)
+    d_rep = torch.from_numpy(words.view(np.int32)).to(dev)
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    L = _native.lib()
+    ws = torch.empty(L.dw_unpack_decimal_rep_workspace_size(n), dtype=torch.uint8, device=dev)
+    _native.check(L.dw_unpack_decimal_rep(_native.ptr(d_code), _native.ptr(d_rep), n, p0, _native.ptr(out),
+                                          ws.data_ptr(), ws.numel(), _native.stream_handle()), "rep")
+    np.testing.assert_array_equal(out.cpu().numpy(), w)
+    assert L.dw_unpack_decimal_rep(_native.ptr(d_code), _native.ptr(d_rep), n, p0, _native.ptr(out),
+                                   ws.data_ptr(), 8, _native.stream_handle()) == _native.DW_E_WORKSPACE
+
+
+def test_run_coded_trace_analysis_identical():
+    """The C4-shaped synthetic power repeats ~80% of samples: it travels
+    run-coded, decodes to the same column, and the pinned-host analysis is
+    identical to the device-resident one."""
+    cfg = synth.scaled(synth.CONFIGS["C4"], 200_000)
+    a, b = synth.make_pair(cfg)
+    p = pack(a)
+    assert p.watts_rep is not None
+    assert p.watts.numel() < 0.4 * a.n_power
+    assert torch.equal(p.device("watts"), a.device("watts"))
+    pin = lambda t: torch.empty(t.shape, dtype=t.dtype, pin_memory=True).copy_(t)  # noqa: E731
+    from paper_2512_08365_b200.columns import PackedColumns
+    hosts = []
+    for c in (a, b):
+        q = pack(c)
+        hosts.append(PackedColumns(q.ts_base, pin(q.ts), pin(q.watts), q.op_start_base, pin(q.op_start),
+                                   pin(q.op_end), q.k_start_base, pin(q.k_start), pin(q.k_end), q.trace_end,
+                                   op_sig=pin(q.op_sig), watts_p0=q.watts_p0, ts_bias=q.ts_bias,
+                                   op_sig_dict=pin(q.op_sig_dict), ts_bits=q.ts_bits, n_power=q.n_power,
+                                   ts_last=q._ts_last, iv_bits=q.iv_bits, n_ops=q.n_ops, n_kernels=q.n_kernels,
+                                   sig_bits=q.sig_bits, watts_rep=pin(q.watts_rep)))
+    ra = analyze(a, b, "samples", 0.10, 20)
+    rh = analyze(hosts[0], hosts[1], "samples", 0.10, 20, copy_stream=torch.cuda.Stream())
+    assert rh.report.total_a == ra.report.total_a and rh.report.total_b == ra.report.total_b
+    assert rh.report.wasted_joules == ra.report.wasted_joules
+    assert [f.pair for f in rh.report.findings] == [f.pair for f in ra.report.findings]
+    # a run-coded column without its bitmap is refused, not misread
+    bad = PackedColumns(p.ts_base, p.ts, p.watts, p.op_start_base, p.op_start, p.op_end, p.k_start_base, p.k_start,
+                        p.k_end, p.trace_end, op_sig=p.op_sig, watts_p0=p.watts_p0, ts_bias=p.ts_bias,
+                        op_sig_dict=p.op_sig_dict, ts_bits=p.ts_bits, n_power=p.n_power, ts_last=p._ts_last,
+                        iv_bits=p.iv_bits, n_ops=p.n_ops, n_kernels=p.n_kernels, sig_bits=p.sig_bits)
+    with pytest.raises(ValueError):
+        bad.device("watts")

@@ -156,3 +156,28 @@ def test_bitfields_refuse_wide_spreads():
     assert _bitfields(np.array([0, 1 << 15]), 15) is None
     assert _bitpack(np.array([5, 3])) is None          # a negative delta: not sorted
     assert _bitpack(np.array([7])) is None             # fewer than two samples
+
+
+def test_run_coded_watts(tmp_path):
+    """Watts that repeat (a meter read faster than it updates) travel as a
+    change bitmap plus one code per change (columns.rep_code); the host
+    decode of the file's columns gives every sample back."""
+    from paper_2512_08365_b200.columns import rep_code
+    rng = np.random.default_rng(5)
+    c = _cols()
+    n = c.n_power
+    runs = rng.integers(1, 12, size=n)
+    w = _round9(np.repeat(rng.uniform(50, 700, n), runs)[:n])
+    c = TraceColumns.from_arrays(c.ts, w, c.op_start, c.op_end, c.k_start, c.k_end, c.k_op)
+    p = pack(c)
+    assert p.watts_rep is not None and np.asarray(p.watts).size < n / 2
+    assert pack(c, runs=False).watts_rep is None
+    save_packed(c, tmp_path / "r.dwc")
+    q = load_packed(tmp_path / "r.dwc")
+    for x in (p, q):
+        bits = np.unpackbits(np.asarray(x.watts_rep).view(np.uint8), bitorder="little")[:n].astype(bool)
+        assert bits[0]
+        np.testing.assert_array_equal(_decode(x.watts_p0, np.asarray(x.watts))[np.cumsum(bits) - 1], w)
+    assert q.host_bytes == p.host_bytes < pack(c, runs=False).host_bytes
+    # no repeats: plain codes
+    assert rep_code(np.arange(1000, dtype=np.uint32)) is None
