@@ -1241,7 +1241,13 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
         }
 
         // the group's next tile, claimed early (read after this tile's barriers)
-        if (ctid == 32) gs.next_it[par ^ 1] = atomicAdd(&sm.claim, 1);
+#ifndef DW_CLAIM_T
+#define DW_CLAIM_T 32
+#endif
+#ifndef DW_TSUM_T
+#define DW_TSUM_T 32
+#endif
+        if (ctid == DW_CLAIM_T) gs.next_it[par ^ 1] = atomicAdd(&sm.claim, 1);
         // ---- pass B: pieces rb .. rb + XPER - 1 (r < last)
         const int rb = r0 + ctid * XPER;
         long long q[XPER];
@@ -1405,7 +1411,7 @@ __global__ void __launch_bounds__(KTHREADS, 1) attribute_exact_kernel(AttrParams
         }
         consumer_sync(g);
         const unsigned long long *P = reinterpret_cast<const unsigned long long *>(s_ts);
-        if (ctid == 32) {  // the exact tile sum (its shares are double buffered)
+        if (ctid == DW_TSUM_T) {  // the exact tile sum (its shares are double buffered)
             i128 t = 0;
 #pragma unroll
             for (int k = 0; k < NCW; ++k) t += join((uint64_t)gs.red[par][k][0], (uint64_t)gs.red[par][k][1]);
