@@ -211,34 +211,44 @@ class JoinDiff:
     def _rows(self, cols_a, cols_b, classify, trace_a, trace_b, ia, ib, ea, eb, la, lb, h) -> list[WasteFinding]:
         """WasteFinding rows from the k rows' columns; ``h`` None: the verdict
         columns derived on the host with the device's rule (judge)."""
+        ia, ib = np.asarray(ia).tolist(), np.asarray(ib).tolist()
+        ea, eb = np.asarray(ea, dtype=np.float64).tolist(), np.asarray(eb, dtype=np.float64).tolist()
+        la, lb = np.asarray(la).tolist(), np.asarray(lb).tolist()
+        k = len(ia)
         if h is None:  # the k rows' verdicts on the host, as the device computed them for all
-            rows = [judge(float(ea[r]), float(eb[r]), int(la[r]), int(lb[r]), 0.0, self.threshold)
-                    for r in range(len(ia))]
-            h = {"ratio": np.array([x[0] for x in rows]), "wasted": np.array([x[1] for x in rows]),
-                 "verdict": np.array([VERDICTS.index(x[2]) for x in rows], dtype=np.int64),
-                 "side": np.array([SIDES.index(x[3]) for x in rows], dtype=np.int64),
-                 "informational": np.array([x[4] for x in rows], dtype=bool)}
-        name = lambda ids, i, n: (ids[i] if ids is not None else synthetic_id("op", i, n))  # noqa: E731
-        cats = ["unknown"] * len(ia)
-        waste = np.nonzero(h["verdict"] == VERDICTS.index(VERDICT_WASTE))[0]
-        if classify and waste.size:
+            rows = [judge(ea[r], eb[r], la[r], lb[r], 0.0, self.threshold) for r in range(k)]
+            ratio = [x[0] for x in rows]
+            wasted = [x[1] for x in rows]
+            verdict = [x[2] for x in rows]
+            side = [x[3] for x in rows]
+            info = [bool(x[4]) for x in rows]
+        else:
+            ratio, wasted = np.asarray(h["ratio"]).tolist(), np.asarray(h["wasted"]).tolist()
+            verdict = [VERDICTS[v] for v in np.asarray(h["verdict"]).tolist()]
+            side = [SIDES[v] for v in np.asarray(h["side"]).tolist()]
+            info = [bool(v) for v in np.asarray(h["informational"]).tolist()]
+
+        def namer(cols):
+            ids = cols.op_ids
+            if ids is not None:
+                return lambda i: ids[i]
+            w = len(str(max(cols.n_ops - 1, 0)))  # synthetic_id's zero padding
+            return lambda i: f"op{i:0{w}d}"
+        name_a, name_b = namer(cols_a), namer(cols_b)
+        cats = ["unknown"] * k
+        waste = [r for r in range(k) if verdict[r] == VERDICT_WASTE]
+        if classify and waste:
             from .diagnose import classify_pairs
-            got = classify_pairs(cols_a, cols_b, [SIDES[h["side"][r]] for r in waste], ia[waste], ib[waste],
-                                 trace_a, trace_b)
-            for r, c in zip(waste.tolist(), got):
+            got = classify_pairs(cols_a, cols_b, [side[r] for r in waste], np.asarray([ia[r] for r in waste]),
+                                 np.asarray([ib[r] for r in waste]), trace_a, trace_b)
+            for r, c in zip(waste, got):
                 cats[r] = c
-        out = []
-        for r in range(len(ia)):
-            na = (name(cols_a.op_ids, int(ia[r]), cols_a.n_ops),) if ia[r] >= 0 else ()
-            nb = (name(cols_b.op_ids, int(ib[r]), cols_b.n_ops),) if ib[r] >= 0 else ()
-            out.append(WasteFinding(
-                pair=SubgraphPair(nodes_a=na, nodes_b=nb), energy_a=float(ea[r]),
-                energy_b=float(eb[r]), energy_ratio=float(h["ratio"][r]),
-                latency_a=int(la[r]), latency_b=int(lb[r]),
-                output_rel_diff=0.0, verdict=VERDICTS[h["verdict"][r]], category=cats[r],
-                wasteful_side=SIDES[h["side"][r]], wasted_joules=float(h["wasted"][r]),
-                informational=bool(h["informational"][r])))
-        return out
+        return [WasteFinding(
+            pair=SubgraphPair(nodes_a=(name_a(ia[r]),) if ia[r] >= 0 else (),
+                              nodes_b=(name_b(ib[r]),) if ib[r] >= 0 else ()),
+            energy_a=ea[r], energy_b=eb[r], energy_ratio=ratio[r], latency_a=la[r], latency_b=lb[r],
+            output_rel_diff=0.0, verdict=verdict[r], category=cats[r], wasteful_side=side[r],
+            wasted_joules=wasted[r], informational=info[r]) for r in range(k)]
 
 
 DEFAULT_MAX_DISTINCT = 1 << 20
