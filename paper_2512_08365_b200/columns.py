@@ -330,7 +330,11 @@ class PackedColumns(TraceColumns):
         with torch.cuda.stream(stream):
             for n in names:
                 staged = []
-                for m in (n, {"op_start": "op_end", "k_start": "k_end", "watts": "watts_rep"}.get(n), raw.get(n)):
+                # companions travel with their column: a decode never issues a
+                # copy of its own (it would queue behind every transfer
+                # already waiting on the copy engine)
+                for m in (n, {"op_start": "op_end", "k_start": "k_end", "watts": "watts_rep",
+                              "op_sig": "op_sig_dict"}.get(n), raw.get(n)):
                     if m is None or getattr(self, m) is None or (m, dev.index) in self._dev \
                             or ("raw", m, dev.index) in self._dev:
                         continue
@@ -363,6 +367,8 @@ class PackedColumns(TraceColumns):
 
     def _raw(self, name):
         src = getattr(self, name)
+        if name == "op_sig_dict" and not isinstance(src, torch.Tensor):
+            return torch.from_numpy(np.ascontiguousarray(np.asarray(src).view(np.int64)))
         if isinstance(src, torch.Tensor):
             return src
         a = np.ascontiguousarray(src)
@@ -459,9 +465,7 @@ class PackedColumns(TraceColumns):
         t = self._dev.get(key)
         if t is None:
             code = self._staged("op_sig", dev)
-            d = self.op_sig_dict
-            d = (d if isinstance(d, torch.Tensor) else torch.from_numpy(np.asarray(d).view(np.int64))).to(
-                dev, non_blocking=True)
+            d = self._staged("op_sig_dict", dev)
             if self.sig_bits is not None:
                 t = torch.empty(self.n_ops, dtype=torch.int64, device=dev)
                 _native.check(_native.lib().dw_unpack_dict_bits(_native.ptr(d), _native.ptr(code), self.sig_bits,

@@ -74,7 +74,9 @@ def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAUL
         # B's copies queue behind A's transfers (not its decodes): concurrent
         # copies would share PCIe and delay A to the end of the transfer
         copy_stream.wait_event(getattr(ca, "copied", None) or a_ready)
-        sig_ready = cb.prefetch(copy_stream, names=("op_sig", "op_start", "op_end"))
+        # (decoded on the side stream too: a decode queued on the copy stream
+        # would hold B's next transfers behind A's attribution for the SMs)
+        sig_ready = cb.prefetch(copy_stream, names=("op_sig", "op_start", "op_end"), decode_stream=_decode_stream())
         # the rest of B decodes column by column on a side stream as it lands
         # (by then A's attribution and the pairing are done), so only the last
         # column's decode trails the last byte

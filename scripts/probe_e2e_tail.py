@@ -55,3 +55,8 @@ for e in tail:
     agg[k] = agg.get(k, 0) + e["dur"]
 for k, v in sorted(agg.items(), key=lambda kv: -kv[1])[:15]:
     print(f"  {1e-3 * v:7.3f} ms  {k}")
+
+for e in h2d:
+    print(f"  H2D {1e-3 * (e['ts'] - t0):8.2f} ms  dur {1e-3 * e['dur']:7.2f} ms  "
+          f"{e.get('args', {}).get('bytes', 0) / 1e6:9.1f} MB  "
+          f"{e.get('args', {}).get('memory bandwidth (GB/s)', 0)} GB/s")
