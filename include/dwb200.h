@@ -218,6 +218,12 @@ int dw_unpack_deltas_w(const void *d_delta, int32_t delta_bytes, int64_t delta_b
  * timestamps into 1-4 bits each. */
 int dw_unpack_bits(const uint32_t *d_words, int32_t width, int64_t bias, int64_t n, int64_t base, int64_t *d_out,
                    void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
+/* Both in one pass: starts from bit-packed deltas as dw_unpack_bits, and
+ * (d_dur_words non-NULL) d_end[i] = d_out[i] + dur_bias + duration field i,
+ * as dw_unpack_bits_dur. */
+int dw_unpack_bits_w(const uint32_t *d_words, int32_t width, int64_t bias, int64_t n, int64_t base, int64_t *d_out,
+                     const uint32_t *d_dur_words, int32_t dur_width, int64_t dur_bias, int64_t *d_end,
+                     void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
 /* Interval ends from bit-packed durations: d_end[i] = d_start[i] + bias +
  * field i (same field layout as dw_unpack_bits; field 0 counts). */
 int dw_unpack_bits_dur(const int64_t *d_start, const uint32_t *d_words, int32_t width, int64_t bias, int64_t n,

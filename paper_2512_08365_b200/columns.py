@@ -409,14 +409,15 @@ class PackedColumns(TraceColumns):
             out = torch.empty(n, dtype=torch.int64, device=dev)
             ws = _native.Workspace.get(L.dw_unpack_workspace_size(n))
             w, b = self.iv_bits[base_name]
-            _native.check(L.dw_unpack_bits(_native.ptr(delta), w, b, n, base, _native.ptr(out), ws.data_ptr(),
-                                           ws.numel(), _native.stream_handle()), "dw_unpack_bits")
-            self._dev[(base_name, dev.index)] = out
+            wd, bd = self.iv_bits[dur_name] if end is not None else (1, 0)
             if end is not None:
                 end = torch.empty(n, dtype=torch.int64, device=dev)
-                wd, bd = self.iv_bits[dur_name]
-                _native.check(L.dw_unpack_bits_dur(_native.ptr(out), _native.ptr(dur), wd, bd, n, _native.ptr(end),
-                                                   _native.stream_handle()), "dw_unpack_bits_dur")
+            # starts and ends in one pass
+            _native.check(L.dw_unpack_bits_w(_native.ptr(delta), w, b, n, base, _native.ptr(out),
+                                             _native.ptr(dur) if end is not None else None, wd, bd, _native.ptr(end),
+                                             ws.data_ptr(), ws.numel(), _native.stream_handle()), "dw_unpack_bits_w")
+            self._dev[(base_name, dev.index)] = out
+            if end is not None:
                 self._dev[(dur_name, dev.index)] = end
             return self._dev[key]
         n = int(delta.numel())

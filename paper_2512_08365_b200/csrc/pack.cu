@@ -5,11 +5,9 @@
 // timestamp columns as 32-bit deltas and its interval ends as 32-bit
 // durations: ts 8 -> 4 bytes per sample, intervals 16 -> 8 bytes.  The
 // host->HBM copy is what bounds the end-to-end path (PCIe), so this cuts the
-// bytes that cross it by ~30 %; the decode here is one CUB scan per column
-// (HBM-bound) plus a fused start + duration pass.
-#include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
-#include <thrust/iterator/transform_iterator.h>
+// bytes that cross it by ~30 %; the decode here is one reduce-then-scan per
+// column (HBM-bound: the packed fields are read twice, the int64 column
+// written once) with the interval ends written by the same pass.
 
 #include "dw_common.cuh"
 
@@ -59,39 +57,119 @@ __global__ void add_duration_kernel(const int64_t *start, const T *dur, int64_t 
         end[i] = __ldcs(start + i) + (int64_t)__ldcs(dur + i);
 }
 
+// ---- delta-column scan: out[i] = V(0) + ... + V(i), V = DeltaAt / BitsAt,
+// optionally end[i] = out[i] + E(i).  Three passes over blocks of US_B
+// elements: the block sums of V, their exclusive scan (rep_scan_kernel, one
+// block), then each block again -- V in registers (US_I consecutive
+// elements per thread), the thread and block prefixes, the results through a
+// padded shared-memory tile so the int64 stores are coalesced.
+constexpr int US_T = 256, US_I = 16, US_B = US_T * US_I;
+
+struct NoEnd {
+    __device__ int64_t operator()(int64_t) const { return 0; }
+};
 template <typename T>
-static size_t scan_bytes_t(int64_t n) {
-    size_t b = 0;
-    auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), DeltaAt<T>{nullptr, 0, 0});
-    cub::DeviceScan::InclusiveSum(nullptr, b, it, (int64_t *)nullptr, (int)std::max<int64_t>(n, 1));
-    return b;
-}
-static size_t scan_bytes_bits(int64_t n) {
-    size_t b = 0;
-    auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), BitsAt{nullptr, 1, 0, 0});
-    cub::DeviceScan::InclusiveSum(nullptr, b, it, (int64_t *)nullptr, (int)std::max<int64_t>(n, 1));
-    return b;
+struct DurAt {  // interval end = start + d[i]
+    const T *d;
+    __device__ int64_t operator()(int64_t i) const { return (int64_t)d[i]; }
+};
+struct BitsDurAt {  // interval end = start + bias + field i (field 0 counts)
+    const uint32_t *w;
+    int width;
+    int64_t bias;
+    __device__ int64_t operator()(int64_t i) const {
+        const int64_t bit = i * (int64_t)width;
+        const int64_t k = bit >> 5;
+        const uint64_t win = (uint64_t)__ldg(w + k) | ((uint64_t)__ldg(w + k + 1) << 32);
+        return bias + (int64_t)((win >> (bit & 31)) & ((1ULL << width) - 1ULL));
+    }
+};
+
+__device__ __forceinline__ int64_t block_sum_i64(int64_t v, int64_t *ws) {  // US_T threads
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int64_t t = 0;
+#pragma unroll
+    for (int w = 0; w < US_T / 32; ++w) t += ws[w];
+    return t;
 }
 
-static size_t scan_bytes(int64_t n) {
-    return std::max(std::max(std::max(scan_bytes_t<uint32_t>(n), scan_bytes_t<uint16_t>(n)), scan_bytes_t<int8_t>(n)),
-                    scan_bytes_bits(n));
+// (both passes persistent: a few resident blocks per SM walk the chunks)
+template <typename V>
+__global__ void __launch_bounds__(US_T) us_sum_kernel(V val, int64_t n, int64_t nb, unsigned long long *bsum) {
+    __shared__ int64_t ws[2][US_T / 32];
+    int par = 0;
+    for (int64_t b = blockIdx.x; b < nb; b += gridDim.x, par ^= 1) {
+        const int64_t i0 = b * (int64_t)US_B;
+        int64_t s = 0;
+#pragma unroll 4
+        for (int k = threadIdx.x; k < US_B; k += US_T)  // striped: coalesced field reads
+            if (i0 + k < n) s += val(i0 + k);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if ((threadIdx.x & 31) == 0) ws[par][threadIdx.x >> 5] = s;
+        __syncthreads();  // (double-buffered: one barrier per chunk)
+        if (threadIdx.x == 0) {
+            int64_t t = 0;
+#pragma unroll
+            for (int w = 0; w < US_T / 32; ++w) t += ws[par][w];
+            bsum[b] = (unsigned long long)t;
+        }
+    }
 }
 
-template <typename T>
-static void scan_deltas(const void *delta, int64_t n, int64_t base, int64_t bias, int64_t *out, void *ws,
-                        size_t bytes, cudaStream_t s) {
-    auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
-                                              DeltaAt<T>{(const T *)delta, base, bias});
-    cub::DeviceScan::InclusiveSum(ws, bytes, it, out, (int)n, s);
-    count_launch(2);
+template <typename V, typename E>
+__global__ void __launch_bounds__(US_T) us_write_kernel(V val, E endv, int64_t n, int64_t nb,
+                                                        const unsigned long long *bpre, int64_t *out, int64_t *end) {
+    __shared__ int64_t tile[US_B + US_B / US_I];  // one pad per thread row: conflict-free 8-byte access
+    __shared__ int64_t wt[US_T / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int64_t i0 = b * (int64_t)US_B;
+    const int64_t r0 = i0 + (int64_t)threadIdx.x * US_I;  // this thread's first element
+    int64_t x[US_I];
+    int64_t run = 0;
+#pragma unroll
+    for (int j = 0; j < US_I; ++j) {
+        run += r0 + j < n ? val(r0 + j) : 0;
+        x[j] = run;
+    }
+    int64_t inc = run;  // block-exclusive prefix of the thread totals
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) wt[warp] = inc;
+    __syncthreads();
+    int64_t pre = (int64_t)bpre[b] + inc - run;
+    for (int w = 0; w < warp; ++w) pre += wt[w];
+    int64_t *row = tile + threadIdx.x * (US_I + 1);
+#pragma unroll
+    for (int j = 0; j < US_I; ++j) row[j] = pre + x[j];
+    __syncthreads();
+    for (int k = threadIdx.x; k < US_B; k += US_T) {
+        const int64_t i = i0 + k;
+        if (i >= n) break;
+        const int64_t v = tile[k + k / US_I];
+        __stcs(out + i, v);
+        if (end) __stcs(end + i, v + endv(i));
+    }
+    __syncthreads();  // the tile and wt are reused by the next chunk
+    }
 }
 
-template <typename T>
-static void add_durations(const int64_t *start, const void *dur, int64_t n, int64_t *end, cudaStream_t s) {
-    add_duration_kernel<T><<<(unsigned)std::min<int64_t>(num_sms() * 8, ceil_div(n, 256)), 256, 0, s>>>(
-        start, (const T *)dur, n, end);
-    count_launch();
+__global__ void __launch_bounds__(1024) rep_scan_kernel(unsigned long long *bsum, int64_t nb);
+
+template <typename V, typename E>
+static void unpack_scan(V val, E endv, int64_t n, int64_t *out, int64_t *end, void *ws, cudaStream_t s) {
+    const int64_t nb = ceil_div(n, US_B);
+    unsigned long long *bsum = (unsigned long long *)ws;
+    const unsigned grid = (unsigned)nb;  // one chunk per block (measured: persistent blocks are slower here)
+    us_sum_kernel<V><<<grid, US_T, 0, s>>>(val, n, nb, bsum);
+    rep_scan_kernel<<<1, 1024, 0, s>>>(bsum, nb);
+    us_write_kernel<V, E><<<grid, US_T, 0, s>>>(val, endv, n, nb, bsum, out, end);
+    count_launch(3);
 }
 
 // 9-significant-digit decimals (the trace format's on-disk precision,
@@ -168,17 +246,24 @@ __global__ void __launch_bounds__(256) rep_count_kernel(const uint32_t *rep, int
     }
 }
 
-// exclusive scan of nb block counts, in place (one block of 1024 threads)
+// exclusive scan of nb block counts, in place (one block of 1024 threads, 8
+// consecutive counts per thread per round)
 __global__ void __launch_bounds__(1024) rep_scan_kernel(unsigned long long *bsum, int64_t nb) {
+    constexpr int PER = 8, ROUND = 1024 * PER;
     __shared__ unsigned long long wt[32];
     __shared__ unsigned long long carry;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    for (int64_t c0 = 0; c0 < nb; c0 += 1024) {
-        const int64_t i = c0 + threadIdx.x;
-        const unsigned long long v = i < nb ? bsum[i] : 0;
-        unsigned long long x = v;
+    for (int64_t c0 = 0; c0 < nb; c0 += ROUND) {
+        const int64_t i = c0 + (int64_t)threadIdx.x * PER;
+        unsigned long long v[PER], t = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            v[j] = i + j < nb ? bsum[i + j] : 0;
+            t += v[j];
+        }
+        unsigned long long x = t;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
@@ -186,11 +271,15 @@ __global__ void __launch_bounds__(1024) rep_scan_kernel(unsigned long long *bsum
         }
         if (lane == 31) wt[warp] = x;
         __syncthreads();
-        unsigned long long off = carry;
+        unsigned long long off = carry + x - t;
         for (int w = 0; w < warp; ++w) off += wt[w];
-        if (i < nb) bsum[i] = off + x - v;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            if (i + j < nb) bsum[i + j] = off;
+            off += v[j];
+        }
         __syncthreads();
-        if (threadIdx.x == 1023) carry = off + x;
+        if (threadIdx.x == 1023) carry = off;
         __syncthreads();
     }
 }
@@ -235,7 +324,7 @@ using namespace dw;
 
 extern "C" {
 
-size_t dw_unpack_workspace_size(int64_t n) { return scan_bytes(n) + 256; }
+size_t dw_unpack_workspace_size(int64_t n) { return 8 * (size_t)(ceil_div(std::max<int64_t>(n, 1), US_B) + 1) + 256; }
 
 int dw_unpack_deltas_w(const void *d_delta, int32_t delta_bytes, int64_t delta_bias, int64_t n, int64_t base,
                        int64_t *d_out, const void *d_dur, int32_t dur_bytes, int64_t *d_end, void *d_workspace,
@@ -247,14 +336,14 @@ int dw_unpack_deltas_w(const void *d_delta, int32_t delta_bytes, int64_t delta_b
     if (n == 0) return DW_OK;
     if (!d_workspace || workspace_bytes < dw_unpack_workspace_size(n)) return DW_E_WORKSPACE;
     cudaStream_t s = (cudaStream_t)stream;
-    if (delta_bytes == 1) scan_deltas<int8_t>(d_delta, n, base, delta_bias, d_out, d_workspace, workspace_bytes, s);
-    else if (delta_bytes == 2)
-        scan_deltas<uint16_t>(d_delta, n, base, delta_bias, d_out, d_workspace, workspace_bytes, s);
-    else scan_deltas<uint32_t>(d_delta, n, base, delta_bias, d_out, d_workspace, workspace_bytes, s);
-    if (d_dur) {
-        if (dur_bytes == 2) add_durations<uint16_t>(d_out, d_dur, n, d_end, s);
-        else add_durations<uint32_t>(d_out, d_dur, n, d_end, s);
-    }
+    auto go = [&](auto val) {
+        if (!d_dur) unpack_scan(val, NoEnd{}, n, d_out, nullptr, d_workspace, s);
+        else if (dur_bytes == 2) unpack_scan(val, DurAt<uint16_t>{(const uint16_t *)d_dur}, n, d_out, d_end, d_workspace, s);
+        else unpack_scan(val, DurAt<uint32_t>{(const uint32_t *)d_dur}, n, d_out, d_end, d_workspace, s);
+    };
+    if (delta_bytes == 1) go(DeltaAt<int8_t>{(const int8_t *)d_delta, base, delta_bias});
+    else if (delta_bytes == 2) go(DeltaAt<uint16_t>{(const uint16_t *)d_delta, base, delta_bias});
+    else go(DeltaAt<uint32_t>{(const uint32_t *)d_delta, base, delta_bias});
     DW_CHECK_LAUNCH();
     return DW_OK;
 }
@@ -264,11 +353,23 @@ int dw_unpack_bits(const uint32_t *d_words, int32_t width, int64_t bias, int64_t
     if (n < 0 || width < 1 || width > 32 || (n && (!d_words || !d_out)) || n >= ((int64_t)1 << 31)) return DW_E_ARG;
     if (n == 0) return DW_OK;
     if (!d_workspace || workspace_bytes < dw_unpack_workspace_size(n)) return DW_E_WORKSPACE;
-    auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0),
-                                              BitsAt{d_words, width, base, bias});
-    size_t b = workspace_bytes;
-    cub::DeviceScan::InclusiveSum(d_workspace, b, it, d_out, (int)n, (cudaStream_t)stream);
-    count_launch(2);
+    unpack_scan(BitsAt{d_words, width, base, bias}, NoEnd{}, n, d_out, nullptr, d_workspace, (cudaStream_t)stream);
+    DW_CHECK_LAUNCH();
+    return DW_OK;
+}
+
+int dw_unpack_bits_w(const uint32_t *d_words, int32_t width, int64_t bias, int64_t n, int64_t base, int64_t *d_out,
+                     const uint32_t *d_dur_words, int32_t dur_width, int64_t dur_bias, int64_t *d_end,
+                     void *d_workspace, size_t workspace_bytes, dw_stream_t stream) {
+    if (!d_dur_words)
+        return dw_unpack_bits(d_words, width, bias, n, base, d_out, d_workspace, workspace_bytes, stream);
+    if (n < 0 || width < 1 || width > 32 || dur_width < 1 || dur_width > 32 || (n && (!d_words || !d_out || !d_end)) ||
+        n >= ((int64_t)1 << 31))
+        return DW_E_ARG;
+    if (n == 0) return DW_OK;
+    if (!d_workspace || workspace_bytes < dw_unpack_workspace_size(n)) return DW_E_WORKSPACE;
+    unpack_scan(BitsAt{d_words, width, base, bias}, BitsDurAt{d_dur_words, dur_width, dur_bias}, n, d_out, d_end,
+                d_workspace, (cudaStream_t)stream);
     DW_CHECK_LAUNCH();
     return DW_OK;
 }
