@@ -815,12 +815,17 @@ def _begin_ledger(trace, method="ground_truth", period_us=DEFAULT_SAMPLER_PERIOD
 
 def _finish_ledger(method, cols, signal, span, overlap, launched):
     per_op, per_k, pending = launched
+    if overlap == "split":
+        # checked and split now, not when the ledger is read: the split
+        # integrals queued early overlap whatever the caller does next
+        st = pending.result()
+        _raise_ledger_errors(cols, st, span)
+        led = _split_ledger(method, cols, signal, st)
+        return lambda: led
 
     def finish() -> EnergyLedger:
         st = pending.result()
         _raise_ledger_errors(cols, st, span)
-        if overlap == "split":
-            return _split_ledger(method, cols, signal, st)
         return EnergyLedger(method=method, per_kernel=JoulesView(cols.k_ids, per_k, "k"),
                             per_operator=JoulesView(cols.op_ids, per_op, "op"),
                             idle_joules=float(st.totals[2]), total_joules=float(st.totals[0]),

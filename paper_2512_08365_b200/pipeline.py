@@ -39,6 +39,14 @@ def _decode_stream() -> "torch.cuda.Stream":
     return _DECODE_STREAMS[dev]
 
 
+def _ledger_errors_first(*pending) -> None:
+    """A ledger's data error outranks a pairing error, as when each ledger
+    was built (and checked) before the pairing started: raise it if any."""
+    for f in pending:
+        if f is not None:
+            f()
+
+
 def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAULT_THRESHOLD,
             k: int = 100, *, lean: bool = True, copy_stream: "torch.cuda.Stream | None" = None,
             summation: str = "exact", overlap: str = "compat") -> Analysis:
@@ -84,12 +92,17 @@ def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAUL
     # both ledgers and the pairing queue before the host waits on any of
     # them (build_ledger's status read deferred; errors raised A first)
     fa = _begin_ledger(ca, method=method, summation=summation, overlap=overlap)
-    if copy_stream is not None:
-        torch.cuda.current_stream().wait_event(sig_ready)
-        prep = join_prepare(ca, cb)
-    fb = _begin_ledger(cb, method=method, summation=summation, overlap=overlap)
-    if prep is None:
-        prep = join_prepare(ca, cb)
+    fb = None
+    try:
+        if copy_stream is not None:
+            torch.cuda.current_stream().wait_event(sig_ready)
+            prep = join_prepare(ca, cb)
+        fb = _begin_ledger(cb, method=method, summation=summation, overlap=overlap)
+        if prep is None:
+            prep = join_prepare(ca, cb)
+    except Exception:
+        _ledger_errors_first(fa, fb)
+        raise
     la, lb = fa(), fb()
     jd = join_diff(ca, cb, la, lb, threshold, k, full_columns=not lean, epw=not lean, prep=prep,
                    columns=FindingColumns.DELTAS if lean else None)
@@ -155,7 +168,11 @@ def analyze_corpus(pairs, method: str = "samples", threshold: float = DEFAULT_TH
         ca, cb = TraceColumns.from_trace(a), TraceColumns.from_trace(b)
         fa = _begin_ledger(ca, method=method, summation=summation)
         fb = _begin_ledger(cb, method=method, summation=summation)
-        prep = join_prepare(ca, cb)
+        try:
+            prep = join_prepare(ca, cb)
+        except Exception:
+            _ledger_errors_first(fa, fb)
+            raise
         la, lb = fa(), fb()
         jd = join_diff(ca, cb, la, lb, threshold, k, full_columns=False, epw=False,
                        columns=FindingColumns.DELTAS, ranked=False, prep=prep)

@@ -381,3 +381,24 @@ def test_mean_power_matches_reference_rule():
     for lo, hi in ((int(ts[10]) + 3, int(ts[400]) - 1), (int(ts[0]), int(ts[-1]))):
         j = oracle.integrate_linear(ts, w, [lo], [hi], oracle.MODE_DEVICE)[0]
         assert E.mean_power(lin, (lo, hi)) == j * 1e6 / (hi - lo)
+
+
+def test_analyze_raises_ledger_errors_first():
+    """pipeline.analyze launches both ledgers and the pairing before it reads
+    any ledger status: a data error still comes from trace A before trace B,
+    and before the pairing's own errors (no signatures here)."""
+    from paper_2512_08365_b200.pipeline import analyze
+    ts = np.array([100, 200, 300], dtype=np.int64)
+    w = np.array([10.0, 20.0, 30.0])
+
+    def cols(k_start):
+        return TraceColumns.from_arrays(ts, w, np.array([100, 150, 250]), np.array([140, 260, 290]),
+                                        np.array(k_start), np.array([120, 160, 280]),
+                                        np.array([0, 1, 2], dtype=np.int32), trace_end=300)
+    good, bad_a, bad_b = cols([110, 150, 255]), cols([110, 90, 255]), cols([110, 150, 20])
+    with pytest.raises(SignalError, match=r"interval \[90,160\]"):
+        analyze(bad_a, bad_b)
+    with pytest.raises(SignalError, match=r"interval \[20,280\]"):
+        analyze(good, bad_b)
+    with pytest.raises(ValueError, match="signatures"):
+        analyze(good, good)
