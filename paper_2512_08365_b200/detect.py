@@ -329,17 +329,19 @@ def _host_keys(findings) -> tuple[np.ndarray, np.ndarray]:
 
 
 def rank_order(key_hi: torch.Tensor, key_lo: Optional[torch.Tensor], k: int, tie_rank=None,
-               n_a: int = 0):
+               n_a: int = 0, summary: Optional[torch.Tensor] = None):
     """Indices of the k best findings (report order) and the device summary
     {n_waste, wasted_joules (exact sum), P} -- dw_rank.  Without key_lo the low
-    key follows the join numbering (tie_rank / n_a)."""
+    key follows the join numbering (tie_rank / n_a).  ``summary``: a zeroed
+    f64 [4] device tensor to write it into (else one is allocated)."""
     dev = _native.device()
     P = int(key_hi.numel())
     L = _native.lib()
     nbytes = L.dw_rank_workspace_size(P, k)
     ws = _native.Workspace.get(nbytes)
     order = torch.empty(max(k, 1), dtype=torch.int64, device=dev)
-    summary = torch.zeros(4, dtype=torch.float64, device=dev)
+    if summary is None:
+        summary = torch.zeros(4, dtype=torch.float64, device=dev)
     fs = _native.Findings(None, None, None, None, None, None, None, None, None,
                           _native.ptr(key_hi), _native.ptr(key_lo), _native.ptr(tie_rank), int(n_a))
     rc = L.dw_rank(P, ctypes.byref(fs), int(k), _native.ptr(order), _native.ptr(summary),

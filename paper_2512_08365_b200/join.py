@@ -133,6 +133,7 @@ class JoinDiff:
     ja: Optional[torch.Tensor] = None    # operator joules of A / B (for lean columns)
     jb: Optional[torch.Tensor] = None
     threshold: float = DEFAULT_THRESHOLD
+    rows_host: Optional[np.ndarray] = None  # dw_topk_rows of ``order``, read back with the counts
 
     def pair_of(self, f: torch.Tensor):
         """(A op, B op) of findings f (device tensors; -1 on an empty side)."""
@@ -151,15 +152,12 @@ class JoinDiff:
         (dw_topk_rows) and one copy; verdicts on the host with the device's
         rule (judge)."""
         k = int(idx.numel())
-        dev = idx.device
-        out = torch.empty((6, max(k, 1)), dtype=torch.int64, device=dev)
-        p = _native.ptr
-        o = idx.contiguous()
-        _native.check(_native.lib().dw_topk_rows(
-            p(o), k, self.n_a, p(self.match_a), p(self.b_only), p(self.ja), p(self.jb),
-            p(cols_a.device("op_start")), p(cols_a.device("op_end")), p(cols_b.device("op_start")),
-            p(cols_b.device("op_end")), p(out), _native.stream_handle()), "dw_topk_rows")
-        h = out[:, :k].cpu().numpy()
+        if idx is self.order and self.rows_host is not None:
+            h = self.rows_host  # gathered by join_diff right after the rank
+        else:
+            out = torch.empty((6, max(k, 1)), dtype=torch.int64, device=idx.device)
+            _topk_rows(idx, k, self, cols_a, cols_b, out)
+            h = out[:, :k].cpu().numpy()
         ia, ib, la, lb = h[0], h[1], h[2], h[3]
         ea, eb = h[4].view(np.float64), h[5].view(np.float64)
         return self._rows(cols_a, cols_b, classify, trace_a, trace_b, ia, ib, ea, eb, la, lb, None)
@@ -271,6 +269,16 @@ class JoinPrep:
     max_distinct: int
 
 
+def _topk_rows(idx, k, jd, cols_a, cols_b, out) -> None:
+    """dw_topk_rows: the k rows' ops, latencies and joules into out [6, k]."""
+    p = _native.ptr
+    o = idx.contiguous()
+    _native.check(_native.lib().dw_topk_rows(
+        p(o), k, jd.n_a, p(jd.match_a), p(jd.b_only), p(jd.ja), p(jd.jb),
+        p(cols_a.device("op_start")), p(cols_a.device("op_end")), p(cols_b.device("op_start")),
+        p(cols_b.device("op_end")), p(out), _native.stream_handle()), "dw_topk_rows")
+
+
 def _side(cols, trace, joules, work, rank, dev):
     p = _native.ptr
     sig = _sig_tensor(cols, trace, dev)
@@ -342,7 +350,12 @@ def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
     fc = FindingColumns(Pmax, dev, full=full_columns, columns=columns, key_lo=False, tie_rank=rank_a, n_a=na)
     epw_a = torch.empty(Pmax, dtype=torch.float64, device=dev) if epw else None
     epw_b = torch.empty(Pmax, dtype=torch.float64, device=dev) if epw else None
-    count = torch.zeros(4, dtype=torch.int64, device=dev)
+    na_ = na + prep.n_b_only
+    kk = min(k, na_)
+    # one device buffer, one read-back: counts [4], rank summary [4] (f64
+    # bits), and -- lean columns -- the top-k report rows [6, k]
+    hb = torch.empty(8 + 6 * max(kk, 1), dtype=torch.int64, device=dev)
+    count = hb[:4]  # written whole by dw_join_findings
     L = _native.lib()
     fs = fc.c_struct()
     p = _native.ptr
@@ -350,22 +363,29 @@ def join_diff(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
                                      float(threshold), ctypes.byref(fs), p(prep.match_a), p(prep.b_only),
                                      prep.n_b_only, p(epw_a), p(epw_b), p(count), prep.ws.data_ptr(),
                                      prep.ws.numel(), _native.stream_handle(stream)), "dw_join_findings")
-    P = na + prep.n_b_only  # the counts are read back with the rank's summary (one transfer)
-    kk = min(k, P)
+    P = na_
+    jd = JoinDiff(P=P, n_a=na, n_matched=0, n_a_only=0, n_b_only=prep.n_b_only, columns=fc,
+                  match_a=prep.match_a[:na], b_only=prep.b_only[:prep.n_b_only], epw_a=epw_a, epw_b=epw_b,
+                  order=None, n_waste=0, wasted_joules=0.0, ja=keep[0], jb=keep[6], threshold=float(threshold))
+    lean = fc.ratio is None and fc.energy_a is None and fc.latency_a is None
     if ranked:
-        order, summary = rank_order(fc.key_hi[:P], None, kk, tie_rank=rank_a, n_a=na)
-        both = torch.cat([count, summary.reshape(-1).view(torch.int64)]).cpu()
-        cnt, sm = both[:4].tolist(), both[4:].view(torch.float64).tolist()
+        summary = hb[4:8].view(torch.float64)
+        summary.zero_()
+        jd.order, _ = rank_order(fc.key_hi[:P], None, kk, tie_rank=rank_a, n_a=na, summary=summary)
+        if lean and kk:
+            _topk_rows(jd.order, kk, jd, ca, cb, hb[8:].view(6, kk))
+        h = hb.cpu().numpy()
+        sm = h[4:8].view(np.float64)
+        jd.n_waste, jd.wasted_joules = int(sm[0]), float(sm[1])
+        if lean and kk:
+            jd.rows_host = h[8:].reshape(6, kk)
     else:
-        order, sm = None, [0, 0.0]
-        cnt = count.cpu().tolist()
-    P2, matched, a_only, b_only = (int(x) for x in cnt)
-    if P2 != P:
-        raise RuntimeError(f"internal: join counted {P2} findings, expected {P}")
-    return JoinDiff(P=P, n_a=na, n_matched=matched, n_a_only=a_only, n_b_only=b_only, columns=fc,
-                    match_a=prep.match_a[:na], b_only=prep.b_only[:b_only],
-                    epw_a=epw_a, epw_b=epw_b, order=order, n_waste=int(sm[0]),
-                    wasted_joules=float(sm[1]), ja=keep[0], jb=keep[6], threshold=float(threshold))
+        h = hb[:4].cpu().numpy()
+    P2, matched, a_only, b_only = (int(x) for x in h[:4])
+    if P2 != P or b_only != prep.n_b_only:
+        raise RuntimeError(f"internal: join counted {P2} findings ({b_only} B-only), expected {P}")
+    jd.n_matched, jd.n_a_only = matched, a_only
+    return jd
 
 
 def join_report(trace_a, trace_b, ledger_a: EnergyLedger, ledger_b: EnergyLedger,
