@@ -246,13 +246,21 @@ def launch_count(reset: bool = False) -> int:
     return int(lib().dw_launch_count(1 if reset else 0))
 
 
+_DEVICES: dict = {}
+
+
 def device() -> torch.device:
     """The CUDA device the GPU path runs on (current torch device)."""
-    if not torch.cuda.is_available():
-        raise NativeUnavailable("no CUDA device: the dwb200 GPU path cannot run "
-                                "(there is no CPU fallback)")
-    lib()
-    return torch.device("cuda", torch.cuda.current_device())
+    idx = torch.cuda.current_device() if _DEVICES else None
+    d = _DEVICES.get(idx)
+    if d is None:  # first call (or a new device): check once, then cache
+        if not torch.cuda.is_available():
+            raise NativeUnavailable("no CUDA device: the dwb200 GPU path cannot run "
+                                    "(there is no CPU fallback)")
+        lib()
+        idx = torch.cuda.current_device()
+        d = _DEVICES.setdefault(idx, torch.device("cuda", idx))
+    return d
 
 
 def stream_handle(stream=None) -> int:
