@@ -148,7 +148,10 @@ __global__ void status_init_kernel(DevStatus *st) {
 // Every PIDX_STRIDE-th interval start of each set: a ~1 MB index the
 // partition searches first (L2-resident), so each tile boundary costs a
 // handful of DRAM sectors instead of a full-depth search over the starts.
-constexpr int64_t PIDX_STRIDE = 1024;
+#ifndef DW_PIDX_STRIDE
+#define DW_PIDX_STRIDE 1024
+#endif
+constexpr int64_t PIDX_STRIDE = DW_PIDX_STRIDE;
 
 struct PartIndex {
     int64_t *p[DW_MAX_SETS];
