@@ -1892,7 +1892,7 @@ __global__ void __launch_bounds__(SUM_THREADS) fx_sum_kernel(const double *x, in
             v[u] = i < n ? __ldcs(x + i) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) acc += fx_from_double(v[u], FX_JOULE_BITS);
+        for (int u = 0; u < U; ++u) acc += fx_joules(v[u]);
     }
     acc = warp_sum_i128(acc);
     if ((threadIdx.x & 31) == 0) {

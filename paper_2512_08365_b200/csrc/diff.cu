@@ -261,7 +261,10 @@ __global__ void waste_sum_kernel(const uint64_t *khi, int64_t P, unsigned long l
     i128 acc = 0;
     unsigned long long cnt = 0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x * 4 + threadIdx.x; b < P; b += stride) {
+    // block-uniform trip count: every lane of a warp runs every iteration, so
+    // the histogram's warp votes below see full warps
+    for (int64_t bb = blockIdx.x * (int64_t)blockDim.x * 4; bb < P; bb += stride) {
+        const int64_t b = bb + threadIdx.x;
         uint64_t k[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -269,15 +272,25 @@ __global__ void waste_sum_kernel(const uint64_t *khi, int64_t P, unsigned long l
             k[u] = i < P ? khi[i] : 0;
         }
         if (hist) {
+            // the first digit is the waste flag and the top exponent bits: a
+            // warp's keys mostly share one bin, so a warp adds 32 at once
+            // instead of 32 same-address shared atomics
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (b + (int64_t)u * blockDim.x < P) atomicAdd(&h[k[u] >> (64 - HIST_BITS)], 1u);
+            for (int u = 0; u < 4; ++u) {
+                const bool ok = b + (int64_t)u * blockDim.x < P;
+                const unsigned bin = (unsigned)(k[u] >> (64 - HIST_BITS));
+                const unsigned b0 = __shfl_sync(0xffffffffu, bin, 0);
+                if (__all_sync(0xffffffffu, ok && bin == b0)) {
+                    if ((threadIdx.x & 31) == 0) atomicAdd(&h[b0], 32u);
+                } else if (ok) {
+                    atomicAdd(&h[bin], 1u);
+                }
+            }
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             if (k[u] >> 63) {
-                acc += fx_from_double(__longlong_as_double((long long)(k[u] & 0x7FFFFFFFFFFFFFFFULL)),
-                                      FX_JOULE_BITS);
+                acc += fx_joules(__longlong_as_double((long long)(k[u] & 0x7FFFFFFFFFFFFFFFULL)));
                 ++cnt;
             }
         }
@@ -1664,7 +1677,7 @@ __global__ void __launch_bounds__(256) seg_waste_kernel(const SegDesc *segs, uns
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < d.P; i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t k = d.khi[i];
         if (k >> 63) {
-            acc += fx_from_double(__longlong_as_double((long long)(k & 0x7FFFFFFFFFFFFFFFULL)), FX_JOULE_BITS);
+            acc += fx_joules(__longlong_as_double((long long)(k & 0x7FFFFFFFFFFFFFFFULL)));
             ++cnt;
         }
     }

@@ -107,6 +107,17 @@ __device__ __forceinline__ bool q40_fast(double x, long long &q) {
     q = __double2ll_rn(__dmul_rn(x, 1099511627776.0));
     return true;
 }
+// fx_from_double(x, FX_JOULE_BITS) with the int128 shifts only for |x| >= 2^10
+// J: below 0.5 J the scaling by 2^64 is exact and cvt.rni rounds half to even
+// (values under 2^-11 J round to 0 either way); in [0.5, 2^10) J every x is a
+// multiple of 2^-53, so x * 2^53 converts exactly and the shift by 11 is the
+// rest of the scale.
+__device__ __forceinline__ i128 fx_joules(double x) {
+    const double a = fabs(x);
+    if (a < 0.5) return (i128)__double2ll_rn(__dmul_rn(x, 18446744073709551616.0));
+    if (a < 1024.0) return (i128)__double2ll_rn(__dmul_rn(x, 9007199254740992.0)) << 11;
+    return fx_from_double(x, FX_JOULE_BITS);
+}
 __device__ __forceinline__ i128 q40(double x) {
     long long q;
     return q40_fast(x, q) ? (i128)q : q_term(x);

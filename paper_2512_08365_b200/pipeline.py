@@ -70,36 +70,39 @@ def analyze(trace_a, trace_b, method: str = "samples", threshold: float = DEFAUL
     slower on C4 -- 35.4 vs 34.5 ms at 12 reserved SMs, worse with more -- so
     the phases run back to back.)
 
-    With ``copy_stream`` (host-resident inputs): B's host->HBM copy runs on
-    that stream after A's, under A's attribution, B's signature and operator
-    columns first, so the pairing (``join_prepare``) runs while the rest of B
-    is still crossing PCIe, and B's later columns decode on a side stream as
-    each lands; only B's ledger and the findings remain after the last byte."""
+    With ``copy_stream`` (host-resident inputs): A's ledger columns copy
+    first (A's attribution starts as they land), then B's ledger columns on
+    ``copy_stream`` (decoded on a side stream column by column as each lands,
+    so B's attribution starts at B's last ledger byte), and the two signature
+    columns last: B's ledger runs while the signatures cross PCIe, and only
+    the pairing, the findings and the top-k trail the last byte (the pairing
+    is the shorter of the two dependent chains -- with B's power columns last,
+    B's whole ledger would trail it instead)."""
     ca, cb = TraceColumns.from_trace(trace_a), TraceColumns.from_trace(trace_b)
     prep = None
+    sig_ready = ()
     if copy_stream is not None:
-        a_ready = ca.prefetch(torch.cuda.current_stream())
+        led_cols = tuple(n for n in TraceColumns.HOT if n != "op_sig")
+        a_ready = ca.prefetch(torch.cuda.current_stream(), names=led_cols)
         # B's copies queue behind A's transfers (not its decodes): concurrent
         # copies would share PCIe and delay A to the end of the transfer
         copy_stream.wait_event(getattr(ca, "copied", None) or a_ready)
-        # (decoded on the side stream too: a decode queued on the copy stream
-        # would hold B's next transfers behind A's attribution for the SMs)
-        sig_ready = cb.prefetch(copy_stream, names=("op_sig", "op_start", "op_end"), decode_stream=_decode_stream())
-        # the rest of B decodes column by column on a side stream as it lands
-        # (by then A's attribution and the pairing are done), so only the last
-        # column's decode trails the last byte
-        cb.prefetch(copy_stream, names=("ts", "watts", "k_start", "k_end"), decode_stream=_decode_stream())
+        # (decoded on a side stream: a decode queued on the copy stream would
+        # hold the next transfers behind A's attribution for the SMs)
+        b_ready = cb.prefetch(copy_stream, names=led_cols, decode_stream=_decode_stream())
+        sig_ready = (ca.prefetch(copy_stream, names=("op_sig",), decode_stream=_decode_stream()),
+                     cb.prefetch(copy_stream, names=("op_sig",), decode_stream=_decode_stream()))
+        # each ledger waits for its own columns only, not for the signatures
+        ca._dev["__ready__"], cb._dev["__ready__"] = a_ready, b_ready
     # both ledgers and the pairing queue before the host waits on any of
     # them (build_ledger's status read deferred; errors raised A first)
     fa = _begin_ledger(ca, method=method, summation=summation, overlap=overlap)
     fb = None
     try:
-        if copy_stream is not None:
-            torch.cuda.current_stream().wait_event(sig_ready)
-            prep = join_prepare(ca, cb)
         fb = _begin_ledger(cb, method=method, summation=summation, overlap=overlap)
-        if prep is None:
-            prep = join_prepare(ca, cb)
+        for ev in sig_ready:
+            torch.cuda.current_stream().wait_event(ev)
+        prep = join_prepare(ca, cb)
     except Exception:
         _ledger_errors_first(fa, fb)
         raise
