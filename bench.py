@@ -453,7 +453,7 @@ def run_ours(args, rank: int, world: int, local: int):
                                pin(pc.op_end), pc.k_start_base, pin(pc.k_start), pin(pc.k_end), c.trace_end,
                                op_sig=pin(pc.op_sig), watts_p0=pc.watts_p0, ts_bias=pc.ts_bias,
                                op_sig_dict=pin(pc.op_sig_dict) if pc.op_sig_dict is not None else None,
-                               ts_bits=pc.ts_bits, n_power=pc.n_power,
+                               ts_bits=pc.ts_bits, ts_step=pc.ts_step, n_power=pc.n_power,
                                ts_last=pc._ts_last if pc.ts_bits is not None else None,
                                iv_bits=pc.iv_bits, n_ops=pc.n_ops, n_kernels=pc.n_kernels,
                                sig_bits=pc.sig_bits,
@@ -470,7 +470,8 @@ def run_ours(args, rank: int, world: int, local: int):
             if a in pc0.iv_bits:
                 return f"{pc0.iv_bits[a][0]}/{pc0.iv_bits[b][0]}-bit packed"
             return f"u{8 * getattr(pc0, a).element_size()}/u{8 * getattr(pc0, b).element_size()}"
-        host_format = (f"packed columns: ts deltas {tsf}, interval deltas/durations "
+        tsk = "residuals from the clock's line" if pc0.ts_step is not None else "deltas"
+        host_format = (f"packed columns: ts {tsk} {tsf}, interval deltas/durations "
                        f"{ivf('op_start', 'op_end')} (ops) {ivf('k_start', 'k_end')} (kernels), watts "
                        + (("run-coded 9-digit decimal codes (change bitmap + u32 code per change, "
                            f"{pc0.watts.numel() / pc0.n_power:.3f} codes/sample)" if pc0.watts_rep is not None

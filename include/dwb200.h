@@ -218,6 +218,15 @@ int dw_unpack_deltas_w(const void *d_delta, int32_t delta_bytes, int64_t delta_b
  * timestamps into 1-4 bits each. */
 int dw_unpack_bits(const uint32_t *d_words, int32_t width, int64_t bias, int64_t n, int64_t base, int64_t *d_out,
                    void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
+/* Timestamps of a clock with a nominal period (power meters polled at a
+ * fixed rate, trace_model.py:63-65's power records), stored as residuals from
+ * the linear predictor pred(i) = base + floor(i * step_fx / 2^32) (step_fx:
+ * the period in 2^-32 us, < 2^63): field i (dw_unpack_bits layout; field 0
+ * counts) holds ts[i] - pred(i) - bias, and d_out[i] = pred(i) + bias + field
+ * i -- one independent decode per element (no scan).  A jittered clock's
+ * residuals span half its deltas' range: one bit fewer per sample.  n < 2^31. */
+int dw_unpack_grid(const uint32_t *d_words, int32_t width, int64_t bias, int64_t n, int64_t base, uint64_t step_fx,
+                   int64_t *d_out, dw_stream_t stream);
 /* Both in one pass: starts from bit-packed deltas as dw_unpack_bits, and
  * (d_dur_words non-NULL) d_end[i] = d_out[i] + dur_bias + duration field i,
  * as dw_unpack_bits_dur. */

@@ -42,7 +42,7 @@ EXPORTED = (
     "dw_attribute_split_workspace_size", "dw_attribute_split", "dw_attribute_window", "dw_fx_sum_exact", "dw_replay",
     "dw_unpack_workspace_size", "dw_unpack_deltas", "dw_unpack_deltas_w", "dw_unpack_decimal",
     "dw_unpack_decimal_rep_workspace_size", "dw_unpack_decimal_rep",
-    "dw_unpack_dict", "dw_unpack_bits", "dw_unpack_bits_w", "dw_unpack_bits_dur", "dw_unpack_dict_bits",
+    "dw_unpack_dict", "dw_unpack_grid", "dw_unpack_bits", "dw_unpack_bits_w", "dw_unpack_bits_dur", "dw_unpack_dict_bits",
     "dw_join_prepare", "dw_join_findings",
     "dw_set_attribute_sms", "dw_ig_nl_count", "dw_ig_nl_write", "dw_ig_classify", "dw_ig_parse_power",
     "dw_ig_parse_op", "dw_ig_parse_kernel", "dw_ig_hash", "dw_ig_id_words", "dw_ig_kernel_lists",
@@ -162,6 +162,7 @@ def lib():
         L.dw_unpack_dict.argtypes = [c_vp, c_vp, c_i32, c_i64, c_vp, c_vp]
         L.dw_unpack_bits.argtypes = [c_vp, c_i32, c_i64, c_i64, c_i64, c_vp, c_vp, ctypes.c_size_t, c_vp]
         L.dw_unpack_bits_dur.argtypes = [c_vp, c_vp, c_i32, c_i64, c_i64, c_vp, c_vp]
+        L.dw_unpack_grid.argtypes = [c_vp, c_i32, c_i64, c_i64, c_i64, ctypes.c_uint64, c_vp, c_vp]
         L.dw_unpack_bits_w.argtypes = [c_vp, c_i32, c_i64, c_i64, c_i64, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp,
                                        ctypes.c_size_t, c_vp]
         L.dw_unpack_dict_bits.argtypes = [c_vp, c_vp, c_i32, c_i64, c_vp, c_vp]

@@ -262,7 +262,7 @@ class PackedColumns(TraceColumns):
     def __init__(self, ts_base, ts_delta, watts, op_base, op_delta, op_dur, k_base, k_delta, k_dur,
                  trace_end, k_op=None, op_sig=None, watts_p0=None, ts_bias=0, op_sig_dict=None,
                  ts_bits=None, n_power=None, ts_last=None, iv_bits=None, n_ops=None, n_kernels=None,
-                 sig_bits=None, watts_rep=None, **kw):
+                 sig_bits=None, watts_rep=None, ts_step=None, **kw):
         super().__init__(ts=ts_delta, watts=watts, trace_end=int(trace_end), op_start=op_delta, op_end=op_dur,
                          k_start=k_delta, k_end=k_dur, k_op=k_op, op_sig=op_sig, ops_sorted=True,
                          kernels_sorted=True, **kw)
@@ -276,6 +276,11 @@ class PackedColumns(TraceColumns):
         self.ts_bias = int(ts_bias)          # int8 / bit-packed ts deltas: delta = ts_bias + code
         self.op_sig_dict = op_sig_dict       # op_sig holds u16/u32 codes into this u64 dictionary
         self.ts_bits = None if ts_bits is None else int(ts_bits)  # ts holds bit-packed 32-bit words
+        # grid-coded timestamps (ts_bits set): fields are residuals from
+        # ts_base + floor(i * ts_step / 2^32) instead of deltas (dw_unpack_grid)
+        self.ts_step = None if ts_step is None else int(ts_step)
+        if self.ts_step is not None and self.ts_bits is None:
+            raise ValueError("grid-coded timestamps are bit-packed (ts_bits)")
         if self.ts_bits is not None:
             self._n_power, self._ts_last = int(n_power), int(ts_last)
             self._dev["first_last"] = (self.ts_base, self._ts_last)
@@ -400,8 +405,12 @@ class PackedColumns(TraceColumns):
             n = self._n_power
             out = torch.empty(n, dtype=torch.int64, device=dev)
             ws = _native.Workspace.get(L.dw_unpack_workspace_size(n))
-            _native.check(L.dw_unpack_bits(_native.ptr(delta), self.ts_bits, bias, n, base, _native.ptr(out),
-                                           ws.data_ptr(), ws.numel(), _native.stream_handle()), "dw_unpack_bits")
+            if self.ts_step is not None:
+                _native.check(L.dw_unpack_grid(_native.ptr(delta), self.ts_bits, bias, n, base, self.ts_step,
+                                               _native.ptr(out), _native.stream_handle()), "dw_unpack_grid")
+            else:
+                _native.check(L.dw_unpack_bits(_native.ptr(delta), self.ts_bits, bias, n, base, _native.ptr(out),
+                                               ws.data_ptr(), ws.numel(), _native.stream_handle()), "dw_unpack_bits")
             self._dev[("ts", dev.index)] = out
             return out
         if base_name in self.iv_bits:
@@ -599,6 +608,35 @@ def _bitpack(x, max_width: int = 8):
     return base, packed[0], packed[1], packed[2]
 
 
+def _gridpack(x, max_width: int):
+    """(base, bias, width, words, step_fx) of a sorted column as residuals
+    from the line through its first and last values (a clock with a nominal
+    period: a jittered clock's residuals span half its deltas' range), in at
+    most max_width bits, else None.  Decoded by dw_unpack_grid."""
+    is_t = isinstance(x, torch.Tensor)
+    n = int(x.shape[0])
+    if n < 3 or n >= (1 << 31) or max_width < 1:
+        return None
+    base = int(x[0].item()) if is_t else int(np.asarray(x)[0])
+    last = int(x[-1].item()) if is_t else int(np.asarray(x)[-1])
+    if last < base:
+        return None
+    step_fx = ((last - base) << 32) // (n - 1)
+    if step_fx >> 63 or (step_fx >> 32) * (n - 1) >= (1 << 62):
+        return None
+    r = x.to(torch.int64).clone() if is_t else np.array(x, dtype=np.int64)
+    C = 1 << 26  # residuals chunk by chunk: no n-long temporaries beyond r
+    for c0 in range(0, n, C):
+        c1 = min(n, c0 + C)
+        i = torch.arange(c0, c1, dtype=torch.int64, device=x.device) if is_t else np.arange(c0, c1, dtype=np.int64)
+        r[c0:c1] -= base + i * (step_fx >> 32) + ((i * (step_fx & 0xFFFFFFFF)) >> 32)
+    packed = _bitfields(r, max_width)
+    del r
+    if packed is None:
+        return None
+    return base, packed[0], packed[1], packed[2], step_fx
+
+
 def _sig_dict(sig):
     """(dictionary u64, codes u16/u32) of the signature column when it has at
     most 2^32 distinct values (it has ~1e6 at C4), else None."""
@@ -716,17 +754,25 @@ def rep_code(code):
     return words, code[new]
 
 
-def pack(cols: TraceColumns, decimal: bool = True, runs: bool = True) -> PackedColumns:
+def pack(cols: TraceColumns, decimal: bool = True, runs: bool = True, grid_ts: bool = True) -> PackedColumns:
     """Packed form of a trace with sorted power, operator and kernel starts
     (ValueError otherwise -- keep such traces unpacked).  Works on host or
     device columns; the result lives where the input does."""
     bits = _bitpack(cols.ts)
     if bits is not None:
         tb, tbias, twidth, td = bits
-        tlast = int(cols.ts[-1].item()) if isinstance(cols.ts, torch.Tensor) else int(np.asarray(cols.ts)[-1])
+        dwidth = twidth
     else:
         tb, tbias, td = _ts_deltas(cols.ts, "power timestamps")
-        twidth, tlast = None, None
+        twidth = None
+        dwidth = 8 * (td.element_size() if isinstance(td, torch.Tensor) else np.asarray(td).itemsize)
+    tlast = int(cols.ts[-1].item()) if isinstance(cols.ts, torch.Tensor) else int(np.asarray(cols.ts)[-1])
+    grid = _gridpack(cols.ts, dwidth - 1) if grid_ts else None
+    tstep = None
+    if grid is not None:  # residuals from the clock's line: fewer bits than its deltas
+        tb, tbias, twidth, td, tstep = grid
+    elif twidth is None:
+        tlast = None
     ob, od = _deltas(cols.op_start, "operator starts")
     kb, kd = _deltas(cols.k_start, "kernel starts")
     o_dur = _durations(cols.op_start, cols.op_end, "operators")
@@ -766,7 +812,7 @@ def pack(cols: TraceColumns, decimal: bool = True, runs: bool = True) -> PackedC
                          k_op=cols.k_op, op_sig=sig, watts_p0=p0, ts_bias=tbias, op_sig_dict=sig_dict,
                          ts_bits=twidth, n_power=cols.n_power, ts_last=tlast, iv_bits=iv_bits,
                          n_ops=cols.n_ops, n_kernels=cols.n_kernels, sig_bits=sig_bits, watts_rep=watts_rep,
-                         op_ids=cols.op_ids, k_ids=cols.k_ids, op_names=cols.op_names, op_work=cols.op_work,
+                         ts_step=tstep, op_ids=cols.op_ids, k_ids=cols.k_ids, op_names=cols.op_names, op_work=cols.op_work,
                          op_rank=cols.op_rank)
 
 
@@ -794,7 +840,7 @@ def save_packed(cols: TraceColumns, path) -> None:
     meta = {"format": "dwc", "version": 2, "trace_end": pc.trace_end, "ts_base": pc.ts_base,
             "op_base": pc.op_start_base, "k_base": pc.k_start_base, "watts_p0": pc.watts_p0,
             "ts_bias": pc.ts_bias, "ts_bits": pc.ts_bits, "n_power": pc.n_power,
-            "ts_last": pc._ts_last if pc.ts_bits is not None else None,
+            "ts_last": pc._ts_last if pc.ts_bits is not None else None, "ts_step": pc.ts_step,
             "iv_bits": {k: list(v) for k, v in pc.iv_bits.items()}, "n_ops": pc.n_ops, "n_kernels": pc.n_kernels,
             "sig_bits": pc.sig_bits, "watts_rep": pc.watts_rep is not None,
             "columns": {}}
@@ -845,4 +891,5 @@ def load_packed(path, pin: bool = False) -> PackedColumns:
                          op_sig_dict=sig_dict, ts_bits=meta.get("ts_bits"), n_power=meta.get("n_power"),
                          ts_last=meta.get("ts_last"), iv_bits={k: tuple(v) for k, v in meta.get("iv_bits", {}).items()},
                          n_ops=meta.get("n_ops"), n_kernels=meta.get("n_kernels"), sig_bits=meta.get("sig_bits"),
-                         watts_rep=as_signed(cols["watts_rep"]) if meta.get("watts_rep") else None)
+                         watts_rep=as_signed(cols["watts_rep"]) if meta.get("watts_rep") else None,
+                         ts_step=meta.get("ts_step"))

@@ -191,6 +191,23 @@ __global__ void dict_bits_decode_kernel(const uint64_t *dict, const uint32_t *w,
     }
 }
 
+// Timestamps of a clock with a nominal period, as residuals from the linear
+// predictor pred(i) = base + i * step_hi + ((i * step_lo) >> 32) (step =
+// step_hi + step_lo / 2^32 us per sample, fixed point): out[i] = pred(i) +
+// bias + field i.  A map, not a scan: every element decodes on its own.
+__global__ void grid_decode_kernel(const uint32_t *w, int width, int64_t bias, int64_t n, int64_t base,
+                                   uint64_t step_hi, uint64_t step_lo, int64_t *out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const uint64_t mask = (1ULL << width) - 1ULL;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+        const int64_t bit = i * (int64_t)width;
+        const int64_t k = bit >> 5;
+        const uint64_t win = (uint64_t)__ldg(w + k) | ((uint64_t)__ldg(w + k + 1) << 32);
+        const uint64_t pred = (uint64_t)base + (uint64_t)i * step_hi + (((uint64_t)i * step_lo) >> 32);
+        __stcs(out + i, (int64_t)(pred + (uint64_t)bias + ((win >> (bit & 31)) & mask)));
+    }
+}
+
 template <typename T>
 __global__ void dict_decode_kernel(const uint64_t *dict, const T *code, int64_t n, uint64_t *out) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -380,6 +397,22 @@ int dw_unpack_bits_dur(const int64_t *d_start, const uint32_t *d_words, int32_t 
     if (n) {
         add_bits_duration_kernel<<<(unsigned)std::min<int64_t>(num_sms() * 8, ceil_div(n, 256)), 256, 0,
                                    (cudaStream_t)stream>>>(d_start, d_words, width, bias, n, d_end);
+        count_launch();
+    }
+    DW_CHECK_LAUNCH();
+    return DW_OK;
+}
+
+int dw_unpack_grid(const uint32_t *d_words, int32_t width, int64_t bias, int64_t n, int64_t base, uint64_t step_fx,
+                   int64_t *d_out, dw_stream_t stream) {
+    // i * step_lo < 2^63 and i * step_hi < 2^63 need n < 2^31 and step_hi < 2^31
+    if (n < 0 || width < 1 || width > 32 || (n && (!d_words || !d_out)) || n >= ((int64_t)1 << 31) ||
+        (step_fx >> 63))
+        return DW_E_ARG;
+    if (n) {
+        grid_decode_kernel<<<(unsigned)std::min<int64_t>(num_sms() * 8, ceil_div(n, 256)), 256, 0,
+                             (cudaStream_t)stream>>>(d_words, width, bias, n, base, step_fx >> 32,
+                                                     step_fx & 0xFFFFFFFFULL, d_out);
         count_launch();
     }
     DW_CHECK_LAUNCH();

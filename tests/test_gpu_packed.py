@@ -45,7 +45,7 @@ def test_decode_exact_and_ledger_identical(tmp_path):
     from paper_2512_08365_b200.columns import PackedColumns
     bare = [PackedColumns(q.ts_base, q.ts, q.watts, q.op_start_base, q.op_start, q.op_end, q.k_start_base,
                           q.k_start, q.k_end, q.trace_end, op_sig=q.op_sig, watts_p0=q.watts_p0, ts_bias=q.ts_bias,
-                          op_sig_dict=q.op_sig_dict, ts_bits=q.ts_bits, n_power=q.n_power,
+                          op_sig_dict=q.op_sig_dict, ts_bits=q.ts_bits, ts_step=q.ts_step, n_power=q.n_power,
                           ts_last=q._ts_last, iv_bits=q.iv_bits, n_ops=q.n_ops, n_kernels=q.n_kernels,
                           sig_bits=q.sig_bits, watts_rep=q.watts_rep)
             for q in (ha, hb)]
@@ -140,7 +140,7 @@ def test_run_coded_trace_analysis_identical():
         hosts.append(PackedColumns(q.ts_base, pin(q.ts), pin(q.watts), q.op_start_base, pin(q.op_start),
                                    pin(q.op_end), q.k_start_base, pin(q.k_start), pin(q.k_end), q.trace_end,
                                    op_sig=pin(q.op_sig), watts_p0=q.watts_p0, ts_bias=q.ts_bias,
-                                   op_sig_dict=pin(q.op_sig_dict), ts_bits=q.ts_bits, n_power=q.n_power,
+                                   op_sig_dict=pin(q.op_sig_dict), ts_bits=q.ts_bits, ts_step=q.ts_step, n_power=q.n_power,
                                    ts_last=q._ts_last, iv_bits=q.iv_bits, n_ops=q.n_ops, n_kernels=q.n_kernels,
                                    sig_bits=q.sig_bits, watts_rep=pin(q.watts_rep)))
     ra = analyze(a, b, "samples", 0.10, 20)
@@ -151,7 +151,43 @@ def test_run_coded_trace_analysis_identical():
     # a run-coded column without its bitmap is refused, not misread
     bad = PackedColumns(p.ts_base, p.ts, p.watts, p.op_start_base, p.op_start, p.op_end, p.k_start_base, p.k_start,
                         p.k_end, p.trace_end, op_sig=p.op_sig, watts_p0=p.watts_p0, ts_bias=p.ts_bias,
-                        op_sig_dict=p.op_sig_dict, ts_bits=p.ts_bits, n_power=p.n_power, ts_last=p._ts_last,
+                        op_sig_dict=p.op_sig_dict, ts_bits=p.ts_bits, ts_step=p.ts_step, n_power=p.n_power, ts_last=p._ts_last,
                         iv_bits=p.iv_bits, n_ops=p.n_ops, n_kernels=p.n_kernels, sig_bits=p.sig_bits)
     with pytest.raises(ValueError):
         bad.device("watts")
+
+
+@pytest.mark.parametrize("jitter,period,n", [(0.3, 50.0, 300_001), (0.49, 1000.0, 1_000_003), (0.1, 7.3, 3),
+                                             (0.45, 123456.7, 70_000), (0.0, 3.0, 200_000)])
+def test_grid_coded_timestamps_decode_exactly(jitter, period, n):
+    """dw_unpack_grid: residuals from the clock's line (any width the packer
+    picks, fields crossing 32-bit words) decode to the exact timestamps, and
+    pack() picks them only when narrower than the deltas."""
+    from paper_2512_08365_b200.columns import TraceColumns
+    rng = np.random.default_rng(n)
+    x = np.arange(n) + (2 * rng.random(n) - 1) * jitter
+    x[0], x[-1] = 0, n - 1
+    ts = (10**12 + np.floor(x * period)).astype(np.int64)
+    c = TraceColumns.from_arrays(ts, np.full(n, 75.0), ts[:1], ts[:1] + 1)
+    p = pack(c)
+    d = pack(c, grid_ts=False)
+    if p.ts_step is not None:
+        assert p.ts_bits < (d.ts_bits or 8 * np.asarray(d.ts).itemsize)
+    assert np.array_equal(p.device("ts").cpu().numpy(), ts)
+    assert p.signal_span() == c.signal_span()
+
+
+def test_c4_clock_is_grid_coded():
+    """C4's jittered clock (synth._power): grid-coded in one bit fewer than
+    its deltas, and the device packer (torch path) agrees with the host one."""
+    cfg = synth.scaled(synth.CONFIGS["C4"], 50_000)
+    a, _ = synth.make_pair(cfg)
+    p = pack(a)
+    d = pack(a, grid_ts=False)
+    assert p.ts_step is not None and p.ts_bits == d.ts_bits - 1
+    assert torch.equal(p.device("ts"), a.device("ts"))
+    ts_host = a.host("ts")
+    q = pack(type(a).from_arrays(ts_host, a.host("watts"), a.host("op_start")[:1], a.host("op_end")[:1]))
+    assert (q.ts_step, q.ts_bias, q.ts_bits) == (p.ts_step, p.ts_bias, p.ts_bits)
+    assert np.array_equal(np.asarray(q.ts).view(np.uint32), np.asarray(p.ts.cpu() if isinstance(p.ts, torch.Tensor)
+                                                                         else p.ts).view(np.uint32))

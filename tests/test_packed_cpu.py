@@ -181,3 +181,42 @@ def test_run_coded_watts(tmp_path):
     assert q.host_bytes == p.host_bytes < pack(c, runs=False).host_bytes
     # no repeats: plain codes
     assert rep_code(np.arange(1000, dtype=np.uint32)) is None
+
+
+def _ungrid(base, bias, width, words, n, step):
+    i = np.arange(n, dtype=np.int64)
+    return base + i * (step >> 32) + ((i * (step & 0xFFFFFFFF)) >> 32) + bias + _fields(words, width, n)
+
+
+@pytest.mark.parametrize("jitter,period", [(0.3, 50.0), (0.45, 1000.0), (0.1, 7.3), (0.49, 123456.7)])
+def test_grid_coded_clock(tmp_path, jitter, period):
+    """A clock read at nominal instants i * period with up to +-jitter periods
+    of read jitter (synth._power): residuals from the line through the first
+    and last sample need one bit fewer than the deltas, so pack() grid-codes
+    them; the host restatement of dw_unpack_grid and the .dwc round trip give
+    the timestamps back exactly."""
+    rng = np.random.default_rng(int(period))
+    n = 20001
+    x = np.arange(n) + (2 * rng.random(n) - 1) * jitter
+    x[0], x[-1] = 0, n - 1
+    ts = (10**11 + np.floor(x * period)).astype(np.int64)
+    assert (np.diff(ts) > 0).all()
+    st = np.sort(rng.integers(ts[0], ts[-1] - 10, size=40))
+    c = TraceColumns.from_arrays(ts, np.full(n, 75.0), st, st + 5)
+    dpk = pack(c, grid_ts=False)
+    for p in (pack(c), None):
+        if p is None:
+            save_packed(c, tmp_path / "g.dwc")
+            p = load_packed(tmp_path / "g.dwc")
+        assert p.ts_step is not None and p.ts_bits < (dpk.ts_bits or 8 * np.asarray(dpk.ts).itemsize)
+        np.testing.assert_array_equal(_ungrid(p.ts_base, p.ts_bias, p.ts_bits, np.asarray(p.ts), n, p.ts_step), ts)
+        assert p.signal_span() == c.signal_span()
+
+
+def test_grid_not_chosen_for_random_walk_clock():
+    """Deltas with independent noise (a drifting clock): the residuals from
+    the line grow like a random walk, so pack() keeps the delta coding."""
+    rng = np.random.default_rng(3)
+    ts = (10**9 + np.cumsum(160 + rng.integers(-40, 41, size=100_000))).astype(np.int64)
+    p = pack(TraceColumns.from_arrays(ts, np.full(ts.size, 75.0), ts[:1], ts[:1] + 1))
+    assert p.ts_step is None and p.ts_bits == 7
