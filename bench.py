@@ -103,6 +103,18 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self.proc is not None and not self.lines:
+            # a timed region shorter than the polling period: one reading
+            # right at its end (clocks have not dropped yet)
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=10).stdout.strip()
+                if out:
+                    self.lines.append(out.splitlines()[-1].strip())
+                    self.post = True
+            except (OSError, subprocess.SubprocessError):
+                pass
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -125,8 +137,11 @@ class ClockSampler:
             for name, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+               "reasons": sorted(reasons), "samples": len(sm)}
+        if getattr(self, "post", False):
+            out["note"] = "region shorter than the 100 ms polling period: one reading at its end"
+        return out
 
 
 def measured_peak_gbs():

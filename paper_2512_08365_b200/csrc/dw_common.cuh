@@ -115,7 +115,7 @@ __device__ __forceinline__ bool q40_fast(double x, long long &q) {
 __device__ __forceinline__ i128 fx_joules(double x) {
     const double a = fabs(x);
     if (a < 0.5) return (i128)__double2ll_rn(__dmul_rn(x, 18446744073709551616.0));
-    if (a < 1024.0) return (i128)__double2ll_rn(__dmul_rn(x, 9007199254740992.0)) << 11;
+    if (a < 1024.0) return (i128)__double2ll_rn(__dmul_rn(x, 9007199254740992.0)) * 2048;  // (no signed shift)
     return fx_from_double(x, FX_JOULE_BITS);
 }
 __device__ __forceinline__ i128 q40(double x) {
