@@ -156,6 +156,16 @@ class CorpusAnalysis:
         return out
 
 
+_CORPUS_STREAMS: dict = {}
+
+
+def _corpus_stream() -> "torch.cuda.Stream":
+    dev = torch.cuda.current_device()
+    if dev not in _CORPUS_STREAMS:
+        _CORPUS_STREAMS[dev] = torch.cuda.Stream()
+    return _CORPUS_STREAMS[dev]
+
+
 def analyze_corpus(pairs, method: str = "samples", threshold: float = DEFAULT_THRESHOLD, k: int = 100, *,
                    summation: str = "exact") -> CorpusAnalysis:
     """A corpus of trace pairs: per pair, both ledgers and
@@ -167,21 +177,57 @@ def analyze_corpus(pairs, method: str = "samples", threshold: float = DEFAULT_TH
     (detect.py:263-266 per pair).  Each pair's ledgers are released after its
     join; only the finding columns stay on the device."""
     summaries, segs = [], []
-    for a, b in pairs:
-        ca, cb = TraceColumns.from_trace(a), TraceColumns.from_trace(b)
-        fa = _begin_ledger(ca, method=method, summation=summation)
-        fb = _begin_ledger(cb, method=method, summation=summation)
-        try:
-            prep = join_prepare(ca, cb)
-        except Exception:
-            _ledger_errors_first(fa, fb)
-            raise
-        la, lb = fa(), fb()
-        jd = join_diff(ca, cb, la, lb, threshold, k, full_columns=False, epw=False,
-                       columns=FindingColumns.DELTAS, ranked=False, prep=prep)
+    pairs = list(pairs)
+    main = torch.cuda.current_stream()
+    # pairs alternate between two streams, and pair i+1's ledgers are queued
+    # before the host blocks on pair i's join: the device works on one pair
+    # while the host waits on (and sets up) the other -- each pair's own work
+    # stays in order on its stream, and every result equals the serial loop's
+    streams = [main, _corpus_stream()] if len(pairs) > 1 else [main]
+    for st in streams[1:]:
+        st.wait_stream(main)  # inputs made on the caller's stream
+
+    def begin(i):
+        with torch.cuda.stream(streams[i % len(streams)]):
+            ca, cb = TraceColumns.from_trace(pairs[i][0]), TraceColumns.from_trace(pairs[i][1])
+            fa = _begin_ledger(ca, method=method, summation=summation)
+            fb = _begin_ledger(cb, method=method, summation=summation)
+        return [ca, cb, fa, fb, None]
+
+    def prepare(i, cur):
+        with torch.cuda.stream(streams[i % len(streams)]):
+            try:
+                cur[4] = join_prepare(cur[0], cur[1])
+            except Exception:
+                _ledger_errors_first(cur[2], cur[3])
+                raise
+
+    def finish(i, cur):
+        ca, cb, fa, fb, prep = cur
+        with torch.cuda.stream(streams[i % len(streams)]):
+            la, lb = fa(), fb()
+            jd = join_diff(ca, cb, la, lb, threshold, k, full_columns=False, epw=False,
+                           columns=FindingColumns.DELTAS, ranked=False, prep=prep)
         summaries.append(PairSummary(la.total_joules, lb.total_joules, jd, 0, 0.0))
         segs.append((jd.columns.key_hi[:jd.P], None, jd.columns.tie_rank, jd.n_a))
-        del la, lb
+
+    if pairs:
+        cur = begin(0)
+        prepare(0, cur)
+        for i in range(len(pairs)):
+            nxt = None
+            if i + 1 < len(pairs):
+                try:
+                    nxt = begin(i + 1)
+                except Exception:
+                    finish(i, cur)  # pair i's errors first, as a serial loop raises them
+                    raise
+            finish(i, cur)
+            if nxt is not None:
+                prepare(i + 1, nxt)
+            cur = nxt
+    for st in streams[1:]:
+        main.wait_stream(st)
     order, summary = rank_order_segmented(segs, k)
     sm = summary.cpu().numpy()
     for i, ps in enumerate(summaries):
