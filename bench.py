@@ -468,7 +468,7 @@ def run_ours(args, rank: int, world: int, local: int):
                                pin(pc.op_end), pc.k_start_base, pin(pc.k_start), pin(pc.k_end), c.trace_end,
                                op_sig=pin(pc.op_sig), watts_p0=pc.watts_p0, ts_bias=pc.ts_bias,
                                op_sig_dict=pin(pc.op_sig_dict) if pc.op_sig_dict is not None else None,
-                               ts_bits=pc.ts_bits, ts_step=pc.ts_step, n_power=pc.n_power,
+                               ts_bits=pc.ts_bits, ts_step=pc.ts_step, watts_bits=pc.watts_bits, n_power=pc.n_power,
                                ts_last=pc._ts_last if pc.ts_bits is not None else None,
                                iv_bits=pc.iv_bits, n_ops=pc.n_ops, n_kernels=pc.n_kernels,
                                sig_bits=pc.sig_bits,
@@ -488,7 +488,9 @@ def run_ours(args, rank: int, world: int, local: int):
         tsk = "residuals from the clock's line" if pc0.ts_step is not None else "deltas"
         host_format = (f"packed columns: ts {tsk} {tsf}, interval deltas/durations "
                        f"{ivf('op_start', 'op_end')} (ops) {ivf('k_start', 'k_end')} (kernels), watts "
-                       + (("run-coded 9-digit decimal codes (change bitmap + u32 code per change, "
+                       + (("run-coded 9-digit decimal codes (change bitmap + "
+                           + (f"{pc0.watts_bits[0]}-bit" if pc0.watts_bits is not None else "u32")
+                           + " code per change, "
                            f"{pc0.watts.numel() / pc0.n_power:.3f} codes/sample)" if pc0.watts_rep is not None
                            else "9-digit decimal codes u32") if pc0.watts_p0 is not None else "f64")
                        + ((f", sig dictionary + {pc0.sig_bits}-bit codes" if pc0.sig_bits is not None else

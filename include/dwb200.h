@@ -259,6 +259,13 @@ int dw_unpack_decimal(const uint32_t *d_code, int64_t n, int32_t p0, double *d_o
 size_t dw_unpack_decimal_rep_workspace_size(int64_t n);
 int dw_unpack_decimal_rep(const uint32_t *d_code, const uint32_t *d_rep, int64_t n, int32_t p0, double *d_out,
                           void *d_workspace, size_t workspace_bytes, dw_stream_t stream);
+/* The same with the stored codes bit-packed: code k = bias + field k (width
+ * bits, dw_unpack_bits layout; field 0 counts).  The packer strips the
+ * decimal zeros every code shares (p0 lowered to match: integer-milliwatt
+ * NVML readings keep ~20 bits) and packs the spread (C4: 30 instead of 32). */
+int dw_unpack_decimal_rep_bits(const uint32_t *d_words, int32_t width, uint32_t bias, const uint32_t *d_rep, int64_t n,
+                               int32_t p0, double *d_out, void *d_workspace, size_t workspace_bytes,
+                               dw_stream_t stream);
 
 /* JSONL ingestion (paper_2512_08365_b200/ingest.py):
  * byte-level stages over the raw file resident in HBM.  The canonical

@@ -41,7 +41,7 @@ EXPORTED = (
     "dw_attribute_workspace_size", "dw_attribute", "dw_ledger", "dw_status", "dw_status_copy", "dw_status_decode",
     "dw_attribute_split_workspace_size", "dw_attribute_split", "dw_attribute_window", "dw_fx_sum_exact", "dw_replay",
     "dw_unpack_workspace_size", "dw_unpack_deltas", "dw_unpack_deltas_w", "dw_unpack_decimal",
-    "dw_unpack_decimal_rep_workspace_size", "dw_unpack_decimal_rep",
+    "dw_unpack_decimal_rep_workspace_size", "dw_unpack_decimal_rep", "dw_unpack_decimal_rep_bits",
     "dw_unpack_dict", "dw_unpack_grid", "dw_unpack_bits", "dw_unpack_bits_w", "dw_unpack_bits_dur", "dw_unpack_dict_bits",
     "dw_join_prepare", "dw_join_findings",
     "dw_set_attribute_sms", "dw_ig_nl_count", "dw_ig_nl_write", "dw_ig_classify", "dw_ig_parse_power",
@@ -170,6 +170,8 @@ def lib():
         L.dw_unpack_decimal_rep_workspace_size.restype = ctypes.c_size_t
         L.dw_unpack_decimal_rep_workspace_size.argtypes = [c_i64]
         L.dw_unpack_decimal_rep.argtypes = [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, ctypes.c_size_t, c_vp]
+        L.dw_unpack_decimal_rep_bits.argtypes = [c_vp, c_i32, ctypes.c_uint32, c_vp, c_i64, c_i32, c_vp, c_vp,
+                                                 ctypes.c_size_t, c_vp]
         L.dw_replay.argtypes = [ctypes.POINTER(Signal), c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp,
                                 c_vp, c_vp]
         L.dw_tensor_norms.argtypes = [c_vp, c_vp, c_i64, c_vp, c_vp]

@@ -262,7 +262,7 @@ class PackedColumns(TraceColumns):
     def __init__(self, ts_base, ts_delta, watts, op_base, op_delta, op_dur, k_base, k_delta, k_dur,
                  trace_end, k_op=None, op_sig=None, watts_p0=None, ts_bias=0, op_sig_dict=None,
                  ts_bits=None, n_power=None, ts_last=None, iv_bits=None, n_ops=None, n_kernels=None,
-                 sig_bits=None, watts_rep=None, ts_step=None, **kw):
+                 sig_bits=None, watts_rep=None, ts_step=None, watts_bits=None, **kw):
         super().__init__(ts=ts_delta, watts=watts, trace_end=int(trace_end), op_start=op_delta, op_end=op_dur,
                          k_start=k_delta, k_end=k_dur, k_op=k_op, op_sig=op_sig, ops_sorted=True,
                          kernels_sorted=True, **kw)
@@ -273,6 +273,10 @@ class PackedColumns(TraceColumns):
         self.watts_rep = watts_rep
         if watts_rep is not None and self.watts_p0 is None:
             raise ValueError("run-coded watts need decimal codes (watts_p0)")
+        # run-coded watts whose stored codes are bit-packed: (width, bias)
+        self.watts_bits = None if watts_bits is None else (int(watts_bits[0]), int(watts_bits[1]))
+        if self.watts_bits is not None and watts_rep is None:
+            raise ValueError("bit-packed watts codes are run-coded (watts_rep)")
         self.ts_bias = int(ts_bias)          # int8 / bit-packed ts deltas: delta = ts_bias + code
         self.op_sig_dict = op_sig_dict       # op_sig holds u16/u32 codes into this u64 dictionary
         self.ts_bits = None if ts_bits is None else int(ts_bits)  # ts holds bit-packed 32-bit words
@@ -457,9 +461,16 @@ class PackedColumns(TraceColumns):
                     raise ValueError(f"watts_rep: {bits.numel()} words for {n} samples")
                 t = torch.empty(n, dtype=torch.float64, device=dev)
                 ws = _native.Workspace.get(L.dw_unpack_decimal_rep_workspace_size(n))
-                _native.check(L.dw_unpack_decimal_rep(_native.ptr(code), _native.ptr(bits), n, self.watts_p0,
-                                                      _native.ptr(t), ws.data_ptr(), ws.numel(),
-                                                      _native.stream_handle()), "dw_unpack_decimal_rep")
+                if self.watts_bits is not None:  # the stored codes bit-packed
+                    wd, wb = self.watts_bits
+                    _native.check(L.dw_unpack_decimal_rep_bits(_native.ptr(code), wd, wb, _native.ptr(bits), n,
+                                                               self.watts_p0, _native.ptr(t), ws.data_ptr(),
+                                                               ws.numel(), _native.stream_handle()),
+                                  "dw_unpack_decimal_rep_bits")
+                else:
+                    _native.check(L.dw_unpack_decimal_rep(_native.ptr(code), _native.ptr(bits), n, self.watts_p0,
+                                                          _native.ptr(t), ws.data_ptr(), ws.numel(),
+                                                          _native.stream_handle()), "dw_unpack_decimal_rep")
             else:
                 if code.numel() != self.n_power:
                     raise ValueError(f"watts: {code.numel()} codes for {self.n_power} samples")
@@ -754,6 +765,29 @@ def rep_code(code):
     return words, code[new]
 
 
+def _pack_codes(code, p0: int):
+    """(p0', (width, bias), words) for a run-coded column's stored decimal
+    codes: the decimal zeros every mantissa shares stripped (p0 lowered by as
+    many, never below 0: the decode divides by 10^(p0'+j) as before, the same
+    correctly rounded double) and the codes bit-packed in the bits their
+    spread needs -- or None unless that is narrower than 32 bits."""
+    is_t = isinstance(code, torch.Tensor)
+    c = (code.to(torch.int64) & 0xFFFFFFFF) if is_t else np.asarray(code).astype(np.int64)
+    if c.shape[0] == 0:
+        return None
+    m, j = c & 0x3FFFFFFF, c >> 30
+    z = 0
+    while z < p0 and bool(((m % 10 ** (z + 1)) == 0).all()):
+        z += 1
+    if z:
+        c = (m // 10 ** z) | (j << 30)
+    packed = _bitfields(c, 31)
+    if packed is None:
+        return None
+    bias, width, words = packed
+    return p0 - z, (width, bias), words
+
+
 def pack(cols: TraceColumns, decimal: bool = True, runs: bool = True, grid_ts: bool = True) -> PackedColumns:
     """Packed form of a trace with sorted power, operator and kernel starts
     (ValueError otherwise -- keep such traces unpacked).  Works on host or
@@ -795,9 +829,12 @@ def pack(cols: TraceColumns, decimal: bool = True, runs: bool = True, grid_ts: b
     dec = decimal_code(cols.watts) if decimal else None
     watts, p0 = (cols.watts, None) if dec is None else (dec[1], dec[0])
     rc = rep_code(watts) if dec is not None and runs else None
-    watts_rep = None
+    watts_rep = watts_bits = None
     if rc is not None:
         watts_rep, watts = rc
+        wp = _pack_codes(watts, p0)
+        if wp is not None:
+            p0, watts_bits, watts = wp
     sd = _sig_dict(cols.op_sig)
     sig, sig_dict = (cols.op_sig, None) if sd is None else (sd[1], sd[0])
     sig_bits = None
@@ -812,7 +849,7 @@ def pack(cols: TraceColumns, decimal: bool = True, runs: bool = True, grid_ts: b
                          k_op=cols.k_op, op_sig=sig, watts_p0=p0, ts_bias=tbias, op_sig_dict=sig_dict,
                          ts_bits=twidth, n_power=cols.n_power, ts_last=tlast, iv_bits=iv_bits,
                          n_ops=cols.n_ops, n_kernels=cols.n_kernels, sig_bits=sig_bits, watts_rep=watts_rep,
-                         ts_step=tstep, op_ids=cols.op_ids, k_ids=cols.k_ids, op_names=cols.op_names, op_work=cols.op_work,
+                         ts_step=tstep, watts_bits=watts_bits, op_ids=cols.op_ids, k_ids=cols.k_ids, op_names=cols.op_names, op_work=cols.op_work,
                          op_rank=cols.op_rank)
 
 
@@ -841,6 +878,7 @@ def save_packed(cols: TraceColumns, path) -> None:
             "op_base": pc.op_start_base, "k_base": pc.k_start_base, "watts_p0": pc.watts_p0,
             "ts_bias": pc.ts_bias, "ts_bits": pc.ts_bits, "n_power": pc.n_power,
             "ts_last": pc._ts_last if pc.ts_bits is not None else None, "ts_step": pc.ts_step,
+            "watts_bits": list(pc.watts_bits) if pc.watts_bits is not None else None,
             "iv_bits": {k: list(v) for k, v in pc.iv_bits.items()}, "n_ops": pc.n_ops, "n_kernels": pc.n_kernels,
             "sig_bits": pc.sig_bits, "watts_rep": pc.watts_rep is not None,
             "columns": {}}
@@ -892,4 +930,4 @@ def load_packed(path, pin: bool = False) -> PackedColumns:
                          ts_last=meta.get("ts_last"), iv_bits={k: tuple(v) for k, v in meta.get("iv_bits", {}).items()},
                          n_ops=meta.get("n_ops"), n_kernels=meta.get("n_kernels"), sig_bits=meta.get("sig_bits"),
                          watts_rep=as_signed(cols["watts_rep"]) if meta.get("watts_rep") else None,
-                         ts_step=meta.get("ts_step"))
+                         ts_step=meta.get("ts_step"), watts_bits=meta.get("watts_bits"))

@@ -301,7 +301,26 @@ __global__ void __launch_bounds__(1024) rep_scan_kernel(unsigned long long *bsum
     }
 }
 
-__global__ void __launch_bounds__(1024) rep_decode_kernel(const uint32_t *code, const uint32_t *rep, int64_t n,
+// the run-coded column's k-th stored code: u32 codes, or bias + the width-bit
+// field k (dw_unpack_bits layout)
+struct U32Codes {
+    const uint32_t *c;
+    __device__ __forceinline__ uint32_t operator()(int64_t k) const { return __ldg(c + k); }
+};
+struct BitCodes {
+    const uint32_t *w;
+    int width;
+    uint32_t bias;
+    __device__ __forceinline__ uint32_t operator()(int64_t k) const {
+        const int64_t bit = k * (int64_t)width;
+        const int64_t q = bit >> 5;
+        const uint64_t win = (uint64_t)__ldg(w + q) | ((uint64_t)__ldg(w + q + 1) << 32);
+        return bias + (uint32_t)((win >> (bit & 31)) & ((1ULL << width) - 1ULL));
+    }
+};
+
+template <typename Codes>
+__global__ void __launch_bounds__(1024) rep_decode_kernel(Codes code, const uint32_t *rep, int64_t n,
                                                           int32_t p0, const unsigned long long *bpre,
                                                           double *out) {
     __shared__ unsigned wt[32];
@@ -330,9 +349,23 @@ __global__ void __launch_bounds__(1024) rep_decode_kernel(const uint32_t *code, 
         if (smp < n) {
             int64_t idx = base + ek + __popc(wk & upto);
             idx = idx < 0 ? 0 : idx;  // only a bitmap without bit 0 (invalid input)
-            __stcs(out + smp, decimal_value(__ldg(code + idx), p0));
+            __stcs(out + smp, decimal_value(code(idx), p0));
         }
     }
+}
+
+template <typename Codes>
+static int unpack_decimal_rep(Codes codes, const uint32_t *d_rep, int64_t n, int32_t p0, double *d_out,
+                              void *d_workspace, size_t workspace_bytes, cudaStream_t s) {
+    if (!d_workspace || workspace_bytes < dw_unpack_decimal_rep_workspace_size(n)) return DW_E_WORKSPACE;
+    const int64_t nwords = (n + 31) >> 5, nb = ceil_div(nwords, REP_WORDS);
+    unsigned long long *bsum = (unsigned long long *)d_workspace;
+    rep_count_kernel<<<(unsigned)nb, 256, 0, s>>>(d_rep, nwords, bsum);
+    rep_scan_kernel<<<1, 1024, 0, s>>>(bsum, nb);
+    rep_decode_kernel<<<(unsigned)nb, 1024, 0, s>>>(codes, d_rep, n, p0, bsum, d_out);
+    count_launch(3);
+    DW_CHECK_LAUNCH();
+    return DW_OK;
 }
 
 }  // namespace dw
@@ -462,16 +495,18 @@ int dw_unpack_decimal_rep(const uint32_t *d_code, const uint32_t *d_rep, int64_t
                           void *d_workspace, size_t workspace_bytes, dw_stream_t stream) {
     if (n < 0 || (n && (!d_code || !d_rep || !d_out)) || p0 < -22 || p0 + 3 > 22) return DW_E_ARG;
     if (n == 0) return DW_OK;
-    if (!d_workspace || workspace_bytes < dw_unpack_decimal_rep_workspace_size(n)) return DW_E_WORKSPACE;
-    cudaStream_t s = (cudaStream_t)stream;
-    const int64_t nwords = (n + 31) >> 5, nb = ceil_div(nwords, REP_WORDS);
-    unsigned long long *bsum = (unsigned long long *)d_workspace;
-    rep_count_kernel<<<(unsigned)nb, 256, 0, s>>>(d_rep, nwords, bsum);
-    rep_scan_kernel<<<1, 1024, 0, s>>>(bsum, nb);
-    rep_decode_kernel<<<(unsigned)nb, 1024, 0, s>>>(d_code, d_rep, n, p0, bsum, d_out);
-    count_launch(3);
-    DW_CHECK_LAUNCH();
-    return DW_OK;
+    return unpack_decimal_rep(U32Codes{d_code}, d_rep, n, p0, d_out, d_workspace, workspace_bytes,
+                              (cudaStream_t)stream);
+}
+
+int dw_unpack_decimal_rep_bits(const uint32_t *d_words, int32_t width, uint32_t bias, const uint32_t *d_rep, int64_t n,
+                               int32_t p0, double *d_out, void *d_workspace, size_t workspace_bytes,
+                               dw_stream_t stream) {
+    if (n < 0 || width < 1 || width > 32 || (n && (!d_words || !d_rep || !d_out)) || p0 < -22 || p0 + 3 > 22)
+        return DW_E_ARG;
+    if (n == 0) return DW_OK;
+    return unpack_decimal_rep(BitCodes{d_words, width, bias}, d_rep, n, p0, d_out, d_workspace, workspace_bytes,
+                              (cudaStream_t)stream);
 }
 
 int dw_unpack_decimal(const uint32_t *d_code, int64_t n, int32_t p0, double *d_out, dw_stream_t stream) {

@@ -23,7 +23,7 @@ for c in (ca, cb):
     hc = PackedColumns(pc.ts_base, pin(pc.ts), pin(pc.watts), pc.op_start_base, pin(pc.op_start), pin(pc.op_end),
                        pc.k_start_base, pin(pc.k_start), pin(pc.k_end), c.trace_end, op_sig=pin(pc.op_sig),
                        watts_p0=pc.watts_p0, ts_bias=pc.ts_bias, op_sig_dict=pc.op_sig_dict.cpu(),
-                       ts_bits=pc.ts_bits, ts_step=pc.ts_step, n_power=pc.n_power,
+                       ts_bits=pc.ts_bits, ts_step=pc.ts_step, watts_bits=pc.watts_bits, n_power=pc.n_power,
                        ts_last=pc._ts_last if pc.ts_bits is not None else None,
                                iv_bits=pc.iv_bits, n_ops=pc.n_ops, n_kernels=pc.n_kernels,
                                sig_bits=pc.sig_bits, watts_rep=None if pc.watts_rep is None else pin(pc.watts_rep))
@@ -69,7 +69,7 @@ for p in pinned:
     q = PackedColumns(p.ts_base, p.ts.cuda(), p.watts.cuda(), p.op_start_base, p.op_start.cuda(), p.op_end.cuda(),
                       p.k_start_base, p.k_start.cuda(), p.k_end.cuda(), p.trace_end, op_sig=p.op_sig.cuda(),
                       watts_p0=p.watts_p0, ts_bias=p.ts_bias, op_sig_dict=p.op_sig_dict,
-                      ts_bits=p.ts_bits, ts_step=p.ts_step, n_power=p.n_power, ts_last=p._ts_last if p.ts_bits is not None else None,
+                      ts_bits=p.ts_bits, ts_step=p.ts_step, watts_bits=p.watts_bits, n_power=p.n_power, ts_last=p._ts_last if p.ts_bits is not None else None,
                       iv_bits=p.iv_bits, n_ops=p.n_ops, n_kernels=p.n_kernels, sig_bits=p.sig_bits,
                       watts_rep=None if p.watts_rep is None else p.watts_rep.cuda())
     q._dev["first_last"] = p._dev["first_last"]

@@ -22,7 +22,7 @@ for c in (ca, cb):
     hc = PackedColumns(pc.ts_base, pin(pc.ts), pin(pc.watts), pc.op_start_base, pin(pc.op_start), pin(pc.op_end),
                        pc.k_start_base, pin(pc.k_start), pin(pc.k_end), c.trace_end, op_sig=pin(pc.op_sig),
                        watts_p0=pc.watts_p0, ts_bias=pc.ts_bias, op_sig_dict=pin(pc.op_sig_dict),
-                       ts_bits=pc.ts_bits, ts_step=pc.ts_step, n_power=pc.n_power,
+                       ts_bits=pc.ts_bits, ts_step=pc.ts_step, watts_bits=pc.watts_bits, n_power=pc.n_power,
                        ts_last=pc._ts_last if pc.ts_bits is not None else None,
                                iv_bits=pc.iv_bits, n_ops=pc.n_ops, n_kernels=pc.n_kernels,
                                sig_bits=pc.sig_bits, watts_rep=None if pc.watts_rep is None else pin(pc.watts_rep))

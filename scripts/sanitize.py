@@ -39,7 +39,7 @@ for c in (a, b):
     hosts.append(PackedColumns(q.ts_base, pin(q.ts), pin(q.watts), q.op_start_base, pin(q.op_start), pin(q.op_end),
                                q.k_start_base, pin(q.k_start), pin(q.k_end), q.trace_end, op_sig=pin(q.op_sig),
                                watts_p0=q.watts_p0, ts_bias=q.ts_bias, op_sig_dict=pin(q.op_sig_dict),
-                               ts_bits=q.ts_bits, ts_step=q.ts_step, n_power=q.n_power, ts_last=q._ts_last, iv_bits=q.iv_bits,
+                               ts_bits=q.ts_bits, ts_step=q.ts_step, watts_bits=q.watts_bits, n_power=q.n_power, ts_last=q._ts_last, iv_bits=q.iv_bits,
                                n_ops=q.n_ops, n_kernels=q.n_kernels, sig_bits=q.sig_bits, watts_rep=pin(q.watts_rep)))
 an = analyze(hosts[0], hosts[1], copy_stream=torch.cuda.Stream())
 print("host-resident analysis", an.join.P)

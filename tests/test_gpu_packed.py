@@ -45,7 +45,7 @@ def test_decode_exact_and_ledger_identical(tmp_path):
     from paper_2512_08365_b200.columns import PackedColumns
     bare = [PackedColumns(q.ts_base, q.ts, q.watts, q.op_start_base, q.op_start, q.op_end, q.k_start_base,
                           q.k_start, q.k_end, q.trace_end, op_sig=q.op_sig, watts_p0=q.watts_p0, ts_bias=q.ts_bias,
-                          op_sig_dict=q.op_sig_dict, ts_bits=q.ts_bits, ts_step=q.ts_step, n_power=q.n_power,
+                          op_sig_dict=q.op_sig_dict, ts_bits=q.ts_bits, ts_step=q.ts_step, watts_bits=q.watts_bits, n_power=q.n_power,
                           ts_last=q._ts_last, iv_bits=q.iv_bits, n_ops=q.n_ops, n_kernels=q.n_kernels,
                           sig_bits=q.sig_bits, watts_rep=q.watts_rep)
             for q in (ha, hb)]
@@ -140,7 +140,7 @@ def test_run_coded_trace_analysis_identical():
         hosts.append(PackedColumns(q.ts_base, pin(q.ts), pin(q.watts), q.op_start_base, pin(q.op_start),
                                    pin(q.op_end), q.k_start_base, pin(q.k_start), pin(q.k_end), q.trace_end,
                                    op_sig=pin(q.op_sig), watts_p0=q.watts_p0, ts_bias=q.ts_bias,
-                                   op_sig_dict=pin(q.op_sig_dict), ts_bits=q.ts_bits, ts_step=q.ts_step, n_power=q.n_power,
+                                   op_sig_dict=pin(q.op_sig_dict), ts_bits=q.ts_bits, ts_step=q.ts_step, watts_bits=q.watts_bits, n_power=q.n_power,
                                    ts_last=q._ts_last, iv_bits=q.iv_bits, n_ops=q.n_ops, n_kernels=q.n_kernels,
                                    sig_bits=q.sig_bits, watts_rep=pin(q.watts_rep)))
     ra = analyze(a, b, "samples", 0.10, 20)
@@ -151,7 +151,8 @@ def test_run_coded_trace_analysis_identical():
     # a run-coded column without its bitmap is refused, not misread
     bad = PackedColumns(p.ts_base, p.ts, p.watts, p.op_start_base, p.op_start, p.op_end, p.k_start_base, p.k_start,
                         p.k_end, p.trace_end, op_sig=p.op_sig, watts_p0=p.watts_p0, ts_bias=p.ts_bias,
-                        op_sig_dict=p.op_sig_dict, ts_bits=p.ts_bits, ts_step=p.ts_step, n_power=p.n_power, ts_last=p._ts_last,
+                        op_sig_dict=p.op_sig_dict, ts_bits=p.ts_bits, ts_step=p.ts_step, n_power=p.n_power,
+                        ts_last=p._ts_last,
                         iv_bits=p.iv_bits, n_ops=p.n_ops, n_kernels=p.n_kernels, sig_bits=p.sig_bits)
     with pytest.raises(ValueError):
         bad.device("watts")
@@ -191,3 +192,40 @@ def test_c4_clock_is_grid_coded():
     assert (q.ts_step, q.ts_bias, q.ts_bits) == (p.ts_step, p.ts_bias, p.ts_bits)
     assert np.array_equal(np.asarray(q.ts).view(np.uint32), np.asarray(p.ts.cpu() if isinstance(p.ts, torch.Tensor)
                                                                          else p.ts).view(np.uint32))
+
+
+@pytest.mark.parametrize("kind", ["c4", "milliwatts", "mixed_decades"])
+def test_bit_packed_watts_codes_decode_exactly(kind):
+    """dw_unpack_decimal_rep_bits: run-coded watts whose stored codes are
+    bit-packed after stripping their shared decimal zeros -- C4's 6-decimal
+    kernel watts (30 bits), integer-milliwatt NVML readings (p0 lowered by 3,
+    ~20 bits), values across decades (several exponents j) -- decode to the
+    exact doubles, and the .dwc file round-trips them."""
+    from paper_2512_08365_b200.columns import TraceColumns
+    from paper_2512_08365_b200.synth import round9
+    rng = np.random.default_rng(len(kind))
+    n = 400_003
+    ts = (10**9 + np.arange(n) * 100).astype(np.int64)
+    runs = np.repeat(np.arange(n // 5 + 1), 5)[:n]
+    if kind == "c4":
+        vals = round9(torch.from_numpy(rng.uniform(150.0, 700.0, n // 5 + 1))).numpy()
+    elif kind == "milliwatts":
+        vals = rng.integers(60_000, 1_000_000, n // 5 + 1) / 1000.0
+    else:
+        vals = round9(torch.from_numpy(rng.uniform(5.0, 5000.0, n // 5 + 1))).numpy()
+    w = vals[runs]
+    c = TraceColumns.from_arrays(ts, w, ts[:1], ts[:1] + 10)
+    p = pack(c)
+    assert p.watts_rep is not None and p.watts_bits is not None
+    plain = pack(c, runs=True)
+    if kind == "milliwatts":
+        assert p.watts_bits[0] <= 20
+    if kind == "c4":
+        assert p.watts_bits[0] == 30
+    assert np.array_equal(p.device("watts").cpu().numpy(), w)
+    import tempfile, os
+    with tempfile.TemporaryDirectory() as d:
+        save_packed(c, os.path.join(d, "w.dwc"))
+        q = load_packed(os.path.join(d, "w.dwc"))
+        assert q.watts_bits == p.watts_bits and q.watts_p0 == p.watts_p0
+        assert np.array_equal(q.device("watts").cpu().numpy(), w)

@@ -177,7 +177,10 @@ def test_run_coded_watts(tmp_path):
     for x in (p, q):
         bits = np.unpackbits(np.asarray(x.watts_rep).view(np.uint8), bitorder="little")[:n].astype(bool)
         assert bits[0]
-        np.testing.assert_array_equal(_decode(x.watts_p0, np.asarray(x.watts))[np.cumsum(bits) - 1], w)
+        codes = np.asarray(x.watts)
+        if x.watts_bits is not None:  # bit-packed codes: bias + fields (columns._pack_codes)
+            codes = (x.watts_bits[1] + _fields(codes, x.watts_bits[0], int(bits.sum()))).astype(np.uint32)
+        np.testing.assert_array_equal(_decode(x.watts_p0, codes)[np.cumsum(bits) - 1], w)
     assert q.host_bytes == p.host_bytes < pack(c, runs=False).host_bytes
     # no repeats: plain codes
     assert rep_code(np.arange(1000, dtype=np.uint32)) is None
