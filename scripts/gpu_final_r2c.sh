@@ -1,8 +1,9 @@
 #!/bin/bash
-# round-2 closing evidence after the late changes: smoke, default bench (C4),
+# round-2 closing evidence after the late changes: GPU tests, smoke, default bench (C4),
 # the reference arm, C5 corpus, C2 / C3 / C3-split, the step's launch list,
 # an ncu capture of the tile kernel and of the waste-sum pass
 mkdir -p gpurun_out; TAG=${1:-r2j}
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_$TAG.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_$TAG.log
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke_$TAG.log
 timeout 1500 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?"
 timeout 1500 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; echo "ref rc=$?"
