@@ -212,16 +212,17 @@ def test_bit_packed_watts_codes_decode_exactly(kind):
     elif kind == "milliwatts":
         vals = rng.integers(60_000, 1_000_000, n // 5 + 1) / 1000.0
     else:
-        vals = round9(torch.from_numpy(rng.uniform(5.0, 5000.0, n // 5 + 1))).numpy()
+        vals = round9(torch.from_numpy(rng.uniform(5.0, 60.0, n // 5 + 1))).numpy()  # j in {0, 1}: 31 bits
     w = vals[runs]
     c = TraceColumns.from_arrays(ts, w, ts[:1], ts[:1] + 10)
     p = pack(c)
     assert p.watts_rep is not None and p.watts_bits is not None
-    plain = pack(c, runs=True)
     if kind == "milliwatts":
         assert p.watts_bits[0] <= 20
     if kind == "c4":
         assert p.watts_bits[0] == 30
+    if kind == "mixed_decades":  # two exponents j: the j bit is inside the packed spread
+        assert p.watts_bits[0] == 31
     assert np.array_equal(p.device("watts").cpu().numpy(), w)
     import tempfile, os
     with tempfile.TemporaryDirectory() as d:
